@@ -1,0 +1,360 @@
+"""Pins of the CPU oracle against things other than itself (-m "not gpu").
+
+Each test cites the passage whose value / closed form / invariant it uses:
+P:n = /root/reference/PAPER.md line n, S:n = SPEC.md line n.  Golden
+values live in tests/golden/spec_examples.json with their citations.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import qpgen
+from oracle import dfom as O
+from oracle import kkt
+
+
+def _a(x):
+    return np.asarray(x, dtype=float)
+
+
+# ------------------------------------------------------------------ geometry
+def test_proj_dist_slack_examples(golden):
+    for ex in golden["proj_K"]:
+        assert np.array_equal(O.proj_K(_a(ex["v"]), np.array(ex["cone"])), _a(ex["out"])), ex["cite"]
+    for ex in golden["dist_K"]:
+        assert O.dist_K(_a(ex["v"]), np.array(ex["cone"])) == pytest.approx(ex["out"]), ex["cite"]
+    for ex in golden["slack"]:
+        out = O.slack(_a(ex["r"]), _a(ex["lam"]), np.array(ex["cone"]), ex["rho"])
+        assert np.array_equal(out, _a(ex["out"])), ex["cite"]
+
+
+def test_lagrangian_value_examples(golden):
+    for ex in golden["lagrangian_value"]:
+        v = O.aug_lagrangian(_a(ex["Q"]), _a(ex["q"]), _a(ex["G"]), _a(ex["g"]),
+                             np.array(ex["cone"]), ex["rho"], _a(ex["u"]), _a(ex["lam"]))
+        assert v == pytest.approx(ex["out"], abs=1e-14), ex["cite"]
+
+
+def test_lagrangian_grad_examples(golden):
+    for ex in golden["lagrangian_grad"]:
+        v = O.aug_lagrangian_grad(_a(ex["Q"]), _a(ex["q"]), _a(ex["G"]), _a(ex["g"]),
+                                  np.array(ex["cone"]), ex["rho"], _a(ex["u"]), _a(ex["lam"]))
+        assert np.allclose(v, _a(ex["out"]), atol=1e-14), ex["cite"]
+
+
+def test_closed_form_matches_min_over_slack():
+    """(auglag1) P:243-251 vs the definition (auglag), min over s in K done
+    numerically per row with a bounded scalar minimiser (independent path)."""
+    from scipy.optimize import minimize_scalar
+    prob = qpgen.tiny(4, 5, seed=3, kind="mixed")
+    rng = np.random.default_rng(11)
+    for rho in (0.5, 2.0):
+        u = rng.uniform(-1, 1, prob.n)
+        lam = rng.normal(size=prob.p)
+        r = prob.G @ u + prob.g
+        val = 0.5 * u @ prob.Q @ u + prob.q @ u
+        for i in range(prob.p):
+            f = lambda s: lam[i] * (r[i] - s) + 0.5 * rho * (r[i] - s) ** 2
+            if prob.cone[i] == qpgen.ZERO:
+                val += f(0.0)
+            else:
+                m = minimize_scalar(f, bounds=(-50.0, 0.0), method="bounded",
+                                    options=dict(xatol=1e-12))
+                val += min(m.fun, f(0.0))
+        cf = O.aug_lagrangian(prob.Q, prob.q, prob.G, prob.g, prob.cone, rho, u, lam)
+        assert cf == pytest.approx(val, rel=1e-9, abs=1e-9)
+
+
+def test_grad_matches_finite_differences():
+    """gradient vs central differences of the value."""
+    prob = qpgen.tiny(6, 5, seed=5, kind="mixed")
+    rng = np.random.default_rng(7)
+    for rho in (0.0, 1.0, 3.0):
+        for _ in range(10):
+            u = rng.uniform(-1, 1, prob.n)
+            lam = rng.normal(size=prob.p)
+            gr = O.aug_lagrangian_grad(prob.Q, prob.q, prob.G, prob.g, prob.cone, rho, u, lam)
+            h = 1e-6
+            fd = np.zeros(prob.n)
+            for j in range(prob.n):
+                e = np.zeros(prob.n)
+                e[j] = h
+                fd[j] = (O.aug_lagrangian(prob.Q, prob.q, prob.G, prob.g, prob.cone, rho, u + e, lam)
+                         - O.aug_lagrangian(prob.Q, prob.q, prob.G, prob.g, prob.cone, rho, u - e, lam)) / (2 * h)
+            assert np.allclose(gr, fd, rtol=1e-5, atol=1e-6)
+
+
+def test_grad_equality_closed_form():
+    """for K = {0}, grad = (Q + rho G'G)u + (q + G'mu + rho G'g)."""
+    prob = qpgen.tiny(7, 4, seed=9, kind="eq")
+    rng = np.random.default_rng(2)
+    u = rng.uniform(-1, 1, prob.n)
+    mu = rng.normal(size=prob.p)
+    for rho in (0.0, 0.7, 5.0):
+        H = prob.Q + rho * prob.G.T @ prob.G
+        ref = H @ u + (prob.q + prob.G.T @ mu + rho * prob.G.T @ prob.g)
+        got = O.aug_lagrangian_grad(prob.Q, prob.q, prob.G, prob.g, prob.cone, rho, u, mu)
+        assert np.allclose(got, ref, rtol=1e-12, atol=1e-12)
+
+
+# ----------------------------------------------------------------- sequences
+def test_theta_identities(golden):
+    th = O.theta_sequence(10001)
+    assert th[1] == 1.0
+    assert th[2] == pytest.approx((1 + math.sqrt(5)) / 2, rel=1e-15)
+    assert th[3] == pytest.approx(golden["theta"]["theta3_approx"], abs=1e-5)
+    S = np.cumsum(th[1:])                                                       # S_k, j=1..k
+    k = np.arange(1, 10002)
+    assert np.all((k + 1) / 2 <= th[1:] + 1e-12) and np.all(th[1:] <= k + 1e-12)
+    assert np.allclose(S, th[1:] ** 2, rtol=1e-9)
+    b = O.beta_fgm(5)
+    assert b[1] == 0.0
+    # beta_2 = (theta_2 - 1)/theta_3 with theta_2 - 1 = (sqrt5 - 1)/2; S:236 prints 0.28172 (typo)
+    assert b[2] == pytest.approx(((math.sqrt(5) - 1) / 2) / th[3], rel=1e-15)
+    assert b[2] == pytest.approx(0.281753525125, abs=1e-11)
+
+
+def test_fom_gm_single_step(golden):
+    """GM on phi(u) = u^2 - 2u (L = 2), x0 = 0 -> x1 = 1 exactly."""
+    ex = golden["fom_gm_step"]
+    x = O.fom(lambda y: 2 * y - 2, np.array([ex["x0"]]), ex["L"], np.array([-10.0]),
+              np.array([10.0]), 1, O.INNER_GM)
+    assert x[0] == ex["x1"]
+
+
+@pytest.mark.parametrize("rule,p", [(O.INNER_GM, 1), (O.INNER_FGM, 2)])
+def test_fom_lemma1_envelope(rule, p):
+    """Lemma 1: phi(x^k) - phi* <= 2 L R^2 / (k+1)^p on random box QPs,
+    phi* and x* from brute-force enumeration (independent)."""
+    for seed in range(4):
+        prob = qpgen.tiny(5, 0, seed=seed, kind="ineq", box=0.6)
+        Q, q = prob.Q, prob.q
+        ref = kkt.brute_force(Q, q, np.zeros((0, 5)), np.zeros(0), prob.lb, prob.ub, np.zeros(0, np.uint8))
+        L = float(np.linalg.eigvalsh(Q)[-1])
+        x0 = np.full(5, 0.6) * np.sign(np.arange(5) - 2.0)
+        R = np.linalg.norm(x0 - ref.u)
+        hist = []
+        O.fom(lambda y: Q @ y + q, x0, L, prob.lb, prob.ub, 200, rule, history=hist)
+        for k, x in enumerate(hist, start=1):
+            gap = 0.5 * x @ Q @ x + q @ x - ref.F
+            assert gap <= 2 * L * R * R / (k + 1) ** p + 1e-12
+
+
+# ------------------------------------------------------------------ DFOM steps
+def test_dual_step_examples(golden):
+    """one DFOM step lambda^1 = [mu^1 + grad/(2 L_d)]_{K_d}.
+    Construction: G = 0, so grad_bar = g regardless of u (rho = 0, s = 0)."""
+    for ex in golden["dual_step"]:
+        g = _a(ex["grad"])
+        res = O.dfom(np.eye(1), np.zeros(1), np.zeros((1, 1)), g, np.array([-1.0]), np.array([1.0]),
+                     np.array(ex["cone"], np.uint8), 0.0, O.DGM, 1, 1, 1.0, ex["L_d"],
+                     project_dual=ex["project_dual"])
+        assert np.array_equal(res.lam, _a(ex["lam"])), ex["cite"]
+
+
+def test_average_examples(golden):
+    """S:349-350 (Eq. average_primal).  Construction: Q = 1, q = 0, G = 1 (ZERO row),
+    rho = 0, L_in = 1, one GM inner step gives u_bar = -mu exactly; g = -4, L_d = 1 makes
+    u_bar^1 = 0 and u_bar^2 = 2."""
+    for ex in golden["average"]:
+        res = O.dfom(np.eye(1), np.zeros(1), np.eye(1), np.array([-4.0]), np.array([-10.0]),
+                     np.array([10.0]), np.array([0], np.uint8), 0.0, ex["alg"], 2, 1, 1.0, 1.0,
+                     inner_rule=O.INNER_GM, keep_trace=True)
+        assert np.array_equal(res.trace_u[0], [0.0]) and np.array_equal(res.trace_u[1], [2.0])
+        if "out" in ex:
+            assert res.x_avg[0] == pytest.approx(ex["out"][0], rel=1e-15), ex["cite"]
+        else:
+            assert res.x_avg[0] == pytest.approx(ex["out_approx"][0], abs=5e-4), ex["cite"]
+            th2 = (1 + math.sqrt(5)) / 2
+            assert res.x_avg[0] == pytest.approx(2 * th2 / (1 + th2), rel=1e-15)
+
+
+def test_dfgm_weight_sum_is_theta_squared():
+    """S_k = theta_k^2 for the DFGM averaging weights."""
+    prob = qpgen.tiny(3, 2, seed=1)
+    for K in (1, 2, 7, 40):
+        res = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 1.0, O.DFGM,
+                     K, 2, 10.0, 1.0)
+        assert res.S == pytest.approx(O.theta_sequence(K)[K] ** 2, rel=1e-12)
+
+
+def test_dgm_last_iterate_is_next_inner_solve():
+    """for DGM the last iterate u_bar(lambda^k) coincides with u_bar^{k+1}
+    (mu^{k+1} = lambda^k, same warm start) -- bit for bit."""
+    prob = qpgen.tiny(6, 4, seed=4)
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 1.0, 0.1)
+    a = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 1.0, O.DGM, 5, 4, L_in, L_d)
+    b = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 1.0, O.DGM, 6, 4, L_in, L_d,
+               keep_trace=True)
+    assert np.array_equal(a.x_last, b.trace_u[5])
+
+
+def test_lipschitz_ld_example(golden):
+    """S:430 / Eq. (Ld): lambda_min = 1, rho = 0, ||G|| = 2 -> L_d = 4."""
+    ex = golden["lipschitz_Ld"]
+    G = np.array([[ex["normG"], 0.0]])
+    Q = np.diag([ex["lambda_min"], 3.0])
+    _, L_d, nG2 = O.lipschitz_constants(Q, G, ex["rho"], ex["lambda_min"])
+    assert nG2 == pytest.approx(ex["normG"] ** 2) and L_d == pytest.approx(ex["L_d"])
+
+
+# ---------------------------------------------------------------- brute force
+def test_bruteforce_examples(golden):
+    for ex in golden["bruteforce"]:
+        n = len(ex["q"])
+        G = _a(ex["G"]).reshape(-1, n)
+        sol = kkt.brute_force(_a(ex["Q"]), _a(ex["q"]), G, _a(ex["g"]), _a(ex["lb"]), _a(ex["ub"]),
+                              np.array(ex["cone"], np.uint8))
+        assert np.allclose(sol.u, ex["u"], atol=1e-12), ex["cite"]
+        assert sol.F == pytest.approx(ex["F"], abs=1e-12), ex["cite"]
+        if "lam" in ex:
+            assert np.allclose(sol.lam, ex["lam"], atol=1e-12), ex["cite"]
+
+
+def test_kkt_equality_example_and_dfom_converges(golden):
+    """u* = (1/2, 1/2), lambda* = -1/2 via the KKT linear solve; DFGM and DGM
+    (rho = 1 and rho = 0) converge to it."""
+    ex = golden["bruteforce"][1]
+    Q, q, G, g = _a(ex["Q"]), _a(ex["q"]), _a(ex["G"]), _a(ex["g"])
+    sol = kkt.kkt_equality(Q, q, G, g)
+    assert np.allclose(sol.u, [0.5, 0.5]) and np.allclose(sol.lam, [-0.5])
+    lb, ub, cone = _a(ex["lb"]), _a(ex["ub"]), np.array(ex["cone"], np.uint8)
+    for rho, alg in ((1.0, O.DFGM), (0.0, O.DFGM), (1.0, O.DGM)):
+        L_in, L_d, _ = O.lipschitz_constants(Q, G, rho, 1.0)
+        res = O.dfom(Q, q, G, g, lb, ub, cone, rho, alg, 400, 50, L_in, L_d)
+        assert np.allclose(res.x_last, sol.u, atol=1e-8)
+        assert np.allclose(res.lam, sol.lam, atol=1e-7)
+
+
+@pytest.mark.parametrize("kind", ["ineq", "mixed", "eq"])
+@pytest.mark.parametrize("rho,alg", [(1.0, O.DFGM), (0.0, O.DFGM), (1.0, O.DGM), (4.0, O.DFGM)])
+def test_dfom_reaches_bruteforce_optimum(kind, rho, alg):
+    """Whole solve vs active-set enumeration: u* unique (Q > 0), so the
+    last iterate must converge to it; lambda stays in K_d; F(x_avg) close too."""
+    for seed in range(2):
+        prob = qpgen.tiny(5, 3, seed=20 + seed, kind=kind, box=0.4)
+        ref = kkt.brute_force(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone)
+        lmin = float(np.linalg.eigvalsh(prob.Q)[0])
+        L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, rho, lmin)
+        outer = 400 if (alg == O.DFGM and rho > 0) else 4000
+        res = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho, alg,
+                     outer, 40, L_in, L_d, keep_trace=True)
+        tol = 2e-6 if rho > 0 else 1e-4      # rho = 0: slow dual (L_d = ||G||^2 / lambda_min(Q))
+        assert np.allclose(res.x_last, ref.u, atol=tol), (seed, np.abs(res.x_last - ref.u).max())
+        for lam in res.trace_lam:                       # lambda^k in K_d
+            assert np.all(lam[prob.cone == qpgen.NONPOS] >= 0.0)
+        F_avg = 0.5 * res.x_avg @ prob.Q @ res.x_avg + prob.q @ res.x_avg
+        assert abs(F_avg - ref.F) <= 5e-2 * (1 + abs(ref.F))
+
+
+def _box_qp_min(H, c, lb, ub):
+    n = H.shape[0]
+    return kkt.brute_force(H, c, np.zeros((0, n)), np.zeros(0), lb, ub, np.zeros(0, np.uint8))
+
+
+def _exact_dual(prob, rho, mu):
+    """d_rho(mu) exactly via enumeration: for rho = 0, or rho > 0 with K = {0}, L_rho(., mu)
+    is a box QP."""
+    Q, q, G, g = prob.Q, prob.q, prob.G, prob.g
+    if rho == 0:
+        sol = _box_qp_min(Q, q + G.T @ mu, prob.lb, prob.ub)
+        return sol.F + mu @ g, sol.u
+    assert np.all(prob.cone == qpgen.ZERO)
+    H = Q + rho * G.T @ G
+    c = q + G.T @ (mu + rho * g)
+    sol = _box_qp_min(H, c, prob.lb, prob.ub)
+    w = g + mu / rho
+    const = 0.5 * rho * w @ w - mu @ mu / (2 * rho)
+    return sol.F + const, sol.u
+
+
+@pytest.mark.parametrize("alg,p_exp", [(O.DGM, 1), (O.DFGM, 2)])
+@pytest.mark.parametrize("kind,rho", [("ineq", 0.0), ("eq", 1.0)])
+def test_theorem1_and_weak_duality(alg, p_exp, kind, rho):
+    """Theorem 1: F* - d(lambda^k) <= 4 L_d R_d^2/(k+1)^p + 2(k+1)^(p-1) eps_in,
+    with d, eps_in = max_k L(u_bar^k, mu^k) - d(mu^k) (duquad_in) and F*, R_d = ||lambda*||
+    from enumeration; weak duality d(lambda^k) <= F* (P:964)."""
+    prob = qpgen.tiny(4, 2, seed=31, kind=kind, box=0.5)
+    ref = kkt.brute_force(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone)
+    lmin = float(np.linalg.eigvalsh(prob.Q)[0])
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, rho, lmin)
+    K = 40
+    res = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho, alg, K, 30,
+                 L_in, L_d, keep_trace=True)
+    eps_in = 0.0
+    for mu, u in zip(res.trace_mu, res.trace_u):
+        d_mu, _ = _exact_dual(prob, rho, mu)
+        Lval = O.aug_lagrangian(prob.Q, prob.q, prob.G, prob.g, prob.cone, rho, u, mu)
+        assert Lval - d_mu >= -1e-10                      # left inequality of (duquad_in)
+        eps_in = max(eps_in, Lval - d_mu)
+    R_d = np.linalg.norm(ref.lam)
+    for k, lam in enumerate(res.trace_lam, start=1):
+        d_lam, _ = _exact_dual(prob, rho, lam)
+        assert d_lam <= ref.F + 1e-10                     # weak duality
+        bound = 4 * L_d * R_d ** 2 / (k + 1) ** p_exp + 2 * (k + 1) ** (p_exp - 1) * eps_in
+        assert ref.F - d_lam <= bound + 1e-10, (k, ref.F - d_lam, bound)
+
+
+def test_inexact_gradient_bound():
+    """(inexact_gradient_rel) P:529-531: ||grad_bar d(mu) - grad d(mu)|| <= sqrt(2 L_d eps_in),
+    with the exact u(mu) from enumeration (rho = 0, K = R_-: grad d = G u(mu) + g)."""
+    prob = qpgen.tiny(5, 3, seed=8, kind="ineq", box=0.5)
+    lmin = float(np.linalg.eigvalsh(prob.Q)[0])
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 0.0, lmin)
+    rng = np.random.default_rng(0)
+    for _ in range(10):
+        mu = np.abs(rng.normal(size=prob.p))
+        x0 = rng.uniform(-0.5, 0.5, prob.n)
+        u_bar = O.inner_solve(prob.Q, prob.q, prob.G, prob.g, prob.cone, 0.0, mu, x0, L_in,
+                              prob.lb, prob.ub, 3)
+        d_mu, u_ex = _exact_dual(prob, 0.0, mu)
+        eps_in = O.aug_lagrangian(prob.Q, prob.q, prob.G, prob.g, prob.cone, 0.0, u_bar, mu) - d_mu
+        gbar = O.inexact_dual_grad(prob.G, prob.g, prob.cone, 0.0, u_bar, mu)
+        gex = prob.G @ u_ex + prob.g
+        assert np.linalg.norm(gbar - gex) <= math.sqrt(2 * L_d * max(eps_in, 0)) + 1e-9
+
+
+# ------------------------------------------------------ batch / sparse forms
+def test_batch_columns_match_single_runs():
+    prob = qpgen.mpc_batch(6, seed=1, N=4)
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 1.0, 0.1)
+    res = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 1.0, O.DFGM, 8, 5,
+                 L_in, L_d)
+    for b in range(6):
+        r1 = O.dfom(prob.Q, prob.q[:, b], prob.G, prob.g[:, b], prob.lb, prob.ub, prob.cone, 1.0,
+                    O.DFGM, 8, 5, L_in, L_d)
+        assert np.allclose(res.x_last[:, b], r1.x_last, rtol=0, atol=1e-13)
+        assert np.allclose(res.lam[:, b], r1.lam, rtol=0, atol=1e-12)
+
+
+def test_sparse_matches_dense():
+    import scipy.sparse as sp
+    prob = qpgen.sparse_banded_eq(n=300, p=100, seed=3)
+    Qd, Gd = prob.Q.toarray(), prob.G.toarray()
+    # Gershgorin (docstring of sparse_banded_eq)
+    ev = np.linalg.eigvalsh(Qd)
+    assert ev[0] >= 0.5 - 1e-12 and ev[-1] <= 3.0 + 1e-12
+    assert prob.Q.nnz == 300 + 2 * sum(300 - d for d in range(1, 6))
+    L_in, L_d, _ = O.lipschitz_constants(Qd, Gd, 5.0, 0.5)
+    a = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 5.0, O.DFGM, 5, 5, L_in, L_d)
+    b = O.dfom(Qd, prob.q, Gd, prob.g, prob.lb, prob.ub, prob.cone, 5.0, O.DFGM, 5, 5, L_in, L_d)
+    assert np.allclose(a.x_last, b.x_last, rtol=0, atol=1e-12)
+
+
+def test_config0_matches_independent_solver():
+    """Config 0 (BASELINE.json configs[0]): DFGM rho = 1, 200 x 50 reaches the optimum found by
+    an independent NLP solver (SciPy SLSQP) -- |F - F*| and dist_K within 1e-6."""
+    from scipy.optimize import minimize
+    prob = qpgen.dense_ineq(50, 25, seed=0)
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 1.0, 0.1)
+    res = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 1.0, O.DFGM, 200, 50,
+                 L_in, L_d)
+    cons = [dict(type="ineq", fun=lambda u: -(prob.G @ u + prob.g), jac=lambda u: -prob.G)]
+    sl = minimize(lambda u: 0.5 * u @ prob.Q @ u + prob.q @ u, np.zeros(50),
+                  jac=lambda u: prob.Q @ u + prob.q, bounds=[(-1, 1)] * 50, constraints=cons,
+                  method="SLSQP", options=dict(ftol=1e-15, maxiter=1000))
+    Fstar = sl.fun
+    F = O.objective(prob.Q, prob.q, res.x_last)
+    assert abs(F - Fstar) <= 1e-6 * (1 + abs(Fstar))
+    assert O.dist_K(prob.G @ res.x_last + prob.g, prob.cone) <= 1e-6
