@@ -358,3 +358,31 @@ def test_config0_matches_independent_solver():
     F = O.objective(prob.Q, prob.q, res.x_last)
     assert abs(F - Fstar) <= 1e-6 * (1 + abs(Fstar))
     assert O.dist_K(prob.G @ res.x_last + prob.g, prob.cone) <= 1e-6
+
+
+def test_fgm_hand_worked_iterates():
+    """FGM on phi(u) = u^2/2 with L = 2, x^0 = 1, worked by hand:
+    x^1 = 1/2, y^2 = x^1 (beta_1 = 0), x^2 = 1/4,
+    y^3 = x^2 + beta_2 (x^2 - x^1) = 0.25 - 0.25 * 0.2817535 = 0.1795616, x^3 = 0.0897808."""
+    hist = []
+    O.fom(lambda y: y, np.array([1.0]), 2.0, np.array([-5.0]), np.array([5.0]), 3, O.INNER_FGM,
+          history=hist)
+    assert hist[0][0] == 0.5 and hist[1][0] == 0.25
+    assert hist[2][0] == pytest.approx(0.0897808, abs=1e-7)
+
+
+def test_fgm_accelerates_over_gm():
+    """Lemma 1: on an ill-conditioned box QP the FGM gap after 200 steps is far
+    below the GM gap (rates 1/k^2 vs 1/k); a wrong momentum sign or index destroys this."""
+    rng = np.random.default_rng(5)
+    U, _ = np.linalg.qr(rng.normal(size=(8, 8)))
+    Q = U @ np.diag(np.logspace(-4, 0, 8)) @ U.T
+    q = rng.normal(size=8)
+    lb, ub = -1e6 * np.ones(8), 1e6 * np.ones(8)
+    ref = kkt.kkt_equality(Q, q, np.zeros((0, 8)), np.zeros(0))      # interior optimum
+    assert np.all(np.abs(ref.u) < 1e6)
+    gaps = {}
+    for rule in (O.INNER_GM, O.INNER_FGM):
+        x = O.fom(lambda y: Q @ y + q, np.zeros(8), 1.0, lb, ub, 200, rule)
+        gaps[rule] = 0.5 * x @ Q @ x + q @ x - ref.F
+    assert gaps[O.INNER_FGM] < 0.5 * gaps[O.INNER_GM]
