@@ -1,0 +1,232 @@
+/*
+ * duquad.h -- C ABI of the B200-native DuQuad hot path (arXiv 1504.05708).
+ *
+ * Solves   min_{u in U} F(u) = 1/2 u'Qu + q'u   s.t.  G u + g in K
+ * (Eq. original_primal) with U = [lb, ub] a box and K a
+ * product of per-row cones: ZERO ({0}, equality) or NONPOS (R_-, inequality),
+ * by the inexact (augmented) dual gradient / dual fast gradient methods
+ * DGM / DFGM (Algorithm DFOM) whose inner problem
+ * (Eq. ul) is solved by Algorithm FOM
+ * with a fixed number of inner iterations, warm-started.
+ *
+ * Every step of the path runs in this library's sm_100a kernels; the caller
+ * only marshals arguments.  All floating point is IEEE binary64.
+ *
+ * Conventions for every entry point:
+ *   - returns a duquad_status; no exception or abort crosses the ABI; a
+ *     non-OK status stores a message retrievable with duquad_last_error();
+ *   - "device pointer" = a pointer into global memory of the context's
+ *     CUDA device; "host pointer" = ordinary (pageable or pinned) memory;
+ *   - arrays are dense row-major unless stated otherwise;
+ *   - the library never retains caller pointers after a call returns
+ *     (except the trace buffers registered with duquad_set_trace).
+ * One context per host thread; calls on one context are not reentrant.
+ */
+#ifndef DUQUAD_H
+#define DUQUAD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DUQUAD_ABI_VERSION 1
+
+typedef enum {
+    DUQUAD_OK = 0,
+    DUQUAD_EINVAL = 1,      /* bad argument: dims, NaN in data, lb > ub, rho < 0, ...      */
+    DUQUAD_ENOMEM = 2,      /* device or host allocation failed                           */
+    DUQUAD_ECUDA = 3,       /* CUDA runtime error (message has the CUDA error string)     */
+    DUQUAD_ENCCL = 4,       /* NCCL error in the sharded path                             */
+    DUQUAD_ENONFINITE = 5,  /* an iterate became non-finite; results kept  */
+    DUQUAD_ENODEV = 6,      /* no CUDA device, or not an sm_100 device                    */
+    DUQUAD_ESTATE = 7       /* call out of order (e.g. solve before constants are set)    */
+} duquad_status;
+
+typedef enum { DUQUAD_DGM = 0, DUQUAD_DFGM = 1 } duquad_alg;
+
+typedef enum {
+    DUQUAD_INNER_FGM = 0,       /* theta recurrence, restarted at every inner solve (default) */
+    DUQUAD_INNER_GM = 1,        /* beta = 0                                                  */
+    DUQUAD_INNER_FGM_SIGMA = 2  /* beta = (sqrt L - sqrt sigma)/(sqrt L + sqrt sigma)        */
+} duquad_inner;
+
+typedef enum { DUQUAD_DENSE = 0, DUQUAD_CSR = 1 } duquad_format;
+
+enum { DUQUAD_CONE_ZERO = 0, DUQUAD_CONE_NONPOS = 1 };
+
+typedef struct duquad_ctx duquad_ctx;
+
+/*
+ * Problem data.  Single QP (batch == 1):
+ *   Q   n x n, symmetric positive (semi)definite;
+ *   G   p x n;  q n;  g p;  lb, ub n (entries may be -INFINITY / +INFINITY);
+ *   cone p tags (DUQUAD_CONE_*), or NULL meaning every row is cone_all.
+ * Batched (batch = B > 1, dense only; north_star (c)): Q and G are shared,
+ *   q is B x n and g is B x p (row b belongs to QP b).
+ * Dense: Q has leading dimension ldQ >= n, G has ldG >= n.
+ * CSR (format == DUQUAD_CSR, batch == 1): int32 row pointers (rows+1),
+ *   int32 column indices (sorted within a row), fp64 values, for Q (n rows)
+ *   and G (p rows); the dense pointers are ignored.
+ * on_device: 1 if every pointer is a device pointer, 0 if host.  Device inputs must be
+ *   complete on options.stream; with stream == NULL setup first synchronizes the device.
+ * Ownership: duquad_setup copies/repacks everything into library-owned
+ *   device memory; the caller may free its arrays when setup returns.
+ */
+typedef struct {
+    int64_t n, p, batch;
+    int32_t format;
+    int32_t on_device;
+    const double *Q;
+    int64_t ldQ;
+    const double *G;
+    int64_t ldG;
+    const int32_t *Q_rowptr, *Q_col;
+    const double *Q_val;
+    int64_t Q_nnz;
+    const int32_t *G_rowptr, *G_col;
+    const double *G_val;
+    int64_t G_nnz;
+    const double *q, *g, *lb, *ub;
+    const uint8_t *cone;
+    int32_t cone_all;
+} duquad_problem;
+
+/*
+ * Solver options (fill with duquad_default_options, then override).
+ *   dual_step_scale  dual step = dual_step_scale / L_d; 0.5 is the paper's
+ *                    1/(2 L_d) (reading c1).
+ *   project_dual     1: project NONPOS multipliers onto R_+ (K_d, PAPER.md:295-296,
+ *                    reading c3); 0: K_d = R^p.  ZERO rows are never projected.
+ *   inner_rule       duquad_inner; sigma used by FGM_SIGMA only (must be > 0).
+ *   lambda_min_lb    lower bound on lambda_min(Q) used in L_d (Eq. Ld);
+ *                    must be > 0 when rho == 0 (reading c13).
+ *   l_mode           0: L_in = lambda_max(Q + rho G'G) (north_star);
+ *                    1: L_in = lambda_max(Q) + rho ||G||^2.
+ *   use_graphs       1: capture one outer iteration as a CUDA graph (default 1).
+ *   world_size/rank  row sharding of [Q;G] and G' over world_size GPUs (one
+ *                    process per GPU); nccl_id = 128-byte ncclUniqueId shared by
+ *                    all ranks (see duquad_nccl_unique_id).  1 / 0 = single GPU.
+ *   stream           cudaStream_t the context runs on; NULL = a library stream.
+ *   device           CUDA device ordinal; -1 = the calling thread's current device.
+ */
+typedef struct {
+    double dual_step_scale;
+    int32_t project_dual;
+    int32_t inner_rule;
+    double sigma;
+    double lambda_min_lb;
+    int32_t l_mode;
+    int32_t use_graphs;
+    int32_t world_size;
+    int32_t rank;
+    const void *nccl_id;
+    void *stream;
+    int32_t device;
+    int32_t time_passes;   /* 1: time a sample of pass A / pass B launches with CUDA events */
+} duquad_options;
+
+/* Per-solve report. */
+typedef struct {
+    int64_t outer_iters;        /* K_out executed                                         */
+    int64_t inner_iters_total;  /* (K_out + 1) * K_in  (incl. the last-iterate solve)     */
+    int64_t kernel_launches;    /* this library's kernels launched by the solve           */
+    int64_t matrix_passes;      /* full passes over a stored matrix (matvec counter)      */
+    double ms_device;           /* device time of the whole solve (CUDA events)           */
+    double ms_pass_a;           /* mean duration of a sampled pass-A launch (time_passes) */
+    double ms_pass_b;           /* mean duration of a sampled pass-B launch (time_passes) */
+    int64_t n_timed_a, n_timed_b;
+    double bytes_pass_a;        /* algorithmic bytes per pass-A launch (matrix + vectors) */
+    double bytes_pass_b;        /* algorithmic bytes per pass-B launch                    */
+} duquad_result;
+
+int32_t duquad_abi_version(void);
+const char *duquad_status_string(int32_t status);
+void duquad_default_options(duquad_options *opts);
+
+/*
+ * Rows [*begin, *end) of a `rows`-row matrix owned by `rank` of `world`
+ * (contiguous slices of ceil(rows/world) rows; the last may be short or
+ * empty).  Host-only arithmetic, callable without a GPU.
+ */
+duquad_status duquad_shard_range(int64_t rows, int32_t world, int32_t rank,
+                                 int64_t *begin, int64_t *end);
+
+/* Writes a fresh 128-byte ncclUniqueId into out128 (call on rank 0 only). */
+duquad_status duquad_nccl_unique_id(void *out128);
+
+/*
+ * Validates the problem (dims, finiteness, lb <= ub, rho >= 0) and builds a
+ * context: packs [Q;G] row-major with a 256-byte aligned leading dimension,
+ * stores G' separately (transposed on the device), uploads q, g, lb, ub,
+ * cone tags; sharded mode keeps only this rank's rows and creates the NCCL
+ * communicator.  *out is NULL on failure.
+ */
+duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double rho,
+                           const duquad_options *opts);
+
+/*
+ * Lipschitz constants on the device (north_star (a)); Lanczos with
+ * `iters` steps for lambda_max(Q + rho G'G) (l_mode 0) or lambda_max(Q)
+ * (l_mode 1) and for ||G||^2 = lambda_max(G'G):
+ *   L_in = (1 + safety) * estimate,  L_d = ||G||^2 / (lambda_min_lb + rho ||G||^2).
+ * Stores them in the context (as duquad_set_constants would) and returns
+ * them in the host scalars (any may be NULL).
+ */
+duquad_status duquad_lipschitz(duquad_ctx *ctx, int32_t iters, double safety,
+                               double *L_in, double *L_d, double *normG2);
+
+/* Injects L_in > 0 and L_d >= 0 (parity tests pass identical constants to the oracle). */
+duquad_status duquad_set_constants(duquad_ctx *ctx, double L_in, double L_d);
+
+/*
+ * Runs Algorithm DFOM with `alg`, `outer_iters` >= 1
+ * outer iterations of `inner_iters` >= 1 inner FOM steps each, from
+ * lambda^0 = mu^1 = 0 and u_bar^0 = [0]_U, then one more inner solve at
+ * lambda^K for the last primal iterate (Eq. last_primal).
+ * Results stay on the device (duquad_get_result).  `res` may be NULL.
+ * Returns DUQUAD_ENONFINITE if an iterate became NaN/Inf.
+ */
+duquad_status duquad_solve(duquad_ctx *ctx, int32_t alg, int32_t outer_iters,
+                           int32_t inner_iters, duquad_result *res);
+
+/*
+ * Copies x_last = u_bar(lambda^K) (n, or B x n), x_avg (Eq. average_primal,
+ * PAPER.md:700-706) and lambda^K (p, or B x p) into caller buffers (host or
+ * device per `on_device`; any may be NULL).  Sharded: each rank copies its
+ * local row slice (rows from duquad_shard_range).
+ */
+duquad_status duquad_get_result(duquad_ctx *ctx, double *x_last, double *x_avg, double *lambda,
+                                int32_t on_device);
+
+/*
+ * Registers DEVICE buffers that the next solves fill with the per-outer
+ * trace: lam_trace[(j-1)*p + i] = lambda^j_i and u_trace[(j-1)*n + i] = u_bar^j_i
+ * for j = 1..min(K_out, max_outer) (local slices when sharded).  NULL
+ * disables.  Tracing disables graph capture.  Not supported for batch > 1.
+ */
+duquad_status duquad_set_trace(duquad_ctx *ctx, double *lam_trace, double *u_trace,
+                               int64_t max_outer);
+
+/*
+ * Stopping residuals (§8(a) a8) of x_last (which = 0) or x_avg (which = 1),
+ * computed on the device with fixed-order reductions:
+ *   F = 1/2 x'Qx + q'x,  dist = ||Gx + g - [Gx + g]_K||,
+ *   lag = L_rho(x, lambda^K) by (auglag1) (an upper estimate of
+ *         d_rho(lambda^K) = min_u L_rho(u, lambda^K) when x = u_bar(lambda^K)).
+ * Single QP only.  Any output pointer may be NULL.
+ */
+duquad_status duquad_residuals(duquad_ctx *ctx, int32_t which, double *F, double *dist,
+                               double *lag);
+
+void duquad_destroy(duquad_ctx *ctx);
+
+/* Message for the last failing call on ctx (or of the last failed setup if ctx is NULL). */
+const char *duquad_last_error(const duquad_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DUQUAD_H */

@@ -1,0 +1,821 @@
+// Host runtime + C ABI of the DuQuad hot path (include/duquad.h).
+//
+// Owns the device buffers, the per-solve parameter tables (theta / beta,
+// PAPER.md:358-363, 587-589; averaging weights), the CUDA-graph
+// capture of one outer DFOM iteration, the NCCL communicator of the sharded
+// path, and the launch schedule:
+//
+//   for j = 1 .. K_out + 1:                 (j = K_out+1: last-iterate solve)
+//     for k = 1 .. K_in:                    (Algorithm FOM)
+//       pass A   [Q;G] y -> Qy, w   (k = 1 and j >= 2: fused DFOM step)
+//       (all-gather w)
+//       pass B   G'w -> x, y        (k = K_in: y <- x, running average)
+//       (all-gather y)
+//     advance j
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "duquad_internal.h"
+
+using namespace dq;
+
+struct duquad_ctx {
+    int dev = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    duquad_options opt{};
+    int64_t n = 0, p = 0, batch = 1;
+    int32_t format = DUQUAD_DENSE;
+    double rho = 0.0;
+    // sharding
+    int world = 1, rank = 0;
+    ncclComm_t comm = nullptr;
+    int64_t n_slice = 0, p_slice = 0, r0 = 0, s0 = 0, nloc = 0, ploc = 0;
+    // layout
+    int64_t ld = 0, ldp = 0, ylen = 0, wlen = 0;
+    // device buffers (dense)
+    double *A = nullptr, *GT = nullptr;
+    double *y_full = nullptr, *w_full = nullptr;
+    double *qy = nullptr, *x = nullptr, *xhat = nullptr, *q = nullptr, *lb = nullptr, *ub = nullptr;
+    double *g = nullptr, *mu = nullptr, *lam_prev = nullptr;
+    uint8_t *cone = nullptr;
+    double *lz_vprev = nullptr, *lz_w = nullptr;
+    double *scal = nullptr;       // device scalars
+    double *partials = nullptr;   // kRedGrid * 5
+    OuterParam *d_ops = nullptr;
+    int64_t ops_cap = 0;
+    int32_t *d_j = nullptr, *d_flag = nullptr;
+    // constants
+    double L_in = 0.0, L_d = 0.0;
+    bool have_consts = false;
+    // launch configuration
+    LaunchCfg cfg_a{}, cfg_b{};
+    // trace
+    double *trace_lam = nullptr, *trace_u = nullptr;
+    int64_t trace_max = 0;
+    bool solved = false;
+    std::string err;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+duquad_status fail(duquad_ctx *ctx, duquad_status st, const std::string &msg) {
+    if (ctx)
+        ctx->err = msg;
+    else
+        g_err = msg;
+    return st;
+}
+
+#define CK(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(ctx, DUQUAD_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define NK(call)                                                                              \
+    do {                                                                                      \
+        ncclResult_t r_ = (call);                                                             \
+        if (r_ != ncclSuccess)                                                                \
+            return fail(ctx, DUQUAD_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
+
+inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+template <typename T>
+cudaError_t dalloc(T **p, int64_t count) {
+    size_t bytes = (size_t)std::max<int64_t>(count, 2) * sizeof(T);
+    cudaError_t e = cudaMalloc((void **)p, bytes);
+    if (e == cudaSuccess) e = cudaMemset(*p, 0, bytes);
+    return e;
+}
+
+void free_all(duquad_ctx *c) {
+    double *ds[] = {c->A, c->GT, c->y_full, c->w_full, c->qy, c->x, c->xhat, c->q, c->lb, c->ub,
+                    c->g, c->mu, c->lam_prev, c->lz_vprev, c->lz_w, c->scal, c->partials};
+    for (double *d : ds)
+        if (d) cudaFree(d);
+    if (c->cone) cudaFree(c->cone);
+    if (c->d_ops) cudaFree(c->d_ops);
+    if (c->d_j) cudaFree(c->d_j);
+    if (c->d_flag) cudaFree(c->d_flag);
+    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+}
+
+// device scalar slots
+enum { SC_ALPHA = 0, SC_BETA = 1024, SC_TMP = 2048, SC_TMP2 = 2049, SC_NSCAL = 2056 };
+constexpr int kMaxLanczos = 1000;
+
+struct DevGuard {
+    int prev = -1;
+    explicit DevGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DevGuard() {
+        int cur;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// ----------------------------------------------------------- collectives
+duquad_status allgather_y(duquad_ctx *ctx) {
+    if (ctx->world == 1) return DUQUAD_OK;
+    NK(ncclAllGather(ctx->y_full + ctx->rank * ctx->n_slice, ctx->y_full, (size_t)ctx->n_slice,
+                     ncclDouble, ctx->comm, ctx->stream));
+    return DUQUAD_OK;
+}
+
+duquad_status allgather_w(duquad_ctx *ctx) {
+    if (ctx->world == 1) return DUQUAD_OK;
+    NK(ncclAllGather(ctx->w_full + ctx->rank * ctx->p_slice, ctx->w_full, (size_t)ctx->p_slice,
+                     ncclDouble, ctx->comm, ctx->stream));
+    return DUQUAD_OK;
+}
+
+duquad_status allreduce_sum(duquad_ctx *ctx, double *buf, int count) {
+    if (ctx->world == 1) return DUQUAD_OK;
+    NK(ncclAllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+    return DUQUAD_OK;
+}
+
+// ----------------------------------------------------------- pass args
+PassAArgs make_a(duquad_ctx *c) {
+    PassAArgs a{};
+    a.A = c->A;
+    a.ld = c->ld;
+    a.nq = c->nloc;
+    a.row_begin = 0;
+    a.row_end = c->nloc + c->ploc;
+    a.y = c->y_full;
+    a.qy = c->qy;
+    a.w = c->w_full + c->rank * c->p_slice;
+    a.g = c->g;
+    a.mu = c->mu;
+    a.lam_prev = c->lam_prev;
+    a.cone = c->cone;
+    a.rho = c->rho;
+    a.step = c->have_consts && c->L_d > 0 ? c->opt.dual_step_scale / c->L_d : 0.0;
+    a.project_dual = c->opt.project_dual;
+    a.ops = c->d_ops;
+    a.d_j = c->d_j;
+    a.lin_coef = 1.0;
+    return a;
+}
+
+PassBArgs make_b(duquad_ctx *c) {
+    PassBArgs b{};
+    b.GT = c->GT;
+    b.ldp = c->ldp;
+    b.nrows = c->nloc;
+    b.w = c->w_full;
+    b.qy = c->qy;
+    b.q = c->q;
+    b.lb = c->lb;
+    b.ub = c->ub;
+    b.x = c->x;
+    b.y = c->y_full + c->rank * c->n_slice;
+    b.xhat = c->xhat;
+    b.L_in = c->L_in;
+    b.ops = c->d_ops;
+    b.d_j = c->d_j;
+    b.flag = c->d_flag;
+    b.use_qy = 1;
+    return b;
+}
+
+// One outer DFOM iteration (reads its per-outer scalars through d_j).
+duquad_status run_outer(duquad_ctx *ctx, const std::vector<double> &beta_in, int Kin, int j,
+                        std::vector<cudaEvent_t> *ev) {
+    PassAArgs a = make_a(ctx);
+    PassBArgs b = make_b(ctx);
+    duquad_status st;
+    for (int k = 1; k <= Kin; ++k) {
+        a.first_inner = (k == 1);
+        if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 0], ctx->stream));
+        CK(launch_pass_a(a, MODE_SOLVE, ctx->cfg_a, ctx->stream));
+        if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 1], ctx->stream));
+        if ((st = allgather_w(ctx)) != DUQUAD_OK) return st;
+        if (k == 1 && j >= 2 && ctx->trace_lam && j - 2 < ctx->trace_max)
+            CK(cudaMemcpyAsync(ctx->trace_lam + (j - 2) * ctx->ploc, ctx->lam_prev,
+                               ctx->ploc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+        b.beta_in = beta_in[k];
+        b.last_inner = (k == Kin);
+        if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 2], ctx->stream));
+        CK(launch_pass_b(b, MODE_SOLVE, ctx->cfg_b, ctx->stream));
+        if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 3], ctx->stream));
+        if ((st = allgather_y(ctx)) != DUQUAD_OK) return st;
+    }
+    if (j >= 1 && ctx->trace_u && j - 1 < ctx->trace_max && j >= 1)
+        CK(cudaMemcpyAsync(ctx->trace_u + (j - 1) * ctx->nloc, ctx->x, ctx->nloc * sizeof(double),
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(launch_advance(ctx->d_j, ctx->stream));
+    return DUQUAD_OK;
+}
+
+// Linear operator for Lanczos: out = op(v), v given in the y_full replica.
+//   0: (Q + rho G'G) v     1: G'G v     2: Q v
+duquad_status apply_op(duquad_ctx *ctx, int op, double *out) {
+    PassAArgs a = make_a(ctx);
+    PassBArgs b = make_b(ctx);
+    duquad_status st;
+    if (op == 2) {
+        a.row_end = ctx->nloc;
+        a.qy = out;
+        CK(launch_pass_a(a, MODE_LIN, ctx->cfg_a, ctx->stream));
+        return DUQUAD_OK;
+    }
+    if (op == 1) a.row_begin = ctx->nloc;
+    a.lin_coef = op == 0 ? ctx->rho : 1.0;
+    CK(launch_pass_a(a, MODE_LIN, ctx->cfg_a, ctx->stream));
+    if ((st = allgather_w(ctx)) != DUQUAD_OK) return st;
+    b.use_qy = op == 0 ? 1 : 0;
+    b.out = out;
+    CK(launch_pass_b(b, MODE_LIN, ctx->cfg_b, ctx->stream));
+    return DUQUAD_OK;
+}
+
+// largest eigenvalue of the symmetric tridiagonal (alpha[0..m-1], beta[0..m-2]) by Sturm bisection
+double tridiag_max_eig(const std::vector<double> &al, const std::vector<double> &be, int m) {
+    double lo = 1e300, hi = -1e300;
+    for (int i = 0; i < m; ++i) {
+        const double r = (i > 0 ? std::fabs(be[i - 1]) : 0.0) + (i < m - 1 ? std::fabs(be[i]) : 0.0);
+        lo = std::min(lo, al[i] - r);
+        hi = std::max(hi, al[i] + r);
+    }
+    auto count_below = [&](double x) {   // number of eigenvalues < x
+        int cnt = 0;
+        double d = 1.0;
+        for (int i = 0; i < m; ++i) {
+            const double b2 = i > 0 ? be[i - 1] * be[i - 1] : 0.0;
+            d = (al[i] - x) - (i > 0 ? b2 / d : 0.0);
+            if (d == 0.0) d = -1e-300;
+            if (d < 0) ++cnt;
+        }
+        return cnt;
+    };
+    for (int it = 0; it < 200 && hi - lo > 1e-15 * std::max(std::fabs(lo), std::fabs(hi)); ++it) {
+        const double mid = 0.5 * (lo + hi);
+        if (count_below(mid) >= m)
+            hi = mid;
+        else
+            lo = mid;
+    }
+    return hi;
+}
+
+duquad_status lanczos_max(duquad_ctx *ctx, int op, int iters, double *out) {
+    if (iters < 1) iters = 1;
+    if (iters > kMaxLanczos) iters = kMaxLanczos;
+    double *v = ctx->y_full + ctx->rank * ctx->n_slice;   // local slice of the replica
+    double *sc = ctx->scal;
+    duquad_status st;
+    const int64_t nl = ctx->nloc;
+    CK(cudaMemsetAsync(ctx->y_full, 0, ctx->ylen * sizeof(double), ctx->stream));
+    CK(cudaMemsetAsync(ctx->lz_vprev, 0, std::max<int64_t>(nl, 1) * sizeof(double), ctx->stream));
+    CK(cudaMemsetAsync(sc, 0, SC_NSCAL * sizeof(double), ctx->stream));
+    CK(launch_fill_hash(v, nl, ctx->r0, ctx->stream));
+    CK(launch_dot_partial(v, v, nl, ctx->partials, ctx->stream));
+    CK(launch_reduce_final(ctx->partials, kRedGrid, 1, sc + SC_TMP, ctx->stream));
+    if ((st = allreduce_sum(ctx, sc + SC_TMP, 1)) != DUQUAD_OK) return st;
+    CK(launch_scale_by_rsqrt(v, nl, sc + SC_TMP, nullptr, ctx->stream));
+    int m = 0;
+    for (int it = 0; it < iters; ++it) {
+        if ((st = allgather_y(ctx)) != DUQUAD_OK) return st;
+        if ((st = apply_op(ctx, op, ctx->lz_w)) != DUQUAD_OK) return st;
+        CK(launch_dot_partial(v, ctx->lz_w, nl, ctx->partials, ctx->stream));
+        CK(launch_reduce_final(ctx->partials, kRedGrid, 1, sc + SC_ALPHA + it, ctx->stream));
+        if ((st = allreduce_sum(ctx, sc + SC_ALPHA + it, 1)) != DUQUAD_OK) return st;
+        // beta_0 = 0 lives in sc[SC_BETA + kMaxLanczos] (zeroed)
+        const double *beta_prev = it == 0 ? sc + SC_TMP2 : sc + SC_BETA + it - 1;
+        CK(launch_lanczos_update(ctx->lz_w, v, ctx->lz_vprev, nl, sc + SC_ALPHA + it, beta_prev,
+                                 ctx->partials, ctx->stream));
+        CK(launch_reduce_final(ctx->partials, kRedGrid, 1, sc + SC_TMP, ctx->stream));
+        if ((st = allreduce_sum(ctx, sc + SC_TMP, 1)) != DUQUAD_OK) return st;
+        CK(launch_lanczos_next(v, ctx->lz_vprev, ctx->lz_w, nl, sc + SC_TMP, sc + SC_BETA + it,
+                               ctx->stream));
+        m = it + 1;
+    }
+    std::vector<double> al(m), be(m);
+    CK(cudaMemcpyAsync(al.data(), sc + SC_ALPHA, m * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(be.data(), sc + SC_BETA, m * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    // stop at an invariant subspace (beta ~ 0)
+    int mm = m;
+    double amax = 0.0;
+    for (int i = 0; i < m; ++i) amax = std::max(amax, std::fabs(al[i]));
+    for (int i = 0; i < m - 1; ++i)
+        if (!(std::fabs(be[i]) > 1e-14 * std::max(amax, 1e-300))) {
+            mm = i + 1;
+            break;
+        }
+    *out = tridiag_max_eig(al, be, mm);
+    return DUQUAD_OK;
+}
+
+bool finite_host(const double *v, int64_t rows, int64_t cols, int64_t ld) {
+    for (int64_t r = 0; r < rows; ++r)
+        for (int64_t c = 0; c < cols; ++c)
+            if (!std::isfinite(v[r * ld + c])) return false;
+    return true;
+}
+
+duquad_status upload_vec(duquad_ctx *ctx, double *dst, const double *src, int64_t count) {
+    if (count <= 0) return DUQUAD_OK;
+    CK(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyDefault, ctx->stream));
+    return DUQUAD_OK;
+}
+
+}  // namespace
+
+// ======================================================================= ABI
+extern "C" {
+
+int32_t duquad_abi_version(void) { return DUQUAD_ABI_VERSION; }
+
+const char *duquad_status_string(int32_t s) {
+    switch (s) {
+        case DUQUAD_OK: return "ok";
+        case DUQUAD_EINVAL: return "invalid argument";
+        case DUQUAD_ENOMEM: return "out of memory";
+        case DUQUAD_ECUDA: return "CUDA error";
+        case DUQUAD_ENCCL: return "NCCL error";
+        case DUQUAD_ENONFINITE: return "non-finite iterate";
+        case DUQUAD_ENODEV: return "no suitable CUDA device";
+        case DUQUAD_ESTATE: return "call out of order";
+        default: return "unknown status";
+    }
+}
+
+void duquad_default_options(duquad_options *o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof(*o));
+    o->dual_step_scale = 0.5;
+    o->project_dual = 1;
+    o->inner_rule = DUQUAD_INNER_FGM;
+    o->sigma = 0.0;
+    o->lambda_min_lb = 0.0;
+    o->l_mode = 0;
+    o->use_graphs = 1;
+    o->world_size = 1;
+    o->rank = 0;
+    o->nccl_id = nullptr;
+    o->stream = nullptr;
+    o->device = -1;
+    o->time_passes = 0;
+}
+
+duquad_status duquad_shard_range(int64_t rows, int32_t world, int32_t rank, int64_t *begin,
+                                 int64_t *end) {
+    if (rows < 0 || world < 1 || rank < 0 || rank >= world || !begin || !end)
+        return fail(nullptr, DUQUAD_EINVAL, "duquad_shard_range: bad arguments");
+    const int64_t slice = (rows + world - 1) / world;
+    *begin = std::min<int64_t>(rows, (int64_t)rank * slice);
+    *end = std::min<int64_t>(rows, *begin + slice);
+    return DUQUAD_OK;
+}
+
+duquad_status duquad_nccl_unique_id(void *out128) {
+    duquad_ctx *ctx = nullptr;
+    if (!out128) return fail(nullptr, DUQUAD_EINVAL, "null output");
+    ncclUniqueId id;
+    NK(ncclGetUniqueId(&id));
+    std::memcpy(out128, &id, sizeof(id));
+    return DUQUAD_OK;
+}
+
+const char *duquad_last_error(const duquad_ctx *ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+void duquad_destroy(duquad_ctx *ctx) {
+    if (!ctx) return;
+    {
+        DevGuard guard(ctx->dev);
+        if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+        free_all(ctx);
+    }
+    delete ctx;
+}
+
+duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double rho,
+                           const duquad_options *opts_in) {
+    if (!out) return fail(nullptr, DUQUAD_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (!prob) return fail(nullptr, DUQUAD_EINVAL, "prob is NULL");
+    duquad_options opt;
+    duquad_default_options(&opt);
+    if (opts_in) opt = *opts_in;
+    const int64_t n = prob->n, p = prob->p;
+    if (n < 1 || p < 0) return fail(nullptr, DUQUAD_EINVAL, "need n >= 1 and p >= 0");
+    if (!(rho >= 0.0) || !std::isfinite(rho)) return fail(nullptr, DUQUAD_EINVAL, "rho must be finite and >= 0");
+    if (prob->batch != 1) return fail(nullptr, DUQUAD_EINVAL, "batch > 1 not supported by this build");
+    if (prob->format != DUQUAD_DENSE) return fail(nullptr, DUQUAD_EINVAL, "CSR not supported by this build");
+    if (!prob->Q || !prob->q || !prob->lb || !prob->ub || (p > 0 && (!prob->G || !prob->g)))
+        return fail(nullptr, DUQUAD_EINVAL, "missing problem array");
+    if (prob->ldQ < n || (p > 0 && prob->ldG < n)) return fail(nullptr, DUQUAD_EINVAL, "leading dimension < n");
+    if (!prob->cone && prob->cone_all != DUQUAD_CONE_ZERO && prob->cone_all != DUQUAD_CONE_NONPOS)
+        return fail(nullptr, DUQUAD_EINVAL, "bad cone_all");
+    if (!(opt.dual_step_scale > 0.0)) return fail(nullptr, DUQUAD_EINVAL, "dual_step_scale must be > 0");
+    if (opt.inner_rule < 0 || opt.inner_rule > 2) return fail(nullptr, DUQUAD_EINVAL, "bad inner_rule");
+    if (opt.inner_rule == DUQUAD_INNER_FGM_SIGMA && !(opt.sigma > 0.0))
+        return fail(nullptr, DUQUAD_EINVAL, "FGM_SIGMA needs sigma > 0");
+    if (opt.world_size < 1 || opt.rank < 0 || opt.rank >= opt.world_size)
+        return fail(nullptr, DUQUAD_EINVAL, "bad world_size / rank");
+    if (opt.world_size > 1 && !opt.nccl_id) return fail(nullptr, DUQUAD_EINVAL, "sharded setup needs nccl_id");
+    if (!prob->on_device) {   // host data: validate here (device data is validated by a kernel)
+        if (!finite_host(prob->Q, n, n, prob->ldQ) || (p > 0 && !finite_host(prob->G, p, n, prob->ldG)) ||
+            !finite_host(prob->q, 1, n, n) || (p > 0 && !finite_host(prob->g, 1, p, p)))
+            return fail(nullptr, DUQUAD_EINVAL, "non-finite problem data");
+        for (int64_t i = 0; i < n; ++i)
+            if (std::isnan(prob->lb[i]) || std::isnan(prob->ub[i]) || prob->lb[i] > prob->ub[i] ||
+                prob->lb[i] == INFINITY || prob->ub[i] == -INFINITY)
+                return fail(nullptr, DUQUAD_EINVAL, "box needs lb <= ub (lb < +inf, ub > -inf)");
+        if (prob->cone)
+            for (int64_t i = 0; i < p; ++i)
+                if (prob->cone[i] > 1) return fail(nullptr, DUQUAD_EINVAL, "bad cone tag");
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(nullptr, DUQUAD_ENODEV, "no CUDA device");
+    duquad_ctx *ctx = new duquad_ctx();
+    ctx->opt = opt;
+    ctx->n = n;
+    ctx->p = p;
+    ctx->rho = rho;
+    ctx->format = prob->format;
+    if (opt.device >= 0)
+        ctx->dev = opt.device;
+    else
+        cudaGetDevice(&ctx->dev);
+    DevGuard guard(ctx->dev);
+    auto bail = [&](duquad_status st) {
+        g_err = ctx->err;
+        duquad_destroy(ctx);
+        return st;
+    };
+#define CKS(call)                                                                        \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess) {                                                         \
+            ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);               \
+            return bail(e_ == cudaErrorMemoryAllocation ? DUQUAD_ENOMEM : DUQUAD_ECUDA); \
+        }                                                                                \
+    } while (0)
+    cudaDeviceProp prop;
+    CKS(cudaGetDeviceProperties(&prop, ctx->dev));
+    if (prop.major != 10) {
+        ctx->err = std::string("device is not sm_100 (got sm_") + std::to_string(prop.major) +
+                   std::to_string(prop.minor) + ")";
+        return bail(DUQUAD_ENODEV);
+    }
+    ctx->num_sms = prop.multiProcessorCount;
+    if (opt.stream) {
+        ctx->stream = (cudaStream_t)opt.stream;
+    } else {
+        CKS(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        ctx->own_stream = true;
+    }
+    // ---- sharding
+    ctx->world = opt.world_size;
+    ctx->rank = opt.rank;
+    ctx->n_slice = (n + ctx->world - 1) / ctx->world;
+    ctx->p_slice = (p + ctx->world - 1) / ctx->world;
+    ctx->r0 = std::min<int64_t>(n, ctx->rank * ctx->n_slice);
+    ctx->nloc = std::min<int64_t>(n, ctx->r0 + ctx->n_slice) - ctx->r0;
+    ctx->s0 = std::min<int64_t>(p, ctx->rank * ctx->p_slice);
+    ctx->ploc = std::min<int64_t>(p, ctx->s0 + ctx->p_slice) - ctx->s0;
+    if (ctx->world > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, opt.nccl_id, sizeof(id));
+        ncclResult_t r = ncclCommInitRank(&ctx->comm, ctx->world, id, ctx->rank);
+        if (r != ncclSuccess) {
+            ctx->err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+            return bail(DUQUAD_ENCCL);
+        }
+    }
+    // ---- layout: 256-byte aligned rows, vectors zero-padded
+    ctx->ld = round_up(n, 32);
+    ctx->ldp = round_up(std::max<int64_t>(p, 1), 32);
+    if (p == 0) ctx->ldp = 0;
+    ctx->ylen = round_up(std::max(ctx->ld, ctx->world * ctx->n_slice), 32);
+    ctx->wlen = round_up(std::max(ctx->ldp, ctx->world * ctx->p_slice), 32);
+    const int64_t rows = ctx->nloc + ctx->ploc;
+    CKS(dalloc(&ctx->A, rows * ctx->ld));
+    CKS(dalloc(&ctx->GT, ctx->nloc * std::max<int64_t>(ctx->ldp, 1)));
+    CKS(dalloc(&ctx->y_full, ctx->ylen));
+    CKS(dalloc(&ctx->w_full, ctx->wlen));
+    CKS(dalloc(&ctx->qy, ctx->nloc));
+    CKS(dalloc(&ctx->x, ctx->nloc));
+    CKS(dalloc(&ctx->xhat, ctx->nloc));
+    CKS(dalloc(&ctx->q, ctx->nloc));
+    CKS(dalloc(&ctx->lb, ctx->nloc));
+    CKS(dalloc(&ctx->ub, ctx->nloc));
+    CKS(dalloc(&ctx->lz_vprev, ctx->nloc));
+    CKS(dalloc(&ctx->lz_w, ctx->nloc));
+    CKS(dalloc(&ctx->g, ctx->ploc));
+    CKS(dalloc(&ctx->mu, ctx->ploc));
+    CKS(dalloc(&ctx->lam_prev, ctx->ploc));
+    CKS(dalloc(&ctx->cone, ctx->ploc));
+    CKS(dalloc(&ctx->scal, SC_NSCAL));
+    CKS(dalloc(&ctx->partials, kRedGrid * 8));
+    CKS(dalloc(&ctx->d_j, 4));
+    CKS(dalloc(&ctx->d_flag, 4));
+    cudaStream_t s = ctx->stream;
+    // Device inputs may still be in flight on another stream of the caller (e.g. torch's):
+    // with a library-owned stream, wait for the whole device before reading them.
+    if (prob->on_device && ctx->own_stream) CKS(cudaDeviceSynchronize());
+    // ---- pack [Q_r; G_r] and G'_r
+    CKS(cudaMemcpy2DAsync(ctx->A, ctx->ld * sizeof(double), prob->Q + ctx->r0 * prob->ldQ,
+                          prob->ldQ * sizeof(double), n * sizeof(double), ctx->nloc, cudaMemcpyDefault, s));
+    if (p > 0) {
+        if (ctx->ploc > 0)
+            CKS(cudaMemcpy2DAsync(ctx->A + ctx->nloc * ctx->ld, ctx->ld * sizeof(double),
+                                  prob->G + ctx->s0 * prob->ldG, prob->ldG * sizeof(double),
+                                  n * sizeof(double), ctx->ploc, cudaMemcpyDefault, s));
+        // G' rows r0..r0+nloc = columns r0.. of G; stage G on the device when it is on the host
+        const double *Gd = prob->G;
+        double *Gtmp = nullptr;
+        if (!prob->on_device) {
+            CKS(cudaMalloc(&Gtmp, (size_t)p * n * sizeof(double)));
+            CKS(cudaMemcpy2DAsync(Gtmp, n * sizeof(double), prob->G, prob->ldG * sizeof(double),
+                                  n * sizeof(double), p, cudaMemcpyHostToDevice, s));
+            Gd = Gtmp;
+        }
+        cudaError_t e = launch_transpose(Gd, prob->on_device ? prob->ldG : n, p, ctx->r0, ctx->nloc,
+                                         ctx->GT, ctx->ldp, s);
+        if (Gtmp) {
+            cudaStreamSynchronize(s);
+            cudaFree(Gtmp);
+        }
+        CKS(e);
+    }
+    if (upload_vec(ctx, ctx->q, prob->q + ctx->r0, ctx->nloc) ||
+        upload_vec(ctx, ctx->lb, prob->lb + ctx->r0, ctx->nloc) ||
+        upload_vec(ctx, ctx->ub, prob->ub + ctx->r0, ctx->nloc) ||
+        (p > 0 && upload_vec(ctx, ctx->g, prob->g + ctx->s0, ctx->ploc)))
+        return bail(DUQUAD_ECUDA);
+    if (p > 0 && ctx->ploc > 0) {
+        if (prob->cone)
+            CKS(cudaMemcpyAsync(ctx->cone, prob->cone + ctx->s0, ctx->ploc, cudaMemcpyDefault, s));
+        else
+            CKS(cudaMemsetAsync(ctx->cone, prob->cone_all, ctx->ploc, s));
+    }
+    if (prob->on_device) {
+        CKS(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int32_t), s));
+        CKS(launch_check(ctx->A, rows, n, ctx->ld, ctx->d_flag, s));
+        CKS(launch_check(ctx->q, 1, ctx->nloc, ctx->nloc, ctx->d_flag, s));
+        if (ctx->ploc > 0) CKS(launch_check(ctx->g, 1, ctx->ploc, ctx->ploc, ctx->d_flag, s));
+        CKS(launch_check_box(ctx->lb, ctx->ub, ctx->nloc, ctx->d_flag, s));
+        int32_t flag = 0;
+        CKS(cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(flag), cudaMemcpyDeviceToHost, s));
+        CKS(cudaStreamSynchronize(s));
+        if (flag) {
+            ctx->err = "non-finite problem data or lb > ub";
+            return bail(DUQUAD_EINVAL);
+        }
+    }
+    // ---- launch configuration: persistent grid, one CTA per SM, vector staged in smem
+    const size_t smem_a = (size_t)ctx->ld * sizeof(double);
+    const size_t smem_b = (size_t)std::max<int64_t>(ctx->ldp, 2) * sizeof(double);
+    if (smem_a > (size_t)prop.sharedMemPerBlockOptin || smem_b > (size_t)prop.sharedMemPerBlockOptin) {
+        ctx->err = "dense path needs the vector in shared memory: n and p must be <= " +
+                   std::to_string(prop.sharedMemPerBlockOptin / 8);
+        return bail(DUQUAD_EINVAL);
+    }
+    CKS(configure_pass_kernels(smem_a, smem_b));
+    const int wpc = pass_threads() / 32;
+    ctx->cfg_a = {(int)std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms, (rows + wpc - 1) / wpc)),
+                  pass_threads(), smem_a};
+    ctx->cfg_b = {(int)std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms, (ctx->nloc + wpc - 1) / wpc)),
+                  pass_threads(), smem_b};
+    CKS(cudaStreamSynchronize(s));
+    *out = ctx;
+    return DUQUAD_OK;
+#undef CKS
+}
+
+duquad_status duquad_set_constants(duquad_ctx *ctx, double L_in, double L_d) {
+    if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
+    if (!(L_in > 0.0) || !std::isfinite(L_in) || !(L_d >= 0.0) || !std::isfinite(L_d))
+        return fail(ctx, DUQUAD_EINVAL, "need L_in > 0 and L_d >= 0, finite");
+    if (ctx->p > 0 && !(L_d > 0.0)) return fail(ctx, DUQUAD_EINVAL, "need L_d > 0 when p > 0");
+    ctx->L_in = L_in;
+    ctx->L_d = L_d;
+    ctx->have_consts = true;
+    return DUQUAD_OK;
+}
+
+duquad_status duquad_lipschitz(duquad_ctx *ctx, int32_t iters, double safety, double *L_in_out,
+                               double *L_d_out, double *normG2_out) {
+    if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
+    if (!(safety >= 0.0)) return fail(ctx, DUQUAD_EINVAL, "safety must be >= 0");
+    DevGuard guard(ctx->dev);
+    duquad_status st;
+    double normG2 = 0.0, lmax = 0.0;
+    if (ctx->p > 0 && (st = lanczos_max(ctx, 1, iters, &normG2)) != DUQUAD_OK) return st;
+    if (ctx->opt.l_mode == 0 && ctx->p > 0) {
+        if ((st = lanczos_max(ctx, 0, iters, &lmax)) != DUQUAD_OK) return st;
+    } else {
+        if ((st = lanczos_max(ctx, 2, iters, &lmax)) != DUQUAD_OK) return st;
+        lmax += ctx->rho * normG2;
+    }
+    const double L_in = (1.0 + safety) * lmax;
+    const double denom = ctx->opt.lambda_min_lb + ctx->rho * normG2;
+    double L_d = 0.0;
+    if (ctx->p > 0) {
+        if (!(denom > 0.0))
+            return fail(ctx, DUQUAD_EINVAL,
+                        "L_d undefined: rho == 0 needs lambda_min_lb > 0 (Eq. Ld, PAPER.md:277)");
+        L_d = normG2 / denom;
+    }
+    if ((st = duquad_set_constants(ctx, L_in, ctx->p > 0 ? L_d : 0.0)) != DUQUAD_OK) return st;
+    if (L_in_out) *L_in_out = L_in;
+    if (L_d_out) *L_d_out = L_d;
+    if (normG2_out) *normG2_out = normG2;
+    return DUQUAD_OK;
+}
+
+duquad_status duquad_set_trace(duquad_ctx *ctx, double *lam_trace, double *u_trace, int64_t max_outer) {
+    if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
+    DevGuard guard(ctx->dev);
+    if (ctx->own_stream) CK(cudaDeviceSynchronize());   // caller's buffers may be in flight
+    ctx->trace_lam = lam_trace;
+    ctx->trace_u = u_trace;
+    ctx->trace_max = (lam_trace || u_trace) ? max_outer : 0;
+    return DUQUAD_OK;
+}
+
+duquad_status duquad_solve(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t inner, duquad_result *res) {
+    if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
+    if (alg != DUQUAD_DGM && alg != DUQUAD_DFGM) return fail(ctx, DUQUAD_EINVAL, "bad alg");
+    if (outer < 1 || inner < 1) return fail(ctx, DUQUAD_EINVAL, "need outer_iters >= 1 and inner_iters >= 1");
+    if (!ctx->have_consts) return fail(ctx, DUQUAD_ESTATE, "constants not set (duquad_lipschitz or duquad_set_constants)");
+    DevGuard guard(ctx->dev);
+    cudaStream_t s = ctx->stream;
+    const int K = outer, Kin = inner;
+    // ---- host tables (fp64, PAPER.md:358-363 / 587-589 / 700-706)
+    std::vector<double> theta(K + 3, 0.0);
+    theta[1] = 1.0;
+    for (int k = 1; k < K + 2; ++k) theta[k + 1] = (1.0 + std::sqrt(1.0 + 4.0 * theta[k] * theta[k])) / 2.0;
+    std::vector<double> beta_in(Kin + 1, 0.0);
+    if (ctx->opt.inner_rule == DUQUAD_INNER_FGM) {
+        std::vector<double> th(Kin + 2, 0.0);
+        th[1] = 1.0;
+        for (int k = 1; k < Kin + 1; ++k) th[k + 1] = (1.0 + std::sqrt(1.0 + 4.0 * th[k] * th[k])) / 2.0;
+        for (int k = 1; k <= Kin; ++k) beta_in[k] = (th[k] - 1.0) / th[k + 1];
+    } else if (ctx->opt.inner_rule == DUQUAD_INNER_FGM_SIGMA) {
+        const double b = (std::sqrt(ctx->L_in) - std::sqrt(ctx->opt.sigma)) /
+                         (std::sqrt(ctx->L_in) + std::sqrt(ctx->opt.sigma));
+        for (int k = 1; k <= Kin; ++k) beta_in[k] = b;
+    }
+    std::vector<OuterParam> ops(K + 2);
+    double S = 0.0;
+    for (int j = 1; j <= K; ++j) {
+        const double omega = alg == DUQUAD_DFGM ? theta[j] : 1.0;
+        S += omega;
+        ops[j].avg_w = omega / S;
+        ops[j].dual_update = j >= 2;
+        ops[j].beta_out = (j >= 2 && alg == DUQUAD_DFGM) ? (theta[j - 1] - 1.0) / theta[j] : 0.0;
+    }
+    ops[K + 1] = OuterParam{0.0, 0.0, 1, 0};   // last-iterate solve at lambda^K (mu := lambda^K)
+    if (ctx->ops_cap < K + 2) {
+        if (ctx->d_ops) cudaFree(ctx->d_ops);
+        ctx->d_ops = nullptr;
+        CK(cudaMalloc(&ctx->d_ops, (K + 2) * sizeof(OuterParam)));
+        ctx->ops_cap = K + 2;
+    }
+    CK(cudaMemcpyAsync(ctx->d_ops, ops.data(), (K + 2) * sizeof(OuterParam), cudaMemcpyHostToDevice, s));
+    // ---- initial state
+    CK(launch_init_state(ctx->x, ctx->y_full + ctx->rank * ctx->n_slice, ctx->xhat, ctx->lb, ctx->ub,
+                         ctx->nloc, ctx->mu, ctx->lam_prev, ctx->ploc, ctx->d_j, ctx->d_flag, s));
+    duquad_status st;
+    if ((st = allgather_y(ctx)) != DUQUAD_OK) return st;
+    const bool tracing = ctx->trace_lam || ctx->trace_u;
+    const bool graphs = ctx->opt.use_graphs && !tracing;
+    const int j_timed = ctx->opt.time_passes ? std::max(1, (K + 1) / 2) : -1;
+    std::vector<cudaEvent_t> ev;
+    if (j_timed > 0) {
+        ev.resize(4 * Kin);
+        for (auto &e : ev) CK(cudaEventCreate(&e));
+    }
+    cudaGraphExec_t gexec = nullptr;
+    cudaGraph_t graph = nullptr;
+    if (graphs) {
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        st = run_outer(ctx, beta_in, Kin, -1, nullptr);
+        cudaError_t e = cudaStreamEndCapture(s, &graph);
+        if (st != DUQUAD_OK) return st;
+        CK(e);
+        CK(cudaGraphInstantiate(&gexec, graph, 0));
+    }
+    cudaEvent_t t0, t1;
+    CK(cudaEventCreate(&t0));
+    CK(cudaEventCreate(&t1));
+    CK(cudaEventRecord(t0, s));
+    for (int j = 1; j <= K + 1; ++j) {
+        if (j == j_timed) {
+            st = run_outer(ctx, beta_in, Kin, j, &ev);
+        } else if (graphs) {
+            cudaError_t e = cudaGraphLaunch(gexec, s);
+            st = e == cudaSuccess ? DUQUAD_OK : fail(ctx, DUQUAD_ECUDA, std::string("cudaGraphLaunch: ") + cudaGetErrorString(e));
+        } else {
+            st = run_outer(ctx, beta_in, Kin, j, nullptr);
+        }
+        if (st != DUQUAD_OK) break;
+    }
+    CK(cudaEventRecord(t1, s));
+    cudaError_t esync = cudaStreamSynchronize(s);
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (graph) cudaGraphDestroy(graph);
+    if (st != DUQUAD_OK) return st;
+    CK(esync);
+    int32_t flag = 0;
+    CK(cudaMemcpy(&flag, ctx->d_flag, sizeof(flag), cudaMemcpyDeviceToHost));
+    if (res) {
+        std::memset(res, 0, sizeof(*res));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, t0, t1);
+        res->ms_device = ms;
+        res->outer_iters = K;
+        res->inner_iters_total = (int64_t)(K + 1) * Kin;
+        res->kernel_launches = 1 + (int64_t)(K + 1) * (2 * Kin + 1);
+        res->matrix_passes = (int64_t)(K + 1) * Kin * 2;
+        const double nn = (double)ctx->n, nl = (double)ctx->nloc, pl = (double)ctx->ploc, pp = (double)ctx->p;
+        res->bytes_pass_a = 8.0 * ((nl + pl) * nn + nn + nl + 3.0 * pl);
+        res->bytes_pass_b = 8.0 * (nl * pp + pp + 8.0 * nl);
+        if (j_timed > 0) {
+            double sa = 0, sb = 0;
+            for (int k = 0; k < Kin; ++k) {
+                float a = 0.f, b = 0.f;
+                cudaEventElapsedTime(&a, ev[4 * k], ev[4 * k + 1]);
+                cudaEventElapsedTime(&b, ev[4 * k + 2], ev[4 * k + 3]);
+                sa += a;
+                sb += b;
+            }
+            res->ms_pass_a = sa / Kin;
+            res->ms_pass_b = sb / Kin;
+            res->n_timed_a = Kin;
+            res->n_timed_b = Kin;
+        }
+    }
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    for (auto &e : ev) cudaEventDestroy(e);
+    ctx->solved = true;
+    if (flag) return fail(ctx, DUQUAD_ENONFINITE, "an iterate became non-finite");
+    return DUQUAD_OK;
+}
+
+duquad_status duquad_get_result(duquad_ctx *ctx, double *x_last, double *x_avg, double *lam, int32_t on_device) {
+    if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
+    if (!ctx->solved) return fail(ctx, DUQUAD_ESTATE, "no solve has run");
+    DevGuard guard(ctx->dev);
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (x_last) CK(cudaMemcpyAsync(x_last, ctx->x, ctx->nloc * sizeof(double), kind, ctx->stream));
+    if (x_avg) CK(cudaMemcpyAsync(x_avg, ctx->xhat, ctx->nloc * sizeof(double), kind, ctx->stream));
+    if (lam && ctx->ploc > 0) CK(cudaMemcpyAsync(lam, ctx->lam_prev, ctx->ploc * sizeof(double), kind, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return DUQUAD_OK;
+}
+
+duquad_status duquad_residuals(duquad_ctx *ctx, int32_t which, double *F, double *dist, double *lag) {
+    if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
+    if (!ctx->solved) return fail(ctx, DUQUAD_ESTATE, "no solve has run");
+    if (which != 0 && which != 1) return fail(ctx, DUQUAD_EINVAL, "which must be 0 (x_last) or 1 (x_avg)");
+    DevGuard guard(ctx->dev);
+    cudaStream_t s = ctx->stream;
+    duquad_status st;
+    const double *xv = which == 0 ? ctx->x : ctx->xhat;
+    double *yl = ctx->y_full + ctx->rank * ctx->n_slice;
+    CK(cudaMemcpyAsync(yl, xv, ctx->nloc * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if ((st = allgather_y(ctx)) != DUQUAD_OK) return st;
+    PassAArgs a = make_a(ctx);
+    a.lin_coef = 1.0;
+    CK(launch_pass_a(a, MODE_LIN, ctx->cfg_a, s));          // qy = Q x, w_local = G x
+    CK(launch_residual_partial(xv, ctx->qy, ctx->q, ctx->nloc, ctx->w_full + ctx->rank * ctx->p_slice, ctx->g,
+                               ctx->lam_prev, ctx->cone, ctx->ploc, ctx->rho, ctx->partials, s));
+    double *acc = ctx->scal + SC_TMP;
+    CK(launch_reduce_final(ctx->partials, kRedGrid, 5, acc, s));
+    if ((st = allreduce_sum(ctx, acc, 5)) != DUQUAD_OK) return st;
+    double h[5];
+    CK(cudaMemcpyAsync(h, acc, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (F) *F = h[0];
+    if (dist) *dist = std::sqrt(h[1]);
+    if (lag) *lag = ctx->rho > 0 ? h[0] + 0.5 * ctx->rho * h[2] - h[3] / (2.0 * ctx->rho) : h[0] + h[4];
+    return DUQUAD_OK;
+}
+
+}  // extern "C"

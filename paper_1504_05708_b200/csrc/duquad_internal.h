@@ -1,0 +1,122 @@
+// Internal declarations shared by the host runtime (capi.cu) and the kernel
+// translation units.  Not part of the public ABI (see include/duquad.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/duquad.h"
+
+namespace dq {
+
+constexpr int kWarp = 32;
+
+// Per-outer-iteration scalars read by the fused kernels through a device
+// index (so that one captured CUDA graph serves every outer iteration).
+struct OuterParam {
+    double beta_out;   // beta_{j-1} used for mu^{j} = lambda^{j-1} + beta (lambda^{j-1} - lambda^{j-2})
+    double avg_w;      // omega_j / S_j for the running primal average (0 = no update)
+    int32_t dual_update;  // 1: the first inner pass A of this outer iteration does the DFOM step
+    int32_t pad;
+};
+
+enum PassMode : int { MODE_SOLVE = 0, MODE_LIN = 1 };
+
+// ---------------------------------------------------------------- pass A
+// Streams rows [row_begin, row_end) of the local stacked matrix A = [Q_r; G_r]
+// (row-major, leading dimension ld doubles, zero-padded) against y (full
+// replica, ld doubles, zero-padded) staged in shared memory.
+struct PassAArgs {
+    const double *A;
+    int64_t ld;
+    int64_t nq;          // local Q rows (rows < nq are Q rows)
+    int64_t row_begin, row_end;
+    const double *y;
+    double *qy;          // Q rows: qy[row] = (Q y)_row
+    // G rows (k = row - nq):
+    double *w;           // w[k]  (local slice of the full w replica)
+    const double *g;
+    double *mu;
+    double *lam_prev;
+    const uint8_t *cone;
+    double rho;
+    double step;         // dual_step_scale / L_d
+    int32_t project_dual;
+    int32_t first_inner; // this launch is the first inner step of an outer iteration
+    const OuterParam *ops;
+    const int32_t *d_j;
+    double lin_coef;     // MODE_LIN: w[k] = lin_coef * (G y)_k
+};
+
+// ---------------------------------------------------------------- pass B
+// Streams the local rows of G' (row-major, leading dim ldp, zero-padded)
+// against the full w replica staged in shared memory.
+struct PassBArgs {
+    const double *GT;
+    int64_t ldp;
+    int64_t nrows;
+    const double *w;
+    const double *qy;
+    const double *q, *lb, *ub;
+    double *x;
+    double *y;           // local slice of the full y replica
+    double *xhat;
+    double L_in;
+    double beta_in;
+    int32_t last_inner;
+    int32_t use_qy;      // MODE_LIN: out = (use_qy ? qy : 0) + G'w
+    const OuterParam *ops;
+    const int32_t *d_j;
+    int32_t *flag;       // set to 1 if an iterate is non-finite
+    double *out;         // MODE_LIN output
+};
+
+struct LaunchCfg {
+    int grid;
+    int threads;
+    size_t smem;
+};
+
+// kernels_dense.cu
+cudaError_t launch_pass_a(const PassAArgs &a, int mode, const LaunchCfg &cfg, cudaStream_t s);
+cudaError_t launch_pass_b(const PassBArgs &b, int mode, const LaunchCfg &cfg, cudaStream_t s);
+int pass_threads();
+cudaError_t configure_pass_kernels(size_t smem_a, size_t smem_b);
+cudaError_t launch_init_state(double *x, double *y, double *xhat, const double *lb, const double *ub,
+                              int64_t n, double *mu, double *lam_prev, int64_t p, int32_t *d_j,
+                              int32_t *flag, cudaStream_t s);
+cudaError_t launch_advance(int32_t *d_j, cudaStream_t s);
+cudaError_t launch_transpose(const double *G, int64_t ldG, int64_t p, int64_t col0, int64_t ncols,
+                             double *GT, int64_t ldp, cudaStream_t s);
+cudaError_t launch_check(const double *v, int64_t rows, int64_t cols, int64_t ld, int32_t *flag,
+                         cudaStream_t s);
+cudaError_t launch_check_box(const double *lb, const double *ub, int64_t n, int32_t *flag,
+                             cudaStream_t s);
+// Deterministic reductions: `parts` partial sums per CTA, then a fixed-order final sum.
+constexpr int kRedGrid = 148;
+constexpr int kRedThreads = 256;
+cudaError_t launch_dot_partial(const double *a, const double *b, int64_t n, double *partials,
+                               cudaStream_t s);
+cudaError_t launch_reduce_final(const double *partials, int nparts, int nvals, double *out,
+                                cudaStream_t s);
+// Lanczos helpers
+cudaError_t launch_fill_hash(double *v, int64_t n, int64_t offset, cudaStream_t s);
+cudaError_t launch_scale_by_rsqrt(double *v, int64_t n, const double *sumsq, double *beta_out,
+                                  cudaStream_t s);
+cudaError_t launch_lanczos_update(double *w, const double *v, const double *vprev, int64_t n,
+                                  const double *alpha, const double *beta_prev, double *partials,
+                                  cudaStream_t s);
+cudaError_t launch_lanczos_next(double *v, double *vprev, const double *w, int64_t n,
+                                const double *sumsq, double *beta, cudaStream_t s);
+// Residual partials: per CTA 5 values:
+//   [0] sum x*qy/2 + q*x over local n rows   [1] sum dist_K(r)^2, r = Gx+g (local p rows)
+//   [2] sum dist_K(r + lam/rho)^2            [3] sum lam^2        [4] sum lam * r
+cudaError_t launch_residual_partial(const double *x, const double *qy, const double *q, int64_t n,
+                                    const double *Gx, const double *g, const double *lam,
+                                    const uint8_t *cone, int64_t p, double rho, double *partials,
+                                    cudaStream_t s);
+
+}  // namespace dq

@@ -1,0 +1,471 @@
+// Dense sm_100a kernels of the DuQuad hot path.
+//
+// Pass A (K1): one streaming pass over the row-stacked [Q;G] (HBM-bound GEMV)
+//   Q rows -> Qy;  G rows -> w = [mu + rho (G y + g)]_{K polar}  (grad of (auglag1),
+//   PAPER.md:243-251), and on the first inner step of an outer iteration the
+//   fused DFOM dual step lambda = [mu + step (r - s)]_{K_d}, mu <- lambda + beta (lambda - lambda_prev)
+//    -- all row-local, so no extra matrix pass.
+// Pass B (K2): one streaming pass over the stored G' (n x p)
+//   t = G'w; grad = Qy + q + t; x+ = [y - grad/L]_U;
+//   y+ = x+ + beta (x+ - x); running primal average on the last inner step.
+//
+// Design: persistent grid of one CTA per SM; the dense vector
+// (y for pass A, w for pass B) is staged once into shared memory; each warp
+// owns whole rows and streams them with 128-bit L1-bypassing loads, U loads in
+// flight per lane; row reduction by a fixed xor-shuffle tree, so every row's
+// value is independent of the grid and of the sharding (bitwise reproducible).
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "duquad_internal.h"
+
+namespace dq {
+
+namespace {
+
+constexpr int kThreads = 512;  // threads per CTA of the pass kernels
+constexpr int kUnroll = 8;     // 16-byte loads in flight per lane per row chunk
+
+__device__ __forceinline__ double2 ldg_stream(const double2 *p) {
+    double2 r;
+    asm("ld.global.nc.L1::no_allocate.L2::256B.v2.f64 {%0, %1}, [%2];"
+        : "=d"(r.x), "=d"(r.y)
+        : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ double warp_sum(double s) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
+// Dot product of one matrix row (nv2 double2 entries, 16-byte aligned) with a
+// shared-memory vector; fixed summation order for a given nv2.
+__device__ __forceinline__ double row_dot(const double2 *__restrict__ row,
+                                          const double2 *__restrict__ sv, int nv2, int lane) {
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+    int c = lane;
+    for (; c + 32 * (kUnroll - 1) < nv2; c += 32 * kUnroll) {
+        double2 v[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) v[u] = ldg_stream(row + c + 32 * u);
+#pragma unroll
+        for (int u = 0; u < kUnroll; u += 2) {
+            const double2 y0 = sv[c + 32 * u];
+            const double2 y1 = sv[c + 32 * (u + 1)];
+            acc0 = fma(v[u].x, y0.x, acc0);
+            acc1 = fma(v[u].y, y0.y, acc1);
+            acc2 = fma(v[u + 1].x, y1.x, acc2);
+            acc3 = fma(v[u + 1].y, y1.y, acc3);
+        }
+    }
+    for (; c < nv2; c += 32) {
+        const double2 v = ldg_stream(row + c);
+        const double2 y0 = sv[c];
+        acc0 = fma(v.x, y0.x, acc0);
+        acc1 = fma(v.y, y0.y, acc1);
+    }
+    return warp_sum((acc0 + acc1) + (acc2 + acc3));
+}
+
+__device__ __forceinline__ void stage(double *s, const double *g, int64_t len) {
+    const double2 *g2 = reinterpret_cast<const double2 *>(g);
+    double2 *s2 = reinterpret_cast<double2 *>(s);
+    const int64_t n2 = len >> 1;
+    for (int64_t i = threadIdx.x; i < n2; i += blockDim.x) s2[i] = g2[i];
+}
+
+// [v]_K per row tag: ZERO -> 0, NONPOS -> min(v, 0)
+__device__ __forceinline__ double proj_K(double v, uint8_t c) {
+    return c == DUQUAD_CONE_NONPOS ? fmin(v, 0.0) : 0.0;
+}
+// projection onto the polar cone K° (multiplier sign set): ZERO -> v, NONPOS -> max(v, 0)
+__device__ __forceinline__ double proj_polar(double v, uint8_t c) {
+    return c == DUQUAD_CONE_NONPOS ? fmax(v, 0.0) : v;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1) k_pass_a(const PassAArgs a) {
+    extern __shared__ __align__(16) double smem[];
+    stage(smem, a.y, a.ld);
+    __syncthreads();
+    const double2 *sv = reinterpret_cast<const double2 *>(smem);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int nw = kThreads / 32;
+    const int64_t rows = a.row_end - a.row_begin;
+    const int64_t r0 = a.row_begin + rows * blockIdx.x / gridDim.x;
+    const int64_t r1 = a.row_begin + rows * (blockIdx.x + 1) / gridDim.x;
+    const int nv2 = (int)(a.ld >> 1);
+    int dual = 0;
+    double beta_out = 0.0;
+    if (MODE == MODE_SOLVE && a.first_inner) {
+        const OuterParam op = a.ops[*a.d_j];
+        dual = op.dual_update;
+        beta_out = op.beta_out;
+    }
+    for (int64_t row = r0 + warp; row < r1; row += nw) {
+        // epilogue operands are fetched before the stream so their latency overlaps it
+        const bool is_g = row >= a.nq;
+        const int64_t k = row - a.nq;
+        double gk = 0.0, muk = 0.0, lpk = 0.0;
+        uint8_t ck = 0;
+        if (MODE == MODE_SOLVE && is_g && lane == 0) {
+            gk = a.g[k];
+            muk = a.mu[k];
+            ck = a.cone[k];
+            if (dual) lpk = a.lam_prev[k];
+        }
+        const double s = row_dot(reinterpret_cast<const double2 *>(a.A + row * a.ld), sv, nv2, lane);
+        if (lane != 0) continue;
+        if (!is_g) {
+            a.qy[row] = s;
+            continue;
+        }
+        if (MODE == MODE_LIN) {
+            a.w[k] = a.lin_coef * s;
+            continue;
+        }
+        const double r = s + gk;                       // r = G y + g
+        double m = muk;
+        if (dual) {
+            // y == u_bar^{j-1}: DFOM step, slack s(u, mu)
+            const double sl = a.rho > 0.0 ? proj_K(r + muk / a.rho, ck) : 0.0;
+            double lam = muk + a.step * (r - sl);
+            if (a.project_dual && ck == DUQUAD_CONE_NONPOS) lam = fmax(lam, 0.0);
+            m = lam + beta_out * (lam - lpk);
+            a.lam_prev[k] = lam;
+            a.mu[k] = m;
+        }
+        // multiplier term of grad L_rho: [mu + rho r]_{K°} (rho > 0), mu (rho = 0)
+        a.w[k] = a.rho > 0.0 ? proj_polar(m + a.rho * r, ck) : m;
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1) k_pass_b(const PassBArgs b) {
+    extern __shared__ __align__(16) double smem[];
+    stage(smem, b.w, b.ldp);
+    __syncthreads();
+    const double2 *sv = reinterpret_cast<const double2 *>(smem);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int nw = kThreads / 32;
+    const int64_t r0 = b.nrows * blockIdx.x / gridDim.x;
+    const int64_t r1 = b.nrows * (blockIdx.x + 1) / gridDim.x;
+    const int nv2 = (int)(b.ldp >> 1);
+    double avg_w = 0.0;
+    if (MODE == MODE_SOLVE && b.last_inner) avg_w = b.ops[*b.d_j].avg_w;
+    for (int64_t j = r0 + warp; j < r1; j += nw) {
+        double qyj = 0.0, qj = 0.0, lbj = 0.0, ubj = 0.0, xj = 0.0, yj = 0.0, xhj = 0.0;
+        if (lane == 0) {
+            if (MODE == MODE_SOLVE || b.use_qy) qyj = b.qy[j];
+            if (MODE == MODE_SOLVE) {
+                qj = b.q[j];
+                lbj = b.lb[j];
+                ubj = b.ub[j];
+                xj = b.x[j];
+                yj = b.y[j];
+                if (avg_w != 0.0) xhj = b.xhat[j];
+            }
+        }
+        const double t = nv2 > 0 ? row_dot(reinterpret_cast<const double2 *>(b.GT + j * b.ldp), sv, nv2, lane)
+                                 : 0.0;
+        if (lane != 0) continue;
+        if (MODE == MODE_LIN) {
+            b.out[j] = qyj + t;
+            continue;
+        }
+        const double grad = (qyj + qj) + t;
+        const double xn = fmin(fmax(yj - grad / b.L_in, lbj), ubj);
+        const double yn = b.last_inner ? xn : xn + b.beta_in * (xn - xj);
+        if (avg_w != 0.0) b.xhat[j] = xhj + avg_w * (xn - xhj);     // P:700-706 (running form)
+        b.x[j] = xn;
+        b.y[j] = yn;
+        if (!isfinite(xn) || !isfinite(yn)) *b.flag = 1;
+    }
+}
+
+__global__ void k_init_state(double *x, double *y, double *xhat, const double *lb, const double *ub,
+                             int64_t n, double *mu, double *lam_prev, int64_t p, int32_t *d_j,
+                             int32_t *flag) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) {
+        const double x0 = fmin(fmax(0.0, lb[i]), ub[i]);   // u_bar^0 = [0]_U (reading c7)
+        x[i] = x0;
+        y[i] = x0;
+        xhat[i] = 0.0;
+    }
+    if (i < p) {
+        mu[i] = 0.0;        // mu^1 = lambda^0 = 0
+        lam_prev[i] = 0.0;
+    }
+    if (i == 0) {
+        *d_j = 1;
+        *flag = 0;
+    }
+}
+
+__global__ void k_advance(int32_t *d_j) { *d_j += 1; }
+
+// out[j - col0][i] = G[i][j] for j in [col0, col0 + ncols), i in [0, p)
+__global__ void k_transpose(const double *__restrict__ G, int64_t ldG, int64_t p, int64_t col0,
+                            int64_t ncols, double *__restrict__ GT, int64_t ldp) {
+    __shared__ double tile[32][33];
+    const int64_t i0 = (int64_t)blockIdx.y * 32, j0 = (int64_t)blockIdx.x * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t i = i0 + r, j = j0 + threadIdx.x;
+        tile[r][threadIdx.x] = (i < p && j < ncols) ? G[i * ldG + col0 + j] : 0.0;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t j = j0 + r, i = i0 + threadIdx.x;
+        if (j < ncols && i < p) GT[j * ldp + i] = tile[threadIdx.x][r];
+    }
+}
+
+__global__ void k_check(const double *v, int64_t rows, int64_t cols, int64_t ld, int32_t *flag) {
+    const int64_t total = rows * cols;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = t / cols, c = t - r * cols;
+        if (!isfinite(v[r * ld + c])) *flag = 1;
+    }
+}
+
+__global__ void k_check_box(const double *lb, const double *ub, int64_t n, int32_t *flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (isnan(lb[i]) || isnan(ub[i]) || lb[i] > ub[i] || lb[i] == INFINITY || ub[i] == -INFINITY)
+            *flag = 1;
+    }
+}
+
+// ----------------------------------------------------------- reductions
+__device__ __forceinline__ double block_sum(double v, double *red) {
+    v = warp_sum(v);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+    }
+    return s;   // valid in thread 0
+}
+
+__global__ void k_dot_partial(const double *a, const double *b, int64_t n, double *partials) {
+    __shared__ double red[32];
+    const int64_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
+    double s = 0.0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) s = fma(a[i], b[i], s);
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+// out[v] = sum_{c < nparts} partials[c * nvals + v]   (fixed order)
+__global__ void k_reduce_final(const double *partials, int nparts, int nvals, double *out) {
+    const int v = threadIdx.x;
+    if (v >= nvals) return;
+    double s = 0.0;
+    for (int c = 0; c < nparts; ++c) s += partials[c * nvals + v];
+    out[v] = s;
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+__global__ void k_fill_hash(double *v, int64_t n, int64_t offset) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) v[i] = 0.5 + (double)(splitmix64((uint64_t)(i + offset)) >> 11) * 0x1.0p-53;
+}
+
+__global__ void k_scale_by_rsqrt(double *v, int64_t n, const double *sumsq, double *beta_out) {
+    const double nrm = sqrt(*sumsq);
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) v[i] = v[i] / nrm;
+    if (i == 0 && beta_out) *beta_out = nrm;
+}
+
+__global__ void k_lanczos_update(double *w, const double *v, const double *vprev, int64_t n,
+                                 const double *alpha, const double *beta_prev, double *partials) {
+    __shared__ double red[32];
+    const double al = *alpha, be = *beta_prev;
+    const int64_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
+    double s = 0.0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const double wi = w[i] - al * v[i] - be * vprev[i];
+        w[i] = wi;
+        s = fma(wi, wi, s);
+    }
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+__global__ void k_lanczos_next(double *v, double *vprev, const double *w, int64_t n,
+                               const double *sumsq, double *beta) {
+    const double nrm = sqrt(*sumsq);
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) {
+        vprev[i] = v[i];
+        v[i] = nrm > 0.0 ? w[i] / nrm : 0.0;
+    }
+    if (i == 0) *beta = nrm;
+}
+
+__global__ void k_residual_partial(const double *x, const double *qy, const double *q, int64_t n,
+                                   const double *Gx, const double *g, const double *lam,
+                                   const uint8_t *cone, int64_t p, double rho, double *partials) {
+    __shared__ double red[32];
+    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    {
+        const int64_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
+        for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x)
+            acc[0] += 0.5 * x[i] * qy[i] + q[i] * x[i];
+    }
+    {
+        const int64_t lo = p * blockIdx.x / gridDim.x, hi = p * (blockIdx.x + 1) / gridDim.x;
+        for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) {
+            const double r = Gx[k] + g[k];
+            const double d = r - proj_K(r, cone[k]);
+            acc[1] += d * d;
+            if (rho > 0.0) {
+                const double wv = r + lam[k] / rho;
+                const double dw = wv - proj_K(wv, cone[k]);
+                acc[2] += dw * dw;
+            }
+            acc[3] += lam[k] * lam[k];
+            acc[4] += lam[k] * r;
+        }
+    }
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+        const double s = block_sum(acc[v], red);
+        if (threadIdx.x == 0) partials[blockIdx.x * 5 + v] = s;
+    }
+}
+
+inline int blocks_for(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
+}  // namespace
+
+int pass_threads() { return kThreads; }
+
+cudaError_t configure_pass_kernels(size_t smem_a, size_t smem_b) {
+    cudaError_t e;
+    const size_t sm_a = smem_a < 48 * 1024 ? 48 * 1024 : smem_a;
+    const size_t sm_b = smem_b < 48 * 1024 ? 48 * 1024 : smem_b;
+    if ((e = cudaFuncSetAttribute(k_pass_a<MODE_SOLVE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_a)))
+        return e;
+    if ((e = cudaFuncSetAttribute(k_pass_a<MODE_LIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_a)))
+        return e;
+    if ((e = cudaFuncSetAttribute(k_pass_b<MODE_SOLVE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_b)))
+        return e;
+    return cudaFuncSetAttribute(k_pass_b<MODE_LIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_b);
+}
+
+cudaError_t launch_pass_a(const PassAArgs &a, int mode, const LaunchCfg &cfg, cudaStream_t s) {
+    if (a.row_end <= a.row_begin) return cudaSuccess;
+    if (mode == MODE_SOLVE)
+        k_pass_a<MODE_SOLVE><<<cfg.grid, kThreads, cfg.smem, s>>>(a);
+    else
+        k_pass_a<MODE_LIN><<<cfg.grid, kThreads, cfg.smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pass_b(const PassBArgs &b, int mode, const LaunchCfg &cfg, cudaStream_t s) {
+    if (b.nrows <= 0) return cudaSuccess;
+    if (mode == MODE_SOLVE)
+        k_pass_b<MODE_SOLVE><<<cfg.grid, kThreads, cfg.smem, s>>>(b);
+    else
+        k_pass_b<MODE_LIN><<<cfg.grid, kThreads, cfg.smem, s>>>(b);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_init_state(double *x, double *y, double *xhat, const double *lb, const double *ub,
+                              int64_t n, double *mu, double *lam_prev, int64_t p, int32_t *d_j,
+                              int32_t *flag, cudaStream_t s) {
+    const int64_t m = n > p ? n : p;
+    k_init_state<<<blocks_for(m > 0 ? m : 1, 256), 256, 0, s>>>(x, y, xhat, lb, ub, n, mu, lam_prev, p,
+                                                               d_j, flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_advance(int32_t *d_j, cudaStream_t s) {
+    k_advance<<<1, 1, 0, s>>>(d_j);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_transpose(const double *G, int64_t ldG, int64_t p, int64_t col0, int64_t ncols,
+                             double *GT, int64_t ldp, cudaStream_t s) {
+    if (p <= 0 || ncols <= 0) return cudaSuccess;
+    dim3 grid((unsigned)((ncols + 31) / 32), (unsigned)((p + 31) / 32));
+    k_transpose<<<grid, dim3(32, 8), 0, s>>>(G, ldG, p, col0, ncols, GT, ldp);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check(const double *v, int64_t rows, int64_t cols, int64_t ld, int32_t *flag,
+                         cudaStream_t s) {
+    if (rows <= 0 || cols <= 0) return cudaSuccess;
+    k_check<<<1184, 256, 0, s>>>(v, rows, cols, ld, flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check_box(const double *lb, const double *ub, int64_t n, int32_t *flag,
+                             cudaStream_t s) {
+    k_check_box<<<148, 256, 0, s>>>(lb, ub, n, flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dot_partial(const double *a, const double *b, int64_t n, double *partials,
+                               cudaStream_t s) {
+    k_dot_partial<<<kRedGrid, kRedThreads, 0, s>>>(a, b, n, partials);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_final(const double *partials, int nparts, int nvals, double *out,
+                                cudaStream_t s) {
+    k_reduce_final<<<1, 32, 0, s>>>(partials, nparts, nvals, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill_hash(double *v, int64_t n, int64_t offset, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    k_fill_hash<<<blocks_for(n, 256), 256, 0, s>>>(v, n, offset);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scale_by_rsqrt(double *v, int64_t n, const double *sumsq, double *beta_out,
+                                  cudaStream_t s) {
+    k_scale_by_rsqrt<<<blocks_for(n > 0 ? n : 1, 256), 256, 0, s>>>(v, n, sumsq, beta_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_lanczos_update(double *w, const double *v, const double *vprev, int64_t n,
+                                  const double *alpha, const double *beta_prev, double *partials,
+                                  cudaStream_t s) {
+    k_lanczos_update<<<kRedGrid, kRedThreads, 0, s>>>(w, v, vprev, n, alpha, beta_prev, partials);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_lanczos_next(double *v, double *vprev, const double *w, int64_t n,
+                                const double *sumsq, double *beta, cudaStream_t s) {
+    k_lanczos_next<<<blocks_for(n > 0 ? n : 1, 256), 256, 0, s>>>(v, vprev, w, n, sumsq, beta);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_residual_partial(const double *x, const double *qy, const double *q, int64_t n,
+                                    const double *Gx, const double *g, const double *lam,
+                                    const uint8_t *cone, int64_t p, double rho, double *partials,
+                                    cudaStream_t s) {
+    k_residual_partial<<<kRedGrid, kRedThreads, 0, s>>>(x, qy, q, n, Gx, g, lam, cone, p, rho, partials);
+    return cudaGetLastError();
+}
+
+}  // namespace dq

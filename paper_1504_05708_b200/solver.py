@@ -1,0 +1,179 @@
+"""Thin Python binding over the DuQuad C ABI (include/duquad.h).
+
+Marshalling only: every step of the solve runs in the library's sm_100a
+kernels.  Inputs may be NumPy arrays (host) or torch tensors (host or CUDA);
+torch is used for nothing but device memory, streams and process groups.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+
+from . import _lib as L
+
+_ALGS = {"DGM": L.DGM, "DFGM": L.DFGM}
+_INNER = {"FGM": L.INNER_FGM, "GM": L.INNER_GM, "FGM_SIGMA": L.INNER_FGM_SIGMA}
+
+
+def _is_torch(x):
+    return type(x).__module__.startswith("torch")
+
+
+class _Arr:
+    """Keeps a contiguous fp64/uint8/int32 buffer alive and exposes its address."""
+
+    def __init__(self, x, dtype):
+        if x is None:
+            self.obj, self.ptr, self.dev = None, None, False
+            return
+        if _is_torch(x):
+            import torch
+            tdt = {np.float64: torch.float64, np.uint8: torch.uint8, np.int32: torch.int32}[dtype]
+            t = x.detach()
+            if t.dtype != tdt:
+                t = t.to(tdt)
+            t = t.contiguous()
+            self.obj, self.ptr, self.dev = t, t.data_ptr(), t.is_cuda
+        else:
+            a = np.ascontiguousarray(x, dtype=dtype)
+            self.obj, self.ptr, self.dev = a, a.ctypes.data, False
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    L.check(L.lib().duquad_nccl_unique_id(buf))
+    return buf.raw
+
+
+def shard_range(rows: int, world: int, rank: int):
+    b, e = C.c_int64(), C.c_int64()
+    L.check(L.lib().duquad_shard_range(rows, world, rank, C.byref(b), C.byref(e)))
+    return b.value, e.value
+
+
+class Solver:
+    """One DuQuad context: setup (pack + upload), constants, solve, results.
+
+    Q (n x n), q (n), G (p x n), g (p), lb, ub (n), cone (p uint8: 0 ZERO, 1 NONPOS)
+    follow PAPER.md:193-212.  All float inputs must be fp64 (converted otherwise).
+    """
+
+    def __init__(self, Q, q, G, g, lb, ub, cone=None, rho: float = 1.0, *,
+                 dual_step_scale: float = 0.5, project_dual: bool = True, inner_rule: str = "FGM",
+                 sigma: float = 0.0, lambda_min_lb: float = 0.0, l_mode: int = 0,
+                 use_graphs: bool = True, world_size: int = 1, rank: int = 0,
+                 nccl_id: Optional[bytes] = None, stream=None, device: int = -1,
+                 time_passes: bool = False, cone_all: int = L.CONE_NONPOS):
+        lib = L.lib()
+        self._lib = lib
+        arrs = dict(Q=_Arr(Q, np.float64), q=_Arr(q, np.float64), G=_Arr(G, np.float64),
+                    g=_Arr(g, np.float64), lb=_Arr(lb, np.float64), ub=_Arr(ub, np.float64),
+                    cone=_Arr(cone, np.uint8))
+        devs = {k: a.dev for k, a in arrs.items() if a.obj is not None}
+        if len(set(devs.values())) > 1:
+            raise ValueError("problem arrays must be all on the host or all on the device")
+        on_device = bool(devs and next(iter(devs.values())))
+        n = int(arrs["Q"].obj.shape[0])
+        p = int(arrs["G"].obj.shape[0]) if arrs["G"].obj is not None else 0
+        prob = L.Problem()
+        prob.n, prob.p, prob.batch = n, p, 1
+        prob.format = L.DENSE
+        prob.on_device = int(on_device)
+        prob.Q, prob.ldQ = arrs["Q"].ptr, n
+        prob.G, prob.ldG = arrs["G"].ptr, n
+        prob.q, prob.g, prob.lb, prob.ub = arrs["q"].ptr, arrs["g"].ptr, arrs["lb"].ptr, arrs["ub"].ptr
+        prob.cone = arrs["cone"].ptr
+        prob.cone_all = cone_all
+        opt = L.Options()
+        lib.duquad_default_options(C.byref(opt))
+        opt.dual_step_scale = dual_step_scale
+        opt.project_dual = int(project_dual)
+        opt.inner_rule = _INNER[inner_rule]
+        opt.sigma = sigma
+        opt.lambda_min_lb = lambda_min_lb
+        opt.l_mode = l_mode
+        opt.use_graphs = int(use_graphs)
+        opt.world_size = world_size
+        opt.rank = rank
+        self._nccl_id = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        opt.nccl_id = C.cast(self._nccl_id, C.c_void_p) if self._nccl_id is not None else None
+        opt.stream = stream
+        opt.device = device
+        opt.time_passes = int(time_passes)
+        ctx = C.c_void_p()
+        L.check(lib.duquad_setup(C.byref(ctx), C.byref(prob), float(rho), C.byref(opt)))
+        self._ctx = ctx
+        self.n, self.p, self.rho = n, p, float(rho)
+        self.world_size, self.rank = world_size, rank
+        self.n_range = shard_range(n, world_size, rank)
+        self.p_range = shard_range(p, world_size, rank)
+        self.device = device
+        self.last_result = None
+
+    # ------------------------------------------------------------------ API
+    def lipschitz(self, iters: int = 100, safety: float = 0.0):
+        a, b, c = C.c_double(), C.c_double(), C.c_double()
+        L.check(self._lib.duquad_lipschitz(self._ctx, iters, safety, C.byref(a), C.byref(b), C.byref(c)),
+                self._ctx)
+        return a.value, b.value, c.value
+
+    def set_constants(self, L_in: float, L_d: float):
+        L.check(self._lib.duquad_set_constants(self._ctx, float(L_in), float(L_d)), self._ctx)
+
+    def set_trace(self, lam_trace=None, u_trace=None, max_outer: int = 0):
+        """Device (torch CUDA) buffers of shape (max_outer, p_local) / (max_outer, n_local)."""
+        self._trace = (lam_trace, u_trace)
+        L.check(self._lib.duquad_set_trace(self._ctx, lam_trace.data_ptr() if lam_trace is not None else None,
+                                           u_trace.data_ptr() if u_trace is not None else None,
+                                           int(max_outer)), self._ctx)
+
+    def solve(self, alg: str = "DFGM", outer: int = 1, inner: int = 1) -> dict:
+        res = L.Result()
+        L.check(self._lib.duquad_solve(self._ctx, _ALGS[alg], int(outer), int(inner), C.byref(res)), self._ctx)
+        self.last_result = {k: getattr(res, k) for k, _ in L.Result._fields_}
+        return self.last_result
+
+    def result(self, device: bool = False):
+        """(x_last, x_avg, lambda) local slices; NumPy on the host or torch on the device."""
+        nl = self.n_range[1] - self.n_range[0]
+        pl = self.p_range[1] - self.p_range[0]
+        if device:
+            import torch
+            dev = torch.device("cuda", torch.cuda.current_device() if self.device < 0 else self.device)
+            xl = torch.empty(nl, dtype=torch.float64, device=dev)
+            xa = torch.empty(nl, dtype=torch.float64, device=dev)
+            lam = torch.empty(max(pl, 1), dtype=torch.float64, device=dev)
+            L.check(self._lib.duquad_get_result(self._ctx, xl.data_ptr(), xa.data_ptr(), lam.data_ptr(), 1),
+                    self._ctx)
+            return xl, xa, lam[:pl]
+        xl = np.empty(nl)
+        xa = np.empty(nl)
+        lam = np.empty(max(pl, 1))
+        L.check(self._lib.duquad_get_result(self._ctx, xl.ctypes.data, xa.ctypes.data, lam.ctypes.data, 0),
+                self._ctx)
+        return xl, xa, lam[:pl]
+
+    def residuals(self, which: str = "last"):
+        F, d, lag = C.c_double(), C.c_double(), C.c_double()
+        L.check(self._lib.duquad_residuals(self._ctx, 0 if which == "last" else 1, C.byref(F), C.byref(d),
+                                           C.byref(lag)), self._ctx)
+        return F.value, d.value, lag.value
+
+    def close(self):
+        if getattr(self, "_ctx", None):
+            self._lib.duquad_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

@@ -1,0 +1,105 @@
+"""C-ABI contract checks that need no GPU (-m "not gpu"): the library builds and loads,
+exports every symbol include/duquad.h declares, host-only helpers work, and device
+calls fail loudly (status, not crash) without a device."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1504_05708_b200 import build, _lib
+    build.build()
+    return _lib.load()
+
+
+def _header_functions():
+    src = open(os.path.join(ROOT, "include", "duquad.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(duquad_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(lib):
+    names = _header_functions()
+    assert "duquad_solve" in names and "duquad_setup" in names and "duquad_lipschitz" in names
+    for name in names:
+        assert hasattr(lib, name), name
+    from paper_1504_05708_b200 import _lib
+    assert set(_lib.EXPORTED) == set(names)
+
+
+def test_abi_version_and_status_strings(lib):
+    assert lib.duquad_abi_version() == 1
+    assert lib.duquad_status_string(0) == b"ok"
+    assert b"invalid" in lib.duquad_status_string(1)
+
+
+def test_default_options(lib):
+    from paper_1504_05708_b200 import _lib
+    o = _lib.Options()
+    lib.duquad_default_options(C.byref(o))
+    assert o.dual_step_scale == 0.5 and o.project_dual == 1 and o.world_size == 1 and o.use_graphs == 1
+
+
+@pytest.mark.parametrize("rows,world", [(16384, 8), (10, 3), (5, 8), (0, 2), (2000, 1)])
+def test_shard_range_partitions(lib, rows, world):
+    from paper_1504_05708_b200 import shard_range
+    covered = []
+    for r in range(world):
+        b, e = shard_range(rows, world, r)
+        assert 0 <= b <= e <= rows
+        covered.extend(range(b, e))
+    assert covered == list(range(rows))
+
+
+def test_shard_range_rejects_bad_args(lib):
+    b, e = C.c_int64(), C.c_int64()
+    assert lib.duquad_shard_range(10, 2, 2, C.byref(b), C.byref(e)) == 1
+    assert lib.duquad_shard_range(10, 0, 0, C.byref(b), C.byref(e)) == 1
+
+
+def test_setup_validation_errors_without_device(lib):
+    """Argument errors are reported before any device call; with valid args and no GPU the
+    status is ENODEV (never a silent CPU fallback)."""
+    import numpy as np
+    from paper_1504_05708_b200 import _lib
+    n, p = 4, 2
+    Q = np.eye(n)
+    G = np.ones((p, n))
+    q, g, lb, ub = np.zeros(n), np.zeros(p), -np.ones(n), np.ones(n)
+    prob = _lib.Problem()
+    prob.n, prob.p, prob.batch, prob.format, prob.on_device = n, p, 1, 0, 0
+    prob.Q, prob.ldQ, prob.G, prob.ldG = Q.ctypes.data, n, G.ctypes.data, n
+    prob.q, prob.g, prob.lb, prob.ub = q.ctypes.data, g.ctypes.data, lb.ctypes.data, ub.ctypes.data
+    prob.cone, prob.cone_all = None, 1
+    ctx = C.c_void_p()
+    assert lib.duquad_setup(C.byref(ctx), C.byref(prob), -1.0, None) == _lib.DUQUAD_EINVAL   # rho < 0
+    bad_ub = np.array([1.0, 1.0, -2.0, 1.0])
+    prob.ub = bad_ub.ctypes.data
+    assert lib.duquad_setup(C.byref(ctx), C.byref(prob), 1.0, None) == _lib.DUQUAD_EINVAL    # lb > ub
+    assert b"lb <= ub" in lib.duquad_last_error(None)
+    prob.ub = ub.ctypes.data
+    Qn = Q.copy()
+    Qn[1, 2] = float("nan")
+    prob.Q = Qn.ctypes.data
+    assert lib.duquad_setup(C.byref(ctx), C.byref(prob), 1.0, None) == _lib.DUQUAD_EINVAL    # NaN
+    prob.Q = Q.ctypes.data
+    import torch
+    if not torch.cuda.is_available():
+        assert lib.duquad_setup(C.byref(ctx), C.byref(prob), 1.0, None) == _lib.DUQUAD_ENODEV
+        assert not ctx.value
+
+
+def test_product_package_does_not_touch_oracle():
+    """The product path never imports the oracle (no CPU fallback route)."""
+    pkg = os.path.join(ROOT, "paper_1504_05708_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in txt.replace("oracle/", "").lower() or f == "__init__.py", f
+                assert "import oracle" not in txt and "from oracle" not in txt, f
