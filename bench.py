@@ -235,11 +235,13 @@ def main():
     clocks.start()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.nvtx.range_push("timed")
     e0.record(stream)
     infos = []
     for _ in range(args.steps):
         infos.append(s.solve("DFGM", K, Kin))
     e1.record(stream)
+    torch.cuda.nvtx.range_pop()
     barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)

@@ -48,6 +48,11 @@ struct duquad_ctx {
     double *g = nullptr, *mu = nullptr, *lam_prev = nullptr;
     uint8_t *cone = nullptr;
     double *lz_vprev = nullptr, *lz_w = nullptr;
+    // CSR storage (format == DUQUAD_CSR): stacked local [Q_r; G_r] and local rows of G'
+    int32_t *a_rp = nullptr, *a_ci = nullptr, *b_rp = nullptr, *b_ci = nullptr;
+    double *a_va = nullptr, *b_va = nullptr;
+    int64_t nnz_a = 0, nnz_b = 0;
+    int gs_a = 4, gs_b = 4;
     double *scal = nullptr;       // device scalars
     double *partials = nullptr;   // kRedGrid * 5
     OuterParam *d_ops = nullptr;
@@ -107,6 +112,11 @@ void free_all(duquad_ctx *c) {
     for (double *d : ds)
         if (d) cudaFree(d);
     if (c->cone) cudaFree(c->cone);
+    int32_t *is[] = {c->a_rp, c->a_ci, c->b_rp, c->b_ci};
+    for (int32_t *d : is)
+        if (d) cudaFree(d);
+    if (c->a_va) cudaFree(c->a_va);
+    if (c->b_va) cudaFree(c->b_va);
     if (c->d_ops) cudaFree(c->d_ops);
     if (c->d_j) cudaFree(c->d_j);
     if (c->d_flag) cudaFree(c->d_flag);
@@ -173,6 +183,11 @@ PassAArgs make_a(duquad_ctx *c) {
     a.ops = c->d_ops;
     a.d_j = c->d_j;
     a.lin_coef = 1.0;
+    a.fmt = c->format;
+    a.gs = c->gs_a;
+    a.rp = c->a_rp;
+    a.ci = c->a_ci;
+    a.va = c->a_va;
     return a;
 }
 
@@ -194,6 +209,11 @@ PassBArgs make_b(duquad_ctx *c) {
     b.d_j = c->d_j;
     b.flag = c->d_flag;
     b.use_qy = 1;
+    b.fmt = c->format;
+    b.gs = c->gs_b;
+    b.rp = c->b_rp;
+    b.ci = c->b_ci;
+    b.va = c->b_va;
     return b;
 }
 
@@ -339,6 +359,85 @@ duquad_status upload_vec(duquad_ctx *ctx, double *dst, const double *src, int64_
     return DUQUAD_OK;
 }
 
+// CSR setup: device copies of Q and G (validated), the stacked local [Q_r; G_r]
+// and the local rows of G' (device transpose, deterministic order).
+duquad_status setup_csr(duquad_ctx *ctx, const duquad_problem *prob) {
+    cudaStream_t s = ctx->stream;
+    const int64_t n = ctx->n, p = ctx->p;
+    const int64_t qnnz = prob->Q_nnz, gnnz = p > 0 ? prob->G_nnz : 0;
+    std::vector<void *> tmp;
+    struct Freer {
+        std::vector<void *> &v;
+        ~Freer() {
+            for (void *q : v) cudaFree(q);
+        }
+    } freer{tmp};
+    auto dev_copy = [&](const void *src, size_t bytes, const void **dst) -> cudaError_t {
+        if (prob->on_device) {
+            *dst = src;
+            return cudaSuccess;
+        }
+        void *d = nullptr;
+        cudaError_t e = cudaMalloc(&d, std::max<size_t>(bytes, 8));
+        if (e) return e;
+        tmp.push_back(d);
+        *dst = d;
+        return bytes ? cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, s) : cudaSuccess;
+    };
+    const int32_t *Qrp, *Qci, *Grp = nullptr, *Gci = nullptr;
+    const double *Qva, *Gva = nullptr;
+    CK(dev_copy(prob->Q_rowptr, (n + 1) * 4, (const void **)&Qrp));
+    CK(dev_copy(prob->Q_col, qnnz * 4, (const void **)&Qci));
+    CK(dev_copy(prob->Q_val, qnnz * 8, (const void **)&Qva));
+    if (p > 0) {
+        CK(dev_copy(prob->G_rowptr, (p + 1) * 4, (const void **)&Grp));
+        CK(dev_copy(prob->G_col, gnnz * 4, (const void **)&Gci));
+        CK(dev_copy(prob->G_val, gnnz * 8, (const void **)&Gva));
+    }
+    CK(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int32_t), s));
+    CK(launch_check_csr(Qrp, Qci, Qva, n, n, qnnz, ctx->d_flag, s));
+    if (p > 0) CK(launch_check_csr(Grp, Gci, Gva, p, n, gnnz, ctx->d_flag, s));
+    int32_t flag = 0;
+    CK(cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(flag), cudaMemcpyDeviceToHost, s));
+    int32_t qb[2] = {0, 0}, gb[2] = {0, 0};
+    CK(cudaMemcpyAsync(&qb[0], Qrp + ctx->r0, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&qb[1], Qrp + ctx->r0 + ctx->nloc, 4, cudaMemcpyDeviceToHost, s));
+    if (p > 0) {
+        CK(cudaMemcpyAsync(&gb[0], Grp + ctx->s0, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&gb[1], Grp + ctx->s0 + ctx->ploc, 4, cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    if (flag) return fail(ctx, DUQUAD_EINVAL, "invalid CSR data (row pointers, column range or non-finite value)");
+    const int64_t nq = qb[1] - qb[0], ng = gb[1] - gb[0];
+    ctx->nnz_a = nq + ng;
+    CK(dalloc(&ctx->a_rp, ctx->nloc + ctx->ploc + 1));
+    CK(dalloc(&ctx->a_ci, ctx->nnz_a));
+    CK(dalloc(&ctx->a_va, ctx->nnz_a));
+    CK(launch_rebase(ctx->a_rp, Qrp + ctx->r0, ctx->nloc + 1, qb[0], 0, s));
+    if (ctx->ploc > 0) CK(launch_rebase(ctx->a_rp + ctx->nloc, Grp + ctx->s0, ctx->ploc + 1, gb[0], (int32_t)nq, s));
+    if (nq) {
+        CK(cudaMemcpyAsync(ctx->a_ci, Qci + qb[0], nq * 4, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(ctx->a_va, Qva + qb[0], nq * 8, cudaMemcpyDeviceToDevice, s));
+    }
+    if (ng) {
+        CK(cudaMemcpyAsync(ctx->a_ci + nq, Gci + gb[0], ng * 4, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(ctx->a_va + nq, Gva + gb[0], ng * 8, cudaMemcpyDeviceToDevice, s));
+    }
+    if (p > 0) {
+        CK(csr_transpose_rows(Grp, Gci, Gva, p, n, gnnz, ctx->r0, ctx->nloc, &ctx->b_rp, &ctx->b_ci, &ctx->b_va,
+                              &ctx->nnz_b, s));
+    } else {
+        CK(dalloc(&ctx->b_rp, ctx->nloc + 1));
+        CK(dalloc(&ctx->b_ci, 1));
+        CK(dalloc(&ctx->b_va, 1));
+    }
+    // group sizes from the GLOBAL mean nnz per row (identical on every rank)
+    ctx->gs_a = csr_group_size((double)(qnnz + gnnz) / (double)(n + p));
+    ctx->gs_b = csr_group_size((double)gnnz / (double)n);
+    CK(cudaStreamSynchronize(s));
+    return DUQUAD_OK;
+}
+
 }  // namespace
 
 // ======================================================================= ABI
@@ -421,10 +520,17 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
     if (n < 1 || p < 0) return fail(nullptr, DUQUAD_EINVAL, "need n >= 1 and p >= 0");
     if (!(rho >= 0.0) || !std::isfinite(rho)) return fail(nullptr, DUQUAD_EINVAL, "rho must be finite and >= 0");
     if (prob->batch != 1) return fail(nullptr, DUQUAD_EINVAL, "batch > 1 not supported by this build");
-    if (prob->format != DUQUAD_DENSE) return fail(nullptr, DUQUAD_EINVAL, "CSR not supported by this build");
-    if (!prob->Q || !prob->q || !prob->lb || !prob->ub || (p > 0 && (!prob->G || !prob->g)))
-        return fail(nullptr, DUQUAD_EINVAL, "missing problem array");
-    if (prob->ldQ < n || (p > 0 && prob->ldG < n)) return fail(nullptr, DUQUAD_EINVAL, "leading dimension < n");
+    const bool csr = prob->format == DUQUAD_CSR;
+    if (prob->format != DUQUAD_DENSE && !csr) return fail(nullptr, DUQUAD_EINVAL, "bad format");
+    if (!prob->q || !prob->lb || !prob->ub || (p > 0 && !prob->g))
+        return fail(nullptr, DUQUAD_EINVAL, "missing problem vector");
+    if (!csr && (!prob->Q || (p > 0 && !prob->G))) return fail(nullptr, DUQUAD_EINVAL, "missing problem matrix");
+    if (csr && (!prob->Q_rowptr || !prob->Q_col || !prob->Q_val ||
+                (p > 0 && (!prob->G_rowptr || !prob->G_col || !prob->G_val)) || prob->Q_nnz < 0 ||
+                prob->G_nnz < 0 || prob->Q_nnz > INT32_MAX || prob->G_nnz > INT32_MAX))
+        return fail(nullptr, DUQUAD_EINVAL, "missing or oversized CSR array (int32 indices)");
+    if (!csr && (prob->ldQ < n || (p > 0 && prob->ldG < n)))
+        return fail(nullptr, DUQUAD_EINVAL, "leading dimension < n");
     if (!prob->cone && prob->cone_all != DUQUAD_CONE_ZERO && prob->cone_all != DUQUAD_CONE_NONPOS)
         return fail(nullptr, DUQUAD_EINVAL, "bad cone_all");
     if (!(opt.dual_step_scale > 0.0)) return fail(nullptr, DUQUAD_EINVAL, "dual_step_scale must be > 0");
@@ -435,7 +541,7 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         return fail(nullptr, DUQUAD_EINVAL, "bad world_size / rank");
     if (opt.world_size > 1 && !opt.nccl_id) return fail(nullptr, DUQUAD_EINVAL, "sharded setup needs nccl_id");
     if (!prob->on_device) {   // host data: validate here (device data is validated by a kernel)
-        if (!finite_host(prob->Q, n, n, prob->ldQ) || (p > 0 && !finite_host(prob->G, p, n, prob->ldG)) ||
+        if ((!csr && (!finite_host(prob->Q, n, n, prob->ldQ) || (p > 0 && !finite_host(prob->G, p, n, prob->ldG)))) ||
             !finite_host(prob->q, 1, n, n) || (p > 0 && !finite_host(prob->g, 1, p, p)))
             return fail(nullptr, DUQUAD_EINVAL, "non-finite problem data");
         for (int64_t i = 0; i < n; ++i)
@@ -512,8 +618,10 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
     ctx->ylen = round_up(std::max(ctx->ld, ctx->world * ctx->n_slice), 32);
     ctx->wlen = round_up(std::max(ctx->ldp, ctx->world * ctx->p_slice), 32);
     const int64_t rows = ctx->nloc + ctx->ploc;
-    CKS(dalloc(&ctx->A, rows * ctx->ld));
-    CKS(dalloc(&ctx->GT, ctx->nloc * std::max<int64_t>(ctx->ldp, 1)));
+    if (!csr) {
+        CKS(dalloc(&ctx->A, rows * ctx->ld));
+        CKS(dalloc(&ctx->GT, ctx->nloc * std::max<int64_t>(ctx->ldp, 1)));
+    }
     CKS(dalloc(&ctx->y_full, ctx->ylen));
     CKS(dalloc(&ctx->w_full, ctx->wlen));
     CKS(dalloc(&ctx->qy, ctx->nloc));
@@ -537,6 +645,10 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
     // with a library-owned stream, wait for the whole device before reading them.
     if (prob->on_device && ctx->own_stream) CKS(cudaDeviceSynchronize());
     // ---- pack [Q_r; G_r] and G'_r
+    if (csr) {
+        duquad_status st = setup_csr(ctx, prob);
+        if (st != DUQUAD_OK) return bail(st);
+    } else {
     CKS(cudaMemcpy2DAsync(ctx->A, ctx->ld * sizeof(double), prob->Q + ctx->r0 * prob->ldQ,
                           prob->ldQ * sizeof(double), n * sizeof(double), ctx->nloc, cudaMemcpyDefault, s));
     if (p > 0) {
@@ -561,6 +673,7 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         }
         CKS(e);
     }
+    }  // dense
     if (upload_vec(ctx, ctx->q, prob->q + ctx->r0, ctx->nloc) ||
         upload_vec(ctx, ctx->lb, prob->lb + ctx->r0, ctx->nloc) ||
         upload_vec(ctx, ctx->ub, prob->ub + ctx->r0, ctx->nloc) ||
@@ -574,7 +687,7 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
     }
     if (prob->on_device) {
         CKS(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int32_t), s));
-        CKS(launch_check(ctx->A, rows, n, ctx->ld, ctx->d_flag, s));
+        if (!csr) CKS(launch_check(ctx->A, rows, n, ctx->ld, ctx->d_flag, s));
         CKS(launch_check(ctx->q, 1, ctx->nloc, ctx->nloc, ctx->d_flag, s));
         if (ctx->ploc > 0) CKS(launch_check(ctx->g, 1, ctx->ploc, ctx->ploc, ctx->d_flag, s));
         CKS(launch_check_box(ctx->lb, ctx->ub, ctx->nloc, ctx->d_flag, s));
@@ -585,6 +698,13 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
             ctx->err = "non-finite problem data or lb > ub";
             return bail(DUQUAD_EINVAL);
         }
+    }
+    if (csr) {   // grid-stride sub-warp SpMV, full occupancy
+        ctx->cfg_a = {ctx->num_sms * 8, 256, 0};
+        ctx->cfg_b = {ctx->num_sms * 8, 256, 0};
+        CKS(cudaStreamSynchronize(s));
+        *out = ctx;
+        return DUQUAD_OK;
     }
     // ---- launch configuration: persistent grid, one CTA per SM, vector staged in smem
     const size_t smem_a = (size_t)ctx->ld * sizeof(double);
@@ -753,8 +873,13 @@ duquad_status duquad_solve(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t 
         res->kernel_launches = 1 + (int64_t)(K + 1) * (2 * Kin + 1);
         res->matrix_passes = (int64_t)(K + 1) * Kin * 2;
         const double nn = (double)ctx->n, nl = (double)ctx->nloc, pl = (double)ctx->ploc, pp = (double)ctx->p;
-        res->bytes_pass_a = 8.0 * ((nl + pl) * nn + nn + nl + 3.0 * pl);
-        res->bytes_pass_b = 8.0 * (nl * pp + pp + 8.0 * nl);
+        if (ctx->format == DUQUAD_CSR) {   // values + indices + row pointers + vectors
+            res->bytes_pass_a = 12.0 * ctx->nnz_a + 4.0 * (nl + pl + 1) + 8.0 * (nn + nl + 3.0 * pl);
+            res->bytes_pass_b = 12.0 * ctx->nnz_b + 4.0 * (nl + 1) + 8.0 * (pp + 8.0 * nl);
+        } else {
+            res->bytes_pass_a = 8.0 * ((nl + pl) * nn + nn + nl + 3.0 * pl);
+            res->bytes_pass_b = 8.0 * (nl * pp + pp + 8.0 * nl);
+        }
         if (j_timed > 0) {
             double sa = 0, sb = 0;
             for (int k = 0; k < Kin; ++k) {

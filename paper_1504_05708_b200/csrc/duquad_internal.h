@@ -49,6 +49,12 @@ struct PassAArgs {
     const OuterParam *ops;
     const int32_t *d_j;
     double lin_coef;     // MODE_LIN: w[k] = lin_coef * (G y)_k
+    // CSR storage of the stacked local [Q_r; G_r] (format == DUQUAD_CSR)
+    int32_t fmt;
+    int32_t gs;          // lanes per row (power of two, 2..32)
+    const int32_t *rp;   // row pointers (rows + 1), rebased to 0
+    const int32_t *ci;   // column indices
+    const double *va;    // values
 };
 
 // ---------------------------------------------------------------- pass B
@@ -72,6 +78,12 @@ struct PassBArgs {
     const int32_t *d_j;
     int32_t *flag;       // set to 1 if an iterate is non-finite
     double *out;         // MODE_LIN output
+    // CSR storage of the local rows of G'
+    int32_t fmt;
+    int32_t gs;
+    const int32_t *rp;
+    const int32_t *ci;
+    const double *va;
 };
 
 struct LaunchCfg {
@@ -79,6 +91,23 @@ struct LaunchCfg {
     int threads;
     size_t smem;
 };
+
+// kernels_csr.cu
+cudaError_t launch_pass_a_csr(const PassAArgs &a, int mode, const LaunchCfg &cfg, cudaStream_t s);
+cudaError_t launch_pass_b_csr(const PassBArgs &b, int mode, const LaunchCfg &cfg, cudaStream_t s);
+// dst[i] = src[i] - sub + add, i < count
+cudaError_t launch_rebase(int32_t *dst, const int32_t *src, int64_t count, int32_t sub, int32_t add,
+                          cudaStream_t s);
+// flag |= CSR structure invalid (row pointers non-monotone / wrong ends, columns out of range,
+// values non-finite)
+cudaError_t launch_check_csr(const int32_t *rp, const int32_t *ci, const double *va, int64_t rows,
+                             int64_t cols, int64_t nnz, int32_t *flag, cudaStream_t s);
+// Transpose of a CSR matrix (rows x cols) restricted to output rows [c0, c0 + nc):
+// builds (rp_t, ci_t, va_t) with columns (original rows) sorted; allocates the outputs.
+cudaError_t csr_transpose_rows(const int32_t *rp, const int32_t *ci, const double *va, int64_t rows,
+                               int64_t cols, int64_t nnz, int64_t c0, int64_t nc, int32_t **rp_t,
+                               int32_t **ci_t, double **va_t, int64_t *nnz_t, cudaStream_t s);
+int csr_group_size(double avg_nnz_per_row);
 
 // kernels_dense.cu
 cudaError_t launch_pass_a(const PassAArgs &a, int mode, const LaunchCfg &cfg, cudaStream_t s);

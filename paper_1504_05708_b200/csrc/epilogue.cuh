@@ -1,0 +1,135 @@
+// Row epilogues shared by every pass kernel (dense, CSR): identical arithmetic
+// whatever produced the row value, so formats and shardings agree bit for bit
+// on the vector part of the step.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "duquad_internal.h"
+
+namespace dq {
+
+// [v]_K per row tag: ZERO -> 0, NONPOS -> min(v, 0)
+__device__ __forceinline__ double proj_K(double v, uint8_t c) {
+    return c == DUQUAD_CONE_NONPOS ? fmin(v, 0.0) : 0.0;
+}
+// projection onto the polar cone K° (multiplier sign set): ZERO -> v, NONPOS -> max(v, 0)
+__device__ __forceinline__ double proj_polar(double v, uint8_t c) {
+    return c == DUQUAD_CONE_NONPOS ? fmax(v, 0.0) : v;
+}
+
+__device__ __forceinline__ double warp_sum(double s) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
+template <int GS>
+__device__ __forceinline__ double group_sum(double s) {
+#pragma unroll
+    for (int o = GS / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
+// ------------------------------------------------------------------ pass A
+struct EpiA {
+    double g, mu, lp;
+    uint8_t c;
+};
+
+struct OuterA {
+    int dual;
+    double beta_out;
+};
+
+__device__ __forceinline__ OuterA outer_a(const PassAArgs &a, int mode) {
+    OuterA o{0, 0.0};
+    if (mode == MODE_SOLVE && a.first_inner) {
+        const OuterParam op = a.ops[*a.d_j];
+        o.dual = op.dual_update;
+        o.beta_out = op.beta_out;
+    }
+    return o;
+}
+
+__device__ __forceinline__ EpiA epi_a_load(const PassAArgs &a, int mode, int64_t row, const OuterA &o) {
+    EpiA e{0.0, 0.0, 0.0, 0};
+    if (mode == MODE_SOLVE && row >= a.nq) {
+        const int64_t k = row - a.nq;
+        e.g = a.g[k];
+        e.mu = a.mu[k];
+        e.c = a.cone[k];
+        if (o.dual) e.lp = a.lam_prev[k];
+    }
+    return e;
+}
+
+// s = (row of [Q;G]) . y
+__device__ __forceinline__ void epi_a_store(const PassAArgs &a, int mode, int64_t row, double s,
+                                            const EpiA &e, const OuterA &o) {
+    if (row < a.nq) {
+        a.qy[row] = s;
+        return;
+    }
+    const int64_t k = row - a.nq;
+    if (mode == MODE_LIN) {
+        a.w[k] = a.lin_coef * s;
+        return;
+    }
+    const double r = s + e.g;                      // r = G y + g
+    double m = e.mu;
+    if (o.dual) {
+        // y == u_bar^{j-1}: DFOM step with the slack s(u, mu)
+        const double sl = a.rho > 0.0 ? proj_K(r + e.mu / a.rho, e.c) : 0.0;
+        double lam = e.mu + a.step * (r - sl);
+        if (a.project_dual && e.c == DUQUAD_CONE_NONPOS) lam = fmax(lam, 0.0);
+        m = lam + o.beta_out * (lam - e.lp);
+        a.lam_prev[k] = lam;
+        a.mu[k] = m;
+    }
+    // multiplier term of grad L_rho: [mu + rho r]_{K°} (rho > 0), mu (rho = 0)
+    a.w[k] = a.rho > 0.0 ? proj_polar(m + a.rho * r, e.c) : m;
+}
+
+// ------------------------------------------------------------------ pass B
+struct EpiB {
+    double qy, q, lb, ub, x, y, xh;
+};
+
+__device__ __forceinline__ double avg_weight(const PassBArgs &b, int mode) {
+    return (mode == MODE_SOLVE && b.last_inner) ? b.ops[*b.d_j].avg_w : 0.0;
+}
+
+__device__ __forceinline__ EpiB epi_b_load(const PassBArgs &b, int mode, int64_t j, double avg_w) {
+    EpiB e{0, 0, 0, 0, 0, 0, 0};
+    if (mode == MODE_SOLVE || b.use_qy) e.qy = b.qy[j];
+    if (mode == MODE_SOLVE) {
+        e.q = b.q[j];
+        e.lb = b.lb[j];
+        e.ub = b.ub[j];
+        e.x = b.x[j];
+        e.y = b.y[j];
+        if (avg_w != 0.0) e.xh = b.xhat[j];
+    }
+    return e;
+}
+
+// t = (row j of G') . w
+__device__ __forceinline__ void epi_b_store(const PassBArgs &b, int mode, int64_t j, double t, const EpiB &e,
+                                            double avg_w) {
+    if (mode == MODE_LIN) {
+        b.out[j] = e.qy + t;
+        return;
+    }
+    const double grad = (e.qy + e.q) + t;
+    const double xn = fmin(fmax(e.y - grad / b.L_in, e.lb), e.ub);
+    const double yn = b.last_inner ? xn : xn + b.beta_in * (xn - e.x);
+    if (avg_w != 0.0) b.xhat[j] = e.xh + avg_w * (xn - e.xh);      // P:700-706 (running form)
+    b.x[j] = xn;
+    b.y[j] = yn;
+    if (!isfinite(xn) || !isfinite(yn)) *b.flag = 1;
+}
+
+}  // namespace dq

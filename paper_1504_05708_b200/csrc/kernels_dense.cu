@@ -20,6 +20,7 @@
 #include <stdint.h>
 
 #include "duquad_internal.h"
+#include "epilogue.cuh"
 
 namespace dq {
 
@@ -34,12 +35,6 @@ __device__ __forceinline__ double2 ldg_stream(const double2 *p) {
         : "=d"(r.x), "=d"(r.y)
         : "l"(p));
     return r;
-}
-
-__device__ __forceinline__ double warp_sum(double s) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    return s;
 }
 
 // Dot product of one matrix row (nv2 double2 entries, 16-byte aligned) with a
@@ -78,15 +73,6 @@ __device__ __forceinline__ void stage(double *s, const double *g, int64_t len) {
     for (int64_t i = threadIdx.x; i < n2; i += blockDim.x) s2[i] = g2[i];
 }
 
-// [v]_K per row tag: ZERO -> 0, NONPOS -> min(v, 0)
-__device__ __forceinline__ double proj_K(double v, uint8_t c) {
-    return c == DUQUAD_CONE_NONPOS ? fmin(v, 0.0) : 0.0;
-}
-// projection onto the polar cone K° (multiplier sign set): ZERO -> v, NONPOS -> max(v, 0)
-__device__ __forceinline__ double proj_polar(double v, uint8_t c) {
-    return c == DUQUAD_CONE_NONPOS ? fmax(v, 0.0) : v;
-}
-
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1) k_pass_a(const PassAArgs a) {
     extern __shared__ __align__(16) double smem[];
@@ -99,48 +85,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass_a(const PassAArgs a) {
     const int64_t r0 = a.row_begin + rows * blockIdx.x / gridDim.x;
     const int64_t r1 = a.row_begin + rows * (blockIdx.x + 1) / gridDim.x;
     const int nv2 = (int)(a.ld >> 1);
-    int dual = 0;
-    double beta_out = 0.0;
-    if (MODE == MODE_SOLVE && a.first_inner) {
-        const OuterParam op = a.ops[*a.d_j];
-        dual = op.dual_update;
-        beta_out = op.beta_out;
-    }
+    const OuterA o = outer_a(a, MODE);
     for (int64_t row = r0 + warp; row < r1; row += nw) {
         // epilogue operands are fetched before the stream so their latency overlaps it
-        const bool is_g = row >= a.nq;
-        const int64_t k = row - a.nq;
-        double gk = 0.0, muk = 0.0, lpk = 0.0;
-        uint8_t ck = 0;
-        if (MODE == MODE_SOLVE && is_g && lane == 0) {
-            gk = a.g[k];
-            muk = a.mu[k];
-            ck = a.cone[k];
-            if (dual) lpk = a.lam_prev[k];
-        }
+        EpiA e{};
+        if (lane == 0) e = epi_a_load(a, MODE, row, o);
         const double s = row_dot(reinterpret_cast<const double2 *>(a.A + row * a.ld), sv, nv2, lane);
-        if (lane != 0) continue;
-        if (!is_g) {
-            a.qy[row] = s;
-            continue;
-        }
-        if (MODE == MODE_LIN) {
-            a.w[k] = a.lin_coef * s;
-            continue;
-        }
-        const double r = s + gk;                       // r = G y + g
-        double m = muk;
-        if (dual) {
-            // y == u_bar^{j-1}: DFOM step, slack s(u, mu)
-            const double sl = a.rho > 0.0 ? proj_K(r + muk / a.rho, ck) : 0.0;
-            double lam = muk + a.step * (r - sl);
-            if (a.project_dual && ck == DUQUAD_CONE_NONPOS) lam = fmax(lam, 0.0);
-            m = lam + beta_out * (lam - lpk);
-            a.lam_prev[k] = lam;
-            a.mu[k] = m;
-        }
-        // multiplier term of grad L_rho: [mu + rho r]_{K°} (rho > 0), mu (rho = 0)
-        a.w[k] = a.rho > 0.0 ? proj_polar(m + a.rho * r, ck) : m;
+        if (lane == 0) epi_a_store(a, MODE, row, s, e, o);
     }
 }
 
@@ -155,35 +106,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass_b(const PassBArgs b) {
     const int64_t r0 = b.nrows * blockIdx.x / gridDim.x;
     const int64_t r1 = b.nrows * (blockIdx.x + 1) / gridDim.x;
     const int nv2 = (int)(b.ldp >> 1);
-    double avg_w = 0.0;
-    if (MODE == MODE_SOLVE && b.last_inner) avg_w = b.ops[*b.d_j].avg_w;
+    const double avg_w = avg_weight(b, MODE);
     for (int64_t j = r0 + warp; j < r1; j += nw) {
-        double qyj = 0.0, qj = 0.0, lbj = 0.0, ubj = 0.0, xj = 0.0, yj = 0.0, xhj = 0.0;
-        if (lane == 0) {
-            if (MODE == MODE_SOLVE || b.use_qy) qyj = b.qy[j];
-            if (MODE == MODE_SOLVE) {
-                qj = b.q[j];
-                lbj = b.lb[j];
-                ubj = b.ub[j];
-                xj = b.x[j];
-                yj = b.y[j];
-                if (avg_w != 0.0) xhj = b.xhat[j];
-            }
-        }
+        EpiB e{};
+        if (lane == 0) e = epi_b_load(b, MODE, j, avg_w);
         const double t = nv2 > 0 ? row_dot(reinterpret_cast<const double2 *>(b.GT + j * b.ldp), sv, nv2, lane)
                                  : 0.0;
-        if (lane != 0) continue;
-        if (MODE == MODE_LIN) {
-            b.out[j] = qyj + t;
-            continue;
-        }
-        const double grad = (qyj + qj) + t;
-        const double xn = fmin(fmax(yj - grad / b.L_in, lbj), ubj);
-        const double yn = b.last_inner ? xn : xn + b.beta_in * (xn - xj);
-        if (avg_w != 0.0) b.xhat[j] = xhj + avg_w * (xn - xhj);     // P:700-706 (running form)
-        b.x[j] = xn;
-        b.y[j] = yn;
-        if (!isfinite(xn) || !isfinite(yn)) *b.flag = 1;
+        if (lane == 0) epi_b_store(b, MODE, j, t, e, avg_w);
     }
 }
 
@@ -372,6 +301,7 @@ cudaError_t configure_pass_kernels(size_t smem_a, size_t smem_b) {
 
 cudaError_t launch_pass_a(const PassAArgs &a, int mode, const LaunchCfg &cfg, cudaStream_t s) {
     if (a.row_end <= a.row_begin) return cudaSuccess;
+    if (a.fmt == DUQUAD_CSR) return launch_pass_a_csr(a, mode, cfg, s);
     if (mode == MODE_SOLVE)
         k_pass_a<MODE_SOLVE><<<cfg.grid, kThreads, cfg.smem, s>>>(a);
     else
@@ -381,6 +311,7 @@ cudaError_t launch_pass_a(const PassAArgs &a, int mode, const LaunchCfg &cfg, cu
 
 cudaError_t launch_pass_b(const PassBArgs &b, int mode, const LaunchCfg &cfg, cudaStream_t s) {
     if (b.nrows <= 0) return cudaSuccess;
+    if (b.fmt == DUQUAD_CSR) return launch_pass_b_csr(b, mode, cfg, s);
     if (mode == MODE_SOLVE)
         k_pass_b<MODE_SOLVE><<<cfg.grid, kThreads, cfg.smem, s>>>(b);
     else

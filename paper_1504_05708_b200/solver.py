@@ -66,50 +66,87 @@ class Solver:
                  use_graphs: bool = True, world_size: int = 1, rank: int = 0,
                  nccl_id: Optional[bytes] = None, stream=None, device: int = -1,
                  time_passes: bool = False, cone_all: int = L.CONE_NONPOS):
+        """Dense Q (n x n) and G (p x n), or scipy.sparse matrices (-> CSR path, row a10)."""
+        if hasattr(Q, "tocsr"):
+            Qc = Q.tocsr()
+            Qc.sort_indices()
+            Gc = G.tocsr()
+            Gc.sort_indices()
+            arrs = dict(Q_rowptr=_Arr(Qc.indptr, np.int32), Q_col=_Arr(Qc.indices, np.int32),
+                        Q_val=_Arr(Qc.data, np.float64), G_rowptr=_Arr(Gc.indptr, np.int32),
+                        G_col=_Arr(Gc.indices, np.int32), G_val=_Arr(Gc.data, np.float64))
+            n, p = Qc.shape[0], Gc.shape[0]
+            fmt, nnz = L.CSR, (Qc.nnz, Gc.nnz)
+        else:
+            arrs = dict(Q=_Arr(Q, np.float64), G=_Arr(G, np.float64))
+            n = int(arrs["Q"].obj.shape[0])
+            p = int(arrs["G"].obj.shape[0]) if arrs["G"].obj is not None else 0
+            fmt, nnz = L.DENSE, (0, 0)
+        self._init(arrs, fmt, n, p, nnz, q, g, lb, ub, cone, rho, cone_all,
+                   dict(dual_step_scale=dual_step_scale, project_dual=project_dual, inner_rule=inner_rule,
+                        sigma=sigma, lambda_min_lb=lambda_min_lb, l_mode=l_mode, use_graphs=use_graphs,
+                        world_size=world_size, rank=rank, nccl_id=nccl_id, stream=stream, device=device,
+                        time_passes=time_passes))
+
+    @classmethod
+    def csr(cls, n, p, Q_rowptr, Q_col, Q_val, G_rowptr, G_col, G_val, q, g, lb, ub, cone=None,
+            rho: float = 1.0, cone_all: int = L.CONE_ZERO, **opts):
+        """CSR problem from raw arrays (NumPy on the host or torch on the device; int32 indices)."""
+        self = cls.__new__(cls)
+        arrs = dict(Q_rowptr=_Arr(Q_rowptr, np.int32), Q_col=_Arr(Q_col, np.int32), Q_val=_Arr(Q_val, np.float64),
+                    G_rowptr=_Arr(G_rowptr, np.int32), G_col=_Arr(G_col, np.int32), G_val=_Arr(G_val, np.float64))
+        nnz = (int(arrs["Q_val"].obj.shape[0]), int(arrs["G_val"].obj.shape[0]))
+        defaults = dict(dual_step_scale=0.5, project_dual=True, inner_rule="FGM", sigma=0.0, lambda_min_lb=0.0,
+                        l_mode=0, use_graphs=True, world_size=1, rank=0, nccl_id=None, stream=None, device=-1,
+                        time_passes=False)
+        defaults.update(opts)
+        self._init(arrs, L.CSR, int(n), int(p), nnz, q, g, lb, ub, cone, rho, cone_all, defaults)
+        return self
+
+    def _init(self, arrs, fmt, n, p, nnz, q, g, lb, ub, cone, rho, cone_all, o):
         lib = L.lib()
         self._lib = lib
-        arrs = dict(Q=_Arr(Q, np.float64), q=_Arr(q, np.float64), G=_Arr(G, np.float64),
-                    g=_Arr(g, np.float64), lb=_Arr(lb, np.float64), ub=_Arr(ub, np.float64),
-                    cone=_Arr(cone, np.uint8))
-        devs = {k: a.dev for k, a in arrs.items() if a.obj is not None}
+        arrs.update(q=_Arr(q, np.float64), g=_Arr(g, np.float64), lb=_Arr(lb, np.float64),
+                    ub=_Arr(ub, np.float64), cone=_Arr(cone, np.uint8))
+        devs = {k: a.dev for k, a in arrs.items() if a.obj is not None and getattr(a.obj, "size", 1) != 0}
         if len(set(devs.values())) > 1:
             raise ValueError("problem arrays must be all on the host or all on the device")
         on_device = bool(devs and next(iter(devs.values())))
-        n = int(arrs["Q"].obj.shape[0])
-        p = int(arrs["G"].obj.shape[0]) if arrs["G"].obj is not None else 0
         prob = L.Problem()
         prob.n, prob.p, prob.batch = n, p, 1
-        prob.format = L.DENSE
+        prob.format = fmt
         prob.on_device = int(on_device)
-        prob.Q, prob.ldQ = arrs["Q"].ptr, n
-        prob.G, prob.ldG = arrs["G"].ptr, n
-        prob.q, prob.g, prob.lb, prob.ub = arrs["q"].ptr, arrs["g"].ptr, arrs["lb"].ptr, arrs["ub"].ptr
-        prob.cone = arrs["cone"].ptr
+        for k, a in arrs.items():
+            setattr(prob, k, a.ptr)
+        prob.ldQ = prob.ldG = n
+        prob.Q_nnz, prob.G_nnz = nnz
         prob.cone_all = cone_all
         opt = L.Options()
         lib.duquad_default_options(C.byref(opt))
-        opt.dual_step_scale = dual_step_scale
-        opt.project_dual = int(project_dual)
-        opt.inner_rule = _INNER[inner_rule]
-        opt.sigma = sigma
-        opt.lambda_min_lb = lambda_min_lb
-        opt.l_mode = l_mode
-        opt.use_graphs = int(use_graphs)
-        opt.world_size = world_size
-        opt.rank = rank
-        self._nccl_id = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        opt.dual_step_scale = o["dual_step_scale"]
+        opt.project_dual = int(o["project_dual"])
+        opt.inner_rule = _INNER[o["inner_rule"]]
+        opt.sigma = o["sigma"]
+        opt.lambda_min_lb = o["lambda_min_lb"]
+        opt.l_mode = o["l_mode"]
+        opt.use_graphs = int(o["use_graphs"])
+        opt.world_size = o["world_size"]
+        opt.rank = o["rank"]
+        nid = o["nccl_id"]
+        self._nccl_id = C.create_string_buffer(nid, 128) if nid is not None else None
         opt.nccl_id = C.cast(self._nccl_id, C.c_void_p) if self._nccl_id is not None else None
-        opt.stream = stream
-        opt.device = device
-        opt.time_passes = int(time_passes)
+        opt.stream = o["stream"]
+        opt.device = o["device"]
+        opt.time_passes = int(o["time_passes"])
         ctx = C.c_void_p()
         L.check(lib.duquad_setup(C.byref(ctx), C.byref(prob), float(rho), C.byref(opt)))
         self._ctx = ctx
         self.n, self.p, self.rho = n, p, float(rho)
-        self.world_size, self.rank = world_size, rank
-        self.n_range = shard_range(n, world_size, rank)
-        self.p_range = shard_range(p, world_size, rank)
-        self.device = device
+        self.format = fmt
+        self.world_size, self.rank = o["world_size"], o["rank"]
+        self.n_range = shard_range(n, self.world_size, self.rank)
+        self.p_range = shard_range(p, self.world_size, self.rank)
+        self.device = o["device"]
         self.last_result = None
 
     # ------------------------------------------------------------------ API

@@ -1,0 +1,148 @@
+"""CSR path (BASELINE.json configs[4]) vs the oracle (-m gpu)."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import qpgen
+from oracle import dfom as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+def relerr(got, want):
+    got, want = np.asarray(got, float), np.asarray(want, float)
+    if want.size == 0:
+        return 0.0
+    return float(np.max(np.abs(got - want)) / (1.0 + np.max(np.abs(want))))
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def _consts_dense(prob, rho, lmin):
+    return O.lipschitz_constants(prob.Q.toarray(), prob.G.toarray(), rho, lmin)
+
+
+def _gpu(prob, rho, alg, K, Kin, L_in, L_d, trace=False, torch=None, **kw):
+    from paper_1504_05708_b200 import Solver
+    s = Solver(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho=rho, **kw)
+    s.set_constants(L_in, L_d)
+    out = {}
+    if trace:
+        tl = torch.zeros((K, max(prob.p, 1)), dtype=torch.float64, device="cuda")
+        tu = torch.zeros((K, prob.n), dtype=torch.float64, device="cuda")
+        s.set_trace(tl, tu, K)
+    s.solve(alg, K, Kin)
+    out["x_last"], out["x_avg"], out["lam"] = s.result()
+    if trace:
+        out["trace_lam"] = tl.cpu().numpy()[:, :prob.p]
+        out["trace_u"] = tu.cpu().numpy()
+    out["solver"] = s
+    return out
+
+
+def _check(g, r, trace=False):
+    assert relerr(g["x_last"], r.x_last) <= TOL
+    assert relerr(g["x_avg"], r.x_avg) <= TOL
+    assert relerr(g["lam"], r.lam) <= TOL
+    if trace:
+        for j in range(len(r.trace_lam)):
+            assert relerr(g["trace_lam"][j], r.trace_lam[j]) <= TOL, j
+            assert relerr(g["trace_u"][j], r.trace_u[j]) <= TOL, j
+
+
+@pytest.mark.parametrize("alg", ["DGM", "DFGM"])
+@pytest.mark.parametrize("K,Kin", [(1, 1), (3, 5), (12, 10)])
+def test_banded_small_parity_with_trace(torch_cuda, alg, K, Kin):
+    prob = qpgen.sparse_banded_eq(n=300, p=100, seed=3)
+    L_in, L_d, _ = _consts_dense(prob, 5.0, 0.5)
+    g = _gpu(prob, 5.0, alg, K, Kin, L_in, L_d, trace=True, torch=torch_cuda)
+    r = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 5.0, alg, K, Kin, L_in, L_d,
+               keep_trace=True)
+    _check(g, r, trace=True)
+
+
+@pytest.mark.parametrize("kind,rho", [("ineq", 1.0), ("mixed", 0.0), ("eq", 2.0)])
+def test_random_sparse_cones(torch_cuda, kind, rho):
+    """Sparse versions of the tiny families (inequality / mixed / equality, rho = 0 too)."""
+    d = qpgen.tiny(150, 60, seed=7, kind=kind)
+    rng = np.random.default_rng(1)
+    mask = rng.random(d.G.shape) < 0.1
+    G = sp.csr_matrix(np.where(mask, d.G, 0.0))
+    g = -(G @ d.meta["x0"]) - np.where(d.cone == qpgen.NONPOS, 0.3, 0.0)
+    Q = sp.csr_matrix(np.where(np.abs(d.Q) > 0.05, d.Q, 0.0) + 0.5 * np.eye(150))
+    prob = qpgen.SparseQP(Q, d.q, G, g, d.lb, d.ub, d.cone)
+    lmin = float(np.linalg.eigvalsh(Q.toarray())[0])
+    assert lmin > 0
+    L_in, L_d, _ = O.lipschitz_constants(Q.toarray(), G.toarray(), rho, lmin)
+    g_ = _gpu(prob, rho, "DFGM", 9, 8, L_in, L_d)
+    r = O.dfom(Q, d.q, G, g, d.lb, d.ub, d.cone, rho, O.DFGM, 9, 8, L_in, L_d)
+    _check(g_, r)
+
+
+def test_csr_matches_dense_path(torch_cuda):
+    """The same QP through the dense and the CSR kernels (different summation order only)."""
+    from paper_1504_05708_b200 import Solver
+    prob = qpgen.sparse_banded_eq(n=500, p=200, seed=5)
+    L_in, L_d, _ = _consts_dense(prob, 5.0, 0.5)
+    a = _gpu(prob, 5.0, "DFGM", 20, 10, L_in, L_d)
+    s = Solver(prob.Q.toarray(), prob.q, prob.G.toarray(), prob.g, prob.lb, prob.ub, prob.cone, rho=5.0)
+    s.set_constants(L_in, L_d)
+    s.solve("DFGM", 20, 10)
+    xl, xa, lam = s.result()
+    assert relerr(a["x_last"], xl) <= 1e-12 and relerr(a["lam"], lam) <= 1e-12
+
+
+def test_device_csr_inputs_and_lipschitz(torch_cuda):
+    from paper_1504_05708_b200 import Solver
+    torch = torch_cuda
+    prob = qpgen.sparse_banded_eq(n=400, p=150, seed=9)
+    Q, G = prob.Q, prob.G
+    dv = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dtype=dt)
+    s = Solver.csr(400, 150, dv(Q.indptr, torch.int32), dv(Q.indices, torch.int32), dv(Q.data, torch.float64),
+                   dv(G.indptr, torch.int32), dv(G.indices, torch.int32), dv(G.data, torch.float64),
+                   dv(prob.q, torch.float64), dv(prob.g, torch.float64), dv(prob.lb, torch.float64),
+                   dv(prob.ub, torch.float64), dv(prob.cone, torch.uint8), rho=5.0, lambda_min_lb=0.5)
+    L_in, L_d, nG2 = s.lipschitz(iters=120)
+    rL, rd, rn = _consts_dense(prob, 5.0, 0.5)
+    assert abs(L_in - rL) <= 1e-9 * rL and abs(nG2 - rn) <= 1e-9 * rn and abs(L_d - rd) <= 1e-9 * rd
+    s.set_constants(rL, rd)
+    s.solve("DGM", 6, 7)
+    xl, xa, lam = s.result()
+    r = O.dfom(Q, prob.q, G, prob.g, prob.lb, prob.ub, prob.cone, 5.0, O.DGM, 6, 7, rL, rd)
+    assert relerr(xl, r.x_last) <= TOL and relerr(lam, r.lam) <= TOL
+
+
+def test_invalid_csr_is_rejected(torch_cuda):
+    from paper_1504_05708_b200 import Solver, DuquadError
+    prob = qpgen.sparse_banded_eq(n=50, p=10, seed=1)
+    G = prob.G.copy()
+    G.indices[3] = 50          # column out of range
+    with pytest.raises(DuquadError) as e:
+        Solver(prob.Q, prob.q, G, prob.g, prob.lb, prob.ub, prob.cone, rho=1.0)
+    assert e.value.status == 1
+
+
+@pytest.fixture(scope="module")
+def c4():
+    return qpgen.sparse_banded_eq()      # BASELINE.json configs[4] at full size
+
+
+def test_config4_full_size_prefix(torch_cuda, c4):
+    """configs[4] at full size (n = 1e6, p = 5e5, 15M + 4M nnz) in the bench launch configuration:
+    DFGM and DGM rho = 5 prefixes against the SciPy-CSR oracle, with per-outer trace."""
+    from paper_1504_05708_b200 import Solver
+    s = Solver(c4.Q, c4.q, c4.G, c4.g, c4.lb, c4.ub, c4.cone, rho=5.0, lambda_min_lb=0.5)
+    L_in, L_d, nG2 = s.lipschitz(iters=40, safety=1e-3)
+    assert 5.0 * nG2 <= L_in <= (3.0 + 5.0 * nG2) * 1.01       # lambda_max(Q) <= 3 (Gershgorin)
+    s.close()
+    for alg in ("DFGM", "DGM"):
+        g = _gpu(c4, 5.0, alg, 4, 6, L_in, L_d, trace=True, torch=torch_cuda)
+        r = O.dfom(c4.Q, c4.q, c4.G, c4.g, c4.lb, c4.ub, c4.cone, 5.0, alg, 4, 6, L_in, L_d, keep_trace=True)
+        _check(g, r, trace=True)
