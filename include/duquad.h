@@ -139,6 +139,8 @@ typedef struct {
     int64_t n_timed_a, n_timed_b;
     double bytes_pass_a;        /* algorithmic bytes per pass-A launch (matrix + vectors) */
     double bytes_pass_b;        /* algorithmic bytes per pass-B launch                    */
+    double flops_pass_a;        /* algorithmic flops per pass-A launch (2 per multiply-add) */
+    double flops_pass_b;
 } duquad_result;
 
 int32_t duquad_abi_version(void);

@@ -62,6 +62,7 @@ class Result(C.Structure):
         ("ms_device", C.c_double), ("ms_pass_a", C.c_double), ("ms_pass_b", C.c_double),
         ("n_timed_a", C.c_int64), ("n_timed_b", C.c_int64),
         ("bytes_pass_a", C.c_double), ("bytes_pass_b", C.c_double),
+        ("flops_pass_a", C.c_double), ("flops_pass_b", C.c_double),
     ]
 
 

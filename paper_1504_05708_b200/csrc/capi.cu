@@ -53,6 +53,10 @@ struct duquad_ctx {
     double *a_va = nullptr, *b_va = nullptr;
     int64_t nnz_a = 0, nnz_b = 0;
     int gs_a = 4, gs_b = 4;
+    // batched storage (batch > 1): QP-major per-QP vectors, strides ld (n-vectors) / ldp (p-vectors)
+    int64_t Btot = 1, Bloc = 1, b0 = 0;
+    double *Yb = nullptr, *Xb = nullptr, *XHb = nullptr, *QYb = nullptr, *qb = nullptr;
+    double *Wb = nullptr, *gb = nullptr, *mub = nullptr, *lpb = nullptr;
     double *scal = nullptr;       // device scalars
     double *partials = nullptr;   // kRedGrid * 5
     OuterParam *d_ops = nullptr;
@@ -107,8 +111,10 @@ cudaError_t dalloc(T **p, int64_t count) {
 }
 
 void free_all(duquad_ctx *c) {
-    double *ds[] = {c->A, c->GT, c->y_full, c->w_full, c->qy, c->x, c->xhat, c->q, c->lb, c->ub,
-                    c->g, c->mu, c->lam_prev, c->lz_vprev, c->lz_w, c->scal, c->partials};
+    double *ds[] = {c->A,   c->GT,  c->y_full, c->w_full, c->qy,       c->x,        c->xhat,     c->q,
+                    c->lb,  c->ub,  c->g,      c->mu,     c->lam_prev, c->lz_vprev, c->lz_w,     c->scal,
+                    c->partials, c->Yb, c->Xb, c->XHb,   c->QYb,      c->qb,       c->Wb,       c->gb,
+                    c->mub, c->lpb};
     for (double *d : ds)
         if (d) cudaFree(d);
     if (c->cone) cudaFree(c->cone);
@@ -217,25 +223,39 @@ PassBArgs make_b(duquad_ctx *c) {
     return b;
 }
 
+BatchedArgs make_batched(duquad_ctx *c, int pass);
+
 // One outer DFOM iteration (reads its per-outer scalars through d_j).
 duquad_status run_outer(duquad_ctx *ctx, const std::vector<double> &beta_in, int Kin, int j,
                         std::vector<cudaEvent_t> *ev) {
     PassAArgs a = make_a(ctx);
     PassBArgs b = make_b(ctx);
+    const bool bt = ctx->Btot > 1;
+    BatchedArgs BA{}, BB{};
+    if (bt) {
+        BA = make_batched(ctx, 0);
+        BB = make_batched(ctx, 1);
+    }
     duquad_status st;
     for (int k = 1; k <= Kin; ++k) {
-        a.first_inner = (k == 1);
+        a.first_inner = BA.a.first_inner = (k == 1);
         if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 0], ctx->stream));
-        CK(launch_pass_a(a, MODE_SOLVE, ctx->cfg_a, ctx->stream));
+        if (bt)
+            CK(launch_batched(BA, 0, MODE_SOLVE, ctx->stream));
+        else
+            CK(launch_pass_a(a, MODE_SOLVE, ctx->cfg_a, ctx->stream));
         if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 1], ctx->stream));
         if ((st = allgather_w(ctx)) != DUQUAD_OK) return st;
         if (k == 1 && j >= 2 && ctx->trace_lam && j - 2 < ctx->trace_max)
             CK(cudaMemcpyAsync(ctx->trace_lam + (j - 2) * ctx->ploc, ctx->lam_prev,
                                ctx->ploc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
-        b.beta_in = beta_in[k];
-        b.last_inner = (k == Kin);
+        b.beta_in = BB.b.beta_in = beta_in[k];
+        b.last_inner = BB.b.last_inner = (k == Kin);
         if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 2], ctx->stream));
-        CK(launch_pass_b(b, MODE_SOLVE, ctx->cfg_b, ctx->stream));
+        if (bt)
+            CK(launch_batched(BB, 1, MODE_SOLVE, ctx->stream));
+        else
+            CK(launch_pass_b(b, MODE_SOLVE, ctx->cfg_b, ctx->stream));
         if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 3], ctx->stream));
         if ((st = allgather_y(ctx)) != DUQUAD_OK) return st;
     }
@@ -244,6 +264,43 @@ duquad_status run_outer(duquad_ctx *ctx, const std::vector<double> &beta_in, int
                            cudaMemcpyDeviceToDevice, ctx->stream));
     CK(launch_advance(ctx->d_j, ctx->stream));
     return DUQUAD_OK;
+}
+
+// Batched passes (row a9): the single-QP argument blocks re-pointed at QP 0 of the
+// QP-major batched vectors; the kernels offset them per QP.
+BatchedArgs make_batched(duquad_ctx *c, int pass) {
+    BatchedArgs ba{};
+    ba.a = make_a(c);
+    ba.b = make_b(c);
+    ba.sn = c->ld;
+    ba.sp = std::max<int64_t>(c->ldp, 2);
+    ba.N = c->Bloc;
+    ba.a.qy = c->QYb;
+    ba.a.w = c->Wb;
+    ba.a.g = c->gb;
+    ba.a.mu = c->mub;
+    ba.a.lam_prev = c->lpb;
+    ba.b.qy = c->QYb;
+    ba.b.q = c->qb;
+    ba.b.x = c->Xb;
+    ba.b.y = c->Yb;
+    ba.b.xhat = c->XHb;
+    if (pass == 0) {   // [Q;G] (n+p x n) . Y
+        ba.Aop = c->A;
+        ba.lda = c->ld;
+        ba.M = c->n + c->p;
+        ba.Bop = c->Yb;
+        ba.ldb = c->ld;
+        ba.K = c->ld;
+    } else {           // G' (n x p) . W
+        ba.Aop = c->GT;
+        ba.lda = c->ldp;
+        ba.M = c->n;
+        ba.Bop = c->Wb;
+        ba.ldb = ba.sp;
+        ba.K = c->ldp;
+    }
+    return ba;
 }
 
 // Linear operator for Lanczos: out = op(v), v given in the y_full replica.
@@ -519,7 +576,10 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
     const int64_t n = prob->n, p = prob->p;
     if (n < 1 || p < 0) return fail(nullptr, DUQUAD_EINVAL, "need n >= 1 and p >= 0");
     if (!(rho >= 0.0) || !std::isfinite(rho)) return fail(nullptr, DUQUAD_EINVAL, "rho must be finite and >= 0");
-    if (prob->batch != 1) return fail(nullptr, DUQUAD_EINVAL, "batch > 1 not supported by this build");
+    if (prob->batch < 1) return fail(nullptr, DUQUAD_EINVAL, "batch must be >= 1");
+    const bool batched = prob->batch > 1;
+    if (batched && prob->format != DUQUAD_DENSE) return fail(nullptr, DUQUAD_EINVAL, "batch > 1 needs dense Q, G");
+    if (batched && (n > 27000 || p > 27000)) return fail(nullptr, DUQUAD_EINVAL, "batched path: n, p too large");
     const bool csr = prob->format == DUQUAD_CSR;
     if (prob->format != DUQUAD_DENSE && !csr) return fail(nullptr, DUQUAD_EINVAL, "bad format");
     if (!prob->q || !prob->lb || !prob->ub || (p > 0 && !prob->g))
@@ -539,10 +599,11 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         return fail(nullptr, DUQUAD_EINVAL, "FGM_SIGMA needs sigma > 0");
     if (opt.world_size < 1 || opt.rank < 0 || opt.rank >= opt.world_size)
         return fail(nullptr, DUQUAD_EINVAL, "bad world_size / rank");
-    if (opt.world_size > 1 && !opt.nccl_id) return fail(nullptr, DUQUAD_EINVAL, "sharded setup needs nccl_id");
+    if (opt.world_size > 1 && !batched && !opt.nccl_id)
+        return fail(nullptr, DUQUAD_EINVAL, "row-sharded setup needs nccl_id");
     if (!prob->on_device) {   // host data: validate here (device data is validated by a kernel)
         if ((!csr && (!finite_host(prob->Q, n, n, prob->ldQ) || (p > 0 && !finite_host(prob->G, p, n, prob->ldG)))) ||
-            !finite_host(prob->q, 1, n, n) || (p > 0 && !finite_host(prob->g, 1, p, p)))
+            !finite_host(prob->q, prob->batch, n, n) || (p > 0 && !finite_host(prob->g, prob->batch, p, p)))
             return fail(nullptr, DUQUAD_EINVAL, "non-finite problem data");
         for (int64_t i = 0; i < n; ++i)
             if (std::isnan(prob->lb[i]) || std::isnan(prob->ub[i]) || prob->lb[i] > prob->ub[i] ||
@@ -593,9 +654,15 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         CKS(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         ctx->own_stream = true;
     }
-    // ---- sharding
-    ctx->world = opt.world_size;
-    ctx->rank = opt.rank;
+    // ---- sharding: rows of one QP over the ranks (NCCL), or, batched, whole QPs (no collective)
+    ctx->world = batched ? 1 : opt.world_size;
+    ctx->rank = batched ? 0 : opt.rank;
+    ctx->Btot = prob->batch;
+    {
+        const int64_t bs = (prob->batch + opt.world_size - 1) / opt.world_size;
+        ctx->b0 = std::min<int64_t>(prob->batch, (int64_t)opt.rank * bs);
+        ctx->Bloc = std::min<int64_t>(prob->batch, ctx->b0 + bs) - ctx->b0;
+    }
     ctx->n_slice = (n + ctx->world - 1) / ctx->world;
     ctx->p_slice = (p + ctx->world - 1) / ctx->world;
     ctx->r0 = std::min<int64_t>(n, ctx->rank * ctx->n_slice);
@@ -685,8 +752,32 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         else
             CKS(cudaMemsetAsync(ctx->cone, prob->cone_all, ctx->ploc, s));
     }
+    if (batched) {   // QP-major per-QP vectors of this rank's QPs [b0, b0 + Bloc)
+        const int64_t B = ctx->Bloc, lp = std::max<int64_t>(ctx->ldp, 2);
+        CKS(dalloc(&ctx->Yb, B * ctx->ld));
+        CKS(dalloc(&ctx->Xb, B * ctx->ld));
+        CKS(dalloc(&ctx->XHb, B * ctx->ld));
+        CKS(dalloc(&ctx->QYb, B * ctx->ld));
+        CKS(dalloc(&ctx->qb, B * ctx->ld));
+        CKS(dalloc(&ctx->Wb, B * lp));
+        CKS(dalloc(&ctx->gb, B * lp));
+        CKS(dalloc(&ctx->mub, B * lp));
+        CKS(dalloc(&ctx->lpb, B * lp));
+        if (B > 0) {
+            CKS(cudaMemcpy2DAsync(ctx->qb, ctx->ld * sizeof(double), prob->q + ctx->b0 * n, n * sizeof(double),
+                                  n * sizeof(double), B, cudaMemcpyDefault, s));
+            if (p > 0)
+                CKS(cudaMemcpy2DAsync(ctx->gb, ctx->ldp * sizeof(double), prob->g + ctx->b0 * p, p * sizeof(double),
+                                      p * sizeof(double), B, cudaMemcpyDefault, s));
+        }
+        CKS(configure_batched_kernels());
+    }
     if (prob->on_device) {
         CKS(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int32_t), s));
+        if (batched) {
+            CKS(launch_check(ctx->qb, ctx->Bloc, n, ctx->ld, ctx->d_flag, s));
+            if (p > 0) CKS(launch_check(ctx->gb, ctx->Bloc, p, ctx->ldp, ctx->d_flag, s));
+        }
         if (!csr) CKS(launch_check(ctx->A, rows, n, ctx->ld, ctx->d_flag, s));
         CKS(launch_check(ctx->q, 1, ctx->nloc, ctx->nloc, ctx->d_flag, s));
         if (ctx->ploc > 0) CKS(launch_check(ctx->g, 1, ctx->ploc, ctx->ploc, ctx->d_flag, s));
@@ -769,6 +860,7 @@ duquad_status duquad_lipschitz(duquad_ctx *ctx, int32_t iters, double safety, do
 
 duquad_status duquad_set_trace(duquad_ctx *ctx, double *lam_trace, double *u_trace, int64_t max_outer) {
     if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
+    if (ctx->Btot > 1 && (lam_trace || u_trace)) return fail(ctx, DUQUAD_EINVAL, "trace: single QP only");
     DevGuard guard(ctx->dev);
     if (ctx->own_stream) CK(cudaDeviceSynchronize());   // caller's buffers may be in flight
     ctx->trace_lam = lam_trace;
@@ -818,8 +910,12 @@ duquad_status duquad_solve(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t 
     }
     CK(cudaMemcpyAsync(ctx->d_ops, ops.data(), (K + 2) * sizeof(OuterParam), cudaMemcpyHostToDevice, s));
     // ---- initial state
-    CK(launch_init_state(ctx->x, ctx->y_full + ctx->rank * ctx->n_slice, ctx->xhat, ctx->lb, ctx->ub,
-                         ctx->nloc, ctx->mu, ctx->lam_prev, ctx->ploc, ctx->d_j, ctx->d_flag, s));
+    if (ctx->Btot > 1)
+        CK(launch_init_batched(ctx->Xb, ctx->Yb, ctx->XHb, ctx->lb, ctx->ub, ctx->n, ctx->ld, ctx->mub, ctx->lpb,
+                               std::max<int64_t>(ctx->ldp, 2), ctx->Bloc, ctx->d_j, ctx->d_flag, s));
+    else
+        CK(launch_init_state(ctx->x, ctx->y_full + ctx->rank * ctx->n_slice, ctx->xhat, ctx->lb, ctx->ub,
+                             ctx->nloc, ctx->mu, ctx->lam_prev, ctx->ploc, ctx->d_j, ctx->d_flag, s));
     duquad_status st;
     if ((st = allgather_y(ctx)) != DUQUAD_OK) return st;
     const bool tracing = ctx->trace_lam || ctx->trace_u;
@@ -873,7 +969,13 @@ duquad_status duquad_solve(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t 
         res->kernel_launches = 1 + (int64_t)(K + 1) * (2 * Kin + 1);
         res->matrix_passes = (int64_t)(K + 1) * Kin * 2;
         const double nn = (double)ctx->n, nl = (double)ctx->nloc, pl = (double)ctx->ploc, pp = (double)ctx->p;
-        if (ctx->format == DUQUAD_CSR) {   // values + indices + row pointers + vectors
+        if (ctx->Btot > 1) {   // shared matrices (L2-resident) + per-QP vectors
+            const double B = (double)ctx->Bloc;
+            res->flops_pass_a = 2.0 * (nn + pp) * nn * B;
+            res->flops_pass_b = 2.0 * nn * pp * B;
+            res->bytes_pass_a = 8.0 * ((nn + pp) * nn + B * (nn + nn + 3.0 * pp));
+            res->bytes_pass_b = 8.0 * (nn * pp + B * (pp + 8.0 * nn));
+        } else if (ctx->format == DUQUAD_CSR) {   // values + indices + row pointers + vectors
             res->bytes_pass_a = 12.0 * ctx->nnz_a + 4.0 * (nl + pl + 1) + 8.0 * (nn + nl + 3.0 * pl);
             res->bytes_pass_b = 12.0 * ctx->nnz_b + 4.0 * (nl + 1) + 8.0 * (pp + 8.0 * nl);
         } else {
@@ -903,10 +1005,14 @@ duquad_status duquad_solve(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t 
     return DUQUAD_OK;
 }
 
+static duquad_status get_result_batched(duquad_ctx *ctx, double *x_last, double *x_avg, double *lam,
+                                        int32_t on_device);
+
 duquad_status duquad_get_result(duquad_ctx *ctx, double *x_last, double *x_avg, double *lam, int32_t on_device) {
     if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
     if (!ctx->solved) return fail(ctx, DUQUAD_ESTATE, "no solve has run");
     DevGuard guard(ctx->dev);
+    if (ctx->Btot > 1) return get_result_batched(ctx, x_last, x_avg, lam, on_device);
     const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     if (x_last) CK(cudaMemcpyAsync(x_last, ctx->x, ctx->nloc * sizeof(double), kind, ctx->stream));
     if (x_avg) CK(cudaMemcpyAsync(x_avg, ctx->xhat, ctx->nloc * sizeof(double), kind, ctx->stream));
@@ -915,10 +1021,26 @@ duquad_status duquad_get_result(duquad_ctx *ctx, double *x_last, double *x_avg, 
     return DUQUAD_OK;
 }
 
+static duquad_status get_result_batched(duquad_ctx *ctx, double *x_last, double *x_avg, double *lam,
+                                        int32_t on_device) {
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    const int64_t n = ctx->n, p = ctx->p, B = ctx->Bloc, sp = std::max<int64_t>(ctx->ldp, 2);
+    if (B > 0) {
+        if (x_last)
+            CK(cudaMemcpy2DAsync(x_last, n * 8, ctx->Xb, ctx->ld * 8, n * 8, B, kind, ctx->stream));
+        if (x_avg)
+            CK(cudaMemcpy2DAsync(x_avg, n * 8, ctx->XHb, ctx->ld * 8, n * 8, B, kind, ctx->stream));
+        if (lam && p > 0) CK(cudaMemcpy2DAsync(lam, p * 8, ctx->lpb, sp * 8, p * 8, B, kind, ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    return DUQUAD_OK;
+}
+
 duquad_status duquad_residuals(duquad_ctx *ctx, int32_t which, double *F, double *dist, double *lag) {
     if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
     if (!ctx->solved) return fail(ctx, DUQUAD_ESTATE, "no solve has run");
     if (which != 0 && which != 1) return fail(ctx, DUQUAD_EINVAL, "which must be 0 (x_last) or 1 (x_avg)");
+    if (ctx->Btot > 1) return fail(ctx, DUQUAD_EINVAL, "residuals: single QP only");
     DevGuard guard(ctx->dev);
     cudaStream_t s = ctx->stream;
     duquad_status st;

@@ -86,6 +86,19 @@ struct PassBArgs {
     const double *va;
 };
 
+// ---------------------------------------------------------------- batched (B QPs, shared Q, G)
+// C[m][b] = sum_k Aop[m][k] Bop[b][k]; per-QP vectors are QP-major with strides sn / sp.
+struct BatchedArgs {
+    const double *Aop;
+    int64_t lda, M;      // valid rows
+    const double *Bop;
+    int64_t ldb, N;      // valid QPs
+    int64_t K;           // reduction length, padded to a multiple of 32 (zero padding)
+    int64_t sn, sp;
+    PassAArgs a;         // pass 0 epilogue (pointers at QP 0)
+    PassBArgs b;         // pass 1 epilogue
+};
+
 struct LaunchCfg {
     int grid;
     int threads;
@@ -108,6 +121,13 @@ cudaError_t csr_transpose_rows(const int32_t *rp, const int32_t *ci, const doubl
                                int64_t cols, int64_t nnz, int64_t c0, int64_t nc, int32_t **rp_t,
                                int32_t **ci_t, double **va_t, int64_t *nnz_t, cudaStream_t s);
 int csr_group_size(double avg_nnz_per_row);
+
+// kernels_batched.cu
+cudaError_t configure_batched_kernels();
+cudaError_t launch_batched(const BatchedArgs &a, int pass, int mode, cudaStream_t s);
+cudaError_t launch_init_batched(double *x, double *y, double *xhat, const double *lb, const double *ub, int64_t n,
+                                int64_t sn, double *mu, double *lam_prev, int64_t sp, int64_t B, int32_t *d_j,
+                                int32_t *flag, cudaStream_t s);
 
 // kernels_dense.cu
 cudaError_t launch_pass_a(const PassAArgs &a, int mode, const LaunchCfg &cfg, cudaStream_t s);

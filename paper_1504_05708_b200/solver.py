@@ -112,8 +112,13 @@ class Solver:
         if len(set(devs.values())) > 1:
             raise ValueError("problem arrays must be all on the host or all on the device")
         on_device = bool(devs and next(iter(devs.values())))
+        # batched mode (row a9): q is B x n and g is B x p (row b = QP b), Q and G shared
+        qshape = tuple(arrs["q"].obj.shape)
+        batch = int(qshape[0]) if len(qshape) == 2 else 1
+        if batch > 1 and tuple(arrs["g"].obj.shape) != (batch, p):
+            raise ValueError("batched g must be B x p")
         prob = L.Problem()
-        prob.n, prob.p, prob.batch = n, p, 1
+        prob.n, prob.p, prob.batch = n, p, batch
         prob.format = fmt
         prob.on_device = int(on_device)
         for k, a in arrs.items():
@@ -144,8 +149,14 @@ class Solver:
         self.n, self.p, self.rho = n, p, float(rho)
         self.format = fmt
         self.world_size, self.rank = o["world_size"], o["rank"]
-        self.n_range = shard_range(n, self.world_size, self.rank)
-        self.p_range = shard_range(p, self.world_size, self.rank)
+        self.batch = batch
+        if batch > 1:     # whole QPs are sharded, not rows
+            self.b_range = shard_range(batch, self.world_size, self.rank)
+            self.n_range, self.p_range = (0, n), (0, p)
+        else:
+            self.b_range = (0, 1)
+            self.n_range = shard_range(n, self.world_size, self.rank)
+            self.p_range = shard_range(p, self.world_size, self.rank)
         self.device = o["device"]
         self.last_result = None
 
@@ -173,24 +184,28 @@ class Solver:
         return self.last_result
 
     def result(self, device: bool = False):
-        """(x_last, x_avg, lambda) local slices; NumPy on the host or torch on the device."""
+        """(x_last, x_avg, lambda) local slices; NumPy on the host or torch on the device.
+        Batched: arrays of shape (B_local, n) / (B_local, p)."""
         nl = self.n_range[1] - self.n_range[0]
         pl = self.p_range[1] - self.p_range[0]
+        bl = self.b_range[1] - self.b_range[0]
+        shp_n = (bl, nl) if self.batch > 1 else (nl,)
+        shp_p = (bl, max(pl, 1)) if self.batch > 1 else (max(pl, 1),)
         if device:
             import torch
             dev = torch.device("cuda", torch.cuda.current_device() if self.device < 0 else self.device)
-            xl = torch.empty(nl, dtype=torch.float64, device=dev)
-            xa = torch.empty(nl, dtype=torch.float64, device=dev)
-            lam = torch.empty(max(pl, 1), dtype=torch.float64, device=dev)
+            xl = torch.empty(shp_n, dtype=torch.float64, device=dev)
+            xa = torch.empty(shp_n, dtype=torch.float64, device=dev)
+            lam = torch.empty(shp_p, dtype=torch.float64, device=dev)
             L.check(self._lib.duquad_get_result(self._ctx, xl.data_ptr(), xa.data_ptr(), lam.data_ptr(), 1),
                     self._ctx)
-            return xl, xa, lam[:pl]
-        xl = np.empty(nl)
-        xa = np.empty(nl)
-        lam = np.empty(max(pl, 1))
+            return xl, xa, lam[..., :pl]
+        xl = np.empty(shp_n)
+        xa = np.empty(shp_n)
+        lam = np.empty(shp_p)
         L.check(self._lib.duquad_get_result(self._ctx, xl.ctypes.data, xa.ctypes.data, lam.ctypes.data, 0),
                 self._ctx)
-        return xl, xa, lam[:pl]
+        return xl, xa, lam[..., :pl]
 
     def residuals(self, which: str = "last"):
         F, d, lag = C.c_double(), C.c_double(), C.c_double()

@@ -1,0 +1,115 @@
+"""Batched MPC path (BASELINE.json configs[3]) vs the oracle (-m gpu).
+
+The oracle runs the same DFOM on the n x B matrix of right-hand sides (each column one QP);
+the GPU runs DMMA GEMMs with the fused epilogues.  Bar: 1e-9 relative per BASELINE.json.
+"""
+import numpy as np
+import pytest
+
+import qpgen
+from oracle import dfom as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+def relerr(got, want):
+    got, want = np.asarray(got, float), np.asarray(want, float)
+    return float(np.max(np.abs(got - want)) / (1.0 + np.max(np.abs(want)))) if want.size else 0.0
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def _solve(prob, rho, alg, K, Kin, L_in, L_d, **kw):
+    from paper_1504_05708_b200 import Solver
+    s = Solver(prob.Q, prob.q.T.copy(), prob.G, prob.g.T.copy(), prob.lb, prob.ub, prob.cone, rho=rho, **kw)
+    s.set_constants(L_in, L_d)
+    info = s.solve(alg, K, Kin)
+    xl, xa, lam = s.result()
+    s.close()
+    return xl, xa, lam, info
+
+
+def _oracle(prob, rho, alg, K, Kin, L_in, L_d):
+    return O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho, alg, K, Kin, L_in, L_d)
+
+
+@pytest.mark.parametrize("alg", ["DGM", "DFGM"])
+@pytest.mark.parametrize("K,Kin", [(1, 1), (4, 6)])
+def test_small_mpc_parity(torch_cuda, alg, K, Kin):
+    prob = qpgen.mpc_batch(50, seed=2, N=4)          # n = 16, p = 96, B = 50 (ragged tiles)
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 1.0, 0.1)
+    xl, xa, lam, _ = _solve(prob, 1.0, alg, K, Kin, L_in, L_d)
+    r = _oracle(prob, 1.0, alg, K, Kin, L_in, L_d)
+    assert relerr(xl, r.x_last.T) <= TOL and relerr(xa, r.x_avg.T) <= TOL and relerr(lam, r.lam.T) <= TOL
+
+
+@pytest.mark.parametrize("B", [2, 37, 200])
+def test_ragged_batches_and_rho0(torch_cuda, B):
+    prob = qpgen.mpc_batch(B, seed=B, N=7)            # n = 28, p = 168
+    for rho in (0.0, 2.0):
+        L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, rho, 0.1)
+        xl, xa, lam, _ = _solve(prob, rho, "DFGM", 5, 5, L_in, L_d)
+        r = _oracle(prob, rho, O.DFGM, 5, 5, L_in, L_d)
+        assert relerr(xl, r.x_last.T) <= TOL and relerr(xa, r.x_avg.T) <= TOL and relerr(lam, r.lam.T) <= TOL
+
+
+def test_batched_equals_single_qp_solves(torch_cuda):
+    """Each column of the batched solve equals the single-QP (GEMV) path on that QP
+    (summation order differs only)."""
+    from paper_1504_05708_b200 import Solver
+    prob = qpgen.mpc_batch(6, seed=4, N=10)
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 1.0, 0.1)
+    xl, xa, lam, _ = _solve(prob, 1.0, "DFGM", 6, 8, L_in, L_d)
+    for b in range(6):
+        s = Solver(prob.Q, prob.q[:, b], prob.G, prob.g[:, b], prob.lb, prob.ub, prob.cone, rho=1.0)
+        s.set_constants(L_in, L_d)
+        s.solve("DFGM", 6, 8)
+        x1, a1, l1 = s.result()
+        assert relerr(xl[b], x1) <= 1e-12 and relerr(lam[b], l1) <= 1e-12
+
+
+def test_batch_sharding_is_exact(torch_cuda):
+    """Batch-sharded multi-GPU mode (whole QPs per rank, no collective): ranks 0..2 of a
+    3-way split solve disjoint QP slices whose concatenation is bitwise the 1-rank result."""
+    from paper_1504_05708_b200 import Solver
+    prob = qpgen.mpc_batch(70, seed=5, N=6)
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 1.0, 0.1)
+    full = _solve(prob, 1.0, "DFGM", 5, 4, L_in, L_d)
+    parts = []
+    for rank in range(3):
+        s = Solver(prob.Q, prob.q.T.copy(), prob.G, prob.g.T.copy(), prob.lb, prob.ub, prob.cone, rho=1.0,
+                   world_size=3, rank=rank)
+        s.set_constants(L_in, L_d)
+        s.solve("DFGM", 5, 4)
+        parts.append(s.result())
+        s.close()
+    for k in range(3):
+        assert np.array_equal(np.concatenate([pt[k] for pt in parts]), full[k])
+
+
+def test_lipschitz_on_batched_context(torch_cuda):
+    from paper_1504_05708_b200 import Solver
+    prob = qpgen.mpc_batch(16, seed=0)
+    s = Solver(prob.Q, prob.q.T.copy(), prob.G, prob.g.T.copy(), prob.lb, prob.ub, prob.cone, rho=1.0,
+               lambda_min_lb=0.1)
+    L_in, L_d, nG2 = s.lipschitz(iters=120)
+    rL, rd, rn = O.lipschitz_constants(prob.Q, prob.G, 1.0, 0.1)
+    assert abs(L_in - rL) <= 1e-9 * rL and abs(nG2 - rn) <= 1e-9 * rn and abs(L_d - rd) <= 1e-9 * rd
+
+
+def test_config3_full_size_configured_counts(torch_cuda):
+    """BASELINE.json configs[3] at full size: B = 8192 MPC QPs (n = 120, p = 720), DFGM rho = 1,
+    50 x 20 (+20 last-iterate steps), in the bench launch configuration."""
+    prob = qpgen.mpc_batch(8192, seed=0)
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 1.0, 0.1)
+    xl, xa, lam, info = _solve(prob, 1.0, "DFGM", 50, 20, L_in, L_d)
+    r = _oracle(prob, 1.0, O.DFGM, 50, 20, L_in, L_d)
+    assert relerr(xl, r.x_last.T) <= TOL and relerr(xa, r.x_avg.T) <= TOL and relerr(lam, r.lam.T) <= TOL
+    assert info["flops_pass_a"] + info["flops_pass_b"] == pytest.approx(3.0672e9, rel=1e-3)
