@@ -125,6 +125,9 @@ typedef struct {
     void *stream;
     int32_t device;
     int32_t time_passes;   /* 1: time a sample of pass A / pass B launches with CUDA events */
+    int32_t small_path;    /* 1 (default): run the whole solve in ONE single-CTA kernel when
+                              [Q;G], G' and the vectors fit in shared memory (single GPU,
+                              dense, batch 1); 0: always use the streaming pass kernels    */
 } duquad_options;
 
 /* Per-solve report. */

@@ -57,6 +57,11 @@ struct duquad_ctx {
     int64_t Btot = 1, Bloc = 1, b0 = 0;
     double *Yb = nullptr, *Xb = nullptr, *XHb = nullptr, *QYb = nullptr, *qb = nullptr;
     double *Wb = nullptr, *gb = nullptr, *mub = nullptr, *lpb = nullptr;
+    // whole-solve single-CTA kernel (small dense QPs)
+    bool small = false;
+    size_t small_smem = 0;
+    double *d_beta = nullptr;
+    int64_t beta_cap = 0;
     double *scal = nullptr;       // device scalars
     double *partials = nullptr;   // kRedGrid * 5
     OuterParam *d_ops = nullptr;
@@ -114,7 +119,7 @@ void free_all(duquad_ctx *c) {
     double *ds[] = {c->A,   c->GT,  c->y_full, c->w_full, c->qy,       c->x,        c->xhat,     c->q,
                     c->lb,  c->ub,  c->g,      c->mu,     c->lam_prev, c->lz_vprev, c->lz_w,     c->scal,
                     c->partials, c->Yb, c->Xb, c->XHb,   c->QYb,      c->qb,       c->Wb,       c->gb,
-                    c->mub, c->lpb};
+                    c->mub, c->lpb, c->d_beta};
     for (double *d : ds)
         if (d) cudaFree(d);
     if (c->cone) cudaFree(c->cone);
@@ -532,6 +537,7 @@ void duquad_default_options(duquad_options *o) {
     o->stream = nullptr;
     o->device = -1;
     o->time_passes = 0;
+    o->small_path = 1;
 }
 
 duquad_status duquad_shard_range(int64_t rows, int32_t world, int32_t rank, int64_t *begin,
@@ -811,6 +817,13 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
                   pass_threads(), smem_a};
     ctx->cfg_b = {(int)std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms, (ctx->nloc + wpc - 1) / wpc)),
                   pass_threads(), smem_b};
+    if (!batched && ctx->world == 1 && opt.small_path) {
+        ctx->small_smem = small_smem_bytes(n, p, ctx->ld, ctx->ldp);
+        if (ctx->small_smem <= (size_t)prop.sharedMemPerBlockOptin) {
+            CKS(configure_small_kernel(ctx->small_smem));
+            ctx->small = true;
+        }
+    }
     CKS(cudaStreamSynchronize(s));
     *out = ctx;
     return DUQUAD_OK;
@@ -918,6 +931,66 @@ duquad_status duquad_solve(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t 
                              ctx->nloc, ctx->mu, ctx->lam_prev, ctx->ploc, ctx->d_j, ctx->d_flag, s));
     duquad_status st;
     if ((st = allgather_y(ctx)) != DUQUAD_OK) return st;
+    if (ctx->small) {   // whole solve in one single-CTA kernel (K4)
+        if (ctx->beta_cap < Kin + 1) {
+            if (ctx->d_beta) cudaFree(ctx->d_beta);
+            ctx->d_beta = nullptr;
+            CK(cudaMalloc(&ctx->d_beta, (Kin + 1) * sizeof(double)));
+            ctx->beta_cap = Kin + 1;
+        }
+        CK(cudaMemcpyAsync(ctx->d_beta, beta_in.data(), (Kin + 1) * sizeof(double), cudaMemcpyHostToDevice, s));
+        SmallArgs sa{};
+        sa.A = ctx->A;
+        sa.GT = ctx->GT;
+        sa.n = ctx->n;
+        sa.p = ctx->p;
+        sa.ld = ctx->ld;
+        sa.ldp = ctx->ldp;
+        sa.q = ctx->q;
+        sa.lb = ctx->lb;
+        sa.ub = ctx->ub;
+        sa.g = ctx->g;
+        sa.cone = ctx->cone;
+        sa.K = K;
+        sa.Kin = Kin;
+        sa.beta_in = ctx->d_beta;
+        sa.a = make_a(ctx);
+        sa.b = make_b(ctx);
+        sa.trace_lam = ctx->trace_lam;
+        sa.trace_u = ctx->trace_u;
+        sa.trace_max = ctx->trace_max;
+        sa.x_out = ctx->x;
+        sa.xhat_out = ctx->xhat;
+        sa.y_out = ctx->y_full;
+        sa.lam_out = ctx->lam_prev;
+        sa.mu_out = ctx->mu;
+        cudaEvent_t t0, t1;
+        CK(cudaEventCreate(&t0));
+        CK(cudaEventCreate(&t1));
+        CK(cudaEventRecord(t0, s));
+        CK(launch_small_solve(sa, ctx->small_smem, s));
+        CK(cudaEventRecord(t1, s));
+        CK(cudaStreamSynchronize(s));
+        int32_t flag = 0;
+        CK(cudaMemcpy(&flag, ctx->d_flag, sizeof(flag), cudaMemcpyDeviceToHost));
+        if (res) {
+            std::memset(res, 0, sizeof(*res));
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, t0, t1);
+            res->ms_device = ms;
+            res->outer_iters = K;
+            res->inner_iters_total = (int64_t)(K + 1) * Kin;
+            res->kernel_launches = 2;
+            res->matrix_passes = (int64_t)(K + 1) * Kin * 2;
+            res->bytes_pass_a = 8.0 * ((double)(ctx->n + ctx->p) * ctx->n);   // from shared memory
+            res->bytes_pass_b = 8.0 * ((double)ctx->n * ctx->p);
+        }
+        cudaEventDestroy(t0);
+        cudaEventDestroy(t1);
+        ctx->solved = true;
+        if (flag) return fail(ctx, DUQUAD_ENONFINITE, "an iterate became non-finite");
+        return DUQUAD_OK;
+    }
     const bool tracing = ctx->trace_lam || ctx->trace_u;
     const bool graphs = ctx->opt.use_graphs && !tracing;
     const int j_timed = ctx->opt.time_passes ? std::max(1, (K + 1) / 2) : -1;

@@ -99,6 +99,21 @@ struct BatchedArgs {
     PassBArgs b;         // pass 1 epilogue
 };
 
+// ---------------------------------------------------------------- whole-solve small kernel (K4)
+struct SmallArgs {
+    const double *A, *GT;          // packed [Q;G] (n+p x ld) and G' (n x ldp) in HBM
+    int64_t n, p, ld, ldp;
+    const double *q, *lb, *ub, *g;
+    const uint8_t *cone;
+    int32_t K, Kin;
+    const double *beta_in;         // device, Kin + 1 entries (1-based)
+    PassAArgs a;                   // scalars (rho, step, project_dual, ops, nq)
+    PassBArgs b;                   // scalars (L_in, ops, flag)
+    double *trace_lam, *trace_u;
+    int64_t trace_max;
+    double *x_out, *xhat_out, *y_out, *lam_out, *mu_out;
+};
+
 struct LaunchCfg {
     int grid;
     int threads;
@@ -121,6 +136,11 @@ cudaError_t csr_transpose_rows(const int32_t *rp, const int32_t *ci, const doubl
                                int64_t cols, int64_t nnz, int64_t c0, int64_t nc, int32_t **rp_t,
                                int32_t **ci_t, double **va_t, int64_t *nnz_t, cudaStream_t s);
 int csr_group_size(double avg_nnz_per_row);
+
+// kernels_small.cu
+size_t small_smem_bytes(int64_t n, int64_t p, int64_t ld, int64_t ldp);
+cudaError_t configure_small_kernel(size_t smem);
+cudaError_t launch_small_solve(const SmallArgs &sa, size_t smem, cudaStream_t s);
 
 // kernels_batched.cu
 cudaError_t configure_batched_kernels();

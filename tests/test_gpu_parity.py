@@ -273,3 +273,19 @@ def test_config2_full_size_prefix(torch_cuda):
     r = O.dfom(h["Q"], h["q"], h["G"], h["g"], h["lb"], h["ub"], h["cone"], 1.0, O.DFGM, 2, 2, L_in, L_d)
     assert relerr(xl, r.x_last) <= TOL and relerr(xa, r.x_avg) <= TOL and relerr(lam, r.lam) <= TOL
     s.close()
+
+
+@pytest.mark.parametrize("n,p,kind", [(50, 25, "ineq"), (37, 13, "mixed"), (33, 0, "ineq"), (90, 45, "eq")])
+def test_small_whole_solve_kernel_is_bitwise_the_stream_path(torch_cuda, n, p, kind):
+    """K4 (one CTA runs the whole solve from shared memory) vs the two-kernel streaming path:
+    same row summation order and the same epilogues, so bit-identical results and traces."""
+    prob = qpgen.tiny(n, p, seed=n, kind=kind)
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 1.0, 0.05)
+    L_d = L_d if p else 1.0
+    a = run_gpu(torch_cuda, prob, 1.0, "DFGM", 9, 7, L_in, L_d, trace=p > 0, small_path=True)
+    b = run_gpu(torch_cuda, prob, 1.0, "DFGM", 9, 7, L_in, L_d, trace=p > 0, small_path=False)
+    assert a["info"]["kernel_launches"] == 2 and b["info"]["kernel_launches"] > 2
+    for k in ("x_last", "x_avg", "lam") + (("trace_lam", "trace_u") if p else ()):
+        assert np.array_equal(a[k], b[k]), k
+    r = run_oracle(prob, 1.0, O.DFGM, 9, 7, L_in, L_d)
+    assert_parity(a, r)
