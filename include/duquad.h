@@ -128,6 +128,9 @@ typedef struct {
     int32_t small_path;    /* 1 (default): run the whole solve in ONE single-CTA kernel when
                               [Q;G], G' and the vectors fit in shared memory (single GPU,
                               dense, batch 1); 0: always use the streaming pass kernels    */
+    int32_t rho0_path;     /* 1 (default): with rho == 0 (dense, batch 1) stream only Q per inner
+                              step, c = q + G'mu formed once per outer iteration;
+                              0: the generic two-pass inner step                           */
 } duquad_options;
 
 /* Per-solve report. */

@@ -51,7 +51,7 @@ class Options(C.Structure):
         ("sigma", C.c_double), ("lambda_min_lb", C.c_double), ("l_mode", C.c_int32),
         ("use_graphs", C.c_int32), ("world_size", C.c_int32), ("rank", C.c_int32),
         ("nccl_id", C.c_void_p), ("stream", C.c_void_p), ("device", C.c_int32),
-        ("time_passes", C.c_int32), ("small_path", C.c_int32),
+        ("time_passes", C.c_int32), ("small_path", C.c_int32), ("rho0_path", C.c_int32),
     ]
 
 

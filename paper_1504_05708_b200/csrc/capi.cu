@@ -57,6 +57,10 @@ struct duquad_ctx {
     int64_t Btot = 1, Bloc = 1, b0 = 0;
     double *Yb = nullptr, *Xb = nullptr, *XHb = nullptr, *QYb = nullptr, *qb = nullptr;
     double *Wb = nullptr, *gb = nullptr, *mub = nullptr, *lpb = nullptr;
+    // rho = 0 specialisation (K3): second y replica (ping-pong) and c = q + G'mu
+    bool rho0 = false;
+    double *y_full2 = nullptr, *cvec = nullptr;
+    LaunchCfg cfg_k3{};
     // whole-solve single-CTA kernel (small dense QPs)
     bool small = false;
     size_t small_smem = 0;
@@ -119,7 +123,7 @@ void free_all(duquad_ctx *c) {
     double *ds[] = {c->A,   c->GT,  c->y_full, c->w_full, c->qy,       c->x,        c->xhat,     c->q,
                     c->lb,  c->ub,  c->g,      c->mu,     c->lam_prev, c->lz_vprev, c->lz_w,     c->scal,
                     c->partials, c->Yb, c->Xb, c->XHb,   c->QYb,      c->qb,       c->Wb,       c->gb,
-                    c->mub, c->lpb, c->d_beta};
+                    c->mub, c->lpb, c->d_beta, c->y_full2, c->cvec};
     for (double *d : ds)
         if (d) cudaFree(d);
     if (c->cone) cudaFree(c->cone);
@@ -153,12 +157,14 @@ struct DevGuard {
 };
 
 // ----------------------------------------------------------- collectives
-duquad_status allgather_y(duquad_ctx *ctx) {
+duquad_status allgather_vec(duquad_ctx *ctx, double *full) {
     if (ctx->world == 1) return DUQUAD_OK;
-    NK(ncclAllGather(ctx->y_full + ctx->rank * ctx->n_slice, ctx->y_full, (size_t)ctx->n_slice,
-                     ncclDouble, ctx->comm, ctx->stream));
+    NK(ncclAllGather(full + ctx->rank * ctx->n_slice, full, (size_t)ctx->n_slice, ncclDouble, ctx->comm,
+                     ctx->stream));
     return DUQUAD_OK;
 }
+
+duquad_status allgather_y(duquad_ctx *ctx) { return allgather_vec(ctx, ctx->y_full); }
 
 duquad_status allgather_w(duquad_ctx *ctx) {
     if (ctx->world == 1) return DUQUAD_OK;
@@ -230,9 +236,61 @@ PassBArgs make_b(duquad_ctx *c) {
 
 BatchedArgs make_batched(duquad_ctx *c, int pass);
 
+// One outer DFOM iteration at rho = 0 with the K3 inner step (row a1'):
+//   1. pass A over the G rows only at y = u_bar^{j-1}: fused DFOM step, w = mu^j
+//   2. c = q + G'w (one pass over G'), and y^1 = u_bar^{j-1} into replica A
+//   3. K_in x K3 (stream Q only), y ping-ponging between replicas A and B.
+duquad_status run_outer_rho0(duquad_ctx *ctx, const std::vector<double> &beta_in, int Kin, int j,
+                             std::vector<cudaEvent_t> *ev) {
+    duquad_status st;
+    double *Y[2] = {ctx->y_full, ctx->y_full2};
+    const int64_t off = ctx->rank * ctx->n_slice;
+    PassAArgs a = make_a(ctx);
+    a.row_begin = ctx->nloc;          // G rows only
+    a.first_inner = 1;
+    a.y = Y[Kin % 2];                 // the replica the previous inner solve finished in
+    CK(launch_pass_a(a, MODE_SOLVE, ctx->cfg_a, ctx->stream));
+    if ((st = allgather_w(ctx)) != DUQUAD_OK) return st;
+    if (j >= 2 && ctx->trace_lam && j - 2 < ctx->trace_max)
+        CK(cudaMemcpyAsync(ctx->trace_lam + (j - 2) * ctx->ploc, ctx->lam_prev, ctx->ploc * sizeof(double),
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+    PassBArgs c = make_b(ctx);
+    c.qy = ctx->q;                    // c = q + G'w
+    c.use_qy = 1;
+    c.out = ctx->cvec;
+    CK(launch_pass_b(c, MODE_LIN, ctx->cfg_b, ctx->stream));
+    CK(cudaMemcpyAsync(Y[0] + off, ctx->x, ctx->nloc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    if ((st = allgather_vec(ctx, Y[0])) != DUQUAD_OK) return st;
+    for (int k = 1; k <= Kin; ++k) {
+        PassAArgs a3 = make_a(ctx);
+        a3.y = Y[(k - 1) % 2];
+        PassBArgs bl = make_b(ctx);
+        bl.q = ctx->cvec;
+        bl.y = Y[(k - 1) % 2] + off;
+        bl.beta_in = beta_in[k];
+        bl.last_inner = (k == Kin);
+        PassBArgs bs = bl;
+        bs.y = Y[k % 2] + off;
+        if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 0], ctx->stream));
+        CK(launch_rho0_step(a3, bl, bs, ctx->cfg_k3, ctx->stream));
+        if (ev) {
+            CK(cudaEventRecord((*ev)[4 * (k - 1) + 1], ctx->stream));
+            CK(cudaEventRecord((*ev)[4 * (k - 1) + 2], ctx->stream));
+            CK(cudaEventRecord((*ev)[4 * (k - 1) + 3], ctx->stream));
+        }
+        if ((st = allgather_vec(ctx, Y[k % 2])) != DUQUAD_OK) return st;
+    }
+    if (j >= 1 && ctx->trace_u && j - 1 < ctx->trace_max)
+        CK(cudaMemcpyAsync(ctx->trace_u + (j - 1) * ctx->nloc, ctx->x, ctx->nloc * sizeof(double),
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(launch_advance(ctx->d_j, ctx->stream));
+    return DUQUAD_OK;
+}
+
 // One outer DFOM iteration (reads its per-outer scalars through d_j).
 duquad_status run_outer(duquad_ctx *ctx, const std::vector<double> &beta_in, int Kin, int j,
                         std::vector<cudaEvent_t> *ev) {
+    if (ctx->rho0) return run_outer_rho0(ctx, beta_in, Kin, j, ev);
     PassAArgs a = make_a(ctx);
     PassBArgs b = make_b(ctx);
     const bool bt = ctx->Btot > 1;
@@ -538,6 +596,7 @@ void duquad_default_options(duquad_options *o) {
     o->device = -1;
     o->time_passes = 0;
     o->small_path = 1;
+    o->rho0_path = 1;
 }
 
 duquad_status duquad_shard_range(int64_t rows, int32_t world, int32_t rank, int64_t *begin,
@@ -817,6 +876,12 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
                   pass_threads(), smem_a};
     ctx->cfg_b = {(int)std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms, (ctx->nloc + wpc - 1) / wpc)),
                   pass_threads(), smem_b};
+    if (!batched && rho == 0.0 && opt.rho0_path) {   // K3: Q-only inner steps
+        CKS(dalloc(&ctx->y_full2, ctx->ylen));
+        CKS(dalloc(&ctx->cvec, ctx->nloc));
+        ctx->cfg_k3 = {ctx->cfg_b.grid, pass_threads(), smem_a};
+        ctx->rho0 = true;
+    }
     if (!batched && ctx->world == 1 && opt.small_path) {
         ctx->small_smem = small_smem_bytes(n, p, ctx->ld, ctx->ldp);
         if (ctx->small_smem <= (size_t)prop.sharedMemPerBlockOptin) {
@@ -1042,7 +1107,12 @@ duquad_status duquad_solve(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t 
         res->kernel_launches = 1 + (int64_t)(K + 1) * (2 * Kin + 1);
         res->matrix_passes = (int64_t)(K + 1) * Kin * 2;
         const double nn = (double)ctx->n, nl = (double)ctx->nloc, pl = (double)ctx->ploc, pp = (double)ctx->p;
-        if (ctx->Btot > 1) {   // shared matrices (L2-resident) + per-QP vectors
+        if (ctx->rho0) {       // K3 inner steps: Q only; per outer: one G pass and one G' pass
+            res->kernel_launches = 1 + (int64_t)(K + 1) * (Kin + 3);
+            res->matrix_passes = (int64_t)(K + 1) * (Kin + 2);
+            res->bytes_pass_a = 8.0 * (nl * nn + nn + 8.0 * nl);   // "pass A" slot = the K3 step
+            res->bytes_pass_b = 0.0;
+        } else if (ctx->Btot > 1) {   // shared matrices (L2-resident) + per-QP vectors
             const double B = (double)ctx->Bloc;
             res->flops_pass_a = 2.0 * (nn + pp) * nn * B;
             res->flops_pass_b = 2.0 * nn * pp * B;

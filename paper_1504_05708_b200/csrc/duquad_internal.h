@@ -153,6 +153,10 @@ cudaError_t launch_init_batched(double *x, double *y, double *xhat, const double
 cudaError_t launch_pass_a(const PassAArgs &a, int mode, const LaunchCfg &cfg, cudaStream_t s);
 cudaError_t launch_pass_b(const PassBArgs &b, int mode, const LaunchCfg &cfg, cudaStream_t s);
 int pass_threads();
+// K3 (rho = 0): grad = Qy + c streamed over Q rows only; bl / bs: epilogue views for load (y = yin,
+// q = c) and store (y = yout)
+cudaError_t launch_rho0_step(const PassAArgs &a, const PassBArgs &bl, const PassBArgs &bs, const LaunchCfg &cfg,
+                             cudaStream_t s);
 cudaError_t configure_pass_kernels(size_t smem_a, size_t smem_b);
 cudaError_t launch_init_state(double *x, double *y, double *xhat, const double *lb, const double *ub,
                               int64_t n, double *mu, double *lam_prev, int64_t p, int32_t *d_j,

@@ -116,6 +116,34 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass_b(const PassBArgs b) {
     }
 }
 
+// K3, the rho = 0 inner step (SURVEY §8(a) row a1'): with rho = 0 the multiplier term of the
+// gradient is G'mu, constant over an inner solve ("only G'mu is computed at each
+// outer iteration"), so c = q + G'mu is formed once per outer iteration and each inner step
+// streams Q only: grad = Qy + c, x+ = [y - grad/L]_U, y+ = x+ + beta (x+ - x).
+// y is read (staged) from yin and written to yout (ping-pong: every CTA stages all of y).
+__global__ void __launch_bounds__(kThreads, 1) k_rho0_step(const PassAArgs a, const PassBArgs bl,
+                                                          const PassBArgs bs) {
+    extern __shared__ __align__(16) double smem[];
+    stage(smem, a.y, a.ld);
+    __syncthreads();
+    const double2 *sv = reinterpret_cast<const double2 *>(smem);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int nw = kThreads / 32;
+    const int64_t r0 = a.nq * blockIdx.x / gridDim.x;
+    const int64_t r1 = a.nq * (blockIdx.x + 1) / gridDim.x;
+    const int nv2 = (int)(a.ld >> 1);
+    const double avg_w = avg_weight(bl, MODE_SOLVE);
+    for (int64_t j = r0 + warp; j < r1; j += nw) {
+        EpiB e{};
+        if (lane == 0) e = epi_b_load(bl, MODE_SOLVE, j, avg_w);     // bl.q = c, bl.y = yin slice
+        const double s = row_dot(reinterpret_cast<const double2 *>(a.A + j * a.ld), sv, nv2, lane);
+        if (lane == 0) {
+            e.qy = s;                                                  // grad = (Qy + c) + 0
+            epi_b_store(bs, MODE_SOLVE, j, 0.0, e, avg_w);             // bs.y = yout slice
+        }
+    }
+}
+
 __global__ void k_init_state(double *x, double *y, double *xhat, const double *lb, const double *ub,
                              int64_t n, double *mu, double *lam_prev, int64_t p, int32_t *d_j,
                              int32_t *flag) {
@@ -296,6 +324,7 @@ cudaError_t configure_pass_kernels(size_t smem_a, size_t smem_b) {
         return e;
     if ((e = cudaFuncSetAttribute(k_pass_b<MODE_SOLVE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_b)))
         return e;
+    if ((e = cudaFuncSetAttribute(k_rho0_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_a))) return e;
     return cudaFuncSetAttribute(k_pass_b<MODE_LIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_b);
 }
 
@@ -316,6 +345,13 @@ cudaError_t launch_pass_b(const PassBArgs &b, int mode, const LaunchCfg &cfg, cu
         k_pass_b<MODE_SOLVE><<<cfg.grid, kThreads, cfg.smem, s>>>(b);
     else
         k_pass_b<MODE_LIN><<<cfg.grid, kThreads, cfg.smem, s>>>(b);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rho0_step(const PassAArgs &a, const PassBArgs &bl, const PassBArgs &bs, const LaunchCfg &cfg,
+                             cudaStream_t s) {
+    if (a.nq <= 0) return cudaSuccess;
+    k_rho0_step<<<cfg.grid, kThreads, cfg.smem, s>>>(a, bl, bs);
     return cudaGetLastError();
 }
 

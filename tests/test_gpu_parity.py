@@ -289,3 +289,17 @@ def test_small_whole_solve_kernel_is_bitwise_the_stream_path(torch_cuda, n, p, k
         assert np.array_equal(a[k], b[k]), k
     r = run_oracle(prob, 1.0, O.DFGM, 9, 7, L_in, L_d)
     assert_parity(a, r)
+
+
+@pytest.mark.parametrize("alg", ["DGM", "DFGM"])
+@pytest.mark.parametrize("K,Kin", [(1, 1), (3, 4), (6, 5)])
+def test_rho0_q_only_inner_step(torch_cuda, c1, c1_consts, alg, K, Kin):
+    """Row a1' (rho = 0): K3 streams Q only per inner step, c = q + G'mu per outer iteration
+    (P:1268-1270); parity with the oracle incl. per-outer traces, odd and even K_in (ping-pong)."""
+    L_in, L_d, _ = c1_consts[0.0]
+    g = run_gpu(torch_cuda, c1, 0.0, alg, K, Kin, L_in, L_d, trace=True)
+    assert g["info"]["kernel_launches"] == 1 + (K + 1) * (Kin + 3)
+    r = run_oracle(c1, 0.0, alg, K, Kin, L_in, L_d, keep_trace=True)
+    assert_parity(g, r, trace=True)
+    h = run_gpu(torch_cuda, c1, 0.0, alg, K, Kin, L_in, L_d, rho0_path=False)
+    assert relerr(g["x_last"], h["x_last"]) <= 1e-13 and relerr(g["lam"], h["lam"]) <= 1e-13
