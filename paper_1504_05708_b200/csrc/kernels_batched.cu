@@ -102,50 +102,83 @@ __global__ void __launch_bounds__(NW * 32) k_batched(const BatchedArgs args) {
         __syncthreads();
     }
 
-    // epilogue: C fragment element (row fr, cols 2*fk, 2*fk+1) of each 8x8 tile
+    // epilogue, stage 1: the C tile goes to shared memory QP-major, Cs[col][row]
+    // (fragment element: row fr, cols 2*fk, 2*fk+1 of each 8x8 tile); the operand buffers are free.
+    constexpr int LDC = BM + 1;
+    double *Cs = smem;
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) Cs[(warp * WN + j * 8 + 2 * fk + h) * LDC + i * 8 + fr] = acc[i][j][h];
+    __syncthreads();
+    // stage 2: a warp owns QP columns, lanes own rows, so the per-QP vectors (QP-major) are
+    // accessed coalesced; the operands of 2 columns x RPL rows are loaded before any store.
+    constexpr int RPL = (BM + 31) / 32;
     if (PASS == 0) {
         const OuterA o = outer_a(args.a, MODE);
+        for (int cb = warp; cb < BN; cb += 2 * NW) {
+            PassAArgs v[2];
+            bool vb[2];
+            EpiA e[2][RPL];
 #pragma unroll
-        for (int i = 0; i < MT; ++i) {
-            const int64_t row = m0 + i * 8 + fr;
-            if (row >= args.M) continue;
+            for (int c = 0; c < 2; ++c) {
+                const int col = cb + c * NW;
+                const int64_t b = n0 + col;
+                vb[c] = col < BN && b < args.N;
+                v[c] = args.a;                   // per-QP view
+                v[c].qy += b * args.sn;
+                v[c].w += b * args.sp;
+                v[c].g += b * args.sp;
+                v[c].mu += b * args.sp;
+                v[c].lam_prev += b * args.sp;
 #pragma unroll
-            for (int j = 0; j < NT; ++j)
+                for (int t = 0; t < RPL; ++t) {
+                    const int r = lane + 32 * t;
+                    if (vb[c] && r < BM && m0 + r < args.M) e[c][t] = epi_a_load(v[c], MODE, m0 + r, o);
+                }
+            }
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int64_t b = n0 + warp * WN + j * 8 + 2 * fk + h;
-                    if (b >= args.N) continue;
-                    PassAArgs v = args.a;                   // per-QP view
-                    v.qy += b * args.sn;
-                    v.w += b * args.sp;
-                    v.g += b * args.sp;
-                    v.mu += b * args.sp;
-                    v.lam_prev += b * args.sp;
-                    const EpiA e = epi_a_load(v, MODE, row, o);
-                    epi_a_store(v, MODE, row, acc[i][j][h], e, o);
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+                for (int t = 0; t < RPL; ++t) {
+                    const int r = lane + 32 * t;
+                    if (vb[c] && r < BM && m0 + r < args.M)
+                        epi_a_store(v[c], MODE, m0 + r, Cs[(cb + c * NW) * LDC + r], e[c][t], o);
                 }
         }
     } else {
         const double avg_w = avg_weight(args.b, MODE);
+        for (int cb = warp; cb < BN; cb += 2 * NW) {
+            PassBArgs v[2];
+            bool vb[2];
+            EpiB e[2][RPL];
 #pragma unroll
-        for (int i = 0; i < MT; ++i) {
-            const int64_t row = m0 + i * 8 + fr;
-            if (row >= args.M) continue;
+            for (int c = 0; c < 2; ++c) {
+                const int col = cb + c * NW;
+                const int64_t b = n0 + col;
+                vb[c] = col < BN && b < args.N;
+                v[c] = args.b;
+                v[c].qy += b * args.sn;
+                v[c].q += b * args.sn;
+                v[c].x += b * args.sn;
+                v[c].y += b * args.sn;
+                v[c].xhat += b * args.sn;
+                if (MODE == MODE_LIN) v[c].out += b * args.sn;
 #pragma unroll
-            for (int j = 0; j < NT; ++j)
+                for (int t = 0; t < RPL; ++t) {
+                    const int r = lane + 32 * t;
+                    if (vb[c] && r < BM && m0 + r < args.M) e[c][t] = epi_b_load(v[c], MODE, m0 + r, avg_w);
+                }
+            }
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int64_t b = n0 + warp * WN + j * 8 + 2 * fk + h;
-                    if (b >= args.N) continue;
-                    PassBArgs v = args.b;
-                    v.qy += b * args.sn;
-                    v.q += b * args.sn;
-                    v.x += b * args.sn;
-                    v.y += b * args.sn;
-                    v.xhat += b * args.sn;
-                    if (MODE == MODE_LIN) v.out += b * args.sn;
-                    const EpiB e = epi_b_load(v, MODE, row, avg_w);
-                    epi_b_store(v, MODE, row, acc[i][j][h], e, avg_w);
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+                for (int t = 0; t < RPL; ++t) {
+                    const int r = lane + 32 * t;
+                    if (vb[c] && r < BM && m0 + r < args.M)
+                        epi_b_store(v[c], MODE, m0 + r, Cs[(cb + c * NW) * LDC + r], e[c][t], avg_w);
                 }
         }
     }

@@ -46,44 +46,103 @@ __device__ __forceinline__ int32_t ld_stream_i32(const int32_t *p, uint64_t pol)
 template <int GS>
 __device__ __forceinline__ double csr_row_dot(const int32_t *__restrict__ ci, const double *__restrict__ va,
                                               const double *__restrict__ v, int32_t lo, int32_t hi, int gl) {
+    // 4 nonzeros per lane per round: all index/value loads issued, then all gathers, then the
+    // FMAs in nonzero order (same per-lane summation order as a plain loop)
+    constexpr int U = 4;
     const uint64_t pol = evict_first_policy();
     double s = 0.0;
-    for (int32_t e = lo + gl; e < hi; e += GS)
-        s = fma(ld_stream_f64(va + e, pol), __ldg(v + ld_stream_i32(ci + e, pol)), s);
+    for (int32_t e0 = lo + gl; e0 < hi; e0 += U * GS) {
+        int32_t c[U];
+        double a[U], x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int32_t e = e0 + u * GS;
+            const bool ok = e < hi;
+            c[u] = ok ? ld_stream_i32(ci + e, pol) : -1;
+            a[u] = ok ? ld_stream_f64(va + e, pol) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u] = c[u] >= 0 ? __ldg(v + c[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (c[u] >= 0) s = fma(a[u], x[u], s);
+    }
     return s;
+}
+
+// Two rows per lane group per round, their loads interleaved (latency of the row-pointer ->
+// index -> gather chain is the limiter of a memory-bound SpMV, not bandwidth).  Each row keeps
+// the summation order of csr_row_dot.
+template <int GS>
+__device__ __forceinline__ void csr_row_dot2(const int32_t *__restrict__ ci, const double *__restrict__ va,
+                                             const double *__restrict__ v, int32_t lo0, int32_t hi0, int32_t lo1,
+                                             int32_t hi1, int gl, double &s0, double &s1) {
+    constexpr int U = 4;
+    const uint64_t pol = evict_first_policy();
+    s0 = 0.0;
+    s1 = 0.0;
+    for (int32_t e0 = lo0 + gl, e1 = lo1 + gl; e0 < hi0 || e1 < hi1; e0 += U * GS, e1 += U * GS) {
+        int32_t c0[U], c1[U];
+        double a0[U], a1[U], x0[U], x1[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int32_t f0 = e0 + u * GS, f1 = e1 + u * GS;
+            c0[u] = f0 < hi0 ? ld_stream_i32(ci + f0, pol) : -1;
+            c1[u] = f1 < hi1 ? ld_stream_i32(ci + f1, pol) : -1;
+            a0[u] = f0 < hi0 ? ld_stream_f64(va + f0, pol) : 0.0;
+            a1[u] = f1 < hi1 ? ld_stream_f64(va + f1, pol) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            x0[u] = c0[u] >= 0 ? __ldg(v + c0[u]) : 0.0;
+            x1[u] = c1[u] >= 0 ? __ldg(v + c1[u]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (c0[u] >= 0) s0 = fma(a0[u], x0[u], s0);
+            if (c1[u] >= 0) s1 = fma(a1[u], x1[u], s1);
+        }
+    }
 }
 
 template <int MODE, int GS>
 __global__ void __launch_bounds__(kCsrThreads) k_pass_a_csr(const PassAArgs a) {
     const int lane = threadIdx.x & 31, gl = lane & (GS - 1), gw = lane / GS;
-    const int64_t groups_per_warp = 32 / GS;
+    const int64_t gpw = 32 / GS;   // lane groups per warp; a warp covers 2 * gpw consecutive rows
     const int64_t warp_id = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
     const int64_t rows = a.row_end - a.row_begin;
     const OuterA o = outer_a(a, MODE);
-    for (int64_t base = warp_id * groups_per_warp; base < rows; base += nwarps * groups_per_warp) {
-        const int64_t idx = base + gw;
-        const bool valid = idx < rows;
-        const int64_t row = a.row_begin + idx;
-        EpiA e{};
-        double s = 0.0;
-        if (valid) {
-            if (gl == 0) e = epi_a_load(a, MODE, row, o);
-            s = csr_row_dot<GS>(a.ci, a.va, a.y, a.rp[row], a.rp[row + 1], gl);
+    for (int64_t base = warp_id * 2 * gpw; base < rows; base += nwarps * 2 * gpw) {
+        const int64_t i0 = base + gw, i1 = base + gpw + gw;
+        const bool v0 = i0 < rows, v1 = i1 < rows;
+        const int64_t r0 = a.row_begin + i0, r1 = a.row_begin + i1;
+        EpiA e0{}, e1{};
+        if (gl == 0) {
+            if (v0) e0 = epi_a_load(a, MODE, r0, o);
+            if (v1) e1 = epi_a_load(a, MODE, r1, o);
         }
-        s = group_sum<GS>(s);
-        if (valid && gl == 0) epi_a_store(a, MODE, row, s, e, o);
+        double s0, s1;
+        csr_row_dot2<GS>(a.ci, a.va, a.y, v0 ? a.rp[r0] : 0, v0 ? a.rp[r0 + 1] : 0, v1 ? a.rp[r1] : 0,
+                         v1 ? a.rp[r1 + 1] : 0, gl, s0, s1);
+        s0 = group_sum<GS>(s0);
+        s1 = group_sum<GS>(s1);
+        if (gl == 0) {
+            if (v0) epi_a_store(a, MODE, r0, s0, e0, o);
+            if (v1) epi_a_store(a, MODE, r1, s1, e1, o);
+        }
     }
 }
 
 template <int MODE, int GS>
 __global__ void __launch_bounds__(kCsrThreads) k_pass_b_csr(const PassBArgs b) {
     const int lane = threadIdx.x & 31, gl = lane & (GS - 1), gw = lane / GS;
-    const int64_t groups_per_warp = 32 / GS;
+    const int64_t gpw = 32 / GS;
     const int64_t warp_id = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
     const double avg_w = avg_weight(b, MODE);
-    for (int64_t base = warp_id * groups_per_warp; base < b.nrows; base += nwarps * groups_per_warp) {
+    // G' rows are short (config 4: Poisson(4) nonzeros): one row per lane group measured faster
+    for (int64_t base = warp_id * gpw; base < b.nrows; base += nwarps * gpw) {
         const int64_t j = base + gw;
         const bool valid = j < b.nrows;
         EpiB e{};

@@ -19,6 +19,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="0,1,3,4")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--cases", type=int, default=99, help="max cases per config")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -49,15 +50,17 @@ def main():
             mk = lambda rho: Solver(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho=rho,
                                     lambda_min_lb=0.5, stream=stream.cuda_stream, time_passes=True)
             cases = [("DFGM", 5.0, 300, 50), ("DGM", 5.0, 300, 20)]
-        for alg, rho, K, Kin in cases:
+        for alg, rho, K, Kin in cases[:args.cases]:
             s = mk(rho)
             L_in, L_d, nG2 = s.lipschitz(iters=80, safety=1e-3)
             s.solve(alg, K, Kin)                       # warm-up (graph build, clocks)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.nvtx.range_push("timed")
             e0.record(stream)
             infos = [s.solve(alg, K, Kin) for _ in range(args.reps)]
             e1.record(stream)
+            torch.cuda.nvtx.range_pop()
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / args.reps
             i = infos[-1]
