@@ -217,7 +217,7 @@ def main():
         nccl_id = obj[0]
 
     d = qpgen.dense_ineq_torch(n, p, seed=0, shift=0.05, device=str(dev))
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)     # the library runs on this stream; events are recorded on it
     s = Solver(d["Q"], d["q"], d["G"], d["g"], d["lb"], d["ub"], d["cone"], rho=rho, lambda_min_lb=0.05,
                world_size=world, rank=rank, nccl_id=nccl_id, stream=stream.cuda_stream, device=local_rank,
                time_passes=True)

@@ -69,8 +69,8 @@ typedef struct duquad_ctx duquad_ctx;
  * CSR (format == DUQUAD_CSR, batch == 1): int32 row pointers (rows+1),
  *   int32 column indices (sorted within a row), fp64 values, for Q (n rows)
  *   and G (p rows); the dense pointers are ignored.
- * on_device: 1 if every pointer is a device pointer, 0 if host.  Device inputs must be
- *   complete on options.stream; with stream == NULL setup first synchronizes the device.
+ * on_device: 1 if every pointer is a device pointer, 0 if host.  With device inputs setup
+ *   first synchronizes the device (inputs may be produced on any stream).
  * Ownership: duquad_setup copies/repacks everything into library-owned
  *   device memory; the caller may free its arrays when setup returns.
  */
@@ -131,6 +131,10 @@ typedef struct {
     int32_t rho0_path;     /* 1 (default): with rho == 0 (dense, batch 1) stream only Q per inner
                               step, c = q + G'mu formed once per outer iteration;
                               0: the generic two-pass inner step                           */
+    int32_t emulate_ranks; /* testing: with world_size > 1, no NCCL communicator is created; the
+                              world_size contexts (one per rank, same device and stream) are
+                              driven together by duquad_solve_emulated, whose all-gathers are
+                              device copies -- the sharded kernels and index math on 1 GPU  */
 } duquad_options;
 
 /* Per-solve report. */
@@ -227,6 +231,17 @@ duquad_status duquad_set_trace(duquad_ctx *ctx, double *lam_trace, double *u_tra
  */
 duquad_status duquad_residuals(duquad_ctx *ctx, int32_t which, double *F, double *dist,
                                double *lag);
+
+/*
+ * Testing entry point for the row-sharded path on ONE device: ctxs[r] (r = 0..P-1) must have
+ * been set up with world_size = P, rank = r, emulate_ranks = 1 and the same stream and device.
+ * Runs duquad_solve's schedule for all ranks in lock step, phase by phase; each all-gather of
+ * the y / w replicas is done with device-to-device copies between the contexts (no waiting
+ * kernels, no collective).  Constants must have been injected (duquad_set_constants) on every
+ * context.  Results per rank as for duquad_solve (duquad_get_result gives local slices).
+ */
+duquad_status duquad_solve_emulated(duquad_ctx **ctxs, int32_t P, int32_t alg, int32_t outer_iters,
+                                    int32_t inner_iters);
 
 void duquad_destroy(duquad_ctx *ctx);
 

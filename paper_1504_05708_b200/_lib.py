@@ -52,6 +52,7 @@ class Options(C.Structure):
         ("use_graphs", C.c_int32), ("world_size", C.c_int32), ("rank", C.c_int32),
         ("nccl_id", C.c_void_p), ("stream", C.c_void_p), ("device", C.c_int32),
         ("time_passes", C.c_int32), ("small_path", C.c_int32), ("rho0_path", C.c_int32),
+        ("emulate_ranks", C.c_int32),
     ]
 
 
@@ -81,6 +82,7 @@ _SIGS = {
     "duquad_set_trace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]),
     "duquad_residuals": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                    C.POINTER(C.c_double)]),
+    "duquad_solve_emulated": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
     "duquad_destroy": (None, [C.c_void_p]),
     "duquad_last_error": (C.c_char_p, [C.c_void_p]),
 }

@@ -37,6 +37,7 @@ struct duquad_ctx {
     double rho = 0.0;
     // sharding
     int world = 1, rank = 0;
+    bool emulated = false;   // P ranks on one device, driven by duquad_solve_emulated
     ncclComm_t comm = nullptr;
     int64_t n_slice = 0, p_slice = 0, r0 = 0, s0 = 0, nloc = 0, ploc = 0;
     // layout
@@ -158,7 +159,7 @@ struct DevGuard {
 
 // ----------------------------------------------------------- collectives
 duquad_status allgather_vec(duquad_ctx *ctx, double *full) {
-    if (ctx->world == 1) return DUQUAD_OK;
+    if (ctx->world == 1 || ctx->emulated) return DUQUAD_OK;
     NK(ncclAllGather(full + ctx->rank * ctx->n_slice, full, (size_t)ctx->n_slice, ncclDouble, ctx->comm,
                      ctx->stream));
     return DUQUAD_OK;
@@ -167,7 +168,7 @@ duquad_status allgather_vec(duquad_ctx *ctx, double *full) {
 duquad_status allgather_y(duquad_ctx *ctx) { return allgather_vec(ctx, ctx->y_full); }
 
 duquad_status allgather_w(duquad_ctx *ctx) {
-    if (ctx->world == 1) return DUQUAD_OK;
+    if (ctx->world == 1 || ctx->emulated) return DUQUAD_OK;
     NK(ncclAllGather(ctx->w_full + ctx->rank * ctx->p_slice, ctx->w_full, (size_t)ctx->p_slice,
                      ncclDouble, ctx->comm, ctx->stream));
     return DUQUAD_OK;
@@ -175,6 +176,7 @@ duquad_status allgather_w(duquad_ctx *ctx) {
 
 duquad_status allreduce_sum(duquad_ctx *ctx, double *buf, int count) {
     if (ctx->world == 1) return DUQUAD_OK;
+    if (ctx->emulated) return fail(ctx, DUQUAD_ESTATE, "not available on emulated ranks (inject constants)");
     NK(ncclAllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
     return DUQUAD_OK;
 }
@@ -236,50 +238,34 @@ PassBArgs make_b(duquad_ctx *c) {
 
 BatchedArgs make_batched(duquad_ctx *c, int pass);
 
-// One outer DFOM iteration at rho = 0 with the K3 inner step (row a1'):
-//   1. pass A over the G rows only at y = u_bar^{j-1}: fused DFOM step, w = mu^j
-//   2. c = q + G'w (one pass over G'), and y^1 = u_bar^{j-1} into replica A
-//   3. K_in x K3 (stream Q only), y ping-ponging between replicas A and B.
-duquad_status run_outer_rho0(duquad_ctx *ctx, const std::vector<double> &beta_in, int Kin, int j,
-                             std::vector<cudaEvent_t> *ev) {
-    duquad_status st;
-    double *Y[2] = {ctx->y_full, ctx->y_full2};
-    const int64_t off = ctx->rank * ctx->n_slice;
-    PassAArgs a = make_a(ctx);
-    a.row_begin = ctx->nloc;          // G rows only
-    a.first_inner = 1;
-    a.y = Y[Kin % 2];                 // the replica the previous inner solve finished in
-    CK(launch_pass_a(a, MODE_SOLVE, ctx->cfg_a, ctx->stream));
-    if ((st = allgather_w(ctx)) != DUQUAD_OK) return st;
+// ---------------------------------------------------------------- outer iteration, by phases
+// An outer DFOM iteration is a fixed sequence of phases, each a kernel (plus trace copies)
+// followed by an optional all-gather of one replica buffer.  run_outer() interleaves them with
+// NCCL all-gathers; duquad_solve_emulated() runs the phases of P contexts in lock step and
+// replaces the all-gather by device copies.
+enum GatherBuf { G_NONE = -1, G_Y = 0, G_Y2 = 1, G_W = 2 };
+
+double *gather_ptr(duquad_ctx *c, int b) { return b == G_W ? c->w_full : (b == G_Y2 ? c->y_full2 : c->y_full); }
+int64_t gather_slice(duquad_ctx *c, int b) { return b == G_W ? c->p_slice : c->n_slice; }
+
+duquad_status gather(duquad_ctx *ctx, int b) {
+    if (b < 0 || ctx->world == 1 || ctx->emulated) return DUQUAD_OK;   // emulated: group driver copies
+    double *full = gather_ptr(ctx, b);
+    const int64_t sl = gather_slice(ctx, b);
+    NK(ncclAllGather(full + ctx->rank * sl, full, (size_t)sl, ncclDouble, ctx->comm, ctx->stream));
+    return DUQUAD_OK;
+}
+
+int num_phases(const duquad_ctx *c, int Kin) { return c->rho0 ? Kin + 3 : 2 * Kin + 1; }
+
+duquad_status trace_lam_copy(duquad_ctx *ctx, int j) {
     if (j >= 2 && ctx->trace_lam && j - 2 < ctx->trace_max)
         CK(cudaMemcpyAsync(ctx->trace_lam + (j - 2) * ctx->ploc, ctx->lam_prev, ctx->ploc * sizeof(double),
                            cudaMemcpyDeviceToDevice, ctx->stream));
-    PassBArgs c = make_b(ctx);
-    c.qy = ctx->q;                    // c = q + G'w
-    c.use_qy = 1;
-    c.out = ctx->cvec;
-    CK(launch_pass_b(c, MODE_LIN, ctx->cfg_b, ctx->stream));
-    CK(cudaMemcpyAsync(Y[0] + off, ctx->x, ctx->nloc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
-    if ((st = allgather_vec(ctx, Y[0])) != DUQUAD_OK) return st;
-    for (int k = 1; k <= Kin; ++k) {
-        PassAArgs a3 = make_a(ctx);
-        a3.y = Y[(k - 1) % 2];
-        PassBArgs bl = make_b(ctx);
-        bl.q = ctx->cvec;
-        bl.y = Y[(k - 1) % 2] + off;
-        bl.beta_in = beta_in[k];
-        bl.last_inner = (k == Kin);
-        PassBArgs bs = bl;
-        bs.y = Y[k % 2] + off;
-        if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 0], ctx->stream));
-        CK(launch_rho0_step(a3, bl, bs, ctx->cfg_k3, ctx->stream));
-        if (ev) {
-            CK(cudaEventRecord((*ev)[4 * (k - 1) + 1], ctx->stream));
-            CK(cudaEventRecord((*ev)[4 * (k - 1) + 2], ctx->stream));
-            CK(cudaEventRecord((*ev)[4 * (k - 1) + 3], ctx->stream));
-        }
-        if ((st = allgather_vec(ctx, Y[k % 2])) != DUQUAD_OK) return st;
-    }
+    return DUQUAD_OK;
+}
+
+duquad_status end_outer(duquad_ctx *ctx, int j) {
     if (j >= 1 && ctx->trace_u && j - 1 < ctx->trace_max)
         CK(cudaMemcpyAsync(ctx->trace_u + (j - 1) * ctx->nloc, ctx->x, ctx->nloc * sizeof(double),
                            cudaMemcpyDeviceToDevice, ctx->stream));
@@ -287,45 +273,103 @@ duquad_status run_outer_rho0(duquad_ctx *ctx, const std::vector<double> &beta_in
     return DUQUAD_OK;
 }
 
-// One outer DFOM iteration (reads its per-outer scalars through d_j).
+// Phase ph of outer iteration j (reads its per-outer scalars through d_j); *gb = buffer to
+// all-gather afterwards.
+//   generic:  ph = 2(k-1): pass A (k = 1: fused DFOM step), gather w;  ph = 2k-1: pass B, gather y
+//   rho = 0 (row a1', K3):  ph 0: pass A over the G rows at y = u_bar^{j-1} (DFOM step, w = mu^j),
+//             gather w;  ph 1: c = q + G'w and y^1 = u_bar^{j-1} into replica A, gather it;
+//             ph 1+k: K3 step k (Q only), y ping-pong between replicas A and B
+//   last phase: trace u_bar^j, advance j
+duquad_status outer_phase(duquad_ctx *ctx, const std::vector<double> &beta_in, int Kin, int j, int ph,
+                          std::vector<cudaEvent_t> *ev, int *gb) {
+    *gb = G_NONE;
+    const int64_t off = ctx->rank * ctx->n_slice;
+    duquad_status st;
+    if (ph == num_phases(ctx, Kin) - 1) return end_outer(ctx, j);
+    if (ctx->rho0) {
+        double *Y[2] = {ctx->y_full, ctx->y_full2};
+        if (ph == 0) {
+            PassAArgs a = make_a(ctx);
+            a.row_begin = ctx->nloc;          // G rows only
+            a.first_inner = 1;
+            a.y = Y[Kin % 2];                 // the replica the previous inner solve finished in
+            CK(launch_pass_a(a, MODE_SOLVE, ctx->cfg_a, ctx->stream));
+            if ((st = trace_lam_copy(ctx, j)) != DUQUAD_OK) return st;
+            *gb = G_W;
+        } else if (ph == 1) {
+            PassBArgs c = make_b(ctx);
+            c.qy = ctx->q;                    // c = q + G'w
+            c.use_qy = 1;
+            c.out = ctx->cvec;
+            CK(launch_pass_b(c, MODE_LIN, ctx->cfg_b, ctx->stream));
+            CK(cudaMemcpyAsync(Y[0] + off, ctx->x, ctx->nloc * sizeof(double), cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+            *gb = G_Y;
+        } else {
+            const int k = ph - 1;
+            PassAArgs a3 = make_a(ctx);
+            a3.y = Y[(k - 1) % 2];
+            PassBArgs bl = make_b(ctx);
+            bl.q = ctx->cvec;
+            bl.y = Y[(k - 1) % 2] + off;
+            bl.beta_in = beta_in[k];
+            bl.last_inner = (k == Kin);
+            PassBArgs bs = bl;
+            bs.y = Y[k % 2] + off;
+            if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 0], ctx->stream));
+            CK(launch_rho0_step(a3, bl, bs, ctx->cfg_k3, ctx->stream));
+            if (ev) {
+                CK(cudaEventRecord((*ev)[4 * (k - 1) + 1], ctx->stream));
+                CK(cudaEventRecord((*ev)[4 * (k - 1) + 2], ctx->stream));
+                CK(cudaEventRecord((*ev)[4 * (k - 1) + 3], ctx->stream));
+            }
+            *gb = (k % 2) ? G_Y2 : G_Y;
+        }
+        return DUQUAD_OK;
+    }
+    const int k = ph / 2 + 1;
+    const bool bt = ctx->Btot > 1;
+    if (ph % 2 == 0) {
+        if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 0], ctx->stream));
+        if (bt) {
+            BatchedArgs BA = make_batched(ctx, 0);
+            BA.a.first_inner = (k == 1);
+            CK(launch_batched(BA, 0, MODE_SOLVE, ctx->stream));
+        } else {
+            PassAArgs a = make_a(ctx);
+            a.first_inner = (k == 1);
+            CK(launch_pass_a(a, MODE_SOLVE, ctx->cfg_a, ctx->stream));
+        }
+        if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 1], ctx->stream));
+        if (k == 1 && (st = trace_lam_copy(ctx, j)) != DUQUAD_OK) return st;
+        *gb = G_W;
+    } else {
+        if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 2], ctx->stream));
+        if (bt) {
+            BatchedArgs BB = make_batched(ctx, 1);
+            BB.b.beta_in = beta_in[k];
+            BB.b.last_inner = (k == Kin);
+            CK(launch_batched(BB, 1, MODE_SOLVE, ctx->stream));
+        } else {
+            PassBArgs b = make_b(ctx);
+            b.beta_in = beta_in[k];
+            b.last_inner = (k == Kin);
+            CK(launch_pass_b(b, MODE_SOLVE, ctx->cfg_b, ctx->stream));
+        }
+        if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 3], ctx->stream));
+        *gb = G_Y;
+    }
+    return DUQUAD_OK;
+}
+
 duquad_status run_outer(duquad_ctx *ctx, const std::vector<double> &beta_in, int Kin, int j,
                         std::vector<cudaEvent_t> *ev) {
-    if (ctx->rho0) return run_outer_rho0(ctx, beta_in, Kin, j, ev);
-    PassAArgs a = make_a(ctx);
-    PassBArgs b = make_b(ctx);
-    const bool bt = ctx->Btot > 1;
-    BatchedArgs BA{}, BB{};
-    if (bt) {
-        BA = make_batched(ctx, 0);
-        BB = make_batched(ctx, 1);
-    }
     duquad_status st;
-    for (int k = 1; k <= Kin; ++k) {
-        a.first_inner = BA.a.first_inner = (k == 1);
-        if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 0], ctx->stream));
-        if (bt)
-            CK(launch_batched(BA, 0, MODE_SOLVE, ctx->stream));
-        else
-            CK(launch_pass_a(a, MODE_SOLVE, ctx->cfg_a, ctx->stream));
-        if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 1], ctx->stream));
-        if ((st = allgather_w(ctx)) != DUQUAD_OK) return st;
-        if (k == 1 && j >= 2 && ctx->trace_lam && j - 2 < ctx->trace_max)
-            CK(cudaMemcpyAsync(ctx->trace_lam + (j - 2) * ctx->ploc, ctx->lam_prev,
-                               ctx->ploc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
-        b.beta_in = BB.b.beta_in = beta_in[k];
-        b.last_inner = BB.b.last_inner = (k == Kin);
-        if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 2], ctx->stream));
-        if (bt)
-            CK(launch_batched(BB, 1, MODE_SOLVE, ctx->stream));
-        else
-            CK(launch_pass_b(b, MODE_SOLVE, ctx->cfg_b, ctx->stream));
-        if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 3], ctx->stream));
-        if ((st = allgather_y(ctx)) != DUQUAD_OK) return st;
+    for (int ph = 0; ph < num_phases(ctx, Kin); ++ph) {
+        int gb;
+        if ((st = outer_phase(ctx, beta_in, Kin, j, ph, ev, &gb)) != DUQUAD_OK) return st;
+        if ((st = gather(ctx, gb)) != DUQUAD_OK) return st;
     }
-    if (j >= 1 && ctx->trace_u && j - 1 < ctx->trace_max && j >= 1)
-        CK(cudaMemcpyAsync(ctx->trace_u + (j - 1) * ctx->nloc, ctx->x, ctx->nloc * sizeof(double),
-                           cudaMemcpyDeviceToDevice, ctx->stream));
-    CK(launch_advance(ctx->d_j, ctx->stream));
     return DUQUAD_OK;
 }
 
@@ -597,6 +641,7 @@ void duquad_default_options(duquad_options *o) {
     o->time_passes = 0;
     o->small_path = 1;
     o->rho0_path = 1;
+    o->emulate_ranks = 0;
 }
 
 duquad_status duquad_shard_range(int64_t rows, int32_t world, int32_t rank, int64_t *begin,
@@ -664,7 +709,7 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         return fail(nullptr, DUQUAD_EINVAL, "FGM_SIGMA needs sigma > 0");
     if (opt.world_size < 1 || opt.rank < 0 || opt.rank >= opt.world_size)
         return fail(nullptr, DUQUAD_EINVAL, "bad world_size / rank");
-    if (opt.world_size > 1 && !batched && !opt.nccl_id)
+    if (opt.world_size > 1 && !batched && !opt.nccl_id && !opt.emulate_ranks)
         return fail(nullptr, DUQUAD_EINVAL, "row-sharded setup needs nccl_id");
     if (!prob->on_device) {   // host data: validate here (device data is validated by a kernel)
         if ((!csr && (!finite_host(prob->Q, n, n, prob->ldQ) || (p > 0 && !finite_host(prob->G, p, n, prob->ldG)))) ||
@@ -734,7 +779,8 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
     ctx->nloc = std::min<int64_t>(n, ctx->r0 + ctx->n_slice) - ctx->r0;
     ctx->s0 = std::min<int64_t>(p, ctx->rank * ctx->p_slice);
     ctx->ploc = std::min<int64_t>(p, ctx->s0 + ctx->p_slice) - ctx->s0;
-    if (ctx->world > 1) {
+    ctx->emulated = ctx->world > 1 && opt.emulate_ranks;
+    if (ctx->world > 1 && !ctx->emulated) {
         ncclUniqueId id;
         std::memcpy(&id, opt.nccl_id, sizeof(id));
         ncclResult_t r = ncclCommInitRank(&ctx->comm, ctx->world, id, ctx->rank);
@@ -774,8 +820,8 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
     CKS(dalloc(&ctx->d_flag, 4));
     cudaStream_t s = ctx->stream;
     // Device inputs may still be in flight on another stream of the caller (e.g. torch's):
-    // with a library-owned stream, wait for the whole device before reading them.
-    if (prob->on_device && ctx->own_stream) CKS(cudaDeviceSynchronize());
+    // wait for the whole device before reading them (setup is not on the hot path).
+    if (prob->on_device) CKS(cudaDeviceSynchronize());
     // ---- pack [Q_r; G_r] and G'_r
     if (csr) {
         duquad_status st = setup_csr(ctx, prob);
@@ -947,19 +993,15 @@ duquad_status duquad_set_trace(duquad_ctx *ctx, double *lam_trace, double *u_tra
     return DUQUAD_OK;
 }
 
-duquad_status duquad_solve(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t inner, duquad_result *res) {
-    if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
-    if (alg != DUQUAD_DGM && alg != DUQUAD_DFGM) return fail(ctx, DUQUAD_EINVAL, "bad alg");
-    if (outer < 1 || inner < 1) return fail(ctx, DUQUAD_EINVAL, "need outer_iters >= 1 and inner_iters >= 1");
-    if (!ctx->have_consts) return fail(ctx, DUQUAD_ESTATE, "constants not set (duquad_lipschitz or duquad_set_constants)");
-    DevGuard guard(ctx->dev);
+// Per-solve host tables (fp64, PAPER.md:358-363 / 587-589 / 700-706), their upload, and the
+// initial state u_bar^0 = [0]_U, mu^1 = lambda^0 = 0 (before the first all-gather of y).
+static duquad_status solve_prepare(duquad_ctx *ctx, int alg, int K, int Kin, std::vector<double> &beta_in) {
     cudaStream_t s = ctx->stream;
-    const int K = outer, Kin = inner;
     // ---- host tables (fp64, PAPER.md:358-363 / 587-589 / 700-706)
     std::vector<double> theta(K + 3, 0.0);
     theta[1] = 1.0;
     for (int k = 1; k < K + 2; ++k) theta[k + 1] = (1.0 + std::sqrt(1.0 + 4.0 * theta[k] * theta[k])) / 2.0;
-    std::vector<double> beta_in(Kin + 1, 0.0);
+    beta_in.assign(Kin + 1, 0.0);
     if (ctx->opt.inner_rule == DUQUAD_INNER_FGM) {
         std::vector<double> th(Kin + 2, 0.0);
         th[1] = 1.0;
@@ -994,6 +1036,22 @@ duquad_status duquad_solve(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t 
     else
         CK(launch_init_state(ctx->x, ctx->y_full + ctx->rank * ctx->n_slice, ctx->xhat, ctx->lb, ctx->ub,
                              ctx->nloc, ctx->mu, ctx->lam_prev, ctx->ploc, ctx->d_j, ctx->d_flag, s));
+    return DUQUAD_OK;
+}
+
+duquad_status duquad_solve(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t inner, duquad_result *res) {
+    if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
+    if (alg != DUQUAD_DGM && alg != DUQUAD_DFGM) return fail(ctx, DUQUAD_EINVAL, "bad alg");
+    if (outer < 1 || inner < 1) return fail(ctx, DUQUAD_EINVAL, "need outer_iters >= 1 and inner_iters >= 1");
+    if (!ctx->have_consts) return fail(ctx, DUQUAD_ESTATE, "constants not set (duquad_lipschitz or duquad_set_constants)");
+    DevGuard guard(ctx->dev);
+    cudaStream_t s = ctx->stream;
+    const int K = outer, Kin = inner;
+    std::vector<double> beta_in;
+    {
+        duquad_status st0 = solve_prepare(ctx, alg, K, Kin, beta_in);
+        if (st0 != DUQUAD_OK) return st0;
+    }
     duquad_status st;
     if ((st = allgather_y(ctx)) != DUQUAD_OK) return st;
     if (ctx->small) {   // whole solve in one single-CTA kernel (K4)
@@ -1145,6 +1203,62 @@ duquad_status duquad_solve(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t 
     for (auto &e : ev) cudaEventDestroy(e);
     ctx->solved = true;
     if (flag) return fail(ctx, DUQUAD_ENONFINITE, "an iterate became non-finite");
+    return DUQUAD_OK;
+}
+
+// all-gather of replica buffer b across emulated ranks: device copies of every rank's slice
+static duquad_status group_gather(duquad_ctx **c, int P, int b) {
+    if (b < 0 || P == 1) return DUQUAD_OK;
+    duquad_ctx *ctx = c[0];
+    const int64_t sl = gather_slice(ctx, b);
+    for (int d = 0; d < P; ++d)
+        for (int s = 0; s < P; ++s)
+            if (s != d && sl > 0)
+                CK(cudaMemcpyAsync(gather_ptr(c[d], b) + s * sl, gather_ptr(c[s], b) + s * sl, sl * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
+    return DUQUAD_OK;
+}
+
+duquad_status duquad_solve_emulated(duquad_ctx **ctxs, int32_t P, int32_t alg, int32_t outer, int32_t inner) {
+    if (!ctxs || P < 1) return fail(nullptr, DUQUAD_EINVAL, "need P >= 1 contexts");
+    for (int r = 0; r < P; ++r) {
+        duquad_ctx *c = ctxs[r];
+        if (!c) return fail(nullptr, DUQUAD_EINVAL, "null context");
+        if (c->world != P || c->rank != r || (P > 1 && !c->emulated) || c->stream != ctxs[0]->stream ||
+            c->dev != ctxs[0]->dev || c->Btot > 1 || c->small || c->n != ctxs[0]->n || c->p != ctxs[0]->p)
+            return fail(ctxs[0], DUQUAD_EINVAL,
+                        "emulated group: contexts must be ranks 0..P-1 of one row-sharded problem with "
+                        "emulate_ranks = 1 and the same device and stream (rank " + std::to_string(r) +
+                            ": world " + std::to_string(c->world) + ", rank " + std::to_string(c->rank) +
+                            ", emulated " + std::to_string(c->emulated) + ", small " + std::to_string(c->small) + ")");
+        if (!c->have_consts) return fail(ctxs[0], DUQUAD_ESTATE, "constants not set");
+    }
+    if (alg != DUQUAD_DGM && alg != DUQUAD_DFGM) return fail(ctxs[0], DUQUAD_EINVAL, "bad alg");
+    if (outer < 1 || inner < 1) return fail(ctxs[0], DUQUAD_EINVAL, "need outer_iters >= 1 and inner_iters >= 1");
+    duquad_ctx *ctx = ctxs[0];
+    DevGuard guard(ctx->dev);
+    const int K = outer, Kin = inner;
+    std::vector<double> beta_in;
+    duquad_status st;
+    for (int r = 0; r < P; ++r)
+        if ((st = solve_prepare(ctxs[r], alg, K, Kin, beta_in)) != DUQUAD_OK) return st;
+    if ((st = group_gather(ctxs, P, G_Y)) != DUQUAD_OK) return st;
+    for (int j = 1; j <= K + 1; ++j)
+        for (int ph = 0; ph < num_phases(ctx, Kin); ++ph) {
+            int gb = G_NONE;
+            for (int r = 0; r < P; ++r)
+                if ((st = outer_phase(ctxs[r], beta_in, Kin, j, ph, nullptr, &gb)) != DUQUAD_OK) return st;
+            if ((st = group_gather(ctxs, P, gb)) != DUQUAD_OK) return st;
+        }
+    CK(cudaStreamSynchronize(ctx->stream));
+    int32_t any = 0;
+    for (int r = 0; r < P; ++r) {
+        int32_t flag = 0;
+        CK(cudaMemcpy(&flag, ctxs[r]->d_flag, sizeof(flag), cudaMemcpyDeviceToHost));
+        any |= flag;
+        ctxs[r]->solved = true;
+    }
+    if (any) return fail(ctx, DUQUAD_ENONFINITE, "an iterate became non-finite");
     return DUQUAD_OK;
 }
 

@@ -53,6 +53,14 @@ def shard_range(rows: int, world: int, rank: int):
     return b.value, e.value
 
 
+def solve_emulated(solvers, alg: str = "DFGM", outer: int = 1, inner: int = 1):
+    """Runs P row-sharded Solvers (ranks 0..P-1, emulate_ranks=True, same device and stream) in
+    lock step on one GPU; all-gathers are device copies (testing the sharded path, row a11)."""
+    arr = (C.c_void_p * len(solvers))(*[s._ctx.value for s in solvers])
+    L.check(L.lib().duquad_solve_emulated(arr, len(solvers), _ALGS[alg], int(outer), int(inner)),
+            solvers[0]._ctx)
+
+
 class Solver:
     """One DuQuad context: setup (pack + upload), constants, solve, results.
 
@@ -66,7 +74,7 @@ class Solver:
                  use_graphs: bool = True, world_size: int = 1, rank: int = 0,
                  nccl_id: Optional[bytes] = None, stream=None, device: int = -1,
                  time_passes: bool = False, cone_all: int = L.CONE_NONPOS, small_path: bool = True,
-                 rho0_path: bool = True):
+                 rho0_path: bool = True, emulate_ranks: bool = False):
         """Dense Q (n x n) and G (p x n), or scipy.sparse matrices (-> CSR path, row a10)."""
         if hasattr(Q, "tocsr"):
             Qc = Q.tocsr()
@@ -87,7 +95,8 @@ class Solver:
                    dict(dual_step_scale=dual_step_scale, project_dual=project_dual, inner_rule=inner_rule,
                         sigma=sigma, lambda_min_lb=lambda_min_lb, l_mode=l_mode, use_graphs=use_graphs,
                         world_size=world_size, rank=rank, nccl_id=nccl_id, stream=stream, device=device,
-                        time_passes=time_passes, small_path=small_path, rho0_path=rho0_path))
+                        time_passes=time_passes, small_path=small_path, rho0_path=rho0_path,
+                        emulate_ranks=emulate_ranks))
 
     @classmethod
     def csr(cls, n, p, Q_rowptr, Q_col, Q_val, G_rowptr, G_col, G_val, q, g, lb, ub, cone=None,
@@ -146,6 +155,7 @@ class Solver:
         opt.time_passes = int(o["time_passes"])
         opt.small_path = int(o.get("small_path", True))
         opt.rho0_path = int(o.get("rho0_path", True))
+        opt.emulate_ranks = int(o.get("emulate_ranks", False))
         ctx = C.c_void_p()
         L.check(lib.duquad_setup(C.byref(ctx), C.byref(prob), float(rho), C.byref(opt)))
         self._ctx = ctx
