@@ -135,6 +135,11 @@ typedef struct {
                               world_size contexts (one per rank, same device and stream) are
                               driven together by duquad_solve_emulated, whose all-gathers are
                               device copies -- the sharded kernels and index math on 1 GPU  */
+    int32_t fused_path;    /* 1 (default): for large dense QPs on one GPU (n >= 4096), the
+                              byte-floor inner step: one streaming kernel reads the upper
+                              triangle of the symmetric Q once and G once (CTA pairs exchange
+                              row sums through distributed shared memory), 8(n(n+1)/2 + pn)
+                              bytes instead of 8(n^2 + 2pn); 0: the two-pass inner step    */
 } duquad_options;
 
 /* Per-solve report. */

@@ -52,7 +52,7 @@ class Options(C.Structure):
         ("use_graphs", C.c_int32), ("world_size", C.c_int32), ("rank", C.c_int32),
         ("nccl_id", C.c_void_p), ("stream", C.c_void_p), ("device", C.c_int32),
         ("time_passes", C.c_int32), ("small_path", C.c_int32), ("rho0_path", C.c_int32),
-        ("emulate_ranks", C.c_int32),
+        ("emulate_ranks", C.c_int32), ("fused_path", C.c_int32),
     ]
 
 

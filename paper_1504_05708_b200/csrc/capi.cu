@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -62,6 +63,11 @@ struct duquad_ctx {
     bool rho0 = false;
     double *y_full2 = nullptr, *cvec = nullptr;
     LaunchCfg cfg_k3{};
+    // byte-floor inner step (symmetric Q read once as a triangle, G read once)
+    bool fused = false;
+    FusedArgs fz{};
+    double *ws = nullptr;
+    int fused_epi_grid = 0;
     // whole-solve single-CTA kernel (small dense QPs)
     bool small = false;
     size_t small_smem = 0;
@@ -124,7 +130,7 @@ void free_all(duquad_ctx *c) {
     double *ds[] = {c->A,   c->GT,  c->y_full, c->w_full, c->qy,       c->x,        c->xhat,     c->q,
                     c->lb,  c->ub,  c->g,      c->mu,     c->lam_prev, c->lz_vprev, c->lz_w,     c->scal,
                     c->partials, c->Yb, c->Xb, c->XHb,   c->QYb,      c->qb,       c->Wb,       c->gb,
-                    c->mub, c->lpb, c->d_beta, c->y_full2, c->cvec};
+                    c->mub, c->lpb, c->d_beta, c->y_full2, c->cvec, c->ws};
     for (double *d : ds)
         if (d) cudaFree(d);
     if (c->cone) cudaFree(c->cone);
@@ -317,11 +323,22 @@ duquad_status outer_phase(duquad_ctx *ctx, const std::vector<double> &beta_in, i
             PassBArgs bs = bl;
             bs.y = Y[k % 2] + off;
             if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 0], ctx->stream));
-            CK(launch_rho0_step(a3, bl, bs, ctx->cfg_k3, ctx->stream));
-            if (ev) {
-                CK(cudaEventRecord((*ev)[4 * (k - 1) + 1], ctx->stream));
-                CK(cudaEventRecord((*ev)[4 * (k - 1) + 2], ctx->stream));
-                CK(cudaEventRecord((*ev)[4 * (k - 1) + 3], ctx->stream));
+            if (ctx->fused) {   // symmetric-Q stream (upper triangle once) + epilogue with c
+                FusedArgs fz = ctx->fz;
+                fz.y = Y[(k - 1) % 2];
+                fz.a = make_a(ctx);
+                CK(launch_fused_stream(fz, ctx->stream));
+                if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 1], ctx->stream));
+                if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 2], ctx->stream));
+                CK(launch_fused_epi(bl, bs, ctx->ws, fz.nb, ctx->fused_epi_grid, ctx->stream));
+                if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 3], ctx->stream));
+            } else {
+                CK(launch_rho0_step(a3, bl, bs, ctx->cfg_k3, ctx->stream));
+                if (ev) {
+                    CK(cudaEventRecord((*ev)[4 * (k - 1) + 1], ctx->stream));
+                    CK(cudaEventRecord((*ev)[4 * (k - 1) + 2], ctx->stream));
+                    CK(cudaEventRecord((*ev)[4 * (k - 1) + 3], ctx->stream));
+                }
             }
             *gb = (k % 2) ? G_Y2 : G_Y;
         }
@@ -329,6 +346,25 @@ duquad_status outer_phase(duquad_ctx *ctx, const std::vector<double> &beta_in, i
     }
     const int k = ph / 2 + 1;
     const bool bt = ctx->Btot > 1;
+    if (ctx->fused) {   // byte-floor step: one stream over the Q triangle and G, then the epilogue
+        if (ph % 2 == 0) {
+            FusedArgs fz = ctx->fz;
+            fz.a = make_a(ctx);
+            fz.a.first_inner = (k == 1);
+            if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 0], ctx->stream));
+            CK(launch_fused_stream(fz, ctx->stream));
+            if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 1], ctx->stream));
+            if (k == 1 && (st = trace_lam_copy(ctx, j)) != DUQUAD_OK) return st;
+        } else {
+            PassBArgs b = make_b(ctx);
+            b.beta_in = beta_in[k];
+            b.last_inner = (k == Kin);
+            if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 2], ctx->stream));
+            CK(launch_fused_epi(b, b, ctx->ws, ctx->fz.nb, ctx->fused_epi_grid, ctx->stream));
+            if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 3], ctx->stream));
+        }
+        return DUQUAD_OK;
+    }
     if (ph % 2 == 0) {
         if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 0], ctx->stream));
         if (bt) {
@@ -642,6 +678,7 @@ void duquad_default_options(duquad_options *o) {
     o->small_path = 1;
     o->rho0_path = 1;
     o->emulate_ranks = 0;
+    o->fused_path = 1;
 }
 
 duquad_status duquad_shard_range(int64_t rows, int32_t world, int32_t rank, int64_t *begin,
@@ -928,6 +965,41 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         ctx->cfg_k3 = {ctx->cfg_b.grid, pass_threads(), smem_a};
         ctx->rho0 = true;
     }
+    if (!batched && ctx->world == 1 && opt.fused_path && n >= 4096) {   // byte-floor inner step
+        const int nchq = fused_nchq(ctx->ld);
+        if (nchq >= 2 && nchq <= 9) {
+            const int nb = ctx->num_sms & ~1;
+            int nq = nb;                        // rho = 0 (K3) or p = 0: Q role only
+            if (!ctx->rho0 && p > 0) {
+                const double bq = 0.5 * (double)n * (double)(n + 1), bg = (double)p * (double)n;
+                nq = 2 * (int)std::llround(0.5 * nb * bq / (bq + bg));
+                nq = std::max(2, std::min(nb - 2, nq));
+            }
+            if (const char *ov = std::getenv("DUQUAD_FUSED_NQ")) nq = std::atoi(ov);   // tuning experiments
+            const int64_t rows_per_q = 2 * (((n + 1) / 2 + nq - 1) / nq);
+            const int slots_q = fused_q_slots(ctx->ld, rows_per_q, prop.sharedMemPerBlockOptin);
+            const size_t fsmem = fused_smem_bytes(ctx->ld, rows_per_q, slots_q);
+            if (slots_q > 0 && fsmem <= (size_t)prop.sharedMemPerBlockOptin) {
+                CKS(dalloc(&ctx->ws, ctx->ld * (int64_t)nb));
+                CKS(configure_fused_kernels(nchq, fsmem));
+                FusedArgs &fz = ctx->fz;
+                fz.Q = ctx->A;
+                fz.G = ctx->A + n * ctx->ld;
+                fz.y = ctx->y_full;
+                fz.ws = ctx->ws;
+                fz.n = n;
+                fz.p = p;
+                fz.ld = ctx->ld;
+                fz.nb = nb;
+                fz.nq_ctas = nq;
+                fz.nchq = nchq;
+                fz.slots_q = slots_q;
+                fz.smem = fsmem;
+                ctx->fused_epi_grid = ctx->num_sms * 8;
+                ctx->fused = true;
+            }
+        }
+    }
     if (!batched && ctx->world == 1 && opt.small_path) {
         ctx->small_smem = small_smem_bytes(n, p, ctx->ld, ctx->ldp);
         if (ctx->small_smem <= (size_t)prop.sharedMemPerBlockOptin) {
@@ -1165,7 +1237,15 @@ duquad_status duquad_solve(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t 
         res->kernel_launches = 1 + (int64_t)(K + 1) * (2 * Kin + 1);
         res->matrix_passes = (int64_t)(K + 1) * Kin * 2;
         const double nn = (double)ctx->n, nl = (double)ctx->nloc, pl = (double)ctx->ploc, pp = (double)ctx->p;
-        if (ctx->rho0) {       // K3 inner steps: Q only; per outer: one G pass and one G' pass
+        if (ctx->fused) {      // byte floor: Q triangle (+ G once) streamed, workspace through L2
+            const double tri = 0.5 * nn * (nn + 1.0), wsb = (double)ctx->fz.nb * (double)ctx->ld;
+            res->bytes_pass_a = 8.0 * (tri + (ctx->rho0 ? 0.0 : pp * nn) + nn + wsb);
+            res->bytes_pass_b = 8.0 * (wsb + 8.0 * nn);
+            if (ctx->rho0) {
+                res->kernel_launches = 1 + (int64_t)(K + 1) * (2 * Kin + 3);
+                res->matrix_passes = (int64_t)(K + 1) * (Kin + 2);
+            }
+        } else if (ctx->rho0) {       // K3 inner steps: Q only; per outer: one G pass and one G' pass
             res->kernel_launches = 1 + (int64_t)(K + 1) * (Kin + 3);
             res->matrix_passes = (int64_t)(K + 1) * (Kin + 2);
             res->bytes_pass_a = 8.0 * (nl * nn + nn + 8.0 * nl);   // "pass A" slot = the K3 step

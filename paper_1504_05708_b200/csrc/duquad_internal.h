@@ -114,6 +114,21 @@ struct SmallArgs {
     double *x_out, *xhat_out, *y_out, *lam_out, *mu_out;
 };
 
+// ---------------------------------------------------------------- byte-floor inner step
+struct FusedArgs {
+    const double *Q;       // [Q] rows of the packed [Q;G] (ld doubles per row)
+    const double *G;       // [G] rows
+    const double *y;       // y replica (ld)
+    double *ws;            // workspace PT[ld][nb]
+    int64_t n, p, ld;
+    int32_t nb;            // grid size (CTAs), even
+    int32_t nq_ctas;       // CTAs with the Q role (even); the rest are G-role pairs
+    int32_t nchq;          // chunks of 2048 columns per row
+    int32_t slots_q;       // Q-role TMA ring depth (16 KB slots)
+    size_t smem;
+    PassAArgs a;           // G-row epilogue (g, mu, lam_prev, cone, rho, step, ops, first_inner)
+};
+
 struct LaunchCfg {
     int grid;
     int threads;
@@ -136,6 +151,15 @@ cudaError_t csr_transpose_rows(const int32_t *rp, const int32_t *ci, const doubl
                                int64_t cols, int64_t nnz, int64_t c0, int64_t nc, int32_t **rp_t,
                                int32_t **ci_t, double **va_t, int64_t *nnz_t, cudaStream_t s);
 int csr_group_size(double avg_nnz_per_row);
+
+// kernels_fused.cu
+int fused_q_slots(int64_t ld, int64_t rows_per_q_cta, size_t optin);
+size_t fused_smem_bytes(int64_t ld, int64_t rows_per_q_cta, int slots_q);
+int fused_nchq(int64_t ld);
+cudaError_t configure_fused_kernels(int nchq, size_t smem);
+cudaError_t launch_fused_stream(const FusedArgs &f, cudaStream_t s);
+cudaError_t launch_fused_epi(const PassBArgs &bl, const PassBArgs &bs, const double *ws, int nb, int grid,
+                             cudaStream_t s);
 
 // kernels_small.cu
 size_t small_smem_bytes(int64_t n, int64_t p, int64_t ld, int64_t ldp);

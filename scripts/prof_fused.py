@@ -1,0 +1,11 @@
+import sys, torch
+sys.path.insert(0, ".")
+import qpgen
+from paper_1504_05708_b200 import Solver
+d = qpgen.dense_ineq_torch(16384, 8192, seed=0, shift=0.05)
+st = torch.cuda.Stream()
+s = Solver(d["Q"], d["q"], d["G"], d["g"], d["lb"], d["ub"], d["cone"], rho=1.0, stream=st.cuda_stream, use_graphs=False)
+s.set_constants(47588.0, 1.0)
+s.solve("DFGM", 1, 2)
+torch.cuda.synchronize()
+print("ok")
