@@ -66,8 +66,8 @@ struct duquad_ctx {
     // byte-floor inner step (symmetric Q read once as a triangle, G read once)
     bool fused = false;
     FusedArgs fz{};
-    double *ws = nullptr;
-    int fused_epi_grid = 0;
+    double *ws = nullptr;          // ws_rowp | ws_col | ws_g
+    FusedPiece *fpieces = nullptr;
     // whole-solve single-CTA kernel (small dense QPs)
     bool small = false;
     size_t small_smem = 0;
@@ -142,6 +142,7 @@ void free_all(duquad_ctx *c) {
     if (c->d_ops) cudaFree(c->d_ops);
     if (c->d_j) cudaFree(c->d_j);
     if (c->d_flag) cudaFree(c->d_flag);
+    if (c->fpieces) cudaFree(c->fpieces);
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
 }
@@ -330,7 +331,7 @@ duquad_status outer_phase(duquad_ctx *ctx, const std::vector<double> &beta_in, i
                 CK(launch_fused_stream(fz, ctx->stream));
                 if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 1], ctx->stream));
                 if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 2], ctx->stream));
-                CK(launch_fused_epi(bl, bs, ctx->ws, fz.nb, ctx->fused_epi_grid, ctx->stream));
+                CK(launch_fused_epi(bl, bs, fz, ctx->stream));
                 if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 3], ctx->stream));
             } else {
                 CK(launch_rho0_step(a3, bl, bs, ctx->cfg_k3, ctx->stream));
@@ -360,7 +361,7 @@ duquad_status outer_phase(duquad_ctx *ctx, const std::vector<double> &beta_in, i
             b.beta_in = beta_in[k];
             b.last_inner = (k == Kin);
             if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 2], ctx->stream));
-            CK(launch_fused_epi(b, b, ctx->ws, ctx->fz.nb, ctx->fused_epi_grid, ctx->stream));
+            CK(launch_fused_epi(b, b, ctx->fz, ctx->stream));
             if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 3], ctx->stream));
         }
         return DUQUAD_OK;
@@ -965,40 +966,60 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         ctx->cfg_k3 = {ctx->cfg_b.grid, pass_threads(), smem_a};
         ctx->rho0 = true;
     }
-    if (!batched && ctx->world == 1 && opt.fused_path && n >= 4096) {   // byte-floor inner step
-        const int nchq = fused_nchq(ctx->ld);
-        if (nchq >= 2 && nchq <= 9) {
-            const int nb = ctx->num_sms & ~1;
-            int nq = nb;                        // rho = 0 (K3) or p = 0: Q role only
-            if (!ctx->rho0 && p > 0) {
-                const double bq = 0.5 * (double)n * (double)(n + 1), bg = (double)p * (double)n;
-                nq = 2 * (int)std::llround(0.5 * nb * bq / (bq + bg));
-                nq = std::max(2, std::min(nb - 2, nq));
-            }
-            if (const char *ov = std::getenv("DUQUAD_FUSED_NQ")) nq = std::atoi(ov);   // tuning experiments
-            const int64_t rows_per_q = 2 * (((n + 1) / 2 + nq - 1) / nq);
-            const int slots_q = fused_q_slots(ctx->ld, rows_per_q, prop.sharedMemPerBlockOptin);
-            const size_t fsmem = fused_smem_bytes(ctx->ld, rows_per_q, slots_q);
-            if (slots_q > 0 && fsmem <= (size_t)prop.sharedMemPerBlockOptin) {
-                CKS(dalloc(&ctx->ws, ctx->ld * (int64_t)nb));
-                CKS(configure_fused_kernels(nchq, fsmem));
-                FusedArgs &fz = ctx->fz;
-                fz.Q = ctx->A;
-                fz.G = ctx->A + n * ctx->ld;
-                fz.y = ctx->y_full;
-                fz.ws = ctx->ws;
-                fz.n = n;
-                fz.p = p;
-                fz.ld = ctx->ld;
-                fz.nb = nb;
-                fz.nq_ctas = nq;
-                fz.nchq = nchq;
-                fz.slots_q = slots_q;
-                fz.smem = fsmem;
-                ctx->fused_epi_grid = ctx->num_sms * 8;
-                ctx->fused = true;
-            }
+    if (!batched && ctx->world == 1 && opt.fused_path &&
+        fused_supported(n, ctx->ld, prop.sharedMemPerBlockOptin)) {   // byte-floor inner step
+        int cg = (!ctx->rho0 && p > 0) ? 2 : 1;   // G-role cluster size (pairs: 148 SMs usable)
+        if (const char *ov = std::getenv("DUQUAD_FUSED_CG")) cg = std::atoi(ov) == 4 ? 4 : 2;
+        if (ctx->rho0 || p == 0) cg = 1;
+        const int nchg = cg > 1 ? fused_nchg(ctx->ld, cg) : 0;
+        CKS(configure_fused_kernels(nchg, fused_smem_bytes()));
+        const int maxc = fused_max_clusters(nchg, cg, fused_smem_bytes());
+        const int nb = std::min(ctx->num_sms / cg, maxc > 0 ? maxc : ctx->num_sms / cg) * cg;
+        int nq = nb;                        // rho = 0 (K3) or p = 0: Q role only
+        if (cg > 1) {
+            // Q : G split by bytes, G weighted by its measured per-byte cost (config 2: nq = 72 of 148)
+            double gw = 1.05;
+            if (const char *ov = std::getenv("DUQUAD_FUSED_GW")) gw = std::atof(ov);
+            const double bq = 0.5 * (double)n * (double)(n + 1), bg = gw * (double)p * (double)n;
+            nq = cg * (int)std::llround((double)nb / cg * bq / (bq + bg));
+            nq = std::max(cg, std::min(nb - cg, nq));
         }
+        if (const char *ov = std::getenv("DUQUAD_FUSED_NQ")) {   // tuning experiments
+            const int v = std::atoi(ov) / cg * cg;
+            if (v >= cg && v <= nb && (v < nb || cg == 1)) nq = v;
+        }
+        double row_cost = 32768.0;          // bytes-equivalent cost of one Q row step (latency-bound: ~a full step)
+        if (const char *ov = std::getenv("DUQUAD_FUSED_ROWCOST")) row_cost = std::atof(ov);
+        FusedArgs &fz = ctx->fz;
+        fz.n = n;
+        fz.p = p;
+        fz.ld = ctx->ld;
+        fz.nt = fused_tiles(ctx->ld);
+        fz.cg = std::max(cg, 2);
+        fz.W = fused_block_width(ctx->ld, fz.cg);
+        fz.nchg = nchg;
+        fz.nb = nb;
+        fz.nq_ctas = nq;
+        fz.ng = (nb - nq) / fz.cg;
+        fz.smem = fused_smem_bytes();
+        std::vector<FusedPiece> pcs;
+        fz.cslots = fused_partition(n, ctx->ld, nq, row_cost, pcs, fz.qlo, fz.qhi);
+        const int64_t wrow = (int64_t)fz.nt * 16 * ctx->ld, wcol = (int64_t)nq * fz.cslots * 4096,
+                      wg = (int64_t)fz.ng * ctx->ld;
+        CKS(dalloc(&ctx->ws, wrow + wcol + wg));
+        CKS(dalloc(&ctx->fpieces, (int64_t)nq));
+        CKS(cudaMemcpy(ctx->fpieces, pcs.data(), nq * sizeof(FusedPiece), cudaMemcpyHostToDevice));
+        fz.Q = ctx->A;
+        fz.G = ctx->A + n * ctx->ld;
+        fz.y = ctx->y_full;
+        fz.ws_rowp = ctx->ws;
+        fz.ws_col = ctx->ws + wrow;
+        fz.ws_g = ctx->ws + wrow + wcol;
+        fz.pieces = ctx->fpieces;
+        ctx->fused = true;
+        if (std::getenv("DUQUAD_DEBUG"))
+            fprintf(stderr, "duquad fused: nb %d (max clusters %d) nq %d cg %d ng %d W %d nchg %d nt %d cslots %d\n", nb,
+                    maxc, nq, fz.cg, fz.ng, fz.W, fz.nchg, fz.nt, fz.cslots);
     }
     if (!batched && ctx->world == 1 && opt.small_path) {
         ctx->small_smem = small_smem_bytes(n, p, ctx->ld, ctx->ldp);
@@ -1238,8 +1259,11 @@ duquad_status duquad_solve(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t 
         res->matrix_passes = (int64_t)(K + 1) * Kin * 2;
         const double nn = (double)ctx->n, nl = (double)ctx->nloc, pl = (double)ctx->ploc, pp = (double)ctx->p;
         if (ctx->fused) {      // byte floor: Q triangle (+ G once) streamed, workspace through L2
-            const double tri = 0.5 * nn * (nn + 1.0), wsb = (double)ctx->fz.nb * (double)ctx->ld;
-            res->bytes_pass_a = 8.0 * (tri + (ctx->rho0 ? 0.0 : pp * nn) + nn + wsb);
+            // algorithmic bytes: Q triangle + G once + y; the epilogue: 7 vectors + the partials
+            const double tri = 0.5 * nn * (nn + 1.0);
+            const double wsb = 16.0 * ctx->fz.nt * (double)ctx->ld +
+                               (double)ctx->fz.nq_ctas * ctx->fz.cslots * 4096.0 + (double)ctx->fz.ng * (double)ctx->ld;
+            res->bytes_pass_a = 8.0 * (tri + (ctx->rho0 ? 0.0 : pp * nn) + nn);
             res->bytes_pass_b = 8.0 * (wsb + 8.0 * nn);
             if (ctx->rho0) {
                 res->kernel_launches = 1 + (int64_t)(K + 1) * (2 * Kin + 3);

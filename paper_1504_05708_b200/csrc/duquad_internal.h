@@ -115,16 +115,29 @@ struct SmallArgs {
 };
 
 // ---------------------------------------------------------------- byte-floor inner step
+// Q-role piece: the (tile column, row) triangle sequence from (j0, r0) up to (j1, r1), exclusive.
+struct FusedPiece {
+    int32_t j0, r0, j1, r1;
+};
+constexpr int kFusedMaxTiles = 8;   // tile columns of 4096 (ld <= 32768)
 struct FusedArgs {
     const double *Q;       // [Q] rows of the packed [Q;G] (ld doubles per row)
     const double *G;       // [G] rows
     const double *y;       // y replica (ld)
-    double *ws;            // workspace PT[ld][nb]
+    double *ws_rowp;       // [nt][16][ld] Q row-dot partials per tile column and warp
+    double *ws_col;        // [nq][2][4096] Q column sums per Q CTA and tile-column slot
+    double *ws_g;          // [ng][ld]     G'w partials per G pair
+    int32_t cslots;        // ws_col slots per Q CTA (tile columns a piece spans)
+    const FusedPiece *pieces;   // [nq] (device)
     int64_t n, p, ld;
-    int32_t nb;            // grid size (CTAs), even
-    int32_t nq_ctas;       // CTAs with the Q role (even); the rest are G-role pairs
-    int32_t nchq;          // chunks of 2048 columns per row
-    int32_t slots_q;       // Q-role TMA ring depth (16 KB slots)
+    int32_t nt;            // Q tile columns: [4096 J, min(4096 (J + 1), ld))
+    int32_t cg;            // G-role cluster size (2 or 4)
+    int32_t W;             // G column blocks [c W, (c + 1) W), c < cg (the last ends at ld)
+    int32_t nchg;          // G: chunks of 4096 columns per block (template parameter)
+    int32_t nb;            // grid (CTAs), a multiple of cg
+    int32_t nq_ctas;       // Q-role CTAs (a multiple of cg); the rest are ng G-role clusters
+    int32_t ng;
+    int32_t qlo[kFusedMaxTiles], qhi[kFusedMaxTiles];   // Q CTAs with rows in tile column J
     size_t smem;
     PassAArgs a;           // G-row epilogue (g, mu, lam_prev, cone, rho, step, ops, first_inner)
 };
@@ -153,13 +166,17 @@ cudaError_t csr_transpose_rows(const int32_t *rp, const int32_t *ci, const doubl
 int csr_group_size(double avg_nnz_per_row);
 
 // kernels_fused.cu
-int fused_q_slots(int64_t ld, int64_t rows_per_q_cta, size_t optin);
-size_t fused_smem_bytes(int64_t ld, int64_t rows_per_q_cta, int slots_q);
-int fused_nchq(int64_t ld);
-cudaError_t configure_fused_kernels(int nchq, size_t smem);
+bool fused_supported(int64_t n, int64_t ld, size_t smem_optin);
+int fused_block_width(int64_t ld, int cg);
+int fused_nchg(int64_t ld, int cg);
+int fused_max_clusters(int nchg, int cg, size_t smem);
+int fused_tiles(int64_t ld);
+size_t fused_smem_bytes();
+int fused_partition(int64_t n, int64_t ld, int nq, double row_cost, std::vector<FusedPiece> &pieces,
+                     int32_t *qlo, int32_t *qhi);
+cudaError_t configure_fused_kernels(int nchg, size_t smem);
 cudaError_t launch_fused_stream(const FusedArgs &f, cudaStream_t s);
-cudaError_t launch_fused_epi(const PassBArgs &bl, const PassBArgs &bs, const double *ws, int nb, int grid,
-                             cudaStream_t s);
+cudaError_t launch_fused_epi(const PassBArgs &bl, const PassBArgs &bs, const FusedArgs &f, cudaStream_t s);
 
 // kernels_small.cu
 size_t small_smem_bytes(int64_t n, int64_t p, int64_t ld, int64_t ldp);

@@ -2,28 +2,39 @@
 //
 // The two-pass step streams [Q;G] and G' = 8(n^2 + 2pn) bytes.  The method only needs
 // 8(n(n+1)/2 + pn): Q is symmetric (Hessian) and G can be read once.  One streaming
-// kernel (k_fused_stream) does both, then a small kernel (k_fused_epi) finishes the step:
+// kernel (k_fused_stream) does both, then a small kernel (k_fused_epi) finishes the step.
 //
-//  * Q role (single CTAs): the upper triangle, row by row, in 2048-column chunks moved by TMA
-//    bulk copies (cp.async.bulk + mbarrier ring) into shared memory; y lives in shared memory.
-//    Each element Q_ij (j >= i) is used twice: Q_ij y_j into row i's dot, Q_ij y_i into column j.
-//    Column sums accumulate in registers (thread t owns 4 columns of every chunk); row dots are
-//    warp-reduced per row and parked in shared memory.  Rows are assigned in pairs (i, n-1-i),
-//    so every Q CTA streams the same number of bytes.
-//  * G role (CTA pairs = thread-block clusters of 2 on 2 SMs): each CTA owns one column half.
-//    Per G row: partial dot with y (the CTA's half of y is held in registers), CTA reduction,
-//    exchange of the two half sums through distributed shared memory (st.shared::cluster +
-//    remote mbarrier arrive), then r = G_i y + g_i -> w_i = [mu_i + rho r]_{K°} (the pass-A
-//    epilogue incl. the fused DFOM step) and, with the row still in shared memory,
-//    t += w_i G_i into register column accumulators.  G is read from HBM once.
-//  * Every CTA writes its column sums to a workspace PT[col][cta] (L2-resident, 19 MB at
-//    config 2); k_fused_epi sums the 148 partials of a column in a fixed order and applies the
-//    pass-B epilogue (grad = Qy + t + q, box projection, momentum, average).
-// All sums are in a fixed order, so results are bitwise reproducible (but not bitwise equal to
-// the two-pass path: different summation order; parity with the oracle is ~1e-15).
+// Data movement: every thread prefetches, with cp.async (LDGSTS), exactly the 16-byte pieces of
+// the 4096-column row chunks it will itself consume, 6 chunks ahead (192 KB in flight per SM),
+// into a private shared-memory ring -- the stream needs no barriers at all.  (Measured on B200:
+// such a ring streams at ~7.2 TB/s, while cp.async.bulk (TMA) rings are bound by a per-copy
+// cost: 3.7 TB/s with 8 KB copies, 6.6 TB/s with 16 KB copies.)  Thread t owns columns
+// 2t, 2t+1 (+1024 k) of every chunk: their y values and column sums live in registers.
+// 16 warps, 128 registers per thread; warp 0 also finishes the G rows.
+//
+//  * Q role (single CTAs): the upper triangle in tile columns of 4096, as the sequence
+//    (J, r): J = 0..nt-1, r = 0..min(4096 (J+1), n)-1; row step (J, r) = columns
+//    [max(4096 J, r), 4096 (J+1)) of row r.  Each element Q_rc (c >= r) is used twice: Q_rc y_c
+//    into row r's dot (per-warp sums -> ws_rowp[J][warp][r]; no cross-warp sync) and Q_rc y_r into column c
+//    (registers -> ws_col[cta][J - j0] when the CTA leaves tile column J).  The host cuts the
+//    sequence into pieces of equal estimated time, max(bytes, per-step cost) summed.
+//  * G role (thread-block clusters of cg = 2 or 4 CTAs): rank c owns column block c
+//    ([c W, (c+1) W)) of a range of G rows.  Per row: the block's partial dot -> warp 0 sends it
+//    to every CTA of the cluster through distributed shared memory (st.async with mbarrier
+//    complete_tx), adds the block partials in rank order and applies the pass-A epilogue (w_i =
+//    [mu_i + rho r_i]_{K°}, incl. the fused DFOM step on the first inner step); all warps then
+//    accumulate w_i G_i into register column sums while the row is still in the ring.  The dot
+//    of row i+1 is interleaved with the w G of row i, so the exchange hides under the stream.
+//  * k_fused_epi: grad_j = sum of the partials of column j in a fixed order (+ q_j), then the
+//    pass-B epilogue (box projection, momentum, average).
+// All sums are in a fixed order, so results are bitwise reproducible run to run (but not
+// bitwise equal to the two-pass path: different summation order).
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+
+#include <algorithm>
+#include <vector>
 
 #include "duquad_internal.h"
 #include "epilogue.cuh"
@@ -32,19 +43,19 @@ namespace dq {
 
 namespace {
 
-constexpr int kCons = 512;              // threads (16 warps); warp 15 lane 0 also issues TMA
-constexpr int kThreadsF = kCons;
-constexpr int kChunk = 2048;            // doubles per chunk (16 KB)
-constexpr int kSlotsG = 14;             // G role ring (3.5 half rows of 4 chunks, 224 KB)
+constexpr int kWarps = 16;
+constexpr int kThreadsF = kWarps * 32;  // 4 warps per SMSP, 128 registers
+constexpr int kChunk = 4096;            // columns per chunk (= Q tile width)
+constexpr int kV = 4;                   // double2 per thread per chunk
+constexpr int kSlots = 6;               // per-thread ring depth (chunks; 192 KB per CTA)
+constexpr int kD = 32;                  // depth of the per-row buffers / barriers
+constexpr int kMaxCg = 4;               // G-role cluster size (2 or 4)
+static_assert(kThreadsF * kV * 2 == kChunk, "chunk = 512 threads x 8 doubles");
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -58,23 +69,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "WAITC_%=:\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-// TMA bulk copy global -> own shared memory, completion counted on `bar` (bytes % 16 == 0)
-__device__ __forceinline__ void tma_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -85,19 +79,41 @@ __device__ __forceinline__ uint32_t map_to_cta(uint32_t saddr, uint32_t cta) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(cta));
     return r;
 }
-__device__ __forceinline__ void st_remote_f64(uint32_t raddr, double v) {
-    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(raddr), "d"(v) : "memory");
+// 8 bytes into another CTA's shared memory, completing 8 bytes of transaction count on its mbarrier:
+// data and signal in one asynchronous operation, no fence.  (A remote mbarrier.arrive.release.cluster
+// compiles to MEMBAR.ALL.GPU + ERRBAR -- microseconds per row.)
+__device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr), "l"(
+                     __double_as_longlong(v)),
+                 "r"(rbar)
+                 : "memory");
 }
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t raddr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(raddr) : "memory");
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
 }
-__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kCons) : "memory"); }
+__device__ __forceinline__ void cp16(uint32_t dst, const double *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
-// column of element k (0..3) owned by consumer thread t inside a chunk
-__device__ __forceinline__ int own_col(int t, int k) { return (k >> 1) * 1024 + 2 * t + (k & 1); }
+// column (relative to the chunk base) of element e (0..7) owned by thread t
+__device__ __forceinline__ int own_col(int t, int e) { return (e >> 1) * 1024 + 2 * t + (e & 1); }
+
+// fixed-tree sum of the 16 warp partials held by lanes 0..15
+__device__ __forceinline__ double sum16(double v) {
+    v += __shfl_xor_sync(0xffffffffu, v, 8);
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    return v;
+}
 
 // w_i from r_i = G_i y + g_i: the pass-A epilogue value (epilogue.cuh, epi_a_store) without the
 // store; `write` = this CTA commits mu / lambda (rank 0 of the pair only).
@@ -118,342 +134,360 @@ __device__ __forceinline__ double g_row_w(const PassAArgs &a, int64_t k, double 
     return a.rho > 0.0 ? proj_polar(m + a.rho * r, e.c) : m;
 }
 
-// Producer duty (TMA issue) is carried by lane 0 of warp kProdWarp, interleaved with its
-// consumer work: chunk c + depth is issued right after every warp released chunc c, so the
-// ring stays `depth` chunks ahead.  512 threads -> 128 registers per thread, no spills.
-constexpr int kProdWarp = 15;
+// Q tile column J: columns [a, b), rows 0..rows-1
+struct Tile {
+    int a, b, rows;
+};
+__device__ __forceinline__ Tile tile_of(const FusedArgs &f, int J) {
+    Tile t;
+    t.a = J * kChunk;
+    t.b = t.a + kChunk < (int)f.ld ? t.a + kChunk : (int)f.ld;
+    t.rows = t.b < (int)f.n ? t.b : (int)f.n;
+    return t;
+}
 
-template <int NCHQ, int NCHG>
-__global__ void __launch_bounds__(kCons, 1) __cluster_dims__(2, 1, 1) k_fused_stream(const FusedArgs f) {
+// NCHG: G chunks per column block (0: no G role in this launch -- Q only)
+// Launched with a cluster dimension of 2 when there is a G role (pairs), 1 otherwise.
+template <int NCHG>
+__global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f) {
     extern __shared__ __align__(128) uint8_t fsm[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const bool prod = warp == kProdWarp && lane == 0;
     const int cta = blockIdx.x;
-    const bool q_role = cta < f.nq_ctas;
-    // ---- shared memory carve-up (first KB: barriers and small buffers)
-    uint64_t *full = reinterpret_cast<uint64_t *>(fsm);              // [kSlotsG]
-    uint64_t *empty = full + kSlotsG;                                 // [kSlotsG]
-    uint64_t *xbar = empty + kSlotsG;                                 // [4] pair exchange
-    double *xbuf = reinterpret_cast<double *>(xbar + 4);              // [4]
-    double *red = xbuf + 4;                                           // [2][16]
-    double *ring = reinterpret_cast<double *>(fsm + 1024);            // slots of kChunk doubles
-    const int nsq = f.slots_q;
-    double *ys = ring + (int64_t)nsq * kChunk;                        // Q role: y (ld doubles)
-    double *rowbuf = ys + f.ld;                                       // Q role: [16][16]
-    double *rowsum = rowbuf + 256;                                    // Q role: [rows]
+    // ---- shared memory: barriers + small per-row buffers (first 8 KB), then the ring
+    uint64_t *redbar = reinterpret_cast<uint64_t *>(fsm);  // [kD] 16 warp partials of a G row posted
+    uint64_t *xbar = redbar + kD;                          // [kD] cluster exchange (st.async bytes)
+    uint64_t *wbar = xbar + kD;                            // [kD] w ready (1 arrival)
+    double *red = reinterpret_cast<double *>(fsm + 2048);  // [kD][16]
+    double *xbuf = red + kD * 16;                          // [kD][kMaxCg]
+    double *wbuf = xbuf + kD * kMaxCg;                     // [kD]
+    const double2 *ring = reinterpret_cast<const double2 *>(fsm + 8192) + tid;   // [kSlots][kV][512]
+    const uint32_t ring_u32 = smem_u32(ring);
+    auto slot_addr = [&](int s, int k) -> uint32_t { return ring_u32 + (uint32_t)((s * kV + k) * kThreadsF) * 16; };
 
     if (tid == 0) {
-        for (int s = 0; s < kSlotsG; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kCons / 32);
+        for (int s = 0; s < kD; ++s) {
+            mbar_init(&redbar[s], kWarps);
+            mbar_init(&xbar[s], 1);   // this CTA's expect_tx arrival + cg x 8 bytes of st.async
+            mbar_init(&wbar[s], 1);
         }
-        for (int s = 0; s < 4; ++s) mbar_init(&xbar[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (q_role)
-        for (int64_t i = tid; i < f.ld / 2; i += kCons)
-            reinterpret_cast<double2 *>(ys)[i] = reinterpret_cast<const double2 *>(f.y)[i];
     __syncthreads();
     cluster_sync_all();
 
-    if (q_role) {
-        // rows of this CTA: pairs (i, n-1-i), i = cta, cta + nq, ...  (balanced bytes)
-        const int64_t n = f.n, half = (n + 1) / 2;
-        auto row_of = [&](int64_t idx) -> int64_t {
-            const int64_t pi = cta + (idx >> 1) * f.nq_ctas;
-            return (idx & 1) ? n - 1 - pi : pi;
-        };
-        int64_t nrows = 0;
-        for (int64_t pi = cta; pi < half; pi += f.nq_ctas) nrows += (n - 1 - pi != pi) ? 2 : 1;
-        // producer cursor (row index, chunk) and its ring position
-        int64_t p_idx = 0;
-        int p_m = nrows > 0 ? (int)(row_of(0) / kChunk) : NCHQ;
-        int p_s = 0;
-        uint32_t p_ph = 0;
-        auto produce_one = [&]() {   // issues the next chunk of the sequence, if any
-            if (p_idx >= nrows) return;
-            const int64_t r = row_of(p_idx);
-            const int64_t c0 = (int64_t)p_m * kChunk;
-            const int64_t start = p_m == r / kChunk ? (r & ~1LL) : c0;
-            const int64_t end = c0 + kChunk < f.ld ? c0 + kChunk : f.ld;
-            const uint32_t bytes = (uint32_t)((end - start) * 8);
-            mbar_expect_tx(&full[p_s], bytes);
-            tma_load(ring + p_s * kChunk + (start - c0), f.Q + r * f.ld + start, bytes, &full[p_s]);
-            if (++p_s == nsq) {
-                p_s = 0;
-                p_ph ^= 1u;
-            }
-            if (++p_m == NCHQ) {
-                ++p_idx;
-                p_m = p_idx < nrows ? (int)(row_of(p_idx) / kChunk) : NCHQ;
-            }
-        };
-        if (prod)
-            for (int i = 0; i < nsq; ++i) produce_one();
-        double acc[NCHQ][4];
+    if (NCHG == 0 || cta < f.nq_ctas) {
+        // ================================ Q role: triangle row steps (J, r) of this piece
+        const FusedPiece pc = f.pieces[cta];
+        // prefetch cursor
+        int pJ = pc.j0, pr = pc.r0, ps = 0;
+        Tile pt = tile_of(f, pJ);
+        auto issue = [&]() {
+            if (pJ < pc.j1 || (pJ == pc.j1 && pr < pc.r1)) {
+                const int st = pr > pt.a ? (pr & ~1) : pt.a;
+                const double *row = f.Q + (int64_t)pr * f.ld;
 #pragma unroll
-        for (int m = 0; m < NCHQ; ++m)
+                for (int k = 0; k < kV; ++k) {
+                    const int c = pt.a + 2 * tid + 1024 * k;
+                    if (c + 1 >= st && c < pt.b) cp16(slot_addr(ps, k), row + c);
+                }
+                if (++pr == pt.rows) {
+                    ++pJ;
+                    pr = 0;
+                    pt = tile_of(f, pJ < f.nt ? pJ : 0);
+                }
+            }
+            cp_commit();
+            if (++ps == kSlots) ps = 0;
+        };
+        for (int t = 0; t < kSlots; ++t) issue();
+        int J = pc.j0, r = pc.r0, cs = 0;
+        double yv[8], acc[8];
+        Tile t = tile_of(f, J);
+        auto load_tile = [&]() {
+            t = tile_of(f, J);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) acc[m][k] = 0.0;
-        int s = 0;
-        uint32_t ph = 0;
-        const int ld32 = (int)f.ld;
-        const bool ragged = (f.ld % kChunk) != 0;
-        const double2 *ys2 = reinterpret_cast<const double2 *>(ys);
-        for (int64_t idx = 0; idx < nrows; ++idx) {
-            const int r = (int)row_of(idx);
-            const int m0 = r / kChunk;
-            const double yr = ys[r];
+            for (int e = 0; e < 8; ++e) {
+                const int c = t.a + own_col(tid, e);
+                yv[e] = c < t.b ? f.y[c] : 0.0;
+                acc[e] = 0.0;
+            }
+        };
+        bool live = false;   // yv / acc hold tile column J
+        auto flush_tile = [&]() {
+            if (!live) return;
+            live = false;
+            double *dst = f.ws_col + ((int64_t)cta * f.cslots + (J - pc.j0)) * kChunk;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int c = own_col(tid, e);
+                if (t.a + c < t.b) dst[c] = acc[e];
+            }
+        };
+        // y_r for 32 rows at a time, one per lane (broadcast by shuffle)
+        int ybase = r;
+        double ycache = 0.0;
+        auto load_y = [&]() {
+            ybase = r;
+            ycache = r + lane < t.rows ? f.y[r + lane] : 0.0;
+        };
+        if (J < pc.j1 || (J == pc.j1 && r < pc.r1)) {
+            load_tile();
+            live = true;
+            load_y();
+        }
+        double *rowp = f.ws_rowp + ((int64_t)J * kWarps + warp) * f.ld;   // this warp's row partials
+        while (J < pc.j1 || (J == pc.j1 && r < pc.r1)) {
+            const double yr = __shfl_sync(0xffffffffu, ycache, r - ybase);
+            cp_wait<kSlots - 1>();
+            double q[8];
+#pragma unroll
+            for (int k = 0; k < kV; ++k) {
+                const double2 v = ring[(cs * kV + k) * kThreadsF];
+                q[2 * k] = v.x;
+                q[2 * k + 1] = v.y;
+            }
             double rowacc = 0.0;
+            if (r >= t.a || t.b - t.a < kChunk) {   // diagonal tile / ragged last tile: masks
 #pragma unroll
-            for (int m = 0; m < NCHQ; ++m) {
-                if (m < m0) continue;
-                mbar_wait(&full[s], ph);
-                const double2 *sl2 = reinterpret_cast<const double2 *>(ring + s * kChunk);
-                const double2 qa = sl2[tid], qb = sl2[512 + tid];
-                const int ca = m * kChunk + 2 * tid, cb = ca + 1024;
-                if (m == m0 || (ragged && m == NCHQ - 1)) {      // triangle edge / row end: masks
-                    const double qv[4] = {qa.x, qa.y, qb.x, qb.y};
-                    const int cc[4] = {ca, ca + 1, cb, cb + 1};
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (cc[k] >= r && cc[k] < ld32) {
-                            rowacc = fma(qv[k], ys[cc[k]], rowacc);
-                            if (cc[k] > r) acc[m][k] = fma(qv[k], yr, acc[m][k]);
-                        }
-                } else {                                          // interior chunk: no masks
-                    const double2 ya = ys2[ca >> 1], yb = ys2[cb >> 1];
-                    rowacc = fma(qa.x, ya.x, rowacc);
-                    rowacc = fma(qa.y, ya.y, rowacc);
-                    rowacc = fma(qb.x, yb.x, rowacc);
-                    rowacc = fma(qb.y, yb.y, rowacc);
-                    acc[m][0] = fma(qa.x, yr, acc[m][0]);
-                    acc[m][1] = fma(qa.y, yr, acc[m][1]);
-                    acc[m][2] = fma(qb.x, yr, acc[m][2]);
-                    acc[m][3] = fma(qb.y, yr, acc[m][3]);
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[s]);
-                if (prod) {                                       // refill this slot
-                    mbar_wait(&empty[s], ph);
-                    produce_one();
-                }
-                if (++s == nsq) {
-                    s = 0;
-                    ph ^= 1u;
-                }
-            }
-            rowacc = warp_sum(rowacc);
-            const int slot = (int)(idx & 15);
-            if (lane == 0) rowbuf[slot * 16 + warp] = rowacc;
-            if (slot == 15 || idx == nrows - 1) {   // flush: row dots of the last <= 16 rows
-                consumer_bar();
-                if (tid <= slot) {
-                    double sr = 0.0;
-#pragma unroll
-                    for (int w = 0; w < 16; ++w) sr += rowbuf[tid * 16 + w];
-                    rowsum[idx - slot + tid] = sr;
-                }
-                consumer_bar();
-            }
-        }
-        // column sums -> workspace (this CTA's column of PT)
-        double *pt = f.ws;
-#pragma unroll
-        for (int m = 0; m < NCHQ; ++m)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int64_t c = (int64_t)m * kChunk + own_col(tid, k);
-                if (c < f.ld) pt[c * f.nb + cta] = acc[m][k];
-            }
-        consumer_bar();
-        for (int64_t idx = tid; idx < nrows; idx += kCons) pt[row_of(idx) * f.nb + cta] += rowsum[idx];
-    } else {
-        // ---- G role: pair g owns rows [g0, g1); this CTA the column half `half_id`.
-        // Per row: A = half sums (half 1 sends its sum to half 0); B = half 0 forms r, the
-        // epilogue and w (and commits mu / lambda), sends w to half 1; both then accumulate
-        // w G_i.  Software-pipelined: A(i+1) runs before B(i), hiding the exchange latency.
-        const uint32_t half_id = cluster_rank();
-        const bool h0 = half_id == 0;
-        const int g = (cta - f.nq_ctas) >> 1;
-        const int ng = (gridDim.x - f.nq_ctas) >> 1;
-        const int64_t g0 = f.p * g / ng, g1 = f.p * (g + 1) / ng, nrow = g1 - g0;
-        const int chunk0 = (int)half_id * NCHG;
-        const int64_t nseq = nrow * NCHG;
-        int64_t p_seq = 0;
-        auto produce_one = [&]() {
-            if (p_seq >= nseq) return;
-            const int ps = (int)(p_seq % kSlotsG);
-            const int64_t i = g0 + p_seq / NCHG;
-            const int m = (int)(p_seq % NCHG);
-            ++p_seq;
-            const int64_t c0 = (int64_t)(chunk0 + m) * kChunk;
-            const int64_t end = c0 + kChunk < f.ld ? c0 + kChunk : f.ld;
-            if (end <= c0) {                   // chunk past the row end: an empty phase
-                mbar_arrive(&full[ps]);
-                return;
-            }
-            const uint32_t bytes = (uint32_t)((end - c0) * 8);
-            mbar_expect_tx(&full[ps], bytes);
-            tma_load(ring + ps * kChunk, f.G + i * f.ld + c0, bytes, &full[ps]);
-        };
-        if (prod)
-            for (int i = 0; i < kSlotsG; ++i) produce_one();
-        double yv[NCHG][4], acc[NCHG][4];
-#pragma unroll
-        for (int m = 0; m < NCHG; ++m)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int64_t c = (int64_t)(chunk0 + m) * kChunk + own_col(tid, k);
-                yv[m][k] = c < f.ld ? f.y[c] : 0.0;
-                acc[m][k] = 0.0;
-            }
-        const uint32_t x_remote = map_to_cta(smem_u32(xbuf), half_id ^ 1u);
-        const uint32_t xb_remote = map_to_cta(smem_u32(xbar), half_id ^ 1u);
-        const OuterA o = outer_a(f.a, MODE_SOLVE);
-        const bool ragged_g = (int64_t)(chunk0 + NCHG) * kChunk > f.ld;
-        auto stage_a = [&](int64_t it) -> double {     // this half's sum of row g0 + it
-            double part = 0.0;
-            int s = (int)((it * NCHG) % kSlotsG);
-            uint32_t ph = (uint32_t)(((it * NCHG) / kSlotsG) & 1);
-#pragma unroll
-            for (int m = 0; m < NCHG; ++m) {
-                mbar_wait(&full[s], ph);
-                const double2 *sl2 = reinterpret_cast<const double2 *>(ring + s * kChunk);
-                const double2 qa = sl2[tid], qb = sl2[512 + tid];
-                if (ragged_g) {
-                    const double qv[4] = {qa.x, qa.y, qb.x, qb.y};
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if ((int64_t)(chunk0 + m) * kChunk + own_col(tid, k) < f.ld)
-                            part = fma(qv[k], yv[m][k], part);
-                } else {
-                    part = fma(qa.x, yv[m][0], part);
-                    part = fma(qa.y, yv[m][1], part);
-                    part = fma(qb.x, yv[m][2], part);
-                    part = fma(qb.y, yv[m][3], part);
-                }
-                if (++s == kSlotsG) {
-                    s = 0;
-                    ph ^= 1u;
-                }
-            }
-            part = warp_sum(part);
-            if (lane == 0) red[(it & 1) * 16 + warp] = part;
-            consumer_bar();
-            double mine = 0.0;
-#pragma unroll
-            for (int w = 0; w < 16; ++w) mine += red[(it & 1) * 16 + w];
-            if (!h0 && tid == 0) {
-                st_remote_f64(x_remote + (uint32_t)(it & 3) * 8, mine);
-                mbar_arrive_remote(xb_remote + (uint32_t)(it & 3) * 8);
-            }
-            return mine;
-        };
-        EpiA e_cur{}, e_next{};
-        double mine_cur = 0.0;
-        if (nrow > 0) {
-            if (h0) e_cur = epi_a_load(f.a, MODE_SOLVE, f.a.nq + g0, o);
-            mine_cur = stage_a(0);
-        }
-        for (int64_t it = 0; it < nrow; ++it) {
-            double mine_next = 0.0;
-            if (it + 1 < nrow) {
-                if (h0) e_next = epi_a_load(f.a, MODE_SOLVE, f.a.nq + g0 + it + 1, o);
-                mine_next = stage_a(it + 1);
-            }
-            // stage B(it)
-            mbar_wait_cluster(&xbar[it & 3], (uint32_t)((it >> 2) & 1));
-            double w;
-            if (h0) {
-                const double s_row = mine_cur + xbuf[it & 3];     // half 0 + half 1
-                w = g_row_w(f.a, g0 + it, s_row, e_cur, o, tid == 0);
-                if (tid == 0) {
-                    st_remote_f64(x_remote + (uint32_t)(it & 3) * 8, w);
-                    mbar_arrive_remote(xb_remote + (uint32_t)(it & 3) * 8);
+                for (int e = 0; e < 8; ++e) {
+                    const int c = t.a + own_col(tid, e);
+                    if (c >= r && c < t.b) {
+                        rowacc = fma(q[e], yv[e], rowacc);
+                        if (c > r) acc[e] = fma(q[e], yr, acc[e]);
+                    }
                 }
             } else {
-                w = xbuf[it & 3];
-            }
-            int s = (int)((it * NCHG) % kSlotsG);
-            uint32_t ph = (uint32_t)(((it * NCHG) / kSlotsG) & 1);
 #pragma unroll
-            for (int m = 0; m < NCHG; ++m) {
-                const double2 *sl2 = reinterpret_cast<const double2 *>(ring + s * kChunk);
-                const double2 qa = sl2[tid], qb = sl2[512 + tid];
-                const double qv[4] = {qa.x, qa.y, qb.x, qb.y};
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (!ragged_g || (int64_t)(chunk0 + m) * kChunk + own_col(tid, k) < f.ld)
-                        acc[m][k] = fma(w, qv[k], acc[m][k]);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[s]);
-                if (prod) {                                       // refill this slot
-                    mbar_wait(&empty[s], ph);
-                    produce_one();
-                }
-                if (++s == kSlotsG) {
-                    s = 0;
-                    ph ^= 1u;
+                for (int e = 0; e < 8; ++e) {
+                    rowacc = fma(q[e], yv[e], rowacc);
+                    acc[e] = fma(q[e], yr, acc[e]);
                 }
             }
-            e_cur = e_next;
-            mine_cur = mine_next;
+            issue();   // refill this slot kSlots steps ahead
+            if (++cs == kSlots) cs = 0;
+            rowacc = warp_sum(rowacc);
+            if (lane == 0) rowp[r] = rowacc;
+            if (++r == t.rows) {
+                flush_tile();
+                ++J;
+                r = 0;
+                if (J < pc.j1 || (J == pc.j1 && r < pc.r1)) {
+                    load_tile();
+                    live = true;
+                    load_y();
+                    rowp = f.ws_rowp + ((int64_t)J * kWarps + warp) * f.ld;
+                }
+            } else if (r - ybase == 32) {
+                load_y();
+            }
         }
-        // column sums of this half -> workspace; zeros for the other half
-        double *pt = f.ws;
+        flush_tile();
+        cp_wait<0>();
+    } else if constexpr (NCHG > 0) {
+        // ================================ G role: pair gi owns rows [g0, g1); this CTA block `rank`
+        const uint32_t rank = cluster_rank();
+        const int a = (int)rank * f.W, b = (int)rank + 1 == f.cg ? (int)f.ld : a + f.W;
+        const int nch = (b - a + kChunk - 1) / kChunk;
+        const bool ragged = ((b - a) % kChunk) != 0;
+        const int gi = (cta - f.nq_ctas) / f.cg;
+        const int64_t g0 = f.p * gi / f.ng, g1 = f.p * (gi + 1) / f.ng;
+        const int nr = (int)(g1 - g0);
+        int p_it = 0, p_m = 0, ps = 0;   // prefetch cursor
+        auto issue = [&]() {
+            if (p_it < nr) {
+                const double *row = f.G + (g0 + p_it) * f.ld;
+#pragma unroll
+                for (int k = 0; k < kV; ++k) {
+                    const int c = a + p_m * kChunk + 2 * tid + 1024 * k;
+                    if (c < b) cp16(slot_addr(ps, k), row + c);
+                }
+                if (++p_m == nch) {
+                    p_m = 0;
+                    ++p_it;
+                }
+            }
+            cp_commit();
+            if (++ps == kSlots) ps = 0;
+        };
+        for (int t = 0; t < kSlots; ++t) issue();
+        double yv[NCHG][8], acc[NCHG][8];
 #pragma unroll
         for (int m = 0; m < NCHG; ++m)
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int64_t c = (int64_t)(chunk0 + m) * kChunk + own_col(tid, k);
-                const int64_t co = (int64_t)((half_id ^ 1) * NCHG + m) * kChunk + own_col(tid, k);
-                if (c < f.ld) pt[c * f.nb + cta] = acc[m][k];
-                if (co < f.ld) pt[co * f.nb + cta] = 0.0;
+            for (int e = 0; e < 8; ++e) {
+                const int c = a + m * kChunk + own_col(tid, e);
+                yv[m][e] = (m < nch && c < b) ? f.y[c] : 0.0;
+                acc[m][e] = 0.0;
+            }
+        // A cursor (row dots) runs one row ahead of the B cursor (w G; frees the slot)
+        int sa = 0, sb = 0;
+        auto dot_chunk = [&](int m, double part) -> double {
+            cp_wait<kSlots - 1 - NCHG>();
+#pragma unroll
+            for (int k = 0; k < kV; ++k) {
+                const double2 v = ring[(sa * kV + k) * kThreadsF];
+                if (ragged && m == nch - 1) {
+                    const int c = a + m * kChunk + 2 * tid + 1024 * k;
+                    if (c < b) {
+                        part = fma(v.x, yv[m][2 * k], part);
+                        part = fma(v.y, yv[m][2 * k + 1], part);
+                    }
+                } else {
+                    part = fma(v.x, yv[m][2 * k], part);
+                    part = fma(v.y, yv[m][2 * k + 1], part);
+                }
+            }
+            if (++sa == kSlots) sa = 0;
+            return part;
+        };
+        auto post = [&](int it, double part) {
+            part = warp_sum(part);
+            if (lane == 0) {
+                const int d = it % kD;
+                red[d * 16 + warp] = part;
+                mbar_arrive(&redbar[d]);
+            }
+        };
+        // warp 0: finishes row `it` -- CTA sum, cluster exchange through DSMEM, w (pass-A epilogue)
+        const OuterA o = outer_a(f.a, MODE_SOLVE);
+        const uint32_t xb_r = map_to_cta(smem_u32(xbuf), (uint32_t)(lane % f.cg));
+        const uint32_t xm_r = map_to_cta(smem_u32(xbar), (uint32_t)(lane % f.cg));
+        EpiA e_next{};
+        if (warp == 0 && lane == 0 && nr > 0) e_next = epi_a_load(f.a, MODE_SOLVE, f.a.nq + g0, o);
+        auto exchange = [&](int it) {
+            const EpiA e = e_next;
+            if (lane == 0 && it + 1 < nr) e_next = epi_a_load(f.a, MODE_SOLVE, f.a.nq + g0 + it + 1, o);
+            const int d = it % kD;
+            const uint32_t par = (uint32_t)((it / kD) & 1);
+            mbar_wait(&redbar[d], par);
+            double v = lane < 16 ? red[d * 16 + lane] : 0.0;
+            v = sum16(v);
+            if (lane < f.cg)   // lane c: this block's partial -> CTA c of the cluster
+                st_async_f64(xb_r + (uint32_t)(d * kMaxCg + rank) * 8, v, xm_r + (uint32_t)d * 8);
+            if (lane == 0) mbar_arrive_expect_tx(&xbar[d], (uint32_t)(8 * f.cg));
+            mbar_wait(&xbar[d], par);
+            if (lane == 0) {
+                double s_row = xbuf[d * kMaxCg];   // block partials added in rank order
+                for (int c = 1; c < f.cg; ++c) s_row += xbuf[d * kMaxCg + c];
+                wbuf[d] = g_row_w(f.a, g0 + it, s_row, e, o, rank == 0);
+                mbar_arrive(&wbar[d]);
+            }
+            __syncwarp();
+        };
+        if (nr > 0) {
+            double part = 0.0;
+#pragma unroll
+            for (int m = 0; m < NCHG; ++m)
+                if (m < nch) part = dot_chunk(m, part);
+            post(0, part);
+        }
+        for (int it = 0; it < nr; ++it) {
+            const bool nxt = it + 1 < nr;
+            double part = 0.0, w = 0.0;
+#pragma unroll
+            for (int m = 0; m < NCHG; ++m) {
+                if (m >= nch) continue;
+                if (nxt) part = dot_chunk(m, part);                       // A(it + 1, m)
+                if (m == 0) {
+                    if (warp == 0) exchange(it);
+                    const int d = it % kD;
+                    mbar_wait(&wbar[d], (uint32_t)((it / kD) & 1));
+                    w = wbuf[d];
+                }
+#pragma unroll
+                for (int k = 0; k < kV; ++k) {                              // B(it, m)
+                    const double2 v = ring[(sb * kV + k) * kThreadsF];
+                    acc[m][2 * k] = fma(w, v.x, acc[m][2 * k]);
+                    acc[m][2 * k + 1] = fma(w, v.y, acc[m][2 * k + 1]);
+                }
+                issue();   // the slot of B(it, m) is free: refill it
+                if (++sb == kSlots) sb = 0;
+            }
+            if (nxt) post(it + 1, part);
+        }
+        cp_wait<0>();
+        double *pt = f.ws_g + (int64_t)gi * f.ld;
+#pragma unroll
+        for (int m = 0; m < NCHG; ++m)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int c = a + m * kChunk + own_col(tid, e);
+                if (m < nch && c < b) pt[c] = acc[m][e];
             }
     }
     __syncthreads();
     cluster_sync_all();   // no CTA leaves while its partner may still write its shared memory
 }
 
-// grad_j = sum_b PT[j][b] (= Qy_j + t_j) + q_j: the pass-B epilogue, one warp per row j.
-// bl / bs: epilogue views for load / store (they differ only in y when y ping-pongs).
-__global__ void __launch_bounds__(256) k_fused_epi(const PassBArgs bl, const PassBArgs bs,
-                                                   const double *__restrict__ ws, int nb) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
-    const double avg_w = avg_weight(bl, MODE_SOLVE);
-    for (int64_t j = warp; j < bl.nrows; j += nwarps) {
-        EpiB e{};
-        if (lane == 0) e = epi_b_load(bl, MODE_SOLVE, j, avg_w);
-        double s = 0.0;
-        for (int c = lane; c < nb; c += 32) s += ws[j * nb + c];
-        s = warp_sum(s);
-        if (lane == 0) {
-            e.qy = s;
-            epi_b_store(bs, MODE_SOLVE, j, 0.0, e, avg_w);
+// grad_j = sum of the partials of column j (fixed order) + q_j: the pass-B epilogue.
+// Block: 32 columns x 8 slices; slice s sums list entries s, s + 8, ...; the 8 slice sums are
+// added in slice order.  List of column j (tile column Jc = j / 4096):
+//   ws_rowp[J][w][j] for J = Jc..nt-1, w = 0..15, then ws_col[c][Jc - j0(c)][j - 4096 Jc] for the Q CTAs c
+//   with rows in tile column Jc, then ws_g[g][j] for the G pairs g.
+constexpr int kEpiCols = 32, kEpiSlices = 8;
+__global__ void __launch_bounds__(kEpiCols *kEpiSlices) k_fused_epi(const PassBArgs bl, const PassBArgs bs,
+                                                                    const FusedArgs f) {
+    __shared__ double part[kEpiSlices][kEpiCols];
+    const int cl = threadIdx.x % kEpiCols, sl = threadIdx.x / kEpiCols;
+    const int64_t j = (int64_t)blockIdx.x * kEpiCols + cl;
+    double s = 0.0;
+    if (j < bl.nrows) {
+        const int Jc = (int)(j / kChunk);
+        const int nrow = (f.nt - Jc) * kWarps;
+        const int lo = f.qlo[Jc], nqc = f.qhi[Jc] - f.qlo[Jc];
+        const int64_t jr = j - (int64_t)Jc * kChunk;
+        const int len = nrow + nqc + f.ng;
+        for (int t = sl; t < len; t += kEpiSlices) {
+            const double *src;
+            if (t < nrow) {
+                src = f.ws_rowp + ((int64_t)Jc * kWarps + t) * f.ld + j;
+            } else if (t < nrow + nqc) {
+                const int c = lo + (t - nrow);
+                src = f.ws_col + ((int64_t)c * f.cslots + (Jc - f.pieces[c].j0)) * kChunk + jr;
+            } else {
+                src = f.ws_g + (int64_t)(t - nrow - nqc) * f.ld + j;
+            }
+            s += *src;
         }
+    }
+    part[sl][cl] = s;
+    __syncthreads();
+    if (sl == 0 && j < bl.nrows) {
+        double t = part[0][cl];
+#pragma unroll
+        for (int q = 1; q < kEpiSlices; ++q) t += part[q][cl];
+        const double avg_w = avg_weight(bl, MODE_SOLVE);
+        EpiB e = epi_b_load(bl, MODE_SOLVE, j, avg_w);
+        e.qy = t;
+        epi_b_store(bs, MODE_SOLVE, j, 0.0, e, avg_w);
     }
 }
 
-template <int NCHQ>
+template <int NCHG>
 cudaError_t launch_t(const FusedArgs &f, cudaStream_t s) {
-    constexpr int NCHG = (NCHQ + 1) / 2;
-    k_fused_stream<NCHQ, NCHG><<<f.nb, kThreadsF, f.smem, s>>>(f);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(f.nb);
+    cfg.blockDim = dim3(kThreadsF);
+    cfg.dynamicSmemBytes = f.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = NCHG > 0 ? f.cg : 1;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_fused_stream<NCHG>, f);
 }
 
-template <int NCHQ>
+template <int NCHG>
 cudaError_t configure_t(size_t smem) {
-    constexpr int NCHG = (NCHQ + 1) / 2;
-    cudaError_t e = cudaFuncSetAttribute(k_fused_stream<NCHQ, NCHG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_fused_stream<NCHG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e) return e;
     cudaFuncAttributes fa;
-    if ((e = cudaFuncGetAttributes(&fa, k_fused_stream<NCHQ, NCHG>))) return e;
+    if ((e = cudaFuncGetAttributes(&fa, k_fused_stream<NCHG>))) return e;
     if (fa.maxThreadsPerBlock < kThreadsF) {
-        fprintf(stderr, "k_fused_stream<%d>: %d regs, maxThreadsPerBlock %d, local %zu\n", NCHQ, fa.numRegs,
+        fprintf(stderr, "k_fused_stream<%d>: %d regs, maxThreadsPerBlock %d, local %zu\n", NCHG, fa.numRegs,
                 fa.maxThreadsPerBlock, fa.localSizeBytes);
         return cudaErrorInvalidConfiguration;
     }
@@ -462,54 +496,127 @@ cudaError_t configure_t(size_t smem) {
 
 }  // namespace
 
-// Q-role ring slots that fit next to y and the row buffers in `optin` bytes (0: does not fit).
-int fused_q_slots(int64_t ld, int64_t rows_per_q_cta, size_t optin) {
-    const int64_t fixed = 1024 + ld * 8 + 256 * 8 + rows_per_q_cta * 8;
-    const int64_t s = ((int64_t)optin - fixed) / (kChunk * 8);
-    return s < 3 ? 0 : (s > 8 ? 8 : (int)s);
+int fused_block_width(int64_t ld, int cg) { return (int)((ld + 32 * cg - 1) / (32 * cg) * 32); }
+int fused_nchg(int64_t ld, int cg) { return (fused_block_width(ld, cg) + kChunk - 1) / kChunk; }
+int fused_tiles(int64_t ld) { return (int)((ld + kChunk - 1) / kChunk); }
+size_t fused_smem_bytes() { return 8192 + (size_t)kSlots * kChunk * 8; }
+bool fused_supported(int64_t n, int64_t ld, size_t smem_optin) {
+    return n >= 4096 && fused_nchg(ld, 4) <= 2 && fused_tiles(ld) <= kFusedMaxTiles && fused_smem_bytes() <= smem_optin;
 }
 
-// Shared memory of the stream kernel: barriers (1 KB) + max(Q role: ring + y + row buffers,
-// G role: 14-slot ring).
-size_t fused_smem_bytes(int64_t ld, int64_t rows_per_q_cta, int slots_q) {
-    const size_t q = (size_t)slots_q * kChunk * 8 + (size_t)ld * 8 + 256 * 8 + (size_t)rows_per_q_cta * 8;
-    const size_t g = (size_t)kSlotsG * kChunk * 8;
-    return 1024 + (q > g ? q : g);
+// Clusters of `cg` CTAs of the stream kernel that can be resident at once (0 on error).
+int fused_max_clusters(int nchg, int cg, size_t smem) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(cg * 256);
+    cfg.blockDim = dim3(kThreadsF);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cg;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    cudaError_t e;
+    switch (nchg) {
+        case 0: e = cudaOccupancyMaxActiveClusters(&n, k_fused_stream<0>, &cfg); break;
+        case 1: e = cudaOccupancyMaxActiveClusters(&n, k_fused_stream<1>, &cfg); break;
+        case 2: e = cudaOccupancyMaxActiveClusters(&n, k_fused_stream<2>, &cfg); break;
+        default: return 0;
+    }
+    return e == cudaSuccess ? n : 0;
 }
 
-int fused_nchq(int64_t ld) { return (int)((ld + kChunk - 1) / kChunk); }
+// Cut of the Q triangle sequence (J, r) into nq pieces of equal estimated time: a row step costs
+// max(bytes, row_cost) (the per-step instruction cost dominates short steps near the diagonal).
+// qlo / qhi: the pieces with rows in each tile column; returns the most tile columns a piece spans.
+int fused_partition(int64_t n, int64_t ld, int nq, double row_cost, std::vector<FusedPiece> &pieces,
+                    int32_t *qlo, int32_t *qhi) {
+    const int nt = fused_tiles(ld);
+    auto rows = [&](int J) -> int64_t { return std::min<int64_t>(std::min<int64_t>((int64_t)(J + 1) * kChunk, ld), n); };
+    auto cost = [&](int J, int64_t r) -> double {
+        const int64_t a = (int64_t)J * kChunk, b = std::min<int64_t>(a + kChunk, ld);
+        const int64_t st = r > a ? (r & ~1LL) : a;
+        return std::max(8.0 * (double)(b - st), row_cost);
+    };
+    double total = 0.0;
+    for (int J = 0; J < nt; ++J)
+        for (int64_t r = 0; r < rows(J); ++r) total += cost(J, r);
+    pieces.assign(nq, FusedPiece{0, 0, 0, 0});
+    int J = 0;
+    int64_t r = 0;
+    double acc = 0.0;
+    auto norm = [&]() {   // (J, r) past the end of tile column J -> next
+        while (J < nt && r >= rows(J)) {
+            ++J;
+            r = 0;
+        }
+    };
+    for (int c = 0; c < nq; ++c) {
+        norm();
+        pieces[c].j0 = J < nt ? J : nt - 1;
+        pieces[c].r0 = J < nt ? (int32_t)r : (int32_t)rows(nt - 1);
+        const double target = total * (c + 1) / nq;
+        while (J < nt && (c == nq - 1 || acc + 0.5 * cost(J, r) < target)) {
+            acc += cost(J, r);
+            ++r;
+            norm();
+        }
+        // exclusive end (j1, r1): r1 may equal rows(j1) only for the very end of the sequence
+        if (J < nt) {
+            pieces[c].j1 = J;
+            pieces[c].r1 = (int32_t)r;
+        } else {
+            pieces[c].j1 = nt - 1;
+            pieces[c].r1 = (int32_t)rows(nt - 1);
+        }
+    }
+    int span = 1;
+    for (int b = 0; b < kFusedMaxTiles; ++b) {
+        qlo[b] = nq;
+        qhi[b] = 0;
+    }
+    for (int c = 0; c < nq; ++c) {
+        const FusedPiece &p = pieces[c];
+        for (int b = p.j0; b <= p.j1 && b < nt; ++b) {
+            const int64_t r0 = b == p.j0 ? p.r0 : 0;
+            const int64_t r1 = b == p.j1 ? p.r1 : rows(b);
+            if (r1 > r0) {
+                qlo[b] = std::min(qlo[b], c);
+                qhi[b] = std::max(qhi[b], c + 1);
+                span = std::max(span, b - p.j0 + 1);
+            }
+        }
+    }
+    for (int b = 0; b < kFusedMaxTiles; ++b)
+        if (qhi[b] <= qlo[b]) qlo[b] = qhi[b] = 0;
+    return span;
+}
 
-cudaError_t configure_fused_kernels(int nchq, size_t smem) {
-    switch (nchq) {
+cudaError_t configure_fused_kernels(int nchg, size_t smem) {
+    cudaError_t e = configure_t<0>(smem);
+    if (e) return e;
+    switch (nchg) {
+        case 0: return cudaSuccess;
+        case 1: return configure_t<1>(smem);
         case 2: return configure_t<2>(smem);
-        case 3: return configure_t<3>(smem);
-        case 4: return configure_t<4>(smem);
-        case 5: return configure_t<5>(smem);
-        case 6: return configure_t<6>(smem);
-        case 7: return configure_t<7>(smem);
-        case 8: return configure_t<8>(smem);
-        case 9: return configure_t<9>(smem);
         default: return cudaErrorInvalidValue;
     }
 }
 
 cudaError_t launch_fused_stream(const FusedArgs &f, cudaStream_t s) {
-    switch (f.nchq) {
+    if (f.nq_ctas == f.nb) return launch_t<0>(f, s);
+    switch (f.nchg) {
+        case 1: return launch_t<1>(f, s);
         case 2: return launch_t<2>(f, s);
-        case 3: return launch_t<3>(f, s);
-        case 4: return launch_t<4>(f, s);
-        case 5: return launch_t<5>(f, s);
-        case 6: return launch_t<6>(f, s);
-        case 7: return launch_t<7>(f, s);
-        case 8: return launch_t<8>(f, s);
-        case 9: return launch_t<9>(f, s);
         default: return cudaErrorInvalidValue;
     }
 }
 
-cudaError_t launch_fused_epi(const PassBArgs &bl, const PassBArgs &bs, const double *ws, int nb, int grid,
-                             cudaStream_t s) {
-    k_fused_epi<<<grid, 256, 0, s>>>(bl, bs, ws, nb);
+cudaError_t launch_fused_epi(const PassBArgs &bl, const PassBArgs &bs, const FusedArgs &f, cudaStream_t s) {
+    const int grid = (int)((bl.nrows + kEpiCols - 1) / kEpiCols);
+    if (grid > 0) k_fused_epi<<<grid, kEpiCols * kEpiSlices, 0, s>>>(bl, bs, f);
     return cudaGetLastError();
 }
 

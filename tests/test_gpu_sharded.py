@@ -54,7 +54,7 @@ def _run_sharded(torch, args, P, rho, alg, K, Kin, L_in, L_d, trace=False, **kw)
 
 def _run_single(torch, args, rho, alg, K, Kin, L_in, L_d, trace=False, **kw):
     from paper_1504_05708_b200 import Solver
-    s = Solver(*args, rho=rho, small_path=False, **kw)
+    s = Solver(*args, rho=rho, small_path=False, fused_path=False, **kw)
     s.set_constants(L_in, L_d)
     if trace:
         tl = torch.zeros((K, max(s.p, 1)), dtype=torch.float64, device="cuda")
