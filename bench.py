@@ -259,13 +259,16 @@ def main():
     peak, peak_src = _peaks()
     ach_a = bytes_a / (ms_a / 1000.0) / 1e9
     ach_b = bytes_b / (ms_b / 1000.0) / 1e9
+    fused = infos[0]["path"] == 1          # DUQUAD_PATH_BYTE_FLOOR
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get("pass_a_dram_bytes")
+            tj = json.load(f)
+            traffic = tj.get("fused_stream_dram_bytes" if fused else "pass_a_dram_bytes")
     except Exception:
         pass
-    step_bytes = 8.0 * (n * n + 2.0 * p * n)
+    step_bytes = 8.0 * (n * n + 2.0 * p * n)                       # north_star layout: [Q;G] + G'
+    floor_bytes = 8.0 * (n * (n + 1) / 2.0 + p * n)                 # method floor: Q triangle + G once
     ms_step = ms_max / args.steps
 
     # ---- end-to-end through the C ABI with host buffers (pinned), copies inside the timed region
@@ -306,15 +309,23 @@ def main():
             "data": "synthetic (qpgen.dense_ineq_torch seed 0, config-2 recipe)",
             "config": dict(workload, parallelism=f"row-shard x{world}" if world > 1 else "single GPU"),
             "solves_per_s": args.steps / (ms_max / 1000.0),
-            "step_hbm_gbs": step_bytes / (ms_step / 1000.0 / inner_per_solve) / 1e9,
-            "roofline": {"bound": "hbm", "kernel": "k_pass_a (stream [Q;G] . y, fused w / dual epilogue)",
+            "path": _lib.PATHS.get(infos[0]["path"], str(infos[0]["path"])),
+            "step_hbm_gbs": {"north_star_bytes": step_bytes / (ms_step / 1000.0 / inner_per_solve) / 1e9,
+                             "floor_bytes": floor_bytes / (ms_step / 1000.0 / inner_per_solve) / 1e9,
+                             "note": "whole inner step (all kernels) at 8(n^2+2pn) resp. 8(n(n+1)/2+pn) bytes"},
+            "roofline": {"bound": "hbm",
+                         "kernel": ("k_fused_stream (Q upper triangle + G read once; row dots, DFOM/w "
+                                    "epilogue, G'w column sums)") if fused else
+                                   "k_pass_a (stream [Q;G] . y, fused w / dual epilogue)",
                          "achieved": ach_a, "peak": peak, "unit": "GB/s", "frac": ach_a / peak,
                          "traffic": traffic, "bytes_per_launch": bytes_a, "ms_per_launch": ms_a,
                          "peak_source": peak_src,
-                         "pass_b": {"achieved": ach_b, "frac": ach_b / peak, "bytes_per_launch": bytes_b,
-                                    "ms_per_launch": ms_b},
-                         "share_of_step": {"pass_a": ms_a * inner_per_solve / ms_step,
-                                           "pass_b": ms_b * inner_per_solve / ms_step}},
+                         ("epilogue" if fused else "pass_b"): {
+                             "kernel": "k_fused_epi" if fused else "k_pass_b",
+                             "achieved": ach_b, "frac": ach_b / peak, "bytes_per_launch": bytes_b,
+                             "ms_per_launch": ms_b},
+                         "share_of_step": {"stream" if fused else "pass_a": ms_a * inner_per_solve / ms_step,
+                                           "epilogue" if fused else "pass_b": ms_b * inner_per_solve / ms_step}},
             "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "constants": {"L_in": L_in, "L_d": L_d, "normG2": normG2},
             "cpu_baseline": cpu,

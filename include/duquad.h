@@ -156,7 +156,25 @@ typedef struct {
     double bytes_pass_b;        /* algorithmic bytes per pass-B launch                    */
     double flops_pass_a;        /* algorithmic flops per pass-A launch (2 per multiply-add) */
     double flops_pass_b;
+    int32_t path;               /* duquad_path: which kernels ran the inner steps           */
+    int32_t reserved;
 } duquad_result;
+
+/* Kernel path of a solve (duquad_result.path).  "pass A" / "pass B" in the report map to:
+ *   TWO_PASS   k_pass_a ([Q;G] y, w) / k_pass_b (G'w, projection, momentum)
+ *   BYTE_FLOOR k_fused_stream (Q triangle + G once) / k_fused_epi (column sums, epilogue)
+ *   RHO0       k_rho0_step (Q y + c) / -            RHO0_FLOOR k_fused_stream (Q only) / k_fused_epi
+ *   BATCHED    DMMA pass 0 / pass 1                 CSR        k_pass_a_csr / k_pass_b_csr
+ *   SMALL      the whole solve in one single-CTA kernel (no per-pass timing)                  */
+typedef enum {
+    DUQUAD_PATH_TWO_PASS = 0,
+    DUQUAD_PATH_BYTE_FLOOR = 1,
+    DUQUAD_PATH_RHO0 = 2,
+    DUQUAD_PATH_RHO0_FLOOR = 3,
+    DUQUAD_PATH_BATCHED = 4,
+    DUQUAD_PATH_CSR = 5,
+    DUQUAD_PATH_SMALL = 6
+} duquad_path;
 
 int32_t duquad_abi_version(void);
 const char *duquad_status_string(int32_t status);

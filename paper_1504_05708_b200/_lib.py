@@ -64,7 +64,11 @@ class Result(C.Structure):
         ("n_timed_a", C.c_int64), ("n_timed_b", C.c_int64),
         ("bytes_pass_a", C.c_double), ("bytes_pass_b", C.c_double),
         ("flops_pass_a", C.c_double), ("flops_pass_b", C.c_double),
+        ("path", C.c_int32), ("reserved", C.c_int32),
     ]
+
+
+PATHS = {0: "two_pass", 1: "byte_floor", 2: "rho0", 3: "rho0_floor", 4: "batched", 5: "csr", 6: "small"}
 
 
 _SIGS = {

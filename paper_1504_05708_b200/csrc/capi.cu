@@ -1194,6 +1194,7 @@ duquad_status duquad_solve(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t 
             float ms = 0.f;
             cudaEventElapsedTime(&ms, t0, t1);
             res->ms_device = ms;
+            res->path = DUQUAD_PATH_SMALL;
             res->outer_iters = K;
             res->inner_iters_total = (int64_t)(K + 1) * Kin;
             res->kernel_launches = 2;
@@ -1253,6 +1254,10 @@ duquad_status duquad_solve(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t 
         float ms = 0.f;
         cudaEventElapsedTime(&ms, t0, t1);
         res->ms_device = ms;
+        res->path = ctx->fused ? (ctx->rho0 ? DUQUAD_PATH_RHO0_FLOOR : DUQUAD_PATH_BYTE_FLOOR)
+                    : ctx->rho0 ? DUQUAD_PATH_RHO0
+                    : ctx->Btot > 1 ? DUQUAD_PATH_BATCHED
+                    : ctx->format == DUQUAD_CSR ? DUQUAD_PATH_CSR : DUQUAD_PATH_TWO_PASS;
         res->outer_iters = K;
         res->inner_iters_total = (int64_t)(K + 1) * Kin;
         res->kernel_launches = 1 + (int64_t)(K + 1) * (2 * Kin + 1);
