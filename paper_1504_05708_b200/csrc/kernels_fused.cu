@@ -5,12 +5,12 @@
 // kernel (k_fused_stream) does both, then a small kernel (k_fused_epi) finishes the step.
 //
 // Data movement: every thread prefetches, with cp.async (LDGSTS), exactly the 16-byte pieces of
-// the 4096-column row chunks it will itself consume, 6 chunks ahead (192 KB in flight per SM),
+// the 4096-column row chunks it will itself consume, 7 chunks ahead (224 KB of ring per SM),
 // into a private shared-memory ring -- the stream needs no barriers at all.  (Measured on B200:
 // such a ring streams at ~7.2 TB/s, while cp.async.bulk (TMA) rings are bound by a per-copy
 // cost: 3.7 TB/s with 8 KB copies, 6.6 TB/s with 16 KB copies.)  Thread t owns columns
 // 2t, 2t+1 (+1024 k) of every chunk: their y values and column sums live in registers.
-// 16 warps, 128 registers per thread; warp 0 also finishes the G rows.
+// 16 warps, 128 registers per thread.
 //
 //  * Q role (single CTAs): the upper triangle in tile columns of 4096, as the sequence
 //    (J, r): J = 0..nt-1, r = 0..min(4096 (J+1), n)-1; row step (J, r) = columns
@@ -19,8 +19,8 @@
 //    (registers -> ws_col[cta][J - j0] when the CTA leaves tile column J).  The host cuts the
 //    sequence into pieces of equal estimated time, max(bytes, per-step cost) summed.
 //  * G role (thread-block clusters of cg = 2 or 4 CTAs): rank c owns column block c
-//    ([c W, (c+1) W)) of a range of G rows.  Per row: the block's partial dot -> warp 0 sends it
-//    to every CTA of the cluster through distributed shared memory (st.async with mbarrier
+//    ([c W, (c+1) W)) of a range of G rows.  Per row: the block's partial dot -> the last warp to
+//    post its partial (shared-memory counter) sends the CTA sum to every CTA of the cluster through distributed shared memory (st.async with mbarrier
 //    complete_tx), adds the block partials in rank order and applies the pass-A epilogue (w_i =
 //    [mu_i + rho r_i]_{K°}, incl. the fused DFOM step on the first inner step); all warps then
 //    accumulate w_i G_i into register column sums while the row is still in the ring.  The dot
@@ -47,8 +47,9 @@ constexpr int kWarps = 16;
 constexpr int kThreadsF = kWarps * 32;  // 4 warps per SMSP, 128 registers
 constexpr int kChunk = 4096;            // columns per chunk (= Q tile width)
 constexpr int kV = 4;                   // double2 per thread per chunk
-constexpr int kSlots = 6;               // per-thread ring depth (chunks; 192 KB per CTA)
-constexpr int kD = 32;                  // depth of the per-row buffers / barriers
+constexpr int kSlots = 7;               // per-thread ring depth (chunks; 224 KB per CTA)
+constexpr int kD = 8;                   // depth of the per-row buffers / barriers (G rows)
+constexpr int kHdr = 3072;              // barriers + per-row buffers; header + ring = 227 KB
 constexpr int kMaxCg = 4;               // G-role cluster size (2 or 4)
 static_assert(kThreadsF * kV * 2 == kChunk, "chunk = 512 threads x 8 doubles");
 
@@ -154,21 +155,22 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int cta = blockIdx.x;
     // ---- shared memory: barriers + small per-row buffers (first 8 KB), then the ring
-    uint64_t *redbar = reinterpret_cast<uint64_t *>(fsm);  // [kD] 16 warp partials of a G row posted
-    uint64_t *xbar = redbar + kD;                          // [kD] cluster exchange (st.async bytes)
+    uint64_t *xbar = reinterpret_cast<uint64_t *>(fsm);    // [kD] cluster exchange (st.async bytes)
     uint64_t *wbar = xbar + kD;                            // [kD] w ready (1 arrival)
-    double *red = reinterpret_cast<double *>(fsm + 2048);  // [kD][16]
-    double *xbuf = red + kD * 16;                          // [kD][kMaxCg]
-    double *wbuf = xbuf + kD * kMaxCg;                     // [kD]
-    const double2 *ring = reinterpret_cast<const double2 *>(fsm + 8192) + tid;   // [kSlots][kV][512]
+    uint32_t *cnt = reinterpret_cast<uint32_t *>(wbar + kD);   // [kD] warps that posted a G row
+    double *red = reinterpret_cast<double *>(fsm + 512);   // [kD][16] warp partials of a G row
+    double *xbuf = red + kD * 16;                          // [kD][kMaxCg] block partials (st.async)
+    double *wbuf = xbuf + kD * kMaxCg;                     // [kD] w of the row
+    double *epib = wbuf + kD;                              // [kD][4] g, mu, lambda_prev, cone of the row
+    const double2 *ring = reinterpret_cast<const double2 *>(fsm + kHdr) + tid;   // [kSlots][kV][512]
     const uint32_t ring_u32 = smem_u32(ring);
     auto slot_addr = [&](int s, int k) -> uint32_t { return ring_u32 + (uint32_t)((s * kV + k) * kThreadsF) * 16; };
 
     if (tid == 0) {
         for (int s = 0; s < kD; ++s) {
-            mbar_init(&redbar[s], kWarps);
             mbar_init(&xbar[s], 1);   // this CTA's expect_tx arrival + cg x 8 bytes of st.async
             mbar_init(&wbar[s], 1);
+            cnt[s] = 0;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -178,110 +180,153 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
     if (NCHG == 0 || cta < f.nq_ctas) {
         // ================================ Q role: triangle row steps (J, r) of this piece
         const FusedPiece pc = f.pieces[cta];
-        // prefetch cursor
-        int pJ = pc.j0, pr = pc.r0, ps = 0;
+        int nsteps = 0;   // row steps of this piece
+        for (int J = pc.j0; J <= pc.j1 && J < f.nt; ++J) {
+            const Tile tj = tile_of(f, J);
+            const int rb = J == pc.j0 ? pc.r0 : 0, re = J == pc.j1 ? pc.r1 : tj.rows;
+            nsteps += re > rb ? re - rb : 0;
+        }
+        const int c2t = 2 * tid;
+        // prefetch cursor: kSlots steps ahead of the consumer, same sequence
+        int p_left = nsteps, pJ = pc.j0, pr = pc.r0, ps = 0;
         Tile pt = tile_of(f, pJ);
+        bool p_rag = pt.b - pt.a < kChunk;
+        const double *prow = f.Q + (int64_t)pr * f.ld + pt.a + c2t;
         auto issue = [&]() {
-            if (pJ < pc.j1 || (pJ == pc.j1 && pr < pc.r1)) {
-                const int st = pr > pt.a ? (pr & ~1) : pt.a;
-                const double *row = f.Q + (int64_t)pr * f.ld;
+            if (p_left > 0) {
+                if (pr < pt.a && !p_rag) {   // off-diagonal full row step
 #pragma unroll
-                for (int k = 0; k < kV; ++k) {
-                    const int c = pt.a + 2 * tid + 1024 * k;
-                    if (c + 1 >= st && c < pt.b) cp16(slot_addr(ps, k), row + c);
+                    for (int k = 0; k < kV; ++k) cp16(slot_addr(ps, k), prow + 1024 * k);
+                } else {                     // diagonal (from column r) / ragged tile
+                    const int st = pr > pt.a ? (pr & ~1) : pt.a;
+#pragma unroll
+                    for (int k = 0; k < kV; ++k) {
+                        const int c = pt.a + c2t + 1024 * k;
+                        if (c >= st && c < pt.b) cp16(slot_addr(ps, k), prow + 1024 * k);
+                    }
                 }
+                --p_left;
+                prow += f.ld;
                 if (++pr == pt.rows) {
                     ++pJ;
                     pr = 0;
                     pt = tile_of(f, pJ < f.nt ? pJ : 0);
+                    p_rag = pt.b - pt.a < kChunk;
+                    prow = f.Q + pt.a + c2t;
                 }
             }
             cp_commit();
             if (++ps == kSlots) ps = 0;
         };
         for (int t = 0; t < kSlots; ++t) issue();
-        int J = pc.j0, r = pc.r0, cs = 0;
-        double yv[8], acc[8];
-        Tile t = tile_of(f, J);
-        auto load_tile = [&]() {
-            t = tile_of(f, J);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const int c = t.a + own_col(tid, e);
-                yv[e] = c < t.b ? f.y[c] : 0.0;
-                acc[e] = 0.0;
-            }
-        };
-        bool live = false;   // yv / acc hold tile column J
-        auto flush_tile = [&]() {
-            if (!live) return;
-            live = false;
-            double *dst = f.ws_col + ((int64_t)cta * f.cslots + (J - pc.j0)) * kChunk;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const int c = own_col(tid, e);
-                if (t.a + c < t.b) dst[c] = acc[e];
-            }
-        };
-        // y_r for 32 rows at a time, one per lane (broadcast by shuffle)
-        int ybase = r;
-        double ycache = 0.0;
-        auto load_y = [&]() {
-            ybase = r;
-            ycache = r + lane < t.rows ? f.y[r + lane] : 0.0;
-        };
-        if (J < pc.j1 || (J == pc.j1 && r < pc.r1)) {
-            load_tile();
-            live = true;
-            load_y();
-        }
-        double *rowp = f.ws_rowp + ((int64_t)J * kWarps + warp) * f.ld;   // this warp's row partials
-        while (J < pc.j1 || (J == pc.j1 && r < pc.r1)) {
-            const double yr = __shfl_sync(0xffffffffu, ycache, r - ybase);
-            cp_wait<kSlots - 1>();
-            double q[8];
+        int cs = 0;
+        auto load_q = [&](double *q) {
 #pragma unroll
             for (int k = 0; k < kV; ++k) {
                 const double2 v = ring[(cs * kV + k) * kThreadsF];
                 q[2 * k] = v.x;
                 q[2 * k + 1] = v.y;
             }
-            double rowacc = 0.0;
-            if (r >= t.a || t.b - t.a < kChunk) {   // diagonal tile / ragged last tile: masks
+            if (++cs == kSlots) cs = 0;
+        };
+        for (int J = pc.j0; J <= pc.j1 && J < f.nt; ++J) {
+            const Tile t = tile_of(f, J);
+            const int rb = J == pc.j0 ? pc.r0 : 0, re = J == pc.j1 ? pc.r1 : t.rows;
+            if (re <= rb) continue;
+            const bool rag = t.b - t.a < kChunk;
+            const int cb = t.a + c2t;   // column of element e: cb + (e >> 1) * 1024 + (e & 1)
+            double yv[8], acc[8];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const int c = t.a + own_col(tid, e);
-                    if (c >= r && c < t.b) {
-                        rowacc = fma(q[e], yv[e], rowacc);
-                        if (c > r) acc[e] = fma(q[e], yr, acc[e]);
+            for (int e = 0; e < 8; ++e) {
+                const int c = cb + (e >> 1) * 1024 + (e & 1);
+                yv[e] = c < t.b ? f.y[c] : 0.0;
+                acc[e] = 0.0;
+            }
+            double *rowp = f.ws_rowp + ((int64_t)J * kWarps + warp) * f.ld;   // this warp's row partials
+            // y_r for 32 rows at a time, one per lane (broadcast by shuffle)
+            int ybase = rb;
+            double ycache = rb + lane < t.rows ? f.y[rb + lane] : 0.0;
+            int r = rb;
+            for (; r + 1 < re; r += 2) {   // two row steps per iteration (independent chains)
+                if (r + 1 - ybase >= 32) {
+                    ybase = r;
+                    ycache = r + lane < t.rows ? f.y[r + lane] : 0.0;
+                }
+                const double y0 = __shfl_sync(0xffffffffu, ycache, r - ybase);
+                const double y1 = __shfl_sync(0xffffffffu, ycache, r + 1 - ybase);
+                cp_wait<kSlots - 2>();
+                double q0[8], q1[8];
+                load_q(q0);
+                load_q(q1);
+                issue();
+                issue();
+                double a0 = 0.0, b0 = 0.0, a1 = 0.0, b1 = 0.0;
+                if (r + 1 < t.a && !rag) {   // both rows above the diagonal tile: no masks
+#pragma unroll
+                    for (int e = 0; e < 8; e += 2) {
+                        a0 = fma(q0[e], yv[e], a0);
+                        b0 = fma(q0[e + 1], yv[e + 1], b0);
+                        a1 = fma(q1[e], yv[e], a1);
+                        b1 = fma(q1[e + 1], yv[e + 1], b1);
+                        acc[e] = fma(q0[e], y0, acc[e]);
+                        acc[e + 1] = fma(q0[e + 1], y0, acc[e + 1]);
+                        acc[e] = fma(q1[e], y1, acc[e]);
+                        acc[e + 1] = fma(q1[e + 1], y1, acc[e + 1]);
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const int c = cb + (e >> 1) * 1024 + (e & 1);
+                        const bool in = c < t.b;
+                        const double d0 = (in && c >= r) ? q0[e] : 0.0, d1 = (in && c >= r + 1) ? q1[e] : 0.0;
+                        if (e & 1) {
+                            b0 = fma(d0, yv[e], b0);
+                            b1 = fma(d1, yv[e], b1);
+                        } else {
+                            a0 = fma(d0, yv[e], a0);
+                            a1 = fma(d1, yv[e], a1);
+                        }
+                        acc[e] = fma(c > r ? d0 : 0.0, y0, acc[e]);
+                        acc[e] = fma(c > r + 1 ? d1 : 0.0, y1, acc[e]);
                     }
                 }
-            } else {
+                // both row sums with one butterfly: lanes < 16 reduce row r, lanes >= 16 row r + 1
+                const double s0 = a0 + b0, s1 = a1 + b1;
+                double mine = (lane & 16) ? s1 : s0;
+                mine += __shfl_xor_sync(0xffffffffu, (lane & 16) ? s0 : s1, 16);
+                mine += __shfl_xor_sync(0xffffffffu, mine, 8);
+                mine += __shfl_xor_sync(0xffffffffu, mine, 4);
+                mine += __shfl_xor_sync(0xffffffffu, mine, 2);
+                mine += __shfl_xor_sync(0xffffffffu, mine, 1);
+                if ((lane & 15) == 0) rowp[r + (lane >> 4)] = mine;
+            }
+            if (r < re) {   // last row of the segment
+                if (r - ybase >= 32) {
+                    ybase = r;
+                    ycache = r + lane < t.rows ? f.y[r + lane] : 0.0;
+                }
+                const double y0 = __shfl_sync(0xffffffffu, ycache, r - ybase);
+                cp_wait<kSlots - 1>();
+                double q0[8];
+                load_q(q0);
+                issue();
+                double a0 = 0.0;
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
-                    rowacc = fma(q[e], yv[e], rowacc);
-                    acc[e] = fma(q[e], yr, acc[e]);
+                    const int c = cb + (e >> 1) * 1024 + (e & 1);
+                    const double d0 = (c < t.b && c >= r) ? q0[e] : 0.0;
+                    a0 = fma(d0, yv[e], a0);
+                    acc[e] = fma(c > r ? d0 : 0.0, y0, acc[e]);
                 }
+                a0 = warp_sum(a0);
+                if (lane == 0) rowp[r] = a0;
             }
-            issue();   // refill this slot kSlots steps ahead
-            if (++cs == kSlots) cs = 0;
-            rowacc = warp_sum(rowacc);
-            if (lane == 0) rowp[r] = rowacc;
-            if (++r == t.rows) {
-                flush_tile();
-                ++J;
-                r = 0;
-                if (J < pc.j1 || (J == pc.j1 && r < pc.r1)) {
-                    load_tile();
-                    live = true;
-                    load_y();
-                    rowp = f.ws_rowp + ((int64_t)J * kWarps + warp) * f.ld;
-                }
-            } else if (r - ybase == 32) {
-                load_y();
-            }
+            // column sums of this tile column -> ws_col[cta][J - j0]
+            double *dst = f.ws_col + ((int64_t)cta * f.cslots + (J - pc.j0)) * kChunk + c2t;
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                if (cb + (e >> 1) * 1024 + (e & 1) < t.b) dst[(e >> 1) * 1024 + (e & 1)] = acc[e];
         }
-        flush_tile();
         cp_wait<0>();
     } else if constexpr (NCHG > 0) {
         // ================================ G role: pair gi owns rows [g0, g1); this CTA block `rank`
@@ -340,40 +385,57 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
             if (++sa == kSlots) sa = 0;
             return part;
         };
-        auto post = [&](int it, double part) {
-            part = warp_sum(part);
-            if (lane == 0) {
-                const int d = it % kD;
-                red[d * 16 + warp] = part;
-                mbar_arrive(&redbar[d]);
-            }
-        };
-        // warp 0: finishes row `it` -- CTA sum, cluster exchange through DSMEM, w (pass-A epilogue)
+        // Row finishing by the LAST warp to post its partial (shared-memory counter): CTA sum of
+        // the 16 warp partials (fixed tree), block partial -> every CTA of the cluster with st.async,
+        // rank-order sum of the block partials, pass-A epilogue -> w.  The epilogue operands of
+        // row it are prefetched into shared memory two rows ahead by thread 0.
         const OuterA o = outer_a(f.a, MODE_SOLVE);
         const uint32_t xb_r = map_to_cta(smem_u32(xbuf), (uint32_t)(lane % f.cg));
         const uint32_t xm_r = map_to_cta(smem_u32(xbar), (uint32_t)(lane % f.cg));
-        EpiA e_next{};
-        if (warp == 0 && lane == 0 && nr > 0) e_next = epi_a_load(f.a, MODE_SOLVE, f.a.nq + g0, o);
-        auto exchange = [&](int it) {
-            const EpiA e = e_next;
-            if (lane == 0 && it + 1 < nr) e_next = epi_a_load(f.a, MODE_SOLVE, f.a.nq + g0 + it + 1, o);
+        auto prefetch_epi = [&](int it) {
+            if (tid == 0 && it < nr) {
+                const EpiA e = epi_a_load(f.a, MODE_SOLVE, f.a.nq + g0 + it, o);
+                double *eb = epib + (it % kD) * 4;
+                eb[0] = e.g;
+                eb[1] = e.mu;
+                eb[2] = e.lp;
+                eb[3] = (double)e.c;
+            }
+        };
+        auto post = [&](int it, double part) {
+            part = warp_sum(part);
             const int d = it % kD;
-            const uint32_t par = (uint32_t)((it / kD) & 1);
-            mbar_wait(&redbar[d], par);
+            uint32_t last = 0;
+            if (lane == 0) {
+                red[d * 16 + warp] = part;
+                __threadfence_block();
+                last = atomicAdd(&cnt[d], 1u) == kWarps - 1;
+            }
+            if (!__shfl_sync(0xffffffffu, last, 0)) return;
+            __threadfence_block();
+            if (lane == 0) cnt[d] = 0;
             double v = lane < 16 ? red[d * 16 + lane] : 0.0;
             v = sum16(v);
             if (lane < f.cg)   // lane c: this block's partial -> CTA c of the cluster
                 st_async_f64(xb_r + (uint32_t)(d * kMaxCg + rank) * 8, v, xm_r + (uint32_t)d * 8);
             if (lane == 0) mbar_arrive_expect_tx(&xbar[d], (uint32_t)(8 * f.cg));
-            mbar_wait(&xbar[d], par);
+            mbar_wait(&xbar[d], (uint32_t)((it / kD) & 1));
             if (lane == 0) {
                 double s_row = xbuf[d * kMaxCg];   // block partials added in rank order
                 for (int c = 1; c < f.cg; ++c) s_row += xbuf[d * kMaxCg + c];
+                const double *eb = epib + d * 4;
+                EpiA e;
+                e.g = eb[0];
+                e.mu = eb[1];
+                e.lp = eb[2];
+                e.c = (uint8_t)eb[3];
                 wbuf[d] = g_row_w(f.a, g0 + it, s_row, e, o, rank == 0);
                 mbar_arrive(&wbar[d]);
             }
             __syncwarp();
         };
+        prefetch_epi(0);
+        prefetch_epi(1);
         if (nr > 0) {
             double part = 0.0;
 #pragma unroll
@@ -384,12 +446,12 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
         for (int it = 0; it < nr; ++it) {
             const bool nxt = it + 1 < nr;
             double part = 0.0, w = 0.0;
+            prefetch_epi(it + 2);
 #pragma unroll
             for (int m = 0; m < NCHG; ++m) {
                 if (m >= nch) continue;
                 if (nxt) part = dot_chunk(m, part);                       // A(it + 1, m)
                 if (m == 0) {
-                    if (warp == 0) exchange(it);
                     const int d = it % kD;
                     mbar_wait(&wbar[d], (uint32_t)((it / kD) & 1));
                     w = wbuf[d];
@@ -499,7 +561,8 @@ cudaError_t configure_t(size_t smem) {
 int fused_block_width(int64_t ld, int cg) { return (int)((ld + 32 * cg - 1) / (32 * cg) * 32); }
 int fused_nchg(int64_t ld, int cg) { return (fused_block_width(ld, cg) + kChunk - 1) / kChunk; }
 int fused_tiles(int64_t ld) { return (int)((ld + kChunk - 1) / kChunk); }
-size_t fused_smem_bytes() { return 8192 + (size_t)kSlots * kChunk * 8; }
+size_t fused_smem_bytes() { return kHdr + (size_t)kSlots * kChunk * 8; }
+static_assert(2 * kD * 8 + kD * 4 <= 512 && 512 + kD * (16 + kMaxCg + 1 + 4) * 8 <= kHdr, "header layout");
 bool fused_supported(int64_t n, int64_t ld, size_t smem_optin) {
     return n >= 4096 && fused_nchg(ld, 4) <= 2 && fused_tiles(ld) <= kFusedMaxTiles && fused_smem_bytes() <= smem_optin;
 }
