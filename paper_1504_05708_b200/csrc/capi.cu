@@ -977,8 +977,8 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         const int nb = std::min(ctx->num_sms / cg, maxc > 0 ? maxc : ctx->num_sms / cg) * cg;
         int nq = nb;                        // rho = 0 (K3) or p = 0: Q role only
         if (cg > 1) {
-            // Q : G split by bytes, G weighted by its measured per-byte cost (config 2: nq = 60 of 148)
-            double gw = 1.45;
+            // Q : G split by bytes, G weighted by its measured per-byte cost (config 2: nq = 64 of 148)
+            double gw = 1.31;
             if (const char *ov = std::getenv("DUQUAD_FUSED_GW")) gw = std::atof(ov);
             const double bq = 0.5 * (double)n * (double)(n + 1), bg = gw * (double)p * (double)n;
             nq = cg * (int)std::llround((double)nb / cg * bq / (bq + bg));

@@ -23,8 +23,10 @@
 //    post its partial (shared-memory counter) sends the CTA sum to every CTA of the cluster through distributed shared memory (st.async with mbarrier
 //    complete_tx), adds the block partials in rank order and applies the pass-A epilogue (w_i =
 //    [mu_i + rho r_i]_{K°}, incl. the fused DFOM step on the first inner step); all warps then
-//    accumulate w_i G_i into register column sums while the row is still in the ring.  The dot
-//    of row i+1 is interleaved with the w G of row i, so the exchange hides under the stream.
+//    accumulate w_i G_i into register column sums from the row values they hold in registers
+//    (the CTA's block of y sits in shared memory after a ring that is pure prefetch); the
+//    first chunk of row i+1 is read and dotted before waiting for w_i, so the exchange hides
+//    under the stream.
 //  * k_fused_epi: grad_j = sum of the partials of column j in a fixed order (+ q_j), then the
 //    pass-B epilogue (box projection, momentum, average).
 // All sums are in a fixed order, so results are bitwise reproducible run to run (but not
@@ -47,7 +49,8 @@ constexpr int kWarps = 16;
 constexpr int kThreadsF = kWarps * 32;  // 4 warps per SMSP, 128 registers
 constexpr int kChunk = 4096;            // columns per chunk (= Q tile width)
 constexpr int kV = 4;                   // double2 per thread per chunk
-constexpr int kSlots = 7;               // per-thread ring depth (chunks; 224 KB per CTA)
+constexpr int kSlots = 7;               // per-thread ring depth (chunks; 224 KB per CTA), Q role
+// G role: a (kSlots - NCHG)-chunk ring + this CTA's block of y (NCHG chunks) in the same space
 constexpr int kD = 8;                   // depth of the per-row buffers / barriers (G rows)
 constexpr int kHdr = 3072;              // barriers + per-row buffers; header + ring = 227 KB
 constexpr int kMaxCg = 4;               // G-role cluster size (2 or 4)
@@ -151,6 +154,7 @@ __device__ __forceinline__ Tile tile_of(const FusedArgs &f, int J) {
 // Launched with a cluster dimension of 2 when there is a G role (pairs), 1 otherwise.
 template <int NCHG>
 __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f) {
+    constexpr int kSlotsG = kSlots - (NCHG > 0 ? NCHG : 1);
     extern __shared__ __align__(128) uint8_t fsm[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int cta = blockIdx.x;
@@ -337,6 +341,18 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
         const int gi = (cta - f.nq_ctas) / f.cg;
         const int64_t g0 = f.p * gi / f.ng, g1 = f.p * (gi + 1) / f.ng;
         const int nr = (int)(g1 - g0);
+        // The G role keeps this CTA's block of y in shared memory (after a kSlotsG-slot ring) and
+        // row values in registers between their dot and their w G, so every ring slot is refilled
+        // as soon as it is read (kSlotsG chunks in flight).  Half-row lag: the first chunk of row
+        // it+1 is read and dotted before waiting for w_it, which hides the cluster exchange.
+        double2 *ysm = reinterpret_cast<double2 *>(fsm + kHdr + kSlotsG * kChunk * 8) + tid;   // [NCHG][kV][512]
+        for (int m = 0; m < NCHG; ++m)
+#pragma unroll
+            for (int k = 0; k < kV; ++k) {
+                const int c = a + m * kChunk + 2 * tid + 1024 * k;
+                ysm[(m * kV + k) * kThreadsF] = (m < nch && c < b) ? *reinterpret_cast<const double2 *>(f.y + c)
+                                                                    : make_double2(0.0, 0.0);
+            }
         int p_it = 0, p_m = 0, ps = 0;   // prefetch cursor
         auto issue = [&]() {
             if (p_it < nr) {
@@ -352,37 +368,34 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
                 }
             }
             cp_commit();
-            if (++ps == kSlots) ps = 0;
+            if (++ps == kSlotsG) ps = 0;
         };
-        for (int t = 0; t < kSlots; ++t) issue();
-        double yv[NCHG][8], acc[NCHG][8];
+        for (int t = 0; t < kSlotsG; ++t) issue();
+        double acc[NCHG][8];
 #pragma unroll
         for (int m = 0; m < NCHG; ++m)
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const int c = a + m * kChunk + own_col(tid, e);
-                yv[m][e] = (m < nch && c < b) ? f.y[c] : 0.0;
-                acc[m][e] = 0.0;
-            }
-        // A cursor (row dots) runs one row ahead of the B cursor (w G; frees the slot)
-        int sa = 0, sb = 0;
-        auto dot_chunk = [&](int m, double part) -> double {
-            cp_wait<kSlots - 1 - NCHG>();
+            for (int e = 0; e < 8; ++e) acc[m][e] = 0.0;
+        int cs = 0;
+        // read chunk m of the next row from the ring into v (slot refilled at once); its dot with y
+        auto take = [&](int m, double *v, double part) -> double {
+            cp_wait<kSlotsG - 1>();
+            const bool rg = ragged && m == nch - 1;
 #pragma unroll
             for (int k = 0; k < kV; ++k) {
-                const double2 v = ring[(sa * kV + k) * kThreadsF];
-                if (ragged && m == nch - 1) {
-                    const int c = a + m * kChunk + 2 * tid + 1024 * k;
-                    if (c < b) {
-                        part = fma(v.x, yv[m][2 * k], part);
-                        part = fma(v.y, yv[m][2 * k + 1], part);
-                    }
-                } else {
-                    part = fma(v.x, yv[m][2 * k], part);
-                    part = fma(v.y, yv[m][2 * k + 1], part);
-                }
+                double2 q = ring[(cs * kV + k) * kThreadsF];
+                if (rg && a + m * kChunk + 2 * tid + 1024 * k >= b) q = make_double2(0.0, 0.0);   // not loaded
+                v[2 * k] = q.x;
+                v[2 * k + 1] = q.y;
             }
-            if (++sa == kSlots) sa = 0;
+            issue();
+            if (++cs == kSlotsG) cs = 0;
+#pragma unroll
+            for (int k = 0; k < kV; ++k) {
+                const double2 yk = ysm[(m * kV + k) * kThreadsF];
+                part = fma(v[2 * k], yk.x, part);
+                part = fma(v[2 * k + 1], yk.y, part);
+            }
             return part;
         };
         // Row finishing by the LAST warp to post its partial (shared-memory counter): CTA sum of
@@ -436,36 +449,35 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
         };
         prefetch_epi(0);
         prefetch_epi(1);
+        double hold[NCHG][8];   // the current row's values (chunks 0..nch-1)
         if (nr > 0) {
             double part = 0.0;
 #pragma unroll
             for (int m = 0; m < NCHG; ++m)
-                if (m < nch) part = dot_chunk(m, part);
+                if (m < nch) part = take(m, hold[m], part);
             post(0, part);
         }
         for (int it = 0; it < nr; ++it) {
             const bool nxt = it + 1 < nr;
-            double part = 0.0, w = 0.0;
             prefetch_epi(it + 2);
+            double next0[8];
+            double part = 0.0;
+            if (nxt) part = take(0, next0, part);                    // row it+1, chunk 0
+            const int d = it % kD;
+            mbar_wait(&wbar[d], (uint32_t)((it / kD) & 1));
+            const double w = wbuf[d];
 #pragma unroll
-            for (int m = 0; m < NCHG; ++m) {
-                if (m >= nch) continue;
-                if (nxt) part = dot_chunk(m, part);                       // A(it + 1, m)
-                if (m == 0) {
-                    const int d = it % kD;
-                    mbar_wait(&wbar[d], (uint32_t)((it / kD) & 1));
-                    w = wbuf[d];
-                }
+            for (int m = 0; m < NCHG; ++m)                              // w G of row it
 #pragma unroll
-                for (int k = 0; k < kV; ++k) {                              // B(it, m)
-                    const double2 v = ring[(sb * kV + k) * kThreadsF];
-                    acc[m][2 * k] = fma(w, v.x, acc[m][2 * k]);
-                    acc[m][2 * k + 1] = fma(w, v.y, acc[m][2 * k + 1]);
-                }
-                issue();   // the slot of B(it, m) is free: refill it
-                if (++sb == kSlots) sb = 0;
+                for (int e = 0; e < 8; ++e) acc[m][e] = fma(w, hold[m][e], acc[m][e]);
+            if (nxt) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) hold[0][e] = next0[e];
+#pragma unroll
+                for (int m = 1; m < NCHG; ++m)
+                    if (m < nch) part = take(m, hold[m], part);         // row it+1, chunks 1..
+                post(it + 1, part);
             }
-            if (nxt) post(it + 1, part);
         }
         cp_wait<0>();
         double *pt = f.ws_g + (int64_t)gi * f.ld;
