@@ -41,7 +41,9 @@ typedef enum {
     DUQUAD_ENCCL = 4,       /* NCCL error in the sharded path                             */
     DUQUAD_ENONFINITE = 5,  /* an iterate became non-finite; results kept  */
     DUQUAD_ENODEV = 6,      /* no CUDA device, or not an sm_100 device                    */
-    DUQUAD_ESTATE = 7       /* call out of order (e.g. solve before constants are set)    */
+    DUQUAD_ESTATE = 7,      /* call out of order (e.g. solve before constants are set)    */
+    DUQUAD_EMAXITER = 8     /* eps_in mode: an inner solve hit inner_max first; the result
+                               and the inner-step counts are still populated              */
 } duquad_status;
 
 typedef enum { DUQUAD_DGM = 0, DUQUAD_DFGM = 1 } duquad_alg;
@@ -225,6 +227,55 @@ duquad_status duquad_set_constants(duquad_ctx *ctx, double L_in, double L_d);
  */
 duquad_status duquad_solve(duquad_ctx *ctx, int32_t alg, int32_t outer_iters,
                            int32_t inner_iters, duquad_result *res);
+
+/*
+ * DFOM with eps_in-driven inner stopping (Eq. duquad_in).
+ * Every inner FGM solve runs until the gradient-map test
+ *     L_in * ||y^k - x^k|| <= sqrt(2 * sigma_L * eps_in)
+ * holds, x^k = [y^k - grad/L_in]_U the step's projected point, or `inner_max` steps ran.  For a
+ * sigma_L-strongly convex L_rho(., mu) the test guarantees L_rho(x^k, mu) - d_rho(mu) <= eps_in
+ * (the inexactness (duquad_in) of Theorem 1).  sigma_L > 0 is the caller's lower bound on
+ * lambda_min(Q + rho G'G) (e.g. lambda_min(Q)), eps_in > 0 (e.g. from duquad_theory_schedule).
+ * The norm is a fixed-order device reduction after each step; converged inner solves skip the
+ * remaining steps of their (graph-captured) loop.  Single GPU, batch 1, any format.
+ * Returns DUQUAD_EMAXITER (result valid) when some inner solve was capped; per-outer step
+ * counts via duquad_get_inner_counts.  res->inner_iters_total = steps actually run.
+ */
+duquad_status duquad_solve_eps(duquad_ctx *ctx, int32_t alg, int32_t outer_iters, int32_t inner_max,
+                               double eps_in, double sigma_L, duquad_result *res);
+
+/*
+ * Per-outer inner-step counts of the last duquad_solve_eps (K_out + 1 entries: the outer
+ * iterations, then the last-iterate solve) and whether each met the eps_in test (1) or was
+ * capped (0).  Either output may be NULL; copies min(max_entries, K_out + 1) entries.
+ */
+duquad_status duquad_get_inner_counts(duquad_ctx *ctx, int32_t *counts, int32_t *converged,
+                                      int32_t max_entries);
+
+/* Theory schedule of DuQuad for a target accuracy eps (host-only arithmetic, no GPU). */
+typedef struct {
+    double eps_in;      /* (choose_ein) PAPER.md:641-647: eps/4 (DGM), eps^1.5/(8 R_d sqrt(2 L_d)) (DFGM) */
+    int64_t k_out;      /* (choose_ein): ceil(8 L_d R_d^2 / eps) (DGM), ceil(sqrt(8 L_d R_d^2 / eps)) (DFGM)  */
+    int64_t k_in;       /* proof of Theorem in:th_last, rounded up:
+                           sqrt(2 L D_U^2 / eps_in) (sigma_L = 0),
+                           sqrt(L / sigma_L) log(L D_U^2 / eps_in) + 1 (sigma_L > 0)              */
+    double rho_star;    /* 8 R_d^2 / eps (Theorem in:th_last)            */
+    int64_t k_total;    /* Theorem in:th_last, PAPER.md:1162-1169 (floor):
+                           24 ||G|| D_U R_d / eps (sigma_L = 0),
+                           16 ||G|| R_d / sqrt(sigma_L eps) log(8 ||G|| D_U R_d / eps) (sigma_L > 0) */
+    int32_t case_id;    /* 1 if lambda_min(Q) > 0 (rho = 0), 2 otherwise (rho > 0) */
+    int32_t reserved;
+} duquad_schedule;
+
+/*
+ * Fills `out` from the algorithm (DUQUAD_DGM/DFGM), the target accuracy eps > 0, the dual
+ * radius R_d = ||lambda*|| > 0 (an estimate), L_d > 0, the inner Lipschitz constant L_in > 0,
+ * sigma_L >= 0, the box diameter D_U > 0, ||G|| >= 0 and a lower bound lambda_min_Q >= 0.
+ * DUQUAD_EINVAL on a non-finite or out-of-range argument.  Pure host arithmetic.
+ */
+duquad_status duquad_theory_schedule(int32_t alg, double eps, double R_d, double L_d, double L_in,
+                                     double sigma_L, double D_U, double normG, double lambda_min_Q,
+                                     duquad_schedule *out);
 
 /*
  * Copies x_last = u_bar(lambda^K) (n, or B x n), x_avg (Eq. average_primal,

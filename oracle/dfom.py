@@ -163,6 +163,23 @@ def fom(grad_fn, x0, L, lb, ub, iters: int, rule: str = INNER_FGM, sigma: float 
     FGM_sigma constant beta.  [reading c5] theta restarts at
     theta_1 = 1 on every call.  [reading c6] returns x^{iters} (not y).
     """
+    x, _, _ = fom_run(grad_fn, x0, L, lb, ub, iters, rule, sigma, history=history)
+    return x
+
+
+def fom_run(grad_fn, x0, L, lb, ub, iters: int, rule: str = INNER_FGM, sigma: float = 0.0,
+            eps_in: Optional[float] = None, sigma_L: Optional[float] = None,
+            history: Optional[list] = None, gm: Optional[list] = None):
+    """Algorithm FOM as in fom(), optionally stopped by the inner accuracy eps_in.
+
+    Stopping test (reading c15 of Eq. duquad_in): after step k,
+    stop with u_bar = x^k when the gradient map at y^k satisfies
+        L * ||y^k - x^k|| <= sqrt(2 * sigma_L * eps_in),
+    which for a sigma_L-strongly convex phi gives phi(x^k) - phi* <= eps_in
+    (phi(x+) - phi* <= ||G_L(y)||^2 / (2 sigma_L) for the gradient map G_L(y) = L (y - x+)).
+    `iters` is then the cap.  Returns (x, steps run, converged).  `gm` collects
+    L * ||y^k - x^k|| per step.
+    """
     if rule == INNER_FGM:
         beta = beta_fgm(iters)
     elif rule == INNER_GM:
@@ -171,24 +188,35 @@ def fom(grad_fn, x0, L, lb, ub, iters: int, rule: str = INNER_FGM, sigma: float 
         beta = np.full(iters + 1, beta_fgm_sigma(L, sigma))
     else:
         raise ValueError(rule)
+    thr = None if eps_in is None else np.sqrt(2.0 * sigma_L * eps_in)
     x_prev = x0.copy()
     y = x0.copy()
     for k in range(1, iters + 1):
         x = clamp_U(y - grad_fn(y) / L, lb, ub)
-        y = x + beta[k] * (x - x_prev)
-        x_prev = x
         if history is not None:
             history.append(x.copy())
-    return x_prev
+        if thr is not None or gm is not None:
+            g_k = L * float(np.linalg.norm(y - x))
+            if gm is not None:
+                gm.append(g_k)
+            if thr is not None and g_k <= thr:
+                return x, k, True
+        y = x + beta[k] * (x - x_prev)
+        x_prev = x
+    return x_prev, iters, thr is None
 
 
 def inner_solve(Q, q, G, g, cone, rho, mu, x0, L_in, lb, ub, iters,
-                rule=INNER_FGM, sigma=0.0):
+                rule=INNER_FGM, sigma=0.0, eps_in=None, sigma_L=None, gm=None, info=None):
     """Step 1 of DuQuad: u_bar(mu) by FOM(L_rho(., mu), U) warm-started at x0
-    (P:601-603)."""
+    (P:601-603); fixed `iters` steps, or stopped by the inner accuracy eps_in (fom_run).
+    `info`, if a list, receives (steps run, converged)."""
     def grad(u):
         return aug_lagrangian_grad(Q, q, G, g, cone, rho, u, mu)
-    return fom(grad, x0, L_in, lb, ub, iters, rule, sigma)
+    x, k, conv = fom_run(grad, x0, L_in, lb, ub, iters, rule, sigma, eps_in, sigma_L, gm=gm)
+    if info is not None:
+        info.append((k, conv))
+    return x
 
 
 def inexact_dual_grad(G, g, cone, rho, u_bar, mu):
@@ -208,12 +236,17 @@ class DfomResult:
     trace_lam: List[np.ndarray] = field(default_factory=list)   # lambda^j, j=1..K
     trace_u: List[np.ndarray] = field(default_factory=list)     # u_bar^j, j=1..K
     trace_mu: List[np.ndarray] = field(default_factory=list)    # mu^j, j=1..K
+    inner_counts: List[int] = field(default_factory=list)       # steps per inner solve (K + 1)
+    converged: List[bool] = field(default_factory=list)         # eps_in test met (eps mode)
+    gm: List[List[float]] = field(default_factory=list)         # L ||y^k - x^k|| per step (record_gm)
 
 
-def dfom(Q, q, G, g, lb, ub, cone, rho: float, alg: str, outer: int, inner: int,
+def dfom(Q, q, G, g, lb, ub, cone, rho: float, alg: str, outer: int, inner,
          L_in: float, L_d: float, inner_rule: str = INNER_FGM, sigma: float = 0.0,
          dual_step_scale: float = 0.5, project_dual: bool = True,
-         lam0: Optional[np.ndarray] = None, keep_trace: bool = False) -> DfomResult:
+         lam0: Optional[np.ndarray] = None, keep_trace: bool = False,
+         eps_in: Optional[float] = None, sigma_L: Optional[float] = None,
+         record_gm: bool = False) -> DfomResult:
     """Algorithm DFOM(d_rho, K_d), with fixed inner iteration counts.
 
     Given lambda^0 = mu^1 in K_d (= 0, [reading c8]), for k >= 1:
@@ -227,9 +260,13 @@ def dfom(Q, q, G, g, lb, ub, cone, rho: float, alg: str, outer: int, inner: int,
     Last iterate: u_bar(lambda^K) by one more inner solve warm-started at
       u_bar^K (Eq. last_primal) [reading c10].
     dual_step_scale = 1/2 gives the paper's 1/(2 L_d); project_dual per [reading c3].
+    `inner`: steps per inner solve (int), or a sequence of K + 1 per-solve counts (the last
+    for the last-iterate solve); with eps_in and sigma_L the inner solves stop by the
+    eps_in test of fom_run (NEXT-1) and `inner` is the cap.
     """
-    if outer < 1 or inner < 1:
-        raise ValueError("outer and inner must be >= 1")
+    counts = [int(inner)] * (outer + 1) if np.ndim(inner) == 0 else [int(c) for c in inner]
+    if outer < 1 or len(counts) != outer + 1 or min(counts) < 1:
+        raise ValueError("outer >= 1 and inner >= 1 (one count per solve: K + 1)")
     p = G.shape[0]
     bshape = (p,) if q.ndim == 1 else (p, q.shape[1])
     theta = theta_sequence(outer + 1)
@@ -239,9 +276,17 @@ def dfom(Q, q, G, g, lb, ub, cone, rho: float, alg: str, outer: int, inner: int,
     xsum = np.zeros(q.shape)
     S = 0.0
     res = DfomResult(None, None, None, None, 0.0)
+    info = []
+
+    def gm_list():
+        if not record_gm:
+            return None
+        res.gm.append([])
+        return res.gm[-1]
+
     for k in range(1, outer + 1):
-        u_bar = inner_solve(Q, q, G, g, cone, rho, mu, u_bar, L_in, lb, ub, inner,
-                            inner_rule, sigma)                                     # step 1
+        u_bar = inner_solve(Q, q, G, g, cone, rho, mu, u_bar, L_in, lb, ub, counts[k - 1],
+                            inner_rule, sigma, eps_in, sigma_L, gm_list(), info)    # step 1
         gbar = inexact_dual_grad(G, g, cone, rho, u_bar, mu)
         lam = proj_Kd(mu + (dual_step_scale / L_d) * gbar, cone, project_dual)     # step 2
         omega = theta[k] if alg == DFGM else 1.0
@@ -259,14 +304,60 @@ def dfom(Q, q, G, g, lb, ub, cone, rho: float, alg: str, outer: int, inner: int,
             res.trace_u.append(u_bar.copy())
         mu = lam + beta_k * (lam - lam_prev)                                       # step 3
         lam_prev = lam
-    x_last = inner_solve(Q, q, G, g, cone, rho, lam_prev, u_bar, L_in, lb, ub, inner,
-                         inner_rule, sigma)
+    x_last = inner_solve(Q, q, G, g, cone, rho, lam_prev, u_bar, L_in, lb, ub, counts[outer],
+                         inner_rule, sigma, eps_in, sigma_L, gm_list(), info)
+    res.inner_counts = [c for c, _ in info]
+    res.converged = [v for _, v in info]
     res.x_last = x_last
     res.x_avg = xsum / S
     res.lam = lam_prev
     res.u_bar_K = u_bar
     res.S = S
     return res
+
+
+# ------------------------------------------------------------ theory schedule (NEXT-1)
+def theory_schedule(alg: str, eps: float, R_d: float, L_d: float, L_in: float, sigma_L: float,
+                    D_U: float, normG: float, lambda_min_Q: float = 0.0) -> dict:
+    """DuQuad's parameter choices for a target accuracy eps.
+
+    eps_in, k_out: Eq. (choose_ein), P:641-652 (each term of Theorem 1's bound
+      (bound_gen_dfg), at most eps/2), counts rounded up.
+    k_in: proof of Theorem in:th_last, P:1168-1173 (Lemma 1 (bound_gen_dfg1), P:386-391,
+      with R_phi <= D_U), rounded up.
+    rho_star = 8 R_d^2 / eps.
+    k_total: Theorem in:th_last, P:1162-1169 (floor, as printed).
+    case: P:252-258, 1 if lambda_min(Q) > 0 (rho = 0), else 2 (rho > 0).
+    """
+    q8 = 8.0 * L_d * R_d ** 2 / eps
+    if alg == DGM:
+        eps_in, k_out = eps / 4.0, int(np.ceil(q8))
+    elif alg == DFGM:
+        eps_in, k_out = eps * np.sqrt(eps) / (8.0 * R_d * np.sqrt(2.0 * L_d)), int(np.ceil(np.sqrt(q8)))
+    else:
+        raise ValueError(alg)
+    if sigma_L > 0:
+        k_in = np.sqrt(L_in / sigma_L) * np.log(L_in * D_U ** 2 / eps_in) + 1.0
+        k_total = 16.0 * normG * R_d / np.sqrt(sigma_L * eps) * np.log(8.0 * normG * D_U * R_d / eps)
+    else:
+        k_in = np.sqrt(2.0 * L_in * D_U ** 2 / eps_in)
+        k_total = 24.0 * normG * D_U * R_d / eps
+    return dict(eps_in=float(eps_in), k_out=k_out, k_in=int(np.ceil(max(k_in, 1.0))),
+                rho_star=8.0 * R_d ** 2 / eps, k_total=int(np.floor(k_total)),
+                case_id=1 if lambda_min_Q > 0 else 2)
+
+
+def theorem1_bound(alg: str, k: int, L_d: float, R_d: float, eps_in: float) -> float:
+    """Right-hand side of Theorem 1 (bound_gen_dfg), P:614-616:
+    4 L_d R_d^2 / (k+1)^p + 2 (k+1)^(p-1) eps_in, p = 1 (DGM) or 2 (DFGM) (Eq. pbetak)."""
+    p = 1 if alg == DGM else 2
+    return 4.0 * L_d * R_d ** 2 / (k + 1) ** p + 2.0 * (k + 1) ** (p - 1) * eps_in
+
+
+def lemma1_bound(k: int, L: float, sigma: float, R: float, p: int = 2) -> float:
+    """Right-hand side of Lemma 1 (bound_gen_dfg1)."""
+    lin = (1.0 - np.sqrt(sigma / L)) ** (k - 1) * L * R ** 2 if sigma > 0 else np.inf
+    return min(lin, 2.0 * L * R ** 2 / (k + 1) ** p)
 
 
 # ------------------------------------------------------------ constants / checks

@@ -20,6 +20,7 @@ DUQUAD_ENCCL = 4
 DUQUAD_ENONFINITE = 5
 DUQUAD_ENODEV = 6
 DUQUAD_ESTATE = 7
+DUQUAD_EMAXITER = 8
 
 DGM = 0
 DFGM = 1
@@ -68,6 +69,13 @@ class Result(C.Structure):
     ]
 
 
+class Schedule(C.Structure):
+    _fields_ = [
+        ("eps_in", C.c_double), ("k_out", C.c_int64), ("k_in", C.c_int64), ("rho_star", C.c_double),
+        ("k_total", C.c_int64), ("case_id", C.c_int32), ("reserved", C.c_int32),
+    ]
+
+
 PATHS = {0: "two_pass", 1: "byte_floor", 2: "rho0", 3: "rho0_floor", 4: "batched", 5: "csr", 6: "small"}
 
 
@@ -87,6 +95,11 @@ _SIGS = {
     "duquad_residuals": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                    C.POINTER(C.c_double)]),
     "duquad_solve_emulated": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
+    "duquad_solve_eps": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_double,
+                                   C.POINTER(Result)]),
+    "duquad_get_inner_counts": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
+    "duquad_theory_schedule": (C.c_int, [C.c_int32, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
+                                         C.c_double, C.c_double, C.c_double, C.POINTER(Schedule)]),
     "duquad_destroy": (None, [C.c_void_p]),
     "duquad_last_error": (C.c_char_p, [C.c_void_p]),
 }

@@ -68,6 +68,14 @@ struct duquad_ctx {
     FusedArgs fz{};
     double *ws = nullptr;          // ws_rowp | ws_col | ws_g
     FusedPiece *fpieces = nullptr;
+    // eps_in-driven inner stopping (duquad_solve_eps): device flag / counters, active during a solve
+    bool eps_mode = false;
+    double eps_thresh2 = 0.0;
+    double *gm_sq = nullptr, *gm_part = nullptr;
+    uint32_t *gm_counter = nullptr;
+    int32_t *d_done = nullptr, *d_counts = nullptr;   // d_counts: [K+1] steps, then [K+1] converged flags
+    int64_t counts_cap = 0;
+    std::vector<int32_t> last_counts, last_conv;
     // whole-solve single-CTA kernel (small dense QPs)
     bool small = false;
     size_t small_smem = 0;
@@ -143,6 +151,11 @@ void free_all(duquad_ctx *c) {
     if (c->d_j) cudaFree(c->d_j);
     if (c->d_flag) cudaFree(c->d_flag);
     if (c->fpieces) cudaFree(c->fpieces);
+    if (c->gm_sq) cudaFree(c->gm_sq);
+    if (c->gm_part) cudaFree(c->gm_part);
+    if (c->gm_counter) cudaFree(c->gm_counter);
+    if (c->d_done) cudaFree(c->d_done);
+    if (c->d_counts) cudaFree(c->d_counts);
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
 }
@@ -214,6 +227,7 @@ PassAArgs make_a(duquad_ctx *c) {
     a.rp = c->a_rp;
     a.ci = c->a_ci;
     a.va = c->a_va;
+    a.skip = c->eps_mode ? c->d_done : nullptr;
     return a;
 }
 
@@ -240,6 +254,8 @@ PassBArgs make_b(duquad_ctx *c) {
     b.rp = c->b_rp;
     b.ci = c->b_ci;
     b.va = c->b_va;
+    b.skip = c->eps_mode ? c->d_done : nullptr;
+    b.gm_sq = c->eps_mode ? c->gm_sq : nullptr;
     return b;
 }
 
@@ -263,7 +279,15 @@ duquad_status gather(duquad_ctx *ctx, int b) {
     return DUQUAD_OK;
 }
 
-int num_phases(const duquad_ctx *c, int Kin) { return c->rho0 ? Kin + 3 : 2 * Kin + 1; }
+int num_phases(const duquad_ctx *c, int Kin) { return (c->rho0 ? Kin + 3 : 2 * Kin + 1) + (c->eps_mode ? 1 : 0); }
+
+// eps_in mode: gradient-map test after inner step k (a no-op once the solve has converged)
+duquad_status inner_check(duquad_ctx *ctx) {
+    if (!ctx->eps_mode) return DUQUAD_OK;
+    CK(launch_inner_check(ctx->gm_sq, ctx->nloc, ctx->gm_part, ctx->gm_counter, ctx->d_done, ctx->eps_thresh2,
+                          ctx->d_counts, ctx->d_j, ctx->stream));
+    return DUQUAD_OK;
+}
 
 duquad_status trace_lam_copy(duquad_ctx *ctx, int j) {
     if (j >= 2 && ctx->trace_lam && j - 2 < ctx->trace_max)
@@ -293,6 +317,12 @@ duquad_status outer_phase(duquad_ctx *ctx, const std::vector<double> &beta_in, i
     const int64_t off = ctx->rank * ctx->n_slice;
     duquad_status st;
     if (ph == num_phases(ctx, Kin) - 1) return end_outer(ctx, j);
+    if (ctx->eps_mode && ph == num_phases(ctx, Kin) - 2) {   // u_bar^j = x: y, average, flag reset
+        double *ydst = ctx->rho0 ? (Kin % 2 ? ctx->y_full2 : ctx->y_full) : ctx->y_full;
+        CK(launch_inner_finish(ctx->x, ydst, ctx->xhat, ctx->nloc, ctx->d_ops, ctx->d_j, ctx->d_done,
+                               ctx->d_counts + ctx->counts_cap, ctx->stream));
+        return DUQUAD_OK;
+    }
     if (ctx->rho0) {
         double *Y[2] = {ctx->y_full, ctx->y_full2};
         if (ph == 0) {
@@ -320,7 +350,7 @@ duquad_status outer_phase(duquad_ctx *ctx, const std::vector<double> &beta_in, i
             bl.q = ctx->cvec;
             bl.y = Y[(k - 1) % 2] + off;
             bl.beta_in = beta_in[k];
-            bl.last_inner = (k == Kin);
+            bl.last_inner = (k == Kin) && !ctx->eps_mode;
             PassBArgs bs = bl;
             bs.y = Y[k % 2] + off;
             if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 0], ctx->stream));
@@ -341,6 +371,7 @@ duquad_status outer_phase(duquad_ctx *ctx, const std::vector<double> &beta_in, i
                     CK(cudaEventRecord((*ev)[4 * (k - 1) + 3], ctx->stream));
                 }
             }
+            if ((st = inner_check(ctx)) != DUQUAD_OK) return st;
             *gb = (k % 2) ? G_Y2 : G_Y;
         }
         return DUQUAD_OK;
@@ -359,10 +390,11 @@ duquad_status outer_phase(duquad_ctx *ctx, const std::vector<double> &beta_in, i
         } else {
             PassBArgs b = make_b(ctx);
             b.beta_in = beta_in[k];
-            b.last_inner = (k == Kin);
+            b.last_inner = (k == Kin) && !ctx->eps_mode;
             if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 2], ctx->stream));
             CK(launch_fused_epi(b, b, ctx->fz, ctx->stream));
             if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 3], ctx->stream));
+            if ((st = inner_check(ctx)) != DUQUAD_OK) return st;
         }
         return DUQUAD_OK;
     }
@@ -390,10 +422,11 @@ duquad_status outer_phase(duquad_ctx *ctx, const std::vector<double> &beta_in, i
         } else {
             PassBArgs b = make_b(ctx);
             b.beta_in = beta_in[k];
-            b.last_inner = (k == Kin);
+            b.last_inner = (k == Kin) && !ctx->eps_mode;
             CK(launch_pass_b(b, MODE_SOLVE, ctx->cfg_b, ctx->stream));
         }
         if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 3], ctx->stream));
+        if ((st = inner_check(ctx)) != DUQUAD_OK) return st;
         *gb = G_Y;
     }
     return DUQUAD_OK;
@@ -656,6 +689,7 @@ const char *duquad_status_string(int32_t s) {
         case DUQUAD_ENONFINITE: return "non-finite iterate";
         case DUQUAD_ENODEV: return "no suitable CUDA device";
         case DUQUAD_ESTATE: return "call out of order";
+        case DUQUAD_EMAXITER: return "inner iteration cap reached (result valid)";
         default: return "unknown status";
     }
 }
@@ -1132,8 +1166,112 @@ static duquad_status solve_prepare(duquad_ctx *ctx, int alg, int K, int Kin, std
     return DUQUAD_OK;
 }
 
+static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t inner, duquad_result *res);
+
 duquad_status duquad_solve(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t inner, duquad_result *res) {
     if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
+    ctx->eps_mode = false;
+    return solve_body(ctx, alg, outer, inner, res);
+}
+
+duquad_status duquad_solve_eps(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t inner_max, double eps_in,
+                               double sigma_L, duquad_result *res) {
+    if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
+    if (!(eps_in > 0.0) || !(sigma_L > 0.0) || !std::isfinite(eps_in) || !std::isfinite(sigma_L))
+        return fail(ctx, DUQUAD_EINVAL, "eps_in and sigma_L must be finite and > 0");
+    if (ctx->world > 1 || ctx->Btot > 1)
+        return fail(ctx, DUQUAD_EINVAL, "eps_in mode: single GPU, batch 1 only (sharded / batched: fixed counts)");
+    if (outer < 1 || inner_max < 1) return fail(ctx, DUQUAD_EINVAL, "need outer_iters >= 1 and inner_max >= 1");
+    if (!ctx->have_consts) return fail(ctx, DUQUAD_ESTATE, "constants not set (duquad_lipschitz or duquad_set_constants)");
+    DevGuard guard(ctx->dev);
+    const int64_t nc = (int64_t)outer + 1;
+    if (!ctx->gm_sq) {
+        CK(dalloc(&ctx->gm_sq, ctx->nloc));
+        CK(dalloc(&ctx->gm_part, (int64_t)kRedGrid));
+        CK(dalloc(&ctx->gm_counter, 2));
+        CK(dalloc(&ctx->d_done, 2));
+    }
+    if (ctx->counts_cap < nc) {
+        if (ctx->d_counts) cudaFree(ctx->d_counts);
+        ctx->d_counts = nullptr;
+        CK(dalloc(&ctx->d_counts, 2 * nc));
+        ctx->counts_cap = nc;
+    }
+    CK(cudaMemsetAsync(ctx->d_counts, 0, 2 * ctx->counts_cap * sizeof(int32_t), ctx->stream));
+    CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(int32_t), ctx->stream));
+    CK(cudaMemsetAsync(ctx->gm_counter, 0, sizeof(uint32_t), ctx->stream));
+    // stop when L_in ||y - x+|| <= sqrt(2 sigma_L eps_in), i.e. sum (y - x+)^2 <= 2 sigma_L eps_in / L_in^2
+    ctx->eps_thresh2 = 2.0 * sigma_L * eps_in / (ctx->L_in * ctx->L_in);
+    ctx->eps_mode = true;
+    duquad_status st = solve_body(ctx, alg, outer, inner_max, res);
+    ctx->eps_mode = false;
+    if (st != DUQUAD_OK && st != DUQUAD_ENONFINITE) return st;
+    std::vector<int32_t> buf(2 * ctx->counts_cap);
+    CK(cudaMemcpy(buf.data(), ctx->d_counts, buf.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    ctx->last_counts.assign(buf.begin(), buf.begin() + nc);
+    ctx->last_conv.assign(buf.begin() + ctx->counts_cap, buf.begin() + ctx->counts_cap + nc);
+    int64_t total = 0;
+    bool capped = false;
+    for (int64_t j = 0; j < nc; ++j) {
+        total += ctx->last_counts[j];
+        capped |= ctx->last_conv[j] == 0;
+    }
+    if (res) {
+        res->inner_iters_total = total;
+        res->matrix_passes = 2 * total;
+    }
+    if (st != DUQUAD_OK) return st;
+    if (capped) return fail(ctx, DUQUAD_EMAXITER, "an inner solve hit inner_max before the eps_in test (result valid)");
+    return DUQUAD_OK;
+}
+
+duquad_status duquad_theory_schedule(int32_t alg, double eps, double R_d, double L_d, double L_in, double sigma_L,
+                                     double D_U, double normG, double lambda_min_Q, duquad_schedule *out) {
+    if (!out) return fail(nullptr, DUQUAD_EINVAL, "out is NULL");
+    if (alg != DUQUAD_DGM && alg != DUQUAD_DFGM) return fail(nullptr, DUQUAD_EINVAL, "bad alg");
+    const double v[] = {eps, R_d, L_d, L_in, sigma_L, D_U, normG, lambda_min_Q};
+    for (double x : v)
+        if (!std::isfinite(x)) return fail(nullptr, DUQUAD_EINVAL, "non-finite schedule argument");
+    if (!(eps > 0) || !(R_d > 0) || !(L_d > 0) || !(L_in > 0) || sigma_L < 0 || !(D_U > 0) || normG < 0 ||
+        lambda_min_Q < 0)
+        return fail(nullptr, DUQUAD_EINVAL, "schedule arguments out of range");
+    std::memset(out, 0, sizeof(*out));
+    const double q = 8.0 * L_d * R_d * R_d / eps;                         // (choose_ein)
+    if (alg == DUQUAD_DGM) {
+        out->eps_in = eps / 4.0;
+        out->k_out = (int64_t)std::ceil(q);
+    } else {
+        out->eps_in = eps * std::sqrt(eps) / (8.0 * R_d * std::sqrt(2.0 * L_d));
+        out->k_out = (int64_t)std::ceil(std::sqrt(q));
+    }
+    const double d2 = D_U * D_U;
+    double kin;
+    if (sigma_L > 0.0)
+        kin = std::sqrt(L_in / sigma_L) * std::log(L_in * d2 / out->eps_in) + 1.0;
+    else
+        kin = std::sqrt(2.0 * L_in * d2 / out->eps_in);
+    out->k_in = (int64_t)std::ceil(std::max(kin, 1.0));
+    out->rho_star = 8.0 * R_d * R_d / eps;
+    out->k_total = sigma_L > 0.0
+                       ? (int64_t)std::floor(16.0 * normG * R_d / std::sqrt(sigma_L * eps) *
+                                             std::log(8.0 * normG * D_U * R_d / eps))
+                       : (int64_t)std::floor(24.0 * normG * D_U * R_d / eps);
+    out->case_id = lambda_min_Q > 0.0 ? 1 : 2;
+    return DUQUAD_OK;
+}
+
+duquad_status duquad_get_inner_counts(duquad_ctx *ctx, int32_t *counts, int32_t *converged, int32_t max_entries) {
+    if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
+    if (max_entries < 0) return fail(ctx, DUQUAD_EINVAL, "max_entries < 0");
+    const int64_t m = std::min<int64_t>(max_entries, (int64_t)ctx->last_counts.size());
+    for (int64_t j = 0; j < m; ++j) {
+        if (counts) counts[j] = ctx->last_counts[j];
+        if (converged) converged[j] = ctx->last_conv[j];
+    }
+    return DUQUAD_OK;
+}
+
+static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t inner, duquad_result *res) {
     if (alg != DUQUAD_DGM && alg != DUQUAD_DFGM) return fail(ctx, DUQUAD_EINVAL, "bad alg");
     if (outer < 1 || inner < 1) return fail(ctx, DUQUAD_EINVAL, "need outer_iters >= 1 and inner_iters >= 1");
     if (!ctx->have_consts) return fail(ctx, DUQUAD_ESTATE, "constants not set (duquad_lipschitz or duquad_set_constants)");
@@ -1147,7 +1285,7 @@ duquad_status duquad_solve(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t 
     }
     duquad_status st;
     if ((st = allgather_y(ctx)) != DUQUAD_OK) return st;
-    if (ctx->small) {   // whole solve in one single-CTA kernel (K4)
+    if (ctx->small && !ctx->eps_mode) {   // whole solve in one single-CTA kernel (K4)
         if (ctx->beta_cap < Kin + 1) {
             if (ctx->d_beta) cudaFree(ctx->d_beta);
             ctx->d_beta = nullptr;

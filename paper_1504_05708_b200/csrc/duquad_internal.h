@@ -55,6 +55,7 @@ struct PassAArgs {
     const int32_t *rp;   // row pointers (rows + 1), rebased to 0
     const int32_t *ci;   // column indices
     const double *va;    // values
+    const int32_t *skip; // eps_in mode: the inner solve has converged -> the launch does nothing
 };
 
 // ---------------------------------------------------------------- pass B
@@ -84,6 +85,8 @@ struct PassBArgs {
     const int32_t *rp;
     const int32_t *ci;
     const double *va;
+    const int32_t *skip; // eps_in mode: the inner solve has converged -> the launch does nothing
+    double *gm_sq;       // eps_in mode: gm_sq[j] = (y_j - x+_j)^2 (gradient-map test)
 };
 
 // ---------------------------------------------------------------- batched (B QPs, shared Q, G)
@@ -203,6 +206,14 @@ cudaError_t launch_init_state(double *x, double *y, double *xhat, const double *
                               int64_t n, double *mu, double *lam_prev, int64_t p, int32_t *d_j,
                               int32_t *flag, cudaStream_t s);
 cudaError_t launch_advance(int32_t *d_j, cudaStream_t s);
+// eps_in mode (duquad_solve_eps): after an inner step, sum gm_sq (fixed order; partials + the last
+// block) -> counts[*d_j - 1] += 1 and *done = 1 if L_in^2 sum <= 2 sigma eps_in (thresh2 = that / L_in^2)
+cudaError_t launch_inner_check(const double *gm_sq, int64_t n, double *partials, uint32_t *counter, int32_t *done,
+                               double thresh2, int32_t *counts, const int32_t *d_j, cudaStream_t s);
+// after the inner loop: y_dst = x (u_bar^j), running average with ops[*d_j].avg_w, conv[*d_j - 1] = *done,
+// *done = 0
+cudaError_t launch_inner_finish(const double *x, double *y_dst, double *xhat, int64_t n, const OuterParam *ops,
+                                const int32_t *d_j, int32_t *done, int32_t *conv, cudaStream_t s);
 cudaError_t launch_transpose(const double *G, int64_t ldG, int64_t p, int64_t col0, int64_t ncols,
                              double *GT, int64_t ldp, cudaStream_t s);
 cudaError_t launch_check(const double *v, int64_t rows, int64_t cols, int64_t ld, int32_t *flag,

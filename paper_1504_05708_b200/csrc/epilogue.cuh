@@ -127,6 +127,10 @@ __device__ __forceinline__ void epi_b_store(const PassBArgs &b, int mode, int64_
     const double xn = fmin(fmax(e.y - grad / b.L_in, e.lb), e.ub);
     const double yn = b.last_inner ? xn : xn + b.beta_in * (xn - e.x);
     if (avg_w != 0.0) b.xhat[j] = e.xh + avg_w * (xn - e.xh);      // P:700-706 (running form)
+    if (b.gm_sq) {                                                 // eps_in mode: ||y - x+||^2 terms
+        const double dd = e.y - xn;
+        b.gm_sq[j] = dd * dd;
+    }
     b.x[j] = xn;
     b.y[j] = yn;
     if (!isfinite(xn) || !isfinite(yn)) *b.flag = 1;

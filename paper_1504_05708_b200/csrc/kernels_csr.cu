@@ -107,6 +107,7 @@ __device__ __forceinline__ void csr_row_dot2(const int32_t *__restrict__ ci, con
 
 template <int MODE, int GS>
 __global__ void __launch_bounds__(kCsrThreads) k_pass_a_csr(const PassAArgs a) {
+    if (a.skip && *a.skip) return;
     const int lane = threadIdx.x & 31, gl = lane & (GS - 1), gw = lane / GS;
     const int64_t gpw = 32 / GS;   // lane groups per warp; a warp covers 2 * gpw consecutive rows
     const int64_t warp_id = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -136,6 +137,7 @@ __global__ void __launch_bounds__(kCsrThreads) k_pass_a_csr(const PassAArgs a) {
 
 template <int MODE, int GS>
 __global__ void __launch_bounds__(kCsrThreads) k_pass_b_csr(const PassBArgs b) {
+    if (b.skip && *b.skip) return;
     const int lane = threadIdx.x & 31, gl = lane & (GS - 1), gw = lane / GS;
     const int64_t gpw = 32 / GS;
     const int64_t warp_id = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;

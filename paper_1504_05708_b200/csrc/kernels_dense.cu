@@ -19,6 +19,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "duquad_internal.h"
 #include "epilogue.cuh"
 
@@ -75,6 +77,7 @@ __device__ __forceinline__ void stage(double *s, const double *g, int64_t len) {
 
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1) k_pass_a(const PassAArgs a) {
+    if (a.skip && *a.skip) return;
     extern __shared__ __align__(16) double smem[];
     stage(smem, a.y, a.ld);
     __syncthreads();
@@ -97,6 +100,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass_a(const PassAArgs a) {
 
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1) k_pass_b(const PassBArgs b) {
+    if (b.skip && *b.skip) return;
     extern __shared__ __align__(16) double smem[];
     stage(smem, b.w, b.ldp);
     __syncthreads();
@@ -123,6 +127,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass_b(const PassBArgs b) {
 // y is read (staged) from yin and written to yout (ping-pong: every CTA stages all of y).
 __global__ void __launch_bounds__(kThreads, 1) k_rho0_step(const PassAArgs a, const PassBArgs bl,
                                                           const PassBArgs bs) {
+    if (a.skip && *a.skip) return;
     extern __shared__ __align__(16) double smem[];
     stage(smem, a.y, a.ld);
     __syncthreads();
@@ -165,6 +170,52 @@ __global__ void k_init_state(double *x, double *y, double *xhat, const double *l
 }
 
 __global__ void k_advance(int32_t *d_j) { *d_j += 1; }
+
+// eps_in mode: gradient-map test after an inner step (fixed-order sum: block partials over
+// contiguous ranges, then the last block to finish adds them in block order)
+__global__ void k_inner_check(const double *gm_sq, int64_t n, double *partials, uint32_t *counter, int32_t *done,
+                              double thresh2, int32_t *counts, const int32_t *d_j) {
+    if (*done) return;
+    __shared__ double red[32];
+    __shared__ bool last;
+    const int64_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
+    double s = 0.0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) s += gm_sq[i];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double b = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b += red[w];
+        partials[blockIdx.x] = b;
+        __threadfence();
+        last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        double t = 0.0;
+        for (int c = 0; c < (int)gridDim.x; ++c) t += partials[c];
+        counts[*d_j - 1] += 1;
+        if (t <= thresh2) *done = 1;
+        *counter = 0;
+    }
+}
+
+__global__ void k_inner_finish(const double *x, double *y_dst, double *xhat, int64_t n, const OuterParam *ops,
+                               const int32_t *d_j, int32_t *done, int32_t *conv) {
+    const double w = ops[*d_j].avg_w;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double xi = x[i];
+        y_dst[i] = xi;                                         // y = u_bar^j for the next outer iteration
+        if (w != 0.0) xhat[i] = xhat[i] + w * (xi - xhat[i]);  // P:700-706 (running form)
+    }
+}
+
+__global__ void k_inner_reset(const int32_t *d_j, int32_t *done, int32_t *conv) {
+    conv[*d_j - 1] = *done;
+    *done = 0;
+}
 
 // out[j - col0][i] = G[i][j] for j in [col0, col0 + ncols), i in [0, p)
 __global__ void k_transpose(const double *__restrict__ G, int64_t ldG, int64_t p, int64_t col0,
@@ -361,6 +412,20 @@ cudaError_t launch_init_state(double *x, double *y, double *xhat, const double *
     const int64_t m = n > p ? n : p;
     k_init_state<<<blocks_for(m > 0 ? m : 1, 256), 256, 0, s>>>(x, y, xhat, lb, ub, n, mu, lam_prev, p,
                                                                d_j, flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_inner_check(const double *gm_sq, int64_t n, double *partials, uint32_t *counter, int32_t *done,
+                               double thresh2, int32_t *counts, const int32_t *d_j, cudaStream_t s) {
+    k_inner_check<<<kRedGrid, kRedThreads, 0, s>>>(gm_sq, n, partials, counter, done, thresh2, counts, d_j);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_inner_finish(const double *x, double *y_dst, double *xhat, int64_t n, const OuterParam *ops,
+                                const int32_t *d_j, int32_t *done, int32_t *conv, cudaStream_t s) {
+    const int grid = (int)std::min<int64_t>(1184, std::max<int64_t>(1, (n + 255) / 256));
+    k_inner_finish<<<grid, 256, 0, s>>>(x, y_dst, xhat, n, ops, d_j, done, conv);
+    k_inner_reset<<<1, 1, 0, s>>>(d_j, done, conv);
     return cudaGetLastError();
 }
 

@@ -154,6 +154,7 @@ __device__ __forceinline__ Tile tile_of(const FusedArgs &f, int J) {
 // Launched with a cluster dimension of 2 when there is a G role (pairs), 1 otherwise.
 template <int NCHG>
 __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f) {
+    if (f.a.skip && *f.a.skip) return;   // eps_in mode: converged (uniform over the grid)
     constexpr int kSlotsG = kSlots - (NCHG > 0 ? NCHG : 1);
     extern __shared__ __align__(128) uint8_t fsm[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -501,6 +502,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
 constexpr int kEpiCols = 32, kEpiSlices = 8;
 __global__ void __launch_bounds__(kEpiCols *kEpiSlices) k_fused_epi(const PassBArgs bl, const PassBArgs bs,
                                                                     const FusedArgs f) {
+    if (bl.skip && *bl.skip) return;
     __shared__ double part[kEpiSlices][kEpiCols];
     const int cl = threadIdx.x % kEpiCols, sl = threadIdx.x / kEpiCols;
     const int64_t j = (int64_t)blockIdx.x * kEpiCols + cl;

@@ -61,6 +61,16 @@ def solve_emulated(solvers, alg: str = "DFGM", outer: int = 1, inner: int = 1):
             solvers[0]._ctx)
 
 
+def theory_schedule(alg: str, eps: float, R_d: float, L_d: float, L_in: float, sigma_L: float, D_U: float,
+                    normG: float, lambda_min_Q: float = 0.0) -> dict:
+    """DuQuad's theory schedule (include/duquad.h duquad_theory_schedule; host arithmetic)."""
+    out = L.Schedule()
+    L.check(L.lib().duquad_theory_schedule(_ALGS[alg], float(eps), float(R_d), float(L_d), float(L_in),
+                                           float(sigma_L), float(D_U), float(normG), float(lambda_min_Q),
+                                           C.byref(out)))
+    return {k: getattr(out, k) for k, _ in L.Schedule._fields_ if k != "reserved"}
+
+
 class Solver:
     """One DuQuad context: setup (pack + upload), constants, solve, results.
 
@@ -196,6 +206,26 @@ class Solver:
         L.check(self._lib.duquad_solve(self._ctx, _ALGS[alg], int(outer), int(inner), C.byref(res)), self._ctx)
         self.last_result = {k: getattr(res, k) for k, _ in L.Result._fields_}
         return self.last_result
+
+    def solve_eps(self, alg: str = "DFGM", outer: int = 1, inner_max: int = 1000, eps_in: float = 1e-6,
+                  sigma_L: float = 1.0) -> dict:
+        """DFOM with eps_in-driven inner stopping (duquad_solve_eps).  The report gets 'inner_counts'
+        and 'converged' (per outer iteration + the last-iterate solve) and 'capped' (EMAXITER)."""
+        res = L.Result()
+        st = self._lib.duquad_solve_eps(self._ctx, _ALGS[alg], int(outer), int(inner_max), float(eps_in),
+                                        float(sigma_L), C.byref(res))
+        if st not in (L.DUQUAD_OK, L.DUQUAD_EMAXITER):
+            L.check(st, self._ctx)
+        info = {k: getattr(res, k) for k, _ in L.Result._fields_}
+        m = int(outer) + 1
+        counts = (C.c_int32 * m)()
+        conv = (C.c_int32 * m)()
+        L.check(self._lib.duquad_get_inner_counts(self._ctx, counts, conv, m), self._ctx)
+        info["inner_counts"] = list(counts)
+        info["converged"] = [bool(c) for c in conv]
+        info["capped"] = st == L.DUQUAD_EMAXITER
+        self.last_result = info
+        return info
 
     def result(self, device: bool = False):
         """(x_last, x_avg, lambda) local slices; NumPy on the host or torch on the device.

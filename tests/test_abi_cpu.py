@@ -103,3 +103,24 @@ def test_product_package_does_not_touch_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in txt.replace("oracle/", "").lower() or f == "__init__.py", f
                 assert "import oracle" not in txt and "from oracle" not in txt, f
+
+
+def test_theory_schedule_host_only(lib):
+    """duquad_theory_schedule is host arithmetic (no device): the same numbers as the oracle's
+    theory_schedule (which tests/test_oracle_pins.py pins to Theorem 1 and Lemma 1)."""
+    from oracle import dfom as O
+    from paper_1504_05708_b200 import theory_schedule, _lib
+    for alg in ("DGM", "DFGM"):
+        for args in [(1e-2, 1.0, 1.0, 40.0, 0.5, 2.0, 3.0, 0.1), (1e-3, 3.7, 0.25, 1e4, 0.0, 1.0, 7.0, 0.0),
+                     (0.5, 12.0, 40.0, 9.0, 1e-3, 2.0, 1.5, 0.0)]:
+            got = theory_schedule(alg, *args)
+            want = O.theory_schedule(alg, *args[:7], lambda_min_Q=args[7])
+            for k in ("k_out", "k_in", "k_total", "case_id"):
+                assert got[k] == want[k], (alg, args, k)
+            for k in ("eps_in", "rho_star"):
+                assert got[k] == pytest.approx(want[k], rel=1e-14), (alg, args, k)
+    out = _lib.Schedule()
+    assert lib.duquad_theory_schedule(1, -1.0, 1, 1, 1, 0, 1, 1, 0, C.byref(out)) == _lib.DUQUAD_EINVAL
+    assert lib.duquad_theory_schedule(1, 1e-2, 1, 1, 1, float("nan"), 1, 1, 0, C.byref(out)) == _lib.DUQUAD_EINVAL
+    assert lib.duquad_theory_schedule(7, 1e-2, 1, 1, 1, 0, 1, 1, 0, C.byref(out)) == _lib.DUQUAD_EINVAL
+    assert lib.duquad_status_string(_lib.DUQUAD_EMAXITER).startswith(b"inner iteration cap")

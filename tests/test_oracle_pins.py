@@ -386,3 +386,77 @@ def test_fgm_accelerates_over_gm():
         x = O.fom(lambda y: Q @ y + q, np.zeros(8), 1.0, lb, ub, 200, rule)
         gaps[rule] = 0.5 * x @ Q @ x + q @ x - ref.F
     assert gaps[O.INNER_FGM] < 0.5 * gaps[O.INNER_GM]
+
+
+# ---------------------------------------------------------------- NEXT-1: eps_in stopping, schedules
+@pytest.mark.parametrize("kind,rho,eps_in", [("ineq", 0.0, 1e-4), ("ineq", 1.0, 1e-6), ("eq", 0.0, 1e-6),
+                                             ("mixed", 2.0, 1e-5)])
+def test_eps_inner_stop_meets_duquad_in(kind, rho, eps_in):
+    """The gradient-map test of fom_run guarantees Eq. (duquad_in), P:445-451:
+    L_rho(u_bar, mu) - d_rho(mu) <= eps_in, with d_rho(mu) from a 20000-step solve (which is
+    within ~1e-13 of the minimum here, so the check is effectively against the exact value)."""
+    prob = qpgen.tiny(8, 5, seed=11, kind=kind, shift=0.3)
+    L_in, _, _ = O.lipschitz_constants(prob.Q, prob.G, rho, 0.1)
+    sigma_L = float(np.linalg.eigvalsh(prob.Q)[0])     # <= lambda_min of the Hessian of L_rho(., mu)
+    rng = np.random.default_rng(3)
+    mu = rng.standard_normal(5) * 2.0
+    x0 = O.clamp_U(np.zeros(8), prob.lb, prob.ub)
+    info, gm = [], []
+    ub = O.inner_solve(prob.Q, prob.q, prob.G, prob.g, prob.cone, rho, mu, x0, L_in, prob.lb, prob.ub, 5000,
+                       eps_in=eps_in, sigma_L=sigma_L, gm=gm, info=info)
+    k, conv = info[0]
+    thr = np.sqrt(2 * sigma_L * eps_in)
+    assert conv and k < 5000 and gm[-1] <= thr and all(v > thr for v in gm[:-1])
+    d_rho, _ = O.dual_value(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho, mu, L_in)
+    gap = O.aug_lagrangian(prob.Q, prob.q, prob.G, prob.g, prob.cone, rho, ub, mu) - d_rho
+    assert -1e-12 <= gap <= eps_in, gap
+    # the fixed-count solve with the same number of steps is the same iterate
+    same = O.inner_solve(prob.Q, prob.q, prob.G, prob.g, prob.cone, rho, mu, x0, L_in, prob.lb, prob.ub, k)
+    assert np.array_equal(same, ub)
+
+
+@pytest.mark.parametrize("alg", [O.DGM, O.DFGM])
+@pytest.mark.parametrize("eps,R_d,L_d", [(1e-2, 1.0, 1.0), (1e-3, 3.7, 0.25), (0.5, 12.0, 40.0),
+                                         (1e-4, 0.2, 7.5)])
+def test_schedule_satisfies_theorem1_and_lemma1(alg, eps, R_d, L_d):
+    """(choose_ein) is derived by making Theorem 1's bound (bound_gen_dfg)
+    at most eps: evaluate that bound at (k_out, eps_in).  k_in comes from Lemma 1
+    (bound_gen_dfg1) with R_phi <= D_U: evaluate Lemma 1 at k_in, both regimes."""
+    for sigma_L, L_in, D_U in [(0.5, 40.0, 2.0), (0.0, 40.0, 2.0), (1e-3, 1e4, 1.0)]:
+        s = O.theory_schedule(alg, eps, R_d, L_d, L_in, sigma_L, D_U, normG=3.0)
+        assert O.theorem1_bound(alg, s["k_out"], L_d, R_d, s["eps_in"]) <= eps * (1 + 1e-12)
+        assert O.lemma1_bound(s["k_in"], L_in, sigma_L, D_U, p=2) <= s["eps_in"] * (1 + 1e-12)
+        # not wasteful: (choose_ein) takes k_out = q (DGM) / sqrt(q) (DFGM), q = 8 L_d R_d^2 / eps,
+        # while the first term needs (k+1)^p >= q; two outer iterations fewer miss eps/2
+        p = 1 if alg == O.DGM else 2
+        assert s["k_out"] < 2 or 4 * L_d * R_d ** 2 / (s["k_out"] - 1) ** p >= eps / 2 * (1 - 1e-9)
+        assert s["rho_star"] == pytest.approx(8 * R_d ** 2 / eps, rel=1e-15)
+    assert O.theory_schedule(alg, eps, R_d, L_d, 40.0, 0.5, 2.0, 3.0, lambda_min_Q=0.1)["case_id"] == 1
+    assert O.theory_schedule(alg, eps, R_d, L_d, 40.0, 0.5, 2.0, 3.0, lambda_min_Q=0.0)["case_id"] == 2
+
+
+@pytest.mark.parametrize("alg", [O.DGM, O.DFGM])
+@pytest.mark.parametrize("seed", [21, 22])
+def test_dfom_on_the_schedule_reaches_eps(alg, seed):
+    """Theorem 1's conclusion: with eps_in and k_out from (choose_ein) and inner solves stopped at
+    accuracy eps_in, F* - d_rho(lambda^{k_out}) <= eps (Case 1: Q > 0, rho = 0), with
+    F* and R_d = ||lambda*|| from brute-force active-set enumeration (oracle.kkt)."""
+    from oracle import kkt
+    prob = qpgen.tiny(6, 4, seed=seed, kind="ineq", shift=1.0)
+    G = 0.4 * prob.G
+    g = 0.4 * prob.g
+    ref = kkt.brute_force(prob.Q, prob.q, G, g, prob.lb, prob.ub, prob.cone)
+    lmin = float(np.linalg.eigvalsh(prob.Q)[0])
+    normG2 = float(np.linalg.eigvalsh(G.T @ G)[-1])
+    L_in = float(np.linalg.eigvalsh(prob.Q)[-1])
+    L_d = normG2 / lmin
+    R_d = max(float(np.linalg.norm(ref.lam)), 1e-3)
+    eps = 0.05
+    s = O.theory_schedule(alg, eps, R_d, L_d, L_in, lmin, 2.0, np.sqrt(normG2), lmin)
+    assert s["case_id"] == 1 and s["k_out"] <= 2000
+    r = O.dfom(prob.Q, prob.q, G, g, prob.lb, prob.ub, prob.cone, 0.0, alg, s["k_out"], 100000, L_in, L_d,
+               eps_in=s["eps_in"], sigma_L=lmin)
+    assert all(r.converged)
+    d, _ = O.dual_value(prob.Q, prob.q, G, g, prob.lb, prob.ub, prob.cone, 0.0, r.lam, L_in)
+    assert ref.F - d <= eps, (ref.F - d, eps)
+    assert ref.F - d >= -1e-9                       # weak duality (P:223-229)
