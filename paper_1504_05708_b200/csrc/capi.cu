@@ -1002,17 +1002,15 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
     }
     if (!batched && ctx->world == 1 && opt.fused_path &&
         fused_supported(n, ctx->ld, prop.sharedMemPerBlockOptin)) {   // byte-floor inner step
-        int cg = (!ctx->rho0 && p > 0) ? 2 : 1;   // G-role cluster size (pairs: 148 SMs usable)
-        if (const char *ov = std::getenv("DUQUAD_FUSED_CG")) cg = std::atoi(ov) == 4 ? 4 : 2;
-        if (ctx->rho0 || p == 0) cg = 1;
+        const int cg = (!ctx->rho0 && p > 0) ? 2 : 1;   // G role: CTA pairs (148 SMs usable)
         const int nchg = cg > 1 ? fused_nchg(ctx->ld, cg) : 0;
         CKS(configure_fused_kernels(nchg, fused_smem_bytes()));
         const int maxc = fused_max_clusters(nchg, cg, fused_smem_bytes());
         const int nb = std::min(ctx->num_sms / cg, maxc > 0 ? maxc : ctx->num_sms / cg) * cg;
         int nq = nb;                        // rho = 0 (K3) or p = 0: Q role only
         if (cg > 1) {
-            // Q : G split by bytes, G weighted by its measured per-byte cost (config 2: nq = 64 of 148)
-            double gw = 1.31;
+            // Q : G split by bytes, G weighted by its measured per-byte cost (config 2: nq = 66 of 148)
+            double gw = 1.24;
             if (const char *ov = std::getenv("DUQUAD_FUSED_GW")) gw = std::atof(ov);
             const double bq = 0.5 * (double)n * (double)(n + 1), bg = gw * (double)p * (double)n;
             nq = cg * (int)std::llround((double)nb / cg * bq / (bq + bg));

@@ -134,7 +134,7 @@ struct FusedArgs {
     const FusedPiece *pieces;   // [nq] (device)
     int64_t n, p, ld;
     int32_t nt;            // Q tile columns: [4096 J, min(4096 (J + 1), ld))
-    int32_t cg;            // G-role cluster size (2 or 4)
+    int32_t cg;            // G-role cluster size (2)
     int32_t W;             // G column blocks [c W, (c + 1) W), c < cg (the last ends at ld)
     int32_t nchg;          // G: chunks of 4096 columns per block (template parameter)
     int32_t nb;            // grid (CTAs), a multiple of cg

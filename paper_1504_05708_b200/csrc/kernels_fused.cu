@@ -18,7 +18,7 @@
 //    into row r's dot (per-warp sums -> ws_rowp[J][warp][r]; no cross-warp sync) and Q_rc y_r into column c
 //    (registers -> ws_col[cta][J - j0] when the CTA leaves tile column J).  The host cuts the
 //    sequence into pieces of equal estimated time, max(bytes, per-step cost) summed.
-//  * G role (thread-block clusters of cg = 2 or 4 CTAs): rank c owns column block c
+//  * G role (CTA pairs = thread-block clusters of 2): rank c owns column block c
 //    ([c W, (c+1) W)) of a range of G rows.  Per row: the block's partial dot -> the last warp to
 //    post its partial (shared-memory counter) sends the CTA sum to every CTA of the cluster through distributed shared memory (st.async with mbarrier
 //    complete_tx), adds the block partials in rank order and applies the pass-A epilogue (w_i =
@@ -53,7 +53,6 @@ constexpr int kSlots = 7;               // per-thread ring depth (chunks; 224 KB
 // G role: a (kSlots - NCHG)-chunk ring + this CTA's block of y (NCHG chunks) in the same space
 constexpr int kD = 8;                   // depth of the per-row buffers / barriers (G rows)
 constexpr int kHdr = 3072;              // barriers + per-row buffers; header + ring = 227 KB
-constexpr int kMaxCg = 4;               // G-role cluster size (2 or 4)
 static_assert(kThreadsF * kV * 2 == kChunk, "chunk = 512 threads x 8 doubles");
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -160,23 +159,15 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int cta = blockIdx.x;
     // ---- shared memory: barriers + small per-row buffers (first 8 KB), then the ring
-    uint64_t *xbar = reinterpret_cast<uint64_t *>(fsm);    // [kD] cluster exchange (st.async bytes)
-    uint64_t *wbar = xbar + kD;                            // [kD] w ready (1 arrival)
-    uint32_t *cnt = reinterpret_cast<uint32_t *>(wbar + kD);   // [kD] warps that posted a G row
-    double *red = reinterpret_cast<double *>(fsm + 512);   // [kD][16] warp partials of a G row
-    double *xbuf = red + kD * 16;                          // [kD][kMaxCg] block partials (st.async)
-    double *wbuf = xbuf + kD * kMaxCg;                     // [kD] w of the row
-    double *epib = wbuf + kD;                              // [kD][4] g, mu, lambda_prev, cone of the row
+    uint64_t *xbar = reinterpret_cast<uint64_t *>(fsm);    // [kD] pair exchange (st.async bytes)
+    double *xbuf = reinterpret_cast<double *>(fsm + 128);  // [kD][32] warp partials of a G row, rank-major
+    double *epib = xbuf + kD * 32;                         // [kD][4] g, mu, lambda_prev, cone of the row
     const double2 *ring = reinterpret_cast<const double2 *>(fsm + kHdr) + tid;   // [kSlots][kV][512]
     const uint32_t ring_u32 = smem_u32(ring);
     auto slot_addr = [&](int s, int k) -> uint32_t { return ring_u32 + (uint32_t)((s * kV + k) * kThreadsF) * 16; };
 
     if (tid == 0) {
-        for (int s = 0; s < kD; ++s) {
-            mbar_init(&xbar[s], 1);   // this CTA's expect_tx arrival + cg x 8 bytes of st.async
-            mbar_init(&wbar[s], 1);
-            cnt[s] = 0;
-        }
+        for (int s = 0; s < kD; ++s) mbar_init(&xbar[s], 1);   // warp 0's expect_tx + 32 x 8 bytes of st.async
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -336,10 +327,10 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
     } else if constexpr (NCHG > 0) {
         // ================================ G role: pair gi owns rows [g0, g1); this CTA block `rank`
         const uint32_t rank = cluster_rank();
-        const int a = (int)rank * f.W, b = (int)rank + 1 == f.cg ? (int)f.ld : a + f.W;
+        const int a = (int)rank * f.W, b = rank == 1 ? (int)f.ld : f.W;
         const int nch = (b - a + kChunk - 1) / kChunk;
         const bool ragged = ((b - a) % kChunk) != 0;
-        const int gi = (cta - f.nq_ctas) / f.cg;
+        const int gi = (cta - f.nq_ctas) >> 1;
         const int64_t g0 = f.p * gi / f.ng, g1 = f.p * (gi + 1) / f.ng;
         const int nr = (int)(g1 - g0);
         // The G role keeps this CTA's block of y in shared memory (after a kSlotsG-slot ring) and
@@ -399,13 +390,13 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
             }
             return part;
         };
-        // Row finishing by the LAST warp to post its partial (shared-memory counter): CTA sum of
-        // the 16 warp partials (fixed tree), block partial -> every CTA of the cluster with st.async,
-        // rank-order sum of the block partials, pass-A epilogue -> w.  The epilogue operands of
-        // row it are prefetched into shared memory two rows ahead by thread 0.
+        // Row finishing: the LAST warp to post its partial (shared-memory counter) forms the CTA sum
+        // of the 16 warp partials (fixed tree) and sends it to every CTA of the cluster with
+        // st.async (completing the rows' exchange barrier); every warp then forms w itself (row_w).
+        // The epilogue operands of row it are prefetched into shared memory two rows ahead.
         const OuterA o = outer_a(f.a, MODE_SOLVE);
-        const uint32_t xb_r = map_to_cta(smem_u32(xbuf), (uint32_t)(lane % f.cg));
-        const uint32_t xm_r = map_to_cta(smem_u32(xbar), (uint32_t)(lane % f.cg));
+        const uint32_t xb_r = map_to_cta(smem_u32(xbuf), (uint32_t)(lane & 1));
+        const uint32_t xm_r = map_to_cta(smem_u32(xbar), (uint32_t)(lane & 1));
         auto prefetch_epi = [&](int it) {
             if (tid == 0 && it < nr) {
                 const EpiA e = epi_a_load(f.a, MODE_SOLVE, f.a.nq + g0 + it, o);
@@ -416,37 +407,34 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
                 eb[3] = (double)e.c;
             }
         };
+        // Row finishing without any intra-CTA hand-off: every warp sends its partial of the row to
+        // both CTAs of the pair (st.async into xbuf[d][rank * 16 + warp], completing 8 bytes of the
+        // row's exchange barrier there; warp 0 arms the barrier for all 32 partials), then waits for
+        // the barrier and forms w itself: fixed butterfly over the 32 partials, pass-A epilogue.
         auto post = [&](int it, double part) {
             part = warp_sum(part);
             const int d = it % kD;
-            uint32_t last = 0;
-            if (lane == 0) {
-                red[d * 16 + warp] = part;
-                __threadfence_block();
-                last = atomicAdd(&cnt[d], 1u) == kWarps - 1;
-            }
-            if (!__shfl_sync(0xffffffffu, last, 0)) return;
-            __threadfence_block();
-            if (lane == 0) cnt[d] = 0;
-            double v = lane < 16 ? red[d * 16 + lane] : 0.0;
-            v = sum16(v);
-            if (lane < f.cg)   // lane c: this block's partial -> CTA c of the cluster
-                st_async_f64(xb_r + (uint32_t)(d * kMaxCg + rank) * 8, v, xm_r + (uint32_t)d * 8);
-            if (lane == 0) mbar_arrive_expect_tx(&xbar[d], (uint32_t)(8 * f.cg));
+            if (lane < 2)   // lane c -> CTA c of the pair
+                st_async_f64(xb_r + (uint32_t)(d * 32 + (int)rank * kWarps + warp) * 8, part,
+                             xm_r + (uint32_t)d * 8);
+            if (warp == 0 && lane == 0) mbar_arrive_expect_tx(&xbar[d], 2u * kWarps * 8u);
+        };
+        auto row_w = [&](int it) -> double {
+            const int d = it % kD;
             mbar_wait(&xbar[d], (uint32_t)((it / kD) & 1));
-            if (lane == 0) {
-                double s_row = xbuf[d * kMaxCg];   // block partials added in rank order
-                for (int c = 1; c < f.cg; ++c) s_row += xbuf[d * kMaxCg + c];
-                const double *eb = epib + d * 4;
-                EpiA e;
-                e.g = eb[0];
-                e.mu = eb[1];
-                e.lp = eb[2];
-                e.c = (uint8_t)eb[3];
-                wbuf[d] = g_row_w(f.a, g0 + it, s_row, e, o, rank == 0);
-                mbar_arrive(&wbar[d]);
-            }
-            __syncwarp();
+            double s_row = xbuf[d * 32 + lane];
+            s_row += __shfl_xor_sync(0xffffffffu, s_row, 16);
+            s_row += __shfl_xor_sync(0xffffffffu, s_row, 8);
+            s_row += __shfl_xor_sync(0xffffffffu, s_row, 4);
+            s_row += __shfl_xor_sync(0xffffffffu, s_row, 2);
+            s_row += __shfl_xor_sync(0xffffffffu, s_row, 1);
+            const double *eb = epib + d * 4;
+            EpiA e;
+            e.g = eb[0];
+            e.mu = eb[1];
+            e.lp = eb[2];
+            e.c = (uint8_t)eb[3];
+            return g_row_w(f.a, g0 + it, s_row, e, o, rank == 0 && warp == 0 && lane == 0);
         };
         prefetch_epi(0);
         prefetch_epi(1);
@@ -464,9 +452,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
             double next0[8];
             double part = 0.0;
             if (nxt) part = take(0, next0, part);                    // row it+1, chunk 0
-            const int d = it % kD;
-            mbar_wait(&wbar[d], (uint32_t)((it / kD) & 1));
-            const double w = wbuf[d];
+            const double w = row_w(it);
 #pragma unroll
             for (int m = 0; m < NCHG; ++m)                              // w G of row it
 #pragma unroll
@@ -548,7 +534,7 @@ cudaError_t launch_t(const FusedArgs &f, cudaStream_t s) {
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = NCHG > 0 ? f.cg : 1;
+    at[0].val.clusterDim.x = NCHG > 0 ? 2 : 1;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
@@ -576,9 +562,9 @@ int fused_block_width(int64_t ld, int cg) { return (int)((ld + 32 * cg - 1) / (3
 int fused_nchg(int64_t ld, int cg) { return (fused_block_width(ld, cg) + kChunk - 1) / kChunk; }
 int fused_tiles(int64_t ld) { return (int)((ld + kChunk - 1) / kChunk); }
 size_t fused_smem_bytes() { return kHdr + (size_t)kSlots * kChunk * 8; }
-static_assert(2 * kD * 8 + kD * 4 <= 512 && 512 + kD * (16 + kMaxCg + 1 + 4) * 8 <= kHdr, "header layout");
+static_assert(kD * 8 <= 128 && 128 + kD * (32 + 4) * 8 <= kHdr, "header layout");
 bool fused_supported(int64_t n, int64_t ld, size_t smem_optin) {
-    return n >= 4096 && fused_nchg(ld, 4) <= 2 && fused_tiles(ld) <= kFusedMaxTiles && fused_smem_bytes() <= smem_optin;
+    return n >= 4096 && fused_nchg(ld, 2) <= 2 && fused_tiles(ld) <= kFusedMaxTiles && fused_smem_bytes() <= smem_optin;
 }
 
 // Clusters of `cg` CTAs of the stream kernel that can be resident at once (0 on error).
