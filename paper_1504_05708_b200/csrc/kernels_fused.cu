@@ -492,6 +492,9 @@ __global__ void __launch_bounds__(kEpiCols *kEpiSlices) k_fused_epi(const PassBA
     __shared__ double part[kEpiSlices][kEpiCols];
     const int cl = threadIdx.x % kEpiCols, sl = threadIdx.x / kEpiCols;
     const int64_t j = (int64_t)blockIdx.x * kEpiCols + cl;
+    const double avg_w = avg_weight(bl, MODE_SOLVE);
+    EpiB e{};
+    if (sl == 0 && j < bl.nrows) e = epi_b_load(bl, MODE_SOLVE, j, avg_w);   // overlaps the partial loads
     double s = 0.0;
     if (j < bl.nrows) {
         const int Jc = (int)(j / kChunk);
@@ -518,8 +521,6 @@ __global__ void __launch_bounds__(kEpiCols *kEpiSlices) k_fused_epi(const PassBA
         double t = part[0][cl];
 #pragma unroll
         for (int q = 1; q < kEpiSlices; ++q) t += part[q][cl];
-        const double avg_w = avg_weight(bl, MODE_SOLVE);
-        EpiB e = epi_b_load(bl, MODE_SOLVE, j, avg_w);
         e.qy = t;
         epi_b_store(bs, MODE_SOLVE, j, 0.0, e, avg_w);
     }
