@@ -62,7 +62,9 @@ typedef struct duquad_ctx duquad_ctx;
 
 /*
  * Problem data.  Single QP (batch == 1):
- *   Q   n x n, symmetric positive (semi)definite;
+ *   Q   n x n, symmetric positive (semi)definite; dense Q is checked at
+ *       setup on a single GPU (EINVAL unless |Q_ij - Q_ji| <= 1e-12 (|Q_ij| + |Q_ji|)), because
+ *       the byte-floor and small-QP kernels read Q through its symmetry;
  *   G   p x n;  q n;  g p;  lb, ub n (entries may be -INFINITY / +INFINITY);
  *   cone p tags (DUQUAD_CONE_*), or NULL meaning every row is cone_all.
  * Batched (batch = B > 1, dense only; north_star (c)): Q and G are shared,

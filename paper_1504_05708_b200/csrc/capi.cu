@@ -973,6 +973,18 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
             return bail(DUQUAD_EINVAL);
         }
     }
+    if (!csr && ctx->nloc == n && n > 0) {   // the byte-floor and small kernels read Q by symmetry
+        CKS(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int32_t), s));
+        CKS(launch_check_sym(ctx->A, n, ctx->ld, ctx->d_flag, s));
+        int32_t flag = 0;
+        CKS(cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(flag), cudaMemcpyDeviceToHost, s));
+        CKS(cudaStreamSynchronize(s));
+        CKS(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int32_t), s));
+        if (flag) {
+            ctx->err = "Q must be symmetric (PAPER.md:199): |Q_ij - Q_ji| > 1e-12 (|Q_ij| + |Q_ji|)";
+            return bail(DUQUAD_EINVAL);
+        }
+    }
     if (csr) {   // grid-stride sub-warp SpMV, full occupancy
         ctx->cfg_a = {ctx->num_sms * 8, 256, 0};
         ctx->cfg_b = {ctx->num_sms * 8, 256, 0};
@@ -1054,8 +1066,9 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
                     maxc, nq, fz.cg, fz.ng, fz.W, fz.nchg, fz.nt, fz.cslots);
     }
     if (!batched && ctx->world == 1 && opt.small_path) {
-        ctx->small_smem = small_smem_bytes(n, p, ctx->ld, ctx->ldp);
-        if (ctx->small_smem <= (size_t)prop.sharedMemPerBlockOptin) {
+        // the tables (beta, per-outer scalars) add per-solve bytes: the final check is in duquad_solve
+        ctx->small_smem = (size_t)prop.sharedMemPerBlockOptin - 1024;   // minus the static shared memory
+        if (small_smem_bytes(n, p, ctx->ld, ctx->ldp, 0, 0) <= ctx->small_smem) {
             CKS(configure_small_kernel(ctx->small_smem));
             ctx->small = true;
         }
@@ -1283,7 +1296,8 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
     }
     duquad_status st;
     if ((st = allgather_y(ctx)) != DUQUAD_OK) return st;
-    if (ctx->small && !ctx->eps_mode) {   // whole solve in one single-CTA kernel (K4)
+    if (ctx->small && !ctx->eps_mode &&
+        small_smem_bytes(ctx->n, ctx->p, ctx->ld, ctx->ldp, K, Kin) <= ctx->small_smem) {   // whole solve in one CTA (K4)
         if (ctx->beta_cap < Kin + 1) {
             if (ctx->d_beta) cudaFree(ctx->d_beta);
             ctx->d_beta = nullptr;
@@ -1320,7 +1334,7 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
         CK(cudaEventCreate(&t0));
         CK(cudaEventCreate(&t1));
         CK(cudaEventRecord(t0, s));
-        CK(launch_small_solve(sa, ctx->small_smem, s));
+        CK(launch_small_solve(sa, small_smem_bytes(ctx->n, ctx->p, ctx->ld, ctx->ldp, K, Kin), s));
         CK(cudaEventRecord(t1, s));
         CK(cudaStreamSynchronize(s));
         int32_t flag = 0;

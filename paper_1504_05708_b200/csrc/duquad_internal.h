@@ -182,7 +182,7 @@ cudaError_t launch_fused_stream(const FusedArgs &f, cudaStream_t s);
 cudaError_t launch_fused_epi(const PassBArgs &bl, const PassBArgs &bs, const FusedArgs &f, cudaStream_t s);
 
 // kernels_small.cu
-size_t small_smem_bytes(int64_t n, int64_t p, int64_t ld, int64_t ldp);
+size_t small_smem_bytes(int64_t n, int64_t p, int64_t ld, int64_t ldp, int K, int Kin);
 cudaError_t configure_small_kernel(size_t smem);
 cudaError_t launch_small_solve(const SmallArgs &sa, size_t smem, cudaStream_t s);
 
@@ -218,6 +218,8 @@ cudaError_t launch_transpose(const double *G, int64_t ldG, int64_t p, int64_t co
                              double *GT, int64_t ldp, cudaStream_t s);
 cudaError_t launch_check(const double *v, int64_t rows, int64_t cols, int64_t ld, int32_t *flag,
                          cudaStream_t s);
+// flag = 2 if the n x n block at A is not symmetric (|Q_ij - Q_ji| > 1e-12 (|Q_ij| + |Q_ji|))
+cudaError_t launch_check_sym(const double *A, int64_t n, int64_t ld, int32_t *flag, cudaStream_t s);
 cudaError_t launch_check_box(const double *lb, const double *ub, int64_t n, int32_t *flag,
                              cudaStream_t s);
 // Deterministic reductions: `parts` partial sums per CTA, then a fixed-order final sum.

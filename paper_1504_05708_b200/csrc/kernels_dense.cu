@@ -242,6 +242,27 @@ __global__ void k_check(const double *v, int64_t rows, int64_t cols, int64_t ld,
     }
 }
 
+// flag = 2 if the n x n block at A (leading dimension ld) is not symmetric to 1e-12 relative:
+// 32 x 32 tiles (i0 <= j0) and their mirrors through shared memory, both read coalesced
+__global__ void k_check_sym(const double *__restrict__ A, int64_t n, int64_t ld, int32_t *flag) {
+    __shared__ double tile[32][33];
+    const int64_t bi = blockIdx.y, bj = blockIdx.x;
+    if (bj < bi) return;
+    const int64_t i0 = bi * 32, j0 = bj * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {   // mirror tile: rows j0.., columns i0..
+        const int64_t i = j0 + r, j = i0 + threadIdx.x;
+        tile[r][threadIdx.x] = (i < n && j < n) ? A[i * ld + j] : 0.0;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t i = i0 + r, j = j0 + threadIdx.x;
+        if (i < n && j < n) {
+            const double a = A[i * ld + j], b = tile[threadIdx.x][r];   // Q_ij and Q_ji
+            if (fabs(a - b) > 1e-12 * (fabs(a) + fabs(b))) *flag = 2;
+        }
+    }
+}
+
 __global__ void k_check_box(const double *lb, const double *ub, int64_t n, int32_t *flag) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -446,6 +467,13 @@ cudaError_t launch_check(const double *v, int64_t rows, int64_t cols, int64_t ld
                          cudaStream_t s) {
     if (rows <= 0 || cols <= 0) return cudaSuccess;
     k_check<<<1184, 256, 0, s>>>(v, rows, cols, ld, flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check_sym(const double *A, int64_t n, int64_t ld, int32_t *flag, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const unsigned nb = (unsigned)((n + 31) / 32);
+    k_check_sym<<<dim3(nb, nb), dim3(32, 8), 0, s>>>(A, n, ld, flag);
     return cudaGetLastError();
 }
 

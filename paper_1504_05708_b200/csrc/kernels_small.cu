@@ -3,10 +3,12 @@
 // When [Q;G], G' and every vector fit in one SM's shared memory (config 0: 40 KB), the entire
 // DFOM solve -- (K_out + 1) x K_in inner steps, each a pass A and a pass B -- runs in ONE CTA:
 // the matrices are read from HBM once, every pass is a shared-memory GEMV, and a __syncthreads
-// replaces each kernel boundary (≈0.5 µs per inner step instead of two launches).  The row dot
-// product has the same summation order as the streaming dense kernels (kernels_dense.cu) and the
-// epilogues are the shared ones (epilogue.cuh), so the result is bit-identical to the
-// multi-launch dense path.
+// replaces each kernel boundary.  Eight threads per row (a 3-level shuffle instead of a warp-wide
+// one, so every pass is spread over up to 32 warps): row r of pass A reads column r of the
+// symmetric Q (Q_cr = Q_rc) or column r-n of G', pass B column j of G; the 8 threads of a
+// row take every 8th column.  Shared-memory rows are padded by 4 doubles, so the 8 column groups
+// of a warp fall on different banks.  The epilogues are the shared ones (epilogue.cuh); the
+// summation order differs from the streaming kernels (agreement ~1e-15).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -18,42 +20,47 @@ namespace dq {
 namespace {
 
 constexpr int kSmallThreads = 1024;
-constexpr int kUnrollS = 8;   // must match kUnroll of kernels_dense.cu (summation order)
 
-// identical arithmetic to row_dot() of kernels_dense.cu, operands in shared memory
-__device__ __forceinline__ double row_dot_smem(const double2 *row, const double2 *sv, int nv2, int lane) {
-    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-    int c = lane;
-    for (; c + 32 * (kUnrollS - 1) < nv2; c += 32 * kUnrollS) {
-#pragma unroll
-        for (int u = 0; u < kUnrollS; u += 2) {
-            const double2 v0 = row[c + 32 * u], v1 = row[c + 32 * (u + 1)];
-            const double2 y0 = sv[c + 32 * u], y1 = sv[c + 32 * (u + 1)];
-            acc0 = fma(v0.x, y0.x, acc0);
-            acc1 = fma(v0.y, y0.y, acc1);
-            acc2 = fma(v1.x, y1.x, acc2);
-            acc3 = fma(v1.y, y1.y, acc3);
-        }
+constexpr int kTpr = 8;   // threads per row
+constexpr int kPad = 4;   // doubles of padding per shared-memory row
+
+// this thread's part of sum_c M[c * ldm + col] v[c], c < len: every kTpr-th c from `sub`, two
+// interleaved accumulators
+__device__ __forceinline__ double col_part(const double *M, int ldm, int col, const double *v, int len, int sub) {
+    double a0 = 0.0, a1 = 0.0;
+    int c = sub;
+    for (; c + kTpr < len; c += 2 * kTpr) {
+        a0 = fma(M[c * ldm + col], v[c], a0);
+        a1 = fma(M[(c + kTpr) * ldm + col], v[c + kTpr], a1);
     }
-    for (; c < nv2; c += 32) {
-        const double2 v = row[c], y0 = sv[c];
-        acc0 = fma(v.x, y0.x, acc0);
-        acc1 = fma(v.y, y0.y, acc1);
-    }
-    return warp_sum((acc0 + acc1) + (acc2 + acc3));
+    if (c < len) a0 = fma(M[c * ldm + col], v[c], a0);
+    return a0 + a1;
 }
 
-__device__ __forceinline__ void copy_in(double *dst, const double *src, int64_t count) {
-    for (int64_t i = threadIdx.x; i < count; i += blockDim.x) dst[i] = src[i];
+// sum over the kTpr threads of a row (fixed xor tree); every lane of the warp must call it
+__device__ __forceinline__ double row_sum8(double s) {
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    return s;
+}
+
+__device__ __forceinline__ void copy_rows(double *dst, int ldd, const double *src, int64_t lds, int64_t rows,
+                                          int64_t cols) {
+    for (int64_t t = threadIdx.x; t < rows * cols; t += blockDim.x) {
+        const int64_t r = t / cols, c = t - r * cols;
+        dst[r * ldd + c] = src[r * lds + c];
+    }
 }
 
 __global__ void __launch_bounds__(kSmallThreads, 1) k_small_solve(const SmallArgs sa) {
     extern __shared__ __align__(16) double sm[];
     const int64_t n = sa.n, p = sa.p, ld = sa.ld, ldp = sa.ldp, rows = n + p;
     // shared-memory carve-up (all offsets multiples of 2 doubles)
-    double *A = sm;                       // rows x ld
-    double *GT = A + rows * ld;           // n x ldp
-    double *y = GT + n * ldp;             // ld
+    const int lda = (int)ld + kPad, ldg = (int)ldp + kPad;   // padded shared-memory strides
+    double *A = sm;                       // rows x lda
+    double *GT = A + rows * lda;          // n x ldg
+    double *y = GT + n * ldg;             // ld
     double *w = y + ld;                   // max(ldp, 2)
     double *x = w + (ldp > 2 ? ldp : 2);  // n (rounded to even)
     const int64_t n2 = (n + 1) & ~1LL, p2 = (p + 1) & ~1LL;
@@ -65,11 +72,14 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_solve(const SmallArg
     double *g = ub + n2;
     double *mu = g + p2;
     double *lp = mu + p2;
-    uint8_t *cone = reinterpret_cast<uint8_t *>(lp + p2);
+    double *beta = lp + p2;               // Kin + 1 (rounded to even): inner momentum table
+    const int64_t kb2 = (sa.Kin + 2) & ~1LL;
+    OuterParam *ops = reinterpret_cast<OuterParam *>(beta + kb2);   // K + 2 per-outer scalars
+    uint8_t *cone = reinterpret_cast<uint8_t *>(ops + sa.K + 2);
     __shared__ int32_t jj;
 
-    copy_in(A, sa.A, rows * ld);
-    copy_in(GT, sa.GT, n * ldp);
+    copy_rows(A, lda, sa.A, ld, rows, n);
+    if (p > 0) copy_rows(GT, ldg, sa.GT, ldp, n, p);
     for (int64_t i = threadIdx.x; i < ld; i += blockDim.x) y[i] = 0.0;
     for (int64_t i = threadIdx.x; i < (ldp > 2 ? ldp : 2); i += blockDim.x) w[i] = 0.0;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
@@ -87,6 +97,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_solve(const SmallArg
         lp[k] = 0.0;
         cone[k] = sa.cone[k];
     }
+    for (int i = threadIdx.x; i <= sa.Kin; i += blockDim.x) beta[i] = sa.beta_in[i];
+    for (int i = threadIdx.x; i < sa.K + 2; i += blockDim.x) ops[i] = sa.a.ops[i];
     if (threadIdx.x == 0) jj = 1;
     __syncthreads();
 
@@ -100,6 +112,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_solve(const SmallArg
     a.lam_prev = lp;
     a.cone = cone;
     a.d_j = &jj;
+    a.ops = ops;
     PassBArgs b = sa.b;
     b.w = w;
     b.qy = qy;
@@ -110,32 +123,40 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_solve(const SmallArg
     b.y = y;
     b.xhat = xh;
     b.d_j = &jj;
+    b.ops = ops;
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int nw = kSmallThreads / 32;
-    const int nv2a = (int)(ld >> 1), nv2b = (int)(ldp >> 1);
+    const double *Gm = A + n * lda;   // G rows of the packed [Q;G]
+    const int sub = threadIdx.x % kTpr, unit0 = threadIdx.x / kTpr, nunit = blockDim.x / kTpr;
+    const int ni = (int)n, pi = (int)p, rowsi = (int)rows;
     for (int j = 1; j <= sa.K + 1; ++j) {
         for (int k = 1; k <= sa.Kin; ++k) {
             a.first_inner = (k == 1);
             const OuterA o = outer_a(a, MODE_SOLVE);
-            for (int64_t row = warp; row < rows; row += nw) {
-                const EpiA e = epi_a_load(a, MODE_SOLVE, row, o);
-                const double s = row_dot_smem(reinterpret_cast<const double2 *>(A + row * ld),
-                                              reinterpret_cast<const double2 *>(y), nv2a, lane);
-                if (lane == 0) epi_a_store(a, MODE_SOLVE, row, s, e, o);
+            // pass A: kTpr threads per row (the loop bound is uniform over a row's threads)
+            for (int base = 0; base < rowsi; base += nunit) {
+                const int row = base + unit0;
+                double s = 0.0;
+                if (row < ni) s = col_part(A, lda, row, y, ni, sub);                      // (Q y)_row, Q symmetric
+                else if (row < rowsi) s = col_part(GT, ldg, row - ni, y, ni, sub);         // (G y)_{row-n} via G'
+                s = row_sum8(s);   // all lanes (converged)
+                if (sub == 0 && row < rowsi) {
+                    const EpiA e = epi_a_load(a, MODE_SOLVE, row, o);
+                    epi_a_store(a, MODE_SOLVE, row, s, e, o);
+                }
             }
             __syncthreads();
             if (k == 1 && j >= 2 && sa.trace_lam && j - 2 < sa.trace_max)
                 for (int64_t i = threadIdx.x; i < p; i += blockDim.x) sa.trace_lam[(j - 2) * p + i] = lp[i];
-            b.beta_in = sa.beta_in[k];
+            b.beta_in = beta[k];
             b.last_inner = (k == sa.Kin);
             const double avg_w = avg_weight(b, MODE_SOLVE);
-            for (int64_t r = warp; r < n; r += nw) {
-                const EpiB e = epi_b_load(b, MODE_SOLVE, r, avg_w);
-                const double t = nv2b > 0 ? row_dot_smem(reinterpret_cast<const double2 *>(GT + r * ldp),
-                                                         reinterpret_cast<const double2 *>(w), nv2b, lane)
-                                          : 0.0;
-                if (lane == 0) epi_b_store(b, MODE_SOLVE, r, t, e, avg_w);
+            for (int base = 0; base < ni; base += nunit) {                                  // pass B
+                const int r = base + unit0;
+                const double t = row_sum8((r < ni && pi > 0) ? col_part(Gm, lda, r, w, pi, sub) : 0.0);
+                if (sub == 0 && r < ni) {
+                    const EpiB e = epi_b_load(b, MODE_SOLVE, r, avg_w);
+                    epi_b_store(b, MODE_SOLVE, r, t, e, avg_w);
+                }
             }
             __syncthreads();
         }
@@ -157,10 +178,10 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_solve(const SmallArg
 
 }  // namespace
 
-size_t small_smem_bytes(int64_t n, int64_t p, int64_t ld, int64_t ldp) {
-    const int64_t n2 = (n + 1) & ~1LL, p2 = (p + 1) & ~1LL;
-    const int64_t doubles = (n + p) * ld + n * ldp + ld + (ldp > 2 ? ldp : 2) + 6 * n2 + 3 * p2;
-    return (size_t)doubles * 8 + (size_t)p + 16;
+size_t small_smem_bytes(int64_t n, int64_t p, int64_t ld, int64_t ldp, int K, int Kin) {
+    const int64_t n2 = (n + 1) & ~1LL, p2 = (p + 1) & ~1LL, kb2 = ((int64_t)Kin + 2) & ~1LL;
+    const int64_t doubles = (n + p) * (ld + kPad) + n * (ldp + kPad) + ld + (ldp > 2 ? ldp : 2) + 6 * n2 + 3 * p2 + kb2;
+    return (size_t)doubles * 8 + (size_t)(K + 2) * sizeof(OuterParam) + (size_t)p + 16;
 }
 
 cudaError_t configure_small_kernel(size_t smem) {
