@@ -1,7 +1,9 @@
 #!/usr/bin/env python
 """Tuning sweep of the byte-floor stream kernel at config 2: device time of one launch (CUDA
-events on the library stream, time_passes) vs the Q/G role split (DUQUAD_FUSED_NQ), plus the
-Q-only (rho = 0) and two-pass references.  Prints one JSON line per case."""
+events on the library stream, time_passes) vs the Q/G role split (argv[1]: list of
+DUQUAD_FUSED_NQ values, 0 = the library's default), the Q-only (rho = 0) kernel for each row-step
+cost of the partition (env ROWCOSTS -> DUQUAD_FUSED_ROWCOST) and the two-pass reference.
+Prints one JSON line per case."""
 import json
 import os
 import sys
@@ -33,11 +35,9 @@ def main():
         s.close()
         return info
 
-    for cg in os.environ.get("CGS", "4").split(","):
-      os.environ["DUQUAD_FUSED_CG"] = cg
-      for nq in nqs:
+    for nq in nqs:
         i = run(1.0, True, nq)
-        print(json.dumps({"case": "fused", "cg": int(cg), "nq": nq, "ms_stream": i["ms_pass_a"], "ms_epi": i["ms_pass_b"],
+        print(json.dumps({"case": "fused", "nq": nq, "ms_stream": i["ms_pass_a"], "ms_epi": i["ms_pass_b"],
                           "floor_gbs": (tri + gb) / i["ms_pass_a"] / 1e6,
                           "it_s": i["inner_iters_total"] / (i["ms_device"] / 1e3)}), flush=True)
     for rc in os.environ.get("ROWCOSTS", "6144").split(","):
