@@ -231,6 +231,16 @@ duquad_status duquad_solve(duquad_ctx *ctx, int32_t alg, int32_t outer_iters,
                            int32_t inner_iters, duquad_result *res);
 
 /*
+ * Warm start (sequential / receding-horizon solves): subsequent solves start
+ * from u_bar^0 = [x0]_U instead of [0]_U (reading c7) and lambda^0 = mu^1 = lambda0 instead of 0
+ * ("Given lambda^0 = mu^1 in K_d": lambda0 must lie in K_d, i.e. >= 0 on NONPOS rows when
+ * project_dual).  x0 is n (batch: B x n, one row per QP), lambda0 is p (B x p), full vectors as
+ * passed to duquad_setup; each context takes its QPs / row slices.  Host or device memory per
+ * `on_device`.  NULL for either resets that one to the default.  Stays in effect until reset.
+ */
+duquad_status duquad_set_initial(duquad_ctx *ctx, const double *x0, const double *lambda0, int32_t on_device);
+
+/*
  * DFOM with eps_in-driven inner stopping (Eq. duquad_in).
  * Every inner FGM solve runs until the gradient-map test
  *     L_in * ||y^k - x^k|| <= sqrt(2 * sigma_L * eps_in)

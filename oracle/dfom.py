@@ -246,7 +246,7 @@ def dfom(Q, q, G, g, lb, ub, cone, rho: float, alg: str, outer: int, inner,
          dual_step_scale: float = 0.5, project_dual: bool = True,
          lam0: Optional[np.ndarray] = None, keep_trace: bool = False,
          eps_in: Optional[float] = None, sigma_L: Optional[float] = None,
-         record_gm: bool = False) -> DfomResult:
+         record_gm: bool = False, x0: Optional[np.ndarray] = None) -> DfomResult:
     """Algorithm DFOM(d_rho, K_d), with fixed inner iteration counts.
 
     Given lambda^0 = mu^1 in K_d (= 0, [reading c8]), for k >= 1:
@@ -263,6 +263,7 @@ def dfom(Q, q, G, g, lb, ub, cone, rho: float, alg: str, outer: int, inner,
     `inner`: steps per inner solve (int), or a sequence of K + 1 per-solve counts (the last
     for the last-iterate solve); with eps_in and sigma_L the inner solves stop by the
     eps_in test of fom_run (NEXT-1) and `inner` is the cap.
+    Warm start (NEXT-2): x0 gives u_bar^0 = [x0]_U, lam0 gives lambda^0 = mu^1 (must lie in K_d).
     """
     counts = [int(inner)] * (outer + 1) if np.ndim(inner) == 0 else [int(c) for c in inner]
     if outer < 1 or len(counts) != outer + 1 or min(counts) < 1:
@@ -272,7 +273,7 @@ def dfom(Q, q, G, g, lb, ub, cone, rho: float, alg: str, outer: int, inner,
     theta = theta_sequence(outer + 1)
     lam_prev = np.zeros(bshape) if lam0 is None else lam0.copy()   # lambda^0
     mu = lam_prev.copy()                                            # mu^1 = lambda^0
-    u_bar = clamp_U(np.zeros(q.shape), lb, ub)                      # u_bar^0
+    u_bar = clamp_U(np.zeros(q.shape) if x0 is None else np.asarray(x0, float), lb, ub)   # u_bar^0
     xsum = np.zeros(q.shape)
     S = 0.0
     res = DfomResult(None, None, None, None, 0.0)

@@ -98,6 +98,7 @@ _SIGS = {
     "duquad_solve_eps": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_double,
                                    C.POINTER(Result)]),
     "duquad_get_inner_counts": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
+    "duquad_set_initial": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
     "duquad_theory_schedule": (C.c_int, [C.c_int32, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
                                          C.c_double, C.c_double, C.c_double, C.POINTER(Schedule)]),
     "duquad_destroy": (None, [C.c_void_p]),

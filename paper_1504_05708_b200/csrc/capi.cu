@@ -68,6 +68,8 @@ struct duquad_ctx {
     FusedArgs fz{};
     double *ws = nullptr;          // ws_rowp | ws_col | ws_g
     FusedPiece *fpieces = nullptr;
+    // warm start (duquad_set_initial): local slices, batched layout for batch > 1
+    double *init_x = nullptr, *init_lam = nullptr;
     // eps_in-driven inner stopping (duquad_solve_eps): device flag / counters, active during a solve
     bool eps_mode = false;
     double eps_thresh2 = 0.0;
@@ -151,6 +153,8 @@ void free_all(duquad_ctx *c) {
     if (c->d_j) cudaFree(c->d_j);
     if (c->d_flag) cudaFree(c->d_flag);
     if (c->fpieces) cudaFree(c->fpieces);
+    if (c->init_x) cudaFree(c->init_x);
+    if (c->init_lam) cudaFree(c->init_lam);
     if (c->gm_sq) cudaFree(c->gm_sq);
     if (c->gm_part) cudaFree(c->gm_part);
     if (c->gm_counter) cudaFree(c->gm_counter);
@@ -1174,6 +1178,52 @@ static duquad_status solve_prepare(duquad_ctx *ctx, int alg, int K, int Kin, std
     else
         CK(launch_init_state(ctx->x, ctx->y_full + ctx->rank * ctx->n_slice, ctx->xhat, ctx->lb, ctx->ub,
                              ctx->nloc, ctx->mu, ctx->lam_prev, ctx->ploc, ctx->d_j, ctx->d_flag, s));
+    if (ctx->init_x || ctx->init_lam) {   // warm start
+        if (ctx->Btot > 1)
+            CK(launch_apply_initial(ctx->Xb, ctx->Yb, ctx->lb, ctx->ub, ctx->n, ctx->ld, ctx->init_x, ctx->mub,
+                                    ctx->lpb, ctx->p, std::max<int64_t>(ctx->ldp, 2), ctx->init_lam, ctx->Bloc, s));
+        else
+            CK(launch_apply_initial(ctx->x, ctx->y_full + ctx->rank * ctx->n_slice, ctx->lb, ctx->ub, ctx->nloc, 0,
+                                    ctx->init_x, ctx->mu, ctx->lam_prev, ctx->ploc, 0, ctx->init_lam, 1, s));
+    }
+    return DUQUAD_OK;
+}
+
+duquad_status duquad_set_initial(duquad_ctx *ctx, const double *x0, const double *lambda0, int32_t on_device) {
+    if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
+    DevGuard guard(ctx->dev);
+    const bool bt = ctx->Btot > 1;
+    const int64_t sn = bt ? ctx->ld : ctx->nloc, sp = bt ? std::max<int64_t>(ctx->ldp, 2) : ctx->ploc;
+    const int64_t B = bt ? ctx->Bloc : 1;
+    // the caller's full vectors: x0 is (batch x) n, lambda0 (batch x) p, row per QP; this context
+    // takes its QPs (batched) or its row slices (row-sharded)
+    const int64_t xoff = bt ? ctx->b0 * ctx->n : ctx->rank * ctx->n_slice;
+    const int64_t loff = bt ? ctx->b0 * ctx->p : ctx->rank * ctx->p_slice;
+    const int64_t nx = bt ? ctx->n : ctx->nloc, nl = bt ? ctx->p : ctx->ploc;
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (x0) {
+        if (!on_device && !finite_host(x0 + xoff, B, nx, bt ? ctx->n : nx))
+            return fail(ctx, DUQUAD_EINVAL, "non-finite x0");
+        if (!ctx->init_x) CK(dalloc(&ctx->init_x, B * sn));
+        if (nx > 0)
+            CK(cudaMemcpy2DAsync(ctx->init_x, sn * sizeof(double), x0 + xoff, (bt ? ctx->n : nx) * sizeof(double),
+                                 nx * sizeof(double), B, kind, ctx->stream));
+    } else if (ctx->init_x) {
+        cudaFree(ctx->init_x);
+        ctx->init_x = nullptr;
+    }
+    if (lambda0) {
+        if (!on_device && !finite_host(lambda0 + loff, B, nl, bt ? ctx->p : nl))
+            return fail(ctx, DUQUAD_EINVAL, "non-finite lambda0");
+        if (!ctx->init_lam) CK(dalloc(&ctx->init_lam, B * std::max<int64_t>(sp, 1)));
+        if (nl > 0)
+            CK(cudaMemcpy2DAsync(ctx->init_lam, std::max<int64_t>(sp, 1) * sizeof(double), lambda0 + loff,
+                                 (bt ? ctx->p : nl) * sizeof(double), nl * sizeof(double), B, kind, ctx->stream));
+    } else if (ctx->init_lam) {
+        cudaFree(ctx->init_lam);
+        ctx->init_lam = nullptr;
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
     return DUQUAD_OK;
 }
 
@@ -1330,6 +1380,8 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
         sa.y_out = ctx->y_full;
         sa.lam_out = ctx->lam_prev;
         sa.mu_out = ctx->mu;
+        sa.x_init = ctx->init_x;
+        sa.lam_init = ctx->init_lam;
         cudaEvent_t t0, t1;
         CK(cudaEventCreate(&t0));
         CK(cudaEventCreate(&t1));

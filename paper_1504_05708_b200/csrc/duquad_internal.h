@@ -115,6 +115,7 @@ struct SmallArgs {
     double *trace_lam, *trace_u;
     int64_t trace_max;
     double *x_out, *xhat_out, *y_out, *lam_out, *mu_out;
+    const double *x_init, *lam_init;   // warm start (NULL: [0]_U and 0)
 };
 
 // ---------------------------------------------------------------- byte-floor inner step
@@ -206,6 +207,10 @@ cudaError_t launch_init_state(double *x, double *y, double *xhat, const double *
                               int64_t n, double *mu, double *lam_prev, int64_t p, int32_t *d_j,
                               int32_t *flag, cudaStream_t s);
 cudaError_t launch_advance(int32_t *d_j, cudaStream_t s);
+// warm start: u_bar^0 = [x0]_U, lambda^0 = mu^1 = lam0 (either may be NULL), B QPs with strides sn / sp
+cudaError_t launch_apply_initial(double *x, double *y, const double *lb, const double *ub, int64_t n, int64_t sn,
+                                 const double *x0, double *mu, double *lam_prev, int64_t p, int64_t sp,
+                                 const double *lam0, int64_t B, cudaStream_t s);
 // eps_in mode (duquad_solve_eps): after an inner step, sum gm_sq (fixed order; partials + the last
 // block) -> counts[*d_j - 1] += 1 and *done = 1 if L_in^2 sum <= 2 sigma eps_in (thresh2 = that / L_in^2)
 cudaError_t launch_inner_check(const double *gm_sq, int64_t n, double *partials, uint32_t *counter, int32_t *done,

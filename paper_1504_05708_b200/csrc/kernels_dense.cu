@@ -171,6 +171,27 @@ __global__ void k_init_state(double *x, double *y, double *xhat, const double *l
 
 __global__ void k_advance(int32_t *d_j) { *d_j += 1; }
 
+// warm start (duquad_set_initial): u_bar^0 = [x0]_U, lambda^0 = mu^1 = lam0, for B QPs with
+// strides sn / sp (B = 1: plain slices); runs after k_init_state / k_init_batched
+__global__ void k_apply_initial(double *x, double *y, const double *lb, const double *ub, int64_t n, int64_t sn,
+                                const double *x0, double *mu, double *lam_prev, int64_t p, int64_t sp,
+                                const double *lam0, int64_t B) {
+    const int64_t m = n > p ? n : p;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < B * m;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = t / m, i = t - b * m;
+        if (x0 && i < n) {
+            const double v = fmin(fmax(x0[b * sn + i], lb[i]), ub[i]);
+            x[b * sn + i] = v;
+            y[b * sn + i] = v;
+        }
+        if (lam0 && i < p) {
+            mu[b * sp + i] = lam0[b * sp + i];
+            lam_prev[b * sp + i] = lam0[b * sp + i];
+        }
+    }
+}
+
 // eps_in mode: gradient-map test after an inner step (fixed-order sum: block partials over
 // contiguous ranges, then the last block to finish adds them in block order)
 __global__ void k_inner_check(const double *gm_sq, int64_t n, double *partials, uint32_t *counter, int32_t *done,
@@ -447,6 +468,15 @@ cudaError_t launch_inner_finish(const double *x, double *y_dst, double *xhat, in
     const int grid = (int)std::min<int64_t>(1184, std::max<int64_t>(1, (n + 255) / 256));
     k_inner_finish<<<grid, 256, 0, s>>>(x, y_dst, xhat, n, ops, d_j, done, conv);
     k_inner_reset<<<1, 1, 0, s>>>(d_j, done, conv);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_apply_initial(double *x, double *y, const double *lb, const double *ub, int64_t n, int64_t sn,
+                                 const double *x0, double *mu, double *lam_prev, int64_t p, int64_t sp,
+                                 const double *lam0, int64_t B, cudaStream_t s) {
+    const int64_t m = B * std::max<int64_t>(std::max<int64_t>(n, p), 1);
+    k_apply_initial<<<(unsigned)std::min<int64_t>(1184, (m + 255) / 256), 256, 0, s>>>(x, y, lb, ub, n, sn, x0, mu,
+                                                                                     lam_prev, p, sp, lam0, B);
     return cudaGetLastError();
 }
 

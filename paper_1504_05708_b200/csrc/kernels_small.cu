@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_solve(const SmallArg
     for (int64_t i = threadIdx.x; i < ld; i += blockDim.x) y[i] = 0.0;
     for (int64_t i = threadIdx.x; i < (ldp > 2 ? ldp : 2); i += blockDim.x) w[i] = 0.0;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const double x0 = fmin(fmax(0.0, sa.lb[i]), sa.ub[i]);   // u_bar^0 = [0]_U (reading c7)
+        const double x0 = fmin(fmax(sa.x_init ? sa.x_init[i] : 0.0, sa.lb[i]), sa.ub[i]);   // [0]_U (c7) or warm start
         x[i] = x0;
         y[i] = x0;
         xh[i] = 0.0;
@@ -93,8 +93,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_solve(const SmallArg
     }
     for (int64_t k = threadIdx.x; k < p; k += blockDim.x) {
         g[k] = sa.g[k];
-        mu[k] = 0.0;   // mu^1 = lambda^0 = 0
-        lp[k] = 0.0;
+        mu[k] = sa.lam_init ? sa.lam_init[k] : 0.0;   // mu^1 = lambda^0 = 0, or the warm start
+        lp[k] = mu[k];
         cone[k] = sa.cone[k];
     }
     for (int i = threadIdx.x; i <= sa.Kin; i += blockDim.x) beta[i] = sa.beta_in[i];

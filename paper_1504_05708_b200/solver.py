@@ -207,6 +207,18 @@ class Solver:
         self.last_result = {k: getattr(res, k) for k, _ in L.Result._fields_}
         return self.last_result
 
+    def set_initial(self, x0=None, lambda0=None):
+        """Warm start for subsequent solves (duquad_set_initial): u_bar^0 = [x0]_U, lambda^0 = lambda0.
+        Full vectors (batch: (B, n) / (B, p)), NumPy or torch (host or CUDA); None resets."""
+        xs = _Arr(x0, np.float64) if x0 is not None else None
+        ls = _Arr(lambda0, np.float64) if lambda0 is not None else None
+        dev = bool((xs and xs.dev) or (ls and ls.dev))
+        if xs and ls and xs.dev != ls.dev:
+            raise ValueError("x0 and lambda0 must both be host or both be device arrays")
+        L.check(self._lib.duquad_set_initial(self._ctx, xs.ptr if xs else None, ls.ptr if ls else None, int(dev)),
+                self._ctx)
+        self._init_keep = (xs, ls)
+
     def solve_eps(self, alg: str = "DFGM", outer: int = 1, inner_max: int = 1000, eps_in: float = 1e-6,
                   sigma_L: float = 1.0) -> dict:
         """DFOM with eps_in-driven inner stopping (duquad_solve_eps).  The report gets 'inner_counts'

@@ -460,3 +460,23 @@ def test_dfom_on_the_schedule_reaches_eps(alg, seed):
     d, _ = O.dual_value(prob.Q, prob.q, G, g, prob.lb, prob.ub, prob.cone, 0.0, r.lam, L_in)
     assert ref.F - d <= eps, (ref.F - d, eps)
     assert ref.F - d >= -1e-9                       # weak duality
+
+
+@pytest.mark.parametrize("alg", [O.DGM, O.DFGM])
+def test_warm_start_at_the_kkt_point_is_a_fixed_point(alg):
+    """Warm start (NEXT-2): started from u_bar^0 = u*, lambda^0 = lambda* (brute-force KKT,
+    oracle.kkt) DFOM stays there -- the dual gradient G u(lambda*) + g - s vanishes at the
+    optimum and u(lambda*) = u* -- while a cold start with the same budget has not
+    converged; rho = 0 (Case 1, K_d = R^p_+)."""
+    from oracle import kkt
+    prob = qpgen.tiny(7, 4, seed=32, kind="ineq", shift=0.5)
+    prob.q = 4.0 * prob.q                              # pushes the minimizer onto a constraint
+    ref = kkt.brute_force(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone)
+    assert np.max(ref.lam) > 1e-3                      # some constraint is active
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 0.0, float(np.linalg.eigvalsh(prob.Q)[0]))
+    warm = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 0.0, alg, 3, 400, L_in, L_d,
+                  x0=ref.u, lam0=ref.lam.copy())
+    assert np.max(np.abs(warm.x_last - ref.u)) <= 1e-8
+    assert np.max(np.abs(warm.lam - ref.lam)) <= 1e-8
+    cold = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 0.0, alg, 3, 400, L_in, L_d)
+    assert np.max(np.abs(cold.lam - ref.lam)) > 1e-4
