@@ -144,6 +144,11 @@ typedef struct {
                               triangle of the symmetric Q once and G once (CTA pairs exchange
                               row sums through distributed shared memory), 8(n(n+1)/2 + pn)
                               bytes instead of 8(n^2 + 2pn); 0: the two-pass inner step    */
+    int32_t persist_path;  /* 1: dense single-GPU QPs whose matrices fit in 100 MB (L2) run every
+                              inner step of a solve in ONE cooperative launch (two passes
+                              separated by grid barriers; bitwise the multi-launch result).
+                              0 (default): one launch per pass in a CUDA graph -- measured as
+                              fast or faster on config 1 (the passes are L2-latency bound)  */
 } duquad_options;
 
 /* Per-solve report. */
@@ -169,7 +174,8 @@ typedef struct {
  *   BYTE_FLOOR k_fused_stream (Q triangle + G once) / k_fused_epi (column sums, epilogue)
  *   RHO0       k_rho0_step (Q y + c) / -            RHO0_FLOOR k_fused_stream (Q only) / k_fused_epi
  *   BATCHED    DMMA pass 0 / pass 1                 CSR        k_pass_a_csr / k_pass_b_csr
- *   SMALL      the whole solve in one single-CTA kernel (no per-pass timing)                  */
+ *   SMALL      the whole solve in one single-CTA kernel (no per-pass timing)
+ *   PERSIST    both passes of every inner step in one cooperative launch (no per-pass timing) */
 typedef enum {
     DUQUAD_PATH_TWO_PASS = 0,
     DUQUAD_PATH_BYTE_FLOOR = 1,
@@ -177,7 +183,9 @@ typedef enum {
     DUQUAD_PATH_RHO0_FLOOR = 3,
     DUQUAD_PATH_BATCHED = 4,
     DUQUAD_PATH_CSR = 5,
-    DUQUAD_PATH_SMALL = 6
+    DUQUAD_PATH_SMALL = 6,
+    DUQUAD_PATH_PERSIST = 7     /* k_persist: the two passes of every inner step in one cooperative
+                                   launch (L2-resident dense QPs, e.g. config 1)              */
 } duquad_path;
 
 int32_t duquad_abi_version(void);

@@ -53,7 +53,7 @@ class Options(C.Structure):
         ("use_graphs", C.c_int32), ("world_size", C.c_int32), ("rank", C.c_int32),
         ("nccl_id", C.c_void_p), ("stream", C.c_void_p), ("device", C.c_int32),
         ("time_passes", C.c_int32), ("small_path", C.c_int32), ("rho0_path", C.c_int32),
-        ("emulate_ranks", C.c_int32), ("fused_path", C.c_int32),
+        ("emulate_ranks", C.c_int32), ("fused_path", C.c_int32), ("persist_path", C.c_int32),
     ]
 
 
@@ -76,7 +76,8 @@ class Schedule(C.Structure):
     ]
 
 
-PATHS = {0: "two_pass", 1: "byte_floor", 2: "rho0", 3: "rho0_floor", 4: "batched", 5: "csr", 6: "small"}
+PATHS = {0: "two_pass", 1: "byte_floor", 2: "rho0", 3: "rho0_floor", 4: "batched", 5: "csr", 6: "small",
+         7: "persist"}
 
 
 _SIGS = {

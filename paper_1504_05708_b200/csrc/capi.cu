@@ -78,6 +78,10 @@ struct duquad_ctx {
     int32_t *d_done = nullptr, *d_counts = nullptr;   // d_counts: [K+1] steps, then [K+1] converged flags
     int64_t counts_cap = 0;
     std::vector<int32_t> last_counts, last_conv;
+    // persistent two-pass solve (L2-resident dense QPs): one cooperative launch per solve
+    bool persist = false;
+    size_t persist_smem = 0;
+    uint32_t *pbar = nullptr;
     // whole-solve single-CTA kernel (small dense QPs)
     bool small = false;
     size_t small_smem = 0;
@@ -153,6 +157,7 @@ void free_all(duquad_ctx *c) {
     if (c->d_j) cudaFree(c->d_j);
     if (c->d_flag) cudaFree(c->d_flag);
     if (c->fpieces) cudaFree(c->fpieces);
+    if (c->pbar) cudaFree(c->pbar);
     if (c->init_x) cudaFree(c->init_x);
     if (c->init_lam) cudaFree(c->init_lam);
     if (c->gm_sq) cudaFree(c->gm_sq);
@@ -718,6 +723,7 @@ void duquad_default_options(duquad_options *o) {
     o->rho0_path = 1;
     o->emulate_ranks = 0;
     o->fused_path = 1;
+    o->persist_path = 0;
 }
 
 duquad_status duquad_shard_range(int64_t rows, int32_t world, int32_t rank, int64_t *begin,
@@ -1069,6 +1075,19 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
             fprintf(stderr, "duquad fused: nb %d (max clusters %d) nq %d cg %d ng %d W %d nchg %d nt %d cslots %d\n", nb,
                     maxc, nq, fz.cg, fz.ng, fz.W, fz.nchg, fz.nt, fz.cslots);
     }
+    {   // persistent two-pass solve for dense single-GPU QPs whose matrices stay in L2
+        const double mbytes = 8.0 * ((double)(n + p) * ctx->ld + (double)n * ctx->ldp);
+        int coop = 0;
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->dev);
+        const char *ov = std::getenv("DUQUAD_PERSIST");
+        if (!batched && ctx->world == 1 && opt.persist_path && !ctx->fused && !ctx->rho0 && coop && mbytes <= 100e6 &&
+            !(ov && std::atoi(ov) == 0)) {
+            ctx->persist_smem = std::max(smem_a, smem_b);
+            CKS(configure_persist(ctx->persist_smem));
+            CKS(dalloc(&ctx->pbar, 2));
+            ctx->persist = true;
+        }
+    }
     if (!batched && ctx->world == 1 && opt.small_path) {
         // the tables (beta, per-outer scalars) add per-solve bytes: the final check is in duquad_solve
         ctx->small_smem = (size_t)prop.sharedMemPerBlockOptin - 1024;   // minus the static shared memory
@@ -1411,6 +1430,43 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
         return DUQUAD_OK;
     }
     const bool tracing = ctx->trace_lam || ctx->trace_u;
+    if (ctx->persist && !tracing && !ctx->eps_mode) {   // the whole solve in one cooperative launch
+        if (ctx->beta_cap < Kin + 1) {
+            if (ctx->d_beta) cudaFree(ctx->d_beta);
+            ctx->d_beta = nullptr;
+            CK(cudaMalloc(&ctx->d_beta, (Kin + 1) * sizeof(double)));
+            ctx->beta_cap = Kin + 1;
+        }
+        CK(cudaMemcpyAsync(ctx->d_beta, beta_in.data(), (Kin + 1) * sizeof(double), cudaMemcpyHostToDevice, s));
+        cudaEvent_t t0, t1;
+        CK(cudaEventCreate(&t0));
+        CK(cudaEventCreate(&t1));
+        CK(cudaEventRecord(t0, s));
+        CK(launch_persist(make_a(ctx), make_b(ctx), ctx->d_beta, K, Kin, ctx->pbar, ctx->num_sms, ctx->persist_smem, s));
+        CK(cudaEventRecord(t1, s));
+        CK(cudaStreamSynchronize(s));
+        int32_t flag = 0;
+        CK(cudaMemcpy(&flag, ctx->d_flag, sizeof(flag), cudaMemcpyDeviceToHost));
+        if (res) {
+            std::memset(res, 0, sizeof(*res));
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, t0, t1);
+            res->ms_device = ms;
+            res->path = DUQUAD_PATH_PERSIST;
+            res->outer_iters = K;
+            res->inner_iters_total = (int64_t)(K + 1) * Kin;
+            res->kernel_launches = 2;
+            res->matrix_passes = (int64_t)(K + 1) * Kin * 2;
+            const double nn = (double)ctx->n, pp = (double)ctx->p;
+            res->bytes_pass_a = 8.0 * ((nn + pp) * nn + nn + nn + 3.0 * pp);
+            res->bytes_pass_b = 8.0 * (nn * pp + pp + 8.0 * nn);
+        }
+        cudaEventDestroy(t0);
+        cudaEventDestroy(t1);
+        ctx->solved = true;
+        if (flag) return fail(ctx, DUQUAD_ENONFINITE, "an iterate became non-finite");
+        return DUQUAD_OK;
+    }
     const bool graphs = ctx->opt.use_graphs && !tracing;
     const int j_timed = ctx->opt.time_passes ? std::max(1, (K + 1) / 2) : -1;
     std::vector<cudaEvent_t> ev;

@@ -207,6 +207,10 @@ cudaError_t launch_init_state(double *x, double *y, double *xhat, const double *
                               int64_t n, double *mu, double *lam_prev, int64_t p, int32_t *d_j,
                               int32_t *flag, cudaStream_t s);
 cudaError_t launch_advance(int32_t *d_j, cudaStream_t s);
+// persistent two-pass solve (one cooperative launch for (K + 1) x Kin inner steps; L2-resident QPs)
+cudaError_t launch_persist(const PassAArgs &a, const PassBArgs &b, const double *beta_in, int K, int Kin,
+                           uint32_t *bar, int grid, size_t smem, cudaStream_t s);
+cudaError_t configure_persist(size_t smem);
 // warm start: u_bar^0 = [x0]_U, lambda^0 = mu^1 = lam0 (either may be NULL), B QPs with strides sn / sp
 cudaError_t launch_apply_initial(double *x, double *y, const double *lb, const double *ub, int64_t n, int64_t sn,
                                  const double *x0, double *mu, double *lam_prev, int64_t p, int64_t sp,

@@ -120,6 +120,87 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass_b(const PassBArgs b) {
     }
 }
 
+// ------------------------------------------------------------------ persistent two-pass solve
+// For dense single-GPU QPs whose matrices sit in L2 (config 1: 64 MB), kernel launches dominate
+// a two-kernel inner step.  k_persist runs the whole solve in ONE cooperative launch: per inner
+// step, pass A (y staged from L2), a grid barrier, pass B (w staged), a grid barrier.  Q rows and
+// G rows are partitioned separately and pass B uses pass A's Q-row partition with the same warp
+// mapping, so qy[j] is written and read by the same thread; the vectors every CTA reads (y, w)
+// are staged with L1-bypassing loads (L1 is not coherent across SMs).  Same row sums and epilogues
+// as k_pass_a / k_pass_b: bitwise the multi-launch result.
+__device__ __forceinline__ void stage_cg(double *s, const double *g, int64_t len) {
+    const double2 *g2 = reinterpret_cast<const double2 *>(g);
+    double2 *s2 = reinterpret_cast<double2 *>(s);
+    for (int64_t i = threadIdx.x; i < (len >> 1); i += blockDim.x) s2[i] = __ldcg(g2 + i);
+}
+
+__device__ __forceinline__ void grid_barrier(uint32_t *bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile uint32_t *gen = bar + 1;
+        const uint32_t g = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            bar[0] = 0;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_persist(const PassAArgs a0, const PassBArgs b0,
+                                                        const double *beta_in, int K, int Kin, uint32_t *bar) {
+    extern __shared__ __align__(16) double smem[];
+    __shared__ int32_t jj;
+    PassAArgs a = a0;
+    PassBArgs b = b0;
+    a.d_j = &jj;
+    b.d_j = &jj;
+    const double2 *sv = reinterpret_cast<const double2 *>(smem);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int nw = kThreads / 32;
+    const int64_t n = a.nq, p = a.row_end - a.nq;
+    const int64_t q0 = n * blockIdx.x / gridDim.x, q1 = n * (blockIdx.x + 1) / gridDim.x;       // Q rows
+    const int64_t g0 = n + p * blockIdx.x / gridDim.x, g1 = n + p * (blockIdx.x + 1) / gridDim.x;   // G rows
+    const int nva = (int)(a.ld >> 1), nvb = (int)(b.ldp >> 1);
+    for (int j = 1; j <= K + 1; ++j) {
+        if (threadIdx.x == 0) jj = j;
+        for (int k = 1; k <= Kin; ++k) {
+            a.first_inner = (k == 1);
+            stage_cg(smem, a.y, a.ld);
+            __syncthreads();
+            const OuterA o = outer_a(a, MODE_SOLVE);
+            for (int h = 0; h < 2; ++h) {   // pass A: this CTA's Q rows, then its G rows
+                const int64_t r0 = h ? g0 : q0, r1 = h ? g1 : q1;
+                for (int64_t row = r0 + warp; row < r1; row += nw) {
+                    EpiA e{};
+                    if (lane == 0) e = epi_a_load(a, MODE_SOLVE, row, o);
+                    const double s = row_dot(reinterpret_cast<const double2 *>(a.A + row * a.ld), sv, nva, lane);
+                    if (lane == 0) epi_a_store(a, MODE_SOLVE, row, s, e, o);
+                }
+            }
+            grid_barrier(bar);   // w complete
+            b.beta_in = beta_in[k];
+            b.last_inner = (k == Kin);
+            stage_cg(smem, b.w, b.ldp);
+            __syncthreads();
+            const double avg_w = avg_weight(b, MODE_SOLVE);
+            for (int64_t r = q0 + warp; r < q1; r += nw) {   // pass B on pass A's Q-row partition
+                EpiB e{};
+                if (lane == 0) e = epi_b_load(b, MODE_SOLVE, r, avg_w);
+                const double t = nvb > 0 ? row_dot(reinterpret_cast<const double2 *>(b.GT + r * b.ldp), sv, nvb, lane)
+                                         : 0.0;
+                if (lane == 0) epi_b_store(b, MODE_SOLVE, r, t, e, avg_w);
+            }
+            grid_barrier(bar);   // y complete
+        }
+    }
+}
+
 // K3, the rho = 0 inner step (SURVEY §8(a) row a1'): with rho = 0 the multiplier term of the
 // gradient is G'mu, constant over an inner solve ("only G'mu is computed at each
 // outer iteration"), so c = q + G'mu is formed once per outer iteration and each inner step
@@ -478,6 +559,25 @@ cudaError_t launch_apply_initial(double *x, double *y, const double *lb, const d
     k_apply_initial<<<(unsigned)std::min<int64_t>(1184, (m + 255) / 256), 256, 0, s>>>(x, y, lb, ub, n, sn, x0, mu,
                                                                                      lam_prev, p, sp, lam0, B);
     return cudaGetLastError();
+}
+
+cudaError_t launch_persist(const PassAArgs &a, const PassBArgs &b, const double *beta_in, int K, int Kin,
+                           uint32_t *bar, int grid, size_t smem, cudaStream_t s) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_persist, a, b, beta_in, K, Kin, bar);
+}
+
+cudaError_t configure_persist(size_t smem) {
+    return cudaFuncSetAttribute(k_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
 cudaError_t launch_advance(int32_t *d_j, cudaStream_t s) {

@@ -36,6 +36,7 @@
 #include <stdio.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "duquad_internal.h"
@@ -565,7 +566,9 @@ int fused_tiles(int64_t ld) { return (int)((ld + kChunk - 1) / kChunk); }
 size_t fused_smem_bytes() { return kHdr + (size_t)kSlots * kChunk * 8; }
 static_assert(kD * 8 <= 128 && 128 + kD * (32 + 4) * 8 <= kHdr, "header layout");
 bool fused_supported(int64_t n, int64_t ld, size_t smem_optin) {
-    return n >= 4096 && fused_nchg(ld, 2) <= 2 && fused_tiles(ld) <= kFusedMaxTiles && fused_smem_bytes() <= smem_optin;
+    int64_t nmin = 4096;   // below, the two-pass path is faster (tuning: DUQUAD_FUSED_NMIN)
+    if (const char *ov = std::getenv("DUQUAD_FUSED_NMIN")) nmin = std::atoll(ov);
+    return n >= nmin && fused_nchg(ld, 2) <= 2 && fused_tiles(ld) <= kFusedMaxTiles && fused_smem_bytes() <= smem_optin;
 }
 
 // Clusters of `cg` CTAs of the stream kernel that can be resident at once (0 on error).

@@ -284,7 +284,7 @@ def test_small_whole_solve_kernel_matches_the_stream_path(torch_cuda, n, p, kind
     L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 1.0, 0.05)
     L_d = L_d if p else 1.0
     a = run_gpu(torch_cuda, prob, 1.0, "DFGM", 9, 7, L_in, L_d, trace=p > 0, small_path=True)
-    b = run_gpu(torch_cuda, prob, 1.0, "DFGM", 9, 7, L_in, L_d, trace=p > 0, small_path=False)
+    b = run_gpu(torch_cuda, prob, 1.0, "DFGM", 9, 7, L_in, L_d, trace=p > 0, small_path=False, persist_path=False)
     assert a["info"]["kernel_launches"] == 2 and b["info"]["kernel_launches"] > 2
     for k in ("x_last", "x_avg", "lam") + (("trace_lam", "trace_u") if p else ()):
         assert relerr(a[k], b[k]) <= 1e-12, k
@@ -317,3 +317,20 @@ def test_asymmetric_q_is_rejected(torch_cuda):
     Q = prob.Q.copy()
     Q[3, 17] *= 1.0 + 1e-15    # rounding-level asymmetry is accepted
     Solver(Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho=1.0).close()
+
+
+@pytest.mark.parametrize("n,p,kind,rho,alg", [(2000, 1000, "ineq", 1.0, "DFGM"), (2000, 1000, "ineq", 10.0, "DGM"),
+                                               (777, 301, "mixed", 2.0, "DFGM"), (130, 0, "ineq", 1.0, "DFGM")])
+def test_persistent_solve_is_bitwise_the_multi_launch_path(torch_cuda, n, p, kind, rho, alg):
+    """k_persist (one cooperative launch per solve, grid barriers between the passes) vs one launch
+    per pass: the same row sums and epilogues -> bit-identical; and parity with the oracle."""
+    prob = qpgen.dense_ineq(n, p, seed=0) if kind == "ineq" and n == 2000 else qpgen.tiny(n, p, seed=n, kind=kind)
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, rho, 0.1)
+    L_d = L_d if p else 1.0
+    a = run_gpu(torch_cuda, prob, rho, alg, 7, 9, L_in, L_d, small_path=False, persist_path=True)
+    b = run_gpu(torch_cuda, prob, rho, alg, 7, 9, L_in, L_d, small_path=False, persist_path=False)
+    assert a["info"]["path"] == 7 and b["info"]["path"] == 0
+    for k in ("x_last", "x_avg", "lam"):
+        assert np.array_equal(a[k], b[k]), k
+    r = run_oracle(prob, rho, O.DFGM if alg == "DFGM" else O.DGM, 7, 9, L_in, L_d)
+    assert_parity(a, r)

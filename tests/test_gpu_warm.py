@@ -66,8 +66,14 @@ def test_warm_start_small_kernel(torch_cuda, alg):
 
 def test_warm_start_two_pass_and_device_inputs(torch_cuda):
     prob = qpgen.tiny(300, 120, seed=3, kind="mixed", shift=0.2)
-    info = _check(torch_cuda, prob, 1.0, "DFGM", 5, 7, device=True, small_path=False)
+    info = _check(torch_cuda, prob, 1.0, "DFGM", 5, 7, device=True, small_path=False, persist_path=False)
     assert info["path"] == 0
+
+
+def test_warm_start_persistent_path(torch_cuda):
+    info = _check(torch_cuda, qpgen.tiny(300, 120, seed=3, kind="mixed", shift=0.2), 1.0, "DGM", 5, 7,
+                  small_path=False, persist_path=True)
+    assert info["path"] == 7
 
 
 def test_warm_start_rho0_path(torch_cuda):
