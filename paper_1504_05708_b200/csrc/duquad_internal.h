@@ -98,6 +98,7 @@ struct BatchedArgs {
     int64_t ldb, N;      // valid QPs
     int64_t K;           // reduction length, padded to a multiple of 32 (zero padding)
     int64_t sn, sp;
+    int64_t ncol8, ngroups;   // QP octets; groups of octets (set by launch_batched)
     PassAArgs a;         // pass 0 epilogue (pointers at QP 0)
     PassBArgs b;         // pass 1 epilogue
 };

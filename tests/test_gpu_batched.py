@@ -113,3 +113,46 @@ def test_config3_full_size_configured_counts(torch_cuda):
     r = _oracle(prob, 1.0, O.DFGM, 50, 20, L_in, L_d)
     assert relerr(xl, r.x_last.T) <= TOL and relerr(xa, r.x_avg.T) <= TOL and relerr(lam, r.lam.T) <= TOL
     assert info["flops_pass_a"] + info["flops_pass_b"] == pytest.approx(3.0672e9, rel=1e-3)
+
+
+def test_tall_blocks_both_passes(torch_cuda):
+    """n = 132 > 128: pass B walks two 128-row blocks and pass A eight (M = 924, ragged last block);
+    K = 160 / 800 after padding (several BK = 32 chunks through the ring)."""
+    prob = qpgen.mpc_batch(45, seed=3, N=33)          # n = 132, p = 792
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 1.0, 0.1)
+    xl, xa, lam, _ = _solve(prob, 1.0, "DFGM", 3, 4, L_in, L_d)
+    r = _oracle(prob, 1.0, O.DFGM, 3, 4, L_in, L_d)
+    assert relerr(xl, r.x_last.T) <= TOL and relerr(xa, r.x_avg.T) <= TOL and relerr(lam, r.lam.T) <= TOL
+
+
+_MULTI_GROUP = r"""
+import sys, numpy as np
+sys.path.insert(0, '.')
+import qpgen
+from oracle import dfom as O
+from paper_1504_05708_b200 import Solver
+prob = qpgen.mpc_batch(203, seed=7, N=33)
+L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 1.0, 0.1)
+s = Solver(prob.Q, prob.q.T.copy(), prob.G, prob.g.T.copy(), prob.lb, prob.ub, prob.cone, rho=1.0)
+s.set_constants(L_in, L_d)
+s.solve('DFGM', 3, 3)
+got = s.result()
+r = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 1.0, 'DFGM', 3, 3, L_in, L_d)
+err = max(float(np.max(np.abs(g - w.T)) / (1 + np.max(np.abs(w)))) for g, w in zip(got, (r.x_last, r.x_avg, r.lam)))
+print('ERR', err)
+"""
+
+
+def test_several_groups_per_cta(torch_cuda):
+    """Grid capped at 3 CTAs (DUQUAD_BATCHED_CTAS, read once per process, hence the subprocess):
+    every CTA walks several QP groups through the same ring and mbarrier phases (203 QPs: 26
+    octets; pass A 6 groups, pass B 9 groups, ragged last octet)."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, DUQUAD_BATCHED_CTAS="3")
+    out = subprocess.run([sys.executable, "-c", _MULTI_GROUP], env=env, capture_output=True, text=True,
+                         timeout=600, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert out.returncode == 0, out.stderr[-2000:]
+    err = float(out.stdout.split("ERR")[-1])
+    assert err <= TOL, err
