@@ -28,10 +28,12 @@ def build(verbose: bool = False) -> str:
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     inc, libdir = _nccl_dirs()
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
-    deps = srcs + glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(ROOT, "include", "duquad.h")]
-    if os.path.exists(OUT) and os.path.getmtime(OUT) >= max(os.path.getmtime(d) for d in deps):
+    deps = srcs + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
+        [os.path.join(ROOT, "include", "duquad.h")]
+    extra = os.environ.get("DUQUAD_NVCC_EXTRA", "").split()   # e.g. instrumentation defines
+    if not extra and os.path.exists(OUT) and os.path.getmtime(OUT) >= max(os.path.getmtime(d) for d in deps):
         return OUT
-    cmd = [nvcc, ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+    cmd = [nvcc, ARCH, *extra, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "-Xcompiler", "-ffp-contract=off", "-Xptxas", "-v" if verbose else "-O3",
            f"-I{inc}", f"-I{os.path.join(ROOT, 'include')}", "-o", OUT + ".tmp", *srcs,
            f"-L{libdir}", "-l:libnccl.so.2", f"-Xlinker=-rpath,{libdir}"]

@@ -59,6 +59,7 @@ struct duquad_ctx {
     int64_t Btot = 1, Bloc = 1, b0 = 0;
     double *Yb = nullptr, *Xb = nullptr, *XHb = nullptr, *QYb = nullptr, *qb = nullptr;
     double *Wb = nullptr, *gb = nullptr, *mub = nullptr, *lpb = nullptr;
+    double *hb = nullptr;   // batched: h = mu + rho g per (QP, G row), refreshed by every DFOM step
     // rho = 0 specialisation (K3): second y replica (ping-pong) and c = q + G'mu
     bool rho0 = false;
     double *y_full2 = nullptr, *cvec = nullptr;
@@ -144,7 +145,7 @@ void free_all(duquad_ctx *c) {
     double *ds[] = {c->A,   c->GT,  c->y_full, c->w_full, c->qy,       c->x,        c->xhat,     c->q,
                     c->lb,  c->ub,  c->g,      c->mu,     c->lam_prev, c->lz_vprev, c->lz_w,     c->scal,
                     c->partials, c->Yb, c->Xb, c->XHb,   c->QYb,      c->qb,       c->Wb,       c->gb,
-                    c->mub, c->lpb, c->d_beta, c->y_full2, c->cvec, c->ws};
+                    c->mub, c->lpb, c->hb, c->d_beta, c->y_full2, c->cvec, c->ws};
     for (double *d : ds)
         if (d) cudaFree(d);
     if (c->cone) cudaFree(c->cone);
@@ -466,6 +467,7 @@ BatchedArgs make_batched(duquad_ctx *c, int pass) {
     ba.a.g = c->gb;
     ba.a.mu = c->mub;
     ba.a.lam_prev = c->lpb;
+    ba.a.h = c->hb;
     ba.b.qy = c->QYb;
     ba.b.q = c->qb;
     ba.b.x = c->Xb;
@@ -956,6 +958,7 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         CKS(dalloc(&ctx->gb, B * lp));
         CKS(dalloc(&ctx->mub, B * lp));
         CKS(dalloc(&ctx->lpb, B * lp));
+        CKS(dalloc(&ctx->hb, B * lp));
         if (B > 0) {
             CKS(cudaMemcpy2DAsync(ctx->qb, ctx->ld * sizeof(double), prob->q + ctx->b0 * n, n * sizeof(double),
                                   n * sizeof(double), B, cudaMemcpyDefault, s));
@@ -1205,6 +1208,9 @@ static duquad_status solve_prepare(duquad_ctx *ctx, int alg, int K, int Kin, std
             CK(launch_apply_initial(ctx->x, ctx->y_full + ctx->rank * ctx->n_slice, ctx->lb, ctx->ub, ctx->nloc, 0,
                                     ctx->init_x, ctx->mu, ctx->lam_prev, ctx->ploc, 0, ctx->init_lam, 1, s));
     }
+    if (ctx->Btot > 1)   // h = mu + rho g for the first outer iteration (no DFOM step there)
+        CK(launch_batched_h(ctx->hb, ctx->mub, ctx->gb, ctx->rho, ctx->p, std::max<int64_t>(ctx->ldp, 2), ctx->Bloc,
+                            s));
     return DUQUAD_OK;
 }
 

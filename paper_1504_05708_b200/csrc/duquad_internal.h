@@ -41,6 +41,7 @@ struct PassAArgs {
     const double *g;
     double *mu;
     double *lam_prev;
+    double *h;           // batched only (else null): h[k] = mu[k] + rho g[k], written by the DFOM step
     const uint8_t *cone;
     double rho;
     double step;         // dual_step_scale / L_d
@@ -98,7 +99,7 @@ struct BatchedArgs {
     int64_t ldb, N;      // valid QPs
     int64_t K;           // reduction length, padded to a multiple of 32 (zero padding)
     int64_t sn, sp;
-    int64_t ncol8, ngroups;   // QP octets; groups of octets (set by launch_batched)
+    int64_t ncol8;       // QP octets (set by launch_batched)
     PassAArgs a;         // pass 0 epilogue (pointers at QP 0)
     PassBArgs b;         // pass 1 epilogue
 };
@@ -194,6 +195,8 @@ cudaError_t launch_batched(const BatchedArgs &a, int pass, int mode, cudaStream_
 cudaError_t launch_init_batched(double *x, double *y, double *xhat, const double *lb, const double *ub, int64_t n,
                                 int64_t sn, double *mu, double *lam_prev, int64_t sp, int64_t B, int32_t *d_j,
                                 int32_t *flag, cudaStream_t s);
+cudaError_t launch_batched_h(double *h, const double *mu, const double *g, double rho, int64_t p, int64_t sp,
+                             int64_t B, cudaStream_t s);
 
 // kernels_dense.cu
 cudaError_t launch_pass_a(const PassAArgs &a, int mode, const LaunchCfg &cfg, cudaStream_t s);

@@ -12,12 +12,13 @@
 namespace dq {
 
 // [v]_K per row tag: ZERO -> 0, NONPOS -> min(v, 0)
+// (select forms: a NaN maps to 0 exactly as fmin/fmax(NaN, 0) would, in 3 SASS instead of ~14)
 __device__ __forceinline__ double proj_K(double v, uint8_t c) {
-    return c == DUQUAD_CONE_NONPOS ? fmin(v, 0.0) : 0.0;
+    return c == DUQUAD_CONE_NONPOS && v < 0.0 ? v : 0.0;
 }
 // projection onto the polar cone K° (multiplier sign set): ZERO -> v, NONPOS -> max(v, 0)
 __device__ __forceinline__ double proj_polar(double v, uint8_t c) {
-    return c == DUQUAD_CONE_NONPOS ? fmax(v, 0.0) : v;
+    return c != DUQUAD_CONE_NONPOS || v > 0.0 ? v : 0.0;
 }
 
 __device__ __forceinline__ double warp_sum(double s) {
@@ -66,6 +67,16 @@ __device__ __forceinline__ EpiA epi_a_load(const PassAArgs &a, int mode, int64_t
     return e;
 }
 
+// The DFOM step of one G row with the slack s(u, mu), given r = G y + g
+// at y == u_bar^{j-1}: returns mu^{j+1} and sets lambda^j.
+__device__ __forceinline__ double dfom_row(double r, double mu, double lp, uint8_t c, double rho, double step,
+                                           int project_dual, double beta_out, double &lam) {
+    const double sl = rho > 0.0 ? proj_K(r + mu / rho, c) : 0.0;
+    lam = mu + step * (r - sl);
+    if (project_dual && c == DUQUAD_CONE_NONPOS) lam = fmax(lam, 0.0);
+    return lam + beta_out * (lam - lp);
+}
+
 // s = (row of [Q;G]) . y
 __device__ __forceinline__ void epi_a_store(const PassAArgs &a, int mode, int64_t row, double s,
                                             const EpiA &e, const OuterA &o) {
@@ -81,13 +92,11 @@ __device__ __forceinline__ void epi_a_store(const PassAArgs &a, int mode, int64_
     const double r = s + e.g;                      // r = G y + g
     double m = e.mu;
     if (o.dual) {
-        // y == u_bar^{j-1}: DFOM step with the slack s(u, mu)
-        const double sl = a.rho > 0.0 ? proj_K(r + e.mu / a.rho, e.c) : 0.0;
-        double lam = e.mu + a.step * (r - sl);
-        if (a.project_dual && e.c == DUQUAD_CONE_NONPOS) lam = fmax(lam, 0.0);
-        m = lam + o.beta_out * (lam - e.lp);
+        double lam;
+        m = dfom_row(r, e.mu, e.lp, e.c, a.rho, a.step, a.project_dual, o.beta_out, lam);
         a.lam_prev[k] = lam;
         a.mu[k] = m;
+        if (a.h) a.h[k] = m + a.rho * e.g;   // batched: the constant part of the next w's
     }
     // multiplier term of grad L_rho: [mu + rho r]_{K°} (rho > 0), mu (rho = 0)
     a.w[k] = a.rho > 0.0 ? proj_polar(m + a.rho * r, e.c) : m;

@@ -9,23 +9,31 @@
 // Per-QP vectors are stored QP-major (B x ld, zero-padded to a multiple of 32), which is exactly
 // the "col" B-operand layout, so no transposes are needed.
 //
-// One persistent, warp-specialised CTA per SM.  The QPs are cut into groups of <= NT octets
-// (8 QPs); a CTA owns whole groups, so there is no inter-CTA traffic.  For each group it walks
-// the rows in blocks of 128 (16 m8 tiles) and the reduction dimension in BK = 32 chunks:
+// One persistent, warp-specialised CTA per SM.  CTA c owns a contiguous range of QP octets
+// (8 QPs), so there is no inter-CTA traffic; it walks the range in groups of <= NT octets, the
+// rows in blocks of 128 (16 m8 tiles) and the reduction dimension in BK = 32 chunks:
 //   - 2 producer warps stream the A chunk (128 x 32) and the B chunk (8*NT x 32) of every step
 //     into a STAGES-deep shared-memory ring with cp.async; each thread's copies arrive on the
 //     stage's "full" mbarrier (cp.async.mbarrier.arrive.noinc);
-//   - 8 math warps (two per SM sub-partition; warp w owns m8 tiles w and w + 8 of the block,
-//     all NT n8 tiles) issue the DMMAs and release the stage on its "empty" mbarrier;
-//   - at the end of a block the math warps park the C tile in shared memory (QP-major) and
-//     6 epilogue warps apply the DFOM epilogue (epilogue.cuh, the single-QP arithmetic on a
-//     per-QP view) while the math warps already run the next block.
-// The DMMA pipe is the bound (1 DMMA.8x8x4 per 16 cycles per sub-partition on this part); the
-// old 2-CTA/SM tile kernel ran it at 30 % (pass A) because its epilogue and the 3.03-wave
-// tail were serialised with the math.
+//   - 8 math warps (two per SM sub-partition; warp w owns m8 tiles w and w + 8 of the block and
+//     all octets of the group) issue the DMMAs and release the stage on its "empty" mbarrier;
+//   - pass A: the math warps apply the epilogue straight from their accumulators.  Outside the
+//     DFOM step it needs one operand per element, h = mu + rho g (constant within an outer
+//     iteration), which each lane loads at the start of the block, so the load latency hides
+//     under the block's DMMAs;
+//   - pass B (one row block, seven operands per element): the math warps park the C tile in
+//     shared memory and 6 epilogue warps apply it while the math warps run the CTA's next group.
+// The DMMA pipe is the bound: 1 DMMA.8x8x4 per 16 cycles per sub-partition (measured,
+// scripts/dmma_bench.cu: 37 TFLOP/s at 1965 MHz, reached with one warp and 4 accumulators).
+// Measured on config 3 (profiles/r01_summary.md): the earlier 2-CTA/SM tile kernel ran the
+// pipe at 30 % in pass A; separate epilogue warps next to DMMA-issuing warps ran ~3x slower than
+// alone, which is why pass A folds its (light) epilogue into the math warps.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
+#ifdef DUQUAD_BATCHED_TRACE
+#include <cstdio>
+#endif
 
 #include "duquad_internal.h"
 #include "epilogue.cuh"
@@ -36,18 +44,18 @@ namespace {
 
 constexpr int BK = 32;
 constexpr int PADK = BK + 4;    // smem row pitch (doubles): the 8x4 fragment loads of a half-warp hit 32 banks
-constexpr int kMathW = 8, kProdW = 2, kEpiW = 6;
-constexpr int kWarpsB = kMathW + kProdW + kEpiW;
-constexpr int kThreadsB = 32 * kWarpsB;
+constexpr int kMathW = 8, kProdW = 2;
 constexpr int kBlkM = 128;      // rows per block: 16 m8 tiles
-constexpr int LDC = kBlkM + 4;  // C tile: Cs[qp][row]
+constexpr int LDC = kBlkM + 2;  // tiles Cs[qp][row]; 2 LDC = 4 mod 16 doubles: fragment-order accesses are conflict-free
 constexpr int kSmemCap = 225 * 1024;
 
-template <int NT>
+template <int PASS, int NT>
 struct Geo {
+    static constexpr int EPIW = PASS == 0 ? 2 : 6;   // pass A: 2 h-staging warps; pass B: 6 epilogue warps
+    static constexpr int THREADS = 32 * (kMathW + kProdW + EPIW);
     static constexpr int BN = 8 * NT;
     static constexpr int SA = kBlkM * PADK, SB = BN * PADK;   // doubles per stage
-    static constexpr int CS = BN * LDC;
+    static constexpr int CS = BN * LDC;   // pass B: parked C tile; pass A: staged h tile (same shape)
     static constexpr int STAGES = (kSmemCap - 8 * CS - 128) / (8 * (SA + SB));
     static constexpr size_t SMEM = 8 * ((size_t)STAGES * (SA + SB) + CS) + 128;
     static_assert(STAGES >= 2, "ring too shallow");
@@ -62,6 +70,9 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
 }
 __device__ __forceinline__ void cp16(double *smem, const double *gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp8(double *smem, const double *gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(su32(smem)), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void mbar_init(uint64_t *b, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count) : "memory");
@@ -82,90 +93,312 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity) {
         : "memory");
 }
 
+#ifdef DUQUAD_BATCHED_TRACE   // instrumentation build only: per-block timeline of CTA 0
+__device__ unsigned long long g_btrace[8 * 64];
+#define BTRACE(slot, cond)                                                             \
+    do {                                                                               \
+        if ((cond) && blockIdx.x == 0 && (threadIdx.x & 31) == 0) {                    \
+            unsigned long long t_;                                                     \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                     \
+            g_btrace[slot] = t_;                                                       \
+        }                                                                              \
+    } while (0)
+#else
+#define BTRACE(slot, cond) \
+    do {                   \
+    } while (0)
+#endif
+
 struct Group {
     int64_t q0;   // first QP
     int nq, nc;   // valid QPs, octets
 };
-__device__ __forceinline__ Group group_of(const BatchedArgs &a, int64_t g) {
-    const int64_t c0 = g * a.ncol8 / a.ngroups, c1 = (g + 1) * a.ncol8 / a.ngroups;
-    Group r;
-    r.q0 = 8 * c0;
-    r.nc = (int)(c1 - c0);
-    const int64_t nq = a.N - r.q0 < 8 * (c1 - c0) ? a.N - r.q0 : 8 * (c1 - c0);
-    r.nq = nq > 0 ? (int)nq : 0;
+// CTA c owns octets [c*ncol8/grid, (c+1)*ncol8/grid) and walks them in ng groups of <= NT octets,
+// the larger groups first (the last group's epilogue is the one left exposed).
+struct Range {
+    int64_t o0, len;
+    int ng;
+};
+template <int NT>
+__device__ __forceinline__ Range cta_range(const BatchedArgs &a) {
+    Range r;
+    r.o0 = (int64_t)blockIdx.x * a.ncol8 / gridDim.x;
+    r.len = ((int64_t)blockIdx.x + 1) * a.ncol8 / gridDim.x - r.o0;
+    r.ng = (int)((r.len + NT - 1) / NT);
     return r;
 }
+__device__ __forceinline__ Group group_of(const BatchedArgs &a, const Range &r, int k) {
+    const int64_t c0 = r.o0 + ((int64_t)k * r.len + r.ng - 1) / r.ng;
+    const int64_t c1 = r.o0 + ((int64_t)(k + 1) * r.len + r.ng - 1) / r.ng;
+    Group g;
+    g.q0 = 8 * c0;
+    g.nc = (int)(c1 - c0);
+    const int64_t nq = a.N - g.q0 < 8 * (c1 - c0) ? a.N - g.q0 : 8 * (c1 - c0);
+    g.nq = nq > 0 ? (int)nq : 0;
+    return g;
+}
 
-// ---------------------------------------------------------------- epilogues (one block of one group)
-// Pass A: 3 QP columns x 4 rows per lane per round, operands loaded before any store.
-__device__ __forceinline__ void epi_block_a(const BatchedArgs &args, const double *Cs, int64_t m0, const Group &gr,
-                                            int wid, int nwk, int lane, const OuterA &o) {
-    constexpr int NCOL = 2, RPL = kBlkM / 32;
-    for (int cb = wid; cb < gr.nq; cb += NCOL * nwk) {
-        EpiA e[NCOL][RPL];
+struct MathCtx {
+    const double *As, *Bs;
+    double *Cs;
+    uint64_t *full, *empty, *cs_full, *cs_empty;
+    uint32_t s, blk;
+    int nkc, warp, lane;
+};
+
+// The K loop of one row block on math warp `warp`: m8 tiles warp and warp + 8 (TWO) or warp only,
+// C octets; every DMMA unconditional so the loop body carries no per-instruction guards.
+template <int ST, int SA, int SB, int C, bool TWO>
+__device__ __forceinline__ void kloop(MathCtx &x, double (&acc)[2][C][2]) {
+    const int fr = x.lane >> 2, fk = x.lane & 3;
 #pragma unroll
-        for (int c = 0; c < NCOL; ++c) {
-            const int col = cb + c * nwk;
-            PassAArgs v = args.a;
-            const int64_t b = gr.q0 + col;
-            v.g += b * args.sp;
-            v.mu += b * args.sp;
-            v.lam_prev += b * args.sp;
+    for (int j = 0; j < C; ++j) acc[0][j][0] = acc[0][j][1] = acc[1][j][0] = acc[1][j][1] = 0.0;
+    for (int kc = 0; kc < x.nkc; ++kc, ++x.s) {
+        const int slot = (int)(x.s % ST);
+        mbar_wait(x.full + slot, (x.s / ST) & 1);
+        const double *as = x.As + slot * SA + (8 * x.warp + fr) * PADK + fk;
+        const double *bs = x.Bs + slot * SB + fr * PADK + fk;
 #pragma unroll
-            for (int t = 0; t < RPL; ++t) {
-                const int64_t row = m0 + lane + 32 * t;
-                if (col < gr.nq && row < args.M) e[c][t] = epi_a_load(v, MODE_SOLVE, row, o);
+        for (int kk = 0; kk < BK; kk += 4) {
+            double bf[C];
+#pragma unroll
+            for (int j = 0; j < C; ++j) bf[j] = bs[j * 8 * PADK + kk];
+            const double a0 = as[kk];
+            const double a1 = TWO ? as[64 * PADK + kk] : 0.0;
+#pragma unroll
+            for (int j = 0; j < C; ++j) {
+                dmma(acc[0][j][0], acc[0][j][1], a0, bf[j]);
+                if (TWO) dmma(acc[1][j][0], acc[1][j][1], a1, bf[j]);
             }
         }
+        mbar_arrive(x.empty + slot);
+    }
+}
+
+// The DFOM step of pass A (first inner step of an outer iteration) for the elements of
+// one math warp, whose accumulators are parked in the tile Cs[qp][row - m0]: epilogue.cuh's
+// dfom_row per element, operands of 7 elements per lane-row loaded before any is used.  Out of
+// line: it runs on 1 launch in K_in and must not cost the hot loop registers.
+__device__ __noinline__ void dual_block(const double *Cs, const double *g, double *mu, double *lam_prev, double *hh,
+                                        double *w, double *qy, const uint8_t *cone, double rho, double step,
+                                        int project_dual, double beta_out, int64_t sn, int64_t sp, int64_t nq,
+                                        int64_t M, int64_t q0, int nqp, int64_t m0, int ne, int ni, int warp,
+                                        int lane) {
+    const int fr = lane >> 2, fk = lane & 3;
+    for (int i = 0; i < ni; ++i) {
+        const int rl = 8 * (warp + 8 * i) + fr;
+        const int64_t row = m0 + rl;
+        if (row >= M) continue;
+        if (row < nq) {   // Q row: qy
+            for (int e = 0; e < ne; ++e) {
+                const int qp = 8 * (e >> 1) + 2 * fk + (e & 1);
+                if (qp < nqp) qy[(q0 + qp) * sn + row] = Cs[qp * LDC + rl];
+            }
+            continue;
+        }
+        const int64_t k = row - nq;
+        const uint8_t c = cone[k];
+        constexpr int E = 7;
+        for (int e0 = 0; e0 < ne; e0 += E) {
+            double gv[E], mv[E], lv[E];
 #pragma unroll
-        for (int c = 0; c < NCOL; ++c) {
-            const int col = cb + c * nwk;
-            PassAArgs v = args.a;
-            const int64_t b = gr.q0 + col;
-            v.qy += b * args.sn;
-            v.w += b * args.sp;
-            v.mu += b * args.sp;
-            v.lam_prev += b * args.sp;
+            for (int u = 0; u < E; ++u) {
+                const int e = e0 + u, qp = 8 * (e >> 1) + 2 * fk + (e & 1);
+                if (e < ne && qp < nqp) {
+                    const int64_t off = (q0 + qp) * sp + k;
+                    gv[u] = g[off];
+                    mv[u] = mu[off];
+                    lv[u] = lam_prev[off];
+                }
+            }
 #pragma unroll
-            for (int t = 0; t < RPL; ++t) {
-                const int r = lane + 32 * t;
-                if (col < gr.nq && m0 + r < args.M)
-                    epi_a_store(v, MODE_SOLVE, m0 + r, Cs[col * LDC + r], e[c][t], o);
+            for (int u = 0; u < E; ++u) {
+                const int e = e0 + u, qp = 8 * (e >> 1) + 2 * fk + (e & 1);
+                if (e < ne && qp < nqp) {
+                    const int64_t off = (q0 + qp) * sp + k;
+                    const double r = Cs[qp * LDC + rl] + gv[u];
+                    double lam;
+                    const double m = dfom_row(r, mv[u], lv[u], c, rho, step, project_dual, beta_out, lam);
+                    lam_prev[off] = lam;
+                    mu[off] = m;
+                    hh[off] = m + rho * gv[u];
+                    w[off] = rho > 0.0 ? proj_polar(m + rho * r, c) : m;
+                }
             }
         }
     }
 }
 
-// Pass B: 1 QP column x 4 rows per lane per round (seven operands each).
+// ---------------------------------------------------------------- pass A: block with in-register epilogue
+// Fragment element (i, j, h) of lane (fr, fk): row m0 + 8 (warp + 8 i) + fr, QP q0 + 8 j + 2 fk + h.
+// Arithmetic: epilogue.cuh's, with [mu + rho (s + g)]_{K°} regrouped as [h + rho s]_{K°} outside
+// the DFOM step (reading c22); h comes from the tile the producers staged in x.Cs
+// (Hs[qp][row - m0]).
+template <int ST, int SA, int SB, int C, bool TWO>
+__device__ __forceinline__ void block_a(MathCtx &x, const BatchedArgs &args, const Group &gr, int64_t m0,
+                                        const OuterA &o) {
+    constexpr int NI = TWO ? 2 : 1;
+    const PassAArgs &A = args.a;
+    const int fr = x.lane >> 2, fk = x.lane & 3;
+    const double rho = A.rho;
+    int64_t row[NI];
+    int kr[NI];   // G-row index, -1 for a Q row, -2 beyond M
+    uint8_t cn[NI];
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+        row[i] = m0 + 8 * (x.warp + 8 * i) + fr;
+        kr[i] = row[i] >= args.M ? -2 : row[i] < A.nq ? -1 : (int)(row[i] - A.nq);
+        cn[i] = kr[i] >= 0 ? A.cone[kr[i]] : 0;   // lands during the K loop
+    }
+    double acc[2][C][2];
+    BTRACE(8 * (x.blk & 63) + 0, x.warp == 0);
+    kloop<ST, SA, SB, C, TWO>(x, acc);
+    BTRACE(8 * (x.blk & 63) + 1, x.warp == 0);
+    mbar_wait(x.cs_full, x.blk & 1);   // the h tile of this block
+    BTRACE(8 * (x.blk & 63) + 3, x.warp == 0);
+    if (!o.dual) {
+        // (1) results in place in the tile: Hs[qp][r] := qy (Q row) or w (G row); immediate offsets
+        double *hs = x.Cs + (2 * fk) * LDC + 8 * x.warp + fr;
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+            const bool q_row = kr[i] == -1;
+#pragma unroll
+            for (int j = 0; j < C; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    double *e = hs + (8 * j + h) * LDC + 64 * i;
+                    const double sv = acc[i][j][h];
+                    *e = q_row ? sv : rho > 0.0 ? proj_polar(*e + rho * sv, cn[i]) : *e;
+                }
+        }
+        __syncwarp();
+        BTRACE(8 * (x.blk & 63) + 7, x.warp == 0);
+        // (2) the warp's rows to global: lane -> (QP it * 4 + lane / 8, row lane % 8), 64-byte runs
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+            const int rl = 8 * (x.warp + 8 * i) + (x.lane & 7);   // block row of this lane
+            const int64_t r = m0 + rl;
+            if (r < args.M) {
+                const bool q_row = r < A.nq;
+                const int64_t ld = q_row ? args.sn : args.sp;
+                double *dst = (q_row ? A.qy + r : A.w + (r - A.nq)) + (gr.q0 + (x.lane >> 3)) * ld;
+                const double *src = x.Cs + (x.lane >> 3) * LDC + rl;
+                const int64_t step = 4 * ld;
+#pragma unroll 4
+                for (int qp = x.lane >> 3; qp < gr.nq; qp += 4, dst += step, src += 4 * LDC) *dst = *src;
+            }
+        }
+    } else {   // the DFOM step (first inner step of an outer iteration), epilogue.cuh's dfom_row
+        // park the accumulators in the (unused) h tile first, so they are not live across the loads
+#pragma unroll
+        for (int j = 0; j < C; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int i = 0; i < NI; ++i) x.Cs[(8 * j + 2 * fk + h) * LDC + (int)(row[i] - m0)] = acc[i][j][h];
+        __syncwarp();
+        dual_block(x.Cs, A.g, A.mu, A.lam_prev, A.h, A.w, A.qy, A.cone, rho, A.step, A.project_dual, o.beta_out,
+                   args.sn, args.sp, A.nq, args.M, gr.q0, gr.nq, m0, 2 * C, TWO ? 2 : 1, x.warp, x.lane);
+    }
+    mbar_arrive(x.cs_empty);
+    BTRACE(8 * (x.blk & 63) + 2, x.warp == 0);
+    ++x.blk;
+}
+
+// ---------------------------------------------------------------- pass B: block parked in smem
+template <int ST, int SA, int SB, int C, bool TWO>
+__device__ __forceinline__ void block_b(MathCtx &x) {
+    const int fr = x.lane >> 2, fk = x.lane & 3;
+    double acc[2][C][2];
+    kloop<ST, SA, SB, C, TWO>(x, acc);
+    // park the C tile QP-major (fragment: row fr, cols 2fk, 2fk+1 of each 8x8 tile)
+    mbar_wait(x.cs_empty, (x.blk & 1) ^ 1);
+#pragma unroll
+    for (int j = 0; j < C; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            x.Cs[(8 * j + 2 * fk + h) * LDC + 8 * x.warp + fr] = acc[0][j][h];
+            if (TWO) x.Cs[(8 * j + 2 * fk + h) * LDC + 8 * (x.warp + 8) + fr] = acc[1][j][h];
+        }
+    mbar_arrive(x.cs_full);
+    ++x.blk;
+}
+
+template <int PASS, int NT, int C>
+__device__ __forceinline__ void block_sel(MathCtx &x, const BatchedArgs &args, const Group &gr, int64_t m0,
+                                          const OuterA &o) {
+    using GE = Geo<PASS, NT>;
+    const bool two = m0 + 8 * (x.warp + 8) < args.M;
+    if (gr.nc == C) {
+        if (PASS == 0) {
+            if (two)
+                block_a<GE::STAGES, GE::SA, GE::SB, C, true>(x, args, gr, m0, o);
+            else
+                block_a<GE::STAGES, GE::SA, GE::SB, C, false>(x, args, gr, m0, o);
+        } else {
+            if (two)
+                block_b<GE::STAGES, GE::SA, GE::SB, C, true>(x);
+            else
+                block_b<GE::STAGES, GE::SA, GE::SB, C, false>(x);
+        }
+    } else if constexpr (C > 1) {
+        block_sel<PASS, NT, C - 1>(x, args, gr, m0, o);
+    }
+}
+
+// Pass B epilogue (one block of one group, from the parked C tile): x+ = clamp(y - (qy + q + G'w)
+// / L_in), momentum, running average.  Lanes own rows m0 + lane + 32 t, so
+// the bounds are loaded once per block; epilogue.cuh's arithmetic expression for expression.
+constexpr int RPL = kBlkM / 32;
 __device__ __forceinline__ void epi_block_b(const BatchedArgs &args, const double *Cs, int64_t m0, const Group &gr,
                                             int wid, int nwk, int lane, double avg_w) {
-    constexpr int RPL = kBlkM / 32;
-    for (int col = wid; col < gr.nq; col += nwk) {
-        PassBArgs v = args.b;
-        const int64_t b = gr.q0 + col;
-        v.qy += b * args.sn;
-        v.q += b * args.sn;
-        v.x += b * args.sn;
-        v.y += b * args.sn;
-        v.xhat += b * args.sn;
-        EpiB e[RPL];
+    const PassBArgs &B = args.b;
+    const double L = B.L_in, beta = B.beta_in;
+    const bool last = B.last_inner != 0;
+    int jj[RPL];
+    double lbv[RPL], ubv[RPL];
 #pragma unroll
-        for (int t = 0; t < RPL; ++t) {
-            const int64_t row = m0 + lane + 32 * t;
-            if (row < args.M) e[t] = epi_b_load(v, MODE_SOLVE, row, avg_w);
-        }
-#pragma unroll
-        for (int t = 0; t < RPL; ++t) {
-            const int r = lane + 32 * t;
-            if (m0 + r < args.M) epi_b_store(v, MODE_SOLVE, m0 + r, Cs[col * LDC + r], e[t], avg_w);
-        }
+    for (int t = 0; t < RPL; ++t) {
+        const int64_t j = m0 + lane + 32 * t;
+        jj[t] = j < args.M ? (int)j : -1;
+        lbv[t] = jj[t] >= 0 ? B.lb[j] : 0.0;
+        ubv[t] = jj[t] >= 0 ? B.ub[j] : 0.0;
     }
+    bool bad = false;
+    for (int col = wid; col < gr.nq; col += nwk) {
+        const int64_t off = (gr.q0 + col) * args.sn;
+        const double *qyp = B.qy + off, *qp = B.q + off;
+        double *xp = B.x + off, *yp = B.y + off, *hp = B.xhat + off;
+        const double *cs = Cs + col * LDC + lane;
+        double vq[RPL], vqy[RPL], vx[RPL], vy[RPL], vh[RPL];
+#pragma unroll
+        for (int t = 0; t < RPL; ++t)
+            if (jj[t] >= 0) {
+                vqy[t] = qyp[jj[t]];
+                vq[t] = qp[jj[t]];
+                vx[t] = xp[jj[t]];
+                vy[t] = yp[jj[t]];
+                vh[t] = avg_w != 0.0 ? hp[jj[t]] : 0.0;
+            }
+#pragma unroll
+        for (int t = 0; t < RPL; ++t)
+            if (jj[t] >= 0) {
+                const double grad = (vqy[t] + vq[t]) + cs[32 * t];
+                const double xn = fmin(fmax(vy[t] - grad / L, lbv[t]), ubv[t]);
+                const double yn = last ? xn : xn + beta * (xn - vx[t]);
+                if (avg_w != 0.0) hp[jj[t]] = vh[t] + avg_w * (xn - vh[t]);
+                xp[jj[t]] = xn;
+                yp[jj[t]] = yn;
+                bad |= !isfinite(xn) || !isfinite(yn);
+            }
+    }
+    if (bad) *B.flag = 1;
 }
 
 // C[m][b] = sum_k A[m][k] * Bop[b][k];  A: M x K row-major (lda), Bop: N x K (ldb), K padded to BK.
 template <int PASS, int NT>
-__global__ void __launch_bounds__(kThreadsB, 1) k_batched(const BatchedArgs args) {
-    using GE = Geo<NT>;
+__global__ void __launch_bounds__(Geo<PASS, NT>::THREADS, 1) k_batched(const BatchedArgs args) {
+    using GE = Geo<PASS, NT>;
     constexpr int ST = GE::STAGES;
     extern __shared__ __align__(16) double smem[];
     double *As = smem;
@@ -179,64 +412,27 @@ __global__ void __launch_bounds__(kThreadsB, 1) k_batched(const BatchedArgs args
             mbar_init(full + s, kProdW * 32);
             mbar_init(empty + s, kMathW * 32);
         }
-        mbar_init(cs_full, kMathW * 32);
-        mbar_init(cs_empty, kEpiW * 32);
+        // pass B: C tile math -> epilogue warps; pass A: h tile producers -> math warps
+        mbar_init(cs_full, PASS == 0 ? GE::EPIW * 32 : kMathW * 32);
+        mbar_init(cs_empty, PASS == 0 ? kMathW * 32 : GE::EPIW * 32);
     }
     __syncthreads();
     const int nmb = (int)((args.M + kBlkM - 1) / kBlkM), nkc = (int)(args.K / BK);
+    const Range rg = cta_range<NT>(args);
+    const OuterA o = PASS == 0 ? outer_a(args.a, MODE_SOLVE) : OuterA{0, 0.0};
 
     if (warp < kMathW) {   // ------------------------------------------------ math warps
-        const int fr = lane >> 2, fk = lane & 3;
-        uint32_t s = 0, blk = 0;
-        for (int64_t g = blockIdx.x; g < args.ngroups; g += gridDim.x) {
-            const Group gr = group_of(args, g);
+        MathCtx x{As, Bs, Cs, full, empty, cs_full, cs_empty, 0u, 0u, nkc, warp, lane};
+        for (int k = 0; k < rg.ng; ++k) {
+            const Group gr = group_of(args, rg, k);
             if (gr.nq == 0) continue;
-            for (int mb = 0; mb < nmb; ++mb) {
-                const int64_t m0 = (int64_t)mb * kBlkM;
-                const bool v0 = m0 + 8 * warp < args.M, v1 = m0 + 8 * (warp + 8) < args.M;
-                double acc[2][NT][2];
-#pragma unroll
-                for (int j = 0; j < NT; ++j) acc[0][j][0] = acc[0][j][1] = acc[1][j][0] = acc[1][j][1] = 0.0;
-                for (int kc = 0; kc < nkc; ++kc, ++s) {
-                    const int slot = (int)(s % ST);
-                    mbar_wait(full + slot, (s / ST) & 1);
-                    const double *as = As + slot * GE::SA + (8 * warp + fr) * PADK + fk;
-                    const double *bs = Bs + slot * GE::SB + fr * PADK + fk;
-#pragma unroll
-                    for (int kk = 0; kk < BK; kk += 4) {
-                        double bf[NT];
-#pragma unroll
-                        for (int j = 0; j < NT; ++j) bf[j] = bs[j * 8 * PADK + kk];
-                        const double a0 = as[kk], a1 = as[64 * PADK + kk];
-#pragma unroll
-                        for (int j = 0; j < NT; ++j)
-                            if (j < gr.nc) {
-                                if (v0) dmma(acc[0][j][0], acc[0][j][1], a0, bf[j]);
-                                if (v1) dmma(acc[1][j][0], acc[1][j][1], a1, bf[j]);
-                            }
-                    }
-                    mbar_arrive(empty + slot);
-                }
-                // park the C tile QP-major (fragment: row fr, cols 2fk, 2fk+1 of each 8x8 tile)
-                mbar_wait(cs_empty, (blk & 1) ^ 1);
-#pragma unroll
-                for (int j = 0; j < NT; ++j)
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        if (j < gr.nc) {
-                            Cs[(8 * j + 2 * fk + h) * LDC + 8 * warp + fr] = acc[0][j][h];
-                            Cs[(8 * j + 2 * fk + h) * LDC + 8 * (warp + 8) + fr] = acc[1][j][h];
-                        }
-                    }
-                mbar_arrive(cs_full);
-                ++blk;
-            }
+            for (int mb = 0; mb < nmb; ++mb) block_sel<PASS, NT, NT>(x, args, gr, (int64_t)mb * kBlkM, o);
         }
     } else if (warp < kMathW + kProdW) {   // ----------------------------------- producer warps
         const int pt = tid - 32 * kMathW;
         uint32_t s = 0;
-        for (int64_t g = blockIdx.x; g < args.ngroups; g += gridDim.x) {
-            const Group gr = group_of(args, g);
+        for (int k = 0; k < rg.ng; ++k) {
+            const Group gr = group_of(args, rg, k);
             if (gr.nq == 0) continue;
             for (int mb = 0; mb < nmb; ++mb) {
                 const int64_t m0 = (int64_t)mb * kBlkM;
@@ -244,6 +440,7 @@ __global__ void __launch_bounds__(kThreadsB, 1) k_batched(const BatchedArgs args
                 for (int kc = 0; kc < nkc; ++kc, ++s) {
                     const int slot = (int)(s % ST);
                     mbar_wait(empty + slot, ((s / ST) & 1) ^ 1);
+                    BTRACE(8 * ((mb + k * nmb) & 63) + 6, PASS == 0 && kc == 0 && warp == kMathW);
                     double *as = As + slot * GE::SA;
                     const double *ag = args.Aop + m0 * args.lda + (int64_t)kc * BK;
                     for (int i = pt; i < rows * (BK / 2); i += 32 * kProdW) {
@@ -260,21 +457,53 @@ __global__ void __launch_bounds__(kThreadsB, 1) k_batched(const BatchedArgs args
                 }
             }
         }
-    } else {   // -------------------------------------------------------------- epilogue warps
+    } else if (PASS == 0) {   // ----------------------------------------------- h-staging warps (pass A)
+        // the block's h tile Hs[qp][row - m0] (G rows; none on DFOM-step launches), QP columns
+        // split over the staging warps; Hs is free once the math warps wrote the previous block out
+        const int st = tid - 32 * (kMathW + kProdW), nst = 32 * GE::EPIW;
+        uint32_t hb = 0;
+        for (int k = 0; k < rg.ng; ++k) {
+            const Group gr = group_of(args, rg, k);
+            if (gr.nq == 0) continue;
+            for (int mb = 0; mb < nmb; ++mb, ++hb) {
+                const int64_t m0 = (int64_t)mb * kBlkM;
+                const int64_t r0 = m0 > args.a.nq ? m0 : args.a.nq;
+                const int64_t r1 = args.M < m0 + kBlkM ? args.M : m0 + kBlkM;
+                mbar_wait(cs_empty, (hb & 1) ^ 1);
+                BTRACE(8 * (hb & 63) + 4, warp == kMathW + kProdW);
+                if (!o.dual && r1 > r0) {
+                    const int nr = (int)(r1 - r0), k0 = (int)(r0 - args.a.nq), d0 = (int)(r0 - m0);
+                    if (((k0 | d0 | (int)args.sp) & 1) == 0) {   // 16-byte pairs (+ an odd tail element)
+                        const int np = (nr + 1) / 2;
+                        for (int i = st; i < gr.nq * np; i += nst) {
+                            const int c = i / np, r = 2 * (i % np);
+                            const double *src = args.a.h + (gr.q0 + c) * args.sp + k0 + r;
+                            if (r + 1 < nr)
+                                cp16(Cs + c * LDC + d0 + r, src);
+                            else
+                                cp8(Cs + c * LDC + d0 + r, src);
+                        }
+                    } else {
+                        for (int i = st; i < gr.nq * nr; i += nst) {
+                            const int c = i / nr, r = i % nr;
+                            cp8(Cs + c * LDC + d0 + r, args.a.h + (gr.q0 + c) * args.sp + k0 + r);
+                        }
+                    }
+                }
+                mbar_arrive_cp(cs_full);
+                BTRACE(8 * (hb & 63) + 5, warp == kMathW + kProdW);
+            }
+        }
+    } else {   // ------------------------------------------------------------------ epilogue warps (pass B)
         const int wid = warp - kMathW - kProdW;
-        const OuterA o = PASS == 0 ? outer_a(args.a, MODE_SOLVE) : OuterA{0, 0.0};
-        const double avg_w = PASS == 1 ? avg_weight(args.b, MODE_SOLVE) : 0.0;
+        const double avg_w = avg_weight(args.b, MODE_SOLVE);
         uint32_t blk = 0;
-        for (int64_t g = blockIdx.x; g < args.ngroups; g += gridDim.x) {
-            const Group gr = group_of(args, g);
+        for (int k = 0; k < rg.ng; ++k) {
+            const Group gr = group_of(args, rg, k);
             if (gr.nq == 0) continue;
             for (int mb = 0; mb < nmb; ++mb) {
                 mbar_wait(cs_full, blk & 1);
-                const int64_t m0 = (int64_t)mb * kBlkM;
-                if (PASS == 0)
-                    epi_block_a(args, Cs, m0, gr, wid, kEpiW, lane, o);
-                else
-                    epi_block_b(args, Cs, m0, gr, wid, kEpiW, lane, avg_w);
+                epi_block_b(args, Cs, (int64_t)mb * kBlkM, gr, wid, GE::EPIW, lane, avg_w);
                 mbar_arrive(cs_empty);
                 ++blk;
             }
@@ -282,9 +511,9 @@ __global__ void __launch_bounds__(kThreadsB, 1) k_batched(const BatchedArgs args
     }
 }
 
-// Pass A reads a (128 x 32) A chunk per (block, chunk) and reuses it over 7 octets (56 QPs);
-// pass B has a single row block (n <= 128 typical) and 4-octet groups, two per CTA, so the
-// epilogue of a CTA's first group overlaps the math of its second.
+// Pass A reuses each (128 x 32) A chunk over 7 octets (56 QPs); pass B (one row block for
+// n <= 128) uses 4-octet groups, two per CTA, so the epilogue of a CTA's first group overlaps
+// the math of its second.
 constexpr int kNTA = 7, kNTB = 4;
 
 int g_num_sms = 0;   // grid cap: the SM count, or DUQUAD_BATCHED_CTAS (tests: several groups per CTA)
@@ -300,17 +529,29 @@ cudaError_t launch_t(BatchedArgs a, cudaStream_t s) {
             if (atoi(e) > 0 && atoi(e) < g_num_sms) g_num_sms = atoi(e);
     }
     a.ncol8 = (a.N + 7) / 8;
-    const int64_t base = (a.ncol8 + NT - 1) / NT;
-    const int64_t nctas = base < g_num_sms ? base : g_num_sms;
-    a.ngroups = (base + nctas - 1) / nctas * nctas;
-    k_batched<PASS, NT><<<(unsigned)nctas, kThreadsB, Geo<NT>::SMEM, s>>>(a);
+    const int64_t nctas = a.ncol8 < g_num_sms ? a.ncol8 : g_num_sms;
+    k_batched<PASS, NT><<<(unsigned)nctas, Geo<PASS, NT>::THREADS, Geo<PASS, NT>::SMEM, s>>>(a);
+#ifdef DUQUAD_BATCHED_TRACE
+    if (PASS == 0) {
+        unsigned long long h[8 * 64];
+        cudaStreamSynchronize(s);
+        cudaMemcpyFromSymbol(h, g_btrace, sizeof h);
+        const unsigned long long t0 = h[0];
+        for (int b = 0; b < 8 && h[8 * b]; ++b) {
+            fprintf(stderr, "blk %d:", b);
+            for (int c = 0; c < 8; ++c) fprintf(stderr, " %7.2f", h[8 * b + c] ? (double)(h[8 * b + c] - t0) / 1e3 : -1.0);
+            fprintf(stderr, "\n");
+        }
+        cudaMemset(g_btrace, 0, 0);
+    }
+#endif
     return cudaGetLastError();
 }
 
 template <int PASS, int NT>
 cudaError_t configure_t() {
     return cudaFuncSetAttribute(k_batched<PASS, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)Geo<NT>::SMEM);
+                                (int)Geo<PASS, NT>::SMEM);
 }
 
 }  // namespace
@@ -325,6 +566,20 @@ cudaError_t launch_batched(const BatchedArgs &a, int pass, int mode, cudaStream_
     if (a.N <= 0 || a.M <= 0) return cudaSuccess;
     if (mode != MODE_SOLVE) return cudaErrorInvalidValue;   // the batched path runs solve passes only
     return pass == 0 ? launch_t<0, kNTA>(a, s) : launch_t<1, kNTB>(a, s);
+}
+
+__global__ void k_batched_h(double *h, const double *mu, const double *g, double rho, int64_t p, int64_t sp,
+                            int64_t B) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < B * sp && t % sp < p) h[t] = mu[t] + rho * g[t];
+}
+
+cudaError_t launch_batched_h(double *h, const double *mu, const double *g, double rho, int64_t p, int64_t sp,
+                             int64_t B, cudaStream_t s) {
+    const int64_t m = B * sp;
+    if (m <= 0) return cudaSuccess;
+    k_batched_h<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(h, mu, g, rho, p, sp, B);
+    return cudaGetLastError();
 }
 
 __global__ void k_init_batched(double *x, double *y, double *xhat, const double *lb, const double *ub, int64_t n,
