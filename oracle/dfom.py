@@ -239,6 +239,7 @@ class DfomResult:
     inner_counts: List[int] = field(default_factory=list)       # steps per inner solve (K + 1)
     converged: List[bool] = field(default_factory=list)         # eps_in test met (eps mode)
     gm: List[List[float]] = field(default_factory=list)         # L ||y^k - x^k|| per step (record_gm)
+    lam_hat: Optional[np.ndarray] = None                          # dual average (dual_average=True)
 
 
 def dfom(Q, q, G, g, lb, ub, cone, rho: float, alg: str, outer: int, inner,
@@ -246,7 +247,8 @@ def dfom(Q, q, G, g, lb, ub, cone, rho: float, alg: str, outer: int, inner,
          dual_step_scale: float = 0.5, project_dual: bool = True,
          lam0: Optional[np.ndarray] = None, keep_trace: bool = False,
          eps_in: Optional[float] = None, sigma_L: Optional[float] = None,
-         record_gm: bool = False, x0: Optional[np.ndarray] = None) -> DfomResult:
+         record_gm: bool = False, x0: Optional[np.ndarray] = None,
+         dual_average: bool = False) -> DfomResult:
     """Algorithm DFOM(d_rho, K_d), with fixed inner iteration counts.
 
     Given lambda^0 = mu^1 in K_d (= 0, [reading c8]), for k >= 1:
@@ -264,10 +266,18 @@ def dfom(Q, q, G, g, lb, ub, cone, rho: float, alg: str, outer: int, inner,
     for the last-iterate solve); with eps_in and sigma_L the inner solves stop by the
     eps_in test of fom_run (NEXT-1) and `inner` is the cap.
     Warm start (NEXT-2): x0 gives u_bar^0 = [x0]_U, lam0 gives lambda^0 = mu^1 (must lie in K_d).
+    DGM dual averaging (NEXT-2): with dual_average=True (DGM only) the returned dual
+    point is lambda^K := [lam_hat + grad_bar d(lam_hat) / (2 L_d)]_{K_d} with the average
+    lam_hat = (1 / (K+1)) sum_{j=0}^{K} lambda^j, grad_bar d(lam_hat) from one more inner solve
+    at mu = lam_hat (warm-started at u_bar^K), and the last iterate is u_bar of that point
+    (warm-started at u_bar(lam_hat)); K + 2 inner solves in all.
     """
-    counts = [int(inner)] * (outer + 1) if np.ndim(inner) == 0 else [int(c) for c in inner]
-    if outer < 1 or len(counts) != outer + 1 or min(counts) < 1:
-        raise ValueError("outer >= 1 and inner >= 1 (one count per solve: K + 1)")
+    nsolve = outer + (2 if dual_average else 1)
+    if dual_average and alg != DGM:
+        raise ValueError("dual averaging is the DGM final-point rule (P:624-626)")
+    counts = [int(inner)] * nsolve if np.ndim(inner) == 0 else [int(c) for c in inner]
+    if outer < 1 or len(counts) != nsolve or min(counts) < 1:
+        raise ValueError("outer >= 1 and inner >= 1 (one count per solve: K + 1, K + 2 with dual_average)")
     p = G.shape[0]
     bshape = (p,) if q.ndim == 1 else (p, q.shape[1])
     theta = theta_sequence(outer + 1)
@@ -276,6 +286,7 @@ def dfom(Q, q, G, g, lb, ub, cone, rho: float, alg: str, outer: int, inner,
     u_bar = clamp_U(np.zeros(q.shape) if x0 is None else np.asarray(x0, float), lb, ub)   # u_bar^0
     xsum = np.zeros(q.shape)
     S = 0.0
+    lam_sum = lam_prev.copy()                                       # sum_{j=0}^{k} lambda^j
     res = DfomResult(None, None, None, None, 0.0)
     info = []
 
@@ -305,7 +316,18 @@ def dfom(Q, q, G, g, lb, ub, cone, rho: float, alg: str, outer: int, inner,
             res.trace_u.append(u_bar.copy())
         mu = lam + beta_k * (lam - lam_prev)                                       # step 3
         lam_prev = lam
-    x_last = inner_solve(Q, q, G, g, cone, rho, lam_prev, u_bar, L_in, lb, ub, counts[outer],
+        lam_sum = lam_sum + lam
+    if dual_average:   # the final dual point from the average of lambda^0..lambda^K
+        lam_hat = lam_sum / (outer + 1)
+        u_hat = inner_solve(Q, q, G, g, cone, rho, lam_hat, u_bar, L_in, lb, ub, counts[outer],
+                            inner_rule, sigma, eps_in, sigma_L, gm_list(), info)
+        lam_prev = proj_Kd(lam_hat + (dual_step_scale / L_d) * inexact_dual_grad(G, g, cone, rho, u_hat, lam_hat),
+                           cone, project_dual)
+        res.lam_hat = lam_hat
+        u_bar_last, c_last = u_hat, counts[outer + 1]
+    else:
+        u_bar_last, c_last = u_bar, counts[outer]
+    x_last = inner_solve(Q, q, G, g, cone, rho, lam_prev, u_bar_last, L_in, lb, ub, c_last,
                          inner_rule, sigma, eps_in, sigma_L, gm_list(), info)
     res.inner_counts = [c for c, _ in info]
     res.converged = [v for _, v in info]

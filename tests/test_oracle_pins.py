@@ -480,3 +480,56 @@ def test_warm_start_at_the_kkt_point_is_a_fixed_point(alg):
     assert np.max(np.abs(warm.lam - ref.lam)) <= 1e-8
     cold = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 0.0, alg, 3, 400, L_in, L_d)
     assert np.max(np.abs(cold.lam - ref.lam)) > 1e-4
+
+
+# ------------------------------------------------------------ DGM dual averaging (NEXT-2)
+def _eq_qp(n=12, p=5, seed=3):
+    rng = np.random.default_rng(seed)
+    R = rng.standard_normal((n, n))
+    Q = 2.0 * np.eye(n) + 0.05 * (R + R.T)                 # kappa(Q) ~ 1.3: FGM converges to ulp fast
+    G = rng.standard_normal((p, n))
+    q, g = rng.standard_normal(n), rng.standard_normal(p)
+    lb, ub = np.full(n, -np.inf), np.full(n, np.inf)       # no box: u_bar(mu) has a closed form
+    cone = np.zeros(p, np.uint8)                           # equality rows: K = {0}, K_d = R^p
+    return Q, q, G, g, lb, ub, cone
+
+
+def test_dgm_dual_average_matches_the_closed_form_affine_recursion():
+    """rho = 0, equality rows, no box: u_bar(mu) = -Q^{-1}(q + G'mu) and grad d(mu) = G u_bar(mu) + g,
+    so DGM is the affine map lambda^{j} = lambda^{j-1} + (Gu_bar(lambda^{j-1}) + g) / (2 L_d).  The
+    averaged final point of P:624-626 and its last iterate follow by plain linear algebra."""
+    Q, q, G, g, lb, ub, cone = _eq_qp()
+    Qi = np.linalg.inv(Q)
+    H = G @ Qi @ G.T
+    L_d = float(np.linalg.eigvalsh(H).max())
+    L_in = float(np.linalg.eigvalsh(Q).max())
+    ubar = lambda mu: -Qi @ (q + G.T @ mu)
+    step = lambda lam: lam + (G @ ubar(lam) + g) / (2.0 * L_d)
+    K = 7
+    lams = [np.zeros(len(g))]
+    for _ in range(K):
+        lams.append(step(lams[-1]))
+    lam_hat = np.mean(lams, axis=0)
+    lam_fin = step(lam_hat)
+    r = O.dfom(Q, q, G, g, lb, ub, cone, 0.0, O.DGM, K, 120, L_in, L_d, dual_average=True)
+    assert np.allclose(r.lam_hat, lam_hat, rtol=0, atol=1e-11)
+    assert np.allclose(r.lam, lam_fin, rtol=0, atol=1e-11)
+    assert np.allclose(r.x_last, ubar(lam_fin), rtol=0, atol=1e-11)
+    # and it is not the plain last dual iterate
+    plain = O.dfom(Q, q, G, g, lb, ub, cone, 0.0, O.DGM, K, 120, L_in, L_d)
+    assert np.allclose(plain.lam, lams[-1], rtol=0, atol=1e-11)
+    assert np.max(np.abs(plain.lam - r.lam)) > 1e-6
+
+
+def test_dgm_dual_average_final_point_in_Kd_and_dgm_only():
+    prob = qpgen.tiny(30, 14, seed=2, kind="mixed", shift=0.3)
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 1.0, 0.2)
+    r = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 1.0, O.DGM, 6, 10, L_in, L_d,
+               dual_average=True)
+    nonpos = prob.cone == 1
+    assert np.all(r.lam[nonpos] >= 0.0)
+    assert r.lam_hat is not None and np.all(r.lam_hat[nonpos] >= 0.0)   # average of points of K_d
+    assert len(r.inner_counts) == 0 or len(r.inner_counts) == 6 + 2
+    with pytest.raises(ValueError):
+        O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 1.0, O.DFGM, 6, 10, L_in, L_d,
+               dual_average=True)
