@@ -149,6 +149,13 @@ typedef struct {
                               separated by grid barriers; bitwise the multi-launch result).
                               0 (default): one launch per pass in a CUDA graph -- measured as
                               fast or faster on config 1 (the passes are L2-latency bound)  */
+    int32_t dual_average;  /* 1 (DGM only; EINVAL with DFGM or in eps_in mode): the final dual point
+                              is lambda^K := [lam_hat + grad_bar d(lam_hat) / (2 L_d)]_{K_d} with the
+                              average lam_hat = (1/(K+1)) sum_{j=0}^{K} lambda^j (PAPER.md:624-626,
+                              the DGM rate of Theorem 1 holds for it); x_last = u_bar(lambda^K).
+                              Costs one more inner solve (at lam_hat); the single-CTA and
+                              persistent kernels defer to the streaming path.  0 (default): the
+                              last dual iterate.                                             */
 } duquad_options;
 
 /* Per-solve report. */

@@ -54,6 +54,7 @@ class Options(C.Structure):
         ("nccl_id", C.c_void_p), ("stream", C.c_void_p), ("device", C.c_int32),
         ("time_passes", C.c_int32), ("small_path", C.c_int32), ("rho0_path", C.c_int32),
         ("emulate_ranks", C.c_int32), ("fused_path", C.c_int32), ("persist_path", C.c_int32),
+        ("dual_average", C.c_int32),
     ]
 
 

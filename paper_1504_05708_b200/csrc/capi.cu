@@ -62,6 +62,8 @@ struct duquad_ctx {
     double *hb = nullptr;   // batched: h = mu + rho g per (QP, G row), refreshed by every DFOM step
     // rho = 0 specialisation (K3): second y replica (ping-pong) and c = q + G'mu
     bool rho0 = false;
+    bool davg = false;   // this solve: DGM dual-averaging final point (options.dual_average)
+    double *lam_hat = nullptr, *lhb = nullptr;   // running dual average (single QP / batched)
     double *y_full2 = nullptr, *cvec = nullptr;
     LaunchCfg cfg_k3{};
     // byte-floor inner step (symmetric Q read once as a triangle, G read once)
@@ -145,7 +147,7 @@ void free_all(duquad_ctx *c) {
     double *ds[] = {c->A,   c->GT,  c->y_full, c->w_full, c->qy,       c->x,        c->xhat,     c->q,
                     c->lb,  c->ub,  c->g,      c->mu,     c->lam_prev, c->lz_vprev, c->lz_w,     c->scal,
                     c->partials, c->Yb, c->Xb, c->XHb,   c->QYb,      c->qb,       c->Wb,       c->gb,
-                    c->mub, c->lpb, c->hb, c->d_beta, c->y_full2, c->cvec, c->ws};
+                    c->mub, c->lpb, c->hb, c->d_beta, c->y_full2, c->cvec, c->ws, c->lam_hat, c->lhb};
     for (double *d : ds)
         if (d) cudaFree(d);
     if (c->cone) cudaFree(c->cone);
@@ -238,6 +240,7 @@ PassAArgs make_a(duquad_ctx *c) {
     a.ci = c->a_ci;
     a.va = c->a_va;
     a.skip = c->eps_mode ? c->d_done : nullptr;
+    a.lam_hat = c->davg ? c->lam_hat : nullptr;
     return a;
 }
 
@@ -468,6 +471,7 @@ BatchedArgs make_batched(duquad_ctx *c, int pass) {
     ba.a.mu = c->mub;
     ba.a.lam_prev = c->lpb;
     ba.a.h = c->hb;
+    ba.a.lam_hat = c->davg ? c->lhb : nullptr;
     ba.b.qy = c->QYb;
     ba.b.q = c->qb;
     ba.b.x = c->Xb;
@@ -726,6 +730,7 @@ void duquad_default_options(duquad_options *o) {
     o->emulate_ranks = 0;
     o->fused_path = 1;
     o->persist_path = 0;
+    o->dual_average = 0;
 }
 
 duquad_status duquad_shard_range(int64_t rows, int32_t world, int32_t rank, int64_t *begin,
@@ -1161,6 +1166,11 @@ duquad_status duquad_set_trace(duquad_ctx *ctx, double *lam_trace, double *u_tra
 // initial state u_bar^0 = [0]_U, mu^1 = lambda^0 = 0 (before the first all-gather of y).
 static duquad_status solve_prepare(duquad_ctx *ctx, int alg, int K, int Kin, std::vector<double> &beta_in) {
     cudaStream_t s = ctx->stream;
+    ctx->davg = ctx->opt.dual_average != 0;
+    if (ctx->davg && alg != DUQUAD_DGM)
+        return fail(ctx, DUQUAD_EINVAL, "dual_average is the DGM final-point rule (PAPER.md:624-626): use alg = DGM");
+    if (ctx->davg && ctx->eps_mode)
+        return fail(ctx, DUQUAD_EINVAL, "dual_average: fixed inner counts only");
     // ---- host tables (fp64, PAPER.md:358-363 / 587-589 / 700-706)
     std::vector<double> theta(K + 3, 0.0);
     theta[1] = 1.0;
@@ -1185,14 +1195,24 @@ static duquad_status solve_prepare(duquad_ctx *ctx, int alg, int K, int Kin, std
         ops[j].dual_update = j >= 2;
         ops[j].beta_out = (j >= 2 && alg == DUQUAD_DFGM) ? (theta[j - 1] - 1.0) / theta[j] : 0.0;
     }
-    ops[K + 1] = OuterParam{0.0, 0.0, 1, 0};   // last-iterate solve at lambda^K (mu := lambda^K)
-    if (ctx->ops_cap < K + 2) {
+    ops[K + 1] = OuterParam{0.0, 0.0, 1, 0, 0.0};   // last-iterate solve at lambda^K (mu := lambda^K)
+    if (ctx->davg) {
+        // DGM dual averaging: the DFOM step of outer j >= 2 computes lambda^{j-1} and
+        // folds it into lam_hat with weight 1/j (lam_hat starts at lambda^0); outer K+1 folds in
+        // lambda^K and sets mu := lam_hat (inner solve at the average); outer K+2 takes the DFOM step
+        // from mu = lam_hat (beta = 0): the final lambda, and its inner solve gives x_last.
+        for (int j = 2; j <= K; ++j) ops[j].lhat_w = 1.0 / j;
+        ops[K + 1] = OuterParam{0.0, 0.0, 1, 1, 1.0 / (K + 1)};
+        ops.push_back(OuterParam{0.0, 0.0, 1, 0, 0.0});
+    }
+    const int nops = (int)ops.size();
+    if (ctx->ops_cap < nops) {
         if (ctx->d_ops) cudaFree(ctx->d_ops);
         ctx->d_ops = nullptr;
-        CK(cudaMalloc(&ctx->d_ops, (K + 2) * sizeof(OuterParam)));
-        ctx->ops_cap = K + 2;
+        CK(cudaMalloc(&ctx->d_ops, nops * sizeof(OuterParam)));
+        ctx->ops_cap = nops;
     }
-    CK(cudaMemcpyAsync(ctx->d_ops, ops.data(), (K + 2) * sizeof(OuterParam), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->d_ops, ops.data(), nops * sizeof(OuterParam), cudaMemcpyHostToDevice, s));
     // ---- initial state
     if (ctx->Btot > 1)
         CK(launch_init_batched(ctx->Xb, ctx->Yb, ctx->XHb, ctx->lb, ctx->ub, ctx->n, ctx->ld, ctx->mub, ctx->lpb,
@@ -1211,6 +1231,14 @@ static duquad_status solve_prepare(duquad_ctx *ctx, int alg, int K, int Kin, std
     if (ctx->Btot > 1)   // h = mu + rho g for the first outer iteration (no DFOM step there)
         CK(launch_batched_h(ctx->hb, ctx->mub, ctx->gb, ctx->rho, ctx->p, std::max<int64_t>(ctx->ldp, 2), ctx->Bloc,
                             s));
+    if (ctx->davg) {   // lam_hat := lambda^0
+        const int64_t cnt = ctx->Btot > 1 ? ctx->Bloc * std::max<int64_t>(ctx->ldp, 2) : ctx->ploc;
+        double *&lh = ctx->Btot > 1 ? ctx->lhb : ctx->lam_hat;
+        if (!lh) CK(dalloc(&lh, cnt));
+        if (cnt > 0)
+            CK(cudaMemcpyAsync(lh, ctx->Btot > 1 ? ctx->lpb : ctx->lam_prev, cnt * sizeof(double),
+                               cudaMemcpyDeviceToDevice, s));
+    }
     return DUQUAD_OK;
 }
 
@@ -1371,7 +1399,7 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
     }
     duquad_status st;
     if ((st = allgather_y(ctx)) != DUQUAD_OK) return st;
-    if (ctx->small && !ctx->eps_mode &&
+    if (ctx->small && !ctx->eps_mode && !ctx->davg &&
         small_smem_bytes(ctx->n, ctx->p, ctx->ld, ctx->ldp, K, Kin) <= ctx->small_smem) {   // whole solve in one CTA (K4)
         if (ctx->beta_cap < Kin + 1) {
             if (ctx->d_beta) cudaFree(ctx->d_beta);
@@ -1436,7 +1464,7 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
         return DUQUAD_OK;
     }
     const bool tracing = ctx->trace_lam || ctx->trace_u;
-    if (ctx->persist && !tracing && !ctx->eps_mode) {   // the whole solve in one cooperative launch
+    if (ctx->persist && !tracing && !ctx->eps_mode && !ctx->davg) {   // the whole solve in one cooperative launch
         if (ctx->beta_cap < Kin + 1) {
             if (ctx->d_beta) cudaFree(ctx->d_beta);
             ctx->d_beta = nullptr;
@@ -1494,7 +1522,8 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
     CK(cudaEventCreate(&t0));
     CK(cudaEventCreate(&t1));
     CK(cudaEventRecord(t0, s));
-    for (int j = 1; j <= K + 1; ++j) {
+    const int nout = K + 1 + (ctx->davg ? 1 : 0);   // + the solve at the dual average
+    for (int j = 1; j <= nout; ++j) {
         if (j == j_timed) {
             st = run_outer(ctx, beta_in, Kin, j, &ev);
         } else if (graphs) {
@@ -1523,9 +1552,9 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
                     : ctx->Btot > 1 ? DUQUAD_PATH_BATCHED
                     : ctx->format == DUQUAD_CSR ? DUQUAD_PATH_CSR : DUQUAD_PATH_TWO_PASS;
         res->outer_iters = K;
-        res->inner_iters_total = (int64_t)(K + 1) * Kin;
-        res->kernel_launches = 1 + (int64_t)(K + 1) * (2 * Kin + 1);
-        res->matrix_passes = (int64_t)(K + 1) * Kin * 2;
+        res->inner_iters_total = (int64_t)nout * Kin;
+        res->kernel_launches = 1 + (int64_t)nout * (2 * Kin + 1);
+        res->matrix_passes = (int64_t)nout * Kin * 2;
         const double nn = (double)ctx->n, nl = (double)ctx->nloc, pl = (double)ctx->ploc, pp = (double)ctx->p;
         if (ctx->fused) {      // byte floor: Q triangle (+ G once) streamed, workspace through L2
             // algorithmic bytes: Q triangle + G once + y; the epilogue: 7 vectors + the partials
@@ -1535,12 +1564,12 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
             res->bytes_pass_a = 8.0 * (tri + (ctx->rho0 ? 0.0 : pp * nn) + nn);
             res->bytes_pass_b = 8.0 * (wsb + 8.0 * nn);
             if (ctx->rho0) {
-                res->kernel_launches = 1 + (int64_t)(K + 1) * (2 * Kin + 3);
-                res->matrix_passes = (int64_t)(K + 1) * (Kin + 2);
+                res->kernel_launches = 1 + (int64_t)nout * (2 * Kin + 3);
+                res->matrix_passes = (int64_t)nout * (Kin + 2);
             }
         } else if (ctx->rho0) {       // K3 inner steps: Q only; per outer: one G pass and one G' pass
-            res->kernel_launches = 1 + (int64_t)(K + 1) * (Kin + 3);
-            res->matrix_passes = (int64_t)(K + 1) * (Kin + 2);
+            res->kernel_launches = 1 + (int64_t)nout * (Kin + 3);
+            res->matrix_passes = (int64_t)nout * (Kin + 2);
             res->bytes_pass_a = 8.0 * (nl * nn + nn + 8.0 * nl);   // "pass A" slot = the K3 step
             res->bytes_pass_b = 0.0;
         } else if (ctx->Btot > 1) {   // shared matrices (L2-resident) + per-QP vectors
@@ -1616,7 +1645,7 @@ duquad_status duquad_solve_emulated(duquad_ctx **ctxs, int32_t P, int32_t alg, i
     for (int r = 0; r < P; ++r)
         if ((st = solve_prepare(ctxs[r], alg, K, Kin, beta_in)) != DUQUAD_OK) return st;
     if ((st = group_gather(ctxs, P, G_Y)) != DUQUAD_OK) return st;
-    for (int j = 1; j <= K + 1; ++j)
+    for (int j = 1; j <= K + 1 + (ctx->davg ? 1 : 0); ++j)
         for (int ph = 0; ph < num_phases(ctx, Kin); ++ph) {
             int gb = G_NONE;
             for (int r = 0; r < P; ++r)

@@ -20,7 +20,8 @@ struct OuterParam {
     double beta_out;   // beta_{j-1} used for mu^{j} = lambda^{j-1} + beta (lambda^{j-1} - lambda^{j-2})
     double avg_w;      // omega_j / S_j for the running primal average (0 = no update)
     int32_t dual_update;  // 1: the first inner pass A of this outer iteration does the DFOM step
-    int32_t pad;
+    int32_t mu_hat;    // DGM dual averaging: mu := the updated dual average lam_hat
+    double lhat_w;     // DGM dual averaging: lam_hat += lhat_w (lambda - lam_hat) at this DFOM step
 };
 
 enum PassMode : int { MODE_SOLVE = 0, MODE_LIN = 1 };
@@ -42,6 +43,7 @@ struct PassAArgs {
     double *mu;
     double *lam_prev;
     double *h;           // batched only (else null): h[k] = mu[k] + rho g[k], written by the DFOM step
+    double *lam_hat;     // DGM dual averaging only (else null): running average of lambda^0..lambda^j
     const uint8_t *cone;
     double rho;
     double step;         // dual_step_scale / L_d

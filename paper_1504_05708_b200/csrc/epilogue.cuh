@@ -36,33 +36,47 @@ __device__ __forceinline__ double group_sum(double s) {
 
 // ------------------------------------------------------------------ pass A
 struct EpiA {
-    double g, mu, lp;
+    double g, mu, lp, lh;
     uint8_t c;
 };
 
 struct OuterA {
     int dual;
     double beta_out;
+    int mu_hat;      // DGM dual averaging: mu := the updated average
+    double lhat_w;   // weight of this step's lambda in the running dual average (0: none)
 };
 
 __device__ __forceinline__ OuterA outer_a(const PassAArgs &a, int mode) {
-    OuterA o{0, 0.0};
+    OuterA o{0, 0.0, 0, 0.0};
     if (mode == MODE_SOLVE && a.first_inner) {
         const OuterParam op = a.ops[*a.d_j];
         o.dual = op.dual_update;
         o.beta_out = op.beta_out;
+        if (a.lam_hat) {
+            o.mu_hat = op.mu_hat;
+            o.lhat_w = op.lhat_w;
+        }
     }
     return o;
 }
 
+// DGM dual averaging: lam_hat_j = lam_hat_{j-1} + (lambda^j - lam_hat_{j-1}) / (j+1), the
+// running form of (1/(j+1)) sum_{i<=j} lambda^i; on the final averaging step mu := lam_hat.
+__device__ __forceinline__ double dual_average(double lh, double lam, double m, const OuterA &o, double &lh_new) {
+    lh_new = lh + o.lhat_w * (lam - lh);
+    return o.mu_hat ? lh_new : m;
+}
+
 __device__ __forceinline__ EpiA epi_a_load(const PassAArgs &a, int mode, int64_t row, const OuterA &o) {
-    EpiA e{0.0, 0.0, 0.0, 0};
+    EpiA e{0.0, 0.0, 0.0, 0.0, 0};
     if (mode == MODE_SOLVE && row >= a.nq) {
         const int64_t k = row - a.nq;
         e.g = a.g[k];
         e.mu = a.mu[k];
         e.c = a.cone[k];
         if (o.dual) e.lp = a.lam_prev[k];
+        if (o.lhat_w != 0.0) e.lh = a.lam_hat[k];
     }
     return e;
 }
@@ -94,6 +108,11 @@ __device__ __forceinline__ void epi_a_store(const PassAArgs &a, int mode, int64_
     if (o.dual) {
         double lam;
         m = dfom_row(r, e.mu, e.lp, e.c, a.rho, a.step, a.project_dual, o.beta_out, lam);
+        if (o.lhat_w != 0.0) {
+            double lh;
+            m = dual_average(e.lh, lam, m, o, lh);
+            a.lam_hat[k] = lh;
+        }
         a.lam_prev[k] = lam;
         a.mu[k] = m;
         if (a.h) a.h[k] = m + a.rho * e.g;   // batched: the constant part of the next w's

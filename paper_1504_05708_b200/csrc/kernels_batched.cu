@@ -181,7 +181,8 @@ __device__ __forceinline__ void kloop(MathCtx &x, double (&acc)[2][C][2]) {
 // line: it runs on 1 launch in K_in and must not cost the hot loop registers.
 __device__ __noinline__ void dual_block(const double *Cs, const double *g, double *mu, double *lam_prev, double *hh,
                                         double *w, double *qy, const uint8_t *cone, double rho, double step,
-                                        int project_dual, double beta_out, int64_t sn, int64_t sp, int64_t nq,
+                                        int project_dual, double beta_out, double *lam_hat, int mu_hat,
+                                        double lhat_w, int64_t sn, int64_t sp, int64_t nq,
                                         int64_t M, int64_t q0, int nqp, int64_t m0, int ne, int ni, int warp,
                                         int lane) {
     const int fr = lane >> 2, fk = lane & 3;
@@ -218,7 +219,13 @@ __device__ __noinline__ void dual_block(const double *Cs, const double *g, doubl
                     const int64_t off = (q0 + qp) * sp + k;
                     const double r = Cs[qp * LDC + rl] + gv[u];
                     double lam;
-                    const double m = dfom_row(r, mv[u], lv[u], c, rho, step, project_dual, beta_out, lam);
+                    double m = dfom_row(r, mv[u], lv[u], c, rho, step, project_dual, beta_out, lam);
+                    if (lhat_w != 0.0) {   // DGM dual averaging
+                        OuterA oa{1, beta_out, mu_hat, lhat_w};
+                        double lh;
+                        m = dual_average(lam_hat[off], lam, m, oa, lh);
+                        lam_hat[off] = lh;
+                    }
                     lam_prev[off] = lam;
                     mu[off] = m;
                     hh[off] = m + rho * gv[u];
@@ -298,7 +305,7 @@ __device__ __forceinline__ void block_a(MathCtx &x, const BatchedArgs &args, con
                 for (int i = 0; i < NI; ++i) x.Cs[(8 * j + 2 * fk + h) * LDC + (int)(row[i] - m0)] = acc[i][j][h];
         __syncwarp();
         dual_block(x.Cs, A.g, A.mu, A.lam_prev, A.h, A.w, A.qy, A.cone, rho, A.step, A.project_dual, o.beta_out,
-                   args.sn, args.sp, A.nq, args.M, gr.q0, gr.nq, m0, 2 * C, TWO ? 2 : 1, x.warp, x.lane);
+                   A.lam_hat, o.mu_hat, o.lhat_w, args.sn, args.sp, A.nq, args.M, gr.q0, gr.nq, m0, 2 * C, TWO ? 2 : 1, x.warp, x.lane);
     }
     mbar_arrive(x.cs_empty);
     BTRACE(8 * (x.blk & 63) + 2, x.warp == 0);

@@ -126,13 +126,14 @@ __device__ __forceinline__ double g_row_w(const PassAArgs &a, int64_t k, double 
     const double r = s + e.g;
     double m = e.mu;
     if (o.dual) {
-        const double sl = a.rho > 0.0 ? proj_K(r + e.mu / a.rho, e.c) : 0.0;
-        double lam = e.mu + a.step * (r - sl);
-        if (a.project_dual && e.c == DUQUAD_CONE_NONPOS) lam = fmax(lam, 0.0);
-        m = lam + o.beta_out * (lam - e.lp);
+        double lam;
+        m = dfom_row(r, e.mu, e.lp, e.c, a.rho, a.step, a.project_dual, o.beta_out, lam);
+        double lh = 0.0;
+        if (o.lhat_w != 0.0) m = dual_average(e.lh, lam, m, o, lh);
         if (write) {
             a.lam_prev[k] = lam;
             a.mu[k] = m;
+            if (o.lhat_w != 0.0) a.lam_hat[k] = lh;
         }
     }
     return a.rho > 0.0 ? proj_polar(m + a.rho * r, e.c) : m;
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
     // ---- shared memory: barriers + small per-row buffers (first 8 KB), then the ring
     uint64_t *xbar = reinterpret_cast<uint64_t *>(fsm);    // [kD] pair exchange (st.async bytes)
     double *xbuf = reinterpret_cast<double *>(fsm + 128);  // [kD][32] warp partials of a G row, rank-major
-    double *epib = xbuf + kD * 32;                         // [kD][4] g, mu, lambda_prev, cone of the row
+    double *epib = xbuf + kD * 32;                         // [kD][5] g, mu, lambda_prev, cone, lam_hat of the row
     const double2 *ring = reinterpret_cast<const double2 *>(fsm + kHdr) + tid;   // [kSlots][kV][512]
     const uint32_t ring_u32 = smem_u32(ring);
     auto slot_addr = [&](int s, int k) -> uint32_t { return ring_u32 + (uint32_t)((s * kV + k) * kThreadsF) * 16; };
@@ -401,11 +402,12 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
         auto prefetch_epi = [&](int it) {
             if (tid == 0 && it < nr) {
                 const EpiA e = epi_a_load(f.a, MODE_SOLVE, f.a.nq + g0 + it, o);
-                double *eb = epib + (it % kD) * 4;
+                double *eb = epib + (it % kD) * 5;
                 eb[0] = e.g;
                 eb[1] = e.mu;
                 eb[2] = e.lp;
                 eb[3] = (double)e.c;
+                eb[4] = e.lh;
             }
         };
         // Row finishing without any intra-CTA hand-off: every warp sends its partial of the row to
@@ -429,12 +431,13 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
             s_row += __shfl_xor_sync(0xffffffffu, s_row, 4);
             s_row += __shfl_xor_sync(0xffffffffu, s_row, 2);
             s_row += __shfl_xor_sync(0xffffffffu, s_row, 1);
-            const double *eb = epib + d * 4;
+            const double *eb = epib + d * 5;
             EpiA e;
             e.g = eb[0];
             e.mu = eb[1];
             e.lp = eb[2];
             e.c = (uint8_t)eb[3];
+            e.lh = eb[4];
             return g_row_w(f.a, g0 + it, s_row, e, o, rank == 0 && warp == 0 && lane == 0);
         };
         prefetch_epi(0);
@@ -564,7 +567,7 @@ int fused_block_width(int64_t ld, int cg) { return (int)((ld + 32 * cg - 1) / (3
 int fused_nchg(int64_t ld, int cg) { return (fused_block_width(ld, cg) + kChunk - 1) / kChunk; }
 int fused_tiles(int64_t ld) { return (int)((ld + kChunk - 1) / kChunk); }
 size_t fused_smem_bytes() { return kHdr + (size_t)kSlots * kChunk * 8; }
-static_assert(kD * 8 <= 128 && 128 + kD * (32 + 4) * 8 <= kHdr, "header layout");
+static_assert(kD * 8 <= 128 && 128 + kD * (32 + 5) * 8 <= kHdr, "header layout");
 bool fused_supported(int64_t n, int64_t ld, size_t smem_optin) {
     int64_t nmin = 4096;   // below, the two-pass path is faster (tuning: DUQUAD_FUSED_NMIN)
     if (const char *ov = std::getenv("DUQUAD_FUSED_NMIN")) nmin = std::atoll(ov);
