@@ -304,6 +304,26 @@ duquad_status duquad_theory_schedule(int32_t alg, double eps, double R_d, double
                                      double sigma_L, double D_U, double normG, double lambda_min_Q,
                                      duquad_schedule *out);
 
+/* Convergence-bound diagnostics of DuQuad (host-only arithmetic, no GPU), for k outer iterations. */
+typedef struct {
+    double dual_gap;    /* Theorem 1 (bound_gen_dfg): F* - d(lambda^k) <=
+                           4 L_d R_d^2 / (k+1)^p + 2 (k+1)^(p-1) eps_in, p = 1 (DGM), 2 (DFGM)        */
+    double drift;       /* (bound_seq_dgm) PAPER.md:736-738: ||lambda^k - lambda*|| <= R_d + sqrt(k eps_in / L_d) */
+    double feas_last;   /* (aux_feas_bound) PAPER.md:805-810: dist_K(G x_last + g) <=
+                           sqrt(2 L_d eps_in) + sqrt(2 L_d dual_gap)                                 */
+    double feas_avg;    /* primal average over k iterates: DGM (feasibility_final) PAPER.md:918-939
+                           4 L_d R_d / k + 2 sqrt(L_d eps_in / k); DFGM (infes_av) PAPER.md:1045-1056
+                           8 L_d R_d / k^2 + 8 sqrt(L_d eps_in / k)                                  */
+} duquad_bounds;
+
+/*
+ * Fills `out` for alg (DUQUAD_DGM/DFGM), k >= 1 outer iterations, L_d > 0, the dual radius
+ * R_d = ||lambda* - lambda^0|| >= 0 and the inner accuracy eps_in >= 0 (reading c23 for
+ * the iterate indexing).  DUQUAD_EINVAL on a non-finite or out-of-range argument.
+ */
+duquad_status duquad_theory_bounds(int32_t alg, int64_t k, double L_d, double R_d, double eps_in,
+                                   duquad_bounds *out);
+
 /*
  * Copies x_last = u_bar(lambda^K) (n, or B x n), x_avg (Eq. average_primal,
  * PAPER.md:700-706) and lambda^K (p, or B x p) into caller buffers (host or

@@ -377,6 +377,27 @@ def theorem1_bound(alg: str, k: int, L_d: float, R_d: float, eps_in: float) -> f
     return 4.0 * L_d * R_d ** 2 / (k + 1) ** p + 2.0 * (k + 1) ** (p - 1) * eps_in
 
 
+def drift_bound(k: int, L_d: float, R_d: float, eps_in: float) -> float:
+    """Multiplier drift (bound_seq_dgm): ||lambda^k - lambda*|| <= R_d + sqrt(k eps_in / L_d)."""
+    return R_d + np.sqrt(k * eps_in / L_d)
+
+
+def feas_last_bound(alg: str, k: int, L_d: float, R_d: float, eps_in: float) -> float:
+    """Infeasibility of the last primal iterate u_bar(lambda^k), (aux_feas_bound) P:805-810:
+    d_K(G u_bar + g) <= sqrt(2 L_d eps_in) + sqrt(2 L_d (F* - d(lambda^k))), the dual gap bounded by
+    Theorem 1."""
+    return np.sqrt(2.0 * L_d * eps_in) + np.sqrt(2.0 * L_d * theorem1_bound(alg, k, L_d, R_d, eps_in))
+
+
+def feas_avg_bound(alg: str, K: int, L_d: float, R_d: float, eps_in: float) -> float:
+    """Infeasibility of the primal average over K outer iterates:
+    DGM (feasibility_final, P:918-939): (2 L_d / K) ||lambda^K - lambda^0|| <= 4 L_d R_d / K + 2 sqrt(L_d eps_in / K);
+    DFGM (infes_av): 8 L_d R_d / K^2 + 8 sqrt(L_d eps_in / K)  (the paper's k+1 = K terms)."""
+    if alg == DGM:
+        return 4.0 * L_d * R_d / K + 2.0 * np.sqrt(L_d * eps_in / K)
+    return 8.0 * L_d * R_d / K ** 2 + 8.0 * np.sqrt(L_d * eps_in / K)
+
+
 def lemma1_bound(k: int, L: float, sigma: float, R: float, p: int = 2) -> float:
     """Right-hand side of Lemma 1 (bound_gen_dfg1)."""
     lin = (1.0 - np.sqrt(sigma / L)) ** (k - 1) * L * R ** 2 if sigma > 0 else np.inf

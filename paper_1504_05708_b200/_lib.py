@@ -77,6 +77,11 @@ class Schedule(C.Structure):
     ]
 
 
+class Bounds(C.Structure):
+    _fields_ = [("dual_gap", C.c_double), ("drift", C.c_double), ("feas_last", C.c_double),
+                ("feas_avg", C.c_double)]
+
+
 PATHS = {0: "two_pass", 1: "byte_floor", 2: "rho0", 3: "rho0_floor", 4: "batched", 5: "csr", 6: "small",
          7: "persist"}
 
@@ -103,6 +108,8 @@ _SIGS = {
     "duquad_set_initial": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
     "duquad_theory_schedule": (C.c_int, [C.c_int32, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
                                          C.c_double, C.c_double, C.c_double, C.POINTER(Schedule)]),
+    "duquad_theory_bounds": (C.c_int, [C.c_int32, C.c_int64, C.c_double, C.c_double, C.c_double,
+                                       C.POINTER(Bounds)]),
     "duquad_destroy": (None, [C.c_void_p]),
     "duquad_last_error": (C.c_char_p, [C.c_void_p]),
 }

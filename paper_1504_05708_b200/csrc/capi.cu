@@ -1374,6 +1374,23 @@ duquad_status duquad_theory_schedule(int32_t alg, double eps, double R_d, double
     return DUQUAD_OK;
 }
 
+duquad_status duquad_theory_bounds(int32_t alg, int64_t k, double L_d, double R_d, double eps_in,
+                                   duquad_bounds *out) {
+    if (!out) return fail(nullptr, DUQUAD_EINVAL, "out is NULL");
+    if (alg != DUQUAD_DGM && alg != DUQUAD_DFGM) return fail(nullptr, DUQUAD_EINVAL, "bad alg");
+    if (!std::isfinite(L_d) || !std::isfinite(R_d) || !std::isfinite(eps_in) || k < 1 || !(L_d > 0) || R_d < 0 ||
+        eps_in < 0)
+        return fail(nullptr, DUQUAD_EINVAL, "bounds arguments out of range");
+    const double k1 = (double)k + 1.0, kk = (double)k;
+    const bool fast = alg == DUQUAD_DFGM;                 // p(beta) = 2 for DFGM, 1 for DGM (Eq. pbetak)
+    out->dual_gap = 4.0 * L_d * R_d * R_d / (fast ? k1 * k1 : k1) + 2.0 * (fast ? k1 : 1.0) * eps_in;
+    out->drift = R_d + std::sqrt(kk * eps_in / L_d);
+    out->feas_last = std::sqrt(2.0 * L_d * eps_in) + std::sqrt(2.0 * L_d * out->dual_gap);
+    out->feas_avg = fast ? 8.0 * L_d * R_d / (kk * kk) + 8.0 * std::sqrt(L_d * eps_in / kk)
+                         : 4.0 * L_d * R_d / kk + 2.0 * std::sqrt(L_d * eps_in / kk);
+    return DUQUAD_OK;
+}
+
 duquad_status duquad_get_inner_counts(duquad_ctx *ctx, int32_t *counts, int32_t *converged, int32_t max_entries) {
     if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
     if (max_entries < 0) return fail(ctx, DUQUAD_EINVAL, "max_entries < 0");

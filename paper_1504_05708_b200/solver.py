@@ -71,6 +71,14 @@ def theory_schedule(alg: str, eps: float, R_d: float, L_d: float, L_in: float, s
     return {k: getattr(out, k) for k, _ in L.Schedule._fields_ if k != "reserved"}
 
 
+def theory_bounds(alg: str, k: int, L_d: float, R_d: float, eps_in: float) -> dict:
+    """Convergence-bound diagnostics after k outer iterations (include/duquad.h duquad_theory_bounds)."""
+    out = L.Bounds()
+    L.check(L.lib().duquad_theory_bounds(_ALGS[alg], int(k), float(L_d), float(R_d), float(eps_in),
+                                         C.byref(out)))
+    return {k_: getattr(out, k_) for k_, _ in L.Bounds._fields_}
+
+
 class Solver:
     """One DuQuad context: setup (pack + upload), constants, solve, results.
 

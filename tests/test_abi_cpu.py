@@ -124,3 +124,20 @@ def test_theory_schedule_host_only(lib):
     assert lib.duquad_theory_schedule(1, 1e-2, 1, 1, 1, float("nan"), 1, 1, 0, C.byref(out)) == _lib.DUQUAD_EINVAL
     assert lib.duquad_theory_schedule(7, 1e-2, 1, 1, 1, 0, 1, 1, 0, C.byref(out)) == _lib.DUQUAD_EINVAL
     assert lib.duquad_status_string(_lib.DUQUAD_EMAXITER).startswith(b"inner iteration cap")
+
+
+def test_theory_bounds_host_only(lib):
+    """duquad_theory_bounds is host arithmetic: the oracle's theorem1 / drift / feasibility bounds
+    (pinned against actual DFOM runs in tests/test_oracle_pins.py)."""
+    from oracle import dfom as O
+    from paper_1504_05708_b200 import theory_bounds, _lib
+    for alg in ("DGM", "DFGM"):
+        for k, L_d, R_d, e in [(1, 2.0, 3.0, 1e-3), (17, 0.7, 12.0, 0.0), (400, 1.0, 0.0, 1e-6)]:
+            b = theory_bounds(alg, k, L_d, R_d, e)
+            assert b["dual_gap"] == pytest.approx(O.theorem1_bound(alg, k, L_d, R_d, e), rel=1e-14)
+            assert b["drift"] == pytest.approx(O.drift_bound(k, L_d, R_d, e), rel=1e-14)
+            assert b["feas_last"] == pytest.approx(O.feas_last_bound(alg, k, L_d, R_d, e), rel=1e-14, abs=1e-300)
+            assert b["feas_avg"] == pytest.approx(O.feas_avg_bound(alg, k, L_d, R_d, e), rel=1e-14, abs=1e-300)
+    for bad in [(0, 1.0, 1.0, 0.0), (3, 0.0, 1.0, 0.0), (3, 1.0, -1.0, 0.0), (3, 1.0, 1.0, float("nan"))]:
+        with pytest.raises(_lib.DuquadError):
+            theory_bounds("DGM", *bad)

@@ -533,3 +533,40 @@ def test_dgm_dual_average_final_point_in_Kd_and_dgm_only():
     with pytest.raises(ValueError):
         O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 1.0, O.DFGM, 6, 10, L_in, L_d,
                dual_average=True)
+
+
+# ------------------------------------------------------------ bound diagnostics (NEXT-2)
+@pytest.mark.parametrize("alg", ["DGM", "DFGM"])
+def test_theory_bounds_hold_on_exact_inner_solves(alg):
+    """Theorem 1, the drift bound and the last / average infeasibility
+    bounds against actual DFOM runs on an equality QP with
+    near-exact inner solves (eps_in ~ 0): lambda*, F* from the closed-form KKT system, d(lambda) in
+    closed form (rho = 0, no box)."""
+    Q, q, G, g, lb, ub, cone = _eq_qp(n=14, p=6, seed=5)
+    sol = kkt.kkt_equality(Q, q, G, g)
+    Qi = np.linalg.inv(Q)
+    L_d = float(np.linalg.eigvalsh(G @ Qi @ G.T).max())
+    L_in = float(np.linalg.eigvalsh(Q).max())
+    R_d = float(np.linalg.norm(sol.lam))                 # lambda^0 = 0
+    ubar = lambda mu: -Qi @ (q + G.T @ mu)
+    dual = lambda lam: O.objective(Q, q, ubar(lam)) + lam @ (G @ ubar(lam) + g)
+    for K in (1, 3, 10, 40):
+        r = O.dfom(Q, q, G, g, lb, ub, cone, 0.0, alg, K, 120, L_in, L_d)
+        gap = sol.F - dual(r.lam)
+        assert -1e-9 <= gap <= O.theorem1_bound(alg, K, L_d, R_d, 0.0) + 1e-9
+        assert np.linalg.norm(r.lam - sol.lam) <= O.drift_bound(K, L_d, R_d, 0.0) + 1e-9
+        assert O.dist_K(G @ r.x_last + g, cone) <= O.feas_last_bound(alg, K, L_d, R_d, 0.0) + 1e-9
+        assert O.dist_K(G @ r.x_avg + g, cone) <= O.feas_avg_bound(alg, K, L_d, R_d, 0.0) + 1e-9
+    # the bounds are informative: at K = 40 they are below their K = 1 values
+    assert O.feas_avg_bound(alg, 40, L_d, R_d, 0.0) < O.feas_avg_bound(alg, 1, L_d, R_d, 0.0)
+
+
+def test_bound_formulas_special_values():
+    """eps_in = 0 and R_d = 0 collapse every bound to 0 except the drift (R_d); DGM vs DFGM rates."""
+    assert O.theorem1_bound("DGM", 9, 2.0, 0.0, 0.0) == 0.0
+    assert O.feas_last_bound("DFGM", 9, 2.0, 0.0, 0.0) == 0.0
+    assert O.drift_bound(9, 2.0, 3.0, 0.0) == 3.0
+    assert O.drift_bound(9, 2.0, 0.0, 8.0) == pytest.approx(6.0)       # sqrt(9 * 8 / 2)
+    assert O.feas_avg_bound("DGM", 4, 1.0, 1.0, 0.0) == pytest.approx(1.0)
+    assert O.feas_avg_bound("DFGM", 4, 1.0, 1.0, 0.0) == pytest.approx(0.5)
+    assert O.theorem1_bound("DFGM", 3, 1.0, 1.0, 0.0) == pytest.approx(4.0 / 16.0)
