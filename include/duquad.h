@@ -149,6 +149,13 @@ typedef struct {
                               separated by grid barriers; bitwise the multi-launch result).
                               0 (default): one launch per pass in a CUDA graph -- measured as
                               fast or faster on config 1 (the passes are L2-latency bound)  */
+    int32_t eq_precompute; /* 1 (default): a dense single-GPU QP whose rows are all equalities
+                              (K = {0}) with rho > 0 forms H = Q + rho G'G once at setup (cuBLAS
+                              DGEMM, 2 n^2 p flops; n x n more device memory) and runs every inner
+                              step on H alone, grad = H u + c with c = q + G'(mu + rho g) once per
+                              outer iteration: 8 n(n+1)/2 bytes
+                              per step on the byte-floor path instead of 8 (n(n+1)/2 + pn).
+                              0: the generic inner step                                      */
     int32_t dual_average;  /* 1 (DGM only; EINVAL with DFGM or in eps_in mode): the final dual point
                               is lambda^K := [lam_hat + grad_bar d(lam_hat) / (2 L_d)]_{K_d} with the
                               average lam_hat = (1/(K+1)) sum_{j=0}^{K} lambda^j (PAPER.md:624-626,
@@ -181,6 +188,9 @@ typedef struct {
  *   BYTE_FLOOR k_fused_stream (Q triangle + G once) / k_fused_epi (column sums, epilogue)
  *   RHO0       k_rho0_step (Q y + c) / -            RHO0_FLOOR k_fused_stream (Q only) / k_fused_epi
  *   BATCHED    DMMA pass 0 / pass 1                 CSR        k_pass_a_csr / k_pass_b_csr
+ *   EQ_H       equality QP (all rows ZERO), rho > 0: k_rho0_step on H = Q + rho G'G (formed once,
+ *              cuBLAS DGEMM) with c = q + G'(mu + rho g) per outer iteration
+ *   EQ_H_FLOOR the same with k_fused_stream over the upper triangle of H
  *   SMALL      the whole solve in one single-CTA kernel (no per-pass timing)
  *   PERSIST    both passes of every inner step in one cooperative launch (no per-pass timing) */
 typedef enum {
@@ -191,8 +201,10 @@ typedef enum {
     DUQUAD_PATH_BATCHED = 4,
     DUQUAD_PATH_CSR = 5,
     DUQUAD_PATH_SMALL = 6,
-    DUQUAD_PATH_PERSIST = 7     /* k_persist: the two passes of every inner step in one cooperative
+    DUQUAD_PATH_PERSIST = 7,    /* k_persist: the two passes of every inner step in one cooperative
                                    launch (L2-resident dense QPs, e.g. config 1)              */
+    DUQUAD_PATH_EQ_H = 8,
+    DUQUAD_PATH_EQ_H_FLOOR = 9
 } duquad_path;
 
 int32_t duquad_abi_version(void);

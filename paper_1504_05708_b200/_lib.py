@@ -54,7 +54,7 @@ class Options(C.Structure):
         ("nccl_id", C.c_void_p), ("stream", C.c_void_p), ("device", C.c_int32),
         ("time_passes", C.c_int32), ("small_path", C.c_int32), ("rho0_path", C.c_int32),
         ("emulate_ranks", C.c_int32), ("fused_path", C.c_int32), ("persist_path", C.c_int32),
-        ("dual_average", C.c_int32),
+        ("eq_precompute", C.c_int32), ("dual_average", C.c_int32),
     ]
 
 
@@ -83,7 +83,7 @@ class Bounds(C.Structure):
 
 
 PATHS = {0: "two_pass", 1: "byte_floor", 2: "rho0", 3: "rho0_floor", 4: "batched", 5: "csr", 6: "small",
-         7: "persist"}
+         7: "persist", 8: "eq_h", 9: "eq_h_floor"}
 
 
 _SIGS = {

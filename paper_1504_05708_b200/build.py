@@ -24,6 +24,16 @@ def _nccl_dirs():
     return os.path.join(base, "include"), os.path.join(base, "lib")
 
 
+def _cublas_libdir():
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    if spec is not None and spec.submodule_search_locations:
+        d = os.path.join(list(spec.submodule_search_locations)[0], "cublas", "lib")
+        if os.path.exists(os.path.join(d, "libcublas.so.12")):
+            return d
+    raise RuntimeError("cuBLAS (nvidia-cublas wheel) not found")
+
+
 def build(verbose: bool = False) -> str:
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     inc, libdir = _nccl_dirs()
@@ -36,7 +46,8 @@ def build(verbose: bool = False) -> str:
     cmd = [nvcc, ARCH, *extra, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "-Xcompiler", "-ffp-contract=off", "-Xptxas", "-v" if verbose else "-O3",
            f"-I{inc}", f"-I{os.path.join(ROOT, 'include')}", "-o", OUT + ".tmp", *srcs,
-           f"-L{libdir}", "-l:libnccl.so.2", f"-Xlinker=-rpath,{libdir}"]
+           f"-L{libdir}", "-l:libnccl.so.2", f"-Xlinker=-rpath,{libdir}",
+           f"-L{_cublas_libdir()}", "-l:libcublas.so.12", f"-Xlinker=-rpath,{_cublas_libdir()}"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + r.stdout + r.stderr)

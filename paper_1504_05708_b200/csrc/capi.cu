@@ -12,6 +12,7 @@
 //       pass B   G'w -> x, y        (k = K_in: y <- x, running average)
 //       (all-gather y)
 //     advance j
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -62,7 +63,9 @@ struct duquad_ctx {
     double *hb = nullptr;   // batched: h = mu + rho g per (QP, G row), refreshed by every DFOM step
     // rho = 0 specialisation (K3): second y replica (ping-pong) and c = q + G'mu
     bool rho0 = false;
-    bool davg = false;   // this solve: DGM dual-averaging final point (options.dual_average)
+    bool davg = false;
+    bool eqh = false;          // equality QP on H = Q + rho G'G (options.eq_precompute, NEXT-3)
+    double *Hq = nullptr;      // H, n x ld row-major (exactly symmetric)   // this solve: DGM dual-averaging final point (options.dual_average)
     double *lam_hat = nullptr, *lhb = nullptr;   // running dual average (single QP / batched)
     double *y_full2 = nullptr, *cvec = nullptr;
     LaunchCfg cfg_k3{};
@@ -147,7 +150,7 @@ void free_all(duquad_ctx *c) {
     double *ds[] = {c->A,   c->GT,  c->y_full, c->w_full, c->qy,       c->x,        c->xhat,     c->q,
                     c->lb,  c->ub,  c->g,      c->mu,     c->lam_prev, c->lz_vprev, c->lz_w,     c->scal,
                     c->partials, c->Yb, c->Xb, c->XHb,   c->QYb,      c->qb,       c->Wb,       c->gb,
-                    c->mub, c->lpb, c->hb, c->d_beta, c->y_full2, c->cvec, c->ws, c->lam_hat, c->lhb};
+                    c->mub, c->lpb, c->hb, c->d_beta, c->y_full2, c->cvec, c->ws, c->lam_hat, c->lhb, c->Hq};
     for (double *d : ds)
         if (d) cudaFree(d);
     if (c->cone) cudaFree(c->cone);
@@ -342,6 +345,7 @@ duquad_status outer_phase(duquad_ctx *ctx, const std::vector<double> &beta_in, i
             PassAArgs a = make_a(ctx);
             a.row_begin = ctx->nloc;          // G rows only
             a.first_inner = 1;
+            a.w_plus_g = ctx->eqh;            // H path: w = mu + rho g, so c = q + G'(mu + rho g)
             a.y = Y[Kin % 2];                 // the replica the previous inner solve finished in
             CK(launch_pass_a(a, MODE_SOLVE, ctx->cfg_a, ctx->stream));
             if ((st = trace_lam_copy(ctx, j)) != DUQUAD_OK) return st;
@@ -358,6 +362,7 @@ duquad_status outer_phase(duquad_ctx *ctx, const std::vector<double> &beta_in, i
         } else {
             const int k = ph - 1;
             PassAArgs a3 = make_a(ctx);
+            if (ctx->eqh) a3.A = ctx->Hq;     // H = Q + rho G'G
             a3.y = Y[(k - 1) % 2];
             PassBArgs bl = make_b(ctx);
             bl.q = ctx->cvec;
@@ -731,6 +736,7 @@ void duquad_default_options(duquad_options *o) {
     o->fused_path = 1;
     o->persist_path = 0;
     o->dual_average = 0;
+    o->eq_precompute = 1;
 }
 
 duquad_status duquad_shard_range(int64_t rows, int32_t world, int32_t rank, int64_t *begin,
@@ -1030,6 +1036,46 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         ctx->cfg_k3 = {ctx->cfg_b.grid, pass_threads(), smem_a};
         ctx->rho0 = true;
     }
+    if (!batched && !csr && ctx->world == 1 && rho > 0.0 && p > 0 && opt.eq_precompute) {
+        // NEXT-3: with every row an equality (K = {0}) the inner gradient is
+        // (Q + rho G'G) u + q + G'(mu + rho g): form H once, then the K3 machinery streams H alone.
+        bool all_zero = true;
+        if (!prob->cone) {
+            all_zero = prob->cone_all == DUQUAD_CONE_ZERO;
+        } else {
+            std::vector<uint8_t> hc((size_t)p);
+            CKS(cudaMemcpy(hc.data(), prob->cone, (size_t)p, cudaMemcpyDefault));
+            for (uint8_t c : hc) all_zero = all_zero && c == DUQUAD_CONE_ZERO;
+        }
+        if (all_zero) {
+            CKS(dalloc(&ctx->Hq, n * ctx->ld));
+            CKS(cudaMemcpyAsync(ctx->Hq, ctx->A, n * ctx->ld * sizeof(double), cudaMemcpyDeviceToDevice, s));
+            // column-major view of the G rows: Gc (ld x p), column k = G row k; H += rho Gc Gc'
+            cublasHandle_t hb = nullptr;
+            if (cublasCreate(&hb) != CUBLAS_STATUS_SUCCESS) {
+                ctx->err = "cublasCreate failed";
+                return bail(DUQUAD_ECUDA);
+            }
+            const double alpha = rho, beta = 1.0;
+            cublasSetStream(hb, s);
+            const cublasStatus_t cs = cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_T, (int)n, (int)n, (int)p, &alpha,
+                                                  ctx->A + n * ctx->ld, (int)ctx->ld, ctx->A + n * ctx->ld,
+                                                  (int)ctx->ld, &beta, ctx->Hq, (int)ctx->ld);
+            cublasDestroy(hb);
+            if (cs != CUBLAS_STATUS_SUCCESS) {
+                ctx->err = "cublasDgemm (H = Q + rho G'G) failed";
+                return bail(DUQUAD_ECUDA);
+            }
+            CKS(launch_mirror_upper(ctx->Hq, n, ctx->ld, s));   // exactly symmetric: H_ji := H_ij, i < j
+            if (!ctx->rho0) {
+                CKS(dalloc(&ctx->y_full2, ctx->ylen));
+                CKS(dalloc(&ctx->cvec, ctx->nloc));
+                ctx->cfg_k3 = {ctx->cfg_b.grid, pass_threads(), smem_a};
+            }
+            ctx->rho0 = true;
+            ctx->eqh = true;
+        }
+    }
     if (!batched && ctx->world == 1 && opt.fused_path &&
         fused_supported(n, ctx->ld, prop.sharedMemPerBlockOptin)) {   // byte-floor inner step
         const int cg = (!ctx->rho0 && p > 0) ? 2 : 1;   // G role: CTA pairs (148 SMs usable)
@@ -1071,7 +1117,7 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         CKS(dalloc(&ctx->ws, wrow + wcol + wg));
         CKS(dalloc(&ctx->fpieces, (int64_t)nq));
         CKS(cudaMemcpy(ctx->fpieces, pcs.data(), nq * sizeof(FusedPiece), cudaMemcpyHostToDevice));
-        fz.Q = ctx->A;
+        fz.Q = ctx->eqh ? ctx->Hq : ctx->A;
         fz.G = ctx->A + n * ctx->ld;
         fz.y = ctx->y_full;
         fz.ws_rowp = ctx->ws;
@@ -1564,7 +1610,8 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
         float ms = 0.f;
         cudaEventElapsedTime(&ms, t0, t1);
         res->ms_device = ms;
-        res->path = ctx->fused ? (ctx->rho0 ? DUQUAD_PATH_RHO0_FLOOR : DUQUAD_PATH_BYTE_FLOOR)
+        res->path = ctx->eqh ? (ctx->fused ? DUQUAD_PATH_EQ_H_FLOOR : DUQUAD_PATH_EQ_H)
+                    : ctx->fused ? (ctx->rho0 ? DUQUAD_PATH_RHO0_FLOOR : DUQUAD_PATH_BYTE_FLOOR)
                     : ctx->rho0 ? DUQUAD_PATH_RHO0
                     : ctx->Btot > 1 ? DUQUAD_PATH_BATCHED
                     : ctx->format == DUQUAD_CSR ? DUQUAD_PATH_CSR : DUQUAD_PATH_TWO_PASS;

@@ -44,6 +44,7 @@ struct PassAArgs {
     double *lam_prev;
     double *h;           // batched only (else null): h[k] = mu[k] + rho g[k], written by the DFOM step
     double *lam_hat;     // DGM dual averaging only (else null): running average of lambda^0..lambda^j
+    int32_t w_plus_g;    // equality-QP H path, DFOM-step launch: w = mu + rho g (c = q + G'w)
     const uint8_t *cone;
     double rho;
     double step;         // dual_step_scale / L_d
@@ -197,6 +198,7 @@ cudaError_t launch_batched(const BatchedArgs &a, int pass, int mode, cudaStream_
 cudaError_t launch_init_batched(double *x, double *y, double *xhat, const double *lb, const double *ub, int64_t n,
                                 int64_t sn, double *mu, double *lam_prev, int64_t sp, int64_t B, int32_t *d_j,
                                 int32_t *flag, cudaStream_t s);
+cudaError_t launch_mirror_upper(double *H, int64_t n, int64_t ld, cudaStream_t s);
 cudaError_t launch_batched_h(double *h, const double *mu, const double *g, double rho, int64_t p, int64_t sp,
                              int64_t B, cudaStream_t s);
 

@@ -117,8 +117,9 @@ __device__ __forceinline__ void epi_a_store(const PassAArgs &a, int mode, int64_
         a.mu[k] = m;
         if (a.h) a.h[k] = m + a.rho * e.g;   // batched: the constant part of the next w's
     }
-    // multiplier term of grad L_rho: [mu + rho r]_{K°} (rho > 0), mu (rho = 0)
-    a.w[k] = a.rho > 0.0 ? proj_polar(m + a.rho * r, e.c) : m;
+    // multiplier term of grad L_rho: [mu + rho r]_{K°} (rho > 0), mu (rho = 0); on the
+    // equality-QP H path the constant part mu + rho g (the rho G'G u part is inside H)
+    a.w[k] = a.w_plus_g ? m + a.rho * e.g : a.rho > 0.0 ? proj_polar(m + a.rho * r, e.c) : m;
 }
 
 // ------------------------------------------------------------------ pass B

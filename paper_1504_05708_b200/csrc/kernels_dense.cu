@@ -252,6 +252,14 @@ __global__ void k_init_state(double *x, double *y, double *xhat, const double *l
 
 __global__ void k_advance(int32_t *d_j) { *d_j += 1; }
 
+// H_ji := H_ij for i < j (row-major, leading dim ld): an exactly symmetric H for the equality path
+__global__ void k_mirror_upper(double *H, int64_t n, int64_t ld) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n * n) return;
+    const int64_t i = t / n, j = t % n;
+    if (i < j) H[j * ld + i] = H[i * ld + j];
+}
+
 // warm start (duquad_set_initial): u_bar^0 = [x0]_U, lambda^0 = mu^1 = lam0, for B QPs with
 // strides sn / sp (B = 1: plain slices); runs after k_init_state / k_init_batched
 __global__ void k_apply_initial(double *x, double *y, const double *lb, const double *ub, int64_t n, int64_t sn,
@@ -628,6 +636,13 @@ cudaError_t launch_reduce_final(const double *partials, int nparts, int nvals, d
 cudaError_t launch_fill_hash(double *v, int64_t n, int64_t offset, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     k_fill_hash<<<blocks_for(n, 256), 256, 0, s>>>(v, n, offset);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mirror_upper(double *H, int64_t n, int64_t ld, cudaStream_t s) {
+    if (n <= 1) return cudaSuccess;
+    const int64_t m = n * n;
+    k_mirror_upper<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(H, n, ld);
     return cudaGetLastError();
 }
 
