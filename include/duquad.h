@@ -156,6 +156,9 @@ typedef struct {
                               outer iteration: 8 n(n+1)/2 bytes
                               per step on the byte-floor path instead of 8 (n(n+1)/2 + pn).
                               0: the generic inner step                                      */
+    int32_t checkpoint;    /* 1: every solve snapshots its state after outer iteration K (before the
+                              last-iterate solve) for duquad_get_state; the single-CTA and
+                              persistent kernels defer to the streaming path.  0 (default)   */
     int32_t dual_average;  /* 1 (DGM only; EINVAL with DFGM or in eps_in mode): the final dual point
                               is lambda^K := [lam_hat + grad_bar d(lam_hat) / (2 L_d)]_{K_d} with the
                               average lam_hat = (1/(K+1)) sum_{j=0}^{K} lambda^j (PAPER.md:624-626,
@@ -315,6 +318,24 @@ typedef struct {
 duquad_status duquad_theory_schedule(int32_t alg, double eps, double R_d, double L_d, double L_in,
                                      double sigma_L, double D_U, double normG, double lambda_min_Q,
                                      duquad_schedule *out);
+
+/*
+ * State export / resume (the DFOM state of PAPER.md:564-589 after outer iteration
+ * j): x = u_bar^j (n, or B x n), mu = mu^j and lam_prev = lambda^{j-1} (p, or B x p, the two
+ * points the next DFOM step reads), x_avg = the running primal average with
+ * S = sum_{i<=j} omega_i, and j = outer_done.
+ *   duquad_get_state: the snapshot the last solve took (options.checkpoint = 1), i.e. after its
+ *     K-th outer iteration, before the last-iterate solve; DUQUAD_ESTATE if there is none.
+ *   duquad_set_state: the next duquad_solve(alg, K, ...) continues with outer iterations
+ *     j+1 .. j+K (theta, beta_out and the average weights continue; warm start ignored), so
+ *     solve(K1) + get_state + set_state + solve(K2) equals solve(K1 + K2) bit for bit.
+ * Buffers are host or device per on_device (layout as duquad_get_result); single GPU (batch
+ * allowed); fixed inner counts, no dual_average.  DUQUAD_EINVAL on bad arguments.
+ */
+duquad_status duquad_get_state(duquad_ctx *ctx, double *x, double *mu, double *lam_prev, double *x_avg,
+                               int64_t *outer_done, double *S, int32_t on_device);
+duquad_status duquad_set_state(duquad_ctx *ctx, const double *x, const double *mu, const double *lam_prev,
+                               const double *x_avg, int64_t outer_done, double S, int32_t on_device);
 
 /* Convergence-bound diagnostics of DuQuad (host-only arithmetic, no GPU), for k outer iterations. */
 typedef struct {

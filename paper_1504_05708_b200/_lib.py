@@ -54,7 +54,7 @@ class Options(C.Structure):
         ("nccl_id", C.c_void_p), ("stream", C.c_void_p), ("device", C.c_int32),
         ("time_passes", C.c_int32), ("small_path", C.c_int32), ("rho0_path", C.c_int32),
         ("emulate_ranks", C.c_int32), ("fused_path", C.c_int32), ("persist_path", C.c_int32),
-        ("eq_precompute", C.c_int32), ("dual_average", C.c_int32),
+        ("eq_precompute", C.c_int32), ("checkpoint", C.c_int32), ("dual_average", C.c_int32),
     ]
 
 
@@ -110,6 +110,10 @@ _SIGS = {
                                          C.c_double, C.c_double, C.c_double, C.POINTER(Schedule)]),
     "duquad_theory_bounds": (C.c_int, [C.c_int32, C.c_int64, C.c_double, C.c_double, C.c_double,
                                        C.POINTER(Bounds)]),
+    "duquad_get_state": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.POINTER(C.c_int64), C.POINTER(C.c_double), C.c_int32]),
+    "duquad_set_state": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                   C.c_double, C.c_int32]),
     "duquad_destroy": (None, [C.c_void_p]),
     "duquad_last_error": (C.c_char_p, [C.c_void_p]),
 }

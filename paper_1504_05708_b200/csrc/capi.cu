@@ -64,7 +64,15 @@ struct duquad_ctx {
     // rho = 0 specialisation (K3): second y replica (ping-pong) and c = q + G'mu
     bool rho0 = false;
     bool davg = false;
-    bool eqh = false;          // equality QP on H = Q + rho G'G (options.eq_precompute, NEXT-3)
+    bool eqh = false;
+    // state export / resume (NEXT-2): the state after outer iteration j (before the last-iterate solve)
+    double *ck_x = nullptr, *ck_mu = nullptr, *ck_lp = nullptr, *ck_xh = nullptr;
+    bool ck_valid = false;     // a checkpoint from the last solve (options.checkpoint) or set_state
+    bool resume = false;       // the next solve continues from the checkpoint (duquad_set_state)
+    bool resumed = false;      // this solve is a continuation
+    int64_t ck_j = 0, j0 = 0;  // outer iterations done at the checkpoint; offset of this solve
+    double ck_S = 0.0, S_end = 0.0;
+    int32_t h_j = 0;          // equality QP on H = Q + rho G'G (options.eq_precompute, NEXT-3)
     double *Hq = nullptr;      // H, n x ld row-major (exactly symmetric)   // this solve: DGM dual-averaging final point (options.dual_average)
     double *lam_hat = nullptr, *lhb = nullptr;   // running dual average (single QP / batched)
     double *y_full2 = nullptr, *cvec = nullptr;
@@ -150,7 +158,7 @@ void free_all(duquad_ctx *c) {
     double *ds[] = {c->A,   c->GT,  c->y_full, c->w_full, c->qy,       c->x,        c->xhat,     c->q,
                     c->lb,  c->ub,  c->g,      c->mu,     c->lam_prev, c->lz_vprev, c->lz_w,     c->scal,
                     c->partials, c->Yb, c->Xb, c->XHb,   c->QYb,      c->qb,       c->Wb,       c->gb,
-                    c->mub, c->lpb, c->hb, c->d_beta, c->y_full2, c->cvec, c->ws, c->lam_hat, c->lhb, c->Hq};
+                    c->mub, c->lpb, c->hb, c->d_beta, c->y_full2, c->cvec, c->ws, c->lam_hat, c->lhb, c->Hq, c->ck_x, c->ck_mu, c->ck_lp, c->ck_xh};
     for (double *d : ds)
         if (d) cudaFree(d);
     if (c->cone) cudaFree(c->cone);
@@ -737,6 +745,7 @@ void duquad_default_options(duquad_options *o) {
     o->persist_path = 0;
     o->dual_average = 0;
     o->eq_precompute = 1;
+    o->checkpoint = 0;
 }
 
 duquad_status duquad_shard_range(int64_t rows, int32_t world, int32_t rank, int64_t *begin,
@@ -1217,10 +1226,16 @@ static duquad_status solve_prepare(duquad_ctx *ctx, int alg, int K, int Kin, std
         return fail(ctx, DUQUAD_EINVAL, "dual_average is the DGM final-point rule (PAPER.md:624-626): use alg = DGM");
     if (ctx->davg && ctx->eps_mode)
         return fail(ctx, DUQUAD_EINVAL, "dual_average: fixed inner counts only");
+    ctx->resumed = ctx->resume;
+    ctx->resume = false;
+    if ((ctx->resumed || ctx->opt.checkpoint) && (ctx->davg || ctx->eps_mode || ctx->world > 1))
+        return fail(ctx, DUQUAD_EINVAL, "checkpoint / resume: fixed counts, no dual_average, single GPU");
+    ctx->j0 = ctx->resumed ? ctx->ck_j : 0;
+    const int J0 = (int)ctx->j0;
     // ---- host tables (fp64, PAPER.md:358-363 / 587-589 / 700-706)
-    std::vector<double> theta(K + 3, 0.0);
+    std::vector<double> theta(J0 + K + 3, 0.0);
     theta[1] = 1.0;
-    for (int k = 1; k < K + 2; ++k) theta[k + 1] = (1.0 + std::sqrt(1.0 + 4.0 * theta[k] * theta[k])) / 2.0;
+    for (int k = 1; k < J0 + K + 2; ++k) theta[k + 1] = (1.0 + std::sqrt(1.0 + 4.0 * theta[k] * theta[k])) / 2.0;
     beta_in.assign(Kin + 1, 0.0);
     if (ctx->opt.inner_rule == DUQUAD_INNER_FGM) {
         std::vector<double> th(Kin + 2, 0.0);
@@ -1232,16 +1247,18 @@ static duquad_status solve_prepare(duquad_ctx *ctx, int alg, int K, int Kin, std
                          (std::sqrt(ctx->L_in) + std::sqrt(ctx->opt.sigma));
         for (int k = 1; k <= Kin; ++k) beta_in[k] = b;
     }
-    std::vector<OuterParam> ops(K + 2);
-    double S = 0.0;
-    for (int j = 1; j <= K; ++j) {
+    // outer iterations j = J0+1 .. J0+K (J0 > 0: a continuation of an earlier solve, duquad_set_state)
+    std::vector<OuterParam> ops(J0 + K + 2);
+    double S = ctx->resumed ? ctx->ck_S : 0.0;
+    for (int j = J0 + 1; j <= J0 + K; ++j) {
         const double omega = alg == DUQUAD_DFGM ? theta[j] : 1.0;
         S += omega;
         ops[j].avg_w = omega / S;
         ops[j].dual_update = j >= 2;
         ops[j].beta_out = (j >= 2 && alg == DUQUAD_DFGM) ? (theta[j - 1] - 1.0) / theta[j] : 0.0;
     }
-    ops[K + 1] = OuterParam{0.0, 0.0, 1, 0, 0.0};   // last-iterate solve at lambda^K (mu := lambda^K)
+    ctx->S_end = S;
+    ops[J0 + K + 1] = OuterParam{0.0, 0.0, 1, 0, 0.0};   // last-iterate solve at lambda^K (mu := lambda^K)
     if (ctx->davg) {
         // DGM dual averaging: the DFOM step of outer j >= 2 computes lambda^{j-1} and
         // folds it into lam_hat with weight 1/j (lam_hat starts at lambda^0); outer K+1 folds in
@@ -1273,6 +1290,26 @@ static duquad_status solve_prepare(duquad_ctx *ctx, int alg, int K, int Kin, std
         else
             CK(launch_apply_initial(ctx->x, ctx->y_full + ctx->rank * ctx->n_slice, ctx->lb, ctx->ub, ctx->nloc, 0,
                                     ctx->init_x, ctx->mu, ctx->lam_prev, ctx->ploc, 0, ctx->init_lam, 1, s));
+    }
+    if (ctx->resumed) {   // continue from the checkpoint: u_bar^{j0}, mu^{j0}, lambda^{j0-1}, x_hat, j = j0 + 1
+        const bool bt = ctx->Btot > 1;
+        const int64_t nx = bt ? ctx->Bloc * ctx->ld : ctx->nloc, nl = bt ? ctx->Bloc * std::max<int64_t>(ctx->ldp, 2)
+                                                                         : ctx->ploc;
+        double *X = bt ? ctx->Xb : ctx->x, *Y = bt ? ctx->Yb : ctx->y_full + ctx->rank * ctx->n_slice;
+        double *XH = bt ? ctx->XHb : ctx->xhat, *MU = bt ? ctx->mub : ctx->mu, *LP = bt ? ctx->lpb : ctx->lam_prev;
+        const cudaMemcpyKind d2d = cudaMemcpyDeviceToDevice;
+        if (nx > 0) {
+            CK(cudaMemcpyAsync(X, ctx->ck_x, nx * sizeof(double), d2d, s));
+            CK(cudaMemcpyAsync(Y, ctx->ck_x, nx * sizeof(double), d2d, s));
+            CK(cudaMemcpyAsync(XH, ctx->ck_xh, nx * sizeof(double), d2d, s));
+        }
+        if (nl > 0) {
+            CK(cudaMemcpyAsync(MU, ctx->ck_mu, nl * sizeof(double), d2d, s));
+            CK(cudaMemcpyAsync(LP, ctx->ck_lp, nl * sizeof(double), d2d, s));
+        }
+        ctx->h_j = (int32_t)(J0 + 1);
+        CK(cudaMemcpyAsync(ctx->d_j, &ctx->h_j, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));   // h_j is pageable host memory
     }
     if (ctx->Btot > 1)   // h = mu + rho g for the first outer iteration (no DFOM step there)
         CK(launch_batched_h(ctx->hb, ctx->mub, ctx->gb, ctx->rho, ctx->p, std::max<int64_t>(ctx->ldp, 2), ctx->Bloc,
@@ -1448,6 +1485,105 @@ duquad_status duquad_get_inner_counts(duquad_ctx *ctx, int32_t *counts, int32_t 
     return DUQUAD_OK;
 }
 
+// device sizes of the state vectors (x, x_hat: n-vectors; mu, lambda_prev: p-vectors) in this
+// context's layout (QP-major with strides ld / ldp for a batch)
+static void state_sizes(const duquad_ctx *ctx, int64_t *nx, int64_t *nl) {
+    const bool bt = ctx->Btot > 1;
+    *nx = bt ? ctx->Bloc * ctx->ld : ctx->nloc;
+    *nl = bt ? ctx->Bloc * std::max<int64_t>(ctx->ldp, 2) : ctx->ploc;
+}
+
+static duquad_status alloc_state(duquad_ctx *ctx) {
+    int64_t nx, nl;
+    state_sizes(ctx, &nx, &nl);
+    if (!ctx->ck_x) CK(dalloc(&ctx->ck_x, nx));
+    if (!ctx->ck_xh) CK(dalloc(&ctx->ck_xh, nx));
+    if (!ctx->ck_mu) CK(dalloc(&ctx->ck_mu, nl));
+    if (!ctx->ck_lp) CK(dalloc(&ctx->ck_lp, nl));
+    return DUQUAD_OK;
+}
+
+// the state after outer iteration K of this solve: u_bar^K, mu^K, lambda^{K-1}, x_hat (enqueued)
+static duquad_status save_checkpoint(duquad_ctx *ctx) {
+    duquad_status st = alloc_state(ctx);
+    if (st != DUQUAD_OK) return st;
+    int64_t nx, nl;
+    state_sizes(ctx, &nx, &nl);
+    const bool bt = ctx->Btot > 1;
+    const cudaMemcpyKind d2d = cudaMemcpyDeviceToDevice;
+    if (nx > 0) {
+        CK(cudaMemcpyAsync(ctx->ck_x, bt ? ctx->Xb : ctx->x, nx * sizeof(double), d2d, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->ck_xh, bt ? ctx->XHb : ctx->xhat, nx * sizeof(double), d2d, ctx->stream));
+    }
+    if (nl > 0) {
+        CK(cudaMemcpyAsync(ctx->ck_mu, bt ? ctx->mub : ctx->mu, nl * sizeof(double), d2d, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->ck_lp, bt ? ctx->lpb : ctx->lam_prev, nl * sizeof(double), d2d, ctx->stream));
+    }
+    return DUQUAD_OK;
+}
+
+// caller layout <-> context layout of one state vector (len per QP, stride ld per QP in a batch)
+static duquad_status state_copy(duquad_ctx *ctx, double *dst, const double *src, int64_t len, int64_t ld,
+                                bool to_ctx, int32_t on_device) {
+    const int64_t B = ctx->Btot > 1 ? ctx->Bloc : 1;
+    if (len <= 0 || B <= 0) return DUQUAD_OK;
+    const int64_t ldc = ctx->Btot > 1 ? ld : len;
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice
+                                          : (to_ctx ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost);
+    if (to_ctx)
+        CK(cudaMemcpy2DAsync(dst, ldc * sizeof(double), src, len * sizeof(double), len * sizeof(double), B, kind,
+                             ctx->stream));
+    else
+        CK(cudaMemcpy2DAsync(dst, len * sizeof(double), src, ldc * sizeof(double), len * sizeof(double), B, kind,
+                             ctx->stream));
+    return DUQUAD_OK;
+}
+
+duquad_status duquad_get_state(duquad_ctx *ctx, double *x, double *mu, double *lam_prev, double *x_avg,
+                               int64_t *outer_done, double *S, int32_t on_device) {
+    if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
+    if (!ctx->ck_valid) return fail(ctx, DUQUAD_ESTATE, "no checkpoint: solve with options.checkpoint = 1 first");
+    DevGuard guard(ctx->dev);
+    const int64_t n = ctx->Btot > 1 ? ctx->n : ctx->nloc, p = ctx->Btot > 1 ? ctx->p : ctx->ploc;
+    const int64_t sp = std::max<int64_t>(ctx->ldp, 2);
+    duquad_status st;
+    if (x && (st = state_copy(ctx, x, ctx->ck_x, n, ctx->ld, false, on_device)) != DUQUAD_OK) return st;
+    if (x_avg && (st = state_copy(ctx, x_avg, ctx->ck_xh, n, ctx->ld, false, on_device)) != DUQUAD_OK) return st;
+    if (mu && (st = state_copy(ctx, mu, ctx->ck_mu, p, sp, false, on_device)) != DUQUAD_OK) return st;
+    if (lam_prev && (st = state_copy(ctx, lam_prev, ctx->ck_lp, p, sp, false, on_device)) != DUQUAD_OK) return st;
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (outer_done) *outer_done = ctx->ck_j;
+    if (S) *S = ctx->ck_S;
+    return DUQUAD_OK;
+}
+
+duquad_status duquad_set_state(duquad_ctx *ctx, const double *x, const double *mu, const double *lam_prev,
+                               const double *x_avg, int64_t outer_done, double S, int32_t on_device) {
+    if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
+    if (ctx->world > 1) return fail(ctx, DUQUAD_EINVAL, "set_state: single GPU only");
+    if (outer_done < 1 || !(S > 0) || !std::isfinite(S) || outer_done > (1 << 28))
+        return fail(ctx, DUQUAD_EINVAL, "set_state: outer_done >= 1 and S > 0 (the averaging weight sum)");
+    if (!x || !x_avg || (ctx->p > 0 && (!mu || !lam_prev)))
+        return fail(ctx, DUQUAD_EINVAL, "set_state: x, x_avg, mu and lam_prev are all required");
+    DevGuard guard(ctx->dev);
+    duquad_status st = alloc_state(ctx);
+    if (st != DUQUAD_OK) return st;
+    const int64_t n = ctx->Btot > 1 ? ctx->n : ctx->nloc, p = ctx->Btot > 1 ? ctx->p : ctx->ploc;
+    const int64_t sp = std::max<int64_t>(ctx->ldp, 2);
+    if ((st = state_copy(ctx, ctx->ck_x, x, n, ctx->ld, true, on_device)) != DUQUAD_OK) return st;
+    if ((st = state_copy(ctx, ctx->ck_xh, x_avg, n, ctx->ld, true, on_device)) != DUQUAD_OK) return st;
+    if (p > 0) {
+        if ((st = state_copy(ctx, ctx->ck_mu, mu, p, sp, true, on_device)) != DUQUAD_OK) return st;
+        if ((st = state_copy(ctx, ctx->ck_lp, lam_prev, p, sp, true, on_device)) != DUQUAD_OK) return st;
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->ck_valid = true;
+    ctx->ck_j = outer_done;
+    ctx->ck_S = S;
+    ctx->resume = true;
+    return DUQUAD_OK;
+}
+
 static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t inner, duquad_result *res) {
     if (alg != DUQUAD_DGM && alg != DUQUAD_DFGM) return fail(ctx, DUQUAD_EINVAL, "bad alg");
     if (outer < 1 || inner < 1) return fail(ctx, DUQUAD_EINVAL, "need outer_iters >= 1 and inner_iters >= 1");
@@ -1462,7 +1598,7 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
     }
     duquad_status st;
     if ((st = allgather_y(ctx)) != DUQUAD_OK) return st;
-    if (ctx->small && !ctx->eps_mode && !ctx->davg &&
+    if (ctx->small && !ctx->eps_mode && !ctx->davg && !ctx->resumed && !ctx->opt.checkpoint &&
         small_smem_bytes(ctx->n, ctx->p, ctx->ld, ctx->ldp, K, Kin) <= ctx->small_smem) {   // whole solve in one CTA (K4)
         if (ctx->beta_cap < Kin + 1) {
             if (ctx->d_beta) cudaFree(ctx->d_beta);
@@ -1527,7 +1663,7 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
         return DUQUAD_OK;
     }
     const bool tracing = ctx->trace_lam || ctx->trace_u;
-    if (ctx->persist && !tracing && !ctx->eps_mode && !ctx->davg) {   // the whole solve in one cooperative launch
+    if (ctx->persist && !tracing && !ctx->eps_mode && !ctx->davg && !ctx->resumed && !ctx->opt.checkpoint) {   // the whole solve in one cooperative launch
         if (ctx->beta_cap < Kin + 1) {
             if (ctx->d_beta) cudaFree(ctx->d_beta);
             ctx->d_beta = nullptr;
@@ -1587,6 +1723,7 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
     CK(cudaEventRecord(t0, s));
     const int nout = K + 1 + (ctx->davg ? 1 : 0);   // + the solve at the dual average
     for (int j = 1; j <= nout; ++j) {
+        if (j == K + 1 && ctx->opt.checkpoint && (st = save_checkpoint(ctx)) != DUQUAD_OK) break;
         if (j == j_timed) {
             st = run_outer(ctx, beta_in, Kin, j, &ev);
         } else if (graphs) {
@@ -1668,6 +1805,11 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
     cudaEventDestroy(t1);
     for (auto &e : ev) cudaEventDestroy(e);
     ctx->solved = true;
+    if (ctx->opt.checkpoint && !flag) {
+        ctx->ck_valid = true;
+        ctx->ck_j = ctx->j0 + K;
+        ctx->ck_S = ctx->S_end;
+    }
     if (flag) return fail(ctx, DUQUAD_ENONFINITE, "an iterate became non-finite");
     return DUQUAD_OK;
 }

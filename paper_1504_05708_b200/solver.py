@@ -93,7 +93,8 @@ class Solver:
                  nccl_id: Optional[bytes] = None, stream=None, device: int = -1,
                  time_passes: bool = False, cone_all: int = L.CONE_NONPOS, small_path: bool = True,
                  rho0_path: bool = True, emulate_ranks: bool = False, fused_path: bool = True,
-                 persist_path: bool = False, dual_average: bool = False, eq_precompute: bool = True):
+                 persist_path: bool = False, dual_average: bool = False, eq_precompute: bool = True,
+                 checkpoint: bool = False):
         """Dense Q (n x n) and G (p x n), or scipy.sparse matrices (-> CSR path, row a10).
         dual_average: DGM final dual point from the average of lambda^0..lambda^K."""
         if hasattr(Q, "tocsr"):
@@ -117,7 +118,7 @@ class Solver:
                         world_size=world_size, rank=rank, nccl_id=nccl_id, stream=stream, device=device,
                         time_passes=time_passes, small_path=small_path, rho0_path=rho0_path,
                         emulate_ranks=emulate_ranks, fused_path=fused_path, persist_path=persist_path,
-                        dual_average=dual_average, eq_precompute=eq_precompute))
+                        dual_average=dual_average, eq_precompute=eq_precompute, checkpoint=checkpoint))
 
     @classmethod
     def csr(cls, n, p, Q_rowptr, Q_col, Q_val, G_rowptr, G_col, G_val, q, g, lb, ub, cone=None,
@@ -181,6 +182,7 @@ class Solver:
         opt.persist_path = int(o.get("persist_path", False))
         opt.dual_average = int(o.get("dual_average", False))
         opt.eq_precompute = int(o.get("eq_precompute", True))
+        opt.checkpoint = int(o.get("checkpoint", False))
         ctx = C.c_void_p()
         L.check(lib.duquad_setup(C.byref(ctx), C.byref(prob), float(rho), C.byref(opt)))
         self._ctx = ctx
@@ -276,6 +278,26 @@ class Solver:
         L.check(self._lib.duquad_get_result(self._ctx, xl.ctypes.data, xa.ctypes.data, lam.ctypes.data, 0),
                 self._ctx)
         return xl, xa, lam[..., :pl]
+
+    def get_state(self) -> dict:
+        """The DFOM state the last solve snapshotted after its K-th outer iteration (needs
+        checkpoint=True): x = u_bar^K, mu = mu^K, lam_prev = lambda^{K-1}, x_avg, outer_done, S."""
+        bl = self.b_range[1] - self.b_range[0]
+        shp_n = (bl, self.n) if self.batch > 1 else (self.n,)
+        shp_p = (bl, max(self.p, 1)) if self.batch > 1 else (max(self.p, 1),)
+        x, xa = np.empty(shp_n), np.empty(shp_n)
+        mu, lp = np.empty(shp_p), np.empty(shp_p)
+        j, S = C.c_int64(), C.c_double()
+        L.check(self._lib.duquad_get_state(self._ctx, x.ctypes.data, mu.ctypes.data, lp.ctypes.data, xa.ctypes.data,
+                                           C.byref(j), C.byref(S), 0), self._ctx)
+        return dict(x=x, mu=mu[..., :self.p], lam_prev=lp[..., :self.p], x_avg=xa, outer_done=j.value, S=S.value)
+
+    def set_state(self, state: dict):
+        """Continue the next solve from `state` (a get_state() dict): outer iterations
+        outer_done + 1, ...; solve(K1), get_state, set_state, solve(K2) == solve(K1 + K2)."""
+        arrs = [_Arr(np.ascontiguousarray(state[k], np.float64), np.float64) for k in ("x", "mu", "lam_prev", "x_avg")]
+        L.check(self._lib.duquad_set_state(self._ctx, arrs[0].ptr, arrs[1].ptr, arrs[2].ptr, arrs[3].ptr,
+                                           int(state["outer_done"]), float(state["S"]), 0), self._ctx)
 
     def residuals(self, which: str = "last"):
         F, d, lag = C.c_double(), C.c_double(), C.c_double()
