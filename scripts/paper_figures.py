@@ -83,8 +83,8 @@ def time_to_eps(prob, rho, lmin, ref, alg, eps_in, sigma_L):
 def fig3(quick):
     rho = 1.0 / EPS
     out = []
-    for n in ((20, 50) if quick else (20, 50, 100, 200, 500)):
-        for inst in range(2 if quick else 5):
+    for n in ((20, 50) if quick else (20, 50, 100)):
+        for inst in range(2 if quick else 3):
             prob = qpgen.tiny(n, n // 2, seed=1000 * n + inst, kind="eq", shift=0.0, psd_rank=max(1, n // 2))
             ref = reference(prob, rho, 1e-3)
             R_d = max(float(np.linalg.norm(ref["lam"])), 1e-3)
@@ -99,7 +99,7 @@ def fig3(quick):
 def fig4(quick):
     out = []
     for n in ((10, 50) if quick else (10, 50, 100, 200, 500)):
-        for inst in range(3 if quick else 10):
+        for inst in range(3 if quick else 5):
             prob = qpgen.dense_ineq(n, max(1, n // 2), seed=5000 * n + inst, shift=0.5)
             lmin = float(np.linalg.eigvalsh(prob.Q).min())
             ref = reference(prob, 0.0, lmin)
