@@ -106,7 +106,8 @@ __device__ __forceinline__ void csr_row_dot2(const int32_t *__restrict__ ci, con
 }
 
 template <int MODE, int GS>
-__global__ void __launch_bounds__(kCsrThreads) k_pass_a_csr(const PassAArgs a) {
+// (kCsrThreads, 4): <= 64 registers, 4 resident CTAs per SM (was 3 at 76): more rows in flight
+__global__ void __launch_bounds__(kCsrThreads, 4) k_pass_a_csr(const PassAArgs a) {
     if (a.skip && *a.skip) return;
     const int lane = threadIdx.x & 31, gl = lane & (GS - 1), gw = lane / GS;
     const int64_t gpw = 32 / GS;   // lane groups per warp; a warp covers 2 * gpw consecutive rows
@@ -144,17 +145,30 @@ __global__ void __launch_bounds__(kCsrThreads) k_pass_b_csr(const PassBArgs b) {
     const int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
     const double avg_w = avg_weight(b, MODE);
     // G' rows are short (config 4: Poisson(4) nonzeros): one row per lane group measured faster
-    for (int64_t base = warp_id * gpw; base < b.nrows; base += nwarps * gpw) {
+    const int64_t stride = nwarps * gpw;
+    int64_t base = warp_id * gpw;
+    int32_t lo = 0, hi = 0, lon = 0, hin = 0;
+    if (base + gw < b.nrows) {
+        lo = b.rp[base + gw];
+        hi = b.rp[base + gw + 1];
+    }
+    for (; base < b.nrows; base += stride) {
         const int64_t j = base + gw;
         const bool valid = j < b.nrows;
+        if (base + stride + gw < b.nrows) {   // next iteration's row pointers, one iteration ahead
+            lon = b.rp[base + stride + gw];
+            hin = b.rp[base + stride + gw + 1];
+        }
         EpiB e{};
         double t = 0.0;
         if (valid) {
             if (gl == 0) e = epi_b_load(b, MODE, j, avg_w);
-            t = csr_row_dot<GS>(b.ci, b.va, b.w, b.rp[j], b.rp[j + 1], gl);
+            t = csr_row_dot<GS>(b.ci, b.va, b.w, lo, hi, gl);
         }
         t = group_sum<GS>(t);
         if (valid && gl == 0) epi_b_store(b, MODE, j, t, e, avg_w);
+        lo = lon;
+        hi = hin;
     }
 }
 
