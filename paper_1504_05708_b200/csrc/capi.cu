@@ -65,6 +65,7 @@ struct duquad_ctx {
     bool rho0 = false;
     bool davg = false;
     bool eqh = false;
+    double *fpart = nullptr, *rs_out = nullptr;   // row-sharded byte floor: partial n-vector, its reduced slice
     // state export / resume (NEXT-2): the state after outer iteration j (before the last-iterate solve)
     double *ck_x = nullptr, *ck_mu = nullptr, *ck_lp = nullptr, *ck_xh = nullptr;
     bool ck_valid = false;     // a checkpoint from the last solve (options.checkpoint) or set_state
@@ -158,7 +159,7 @@ void free_all(duquad_ctx *c) {
     double *ds[] = {c->A,   c->GT,  c->y_full, c->w_full, c->qy,       c->x,        c->xhat,     c->q,
                     c->lb,  c->ub,  c->g,      c->mu,     c->lam_prev, c->lz_vprev, c->lz_w,     c->scal,
                     c->partials, c->Yb, c->Xb, c->XHb,   c->QYb,      c->qb,       c->Wb,       c->gb,
-                    c->mub, c->lpb, c->hb, c->d_beta, c->y_full2, c->cvec, c->ws, c->lam_hat, c->lhb, c->Hq, c->ck_x, c->ck_mu, c->ck_lp, c->ck_xh};
+                    c->mub, c->lpb, c->hb, c->d_beta, c->y_full2, c->cvec, c->ws, c->lam_hat, c->lhb, c->Hq, c->ck_x, c->ck_mu, c->ck_lp, c->ck_xh, c->fpart, c->rs_out};
     for (double *d : ds)
         if (d) cudaFree(d);
     if (c->cone) cudaFree(c->cone);
@@ -290,13 +291,18 @@ BatchedArgs make_batched(duquad_ctx *c, int pass);
 // followed by an optional all-gather of one replica buffer.  run_outer() interleaves them with
 // NCCL all-gathers; duquad_solve_emulated() runs the phases of P contexts in lock step and
 // replaces the all-gather by device copies.
-enum GatherBuf { G_NONE = -1, G_Y = 0, G_Y2 = 1, G_W = 2 };
+enum GatherBuf { G_NONE = -1, G_Y = 0, G_Y2 = 1, G_W = 2, G_RS = 3 };   // G_RS: reduce-scatter of fpart
 
 double *gather_ptr(duquad_ctx *c, int b) { return b == G_W ? c->w_full : (b == G_Y2 ? c->y_full2 : c->y_full); }
 int64_t gather_slice(duquad_ctx *c, int b) { return b == G_W ? c->p_slice : c->n_slice; }
 
 duquad_status gather(duquad_ctx *ctx, int b) {
     if (b < 0 || ctx->world == 1 || ctx->emulated) return DUQUAD_OK;   // emulated: group driver copies
+    if (b == G_RS) {
+        NK(ncclReduceScatter(ctx->fpart, ctx->rs_out, (size_t)ctx->n_slice, ncclDouble, ncclSum, ctx->comm,
+                             ctx->stream));
+        return DUQUAD_OK;
+    }
     double *full = gather_ptr(ctx, b);
     const int64_t sl = gather_slice(ctx, b);
     NK(ncclAllGather(full + ctx->rank * sl, full, (size_t)sl, ncclDouble, ctx->comm, ctx->stream));
@@ -413,12 +419,22 @@ duquad_status outer_phase(duquad_ctx *ctx, const std::vector<double> &beta_in, i
             CK(launch_fused_stream(fz, ctx->stream));
             if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 1], ctx->stream));
             if (k == 1 && (st = trace_lam_copy(ctx, j)) != DUQUAD_OK) return st;
+            if (ctx->world > 1) {   // this rank's partial n-vector, then the reduce-scatter over the slices
+                fz.partial = ctx->fpart;
+                CK(launch_fused_epi(make_b(ctx), make_b(ctx), fz, ctx->stream));
+                *gb = G_RS;
+            }
         } else {
             PassBArgs b = make_b(ctx);
             b.beta_in = beta_in[k];
             b.last_inner = (k == Kin) && !ctx->eps_mode;
             if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 2], ctx->stream));
-            CK(launch_fused_epi(b, b, ctx->fz, ctx->stream));
+            if (ctx->world > 1) {
+                CK(launch_slice_epi(b, b, ctx->rs_out, ctx->stream));
+                *gb = G_Y;
+            } else {
+                CK(launch_fused_epi(b, b, ctx->fz, ctx->stream));
+            }
             if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 3], ctx->stream));
             if ((st = inner_check(ctx)) != DUQUAD_OK) return st;
         }
@@ -1085,8 +1101,11 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
             ctx->eqh = true;
         }
     }
-    if (!batched && ctx->world == 1 && opt.fused_path &&
-        fused_supported(n, ctx->ld, prop.sharedMemPerBlockOptin)) {   // byte-floor inner step
+    // byte-floor inner step: single GPU, or row-sharded with rho > 0 (each rank streams the upper
+    // triangle of its rows and its G rows; the ranks' partial n-vectors are reduce-scattered)
+    const bool shard_floor = ctx->world > 1 && !csr && rho > 0.0 && !ctx->rho0;
+    if (!batched && (ctx->world == 1 || shard_floor) && opt.fused_path &&
+        fused_supported(n, ctx->ld, prop.sharedMemPerBlockOptin)) {
         const int cg = (!ctx->rho0 && p > 0) ? 2 : 1;   // G role: CTA pairs (148 SMs usable)
         const int nchg = cg > 1 ? fused_nchg(ctx->ld, cg) : 0;
         CKS(configure_fused_kernels(nchg, fused_smem_bytes()));
@@ -1097,7 +1116,9 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
             // Q : G split by bytes, G weighted by its measured per-byte cost (config 2: nq = 66 of 148)
             double gw = 1.24;
             if (const char *ov = std::getenv("DUQUAD_FUSED_GW")) gw = std::atof(ov);
-            const double bq = 0.5 * (double)n * (double)(n + 1), bg = gw * (double)p * (double)n;
+            const double qa = (double)ctx->r0, qb = (double)(ctx->r0 + ctx->nloc);   // this rank's Q rows
+            const double bq = (qb - qa) * (double)n - 0.5 * (qb * qb - qa * qa) + 0.5 * (qb - qa),
+                         bg = gw * (double)ctx->ploc * (double)n;
             nq = cg * (int)std::llround((double)nb / cg * bq / (bq + bg));
             nq = std::max(cg, std::min(nb - cg, nq));
         }
@@ -1120,14 +1141,22 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         fz.ng = (nb - nq) / fz.cg;
         fz.smem = fused_smem_bytes();
         std::vector<FusedPiece> pcs;
-        fz.cslots = fused_partition(n, ctx->ld, nq, row_cost, pcs, fz.qlo, fz.qhi);
+        fz.qa = ctx->r0;
+        fz.qb = ctx->r0 + ctx->nloc;
+        fz.partial = nullptr;
+        fz.cslots = fused_partition(n, ctx->ld, nq, row_cost, pcs, fz.qlo, fz.qhi, fz.qa, fz.qb);
         const int64_t wrow = (int64_t)fz.nt * 16 * ctx->ld, wcol = (int64_t)nq * fz.cslots * 4096,
                       wg = (int64_t)fz.ng * ctx->ld;
         CKS(dalloc(&ctx->ws, wrow + wcol + wg));
         CKS(dalloc(&ctx->fpieces, (int64_t)nq));
         CKS(cudaMemcpy(ctx->fpieces, pcs.data(), nq * sizeof(FusedPiece), cudaMemcpyHostToDevice));
         fz.Q = ctx->eqh ? ctx->Hq : ctx->A;
-        fz.G = ctx->A + n * ctx->ld;
+        fz.G = ctx->A + ctx->nloc * ctx->ld;
+        fz.p = ctx->ploc;
+        if (ctx->world > 1) {
+            CKS(dalloc(&ctx->fpart, ctx->world * ctx->n_slice));
+            CKS(dalloc(&ctx->rs_out, ctx->n_slice));
+        }
         fz.y = ctx->y_full;
         fz.ws_rowp = ctx->ws;
         fz.ws_col = ctx->ws + wrow;
@@ -1759,10 +1788,12 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
         const double nn = (double)ctx->n, nl = (double)ctx->nloc, pl = (double)ctx->ploc, pp = (double)ctx->p;
         if (ctx->fused) {      // byte floor: Q triangle (+ G once) streamed, workspace through L2
             // algorithmic bytes: Q triangle + G once + y; the epilogue: 7 vectors + the partials
-            const double tri = 0.5 * nn * (nn + 1.0);
+            // (row-sharded: this rank's rows [qa, qb) of the triangle and its G rows)
+            const double qa = (double)ctx->fz.qa, qb = (double)ctx->fz.qb;
+            const double tri = (qb - qa) * nn - 0.5 * (qb * qb - qa * qa) + 0.5 * (qb - qa);
             const double wsb = 16.0 * ctx->fz.nt * (double)ctx->ld +
                                (double)ctx->fz.nq_ctas * ctx->fz.cslots * 4096.0 + (double)ctx->fz.ng * (double)ctx->ld;
-            res->bytes_pass_a = 8.0 * (tri + (ctx->rho0 ? 0.0 : pp * nn) + nn);
+            res->bytes_pass_a = 8.0 * (tri + (ctx->rho0 ? 0.0 : pl * nn) + nn);
             res->bytes_pass_b = 8.0 * (wsb + 8.0 * nn);
             if (ctx->rho0) {
                 res->kernel_launches = 1 + (int64_t)nout * (2 * Kin + 3);
@@ -1818,6 +1849,15 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
 static duquad_status group_gather(duquad_ctx **c, int P, int b) {
     if (b < 0 || P == 1) return DUQUAD_OK;
     duquad_ctx *ctx = c[0];
+    if (b == G_RS) {   // reduce-scatter: slice r = sum over ranks q (in order) of fpart_q[slice r]
+        const int64_t sl = ctx->n_slice;
+        for (int r = 0; r < P; ++r) {
+            CK(cudaMemcpyAsync(c[r]->rs_out, c[0]->fpart + r * sl, sl * sizeof(double), cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+            for (int q = 1; q < P; ++q) CK(launch_vec_add(c[r]->rs_out, c[q]->fpart + r * sl, sl, ctx->stream));
+        }
+        return DUQUAD_OK;
+    }
     const int64_t sl = gather_slice(ctx, b);
     for (int d = 0; d < P; ++d)
         for (int s = 0; s < P; ++s)

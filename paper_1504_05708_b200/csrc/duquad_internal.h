@@ -147,6 +147,8 @@ struct FusedArgs {
     int32_t nq_ctas;       // Q-role CTAs (a multiple of cg); the rest are ng G-role clusters
     int32_t ng;
     int32_t qlo[kFusedMaxTiles], qhi[kFusedMaxTiles];   // Q CTAs with rows in tile column J
+    int64_t qa, qb;        // this rank's Q rows [qa, qb) (global; Q row 0 is row qa); single GPU: [0, n)
+    double *partial;       // row-sharded epilogue mode: write the rank's partial n-vector here, no epilogue
     size_t smem;
     PassAArgs a;           // G-row epilogue (g, mu, lam_prev, cone, rho, step, ops, first_inner)
 };
@@ -181,8 +183,10 @@ int fused_nchg(int64_t ld, int cg);
 int fused_max_clusters(int nchg, int cg, size_t smem);
 int fused_tiles(int64_t ld);
 size_t fused_smem_bytes();
+cudaError_t launch_slice_epi(const PassBArgs &bl, const PassBArgs &bs, const double *sum, cudaStream_t s);
+cudaError_t launch_vec_add(double *dst, const double *src, int64_t n, cudaStream_t s);
 int fused_partition(int64_t n, int64_t ld, int nq, double row_cost, std::vector<FusedPiece> &pieces,
-                     int32_t *qlo, int32_t *qhi);
+                    int32_t *qlo, int32_t *qhi, int64_t qa, int64_t qb);
 cudaError_t configure_fused_kernels(int nchg, size_t smem);
 cudaError_t launch_fused_stream(const FusedArgs &f, cudaStream_t s);
 cudaError_t launch_fused_epi(const PassBArgs &bl, const PassBArgs &bs, const FusedArgs &f, cudaStream_t s);

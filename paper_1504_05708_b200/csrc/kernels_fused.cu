@@ -148,6 +148,7 @@ __device__ __forceinline__ Tile tile_of(const FusedArgs &f, int J) {
     t.a = J * kChunk;
     t.b = t.a + kChunk < (int)f.ld ? t.a + kChunk : (int)f.ld;
     t.rows = t.b < (int)f.n ? t.b : (int)f.n;
+    if (t.rows > (int)f.qb) t.rows = (int)f.qb;   // row-sharded: this rank's rows end at qb
     return t;
 }
 
@@ -181,7 +182,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
         int nsteps = 0;   // row steps of this piece
         for (int J = pc.j0; J <= pc.j1 && J < f.nt; ++J) {
             const Tile tj = tile_of(f, J);
-            const int rb = J == pc.j0 ? pc.r0 : 0, re = J == pc.j1 ? pc.r1 : tj.rows;
+            const int rb = J == pc.j0 ? pc.r0 : (int)f.qa, re = J == pc.j1 ? pc.r1 : tj.rows;
             nsteps += re > rb ? re - rb : 0;
         }
         const int c2t = 2 * tid;
@@ -189,7 +190,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
         int p_left = nsteps, pJ = pc.j0, pr = pc.r0, ps = 0;
         Tile pt = tile_of(f, pJ);
         bool p_rag = pt.b - pt.a < kChunk;
-        const double *prow = f.Q + (int64_t)pr * f.ld + pt.a + c2t;
+        const double *prow = f.Q + (int64_t)(pr - f.qa) * f.ld + pt.a + c2t;   // f.Q row 0 = global row qa
         auto issue = [&]() {
             if (p_left > 0) {
                 if (pr < pt.a && !p_rag) {   // off-diagonal full row step
@@ -207,7 +208,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
                 prow += f.ld;
                 if (++pr == pt.rows) {
                     ++pJ;
-                    pr = 0;
+                    pr = (int)f.qa;
                     pt = tile_of(f, pJ < f.nt ? pJ : 0);
                     p_rag = pt.b - pt.a < kChunk;
                     prow = f.Q + pt.a + c2t;
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
         };
         for (int J = pc.j0; J <= pc.j1 && J < f.nt; ++J) {
             const Tile t = tile_of(f, J);
-            const int rb = J == pc.j0 ? pc.r0 : 0, re = J == pc.j1 ? pc.r1 : t.rows;
+            const int rb = J == pc.j0 ? pc.r0 : (int)f.qa, re = J == pc.j1 ? pc.r1 : t.rows;
             if (re <= rb) continue;
             const bool rag = t.b - t.a < kChunk;
             const int cb = t.a + c2t;   // column of element e: cb + (e >> 1) * 1024 + (e & 1)
@@ -497,12 +498,14 @@ __global__ void __launch_bounds__(kEpiCols *kEpiSlices) k_fused_epi(const PassBA
     const int cl = threadIdx.x % kEpiCols, sl = threadIdx.x / kEpiCols;
     const int64_t j = (int64_t)blockIdx.x * kEpiCols + cl;
     const double avg_w = avg_weight(bl, MODE_SOLVE);
+    const bool partial = f.partial != nullptr;   // row-sharded: the rank's partial n-vector, no epilogue
+    const int64_t nr = partial ? f.n : bl.nrows;
     EpiB e{};
-    if (sl == 0 && j < bl.nrows) e = epi_b_load(bl, MODE_SOLVE, j, avg_w);   // overlaps the partial loads
+    if (!partial && sl == 0 && j < nr) e = epi_b_load(bl, MODE_SOLVE, j, avg_w);   // overlaps the partial loads
     double s = 0.0;
-    if (j < bl.nrows) {
+    if (j < nr) {
         const int Jc = (int)(j / kChunk);
-        const int nrow = (f.nt - Jc) * kWarps;
+        const int nrow = (j >= f.qa && j < f.qb) ? (f.nt - Jc) * kWarps : 0;   // row dots: this rank's rows
         const int lo = f.qlo[Jc], nqc = f.qhi[Jc] - f.qlo[Jc];
         const int64_t jr = j - (int64_t)Jc * kChunk;
         const int len = nrow + nqc + f.ng;
@@ -521,13 +524,34 @@ __global__ void __launch_bounds__(kEpiCols *kEpiSlices) k_fused_epi(const PassBA
     }
     part[sl][cl] = s;
     __syncthreads();
-    if (sl == 0 && j < bl.nrows) {
+    if (sl == 0 && j < nr) {
         double t = part[0][cl];
 #pragma unroll
         for (int q = 1; q < kEpiSlices; ++q) t += part[q][cl];
+        if (partial) {
+            f.partial[j] = t;
+            return;
+        }
         e.qy = t;
         epi_b_store(bs, MODE_SOLVE, j, 0.0, e, avg_w);
     }
+}
+
+// Row-sharded byte floor, after the reduce-scatter of the ranks' partial vectors: grad_j = sum_j + q_j
+// and the pass-B epilogue on this rank's rows (the arithmetic of k_fused_epi's last step).
+__global__ void k_slice_epi(const PassBArgs bl, const PassBArgs bs, const double *sum) {
+    if (bl.skip && *bl.skip) return;
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= bl.nrows) return;
+    const double avg_w = avg_weight(bl, MODE_SOLVE);
+    EpiB e = epi_b_load(bl, MODE_SOLVE, j, avg_w);
+    e.qy = sum[j];
+    epi_b_store(bs, MODE_SOLVE, j, 0.0, e, avg_w);
+}
+
+__global__ void k_vec_add(double *dst, const double *src, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] += src[i];
 }
 
 template <int NCHG>
@@ -602,9 +626,12 @@ int fused_max_clusters(int nchg, int cg, size_t smem) {
 // max(bytes, row_cost) (the per-step instruction cost dominates short steps near the diagonal).
 // qlo / qhi: the pieces with rows in each tile column; returns the most tile columns a piece spans.
 int fused_partition(int64_t n, int64_t ld, int nq, double row_cost, std::vector<FusedPiece> &pieces,
-                    int32_t *qlo, int32_t *qhi) {
+                    int32_t *qlo, int32_t *qhi, int64_t qa, int64_t qb) {
     const int nt = fused_tiles(ld);
-    auto rows = [&](int J) -> int64_t { return std::min<int64_t>(std::min<int64_t>((int64_t)(J + 1) * kChunk, ld), n); };
+    // rows of tile column J in this rank's row range [qa, qb) (single GPU: [0, n)): [qa, rows(J))
+    auto rows = [&](int J) -> int64_t {
+        return std::min<int64_t>(std::min<int64_t>(std::min<int64_t>((int64_t)(J + 1) * kChunk, ld), n), qb);
+    };
     auto cost = [&](int J, int64_t r) -> double {
         const int64_t a = (int64_t)J * kChunk, b = std::min<int64_t>(a + kChunk, ld);
         const int64_t st = r > a ? (r & ~1LL) : a;
@@ -612,15 +639,15 @@ int fused_partition(int64_t n, int64_t ld, int nq, double row_cost, std::vector<
     };
     double total = 0.0;
     for (int J = 0; J < nt; ++J)
-        for (int64_t r = 0; r < rows(J); ++r) total += cost(J, r);
+        for (int64_t r = qa; r < rows(J); ++r) total += cost(J, r);
     pieces.assign(nq, FusedPiece{0, 0, 0, 0});
     int J = 0;
-    int64_t r = 0;
+    int64_t r = qa;
     double acc = 0.0;
     auto norm = [&]() {   // (J, r) past the end of tile column J -> next
         while (J < nt && r >= rows(J)) {
             ++J;
-            r = 0;
+            r = qa;
         }
     };
     for (int c = 0; c < nq; ++c) {
@@ -650,7 +677,7 @@ int fused_partition(int64_t n, int64_t ld, int nq, double row_cost, std::vector<
     for (int c = 0; c < nq; ++c) {
         const FusedPiece &p = pieces[c];
         for (int b = p.j0; b <= p.j1 && b < nt; ++b) {
-            const int64_t r0 = b == p.j0 ? p.r0 : 0;
+            const int64_t r0 = b == p.j0 ? p.r0 : qa;
             const int64_t r1 = b == p.j1 ? p.r1 : rows(b);
             if (r1 > r0) {
                 qlo[b] = std::min(qlo[b], c);
@@ -684,8 +711,18 @@ cudaError_t launch_fused_stream(const FusedArgs &f, cudaStream_t s) {
     }
 }
 
+cudaError_t launch_slice_epi(const PassBArgs &bl, const PassBArgs &bs, const double *sum, cudaStream_t s) {
+    if (bl.nrows > 0) k_slice_epi<<<(unsigned)((bl.nrows + 255) / 256), 256, 0, s>>>(bl, bs, sum);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vec_add(double *dst, const double *src, int64_t n, cudaStream_t s) {
+    if (n > 0) k_vec_add<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dst, src, n);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_fused_epi(const PassBArgs &bl, const PassBArgs &bs, const FusedArgs &f, cudaStream_t s) {
-    const int grid = (int)((bl.nrows + kEpiCols - 1) / kEpiCols);
+    const int grid = (int)(((f.partial ? f.n : bl.nrows) + kEpiCols - 1) / kEpiCols);
     if (grid > 0) k_fused_epi<<<grid, kEpiCols * kEpiSlices, 0, s>>>(bl, bs, f);
     return cudaGetLastError();
 }

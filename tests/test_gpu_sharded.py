@@ -115,7 +115,29 @@ def test_config2_full_size_8_way_sharding(torch_cuda):
     d = qpgen.dense_ineq_torch(16384, 8192, seed=0, shift=0.05)
     args = [d[k] for k in ("Q", "q", "G", "g", "lb", "ub", "cone")]
     L_in, L_d = 47588.0, 1.0 / (1.0 + 0.05 / 47539.5)
-    a = _run_sharded(torch_cuda, args, 8, 1.0, "DFGM", 2, 3, L_in, L_d)
+    a = _run_sharded(torch_cuda, args, 8, 1.0, "DFGM", 2, 3, L_in, L_d, fused_path=False)
     b = _run_single(torch_cuda, args, 1.0, "DFGM", 2, 3, L_in, L_d)
     for k in ("x_last", "x_avg", "lam"):
         assert np.array_equal(a[k], b[k]), k
+    # the row-sharded byte-floor step (default at this size) agrees with the two-pass solve
+    c = _run_sharded(torch_cuda, args, 8, 1.0, "DFGM", 2, 3, L_in, L_d)
+    for k in ("x_last", "x_avg", "lam"):
+        assert relerr(c[k], b[k]) <= 1e-10, (k, relerr(c[k], b[k]))
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+@pytest.mark.parametrize("alg", ["DFGM", "DGM"])
+def test_sharded_byte_floor_vs_oracle(torch_cuda, P, alg):
+    """Row-sharded byte floor (n >= 4096, rho > 0): each rank streams the upper triangle of its Q
+    rows and its G rows; the partial n-vectors are reduce-scattered (emulated: summed in rank order)
+    -- against the oracle, and deterministic."""
+    prob = qpgen.dense_ineq(4096, 2048, seed=1, shift=0.05)
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 1.0, 0.05)
+    a = _run_sharded(torch_cuda, _dense_args(prob), P, 1.0, alg, 2, 4, L_in, L_d, trace=True)
+    a2 = _run_sharded(torch_cuda, _dense_args(prob), P, 1.0, alg, 2, 4, L_in, L_d)
+    r = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 1.0, alg, 2, 4, L_in, L_d,
+               keep_trace=True)
+    for k, want in (("x_last", r.x_last), ("x_avg", r.x_avg), ("lam", r.lam)):
+        assert relerr(a[k], want) <= 1e-9, (k, relerr(a[k], want))
+        assert np.array_equal(a[k], a2[k])
+    assert relerr(a["trace_u"], np.array(r.trace_u)) <= 1e-9
