@@ -337,6 +337,15 @@ duquad_status duquad_get_state(duquad_ctx *ctx, double *x, double *mu, double *l
 duquad_status duquad_set_state(duquad_ctx *ctx, const double *x, const double *mu, const double *lam_prev,
                                const double *x_avg, int64_t outer_done, double S, int32_t on_device);
 
+/*
+ * This context's rows: Q rows [r0, r0 + nloc) and constraint rows [s0, s0 + ploc) of the global
+ * problem (the slices duquad_get_result returns for a row-sharded context; a batched context
+ * reports the whole QP).  The constraint rows are equal slices except on the row-sharded
+ * byte-floor path (dense, rho > 0, n >= 4096), where they are balanced against the ranks' Q
+ * triangle slabs.  Any output pointer may be NULL.
+ */
+duquad_status duquad_local_ranges(const duquad_ctx *ctx, int64_t *r0, int64_t *nloc, int64_t *s0, int64_t *ploc);
+
 /* Convergence-bound diagnostics of DuQuad (host-only arithmetic, no GPU), for k outer iterations. */
 typedef struct {
     double dual_gap;    /* Theorem 1 (bound_gen_dfg): F* - d(lambda^k) <=

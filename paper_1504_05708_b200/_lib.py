@@ -114,6 +114,8 @@ _SIGS = {
                                    C.POINTER(C.c_int64), C.POINTER(C.c_double), C.c_int32]),
     "duquad_set_state": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                    C.c_double, C.c_int32]),
+    "duquad_local_ranges": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                      C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "duquad_destroy": (None, [C.c_void_p]),
     "duquad_last_error": (C.c_char_p, [C.c_void_p]),
 }

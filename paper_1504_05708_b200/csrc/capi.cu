@@ -42,6 +42,8 @@ struct duquad_ctx {
     bool emulated = false;   // P ranks on one device, driven by duquad_solve_emulated
     ncclComm_t comm = nullptr;
     int64_t n_slice = 0, p_slice = 0, r0 = 0, s0 = 0, nloc = 0, ploc = 0;
+    std::vector<int64_t> gs0, gcnt;   // G rows [gs0[r], gs0[r] + gcnt[r]) of every rank (contiguous, ascending)
+    bool floor_shard = false;         // row-sharded byte floor (G rows balanced against the Q triangle slabs)
     // layout
     int64_t ld = 0, ldp = 0, ylen = 0, wlen = 0;
     // device buffers (dense)
@@ -211,10 +213,21 @@ duquad_status allgather_vec(duquad_ctx *ctx, double *full) {
 
 duquad_status allgather_y(duquad_ctx *ctx) { return allgather_vec(ctx, ctx->y_full); }
 
+// w replica: every rank's G-row slice in global order.  Equal slices: one all-gather; the balanced
+// partition of the row-sharded byte floor: one broadcast per rank inside a group.
 duquad_status allgather_w(duquad_ctx *ctx) {
     if (ctx->world == 1 || ctx->emulated) return DUQUAD_OK;
-    NK(ncclAllGather(ctx->w_full + ctx->rank * ctx->p_slice, ctx->w_full, (size_t)ctx->p_slice,
-                     ncclDouble, ctx->comm, ctx->stream));
+    if (!ctx->floor_shard) {
+        NK(ncclAllGather(ctx->w_full + ctx->rank * ctx->p_slice, ctx->w_full, (size_t)ctx->p_slice,
+                         ncclDouble, ctx->comm, ctx->stream));
+        return DUQUAD_OK;
+    }
+    NK(ncclGroupStart());
+    for (int r = 0; r < ctx->world; ++r)
+        if (ctx->gcnt[r] > 0)
+            NK(ncclBroadcast(ctx->w_full + ctx->gs0[r], ctx->w_full + ctx->gs0[r], (size_t)ctx->gcnt[r], ncclDouble,
+                             r, ctx->comm, ctx->stream));
+    NK(ncclGroupEnd());
     return DUQUAD_OK;
 }
 
@@ -235,7 +248,7 @@ PassAArgs make_a(duquad_ctx *c) {
     a.row_end = c->nloc + c->ploc;
     a.y = c->y_full;
     a.qy = c->qy;
-    a.w = c->w_full + c->rank * c->p_slice;
+    a.w = c->w_full + c->s0;
     a.g = c->g;
     a.mu = c->mu;
     a.lam_prev = c->lam_prev;
@@ -298,6 +311,7 @@ int64_t gather_slice(duquad_ctx *c, int b) { return b == G_W ? c->p_slice : c->n
 
 duquad_status gather(duquad_ctx *ctx, int b) {
     if (b < 0 || ctx->world == 1 || ctx->emulated) return DUQUAD_OK;   // emulated: group driver copies
+    if (b == G_W) return allgather_w(ctx);
     if (b == G_RS) {
         NK(ncclReduceScatter(ctx->fpart, ctx->rs_out, (size_t)ctx->n_slice, ncclDouble, ncclSum, ctx->comm,
                              ctx->stream));
@@ -897,8 +911,44 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
     ctx->p_slice = (p + ctx->world - 1) / ctx->world;
     ctx->r0 = std::min<int64_t>(n, ctx->rank * ctx->n_slice);
     ctx->nloc = std::min<int64_t>(n, ctx->r0 + ctx->n_slice) - ctx->r0;
-    ctx->s0 = std::min<int64_t>(p, ctx->rank * ctx->p_slice);
-    ctx->ploc = std::min<int64_t>(p, ctx->s0 + ctx->p_slice) - ctx->s0;
+    // G rows: equal slices, except for the row-sharded byte floor, where rank r's triangle slab of Q
+    // (rows r0..r0+nloc, columns >= row) shrinks with r: there the G rows are split so that every
+    // rank streams the same number of matrix elements (slab + G rows x n), contiguous and ascending
+    ctx->floor_shard = ctx->world > 1 && !csr && !batched && rho > 0.0 && p > 0 && opt.fused_path &&
+                       fused_supported(n, round_up(n, 32), prop.sharedMemPerBlockOptin);
+    ctx->gs0.assign(ctx->world, 0);
+    ctx->gcnt.assign(ctx->world, 0);
+    if (ctx->floor_shard) {
+        std::vector<double> want(ctx->world);
+        double tot = (double)p * (double)n;
+        std::vector<double> slab(ctx->world);
+        for (int r = 0; r < ctx->world; ++r) {
+            const double qa = (double)std::min<int64_t>(n, r * ctx->n_slice);
+            const double qb = (double)std::min<int64_t>(n, (r + 1) * ctx->n_slice);
+            slab[r] = (qb - qa) * (double)n - 0.5 * (qb * qb - qa * qa) + 0.5 * (qb - qa);
+            tot += slab[r];
+        }
+        double sw = 0.0;
+        for (int r = 0; r < ctx->world; ++r) sw += (want[r] = std::max(0.0, (tot / ctx->world - slab[r]) / n));
+        int64_t given = 0;
+        std::vector<std::pair<double, int>> frac;
+        for (int r = 0; r < ctx->world; ++r) {
+            const double x = sw > 0.0 ? want[r] * (double)p / sw : (double)p / ctx->world;
+            ctx->gcnt[r] = (int64_t)std::floor(x);
+            given += ctx->gcnt[r];
+            frac.push_back({-(x - std::floor(x)), r});
+        }
+        std::sort(frac.begin(), frac.end());
+        for (int64_t i = 0; given < p; ++i, ++given) ++ctx->gcnt[frac[(size_t)(i % ctx->world)].second];
+        for (int r = 1; r < ctx->world; ++r) ctx->gs0[r] = ctx->gs0[r - 1] + ctx->gcnt[r - 1];
+    } else {
+        for (int r = 0; r < ctx->world; ++r) {
+            ctx->gs0[r] = std::min<int64_t>(p, r * ctx->p_slice);
+            ctx->gcnt[r] = std::min<int64_t>(p, ctx->gs0[r] + ctx->p_slice) - ctx->gs0[r];
+        }
+    }
+    ctx->s0 = ctx->gs0[ctx->rank];
+    ctx->ploc = ctx->gcnt[ctx->rank];
     ctx->emulated = ctx->world > 1 && opt.emulate_ranks;
     if (ctx->world > 1 && !ctx->emulated) {
         ncclUniqueId id;
@@ -1363,7 +1413,7 @@ duquad_status duquad_set_initial(duquad_ctx *ctx, const double *x0, const double
     // the caller's full vectors: x0 is (batch x) n, lambda0 (batch x) p, row per QP; this context
     // takes its QPs (batched) or its row slices (row-sharded)
     const int64_t xoff = bt ? ctx->b0 * ctx->n : ctx->rank * ctx->n_slice;
-    const int64_t loff = bt ? ctx->b0 * ctx->p : ctx->rank * ctx->p_slice;
+    const int64_t loff = bt ? ctx->b0 * ctx->p : ctx->s0;
     const int64_t nx = bt ? ctx->n : ctx->nloc, nl = bt ? ctx->p : ctx->ploc;
     const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     if (x0) {
@@ -1483,6 +1533,15 @@ duquad_status duquad_theory_schedule(int32_t alg, double eps, double R_d, double
                                              std::log(8.0 * normG * D_U * R_d / eps))
                        : (int64_t)std::floor(24.0 * normG * D_U * R_d / eps);
     out->case_id = lambda_min_Q > 0.0 ? 1 : 2;
+    return DUQUAD_OK;
+}
+
+duquad_status duquad_local_ranges(const duquad_ctx *ctx, int64_t *r0, int64_t *nloc, int64_t *s0, int64_t *ploc) {
+    if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
+    if (r0) *r0 = ctx->Btot > 1 ? 0 : ctx->r0;
+    if (nloc) *nloc = ctx->Btot > 1 ? ctx->n : ctx->nloc;
+    if (s0) *s0 = ctx->Btot > 1 ? 0 : ctx->s0;
+    if (ploc) *ploc = ctx->Btot > 1 ? ctx->p : ctx->ploc;
     return DUQUAD_OK;
 }
 
@@ -1860,10 +1919,12 @@ static duquad_status group_gather(duquad_ctx **c, int P, int b) {
     }
     const int64_t sl = gather_slice(ctx, b);
     for (int d = 0; d < P; ++d)
-        for (int s = 0; s < P; ++s)
-            if (s != d && sl > 0)
-                CK(cudaMemcpyAsync(gather_ptr(c[d], b) + s * sl, gather_ptr(c[s], b) + s * sl, sl * sizeof(double),
+        for (int s = 0; s < P; ++s) {
+            const int64_t off = b == G_W ? ctx->gs0[s] : s * sl, cnt = b == G_W ? ctx->gcnt[s] : sl;
+            if (s != d && cnt > 0)
+                CK(cudaMemcpyAsync(gather_ptr(c[d], b) + off, gather_ptr(c[s], b) + off, cnt * sizeof(double),
                                    cudaMemcpyDeviceToDevice, ctx->stream));
+        }
     return DUQUAD_OK;
 }
 
@@ -1956,7 +2017,7 @@ duquad_status duquad_residuals(duquad_ctx *ctx, int32_t which, double *F, double
     PassAArgs a = make_a(ctx);
     a.lin_coef = 1.0;
     CK(launch_pass_a(a, MODE_LIN, ctx->cfg_a, s));          // qy = Q x, w_local = G x
-    CK(launch_residual_partial(xv, ctx->qy, ctx->q, ctx->nloc, ctx->w_full + ctx->rank * ctx->p_slice, ctx->g,
+    CK(launch_residual_partial(xv, ctx->qy, ctx->q, ctx->nloc, ctx->w_full + ctx->s0, ctx->g,
                                ctx->lam_prev, ctx->cone, ctx->ploc, ctx->rho, ctx->partials, s));
     double *acc = ctx->scal + SC_TMP;
     CK(launch_reduce_final(ctx->partials, kRedGrid, 5, acc, s));

@@ -195,8 +195,10 @@ class Solver:
             self.n_range, self.p_range = (0, n), (0, p)
         else:
             self.b_range = (0, 1)
-            self.n_range = shard_range(n, self.world_size, self.rank)
-            self.p_range = shard_range(p, self.world_size, self.rank)
+            r0, nl, s0, pl = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()   # the context's row ranges
+            L.check(lib.duquad_local_ranges(ctx, C.byref(r0), C.byref(nl), C.byref(s0), C.byref(pl)), ctx)
+            self.n_range = (r0.value, r0.value + nl.value)
+            self.p_range = (s0.value, s0.value + pl.value)
         self.device = o["device"]
         self.last_result = None
 
