@@ -141,3 +141,32 @@ def test_sharded_byte_floor_vs_oracle(torch_cuda, P, alg):
         assert relerr(a[k], want) <= 1e-9, (k, relerr(a[k], want))
         assert np.array_equal(a[k], a2[k])
     assert relerr(a["trace_u"], np.array(r.trace_u)) <= 1e-9
+
+
+def test_sharded_byte_floor_ragged_warm_start_and_dual_average(torch_cuda):
+    """Row-sharded byte floor on a ragged split (n = 4100 over 3 ranks, p = 1500 balanced against the
+    slabs), warm-started, with the DGM dual-averaging final point -- against the oracle."""
+    from paper_1504_05708_b200 import Solver, solve_emulated
+    import torch
+    prob = qpgen.dense_ineq(4100, 1500, seed=9, shift=0.05)
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 2.0, 0.05)
+    rng = np.random.default_rng(1)
+    x0, lam0 = rng.uniform(-2, 2, 4100), np.abs(rng.standard_normal(1500))
+    st = torch.cuda.Stream()
+    ss = [Solver(*_dense_args(prob), rho=2.0, world_size=3, rank=r, emulate_ranks=True, stream=st.cuda_stream,
+                 dual_average=True) for r in range(3)]
+    prs = [s.p_range for s in ss]
+    assert prs[0][0] == 0 and prs[-1][1] == 1500 and all(a[1] == b[0] for a, b in zip(prs, prs[1:]))
+    assert prs[0][1] - prs[0][0] < prs[-1][1] - prs[-1][0]          # the first slab is the largest
+    for s in ss:
+        s.set_constants(L_in, L_d)
+        s.set_initial(x0, lam0)
+    solve_emulated(ss, "DGM", 3, 4)
+    parts = [s.result() for s in ss]
+    for s in ss:
+        s.close()
+    got = [np.concatenate([pt[i] for pt in parts]) for i in range(3)]
+    r = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 2.0, "DGM", 3, 4, L_in, L_d,
+               x0=x0, lam0=lam0, dual_average=True)
+    for g, w in zip(got, (r.x_last, r.x_avg, r.lam)):
+        assert relerr(g, w) <= 1e-9, relerr(g, w)
