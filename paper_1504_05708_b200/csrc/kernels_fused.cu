@@ -509,18 +509,25 @@ __global__ void __launch_bounds__(kEpiCols *kEpiSlices) k_fused_epi(const PassBA
         const int lo = f.qlo[Jc], nqc = f.qhi[Jc] - f.qlo[Jc];
         const int64_t jr = j - (int64_t)Jc * kChunk;
         const int len = nrow + nqc + f.ng;
-        for (int t = sl; t < len; t += kEpiSlices) {
-            const double *src;
-            if (t < nrow) {
-                src = f.ws_rowp + ((int64_t)Jc * kWarps + t) * f.ld + j;
-            } else if (t < nrow + nqc) {
+        auto at = [&](int t) -> const double * {
+            if (t < nrow) return f.ws_rowp + ((int64_t)Jc * kWarps + t) * f.ld + j;
+            if (t < nrow + nqc) {
                 const int c = lo + (t - nrow);
-                src = f.ws_col + ((int64_t)c * f.cslots + (Jc - f.pieces[c].j0)) * kChunk + jr;
-            } else {
-                src = f.ws_g + (int64_t)(t - nrow - nqc) * f.ld + j;
+                return f.ws_col + ((int64_t)c * f.cslots + (Jc - f.pieces[c].j0)) * kChunk + jr;
             }
-            s += *src;
+            return f.ws_g + (int64_t)(t - nrow - nqc) * f.ld + j;
+        };
+        // eight list entries in flight per thread, added in list order (the same sum, bit for bit)
+        constexpr int U = 8;
+        int t = sl;
+        for (; t + (U - 1) * kEpiSlices < len; t += U * kEpiSlices) {
+            double v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = __ldcg(at(t + u * kEpiSlices));
+#pragma unroll
+            for (int u = 0; u < U; ++u) s += v[u];
         }
+        for (; t < len; t += kEpiSlices) s += __ldcg(at(t));
     }
     part[sl][cl] = s;
     __syncthreads();
