@@ -279,7 +279,8 @@ duquad_status duquad_set_initial(duquad_ctx *ctx, const double *x0, const double
  * (the inexactness (duquad_in) of Theorem 1).  sigma_L > 0 is the caller's lower bound on
  * lambda_min(Q + rho G'G) (e.g. lambda_min(Q)), eps_in > 0 (e.g. from duquad_theory_schedule).
  * The norm is a fixed-order device reduction after each step; converged inner solves skip the
- * remaining steps of their (graph-captured) loop.  Single GPU, batch 1, any format.
+ * remaining steps of their (graph-captured) loop.  Batch 1, any format; row-sharded groups
+ * all-reduce the test's sum (one double per inner step), so every rank decides alike.
  * Returns DUQUAD_EMAXITER (result valid) when some inner solve was capped; per-outer step
  * counts via duquad_get_inner_counts.  res->inner_iters_total = steps actually run.
  */
@@ -405,6 +406,14 @@ duquad_status duquad_residuals(duquad_ctx *ctx, int32_t which, double *F, double
  */
 duquad_status duquad_solve_emulated(duquad_ctx **ctxs, int32_t P, int32_t alg, int32_t outer_iters,
                                     int32_t inner_iters);
+
+/*
+ * duquad_solve_eps on an emulated row-sharded group (see above): the stop test's sum of
+ * (y - x+)^2 is the sum over the ranks (added in rank order here; ncclAllReduce on a real group),
+ * so every rank takes the same decision.  Counts per rank via duquad_get_inner_counts.
+ */
+duquad_status duquad_solve_eps_emulated(duquad_ctx **ctxs, int32_t P, int32_t alg, int32_t outer_iters,
+                                        int32_t inner_max, double eps_in, double sigma_L);
 
 void duquad_destroy(duquad_ctx *ctx);
 

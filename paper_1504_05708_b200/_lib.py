@@ -102,6 +102,8 @@ _SIGS = {
     "duquad_residuals": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                    C.POINTER(C.c_double)]),
     "duquad_solve_emulated": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
+    "duquad_solve_eps_emulated": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                            C.c_double, C.c_double]),
     "duquad_solve_eps": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_double,
                                    C.POINTER(Result)]),
     "duquad_get_inner_counts": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),

@@ -92,6 +92,8 @@ struct duquad_ctx {
     bool eps_mode = false;
     double eps_thresh2 = 0.0;
     double *gm_sq = nullptr, *gm_part = nullptr;
+    double *gm_tot = nullptr;    // row-sharded eps_in mode: this rank's sum, then the all-reduced one
+    bool pend_decide = false;    // a stop decision waits for the all-reduce (issued with the y gather)
     uint32_t *gm_counter = nullptr;
     int32_t *d_done = nullptr, *d_counts = nullptr;   // d_counts: [K+1] steps, then [K+1] converged flags
     int64_t counts_cap = 0;
@@ -180,6 +182,7 @@ void free_all(duquad_ctx *c) {
     if (c->init_lam) cudaFree(c->init_lam);
     if (c->gm_sq) cudaFree(c->gm_sq);
     if (c->gm_part) cudaFree(c->gm_part);
+    if (c->gm_tot) cudaFree(c->gm_tot);
     if (c->gm_counter) cudaFree(c->gm_counter);
     if (c->d_done) cudaFree(c->d_done);
     if (c->d_counts) cudaFree(c->d_counts);
@@ -310,7 +313,19 @@ enum GatherBuf { G_NONE = -1, G_Y = 0, G_Y2 = 1, G_W = 2, G_RS = 3 };   // G_RS:
 double *gather_ptr(duquad_ctx *c, int b) { return b == G_W ? c->w_full : (b == G_Y2 ? c->y_full2 : c->y_full); }
 int64_t gather_slice(duquad_ctx *c, int b) { return b == G_W ? c->p_slice : c->n_slice; }
 
+duquad_status gather_impl(duquad_ctx *ctx, int b);
+// the gather of the phase, then (row-sharded eps_in mode) the all-reduce of the stop test's sum and
+// the decision, identical on every rank
 duquad_status gather(duquad_ctx *ctx, int b) {
+    duquad_status st = gather_impl(ctx, b);
+    if (st != DUQUAD_OK || !ctx->pend_decide || ctx->emulated) return st;
+    ctx->pend_decide = false;
+    NK(ncclAllReduce(ctx->gm_tot, ctx->gm_tot, 1, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+    CK(launch_inner_decide(ctx->gm_tot, ctx->d_done, ctx->eps_thresh2, ctx->d_counts, ctx->d_j, ctx->stream));
+    return DUQUAD_OK;
+}
+
+duquad_status gather_impl(duquad_ctx *ctx, int b) {
     if (b < 0 || ctx->world == 1 || ctx->emulated) return DUQUAD_OK;   // emulated: group driver copies
     if (b == G_W) return allgather_w(ctx);
     if (b == G_RS) {
@@ -330,7 +345,8 @@ int num_phases(const duquad_ctx *c, int Kin) { return (c->rho0 ? Kin + 3 : 2 * K
 duquad_status inner_check(duquad_ctx *ctx) {
     if (!ctx->eps_mode) return DUQUAD_OK;
     CK(launch_inner_check(ctx->gm_sq, ctx->nloc, ctx->gm_part, ctx->gm_counter, ctx->d_done, ctx->eps_thresh2,
-                          ctx->d_counts, ctx->d_j, ctx->stream));
+                          ctx->d_counts, ctx->d_j, ctx->world > 1 ? ctx->gm_tot : nullptr, ctx->stream));
+    ctx->pend_decide = ctx->world > 1;
     return DUQUAD_OK;
 }
 
@@ -363,9 +379,11 @@ duquad_status outer_phase(duquad_ctx *ctx, const std::vector<double> &beta_in, i
     duquad_status st;
     if (ph == num_phases(ctx, Kin) - 1) return end_outer(ctx, j);
     if (ctx->eps_mode && ph == num_phases(ctx, Kin) - 2) {   // u_bar^j = x: y, average, flag reset
-        double *ydst = ctx->rho0 ? (Kin % 2 ? ctx->y_full2 : ctx->y_full) : ctx->y_full;
+        const bool y2 = ctx->rho0 && Kin % 2;
+        double *ydst = (y2 ? ctx->y_full2 : ctx->y_full) + ctx->rank * ctx->n_slice;   // this rank's slice
         CK(launch_inner_finish(ctx->x, ydst, ctx->xhat, ctx->nloc, ctx->d_ops, ctx->d_j, ctx->d_done,
                                ctx->d_counts + ctx->counts_cap, ctx->stream));
+        *gb = ctx->world > 1 ? (y2 ? G_Y2 : G_Y) : G_NONE;   // row-sharded: the new y slices to every rank
         return DUQUAD_OK;
     }
     if (ctx->rho0) {
@@ -1467,22 +1485,16 @@ duquad_status duquad_solve(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t 
     return solve_body(ctx, alg, outer, inner, res);
 }
 
-duquad_status duquad_solve_eps(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t inner_max, double eps_in,
-                               double sigma_L, duquad_result *res) {
-    if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
-    if (!(eps_in > 0.0) || !(sigma_L > 0.0) || !std::isfinite(eps_in) || !std::isfinite(sigma_L))
-        return fail(ctx, DUQUAD_EINVAL, "eps_in and sigma_L must be finite and > 0");
-    if (ctx->world > 1 || ctx->Btot > 1)
-        return fail(ctx, DUQUAD_EINVAL, "eps_in mode: single GPU, batch 1 only (sharded / batched: fixed counts)");
-    if (outer < 1 || inner_max < 1) return fail(ctx, DUQUAD_EINVAL, "need outer_iters >= 1 and inner_max >= 1");
-    if (!ctx->have_consts) return fail(ctx, DUQUAD_ESTATE, "constants not set (duquad_lipschitz or duquad_set_constants)");
-    DevGuard guard(ctx->dev);
+// eps_in mode around a solve: buffers, counters and the threshold, then (after) the per-solve
+// counts and the EMAXITER status
+static duquad_status eps_begin(duquad_ctx *ctx, int32_t outer, double eps_in, double sigma_L) {
     const int64_t nc = (int64_t)outer + 1;
     if (!ctx->gm_sq) {
-        CK(dalloc(&ctx->gm_sq, ctx->nloc));
+        CK(dalloc(&ctx->gm_sq, std::max<int64_t>(ctx->nloc, 1)));
         CK(dalloc(&ctx->gm_part, (int64_t)kRedGrid));
         CK(dalloc(&ctx->gm_counter, 2));
         CK(dalloc(&ctx->d_done, 2));
+        CK(dalloc(&ctx->gm_tot, 2));
     }
     if (ctx->counts_cap < nc) {
         if (ctx->d_counts) cudaFree(ctx->d_counts);
@@ -1496,7 +1508,12 @@ duquad_status duquad_solve_eps(duquad_ctx *ctx, int32_t alg, int32_t outer, int3
     // stop when L_in ||y - x+|| <= sqrt(2 sigma_L eps_in), i.e. sum (y - x+)^2 <= 2 sigma_L eps_in / L_in^2
     ctx->eps_thresh2 = 2.0 * sigma_L * eps_in / (ctx->L_in * ctx->L_in);
     ctx->eps_mode = true;
-    duquad_status st = solve_body(ctx, alg, outer, inner_max, res);
+    ctx->pend_decide = false;
+    return DUQUAD_OK;
+}
+
+static duquad_status eps_end(duquad_ctx *ctx, int32_t outer, duquad_status st, duquad_result *res) {
+    const int64_t nc = (int64_t)outer + 1;
     ctx->eps_mode = false;
     if (st != DUQUAD_OK && st != DUQUAD_ENONFINITE) return st;
     std::vector<int32_t> buf(2 * ctx->counts_cap);
@@ -1516,6 +1533,22 @@ duquad_status duquad_solve_eps(duquad_ctx *ctx, int32_t alg, int32_t outer, int3
     if (st != DUQUAD_OK) return st;
     if (capped) return fail(ctx, DUQUAD_EMAXITER, "an inner solve hit inner_max before the eps_in test (result valid)");
     return DUQUAD_OK;
+}
+
+duquad_status duquad_solve_eps(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t inner_max, double eps_in,
+                               double sigma_L, duquad_result *res) {
+    if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
+    if (!(eps_in > 0.0) || !(sigma_L > 0.0) || !std::isfinite(eps_in) || !std::isfinite(sigma_L))
+        return fail(ctx, DUQUAD_EINVAL, "eps_in and sigma_L must be finite and > 0");
+    if (ctx->Btot > 1) return fail(ctx, DUQUAD_EINVAL, "eps_in mode: not for a batch (fixed counts)");
+    if (ctx->emulated) return fail(ctx, DUQUAD_EINVAL, "emulated ranks: use duquad_solve_eps_emulated");
+    if (outer < 1 || inner_max < 1) return fail(ctx, DUQUAD_EINVAL, "need outer_iters >= 1 and inner_max >= 1");
+    if (!ctx->have_consts) return fail(ctx, DUQUAD_ESTATE, "constants not set (duquad_lipschitz or duquad_set_constants)");
+    DevGuard guard(ctx->dev);
+    duquad_status st = eps_begin(ctx, outer, eps_in, sigma_L);
+    if (st != DUQUAD_OK) return st;
+    st = solve_body(ctx, alg, outer, inner_max, res);
+    return eps_end(ctx, outer, st, res);
 }
 
 duquad_status duquad_theory_schedule(int32_t alg, double eps, double R_d, double L_d, double L_in, double sigma_L,
@@ -1922,7 +1955,25 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
 }
 
 // all-gather of replica buffer b across emulated ranks: device copies of every rank's slice
+static duquad_status group_gather_impl(duquad_ctx **c, int P, int b);
 static duquad_status group_gather(duquad_ctx **c, int P, int b) {
+    duquad_status st = group_gather_impl(c, P, b);
+    if (st != DUQUAD_OK || P == 1 || !c[0]->pend_decide) return st;
+    // emulated all-reduce of the stop test's sum: ranks added in order, the result to every rank
+    duquad_ctx *ctx = c[0];
+    double *acc = c[0]->gm_part;   // scratch (the partial sums of the check kernel are consumed)
+    CK(cudaMemcpyAsync(acc, c[0]->gm_tot, sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    for (int q = 1; q < P; ++q) CK(launch_vec_add(acc, c[q]->gm_tot, 1, ctx->stream));
+    for (int r = 0; r < P; ++r) {
+        CK(cudaMemcpyAsync(c[r]->gm_tot, acc, sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+        CK(launch_inner_decide(c[r]->gm_tot, c[r]->d_done, c[r]->eps_thresh2, c[r]->d_counts, c[r]->d_j,
+                               ctx->stream));
+        c[r]->pend_decide = false;
+    }
+    return DUQUAD_OK;
+}
+
+static duquad_status group_gather_impl(duquad_ctx **c, int P, int b) {
     if (b < 0 || P == 1) return DUQUAD_OK;
     duquad_ctx *ctx = c[0];
     if (b == G_RS) {   // reduce-scatter: slice r = sum over ranks q (in order) of fpart_q[slice r]
@@ -1945,7 +1996,38 @@ static duquad_status group_gather(duquad_ctx **c, int P, int b) {
     return DUQUAD_OK;
 }
 
+static duquad_status solve_emulated_impl(duquad_ctx **ctxs, int32_t P, int32_t alg, int32_t outer, int32_t inner);
+
+duquad_status duquad_solve_eps_emulated(duquad_ctx **ctxs, int32_t P, int32_t alg, int32_t outer, int32_t inner_max,
+                                        double eps_in, double sigma_L) {
+    if (!ctxs || P < 1 || !ctxs[0]) return fail(nullptr, DUQUAD_EINVAL, "need P >= 1 contexts");
+    if (!(eps_in > 0.0) || !(sigma_L > 0.0) || !std::isfinite(eps_in) || !std::isfinite(sigma_L))
+        return fail(ctxs[0], DUQUAD_EINVAL, "eps_in and sigma_L must be finite and > 0");
+    if (outer < 1 || inner_max < 1) return fail(ctxs[0], DUQUAD_EINVAL, "need outer_iters >= 1 and inner_max >= 1");
+    for (int r = 0; r < P; ++r)
+        if (!ctxs[r] || !ctxs[r]->have_consts || ctxs[r]->Btot > 1)
+            return fail(ctxs[0], DUQUAD_EINVAL, "emulated eps_in group: set-up single-QP contexts with constants");
+    DevGuard guard(ctxs[0]->dev);
+    duquad_status st;
+    for (int r = 0; r < P; ++r)
+        if ((st = eps_begin(ctxs[r], outer, eps_in, sigma_L)) != DUQUAD_OK) return st;
+    st = solve_emulated_impl(ctxs, P, alg, outer, inner_max);
+    duquad_status out = DUQUAD_OK;
+    for (int r = 0; r < P; ++r) {
+        const duquad_status e = eps_end(ctxs[r], outer, st, nullptr);
+        if (out == DUQUAD_OK) out = e;
+    }
+    return out;
+}
+
 duquad_status duquad_solve_emulated(duquad_ctx **ctxs, int32_t P, int32_t alg, int32_t outer, int32_t inner) {
+    if (ctxs && P >= 1)
+        for (int r = 0; r < P; ++r)
+            if (ctxs[r]) ctxs[r]->eps_mode = false;
+    return solve_emulated_impl(ctxs, P, alg, outer, inner);
+}
+
+static duquad_status solve_emulated_impl(duquad_ctx **ctxs, int32_t P, int32_t alg, int32_t outer, int32_t inner) {
     if (!ctxs || P < 1) return fail(nullptr, DUQUAD_EINVAL, "need P >= 1 contexts");
     for (int r = 0; r < P; ++r) {
         duquad_ctx *c = ctxs[r];

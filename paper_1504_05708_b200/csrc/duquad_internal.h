@@ -230,7 +230,9 @@ cudaError_t launch_apply_initial(double *x, double *y, const double *lb, const d
 // eps_in mode (duquad_solve_eps): after an inner step, sum gm_sq (fixed order; partials + the last
 // block) -> counts[*d_j - 1] += 1 and *done = 1 if L_in^2 sum <= 2 sigma eps_in (thresh2 = that / L_in^2)
 cudaError_t launch_inner_check(const double *gm_sq, int64_t n, double *partials, uint32_t *counter, int32_t *done,
-                               double thresh2, int32_t *counts, const int32_t *d_j, cudaStream_t s);
+                               double thresh2, int32_t *counts, const int32_t *d_j, double *out_sum, cudaStream_t s);
+cudaError_t launch_inner_decide(const double *sum, int32_t *done, double thresh2, int32_t *counts,
+                                const int32_t *d_j, cudaStream_t s);
 // after the inner loop: y_dst = x (u_bar^j), running average with ops[*d_j].avg_w, conv[*d_j - 1] = *done,
 // *done = 0
 cudaError_t launch_inner_finish(const double *x, double *y_dst, double *xhat, int64_t n, const OuterParam *ops,

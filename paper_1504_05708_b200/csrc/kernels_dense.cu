@@ -283,8 +283,10 @@ __global__ void k_apply_initial(double *x, double *y, const double *lb, const do
 
 // eps_in mode: gradient-map test after an inner step (fixed-order sum: block partials over
 // contiguous ranges, then the last block to finish adds them in block order)
+// out_sum (row-sharded): write this rank's fixed-order sum there and leave the decision to
+// k_inner_decide after the all-reduce
 __global__ void k_inner_check(const double *gm_sq, int64_t n, double *partials, uint32_t *counter, int32_t *done,
-                              double thresh2, int32_t *counts, const int32_t *d_j) {
+                              double thresh2, int32_t *counts, const int32_t *d_j, double *out_sum) {
     if (*done) return;
     __shared__ double red[32];
     __shared__ bool last;
@@ -306,10 +308,21 @@ __global__ void k_inner_check(const double *gm_sq, int64_t n, double *partials, 
         __threadfence();
         double t = 0.0;
         for (int c = 0; c < (int)gridDim.x; ++c) t += partials[c];
+        *counter = 0;
+        if (out_sum) {
+            *out_sum = t;
+            return;
+        }
         counts[*d_j - 1] += 1;
         if (t <= thresh2) *done = 1;
-        *counter = 0;
     }
+}
+
+// the decision of k_inner_check on the all-reduced sum (identical on every rank)
+__global__ void k_inner_decide(const double *sum, int32_t *done, double thresh2, int32_t *counts, const int32_t *d_j) {
+    if (*done) return;
+    counts[*d_j - 1] += 1;
+    if (*sum <= thresh2) *done = 1;
 }
 
 __global__ void k_inner_finish(const double *x, double *y_dst, double *xhat, int64_t n, const OuterParam *ops,
@@ -547,8 +560,15 @@ cudaError_t launch_init_state(double *x, double *y, double *xhat, const double *
 }
 
 cudaError_t launch_inner_check(const double *gm_sq, int64_t n, double *partials, uint32_t *counter, int32_t *done,
-                               double thresh2, int32_t *counts, const int32_t *d_j, cudaStream_t s) {
-    k_inner_check<<<kRedGrid, kRedThreads, 0, s>>>(gm_sq, n, partials, counter, done, thresh2, counts, d_j);
+                               double thresh2, int32_t *counts, const int32_t *d_j, double *out_sum, cudaStream_t s) {
+    k_inner_check<<<kRedGrid, kRedThreads, 0, s>>>(gm_sq, n, partials, counter, done, thresh2, counts, d_j,
+                                                   out_sum);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_inner_decide(const double *sum, int32_t *done, double thresh2, int32_t *counts,
+                                const int32_t *d_j, cudaStream_t s) {
+    k_inner_decide<<<1, 1, 0, s>>>(sum, done, thresh2, counts, d_j);
     return cudaGetLastError();
 }
 

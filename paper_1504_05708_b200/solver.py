@@ -61,6 +61,25 @@ def solve_emulated(solvers, alg: str = "DFGM", outer: int = 1, inner: int = 1):
             solvers[0]._ctx)
 
 
+def solve_emulated_eps(solvers, alg: str, outer: int, inner_max: int, eps_in: float, sigma_L: float) -> dict:
+    """solve_emulated with eps_in-driven inner stopping (duquad_solve_eps_emulated): the stop test's
+    sum is all-reduced over the ranks (emulated: added in rank order), so every rank takes the same
+    decision.  Returns the per-solve counts / converged flags (identical on every rank)."""
+    arr = (C.c_void_p * len(solvers))(*[s._ctx.value for s in solvers])
+    st = L.lib().duquad_solve_eps_emulated(arr, len(solvers), _ALGS[alg], int(outer), int(inner_max), float(eps_in),
+                                           float(sigma_L))
+    if st not in (L.DUQUAD_OK, L.DUQUAD_EMAXITER):
+        L.check(st, solvers[0]._ctx)
+    m = int(outer) + 1
+    out = []
+    for s in solvers:
+        counts, conv = (C.c_int32 * m)(), (C.c_int32 * m)()
+        L.check(L.lib().duquad_get_inner_counts(s._ctx, counts, conv, m), s._ctx)
+        out.append((list(counts), [bool(c) for c in conv]))
+    assert all(o == out[0] for o in out), "ranks disagree on the stop decisions"
+    return dict(inner_counts=out[0][0], converged=out[0][1], capped=st == L.DUQUAD_EMAXITER)
+
+
 def theory_schedule(alg: str, eps: float, R_d: float, L_d: float, L_in: float, sigma_L: float, D_U: float,
                     normG: float, lambda_min_Q: float = 0.0) -> dict:
     """DuQuad's theory schedule (include/duquad.h duquad_theory_schedule; host arithmetic)."""

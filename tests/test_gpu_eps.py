@@ -140,3 +140,29 @@ def test_eps_mode_rejects_bad_arguments(torch_cuda):
         with pytest.raises(DuquadError):
             s.solve_eps("DFGM", 2, 10, eps_in, sig)
     s.close()
+
+
+@pytest.mark.parametrize("P,n,p", [(2, 301, 97), (3, 4100, 1500)])
+def test_eps_mode_row_sharded_emulated(torch_cuda, P, n, p):
+    """Row-sharded eps_in mode (emulated ranks on one GPU): the stop test's sum is all-reduced over
+    the ranks, every rank takes the same decision; two-pass (n = 301) and the row-sharded byte floor
+    (n = 4100) -- the oracle replays the counts and every decision is checked."""
+    from paper_1504_05708_b200 import Solver, solve_emulated_eps
+    import torch
+    prob = qpgen.dense_ineq(n, p, seed=3, shift=0.1)
+    prob.G *= 0.05
+    prob.g *= 0.05
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 1.0, 0.1)
+    eps_in, sigma_L, K, kmax = 1e-4, 0.1, 3, 120
+    st = torch.cuda.Stream()
+    ss = [Solver(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho=1.0, world_size=P, rank=r,
+                 emulate_ranks=True, stream=st.cuda_stream, small_path=False) for r in range(P)]
+    for s in ss:
+        s.set_constants(L_in, L_d)
+    info = solve_emulated_eps(ss, "DFGM", K, kmax, eps_in, sigma_L)
+    parts = [s.result() for s in ss]
+    for s in ss:
+        s.close()
+    xl, xa, lam = (np.concatenate([pt[i] for pt in parts]) for i in range(3))
+    info["inner_iters_total"] = sum(info["inner_counts"])
+    _check(prob, 1.0, "DFGM", K, kmax, eps_in, sigma_L, L_in, L_d, info, xl, xa, lam)
