@@ -330,8 +330,9 @@ duquad_status duquad_theory_schedule(int32_t alg, double eps, double R_d, double
  *   duquad_set_state: the next duquad_solve(alg, K, ...) continues with outer iterations
  *     j+1 .. j+K (theta, beta_out and the average weights continue; warm start ignored), so
  *     solve(K1) + get_state + set_state + solve(K2) equals solve(K1 + K2) bit for bit.
- * Buffers are host or device per on_device (layout as duquad_get_result); single GPU (batch
- * allowed); fixed inner counts, no dual_average.  DUQUAD_EINVAL on bad arguments.
+ * Buffers are host or device per on_device (layout as duquad_get_result: a row-sharded rank
+ * exports and imports its own slices); fixed inner counts, no dual_average.  DUQUAD_EINVAL on
+ * bad arguments.
  */
 duquad_status duquad_get_state(duquad_ctx *ctx, double *x, double *mu, double *lam_prev, double *x_avg,
                                int64_t *outer_done, double *S, int32_t on_device);

@@ -1342,8 +1342,8 @@ static duquad_status solve_prepare(duquad_ctx *ctx, int alg, int K, int Kin, std
         return fail(ctx, DUQUAD_EINVAL, "dual_average: fixed inner counts only");
     ctx->resumed = ctx->resume;
     ctx->resume = false;
-    if ((ctx->resumed || ctx->opt.checkpoint) && (ctx->davg || ctx->eps_mode || ctx->world > 1))
-        return fail(ctx, DUQUAD_EINVAL, "checkpoint / resume: fixed counts, no dual_average, single GPU");
+    if ((ctx->resumed || ctx->opt.checkpoint) && (ctx->davg || ctx->eps_mode))
+        return fail(ctx, DUQUAD_EINVAL, "checkpoint / resume: fixed counts, no dual_average");
     ctx->j0 = ctx->resumed ? ctx->ck_j : 0;
     const int J0 = (int)ctx->j0;
     // ---- host tables (fp64, PAPER.md:358-363 / 587-589 / 700-706)
@@ -1698,7 +1698,6 @@ duquad_status duquad_get_state(duquad_ctx *ctx, double *x, double *mu, double *l
 duquad_status duquad_set_state(duquad_ctx *ctx, const double *x, const double *mu, const double *lam_prev,
                                const double *x_avg, int64_t outer_done, double S, int32_t on_device) {
     if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
-    if (ctx->world > 1) return fail(ctx, DUQUAD_EINVAL, "set_state: single GPU only");
     if (outer_done < 1 || !(S > 0) || !std::isfinite(S) || outer_done > (1 << 28))
         return fail(ctx, DUQUAD_EINVAL, "set_state: outer_done >= 1 and S > 0 (the averaging weight sum)");
     if (!x || !x_avg || (ctx->p > 0 && (!mu || !lam_prev)))
@@ -2051,13 +2050,17 @@ static duquad_status solve_emulated_impl(duquad_ctx **ctxs, int32_t P, int32_t a
     for (int r = 0; r < P; ++r)
         if ((st = solve_prepare(ctxs[r], alg, K, Kin, beta_in)) != DUQUAD_OK) return st;
     if ((st = group_gather(ctxs, P, G_Y)) != DUQUAD_OK) return st;
-    for (int j = 1; j <= K + 1 + (ctx->davg ? 1 : 0); ++j)
+    for (int j = 1; j <= K + 1 + (ctx->davg ? 1 : 0); ++j) {
+        if (j == K + 1)
+            for (int r = 0; r < P; ++r)
+                if (ctxs[r]->opt.checkpoint && (st = save_checkpoint(ctxs[r])) != DUQUAD_OK) return st;
         for (int ph = 0; ph < num_phases(ctx, Kin); ++ph) {
             int gb = G_NONE;
             for (int r = 0; r < P; ++r)
                 if ((st = outer_phase(ctxs[r], beta_in, Kin, j, ph, nullptr, &gb)) != DUQUAD_OK) return st;
             if ((st = group_gather(ctxs, P, gb)) != DUQUAD_OK) return st;
         }
+    }
     CK(cudaStreamSynchronize(ctx->stream));
     int32_t any = 0;
     for (int r = 0; r < P; ++r) {
@@ -2065,6 +2068,11 @@ static duquad_status solve_emulated_impl(duquad_ctx **ctxs, int32_t P, int32_t a
         CK(cudaMemcpy(&flag, ctxs[r]->d_flag, sizeof(flag), cudaMemcpyDeviceToHost));
         any |= flag;
         ctxs[r]->solved = true;
+        if (ctxs[r]->opt.checkpoint && !flag) {
+            ctxs[r]->ck_valid = true;
+            ctxs[r]->ck_j = ctxs[r]->j0 + K;
+            ctxs[r]->ck_S = ctxs[r]->S_end;
+        }
     }
     if (any) return fail(ctx, DUQUAD_ENONFINITE, "an iterate became non-finite");
     return DUQUAD_OK;

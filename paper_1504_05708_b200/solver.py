@@ -304,14 +304,16 @@ class Solver:
         """The DFOM state the last solve snapshotted after its K-th outer iteration (needs
         checkpoint=True): x = u_bar^K, mu = mu^K, lam_prev = lambda^{K-1}, x_avg, outer_done, S."""
         bl = self.b_range[1] - self.b_range[0]
-        shp_n = (bl, self.n) if self.batch > 1 else (self.n,)
-        shp_p = (bl, max(self.p, 1)) if self.batch > 1 else (max(self.p, 1),)
+        nl = self.n_range[1] - self.n_range[0]     # row-sharded: this rank's slices
+        pl = self.p_range[1] - self.p_range[0]
+        shp_n = (bl, nl) if self.batch > 1 else (nl,)
+        shp_p = (bl, max(pl, 1)) if self.batch > 1 else (max(pl, 1),)
         x, xa = np.empty(shp_n), np.empty(shp_n)
         mu, lp = np.empty(shp_p), np.empty(shp_p)
         j, S = C.c_int64(), C.c_double()
         L.check(self._lib.duquad_get_state(self._ctx, x.ctypes.data, mu.ctypes.data, lp.ctypes.data, xa.ctypes.data,
                                            C.byref(j), C.byref(S), 0), self._ctx)
-        return dict(x=x, mu=mu[..., :self.p], lam_prev=lp[..., :self.p], x_avg=xa, outer_done=j.value, S=S.value)
+        return dict(x=x, mu=mu[..., :pl], lam_prev=lp[..., :pl], x_avg=xa, outer_done=j.value, S=S.value)
 
     def set_state(self, state: dict):
         """Continue the next solve from `state` (a get_state() dict): outer iterations

@@ -118,3 +118,36 @@ def test_state_errors(torch_cuda):
     with pytest.raises(DuquadError):
         s.solve("DGM", 2, 3)                            # checkpoint + dual averaging: not combined
     s.close()
+
+
+@pytest.mark.parametrize("n,p", [(301, 97), (4100, 1500)])
+def test_resume_row_sharded_emulated(torch_cuda, n, p):
+    """Row-sharded (3 emulated ranks; two-pass at n = 301, the sharded byte floor at n = 4100): each
+    rank exports and re-imports its own slices; the continuation is bitwise the uninterrupted solve."""
+    from paper_1504_05708_b200 import Solver, solve_emulated
+    import torch
+    prob = qpgen.dense_ineq(n, p, seed=2, shift=0.1)
+    L = O.lipschitz_constants(prob.Q, prob.G, 1.0, 0.1)[:2]
+    st = torch.cuda.Stream()
+
+    def group():
+        ss = [Solver(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho=1.0, world_size=3, rank=r,
+                     emulate_ranks=True, stream=st.cuda_stream, small_path=False, checkpoint=True) for r in range(3)]
+        for s in ss:
+            s.set_constants(*L)
+        return ss
+
+    a = group()
+    solve_emulated(a, "DFGM", 5, 4)
+    full = [np.concatenate([s.result()[i] for s in a]) for i in range(3)]
+    solve_emulated(a, "DFGM", 2, 4)
+    states = [s.get_state() for s in a]
+    b = group()
+    for s, stt in zip(b, states):
+        s.set_state(stt)
+    solve_emulated(b, "DFGM", 3, 4)
+    part = [np.concatenate([s.result()[i] for s in b]) for i in range(3)]
+    for s in a + b:
+        s.close()
+    for x, y in zip(full, part):
+        assert np.array_equal(x, y), np.max(np.abs(x - y))
