@@ -93,6 +93,9 @@ struct duquad_ctx {
     double eps_thresh2 = 0.0;
     double *gm_sq = nullptr, *gm_part = nullptr;
     double *gm_tot = nullptr;    // row-sharded eps_in mode: this rank's sum, then the all-reduced one
+    double *gm_b = nullptr;      // batched eps_in mode: per-QP sums, stop flags, number stopped
+    int32_t *done_b = nullptr, *ndone = nullptr;
+    int64_t eps_nc = 0;          // eps_in mode: solves per QP (K + 1)
     bool pend_decide = false;    // a stop decision waits for the all-reduce (issued with the y gather)
     uint32_t *gm_counter = nullptr;
     int32_t *d_done = nullptr, *d_counts = nullptr;   // d_counts: [K+1] steps, then [K+1] converged flags
@@ -183,6 +186,9 @@ void free_all(duquad_ctx *c) {
     if (c->gm_sq) cudaFree(c->gm_sq);
     if (c->gm_part) cudaFree(c->gm_part);
     if (c->gm_tot) cudaFree(c->gm_tot);
+    if (c->gm_b) cudaFree(c->gm_b);
+    if (c->done_b) cudaFree(c->done_b);
+    if (c->ndone) cudaFree(c->ndone);
     if (c->gm_counter) cudaFree(c->gm_counter);
     if (c->d_done) cudaFree(c->d_done);
     if (c->d_counts) cudaFree(c->d_counts);
@@ -344,6 +350,11 @@ int num_phases(const duquad_ctx *c, int Kin) { return (c->rho0 ? Kin + 3 : 2 * K
 // eps_in mode: gradient-map test after inner step k (a no-op once the solve has converged)
 duquad_status inner_check(duquad_ctx *ctx) {
     if (!ctx->eps_mode) return DUQUAD_OK;
+    if (ctx->Btot > 1) {   // per-QP decisions on the sums the pass-B epilogue accumulated
+        CK(launch_batched_decide(ctx->gm_b, ctx->done_b, ctx->ndone, ctx->eps_thresh2, ctx->d_counts, ctx->eps_nc,
+                                 ctx->d_j, ctx->Bloc, ctx->stream));
+        return DUQUAD_OK;
+    }
     CK(launch_inner_check(ctx->gm_sq, ctx->nloc, ctx->gm_part, ctx->gm_counter, ctx->d_done, ctx->eps_thresh2,
                           ctx->d_counts, ctx->d_j, ctx->world > 1 ? ctx->gm_tot : nullptr, ctx->stream));
     ctx->pend_decide = ctx->world > 1;
@@ -379,6 +390,12 @@ duquad_status outer_phase(duquad_ctx *ctx, const std::vector<double> &beta_in, i
     duquad_status st;
     if (ph == num_phases(ctx, Kin) - 1) return end_outer(ctx, j);
     if (ctx->eps_mode && ph == num_phases(ctx, Kin) - 2) {   // u_bar^j = x: y, average, flag reset
+        if (ctx->Btot > 1) {
+            CK(launch_batched_finish(ctx->Xb, ctx->Yb, ctx->XHb, ctx->n, ctx->ld, ctx->Bloc, ctx->d_ops, ctx->d_j,
+                                     ctx->done_b, ctx->ndone, ctx->d_counts + ctx->counts_cap, ctx->eps_nc,
+                                     ctx->stream));
+            return DUQUAD_OK;
+        }
         const bool y2 = ctx->rho0 && Kin % 2;
         double *ydst = (y2 ? ctx->y_full2 : ctx->y_full) + ctx->rank * ctx->n_slice;   // this rank's slice
         CK(launch_inner_finish(ctx->x, ydst, ctx->xhat, ctx->nloc, ctx->d_ops, ctx->d_j, ctx->d_done,
@@ -492,7 +509,7 @@ duquad_status outer_phase(duquad_ctx *ctx, const std::vector<double> &beta_in, i
         if (bt) {
             BatchedArgs BB = make_batched(ctx, 1);
             BB.b.beta_in = beta_in[k];
-            BB.b.last_inner = (k == Kin);
+            BB.b.last_inner = (k == Kin) && !ctx->eps_mode;
             CK(launch_batched(BB, 1, MODE_SOLVE, ctx->stream));
         } else {
             PassBArgs b = make_b(ctx);
@@ -534,6 +551,11 @@ BatchedArgs make_batched(duquad_ctx *c, int pass) {
     ba.a.lam_prev = c->lpb;
     ba.a.h = c->hb;
     ba.a.lam_hat = c->davg ? c->lhb : nullptr;
+    if (c->eps_mode) {
+        ba.gm_b = c->gm_b;
+        ba.done_b = c->done_b;
+        ba.ndone = c->ndone;
+    }
     ba.b.qy = c->QYb;
     ba.b.q = c->qb;
     ba.b.x = c->Xb;
@@ -1488,7 +1510,19 @@ duquad_status duquad_solve(duquad_ctx *ctx, int32_t alg, int32_t outer, int32_t 
 // eps_in mode around a solve: buffers, counters and the threshold, then (after) the per-solve
 // counts and the EMAXITER status
 static duquad_status eps_begin(duquad_ctx *ctx, int32_t outer, double eps_in, double sigma_L) {
-    const int64_t nc = (int64_t)outer + 1;
+    const int64_t B = ctx->Btot > 1 ? ctx->Bloc : 1;
+    const int64_t nc = ((int64_t)outer + 1) * B;   // per QP (batched: QP-major [QP][solve])
+    ctx->eps_nc = (int64_t)outer + 1;
+    if (ctx->Btot > 1) {
+        if (ctx->gm_b) cudaFree(ctx->gm_b);
+        if (ctx->done_b) cudaFree(ctx->done_b);
+        if (!ctx->ndone) CK(dalloc(&ctx->ndone, 2));
+        ctx->gm_b = nullptr;
+        ctx->done_b = nullptr;
+        CK(dalloc(&ctx->gm_b, B));
+        CK(dalloc(&ctx->done_b, B));
+        CK(cudaMemsetAsync(ctx->ndone, 0, sizeof(int32_t), ctx->stream));
+    }
     if (!ctx->gm_sq) {
         CK(dalloc(&ctx->gm_sq, std::max<int64_t>(ctx->nloc, 1)));
         CK(dalloc(&ctx->gm_part, (int64_t)kRedGrid));
@@ -1513,7 +1547,7 @@ static duquad_status eps_begin(duquad_ctx *ctx, int32_t outer, double eps_in, do
 }
 
 static duquad_status eps_end(duquad_ctx *ctx, int32_t outer, duquad_status st, duquad_result *res) {
-    const int64_t nc = (int64_t)outer + 1;
+    const int64_t nc = ((int64_t)outer + 1) * (ctx->Btot > 1 ? ctx->Bloc : 1);
     ctx->eps_mode = false;
     if (st != DUQUAD_OK && st != DUQUAD_ENONFINITE) return st;
     std::vector<int32_t> buf(2 * ctx->counts_cap);
@@ -1527,7 +1561,7 @@ static duquad_status eps_end(duquad_ctx *ctx, int32_t outer, duquad_status st, d
         capped |= ctx->last_conv[j] == 0;
     }
     if (res) {
-        res->inner_iters_total = total;
+        res->inner_iters_total = total;   // batched: summed over the QPs
         res->matrix_passes = 2 * total;
     }
     if (st != DUQUAD_OK) return st;
@@ -1540,7 +1574,6 @@ duquad_status duquad_solve_eps(duquad_ctx *ctx, int32_t alg, int32_t outer, int3
     if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
     if (!(eps_in > 0.0) || !(sigma_L > 0.0) || !std::isfinite(eps_in) || !std::isfinite(sigma_L))
         return fail(ctx, DUQUAD_EINVAL, "eps_in and sigma_L must be finite and > 0");
-    if (ctx->Btot > 1) return fail(ctx, DUQUAD_EINVAL, "eps_in mode: not for a batch (fixed counts)");
     if (ctx->emulated) return fail(ctx, DUQUAD_EINVAL, "emulated ranks: use duquad_solve_eps_emulated");
     if (outer < 1 || inner_max < 1) return fail(ctx, DUQUAD_EINVAL, "need outer_iters >= 1 and inner_max >= 1");
     if (!ctx->have_consts) return fail(ctx, DUQUAD_ESTATE, "constants not set (duquad_lipschitz or duquad_set_constants)");

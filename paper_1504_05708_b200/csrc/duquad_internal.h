@@ -103,6 +103,10 @@ struct BatchedArgs {
     int64_t K;           // reduction length, padded to a multiple of 32 (zero padding)
     int64_t sn, sp;
     int64_t ncol8;       // QP octets (set by launch_batched)
+    // eps_in mode (else null): per-QP stop-test sums, stop flags, number of stopped QPs
+    double *gm_b;
+    int32_t *done_b;
+    const int32_t *ndone;
     PassAArgs a;         // pass 0 epilogue (pointers at QP 0)
     PassBArgs b;         // pass 1 epilogue
 };
@@ -203,6 +207,11 @@ cudaError_t launch_init_batched(double *x, double *y, double *xhat, const double
                                 int64_t sn, double *mu, double *lam_prev, int64_t sp, int64_t B, int32_t *d_j,
                                 int32_t *flag, cudaStream_t s);
 cudaError_t launch_mirror_upper(double *H, int64_t n, int64_t ld, cudaStream_t s);
+cudaError_t launch_batched_decide(double *gm_b, int32_t *done_b, int32_t *ndone, double thresh2, int32_t *counts,
+                                  int64_t nc, const int32_t *d_j, int64_t B, cudaStream_t s);
+cudaError_t launch_batched_finish(const double *x, double *y, double *xhat, int64_t n, int64_t sn, int64_t B,
+                                  const OuterParam *ops, const int32_t *d_j, int32_t *done_b, int32_t *ndone,
+                                  int32_t *conv, int64_t nc, cudaStream_t s);
 cudaError_t launch_batched_h(double *h, const double *mu, const double *g, double rho, int64_t p, int64_t sp,
                              int64_t B, cudaStream_t s);
 

@@ -31,6 +31,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
+
+#include <algorithm>
 #ifdef DUQUAD_BATCHED_TRACE
 #include <cstdio>
 #endif
@@ -373,6 +375,7 @@ __device__ __forceinline__ void epi_block_b(const BatchedArgs &args, const doubl
     }
     bool bad = false;
     for (int col = wid; col < gr.nq; col += nwk) {
+        if (args.done_b && args.done_b[gr.q0 + col]) continue;   // eps_in mode: this QP's inner solve stopped
         const int64_t off = (gr.q0 + col) * args.sn;
         const double *qyp = B.qy + off, *qp = B.q + off;
         double *xp = B.x + off, *yp = B.y + off, *hp = B.xhat + off;
@@ -397,7 +400,20 @@ __device__ __forceinline__ void epi_block_b(const BatchedArgs &args, const doubl
                 xp[jj[t]] = xn;
                 yp[jj[t]] = yn;
                 bad |= !isfinite(xn) || !isfinite(yn);
+                if (args.gm_b) {   // eps_in mode: (y - x+)^2, this column's rows
+                    const double dd = vy[t] - xn;
+                    vh[t] = dd * dd;
+                }
+            } else {
+                vh[t] = 0.0;
             }
+        if (args.gm_b) {   // the QP's sum: rows in lane order, blocks in order (one warp per column)
+            double gsum = 0.0;
+#pragma unroll
+            for (int t = 0; t < RPL; ++t) gsum += vh[t];
+            gsum = warp_sum(gsum);
+            if (lane == 0) atomicAdd(&args.gm_b[gr.q0 + col], gsum);
+        }
     }
     if (bad) *B.flag = 1;
 }
@@ -406,6 +422,7 @@ __device__ __forceinline__ void epi_block_b(const BatchedArgs &args, const doubl
 template <int PASS, int NT>
 __global__ void __launch_bounds__(Geo<PASS, NT>::THREADS, 1) k_batched(const BatchedArgs args) {
     using GE = Geo<PASS, NT>;
+    if (args.ndone && *args.ndone >= args.N) return;   // eps_in mode: every QP's inner solve has stopped
     constexpr int ST = GE::STAGES;
     extern __shared__ __align__(16) double smem[];
     double *As = smem;
@@ -573,6 +590,62 @@ cudaError_t launch_batched(const BatchedArgs &a, int pass, int mode, cudaStream_
     if (a.N <= 0 || a.M <= 0) return cudaSuccess;
     if (mode != MODE_SOLVE) return cudaErrorInvalidValue;   // the batched path runs solve passes only
     return pass == 0 ? launch_t<0, kNTA>(a, s) : launch_t<1, kNTB>(a, s);
+}
+
+// eps_in mode (per QP): the stop test on the QP's sum of (y - x+)^2, then the sum is cleared
+__global__ void k_batched_decide(double *gm_b, int32_t *done_b, int32_t *ndone, double thresh2, int32_t *counts,
+                                 int64_t nc, const int32_t *d_j, int64_t B) {
+    const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q >= B) return;
+    if (!done_b[q]) {
+        counts[q * nc + *d_j - 1] += 1;
+        if (gm_b[q] <= thresh2) {
+            done_b[q] = 1;
+            atomicAdd(ndone, 1);
+        }
+    }
+    gm_b[q] = 0.0;
+}
+
+// end of an inner solve in eps_in mode: y = x (warm start), running average, the QP's
+// converged flag recorded and its stop flag cleared for the next outer iteration
+__global__ void k_batched_finish(const double *x, double *y, double *xhat, int64_t n, int64_t sn, int64_t B,
+                                 const OuterParam *ops, const int32_t *d_j, int32_t *done_b, int32_t *conv,
+                                 int64_t nc) {
+    const double w = ops[*d_j].avg_w;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < B * sn; t += (int64_t)gridDim.x * blockDim.x) {
+        if (t % sn >= n) continue;
+        const double xi = x[t];
+        y[t] = xi;
+        if (w != 0.0) xhat[t] = xhat[t] + w * (xi - xhat[t]);
+    }
+}
+
+__global__ void k_batched_reset(int32_t *done_b, int32_t *ndone, int32_t *conv, int64_t nc, const int32_t *d_j,
+                                int64_t B) {
+    const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q < B) {
+        conv[q * nc + *d_j - 1] = done_b[q];
+        done_b[q] = 0;
+    }
+    if (q == 0) *ndone = 0;
+}
+
+cudaError_t launch_batched_decide(double *gm_b, int32_t *done_b, int32_t *ndone, double thresh2, int32_t *counts,
+                                  int64_t nc, const int32_t *d_j, int64_t B, cudaStream_t s) {
+    if (B > 0) k_batched_decide<<<(unsigned)((B + 255) / 256), 256, 0, s>>>(gm_b, done_b, ndone, thresh2, counts, nc, d_j, B);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_batched_finish(const double *x, double *y, double *xhat, int64_t n, int64_t sn, int64_t B,
+                                  const OuterParam *ops, const int32_t *d_j, int32_t *done_b, int32_t *ndone,
+                                  int32_t *conv, int64_t nc, cudaStream_t s) {
+    if (B <= 0) return cudaSuccess;
+    const int64_t m = B * sn;
+    k_batched_finish<<<(unsigned)std::min<int64_t>(1184, (m + 255) / 256), 256, 0, s>>>(x, y, xhat, n, sn, B, ops, d_j,
+                                                                                       done_b, conv, nc);
+    k_batched_reset<<<(unsigned)((B + 255) / 256), 256, 0, s>>>(done_b, ndone, conv, nc, d_j, B);
+    return cudaGetLastError();
 }
 
 __global__ void k_batched_h(double *h, const double *mu, const double *g, double rho, int64_t p, int64_t sp,

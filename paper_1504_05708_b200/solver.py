@@ -266,12 +266,17 @@ class Solver:
         if st not in (L.DUQUAD_OK, L.DUQUAD_EMAXITER):
             L.check(st, self._ctx)
         info = {k: getattr(res, k) for k, _ in L.Result._fields_}
-        m = int(outer) + 1
+        bl = self.b_range[1] - self.b_range[0] if self.batch > 1 else 1
+        m = (int(outer) + 1) * bl
         counts = (C.c_int32 * m)()
         conv = (C.c_int32 * m)()
         L.check(self._lib.duquad_get_inner_counts(self._ctx, counts, conv, m), self._ctx)
         info["inner_counts"] = list(counts)
         info["converged"] = [bool(c) for c in conv]
+        if self.batch > 1:   # per QP: [QP][solve]
+            k1 = int(outer) + 1
+            info["inner_counts"] = [info["inner_counts"][b * k1:(b + 1) * k1] for b in range(bl)]
+            info["converged"] = [info["converged"][b * k1:(b + 1) * k1] for b in range(bl)]
         info["capped"] = st == L.DUQUAD_EMAXITER
         self.last_result = info
         return info

@@ -166,3 +166,28 @@ def test_eps_mode_row_sharded_emulated(torch_cuda, P, n, p):
     xl, xa, lam = (np.concatenate([pt[i] for pt in parts]) for i in range(3))
     info["inner_iters_total"] = sum(info["inner_counts"])
     _check(prob, 1.0, "DFGM", K, kmax, eps_in, sigma_L, L_in, L_d, info, xl, xa, lam)
+
+
+def test_eps_mode_batched_per_qp_decisions(torch_cuda):
+    """Batched eps_in mode: every QP of the batch stops on its own gradient-map test; the oracle
+    replays each QP's counts (iterates to 1e-9) and checks each of its stop decisions."""
+    from types import SimpleNamespace
+    from paper_1504_05708_b200 import Solver
+    B = 9
+    prob = qpgen.mpc_batch(B, seed=5, N=4)                # n = 16, p = 96
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 1.0, 0.1)
+    eps_in, sigma_L, K, kmax = 1e-7, 0.1, 4, 400
+    s = Solver(prob.Q, prob.q.T.copy(), prob.G, prob.g.T.copy(), prob.lb, prob.ub, prob.cone, rho=1.0)
+    s.set_constants(L_in, L_d)
+    info = s.solve_eps("DFGM", K, kmax, eps_in, sigma_L)
+    xl, xa, lam = s.result()
+    s.close()
+    assert info["path"] == 4 and len(info["inner_counts"]) == B
+    assert len({tuple(c) for c in info["inner_counts"]}) > 1      # the QPs stop at different steps
+    for b in range(B):
+        qb = SimpleNamespace(Q=prob.Q, q=prob.q[:, b], G=prob.G, g=prob.g[:, b], lb=prob.lb, ub=prob.ub,
+                             cone=prob.cone)
+        ib = dict(inner_counts=info["inner_counts"][b], converged=info["converged"][b],
+                  inner_iters_total=sum(info["inner_counts"][b]),
+                  capped=not all(info["converged"][b]))
+        _check(qb, 1.0, "DFGM", K, kmax, eps_in, sigma_L, L_in, L_d, ib, xl[b], xa[b], lam[b])
