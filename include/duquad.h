@@ -279,10 +279,13 @@ duquad_status duquad_set_initial(duquad_ctx *ctx, const double *x0, const double
  * (the inexactness (duquad_in) of Theorem 1).  sigma_L > 0 is the caller's lower bound on
  * lambda_min(Q + rho G'G) (e.g. lambda_min(Q)), eps_in > 0 (e.g. from duquad_theory_schedule).
  * The norm is a fixed-order device reduction after each step; converged inner solves skip the
- * remaining steps of their (graph-captured) loop.  Batch 1, any format; row-sharded groups
- * all-reduce the test's sum (one double per inner step), so every rank decides alike.
+ * remaining steps of their (graph-captured) loop.  Any format; row-sharded groups all-reduce
+ * the test's sum (one double per inner step), so every rank decides alike; a batch decides per
+ * QP (stopped QPs are left untouched by the remaining steps, whose kernels exit once every QP
+ * stopped) and reports counts QP-major, [QP][solve].
  * Returns DUQUAD_EMAXITER (result valid) when some inner solve was capped; per-outer step
- * counts via duquad_get_inner_counts.  res->inner_iters_total = steps actually run.
+ * counts via duquad_get_inner_counts.  res->inner_iters_total = steps actually run (summed over
+ * the QPs of a batch).
  */
 duquad_status duquad_solve_eps(duquad_ctx *ctx, int32_t alg, int32_t outer_iters, int32_t inner_max,
                                double eps_in, double sigma_L, duquad_result *res);
