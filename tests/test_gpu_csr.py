@@ -146,3 +146,27 @@ def test_config4_full_size_prefix(torch_cuda, c4):
         g = _gpu(c4, 5.0, alg, 4, 6, L_in, L_d, trace=True, torch=torch_cuda)
         r = O.dfom(c4.Q, c4.q, c4.G, c4.g, c4.lb, c4.ub, c4.cone, 5.0, alg, 4, 6, L_in, L_d, keep_trace=True)
         _check(g, r, trace=True)
+
+
+def test_csr_empty_rows(torch_cuda):
+    """CSR rows without nonzeros (in G and in the stacked [Q;G]) next to regular ones."""
+    import scipy.sparse as sp
+    from paper_1504_05708_b200 import Solver
+    prob = qpgen.sparse_banded_eq(n=3001, p=1201, seed=7)
+    G = prob.G.tolil()
+    for r in (0, 5, 600, 1200):
+        G.rows[r] = []
+        G.data[r] = []
+    G = G.tocsr()
+    g = prob.g.copy()
+    g[[0, 5, 600, 1200]] = 0.0
+    Gd = G.toarray()
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q.toarray(), Gd, 5.0, 0.5)
+    s = Solver(prob.Q, prob.q, G, g, prob.lb, prob.ub, prob.cone, rho=5.0)
+    s.set_constants(L_in, L_d)
+    assert s.solve("DFGM", 3, 4)["path"] == 5
+    got = s.result()
+    s.close()
+    r = O.dfom(prob.Q, prob.q, G, g, prob.lb, prob.ub, prob.cone, 5.0, "DFGM", 3, 4, L_in, L_d)
+    for a, b in zip(got, (r.x_last, r.x_avg, r.lam)):
+        assert relerr(a, b) <= 1e-9, relerr(a, b)

@@ -98,3 +98,21 @@ def test_fused_config2_full_size(torch_cuda):
     r = O.dfom(h["Q"], h["q"], h["G"], h["g"], h["lb"], h["ub"], h["cone"], 1.0, O.DFGM, 2, 3, L_in, L_d)
     assert relerr(xl, r.x_last) <= TOL and relerr(xa, r.x_avg) <= TOL and relerr(lam, r.lam) <= TOL
     s.close()
+
+
+def test_fused_mixed_cones_ragged_infinite_bounds(torch_cuda):
+    """Byte floor on a ragged n = 4103 with alternating equality / inequality rows and a box that is
+    infinite on some coordinates."""
+    from paper_1504_05708_b200 import Solver
+    prob = qpgen.tiny(4103, 1001, seed=21, kind="mixed", shift=0.1)
+    prob.lb[::5] = -np.inf
+    prob.ub[1::7] = np.inf
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 1.0, 0.1)
+    s = Solver(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho=1.0)
+    s.set_constants(L_in, L_d)
+    assert s.solve("DFGM", 2, 3)["path"] == 1
+    got = s.result()
+    s.close()
+    r = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 1.0, "DFGM", 2, 3, L_in, L_d)
+    for g, w in zip(got, (r.x_last, r.x_avg, r.lam)):
+        assert relerr(g, w) <= 1e-9, relerr(g, w)
