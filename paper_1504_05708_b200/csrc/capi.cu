@@ -1142,8 +1142,8 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         }
     }
     if (csr) {   // grid-stride sub-warp SpMV, full occupancy
-        ctx->cfg_a = {ctx->num_sms * 8, 256, 0};
-        ctx->cfg_b = {ctx->num_sms * 8, 256, 0};
+        ctx->cfg_a = {ctx->num_sms * csr_blocks_per_sm(0, ctx->gs_a), 256, 0};   // whole waves
+        ctx->cfg_b = {ctx->num_sms * csr_blocks_per_sm(1, ctx->gs_b), 256, 0};
         CKS(cudaStreamSynchronize(s));
         *out = ctx;
         return DUQUAD_OK;

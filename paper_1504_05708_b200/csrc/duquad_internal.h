@@ -164,6 +164,7 @@ struct LaunchCfg {
 };
 
 // kernels_csr.cu
+int csr_blocks_per_sm(int pass, int gs);
 cudaError_t launch_pass_a_csr(const PassAArgs &a, int mode, const LaunchCfg &cfg, cudaStream_t s);
 cudaError_t launch_pass_b_csr(const PassBArgs &b, int mode, const LaunchCfg &cfg, cudaStream_t s);
 // dst[i] = src[i] - sub + add, i < count

@@ -172,6 +172,13 @@ __global__ void __launch_bounds__(kCsrThreads) k_pass_b_csr(const PassBArgs b) {
     }
 }
 
+template <typename K>
+int occ(K kern) {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kCsrThreads, 0) != cudaSuccess || b < 1) b = 1;
+    return b;
+}
+
 template <int MODE>
 cudaError_t dispatch_a(const PassAArgs &a, const LaunchCfg &cfg, cudaStream_t s) {
     switch (a.gs) {
@@ -236,6 +243,27 @@ __global__ void k_sub_i64_to_i32(const int64_t *src, int64_t count, int64_t sub,
 inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
 }  // namespace
+
+// resident CTAs per SM of the solve-mode pass kernels for group size gs (the grid is sized to whole
+// waves: a grid-stride loop over rows, so a partial last wave would idle SMs)
+int csr_blocks_per_sm(int pass, int gs) {
+    if (pass == 0) {
+        switch (gs) {
+            case 2: return occ(k_pass_a_csr<MODE_SOLVE, 2>);
+            case 4: return occ(k_pass_a_csr<MODE_SOLVE, 4>);
+            case 8: return occ(k_pass_a_csr<MODE_SOLVE, 8>);
+            case 16: return occ(k_pass_a_csr<MODE_SOLVE, 16>);
+            default: return occ(k_pass_a_csr<MODE_SOLVE, 32>);
+        }
+    }
+    switch (gs) {
+        case 2: return occ(k_pass_b_csr<MODE_SOLVE, 2>);
+        case 4: return occ(k_pass_b_csr<MODE_SOLVE, 4>);
+        case 8: return occ(k_pass_b_csr<MODE_SOLVE, 8>);
+        case 16: return occ(k_pass_b_csr<MODE_SOLVE, 16>);
+        default: return occ(k_pass_b_csr<MODE_SOLVE, 32>);
+    }
+}
 
 int csr_group_size(double m) {
     int gs = 2;
