@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define DUQUAD_ABI_VERSION 1
+#define DUQUAD_ABI_VERSION 2   /* 2: options gained eq_precompute, checkpoint, dual_average */
 
 typedef enum {
     DUQUAD_OK = 0,
