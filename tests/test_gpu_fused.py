@@ -116,3 +116,30 @@ def test_fused_mixed_cones_ragged_infinite_bounds(torch_cuda):
     r = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 1.0, "DFGM", 2, 3, L_in, L_d)
     for g, w in zip(got, (r.x_last, r.x_avg, r.lam)):
         assert relerr(g, w) <= 1e-9, relerr(g, w)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_fused_random_shapes_match_two_pass(torch_cuda, seed):
+    """Randomised shapes for the byte floor's partitioning (ragged tile columns, Q pieces, G pairs
+    and column blocks): n in [4096, 8200], p from 0 / a handful of rows to > n / 2, mixed cones --
+    against the two-pass path on the same problem (different summation order: 1e-11)."""
+    from paper_1504_05708_b200 import Solver
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(4096, 8200))
+    p = int([0, 1, 3, int(rng.integers(5, 300)), int(rng.integers(300, n // 2)), int(rng.integers(n // 2, n))][seed])
+    prob = qpgen.tiny(n, max(p, 1), seed=seed, kind="mixed", shift=0.2)
+    if p == 0:
+        prob.G, prob.g, prob.cone = prob.G[:0], prob.g[:0], prob.cone[:0]
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 1.0, 0.2) if p else (
+        float(np.linalg.eigvalsh(prob.Q).max()) * 1.01, 0.0, 0.0)
+    out = []
+    for fused in (True, False):
+        s = Solver(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho=1.0, fused_path=fused,
+                   eq_precompute=False)
+        s.set_constants(L_in, L_d)
+        info = s.solve("DFGM", 2, 3)
+        assert (info["path"] == 1) == fused, (info["path"], fused)
+        out.append(s.result())
+        s.close()
+    for a, b in zip(*out):
+        assert relerr(a, b) <= 1e-11, (n, p, relerr(a, b))
