@@ -156,3 +156,18 @@ def test_several_groups_per_cta(torch_cuda):
     assert out.returncode == 0, out.stderr[-2000:]
     err = float(out.stdout.split("ERR")[-1])
     assert err <= TOL, err
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_random_batched_shapes(torch_cuda, seed):
+    """Randomised batch sizes and horizons for the persistent DMMA kernels: ragged octets, n across
+    the 128-row block boundary, p with ragged 32-column chunks."""
+    rng = np.random.default_rng(300 + seed)
+    B = int(rng.integers(2, 260))
+    N = int([2, 9, 31, 33, 40][seed])                  # n = 4N: 8 ... 160
+    prob = qpgen.mpc_batch(B, seed=seed, N=N)
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 1.0, 0.1)
+    xl, xa, lam, info = _solve(prob, 1.0, "DFGM", 2, 3, L_in, L_d)
+    assert info["path"] == 4
+    r = _oracle(prob, 1.0, O.DFGM, 2, 3, L_in, L_d)
+    assert relerr(xl, r.x_last.T) <= TOL and relerr(xa, r.x_avg.T) <= TOL and relerr(lam, r.lam.T) <= TOL
