@@ -320,6 +320,7 @@ def main():
                          "achieved": ach_a, "peak": peak, "unit": "GB/s", "frac": ach_a / peak,
                          "traffic": traffic, "bytes_per_launch": bytes_a, "ms_per_launch": ms_a,
                          "peak_source": peak_src,
+                         "frac_of_nominal_8tbs": ach_a / 8000.0,   # also vs the nominal ~8 TB/s
                          ("epilogue" if fused else "pass_b"): {
                              "kernel": "k_fused_epi" if fused else "k_pass_b",
                              "achieved": ach_b, "frac": ach_b / peak, "bytes_per_launch": bytes_b,
