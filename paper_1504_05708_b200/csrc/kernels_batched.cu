@@ -17,10 +17,11 @@
 //     stage's "full" mbarrier (cp.async.mbarrier.arrive.noinc);
 //   - 8 math warps (two per SM sub-partition; warp w owns m8 tiles w and w + 8 of the block and
 //     all octets of the group) issue the DMMAs and release the stage on its "empty" mbarrier;
-//   - pass A: the math warps apply the epilogue straight from their accumulators.  Outside the
-//     DFOM step it needs one operand per element, h = mu + rho g (constant within an outer
-//     iteration), which each lane loads at the start of the block, so the load latency hides
-//     under the block's DMMAs;
+//   - pass A: the math warps apply the epilogue themselves.  Outside the DFOM step it needs one
+//     operand per element, h = mu + rho g (constant within an outer iteration); two staging warps
+//     copy the block's h tile into shared memory while the math warps run the block's DMMAs, the
+//     math warps overwrite it in place with qy / w and write it out in 64-byte runs (the DFOM
+//     step itself runs out of line, dual_block);
 //   - pass B (one row block, seven operands per element): the math warps park the C tile in
 //     shared memory and 6 epilogue warps apply it while the math warps run the CTA's next group.
 // The DMMA pipe is the bound: 1 DMMA.8x8x4 per 16 cycles per sub-partition (measured,
