@@ -40,30 +40,27 @@ __device__ __forceinline__ double2 ldg_stream(const double2 *p) {
 }
 
 // Dot product of one matrix row (nv2 double2 entries, 16-byte aligned) with a
-// shared-memory vector; fixed summation order for a given nv2.
+// shared-memory vector; fixed summation order for a given nv2.  Every chunk, the ragged last one
+// included, issues its kUnroll loads together (predicated, zeros past the row end: fma(0, 0, acc)
+// = acc exactly), so a row costs ceil(nv2 / (32 kUnroll)) memory round trips.
 __device__ __forceinline__ double row_dot(const double2 *__restrict__ row,
                                           const double2 *__restrict__ sv, int nv2, int lane) {
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-    int c = lane;
-    for (; c + 32 * (kUnroll - 1) < nv2; c += 32 * kUnroll) {
-        double2 v[kUnroll];
+    for (int c = lane; c - lane < nv2; c += 32 * kUnroll) {
+        double2 v[kUnroll], y[kUnroll];
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) v[u] = ldg_stream(row + c + 32 * u);
+        for (int u = 0; u < kUnroll; ++u) {
+            const bool in = c + 32 * u < nv2;
+            v[u] = in ? ldg_stream(row + c + 32 * u) : make_double2(0.0, 0.0);
+            y[u] = in ? sv[c + 32 * u] : make_double2(0.0, 0.0);
+        }
 #pragma unroll
         for (int u = 0; u < kUnroll; u += 2) {
-            const double2 y0 = sv[c + 32 * u];
-            const double2 y1 = sv[c + 32 * (u + 1)];
-            acc0 = fma(v[u].x, y0.x, acc0);
-            acc1 = fma(v[u].y, y0.y, acc1);
-            acc2 = fma(v[u + 1].x, y1.x, acc2);
-            acc3 = fma(v[u + 1].y, y1.y, acc3);
+            acc0 = fma(v[u].x, y[u].x, acc0);
+            acc1 = fma(v[u].y, y[u].y, acc1);
+            acc2 = fma(v[u + 1].x, y[u + 1].x, acc2);
+            acc3 = fma(v[u + 1].y, y[u + 1].y, acc3);
         }
-    }
-    for (; c < nv2; c += 32) {
-        const double2 v = ldg_stream(row + c);
-        const double2 y0 = sv[c];
-        acc0 = fma(v.x, y0.x, acc0);
-        acc1 = fma(v.y, y0.y, acc1);
     }
     return warp_sum((acc0 + acc1) + (acc2 + acc3));
 }
