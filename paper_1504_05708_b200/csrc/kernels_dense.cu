@@ -29,7 +29,7 @@ namespace dq {
 namespace {
 
 constexpr int kThreads = 512;  // threads per CTA of the pass kernels
-constexpr int kUnroll = 8;     // 16-byte loads in flight per lane per row chunk
+constexpr int kUnroll = 16;    // 16-byte loads in flight per lane per row chunk
 
 __device__ __forceinline__ double2 ldg_stream(const double2 *p) {
     double2 r;
@@ -47,19 +47,18 @@ __device__ __forceinline__ double row_dot(const double2 *__restrict__ row,
                                           const double2 *__restrict__ sv, int nv2, int lane) {
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
     for (int c = lane; c - lane < nv2; c += 32 * kUnroll) {
-        double2 v[kUnroll], y[kUnroll];
+        double2 v[kUnroll];
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            const bool in = c + 32 * u < nv2;
-            v[u] = in ? ldg_stream(row + c + 32 * u) : make_double2(0.0, 0.0);
-            y[u] = in ? sv[c + 32 * u] : make_double2(0.0, 0.0);
-        }
+        for (int u = 0; u < kUnroll; ++u)
+            v[u] = c + 32 * u < nv2 ? ldg_stream(row + c + 32 * u) : make_double2(0.0, 0.0);
 #pragma unroll
         for (int u = 0; u < kUnroll; u += 2) {
-            acc0 = fma(v[u].x, y[u].x, acc0);
-            acc1 = fma(v[u].y, y[u].y, acc1);
-            acc2 = fma(v[u + 1].x, y[u + 1].x, acc2);
-            acc3 = fma(v[u + 1].y, y[u + 1].y, acc3);
+            const double2 y0 = c + 32 * u < nv2 ? sv[c + 32 * u] : make_double2(0.0, 0.0);
+            const double2 y1 = c + 32 * (u + 1) < nv2 ? sv[c + 32 * (u + 1)] : make_double2(0.0, 0.0);
+            acc0 = fma(v[u].x, y0.x, acc0);
+            acc1 = fma(v[u].y, y0.y, acc1);
+            acc2 = fma(v[u + 1].x, y1.x, acc2);
+            acc3 = fma(v[u + 1].y, y1.y, acc3);
         }
     }
     return warp_sum((acc0 + acc1) + (acc2 + acc3));
