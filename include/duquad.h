@@ -31,7 +31,8 @@
 extern "C" {
 #endif
 
-#define DUQUAD_ABI_VERSION 2   /* 2: options gained eq_precompute, checkpoint, dual_average */
+#define DUQUAD_ABI_VERSION 3   /* 2: options gained eq_precompute, checkpoint, dual_average;
+                                  3: nccl_self */
 
 typedef enum {
     DUQUAD_OK = 0,
@@ -166,6 +167,12 @@ typedef struct {
                               Costs one more inner solve (at lam_hat); the single-CTA and
                               persistent kernels defer to the streaming path.  0 (default): the
                               last dual iterate.                                             */
+    int32_t nccl_self;     /* 1 (world_size 1, not batched): run the ROW-SHARDED code path (its
+                              kernels, NCCL all-gathers / reduce-scatter / broadcasts /
+                              all-reduce, their CUDA-graph capture) on a one-rank NCCL
+                              communicator the library creates itself (nccl_id ignored): the
+                              collective call sequence of a P-GPU run, exercised on one GPU.
+                              Results agree with the oracle like any solve.  0 (default)      */
 } duquad_options;
 
 /* Per-solve report. */

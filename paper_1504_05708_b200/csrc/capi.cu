@@ -40,6 +40,7 @@ struct duquad_ctx {
     double rho = 0.0;
     // sharding
     int world = 1, rank = 0;
+    bool sharded = false;    // world > 1, or nccl_self: the row-sharded code path and its collectives
     bool emulated = false;   // P ranks on one device, driven by duquad_solve_emulated
     ncclComm_t comm = nullptr;
     int64_t n_slice = 0, p_slice = 0, r0 = 0, s0 = 0, nloc = 0, ploc = 0;
@@ -215,7 +216,7 @@ struct DevGuard {
 
 // ----------------------------------------------------------- collectives
 duquad_status allgather_vec(duquad_ctx *ctx, double *full) {
-    if (ctx->world == 1 || ctx->emulated) return DUQUAD_OK;
+    if (!ctx->sharded || ctx->emulated) return DUQUAD_OK;
     NK(ncclAllGather(full + ctx->rank * ctx->n_slice, full, (size_t)ctx->n_slice, ncclDouble, ctx->comm,
                      ctx->stream));
     return DUQUAD_OK;
@@ -226,7 +227,7 @@ duquad_status allgather_y(duquad_ctx *ctx) { return allgather_vec(ctx, ctx->y_fu
 // w replica: every rank's G-row slice in global order.  Equal slices: one all-gather; the balanced
 // partition of the row-sharded byte floor: one broadcast per rank inside a group.
 duquad_status allgather_w(duquad_ctx *ctx) {
-    if (ctx->world == 1 || ctx->emulated) return DUQUAD_OK;
+    if (!ctx->sharded || ctx->emulated) return DUQUAD_OK;
     if (!ctx->floor_shard) {
         NK(ncclAllGather(ctx->w_full + ctx->rank * ctx->p_slice, ctx->w_full, (size_t)ctx->p_slice,
                          ncclDouble, ctx->comm, ctx->stream));
@@ -242,7 +243,7 @@ duquad_status allgather_w(duquad_ctx *ctx) {
 }
 
 duquad_status allreduce_sum(duquad_ctx *ctx, double *buf, int count) {
-    if (ctx->world == 1) return DUQUAD_OK;
+    if (!ctx->sharded) return DUQUAD_OK;
     if (ctx->emulated) return fail(ctx, DUQUAD_ESTATE, "not available on emulated ranks (inject constants)");
     NK(ncclAllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
     return DUQUAD_OK;
@@ -332,7 +333,7 @@ duquad_status gather(duquad_ctx *ctx, int b) {
 }
 
 duquad_status gather_impl(duquad_ctx *ctx, int b) {
-    if (b < 0 || ctx->world == 1 || ctx->emulated) return DUQUAD_OK;   // emulated: group driver copies
+    if (b < 0 || !ctx->sharded || ctx->emulated) return DUQUAD_OK;   // emulated: group driver copies
     if (b == G_W) return allgather_w(ctx);
     if (b == G_RS) {
         NK(ncclReduceScatter(ctx->fpart, ctx->rs_out, (size_t)ctx->n_slice, ncclDouble, ncclSum, ctx->comm,
@@ -356,8 +357,8 @@ duquad_status inner_check(duquad_ctx *ctx) {
         return DUQUAD_OK;
     }
     CK(launch_inner_check(ctx->gm_sq, ctx->nloc, ctx->gm_part, ctx->gm_counter, ctx->d_done, ctx->eps_thresh2,
-                          ctx->d_counts, ctx->d_j, ctx->world > 1 ? ctx->gm_tot : nullptr, ctx->stream));
-    ctx->pend_decide = ctx->world > 1;
+                          ctx->d_counts, ctx->d_j, ctx->sharded ? ctx->gm_tot : nullptr, ctx->stream));
+    ctx->pend_decide = ctx->sharded;
     return DUQUAD_OK;
 }
 
@@ -400,7 +401,7 @@ duquad_status outer_phase(duquad_ctx *ctx, const std::vector<double> &beta_in, i
         double *ydst = (y2 ? ctx->y_full2 : ctx->y_full) + ctx->rank * ctx->n_slice;   // this rank's slice
         CK(launch_inner_finish(ctx->x, ydst, ctx->xhat, ctx->nloc, ctx->d_ops, ctx->d_j, ctx->d_done,
                                ctx->d_counts + ctx->counts_cap, ctx->stream));
-        *gb = ctx->world > 1 ? (y2 ? G_Y2 : G_Y) : G_NONE;   // row-sharded: the new y slices to every rank
+        *gb = ctx->sharded ? (y2 ? G_Y2 : G_Y) : G_NONE;   // row-sharded: the new y slices to every rank
         return DUQUAD_OK;
     }
     if (ctx->rho0) {
@@ -469,7 +470,7 @@ duquad_status outer_phase(duquad_ctx *ctx, const std::vector<double> &beta_in, i
             CK(launch_fused_stream(fz, ctx->stream));
             if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 1], ctx->stream));
             if (k == 1 && (st = trace_lam_copy(ctx, j)) != DUQUAD_OK) return st;
-            if (ctx->world > 1) {   // this rank's partial n-vector, then the reduce-scatter over the slices
+            if (ctx->sharded) {   // this rank's partial n-vector, then the reduce-scatter over the slices
                 fz.partial = ctx->fpart;
                 CK(launch_fused_epi(make_b(ctx), make_b(ctx), fz, ctx->stream));
                 *gb = G_RS;
@@ -479,7 +480,7 @@ duquad_status outer_phase(duquad_ctx *ctx, const std::vector<double> &beta_in, i
             b.beta_in = beta_in[k];
             b.last_inner = (k == Kin) && !ctx->eps_mode;
             if (ev) CK(cudaEventRecord((*ev)[4 * (k - 1) + 2], ctx->stream));
-            if (ctx->world > 1) {
+            if (ctx->sharded) {
                 CK(launch_slice_epi(b, b, ctx->rs_out, ctx->stream));
                 *gb = G_Y;
             } else {
@@ -833,6 +834,7 @@ void duquad_default_options(duquad_options *o) {
     o->dual_average = 0;
     o->eq_precompute = 1;
     o->checkpoint = 0;
+    o->nccl_self = 0;
 }
 
 duquad_status duquad_shard_range(int64_t rows, int32_t world, int32_t rank, int64_t *begin,
@@ -958,6 +960,7 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
     // ---- sharding: rows of one QP over the ranks (NCCL), or, batched, whole QPs (no collective)
     ctx->world = batched ? 1 : opt.world_size;
     ctx->rank = batched ? 0 : opt.rank;
+    ctx->sharded = ctx->world > 1 || (opt.nccl_self && !batched);
     ctx->Btot = prob->batch;
     {
         const int64_t bs = (prob->batch + opt.world_size - 1) / opt.world_size;
@@ -971,7 +974,7 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
     // G rows: equal slices, except for the row-sharded byte floor, where rank r's triangle slab of Q
     // (rows r0..r0+nloc, columns >= row) shrinks with r: there the G rows are split so that every
     // rank streams the same number of matrix elements (slab + G rows x n), contiguous and ascending
-    ctx->floor_shard = ctx->world > 1 && !csr && !batched && rho > 0.0 && p > 0 && opt.fused_path &&
+    ctx->floor_shard = ctx->sharded && !csr && !batched && rho > 0.0 && p > 0 && opt.fused_path &&
                        fused_supported(n, round_up(n, 32), prop.sharedMemPerBlockOptin);
     ctx->gs0.assign(ctx->world, 0);
     ctx->gcnt.assign(ctx->world, 0);
@@ -1007,10 +1010,14 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
     ctx->s0 = ctx->gs0[ctx->rank];
     ctx->ploc = ctx->gcnt[ctx->rank];
     ctx->emulated = ctx->world > 1 && opt.emulate_ranks;
-    if (ctx->world > 1 && !ctx->emulated) {
+    if (ctx->sharded && !ctx->emulated) {
         ncclUniqueId id;
-        std::memcpy(&id, opt.nccl_id, sizeof(id));
-        ncclResult_t r = ncclCommInitRank(&ctx->comm, ctx->world, id, ctx->rank);
+        ncclResult_t r = ncclSuccess;
+        if (ctx->world == 1)   // nccl_self: a one-rank communicator of our own
+            r = ncclGetUniqueId(&id);
+        else
+            std::memcpy(&id, opt.nccl_id, sizeof(id));
+        if (r == ncclSuccess) r = ncclCommInitRank(&ctx->comm, ctx->world, id, ctx->rank);
         if (r != ncclSuccess) {
             ctx->err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
             return bail(DUQUAD_ENCCL);
@@ -1168,7 +1175,7 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         ctx->cfg_k3 = {ctx->cfg_b.grid, pass_threads(), smem_a};
         ctx->rho0 = true;
     }
-    if (!batched && !csr && ctx->world == 1 && rho > 0.0 && p > 0 && opt.eq_precompute) {
+    if (!batched && !csr && !ctx->sharded && rho > 0.0 && p > 0 && opt.eq_precompute) {
         // NEXT-3: with every row an equality (K = {0}) the inner gradient is
         // (Q + rho G'G) u + q + G'(mu + rho g): form H once, then the K3 machinery streams H alone.
         bool all_zero = true;
@@ -1210,8 +1217,8 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
     }
     // byte-floor inner step: single GPU, or row-sharded with rho > 0 (each rank streams the upper
     // triangle of its rows and its G rows; the ranks' partial n-vectors are reduce-scattered)
-    const bool shard_floor = ctx->world > 1 && !csr && rho > 0.0 && !ctx->rho0;
-    if (!batched && (ctx->world == 1 || shard_floor) && opt.fused_path &&
+    const bool shard_floor = ctx->sharded && !csr && rho > 0.0 && !ctx->rho0;
+    if (!batched && (!ctx->sharded || shard_floor) && opt.fused_path &&
         fused_supported(n, ctx->ld, prop.sharedMemPerBlockOptin)) {
         const int cg = (!ctx->rho0 && p > 0) ? 2 : 1;   // G role: CTA pairs (148 SMs usable)
         const int nchg = cg > 1 ? fused_nchg(ctx->ld, cg) : 0;
@@ -1260,7 +1267,7 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         fz.Q = ctx->eqh ? ctx->Hq : ctx->A;
         fz.G = ctx->A + ctx->nloc * ctx->ld;
         fz.p = ctx->ploc;
-        if (ctx->world > 1) {
+        if (ctx->sharded) {
             CKS(dalloc(&ctx->fpart, ctx->world * ctx->n_slice));
             CKS(dalloc(&ctx->rs_out, ctx->n_slice));
         }
@@ -1279,7 +1286,7 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         int coop = 0;
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->dev);
         const char *ov = std::getenv("DUQUAD_PERSIST");
-        if (!batched && ctx->world == 1 && opt.persist_path && !ctx->fused && !ctx->rho0 && coop && mbytes <= 100e6 &&
+        if (!batched && !ctx->sharded && opt.persist_path && !ctx->fused && !ctx->rho0 && coop && mbytes <= 100e6 &&
             !(ov && std::atoi(ov) == 0)) {
             ctx->persist_smem = std::max(smem_a, smem_b);
             CKS(configure_persist(ctx->persist_smem));
@@ -1287,7 +1294,7 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
             ctx->persist = true;
         }
     }
-    if (!batched && ctx->world == 1 && opt.small_path) {
+    if (!batched && !ctx->sharded && opt.small_path) {
         // the tables (beta, per-outer scalars) add per-solve bytes: the final check is in duquad_solve
         ctx->small_smem = (size_t)prop.sharedMemPerBlockOptin - 1024;   // minus the static shared memory
         if (small_smem_bytes(n, p, ctx->ld, ctx->ldp, 0, 0) <= ctx->small_smem) {

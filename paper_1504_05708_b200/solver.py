@@ -113,9 +113,10 @@ class Solver:
                  time_passes: bool = False, cone_all: int = L.CONE_NONPOS, small_path: bool = True,
                  rho0_path: bool = True, emulate_ranks: bool = False, fused_path: bool = True,
                  persist_path: bool = False, dual_average: bool = False, eq_precompute: bool = True,
-                 checkpoint: bool = False):
+                 checkpoint: bool = False, nccl_self: bool = False):
         """Dense Q (n x n) and G (p x n), or scipy.sparse matrices (-> CSR path, row a10).
-        dual_average: DGM final dual point from the average of lambda^0..lambda^K."""
+        dual_average: DGM final dual point from the average of lambda^0..lambda^K.
+        nccl_self: world_size 1 on the row-sharded code path over a one-rank NCCL communicator."""
         if hasattr(Q, "tocsr"):
             Qc = Q.tocsr()
             Qc.sort_indices()
@@ -137,7 +138,8 @@ class Solver:
                         world_size=world_size, rank=rank, nccl_id=nccl_id, stream=stream, device=device,
                         time_passes=time_passes, small_path=small_path, rho0_path=rho0_path,
                         emulate_ranks=emulate_ranks, fused_path=fused_path, persist_path=persist_path,
-                        dual_average=dual_average, eq_precompute=eq_precompute, checkpoint=checkpoint))
+                        dual_average=dual_average, eq_precompute=eq_precompute, checkpoint=checkpoint,
+                        nccl_self=nccl_self))
 
     @classmethod
     def csr(cls, n, p, Q_rowptr, Q_col, Q_val, G_rowptr, G_col, G_val, q, g, lb, ub, cone=None,
@@ -202,6 +204,7 @@ class Solver:
         opt.dual_average = int(o.get("dual_average", False))
         opt.eq_precompute = int(o.get("eq_precompute", True))
         opt.checkpoint = int(o.get("checkpoint", False))
+        opt.nccl_self = int(o.get("nccl_self", False))
         ctx = C.c_void_p()
         L.check(lib.duquad_setup(C.byref(ctx), C.byref(prob), float(rho), C.byref(opt)))
         self._ctx = ctx

@@ -36,3 +36,19 @@ for P in (2, 4, 8):
             s.close()
         del ss
         torch.cuda.empty_cache()
+
+# P = 1 on the REAL row-sharded schedule (nccl_self: one-rank NCCL communicator, graph-captured
+# reduce-scatter / all-gathers) next to the plain single-GPU schedule: the schedule's own overhead
+for ns in (True, False):
+    s = Solver(*args, rho=1.0, nccl_self=ns)
+    s.set_constants(L_in, L_d)
+    s.solve("DFGM", 1, 2)
+    torch.cuda.synchronize()
+    K, Kin = 2, 20
+    t0 = time.perf_counter()
+    info = s.solve("DFGM", K, Kin)
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1e3
+    print(json.dumps(dict(P=1, path="byte_floor", nccl_self=ns, path_code=info["path"],
+                          ms_per_step=ms / ((K + 1) * Kin))), flush=True)
+    s.close()
