@@ -168,15 +168,19 @@ s = Solver(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho=1.0,
 s.set_constants(50.0, 1.0)
 info = s.solve("DFGM", 2, 3)
 print("PATH", info["path"], flush=True)
+print("LIP", s.lipschitz(5), "RES", s.residuals(), flush=True)   # w replica + all-reduced dots
 s.close()
 """
 
 
-@pytest.mark.parametrize("n,p,fused,need", [(301, 97, "0", ("AllGather",)),
-                                            (4100, 1500, "1", ("AllGather", "ReduceScatter"))])
+@pytest.mark.parametrize("n,p,fused,need", [(301, 97, "0", ("AllGather", "AllReduce")),
+                                            (4100, 1500, "1", ("AllGather", "ReduceScatter", "Broadcast",
+                                                                        "AllReduce"))])
 def test_collectives_are_really_issued(torch_cuda, n, p, fused, need):
     """NCCL's own log (NCCL_DEBUG_SUBSYS=COLL) shows the collectives the sharded schedule issues:
-    the y / w all-gathers on the two-pass path, the reduce-scatter and y all-gathers on the byte floor."""
+    the y / w all-gathers on the two-pass path; on the byte floor the reduce-scatter, the y
+    all-gathers and (Lanczos / residuals) the grouped broadcasts of the balanced w replica; the
+    all-reduced dot products on both."""
     import os
     import subprocess
     import sys
