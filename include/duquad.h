@@ -407,6 +407,34 @@ duquad_status duquad_set_trace(duquad_ctx *ctx, double *lam_trace, double *u_tra
 duquad_status duquad_residuals(duquad_ctx *ctx, int32_t which, double *F, double *dist,
                                double *lag);
 
+/* Report of duquad_solve_monitored. */
+typedef struct {
+    int64_t outer_done;   /* outer iterations of the returned iterates (a multiple of check_every,
+                             or outer_max)                                                    */
+    int32_t checks;       /* residual checks made                                             */
+    int32_t converged;    /* 1: the stopping test held at outer_done                           */
+    double F, dist, lag;  /* duquad_residuals of the checked iterate at outer_done            */
+} duquad_monitor;
+
+/*
+ * Stopping residuals every T outer iterations (§8(a) a8; the paper's stopping test, P:415-423,
+ * P:1372-1378): runs DFOM in segments of check_every = T outer iterations; after
+ * each segment the checked iterate (which = 0: the last iterate x_last = u_bar(lambda^j), which = 1:
+ * the primal average x_avg) gets duquad_residuals, and the solve stops at the first j with
+ *     |F - F_star| <= eps  and  dist_K(Gx + g) <= eps          (F_star finite), or
+ *     dist_K(Gx + g) <= eps                                     (F_star = NaN: no reference value),
+ * else at j = outer_max.  Segments continue one another through the state checkpoint
+ * (duquad_get_state / set_state semantics: theta, beta_out and the average weights continue), so
+ * the returned iterates (duquad_get_result) are bitwise those of duquad_solve(alg, outer_done,
+ * inner_iters); res is the last segment's report.  Cost per check: the segment's last-iterate
+ * inner solve and one residual pass, 5 doubles to the host.  Fixed inner counts; not with
+ * options.dual_average or batch > 1 (EINVAL).  Afterwards duquad_get_state returns the state at
+ * outer_done; the next plain duquad_solve starts fresh as usual.
+ */
+duquad_status duquad_solve_monitored(duquad_ctx *ctx, int32_t alg, int32_t outer_max, int32_t inner_iters,
+                                     int32_t check_every, int32_t which, double eps, double F_star,
+                                     duquad_monitor *mon, duquad_result *res);
+
 /*
  * Testing entry point for the row-sharded path on ONE device: ctxs[r] (r = 0..P-1) must have
  * been set up with world_size = P, rank = r, emulate_ranks = 1 and the same stream and device.

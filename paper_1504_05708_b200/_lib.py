@@ -59,6 +59,11 @@ class Options(C.Structure):
     ]
 
 
+class Monitor(C.Structure):
+    _fields_ = [("outer_done", C.c_int64), ("checks", C.c_int32), ("converged", C.c_int32),
+                ("F", C.c_double), ("dist", C.c_double), ("lag", C.c_double)]
+
+
 class Result(C.Structure):
     _fields_ = [
         ("outer_iters", C.c_int64), ("inner_iters_total", C.c_int64),
@@ -100,6 +105,8 @@ _SIGS = {
     "duquad_solve": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(Result)]),
     "duquad_get_result": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
     "duquad_set_trace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]),
+    "duquad_solve_monitored": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                         C.c_double, C.c_double, C.POINTER(Monitor), C.POINTER(Result)]),
     "duquad_residuals": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                    C.POINTER(C.c_double)]),
     "duquad_solve_emulated": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int32, C.c_int32]),

@@ -2178,4 +2178,38 @@ duquad_status duquad_residuals(duquad_ctx *ctx, int32_t which, double *F, double
     return DUQUAD_OK;
 }
 
+duquad_status duquad_solve_monitored(duquad_ctx *ctx, int32_t alg, int32_t outer_max, int32_t inner_iters,
+                                     int32_t check_every, int32_t which, double eps, double F_star,
+                                     duquad_monitor *mon, duquad_result *res) {
+    if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
+    if (outer_max < 1 || check_every < 1 || (which != 0 && which != 1) || !(eps > 0) || std::isinf(F_star))
+        return fail(ctx, DUQUAD_EINVAL, "solve_monitored: outer_max, check_every >= 1; which 0/1; eps > 0; F_star finite or NaN");
+    if (ctx->Btot > 1 || ctx->davg)
+        return fail(ctx, DUQUAD_EINVAL, "solve_monitored: single QP, no dual_average");
+    if (ctx->emulated) return fail(ctx, DUQUAD_EINVAL, "solve_monitored: not on emulated ranks");
+    ctx->eps_mode = false;
+    const int32_t ck_opt = ctx->opt.checkpoint;
+    ctx->opt.checkpoint = 1;   // every segment ends with a snapshot the next one continues from
+    duquad_monitor m{};
+    duquad_status st = DUQUAD_OK;
+    int64_t done = 0;
+    while (done < outer_max) {
+        const int32_t K = (int32_t)std::min<int64_t>(check_every, outer_max - done);
+        if (done > 0) ctx->resume = true;   // continue from the previous segment's checkpoint
+        if ((st = solve_body(ctx, alg, K, inner_iters, res)) != DUQUAD_OK) break;
+        done += K;
+        if ((st = duquad_residuals(ctx, which, &m.F, &m.dist, &m.lag)) != DUQUAD_OK) break;
+        ++m.checks;
+        if (m.dist <= eps && (std::isnan(F_star) || std::fabs(m.F - F_star) <= eps)) {
+            m.converged = 1;
+            break;
+        }
+    }
+    ctx->opt.checkpoint = ck_opt;
+    ctx->resume = false;
+    m.outer_done = done;
+    if (mon) *mon = m;
+    return st;
+}
+
 }  // extern "C"

@@ -330,6 +330,22 @@ class Solver:
         L.check(self._lib.duquad_set_state(self._ctx, arrs[0].ptr, arrs[1].ptr, arrs[2].ptr, arrs[3].ptr,
                                            int(state["outer_done"]), float(state["S"]), 0), self._ctx)
 
+    def solve_monitored(self, alg: str = "DFGM", outer_max: int = 1, inner: int = 1, check_every: int = 1,
+                        which: str = "avg", eps: float = 1e-2, F_star: float = float("nan")) -> dict:
+        """DFOM with the paper's stopping test checked every check_every outer iterations
+        (duquad_solve_monitored): stop at the first checked j with |F - F_star| <= eps and
+        dist_K <= eps (dist only if F_star is NaN).  The report adds 'outer_done', 'checks',
+        'converged', 'F', 'dist', 'lag'; result() is bitwise solve(alg, outer_done, inner)'s."""
+        res, mon = L.Result(), L.Monitor()
+        L.check(self._lib.duquad_solve_monitored(self._ctx, _ALGS[alg], int(outer_max), int(inner), int(check_every),
+                                                 0 if which == "last" else 1, float(eps), float(F_star),
+                                                 C.byref(mon), C.byref(res)), self._ctx)
+        info = {k: getattr(res, k) for k, _ in L.Result._fields_}
+        info.update({k: getattr(mon, k) for k, _ in L.Monitor._fields_})
+        info["converged"] = bool(info["converged"])
+        self.last_result = info
+        return info
+
     def residuals(self, which: str = "last"):
         F, d, lag = C.c_double(), C.c_double(), C.c_double()
         L.check(self._lib.duquad_residuals(self._ctx, 0 if which == "last" else 1, C.byref(F), C.byref(d),

@@ -1,0 +1,144 @@
+"""Stopping residuals every T outer iterations (duquad_solve_monitored, -m gpu).
+
+The paper's stopping test: stop at the first checked outer
+iteration j whose checked iterate u (x_last or x_avg) has |F(u) - F*| <= eps and dist_K(Gu + g)
+<= eps.  Checked against the oracle: the oracle's residuals at every checked j (dfom run for j
+outer iterations) decide where the solve must stop; the GPU's returned iterates are bitwise a plain
+solve(j); its reported F / dist match the oracle's at j to 1e-9."""
+import math
+
+import numpy as np
+import pytest
+
+import qpgen
+from oracle import dfom as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def relerr(got, want):
+    got, want = np.asarray(got, float), np.asarray(want, float)
+    return float(np.max(np.abs(got - want)) / (1.0 + np.max(np.abs(want)))) if want.size else 0.0
+
+
+def _oracle_checks(prob, rho, alg, T, jmax, Kin, L_in, L_d, which):
+    """(j, F, dist) of the checked iterate at j = T, 2T, ..., jmax, straight from the oracle."""
+    out = []
+    for j in range(T, jmax + 1, T):
+        r = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho, alg, j, Kin, L_in, L_d)
+        x = r.x_last if which == "last" else r.x_avg
+        out.append((j, O.objective(prob.Q, prob.q, x), float(O.dist_K(prob.G @ x + prob.g, prob.cone))))
+    return out
+
+
+def _eps_at(checks, j, F_star):
+    """A tolerance the oracle's checked iterate meets at outer iteration j (1e-6 above its residual
+    level, so no check sits within rounding of the threshold); never below 1e-10."""
+    lvl = [max(abs(F - F_star) if not math.isnan(F_star) else 0.0, d) for _, F, d in checks]
+    v = lvl[[c[0] for c in checks].index(j)]
+    if v < 1e-10:
+        v = min(x for x in lvl if x >= 1e-10)
+    return v * (1 + 1e-6)
+
+
+def _passes(F, d, eps, F_star, slack):
+    return d <= eps * (1 + slack) and (math.isnan(F_star) or abs(F - F_star) <= eps * (1 + slack))
+
+
+def _run(prob, rho, alg, Kmax, Kin, T, which, eps, F_star, L_in, L_d, **kw):
+    from paper_1504_05708_b200 import Solver
+    s = Solver(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho=rho, **kw)
+    s.set_constants(L_in, L_d)
+    info = s.solve_monitored(alg, Kmax, Kin, T, which, eps, F_star)
+    got = s.result()
+    st = s.get_state()
+    s.close()
+    t = Solver(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho=rho, **kw)
+    t.set_constants(L_in, L_d)
+    t.solve(alg, info["outer_done"], Kin)
+    plain = t.result()
+    t.close()
+    return info, got, plain, st
+
+
+@pytest.mark.parametrize("which", ["last", "avg"])
+@pytest.mark.parametrize("alg", ["DGM", "DFGM"])
+def test_monitored_stops_at_the_oracles_first_pass(torch_cuda, alg, which):
+    prob = qpgen.dense_ineq(50, 25, seed=0)
+    rho, Kin, T, Kmax = 1.0, 10, 4, 120
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, rho, 0.1)
+    ref = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho, "DFGM", 600, 50, L_in, L_d)
+    F_star = O.objective(prob.Q, prob.q, ref.x_last)
+    checks = _oracle_checks(prob, rho, alg, T, Kmax, Kin, L_in, L_d, which)
+    eps = _eps_at(checks, 40, F_star)   # the oracle's residual level at j = 40: the test stops mid-run
+    first = next(j for j, F, d in checks if _passes(F, d, eps, F_star, 0.0))
+    info, got, plain, st = _run(prob, rho, alg, Kmax, Kin, T, which, eps, F_star, L_in, L_d, small_path=False)
+    assert info["converged"] and info["outer_done"] == first and info["checks"] == first // T
+    for a, b in zip(got, plain):
+        assert np.array_equal(a, b)
+    _, F, d = [c for c in checks if c[0] == first][0]
+    assert abs(info["F"] - F) <= TOL * (1 + abs(F)) and abs(info["dist"] - d) <= TOL * (1 + d)
+    assert st["outer_done"] == first
+
+
+def test_monitored_cap_and_dist_only(torch_cuda):
+    """Unreachable eps: every check fails, the solve runs to outer_max (a ragged last segment);
+    F_star = NaN tests dist_K alone."""
+    prob = qpgen.tiny(37, 13, seed=5, kind="mixed", shift=0.2)
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 2.0, 0.2)
+    info, got, plain, _ = _run(prob, 2.0, "DFGM", 11, 6, 4, "last", 1e-15, 0.0, L_in, L_d, small_path=False)
+    assert not info["converged"] and info["outer_done"] == 11 and info["checks"] == 3
+    for a, b in zip(got, plain):
+        assert np.array_equal(a, b)
+    checks = _oracle_checks(prob, 2.0, "DFGM", 5, 30, 6, L_in, L_d, "avg")
+    eps = _eps_at(checks, 15, float("nan"))     # dist of x_avg at j = 15
+    first = next(j for j, F, d in checks if _passes(F, d, eps, float("nan"), 0.0))
+    info, got, plain, _ = _run(prob, 2.0, "DFGM", 30, 6, 5, "avg", eps, float("nan"), L_in, L_d, small_path=False)
+    assert info["converged"] and info["outer_done"] == first
+    for a, b in zip(got, plain):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(nccl_self=True)])
+def test_monitored_byte_floor(torch_cuda, kw):
+    """n >= 4096: the byte-floor path (single GPU, and the row-sharded schedule on real NCCL)."""
+    prob = qpgen.dense_ineq(4096, 2048, seed=1, shift=0.05)
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 1.0, 0.05)
+    checks = _oracle_checks(prob, 1.0, "DFGM", 2, 8, 3, L_in, L_d, "last")
+    eps = _eps_at(checks, 6, float("nan"))
+    first = next(j for j, F, d in checks if _passes(F, d, eps, float("nan"), 0.0))
+    info, got, plain, _ = _run(prob, 1.0, "DFGM", 8, 3, 2, "last", eps, float("nan"), L_in, L_d, **kw)
+    assert info["path"] in (1, 3) and info["converged"] and info["outer_done"] == first
+    r = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 1.0, "DFGM", first, 3, L_in, L_d)
+    for a, b in zip(got, (r.x_last, r.x_avg, r.lam)):
+        assert relerr(a, b) <= TOL
+    if not kw:   # single GPU: bitwise a plain solve(first)
+        for a, b in zip(got, plain):
+            assert np.array_equal(a, b)
+
+
+def test_monitored_rejects_bad_arguments(torch_cuda):
+    from paper_1504_05708_b200 import Solver, DuquadError
+    prob = qpgen.dense_ineq(50, 25, seed=0)
+    s = Solver(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho=1.0)
+    s.set_constants(100.0, 1.0)
+    for args in [(0, 5, 1, "avg", 1e-3), (10, 5, 0, "avg", 1e-3), (10, 5, 2, "avg", 0.0), (10, 5, 2, "avg", -1.0)]:
+        with pytest.raises(DuquadError):
+            s.solve_monitored("DFGM", args[0], args[1], args[2], args[3], args[4])
+    with pytest.raises(DuquadError):
+        s.solve_monitored("DFGM", 10, 5, 2, "avg", 1e-3, float("inf"))
+    s.close()
+    d = Solver(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho=1.0, dual_average=True)
+    d.set_constants(100.0, 1.0)
+    with pytest.raises(DuquadError):
+        d.solve_monitored("DGM", 10, 5, 2, "avg", 1e-3)
+    d.close()
