@@ -409,31 +409,42 @@ duquad_status duquad_residuals(duquad_ctx *ctx, int32_t which, double *F, double
 
 /* Report of duquad_solve_monitored. */
 typedef struct {
-    int64_t outer_done;   /* outer iterations of the returned iterates (a multiple of check_every,
-                             or outer_max)                                                    */
-    int32_t checks;       /* residual checks made                                             */
-    int32_t converged;    /* 1: the stopping test held at outer_done                           */
-    double F, dist, lag;  /* duquad_residuals of the checked iterate at outer_done            */
+    int64_t outer_done;    /* outer iterations of the returned iterates (a multiple of check_every,
+                              or outer_max)                                                   */
+    int64_t inner_total;   /* inner iterations executed, all segments (incl. their last-iterate
+                              solves)                                                          */
+    int64_t passes_total;  /* matrix passes executed, all segments                            */
+    int32_t checks;        /* residual checks made                                            */
+    int32_t converged;     /* 1: the stopping test held at outer_done                          */
+    double F, dist;        /* F and dist_K of the checked iterate at outer_done                */
+    double dual;           /* L_rho(x_last, lambda^j) = the inexact dual value d_bar(lambda^j)  */
 } duquad_monitor;
 
 /*
  * Stopping residuals every T outer iterations (§8(a) a8; the paper's stopping test, P:415-423,
- * P:1372-1378): runs DFOM in segments of check_every = T outer iterations; after
- * each segment the checked iterate (which = 0: the last iterate x_last = u_bar(lambda^j), which = 1:
- * the primal average x_avg) gets duquad_residuals, and the solve stops at the first j with
- *     |F - F_star| <= eps  and  dist_K(Gx + g) <= eps          (F_star finite), or
- *     dist_K(Gx + g) <= eps                                     (F_star = NaN: no reference value),
+ * P:1372-1378): runs DFOM in segments of check_every = T outer iterations.  After
+ * each segment, duquad_residuals of x_last = u_bar(lambda^j) and of x_avg; the checked iterate
+ * is which = 0 (x_last) or 1 (x_avg), and the solve stops at the first checked j with
+ *     dist_K(Gx + g) <= eps  and  |F(x) - F_star| <= eps                     (F_star finite:
+ *                                                     the paper's test with a known optimum), or
+ *     dist_K(Gx + g) <= eps  and  |F(x) - d_bar(lambda^j)| <= eps (1 + |F(x)|)   (F_star = NaN:
+ *         no reference value; d_bar(lambda^j) = L_rho(u_bar(lambda^j), lambda^j), the inexact dual
+ *         value, so this is a primal-dual gap test -- reading c24),
  * else at j = outer_max.  Segments continue one another through the state checkpoint
  * (duquad_get_state / set_state semantics: theta, beta_out and the average weights continue), so
  * the returned iterates (duquad_get_result) are bitwise those of duquad_solve(alg, outer_done,
- * inner_iters); res is the last segment's report.  Cost per check: the segment's last-iterate
- * inner solve and one residual pass, 5 doubles to the host.  Fixed inner counts; not with
- * options.dual_average or batch > 1 (EINVAL).  Afterwards duquad_get_state returns the state at
- * outer_done; the next plain duquad_solve starts fresh as usual.
+ * inner_iters); res (may be NULL) is the last segment's report.  Cost per check: the segment's
+ * last-iterate inner solve and two residual passes, 10 doubles to the host.
+ * history (NULL, or 8 * ceil(outer_max / check_every) doubles, caller-owned): one row per check,
+ *     j, d_bar(lambda^j), F(x_last), F(x_avg), dist(x_last), dist(x_avg), inner iterations so far,
+ *     matrix passes so far  -- the SPEC trace fields (k, dual_val, f_last, f_avg, infeas_last,
+ *     infeas_avg, inner_iters, cum_matvecs).
+ * Fixed inner counts; single QP (batch 1); not with options.dual_average (EINVAL).  Afterwards
+ * duquad_get_state returns the state at outer_done; the next plain duquad_solve starts fresh.
  */
 duquad_status duquad_solve_monitored(duquad_ctx *ctx, int32_t alg, int32_t outer_max, int32_t inner_iters,
                                      int32_t check_every, int32_t which, double eps, double F_star,
-                                     duquad_monitor *mon, duquad_result *res);
+                                     duquad_monitor *mon, double *history, duquad_result *res);
 
 /*
  * Testing entry point for the row-sharded path on ONE device: ctxs[r] (r = 0..P-1) must have

@@ -60,8 +60,9 @@ class Options(C.Structure):
 
 
 class Monitor(C.Structure):
-    _fields_ = [("outer_done", C.c_int64), ("checks", C.c_int32), ("converged", C.c_int32),
-                ("F", C.c_double), ("dist", C.c_double), ("lag", C.c_double)]
+    _fields_ = [("outer_done", C.c_int64), ("inner_total", C.c_int64), ("passes_total", C.c_int64),
+                ("checks", C.c_int32), ("converged", C.c_int32), ("F", C.c_double), ("dist", C.c_double),
+                ("dual", C.c_double)]
 
 
 class Result(C.Structure):
@@ -106,7 +107,8 @@ _SIGS = {
     "duquad_get_result": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
     "duquad_set_trace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]),
     "duquad_solve_monitored": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
-                                         C.c_double, C.c_double, C.POINTER(Monitor), C.POINTER(Result)]),
+                                         C.c_double, C.c_double, C.POINTER(Monitor), C.POINTER(C.c_double),
+                                         C.POINTER(Result)]),
     "duquad_residuals": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                    C.POINTER(C.c_double)]),
     "duquad_solve_emulated": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int32, C.c_int32]),

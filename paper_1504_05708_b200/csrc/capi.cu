@@ -2180,7 +2180,7 @@ duquad_status duquad_residuals(duquad_ctx *ctx, int32_t which, double *F, double
 
 duquad_status duquad_solve_monitored(duquad_ctx *ctx, int32_t alg, int32_t outer_max, int32_t inner_iters,
                                      int32_t check_every, int32_t which, double eps, double F_star,
-                                     duquad_monitor *mon, duquad_result *res) {
+                                     duquad_monitor *mon, double *history, duquad_result *res) {
     if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
     if (outer_max < 1 || check_every < 1 || (which != 0 && which != 1) || !(eps > 0) || std::isinf(F_star))
         return fail(ctx, DUQUAD_EINVAL, "solve_monitored: outer_max, check_every >= 1; which 0/1; eps > 0; F_star finite or NaN");
@@ -2191,16 +2191,38 @@ duquad_status duquad_solve_monitored(duquad_ctx *ctx, int32_t alg, int32_t outer
     const int32_t ck_opt = ctx->opt.checkpoint;
     ctx->opt.checkpoint = 1;   // every segment ends with a snapshot the next one continues from
     duquad_monitor m{};
+    duquad_result seg{};
     duquad_status st = DUQUAD_OK;
     int64_t done = 0;
     while (done < outer_max) {
         const int32_t K = (int32_t)std::min<int64_t>(check_every, outer_max - done);
         if (done > 0) ctx->resume = true;   // continue from the previous segment's checkpoint
-        if ((st = solve_body(ctx, alg, K, inner_iters, res)) != DUQUAD_OK) break;
+        if ((st = solve_body(ctx, alg, K, inner_iters, &seg)) != DUQUAD_OK) break;
         done += K;
-        if ((st = duquad_residuals(ctx, which, &m.F, &m.dist, &m.lag)) != DUQUAD_OK) break;
+        m.inner_total += seg.inner_iters_total;
+        m.passes_total += seg.matrix_passes;
+        // residuals of both iterates; lag of x_last = u_bar(lambda^j) is the inexact dual value
+        double F[2], d[2], lg[2];
+        if ((st = duquad_residuals(ctx, 0, &F[0], &d[0], &lg[0])) != DUQUAD_OK) break;
+        if ((st = duquad_residuals(ctx, 1, &F[1], &d[1], &lg[1])) != DUQUAD_OK) break;
+        m.F = F[which];
+        m.dist = d[which];
+        m.dual = lg[0];
+        if (history) {
+            double *h = history + 8 * (int64_t)m.checks;
+            h[0] = (double)(ctx->ck_j);
+            h[1] = lg[0];
+            h[2] = F[0];
+            h[3] = F[1];
+            h[4] = d[0];
+            h[5] = d[1];
+            h[6] = (double)m.inner_total;
+            h[7] = (double)m.passes_total;
+        }
         ++m.checks;
-        if (m.dist <= eps && (std::isnan(F_star) || std::fabs(m.F - F_star) <= eps)) {
+        const bool obj_ok = std::isnan(F_star) ? std::fabs(m.F - m.dual) <= eps * (1.0 + std::fabs(m.F))
+                                               : std::fabs(m.F - F_star) <= eps;
+        if (m.dist <= eps && obj_ok) {
             m.converged = 1;
             break;
         }
@@ -2209,6 +2231,7 @@ duquad_status duquad_solve_monitored(duquad_ctx *ctx, int32_t alg, int32_t outer
     ctx->resume = false;
     m.outer_done = done;
     if (mon) *mon = m;
+    if (res) *res = seg;
     return st;
 }
 

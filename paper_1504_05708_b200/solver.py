@@ -330,21 +330,37 @@ class Solver:
         L.check(self._lib.duquad_set_state(self._ctx, arrs[0].ptr, arrs[1].ptr, arrs[2].ptr, arrs[3].ptr,
                                            int(state["outer_done"]), float(state["S"]), 0), self._ctx)
 
+    TRACE_FIELDS = ("k", "dual_val", "f_last", "f_avg", "infeas_last", "infeas_avg", "inner_iters", "cum_matvecs")
+
     def solve_monitored(self, alg: str = "DFGM", outer_max: int = 1, inner: int = 1, check_every: int = 1,
                         which: str = "avg", eps: float = 1e-2, F_star: float = float("nan")) -> dict:
-        """DFOM with the paper's stopping test checked every check_every outer iterations
-        (duquad_solve_monitored): stop at the first checked j with |F - F_star| <= eps and
-        dist_K <= eps (dist only if F_star is NaN).  The report adds 'outer_done', 'checks',
-        'converged', 'F', 'dist', 'lag'; result() is bitwise solve(alg, outer_done, inner)'s."""
+        """DFOM with the stopping test checked every check_every outer iterations
+        (duquad_solve_monitored): stop at the first checked j with dist_K <= eps and
+        |F - F_star| <= eps, or (F_star NaN) |F - d_bar(lambda^j)| <= eps (1 + |F|).  The report
+        adds the duquad_monitor fields and 'history' (one dict per check, TRACE_FIELDS);
+        result() is bitwise solve(alg, outer_done, inner)'s."""
         res, mon = L.Result(), L.Monitor()
+        cap = -(-int(outer_max) // max(int(check_every), 1))
+        hist = (C.c_double * (8 * max(cap, 1)))()
         L.check(self._lib.duquad_solve_monitored(self._ctx, _ALGS[alg], int(outer_max), int(inner), int(check_every),
                                                  0 if which == "last" else 1, float(eps), float(F_star),
-                                                 C.byref(mon), C.byref(res)), self._ctx)
+                                                 C.byref(mon), hist, C.byref(res)), self._ctx)
         info = {k: getattr(res, k) for k, _ in L.Result._fields_}
         info.update({k: getattr(mon, k) for k, _ in L.Monitor._fields_})
         info["converged"] = bool(info["converged"])
+        h = np.frombuffer(hist, dtype=np.float64).reshape(-1, 8)[:info["checks"]]
+        info["history"] = [dict(zip(self.TRACE_FIELDS, (int(r[0]), *map(float, r[1:6]), int(r[6]), int(r[7]))))
+                           for r in h]
         self.last_result = info
         return info
+
+    @classmethod
+    def write_trace_csv(cls, path, history):
+        """The per-check history of solve_monitored as CSV (SPEC trace export header)."""
+        with open(path, "w") as f:
+            f.write(",".join(cls.TRACE_FIELDS) + "\n")
+            for r in history:
+                f.write(",".join(repr(r[k]) for k in cls.TRACE_FIELDS) + "\n")
 
     def residuals(self, which: str = "last"):
         F, d, lag = C.c_double(), C.c_double(), C.c_double()
