@@ -517,17 +517,16 @@ __global__ void __launch_bounds__(kEpiCols *kEpiSlices) k_fused_epi(const PassBA
             }
             return f.ws_g + (int64_t)(t - nrow - nqc) * f.ld + j;
         };
-        // eight list entries in flight per thread, added in list order (the same sum, bit for bit)
-        constexpr int U = 8;
-        int t = sl;
-        for (; t + (U - 1) * kEpiSlices < len; t += U * kEpiSlices) {
+        // sixteen list entries in flight per thread, the ragged last batch included (predicated,
+        // zeros past the end: s + 0 = s), added in list order (the same sum, bit for bit)
+        constexpr int U = 16;
+        for (int t = sl; t < len; t += U * kEpiSlices) {
             double v[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) v[u] = __ldcg(at(t + u * kEpiSlices));
+            for (int u = 0; u < U; ++u) v[u] = t + u * kEpiSlices < len ? __ldcg(at(t + u * kEpiSlices)) : 0.0;
 #pragma unroll
             for (int u = 0; u < U; ++u) s += v[u];
         }
-        for (; t < len; t += kEpiSlices) s += __ldcg(at(t));
     }
     part[sl][cl] = s;
     __syncthreads();
