@@ -1444,6 +1444,10 @@ static duquad_status solve_prepare(duquad_ctx *ctx, int alg, int K, int Kin, std
         if (nx > 0) {
             CK(cudaMemcpyAsync(X, ctx->ck_x, nx * sizeof(double), d2d, s));
             CK(cudaMemcpyAsync(Y, ctx->ck_x, nx * sizeof(double), d2d, s));
+            // the rho = 0 / EQ_H paths' DFOM step reads y from the replica the previous inner solve
+            // finished in, Y[K_in % 2]: both replicas start at u_bar^{j0}
+            if (!bt && ctx->y_full2)
+                CK(cudaMemcpyAsync(ctx->y_full2 + ctx->rank * ctx->n_slice, ctx->ck_x, nx * sizeof(double), d2d, s));
             CK(cudaMemcpyAsync(XH, ctx->ck_xh, nx * sizeof(double), d2d, s));
         }
         if (nl > 0) {
@@ -1775,6 +1779,7 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
     }
     duquad_status st;
     if ((st = allgather_y(ctx)) != DUQUAD_OK) return st;
+    if (ctx->resumed && ctx->y_full2 && (st = allgather_vec(ctx, ctx->y_full2)) != DUQUAD_OK) return st;
     if (ctx->small && !ctx->eps_mode && !ctx->davg && !ctx->resumed && !ctx->opt.checkpoint &&
         small_smem_bytes(ctx->n, ctx->p, ctx->ld, ctx->ldp, K, Kin) <= ctx->small_smem) {   // whole solve in one CTA (K4)
         if (ctx->beta_cap < Kin + 1) {
@@ -2090,6 +2095,7 @@ static duquad_status solve_emulated_impl(duquad_ctx **ctxs, int32_t P, int32_t a
     for (int r = 0; r < P; ++r)
         if ((st = solve_prepare(ctxs[r], alg, K, Kin, beta_in)) != DUQUAD_OK) return st;
     if ((st = group_gather(ctxs, P, G_Y)) != DUQUAD_OK) return st;
+    if (ctx->resumed && ctx->y_full2 && (st = group_gather(ctxs, P, G_Y2)) != DUQUAD_OK) return st;
     for (int j = 1; j <= K + 1 + (ctx->davg ? 1 : 0); ++j) {
         if (j == K + 1)
             for (int r = 0; r < P; ++r)

@@ -173,3 +173,29 @@ def test_monitored_rejects_bad_arguments(torch_cuda):
     with pytest.raises(DuquadError):
         d.solve_monitored("DGM", 10, 5, 2, "avg", 1e-3)
     d.close()
+
+
+@pytest.mark.parametrize("case", ["csr", "rho0", "eq_h"])
+def test_monitored_other_paths(torch_cuda, case):
+    """The CSR, rho = 0 (K3) and equality-H paths: stop where the oracle's checks say, iterates bitwise
+    a plain solve(j), history rows equal to the oracle's."""
+    if case == "csr":
+        prob, rho, lmin, kw = qpgen.sparse_banded_eq(n=3001, p=1201, seed=4), 5.0, 0.5, {}
+        Qd, Gd = prob.Q.toarray(), prob.G.toarray()
+    elif case == "rho0":
+        prob, rho, lmin, kw = qpgen.dense_ineq(600, 300, seed=2, shift=0.1), 0.0, 0.1, dict(small_path=False)
+        Qd, Gd = prob.Q, prob.G
+    else:
+        prob, rho, lmin, kw = qpgen.tiny(500, 150, seed=14, kind="eq"), 1.0, 0.2, dict(small_path=False)
+        Qd, Gd = prob.Q, prob.G
+    L_in, L_d, _ = O.lipschitz_constants(Qd, Gd, rho, lmin)
+    T, Kmax, Kin = 2, 12, 5
+    checks = _oracle_checks(prob, rho, "DFGM", T, Kmax, Kin, L_in, L_d)
+    eps = _eps_at(checks, 8, "avg", float("nan"))
+    first = _first(checks, "avg", eps, float("nan"))
+    info, got, plain, _ = _run(prob, rho, "DFGM", Kmax, Kin, T, "avg", eps, float("nan"), L_in, L_d, **kw)
+    assert info["path"] == {"csr": 5, "rho0": 2, "eq_h": 8}[case], info["path"]
+    assert info["converged"] and info["outer_done"] == first
+    for a, b in zip(got, plain):
+        assert np.array_equal(a, b)
+    _check_history(info, checks, Kin)

@@ -79,6 +79,50 @@ def test_resume_byte_floor_rho0_eq_h_csr(torch_cuda):
                            lmin=0.5)["path"] == 5
 
 
+@pytest.mark.parametrize("fresh", [False, True])
+def test_resume_odd_inner_count(torch_cuda, fresh):
+    """Odd K_in on the paths that ping-pong y between two replicas (rho = 0 K3, its Q-only byte floor,
+    EQ_H): the DFOM step after a resume reads the replica the previous inner solve finished in,
+    Y[K_in % 2], so both replicas must restart at u_bar^{j0} (regression: only Y[0] was)."""
+    assert _resume_bitwise(qpgen.dense_ineq(600, 300, seed=2), 0.0, "DFGM", 2, 3, 5, lmin=0.1,
+                           small_path=False, fresh=fresh)["path"] == 2
+    assert _resume_bitwise(qpgen.tiny(500, 150, seed=14, kind="eq"), 1.0, "DFGM", 2, 3, 3,
+                           small_path=False, fresh=fresh)["path"] == 8
+    assert _resume_bitwise(qpgen.dense_ineq(4096, 2048, seed=1, shift=0.05), 0.0, "DFGM", 1, 2, 3,
+                           lmin=0.05, fresh=fresh)["path"] == 3
+
+
+def test_resume_odd_inner_count_sharded_rho0(torch_cuda):
+    """The same on 3 emulated row-sharded ranks at rho = 0: the second replica is re-gathered."""
+    from paper_1504_05708_b200 import Solver, solve_emulated
+    import torch
+    prob = qpgen.dense_ineq(301, 97, seed=2, shift=0.1)
+    L = O.lipschitz_constants(prob.Q, prob.G, 0.0, 0.1)[:2]
+    st = torch.cuda.Stream()
+
+    def group():
+        ss = [Solver(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho=0.0, world_size=3, rank=r,
+                     emulate_ranks=True, stream=st.cuda_stream, small_path=False, checkpoint=True) for r in range(3)]
+        for s in ss:
+            s.set_constants(*L)
+        return ss
+
+    a = group()
+    solve_emulated(a, "DFGM", 5, 5)
+    full = [np.concatenate([s.result()[i] for s in a]) for i in range(3)]
+    solve_emulated(a, "DFGM", 2, 5)
+    states = [s.get_state() for s in a]
+    b = group()
+    for s, stt in zip(b, states):
+        s.set_state(stt)
+    solve_emulated(b, "DFGM", 3, 5)
+    part = [np.concatenate([s.result()[i] for s in b]) for i in range(3)]
+    for s in a + b:
+        s.close()
+    for x, y in zip(full, part):
+        assert np.array_equal(x, y), np.max(np.abs(x - y))
+
+
 def test_resume_batched(torch_cuda):
     _resume_bitwise(qpgen.mpc_batch(37, seed=0), 1.0, "DFGM", 2, 3, 5, lmin=0.1, batched=True)
 
