@@ -132,3 +132,13 @@ def test_warm_start_sharded_emulated(torch_cuda):
     r = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 1.0, "DFGM", 5, 6, L_in, L_d,
                x0=x0, lam0=lam0)
     assert relerr(xl, r.x_last) <= TOL and relerr(lam, r.lam) <= TOL
+
+
+@pytest.mark.parametrize("Kin", [5, 7])
+def test_warm_start_ping_pong_paths_odd_inner_count(torch_cuda, Kin):
+    """rho = 0 (K3) and EQ_H ping-pong y between two replicas; odd K_in makes the DFOM step read
+    the second one: cold and warm starts must still match the oracle."""
+    info = _check(torch_cuda, qpgen.dense_ineq(600, 300, seed=2), 0.0, "DFGM", 4, Kin, small_path=False)
+    assert info["path"] == 2
+    info = _check(torch_cuda, qpgen.tiny(500, 150, seed=14, kind="eq"), 1.0, "DGM", 3, Kin, small_path=False)
+    assert info["path"] == 8
