@@ -191,3 +191,14 @@ def test_eps_mode_batched_per_qp_decisions(torch_cuda):
                   inner_iters_total=sum(info["inner_counts"][b]),
                   capped=not all(info["converged"][b]))
         _check(qb, 1.0, "DFGM", K, kmax, eps_in, sigma_L, L_in, L_d, ib, xl[b], xa[b], lam[b])
+
+
+@pytest.mark.parametrize("kmax", [199, 201])
+def test_eps_mode_ping_pong_paths_odd_cap(torch_cuda, kmax):
+    """rho = 0 (K3) with an odd inner cap: the converged solves end in either y replica, and the
+    next DFOM step must read the one holding u_bar^j (the finish kernel's target)."""
+    prob = qpgen.dense_ineq(600, 300, seed=2, shift=0.1)
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 0.0, 0.1)
+    info, xl, xa, lam = _run(prob, 0.0, "DFGM", 6, kmax, 1e-7, 0.1, L_in, L_d, small_path=False)
+    assert info["path"] == 2
+    _check(prob, 0.0, "DFGM", 6, kmax, 1e-7, 0.1, L_in, L_d, info, xl, xa, lam)
