@@ -63,9 +63,11 @@ typedef struct duquad_ctx duquad_ctx;
 
 /*
  * Problem data.  Single QP (batch == 1):
- *   Q   n x n, symmetric positive (semi)definite; dense Q is checked at
- *       setup on a single GPU (EINVAL unless |Q_ij - Q_ji| <= 1e-12 (|Q_ij| + |Q_ji|)), because
- *       the byte-floor and small-QP kernels read Q through its symmetry;
+ *   Q   n x n, symmetric positive (semi)definite; Q's symmetry is checked
+ *       at setup on every path and rank count (EINVAL unless |Q_ij - Q_ji| <= 1e-12 (|Q_ij| +
+ *       |Q_ji|)), because the byte-floor and small-QP kernels read Q through its symmetry (a
+ *       row-sharded rank checks the caller's full Q; CSR: Q and its transpose must have the same
+ *       pattern, i.e. both triangles stored, and the same values);
  *   G   p x n;  q n;  g p;  lb, ub n (entries may be -INFINITY / +INFINITY);
  *   cone p tags (DUQUAD_CONE_*), or NULL meaning every row is cone_all.
  * Batched (batch = B > 1, dense only; north_star (c)): Q and G are shared,
@@ -245,10 +247,16 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
 /*
  * Lipschitz constants on the device (north_star (a)); Lanczos with
  * `iters` steps for lambda_max(Q + rho G'G) (l_mode 0) or lambda_max(Q)
- * (l_mode 1) and for ||G||^2 = lambda_max(G'G):
- *   L_in = (1 + safety) * estimate,  L_d = ||G||^2 / (lambda_min_lb + rho ||G||^2).
- * Stores them in the context (as duquad_set_constants would) and returns
- * them in the host scalars (any may be NULL).
+ * (l_mode 1) and for ||G||^2 = lambda_max(G'G).  Lanczos returns Ritz values,
+ * which never exceed the true eigenvalues, so `safety` >= 0 inflates both
+ * estimates (recommended 1e-6, SPEC.md:76's delta_safe; the Python binding's
+ * default) and both constants come out as over-estimates:
+ *   L_in = (1 + safety) * estimate,
+ *   L_d  = nG2' / (lambda_min_lb + rho nG2'),  nG2' = (1 + safety) ||G||^2
+ * (Eq. Ld; L_d is increasing in ||G||^2).  Stores them in the
+ * context (as duquad_set_constants would) and returns them in the host scalars
+ * (any may be NULL); *normG2 is the raw (uninflated) estimate.
+ * DUQUAD_EINVAL: safety < 0, or rho == 0 with lambda_min_lb <= 0 and p > 0.
  */
 duquad_status duquad_lipschitz(duquad_ctx *ctx, int32_t iters, double safety,
                                double *L_in, double *L_d, double *normG2);
@@ -275,6 +283,8 @@ duquad_status duquad_solve(duquad_ctx *ctx, int32_t alg, int32_t outer_iters,
  * passed to duquad_setup; each context takes its QPs / row slices.  Host or device memory per
  * `on_device`.  NULL for either resets that one to the default.  Stays in effect until reset.
  */
+/* With on_device = 1 the call first synchronizes the device (cudaDeviceSynchronize), so buffers
+ * still being written on any stream (e.g. torch's current stream) are complete before the copy. */
 duquad_status duquad_set_initial(duquad_ctx *ctx, const double *x0, const double *lambda0, int32_t on_device);
 
 /*
@@ -316,19 +326,22 @@ typedef struct {
     int64_t k_total;    /* Theorem in:th_last, PAPER.md:1162-1169 (floor):
                            24 ||G|| D_U R_d / eps (sigma_L = 0),
                            16 ||G|| R_d / sqrt(sigma_L eps) log(8 ||G|| D_U R_d / eps) (sigma_L > 0) */
-    int32_t case_id;    /* 1 if lambda_min(Q) > 0 (rho = 0), 2 otherwise (rho > 0) */
+    int32_t case_id;    /* 1 (Q > 0, rho = 0) iff lambda_min(Q) > tau_pd =
+                           1e-7 max(1, lambda_max(Q)) (SPEC.md:186's threshold), else 2 (rho > 0) */
     int32_t reserved;
 } duquad_schedule;
 
 /*
  * Fills `out` from the algorithm (DUQUAD_DGM/DFGM), the target accuracy eps > 0, the dual
  * radius R_d = ||lambda*|| > 0 (an estimate), L_d > 0, the inner Lipschitz constant L_in > 0,
- * sigma_L >= 0, the box diameter D_U > 0, ||G|| >= 0 and a lower bound lambda_min_Q >= 0.
+ * sigma_L >= 0, the box diameter D_U > 0, ||G|| >= 0, an estimate lambda_min_Q >= 0 of
+ * lambda_min(Q) and lambda_max_Q >= 0 of lambda_max(Q) (0 if unknown: tau_pd = 1e-7).
+ * Counts are clamped to [0, 2^62]; k_total's log argument to >= 1 (so ||G|| = 0 gives 0).
  * DUQUAD_EINVAL on a non-finite or out-of-range argument.  Pure host arithmetic.
  */
 duquad_status duquad_theory_schedule(int32_t alg, double eps, double R_d, double L_d, double L_in,
                                      double sigma_L, double D_U, double normG, double lambda_min_Q,
-                                     duquad_schedule *out);
+                                     double lambda_max_Q, duquad_schedule *out);
 
 /*
  * State export / resume (the DFOM state of PAPER.md:564-589 after outer iteration
@@ -341,8 +354,9 @@ duquad_status duquad_theory_schedule(int32_t alg, double eps, double R_d, double
  *     j+1 .. j+K (theta, beta_out and the average weights continue; warm start ignored), so
  *     solve(K1) + get_state + set_state + solve(K2) equals solve(K1 + K2) bit for bit.
  * Buffers are host or device per on_device (layout as duquad_get_result: a row-sharded rank
- * exports and imports its own slices); fixed inner counts, no dual_average.  DUQUAD_EINVAL on
- * bad arguments.
+ * exports and imports its own slices); fixed inner counts, no dual_average.  With on_device = 1,
+ * set_state first synchronizes the device (inputs in flight on another stream are complete) and
+ * get_state returns after its copies completed.  DUQUAD_EINVAL on bad arguments.
  */
 duquad_status duquad_get_state(duquad_ctx *ctx, double *x, double *mu, double *lam_prev, double *x_avg,
                                int64_t *outer_done, double *S, int32_t on_device);

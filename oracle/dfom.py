@@ -341,7 +341,7 @@ def dfom(Q, q, G, g, lb, ub, cone, rho: float, alg: str, outer: int, inner,
 
 # ------------------------------------------------------------ theory schedule (NEXT-1)
 def theory_schedule(alg: str, eps: float, R_d: float, L_d: float, L_in: float, sigma_L: float,
-                    D_U: float, normG: float, lambda_min_Q: float = 0.0) -> dict:
+                    D_U: float, normG: float, lambda_min_Q: float = 0.0, lambda_max_Q: float = 0.0) -> dict:
     """DuQuad's parameter choices for a target accuracy eps.
 
     eps_in, k_out: Eq. (choose_ein), P:641-652 (each term of Theorem 1's bound
@@ -349,8 +349,10 @@ def theory_schedule(alg: str, eps: float, R_d: float, L_d: float, L_in: float, s
     k_in: proof of Theorem in:th_last, P:1168-1173 (Lemma 1 (bound_gen_dfg1), P:386-391,
       with R_phi <= D_U), rounded up.
     rho_star = 8 R_d^2 / eps.
-    k_total: Theorem in:th_last, P:1162-1169 (floor, as printed).
-    case: P:252-258, 1 if lambda_min(Q) > 0 (rho = 0), else 2 (rho > 0).
+    k_total: Theorem in:th_last, P:1162-1169 (floor, as printed); the log's argument is taken as
+      at least 1 (||G|| = 0 couples nothing: 0 outer work, not 0 * log 0).
+    case: P:252-258, 1 if Q > 0 (rho = 0), else 2 (rho > 0); "Q > 0" numerically as
+      lambda_min(Q) > tau_pd = 1e-7 max(1, lambda_max(Q)) (reading c25).
     """
     q8 = 8.0 * L_d * R_d ** 2 / eps
     if alg == DGM:
@@ -361,13 +363,13 @@ def theory_schedule(alg: str, eps: float, R_d: float, L_d: float, L_in: float, s
         raise ValueError(alg)
     if sigma_L > 0:
         k_in = np.sqrt(L_in / sigma_L) * np.log(L_in * D_U ** 2 / eps_in) + 1.0
-        k_total = 16.0 * normG * R_d / np.sqrt(sigma_L * eps) * np.log(8.0 * normG * D_U * R_d / eps)
+        k_total = 16.0 * normG * R_d / np.sqrt(sigma_L * eps) * np.log(max(1.0, 8.0 * normG * D_U * R_d / eps))
     else:
         k_in = np.sqrt(2.0 * L_in * D_U ** 2 / eps_in)
         k_total = 24.0 * normG * D_U * R_d / eps
     return dict(eps_in=float(eps_in), k_out=k_out, k_in=int(np.ceil(max(k_in, 1.0))),
                 rho_star=8.0 * R_d ** 2 / eps, k_total=int(np.floor(k_total)),
-                case_id=1 if lambda_min_Q > 0 else 2)
+                case_id=1 if lambda_min_Q > 1e-7 * max(1.0, lambda_max_Q) else 2)
 
 
 def theorem1_bound(alg: str, k: int, L_d: float, R_d: float, eps_in: float) -> float:
@@ -422,8 +424,11 @@ def lipschitz_constants(Q, G, rho: float, lambda_min_lb: float, l_mode: int = 0,
     else:
         lmax = float(np.linalg.eigvalsh(Q)[-1]) + rho * normG2
     L_in = (1.0 + safety) * lmax
-    denom = lambda_min_lb + rho * normG2
-    L_d = normG2 / denom if denom > 0 else float("inf")
+    # safety inflates every eigen-derived constant (SPEC.md:76 delta_safe): L_d is increasing
+    # in ||G||^2, so it is formed from the inflated value; the raw ||G||^2 is returned
+    nG2_up = (1.0 + safety) * normG2
+    denom = lambda_min_lb + rho * nG2_up
+    L_d = nG2_up / denom if denom > 0 else float("inf")
     return L_in, L_d, normG2
 
 

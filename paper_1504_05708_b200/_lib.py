@@ -119,7 +119,7 @@ _SIGS = {
     "duquad_get_inner_counts": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
     "duquad_set_initial": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
     "duquad_theory_schedule": (C.c_int, [C.c_int32, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
-                                         C.c_double, C.c_double, C.c_double, C.POINTER(Schedule)]),
+                                         C.c_double, C.c_double, C.c_double, C.c_double, C.POINTER(Schedule)]),
     "duquad_theory_bounds": (C.c_int, [C.c_int32, C.c_int64, C.c_double, C.c_double, C.c_double,
                                        C.POINTER(Bounds)]),
     "duquad_get_state": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

@@ -758,6 +758,23 @@ duquad_status setup_csr(duquad_ctx *ctx, const duquad_problem *prob) {
     }
     CK(cudaStreamSynchronize(s));
     if (flag) return fail(ctx, DUQUAD_EINVAL, "invalid CSR data (row pointers, column range or non-finite value)");
+    {   // Q symmetric: Q' (device transpose of the full Q) has Q's pattern and values
+        int32_t *trp = nullptr, *tci = nullptr;
+        double *tva = nullptr;
+        int64_t tnnz = 0;
+        cudaError_t e = csr_transpose_rows(Qrp, Qci, Qva, n, n, qnnz, 0, n, &trp, &tci, &tva, &tnnz, s);
+        if (e == cudaSuccess) e = launch_csr_sym_cmp(Qrp, Qci, Qva, trp, tci, tva, n, qnnz, ctx->d_flag, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(flag), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        cudaFree(trp);
+        cudaFree(tci);
+        cudaFree(tva);
+        CK(e);
+        if (flag || tnnz != qnnz)
+            return fail(ctx, DUQUAD_EINVAL,
+                        "Q must be symmetric (PAPER.md:199): the CSR pattern and values of Q and Q' must agree "
+                        "(|Q_ij - Q_ji| <= 1e-12 (|Q_ij| + |Q_ji|); store both triangles)");
+    }
     const int64_t nq = qb[1] - qb[0], ng = gb[1] - gb[0];
     ctx->nnz_a = nq + ng;
     CK(dalloc(&ctx->a_rp, ctx->nloc + ctx->ploc + 1));
@@ -1136,12 +1153,30 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
             return bail(DUQUAD_EINVAL);
         }
     }
-    if (!csr && ctx->nloc == n && n > 0) {   // the byte-floor and small kernels read Q by symmetry
+    if (!csr && n > 0) {   // the byte-floor and small kernels read Q by symmetry
+        // A row-sharded rank holds only its rows: check the caller's full Q instead, so that an
+        // asymmetric Q is rejected alike on every rank count and every kernel path
+        const double *Qs = ctx->A;
+        int64_t ldq = ctx->ld;
+        double *Qtmp = nullptr;
+        if (ctx->nloc != n) {
+            if (prob->on_device) {
+                Qs = prob->Q;
+                ldq = prob->ldQ;
+            } else {
+                CKS(cudaMalloc(&Qtmp, (size_t)n * n * sizeof(double)));
+                CKS(cudaMemcpy2DAsync(Qtmp, n * sizeof(double), prob->Q, prob->ldQ * sizeof(double),
+                                      n * sizeof(double), n, cudaMemcpyHostToDevice, s));
+                Qs = Qtmp;
+                ldq = n;
+            }
+        }
         CKS(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int32_t), s));
-        CKS(launch_check_sym(ctx->A, n, ctx->ld, ctx->d_flag, s));
+        CKS(launch_check_sym(Qs, n, ldq, ctx->d_flag, s));
         int32_t flag = 0;
         CKS(cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(flag), cudaMemcpyDeviceToHost, s));
         CKS(cudaStreamSynchronize(s));
+        if (Qtmp) cudaFree(Qtmp);
         CKS(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int32_t), s));
         if (flag) {
             ctx->err = "Q must be symmetric (PAPER.md:199): |Q_ij - Q_ji| > 1e-12 (|Q_ij| + |Q_ji|)";
@@ -1333,14 +1368,19 @@ duquad_status duquad_lipschitz(duquad_ctx *ctx, int32_t iters, double safety, do
         if ((st = lanczos_max(ctx, 2, iters, &lmax)) != DUQUAD_OK) return st;
         lmax += ctx->rho * normG2;
     }
+    // The Lanczos values are Ritz values, never above the true eigenvalues: both constants must
+    // over-estimate, so the safety factor inflates lambda_max and ||G||^2 alike.  L_d =
+    // nG2 / (lambda_min_lb + rho nG2) is increasing in nG2, so it is formed from the inflated
+    // ||G||^2 (for l_mode 1, L_in's rho ||G||^2 term is inflated by the outer (1 + safety)).
     const double L_in = (1.0 + safety) * lmax;
-    const double denom = ctx->opt.lambda_min_lb + ctx->rho * normG2;
+    const double normG2_up = (1.0 + safety) * normG2;
+    const double denom = ctx->opt.lambda_min_lb + ctx->rho * normG2_up;
     double L_d = 0.0;
     if (ctx->p > 0) {
         if (!(denom > 0.0))
             return fail(ctx, DUQUAD_EINVAL,
                         "L_d undefined: rho == 0 needs lambda_min_lb > 0 (Eq. Ld, PAPER.md:277)");
-        L_d = normG2 / denom;
+        L_d = normG2_up / denom;
     }
     if ((st = duquad_set_constants(ctx, L_in, ctx->p > 0 ? L_d : 0.0)) != DUQUAD_OK) return st;
     if (L_in_out) *L_in_out = L_in;
@@ -1475,6 +1515,9 @@ static duquad_status solve_prepare(duquad_ctx *ctx, int alg, int K, int Kin, std
 duquad_status duquad_set_initial(duquad_ctx *ctx, const double *x0, const double *lambda0, int32_t on_device) {
     if (!ctx) return fail(nullptr, DUQUAD_EINVAL, "ctx is NULL");
     DevGuard guard(ctx->dev);
+    // device inputs may still be in flight on the caller's stream (as in duquad_setup): the copies
+    // below run on the library's own stream, so wait for all prior work on the device first
+    if (on_device) CK(cudaDeviceSynchronize());
     const bool bt = ctx->Btot > 1;
     const int64_t sn = bt ? ctx->ld : ctx->nloc, sp = bt ? std::max<int64_t>(ctx->ldp, 2) : ctx->ploc;
     const int64_t B = bt ? ctx->Bloc : 1;
@@ -1573,7 +1616,10 @@ static duquad_status eps_end(duquad_ctx *ctx, int32_t outer, duquad_status st, d
     }
     if (res) {
         res->inner_iters_total = total;   // batched: summed over the QPs
-        res->matrix_passes = 2 * total;
+        // the matvec accounting of the fixed-count solve: two passes per inner step,
+        // except on the Q-only paths (rho = 0, EQ_H), whose inner step is one pass plus two passes
+        // (G u_bar, G' mu) per inner solve, i.e. per outer iteration and the last-iterate solve
+        res->matrix_passes = ctx->rho0 && ctx->Btot == 1 ? total + 2 * (int64_t)(outer + 1) : 2 * total;
     }
     if (st != DUQUAD_OK) return st;
     if (capped) return fail(ctx, DUQUAD_EMAXITER, "an inner solve hit inner_max before the eps_in test (result valid)");
@@ -1596,23 +1642,26 @@ duquad_status duquad_solve_eps(duquad_ctx *ctx, int32_t alg, int32_t outer, int3
 }
 
 duquad_status duquad_theory_schedule(int32_t alg, double eps, double R_d, double L_d, double L_in, double sigma_L,
-                                     double D_U, double normG, double lambda_min_Q, duquad_schedule *out) {
+                                     double D_U, double normG, double lambda_min_Q, double lambda_max_Q,
+                                     duquad_schedule *out) {
     if (!out) return fail(nullptr, DUQUAD_EINVAL, "out is NULL");
     if (alg != DUQUAD_DGM && alg != DUQUAD_DFGM) return fail(nullptr, DUQUAD_EINVAL, "bad alg");
-    const double v[] = {eps, R_d, L_d, L_in, sigma_L, D_U, normG, lambda_min_Q};
+    const double v[] = {eps, R_d, L_d, L_in, sigma_L, D_U, normG, lambda_min_Q, lambda_max_Q};
     for (double x : v)
         if (!std::isfinite(x)) return fail(nullptr, DUQUAD_EINVAL, "non-finite schedule argument");
     if (!(eps > 0) || !(R_d > 0) || !(L_d > 0) || !(L_in > 0) || sigma_L < 0 || !(D_U > 0) || normG < 0 ||
-        lambda_min_Q < 0)
+        lambda_min_Q < 0 || lambda_max_Q < 0)
         return fail(nullptr, DUQUAD_EINVAL, "schedule arguments out of range");
     std::memset(out, 0, sizeof(*out));
+    // counts are formed in double and clamped to [0, 2^62] before the integer conversion
+    auto to_count = [](double x) { return x > 0.0 ? (int64_t)std::min(x, 4.6116860184273879e18) : (int64_t)0; };
     const double q = 8.0 * L_d * R_d * R_d / eps;                         // (choose_ein)
     if (alg == DUQUAD_DGM) {
         out->eps_in = eps / 4.0;
-        out->k_out = (int64_t)std::ceil(q);
+        out->k_out = to_count(std::ceil(q));
     } else {
         out->eps_in = eps * std::sqrt(eps) / (8.0 * R_d * std::sqrt(2.0 * L_d));
-        out->k_out = (int64_t)std::ceil(std::sqrt(q));
+        out->k_out = to_count(std::ceil(std::sqrt(q)));
     }
     const double d2 = D_U * D_U;
     double kin;
@@ -1620,13 +1669,17 @@ duquad_status duquad_theory_schedule(int32_t alg, double eps, double R_d, double
         kin = std::sqrt(L_in / sigma_L) * std::log(L_in * d2 / out->eps_in) + 1.0;
     else
         kin = std::sqrt(2.0 * L_in * d2 / out->eps_in);
-    out->k_in = (int64_t)std::ceil(std::max(kin, 1.0));
+    out->k_in = to_count(std::ceil(std::max(kin, 1.0)));
     out->rho_star = 8.0 * R_d * R_d / eps;
-    out->k_total = sigma_L > 0.0
-                       ? (int64_t)std::floor(16.0 * normG * R_d / std::sqrt(sigma_L * eps) *
-                                             std::log(8.0 * normG * D_U * R_d / eps))
-                       : (int64_t)std::floor(24.0 * normG * D_U * R_d / eps);
-    out->case_id = lambda_min_Q > 0.0 ? 1 : 2;
+    // the log's argument is clamped to >= 1 (normG == 0 would give 0 * log 0 = NaN; an argument
+    // below 1 a negative count)
+    const double kt = sigma_L > 0.0 ? 16.0 * normG * R_d / std::sqrt(sigma_L * eps) *
+                                          std::log(std::max(1.0, 8.0 * normG * D_U * R_d / eps))
+                                    : 24.0 * normG * D_U * R_d / eps;
+    out->k_total = to_count(std::floor(kt));
+    // Case 1 (Q > 0, rho = 0) iff lambda_min(Q) > tau_pd = 1e-7 max(1, lambda_max(Q))
+    // (SPEC.md:186's numerical threshold for the paper's dichotomy; reading c25)
+    out->case_id = lambda_min_Q > 1e-7 * std::max(1.0, lambda_max_Q) ? 1 : 2;
     return DUQUAD_OK;
 }
 
@@ -1747,6 +1800,7 @@ duquad_status duquad_set_state(duquad_ctx *ctx, const double *x, const double *m
     if (!x || !x_avg || (ctx->p > 0 && (!mu || !lam_prev)))
         return fail(ctx, DUQUAD_EINVAL, "set_state: x, x_avg, mu and lam_prev are all required");
     DevGuard guard(ctx->dev);
+    if (on_device) CK(cudaDeviceSynchronize());   // caller's device buffers may still be in flight
     duquad_status st = alloc_state(ctx);
     if (st != DUQUAD_OK) return st;
     const int64_t n = ctx->Btot > 1 ? ctx->n : ctx->nloc, p = ctx->Btot > 1 ? ctx->p : ctx->ploc;

@@ -174,6 +174,11 @@ cudaError_t launch_rebase(int32_t *dst, const int32_t *src, int64_t count, int32
 // values non-finite)
 cudaError_t launch_check_csr(const int32_t *rp, const int32_t *ci, const double *va, int64_t rows,
                              int64_t cols, int64_t nnz, int32_t *flag, cudaStream_t s);
+// flag = 3 unless (rp, ci, va) and its transpose (trp, tci, tva) agree: same pattern, values to
+// 1e-12 relative (the Q symmetry check of the CSR path)
+cudaError_t launch_csr_sym_cmp(const int32_t *rp, const int32_t *ci, const double *va, const int32_t *trp,
+                               const int32_t *tci, const double *tva, int64_t rows, int64_t nnz, int32_t *flag,
+                               cudaStream_t s);
 // Transpose of a CSR matrix (rows x cols) restricted to output rows [c0, c0 + nc):
 // builds (rp_t, ci_t, va_t) with columns (original rows) sorted; allocates the outputs.
 cudaError_t csr_transpose_rows(const int32_t *rp, const int32_t *ci, const double *va, int64_t rows,

@@ -219,6 +219,20 @@ __global__ void k_check_csr(const int32_t *rp, const int32_t *ci, const double *
         if (ci[e] < 0 || ci[e] >= cols || !isfinite(va[e])) *flag = 1;
 }
 
+// Q and its transpose T (both sorted CSR, same nnz): identical row pointers and column indices,
+// values equal to 1e-12 relative (the dense path's k_check_sym tolerance)
+__global__ void k_csr_sym_cmp(const int32_t *rp, const int32_t *ci, const double *va, const int32_t *trp,
+                              const int32_t *tci, const double *tva, int64_t rows, int64_t nnz, int32_t *flag) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (int64_t i = t0; i <= rows; i += stride)
+        if (rp[i] != trp[i]) *flag = 3;
+    for (int64_t e = t0; e < nnz; e += stride) {
+        const double a = va[e], b = tva[e];
+        if (ci[e] != tci[e] || fabs(a - b) > 1e-12 * (fabs(a) + fabs(b))) *flag = 3;
+    }
+}
+
 __global__ void k_expand_rows(const int32_t *rp, int64_t rows, int64_t *keys, const int32_t *ci) {
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (r >= rows) return;
@@ -291,6 +305,13 @@ cudaError_t launch_rebase(int32_t *dst, const int32_t *src, int64_t count, int32
 cudaError_t launch_check_csr(const int32_t *rp, const int32_t *ci, const double *va, int64_t rows,
                              int64_t cols, int64_t nnz, int32_t *flag, cudaStream_t s) {
     k_check_csr<<<592, 256, 0, s>>>(rp, ci, va, rows, cols, nnz, flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_csr_sym_cmp(const int32_t *rp, const int32_t *ci, const double *va, const int32_t *trp,
+                               const int32_t *tci, const double *tva, int64_t rows, int64_t nnz, int32_t *flag,
+                               cudaStream_t s) {
+    k_csr_sym_cmp<<<592, 256, 0, s>>>(rp, ci, va, trp, tci, tva, rows, nnz, flag);
     return cudaGetLastError();
 }
 

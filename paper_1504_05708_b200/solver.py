@@ -81,11 +81,13 @@ def solve_emulated_eps(solvers, alg: str, outer: int, inner_max: int, eps_in: fl
 
 
 def theory_schedule(alg: str, eps: float, R_d: float, L_d: float, L_in: float, sigma_L: float, D_U: float,
-                    normG: float, lambda_min_Q: float = 0.0) -> dict:
-    """DuQuad's theory schedule (include/duquad.h duquad_theory_schedule; host arithmetic)."""
+                    normG: float, lambda_min_Q: float = 0.0, lambda_max_Q: float = 0.0) -> dict:
+    """DuQuad's theory schedule (include/duquad.h duquad_theory_schedule; host arithmetic).
+    case_id 1 iff lambda_min_Q > 1e-7 max(1, lambda_max_Q) (SPEC.md:186's tau_pd)."""
     out = L.Schedule()
     L.check(L.lib().duquad_theory_schedule(_ALGS[alg], float(eps), float(R_d), float(L_d), float(L_in),
                                            float(sigma_L), float(D_U), float(normG), float(lambda_min_Q),
+                                           float(lambda_max_Q),
                                            C.byref(out)))
     return {k: getattr(out, k) for k, _ in L.Schedule._fields_ if k != "reserved"}
 
@@ -225,7 +227,10 @@ class Solver:
         self.last_result = None
 
     # ------------------------------------------------------------------ API
-    def lipschitz(self, iters: int = 100, safety: float = 0.0):
+    def lipschitz(self, iters: int = 100, safety: float = 1e-6):
+        """duquad_lipschitz: (L_in, L_d, ||G||^2).  `safety` inflates both eigen estimates (Lanczos
+        Ritz values never exceed the true eigenvalues, so L_in and L_d must be over-estimates;
+        SPEC.md:76's delta_safe = 1e-6); the returned ||G||^2 is the raw estimate."""
         a, b, c = C.c_double(), C.c_double(), C.c_double()
         L.check(self._lib.duquad_lipschitz(self._ctx, iters, safety, C.byref(a), C.byref(b), C.byref(c)),
                 self._ctx)

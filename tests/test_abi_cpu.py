@@ -111,18 +111,25 @@ def test_theory_schedule_host_only(lib):
     from oracle import dfom as O
     from paper_1504_05708_b200 import theory_schedule, _lib
     for alg in ("DGM", "DFGM"):
-        for args in [(1e-2, 1.0, 1.0, 40.0, 0.5, 2.0, 3.0, 0.1), (1e-3, 3.7, 0.25, 1e4, 0.0, 1.0, 7.0, 0.0),
-                     (0.5, 12.0, 40.0, 9.0, 1e-3, 2.0, 1.5, 0.0)]:
+        for args in [(1e-2, 1.0, 1.0, 40.0, 0.5, 2.0, 3.0, 0.1, 2.0), (1e-3, 3.7, 0.25, 1e4, 0.0, 1.0, 7.0, 0.0, 0.0),
+                     (0.5, 12.0, 40.0, 9.0, 1e-3, 2.0, 1.5, 0.0, 5.0), (1e-2, 1.0, 1.0, 40.0, 0.5, 2.0, 0.0, 1e-12, 1.0),
+                     (1e-2, 1.0, 1.0, 40.0, 0.5, 2.0, 3.0, 2e-7, 1.0), (1e-2, 1.0, 1.0, 40.0, 0.5, 2.0, 3.0, 2e-7, 3.0)]:
             got = theory_schedule(alg, *args)
-            want = O.theory_schedule(alg, *args[:7], lambda_min_Q=args[7])
+            want = O.theory_schedule(alg, *args[:7], lambda_min_Q=args[7], lambda_max_Q=args[8])
             for k in ("k_out", "k_in", "k_total", "case_id"):
                 assert got[k] == want[k], (alg, args, k)
             for k in ("eps_in", "rho_star"):
                 assert got[k] == pytest.approx(want[k], rel=1e-14), (alg, args, k)
+    # ||G|| = 0 with sigma_L > 0: k_total = 0 (the log's argument clamped to 1), not 0 * log 0
+    assert theory_schedule("DFGM", 1e-2, 1.0, 1.0, 40.0, 0.5, 2.0, 0.0)["k_total"] == 0
+    # Q = I is Case 1, Q = 0 Case 2, Q = diag(1, 1e-12) Case 2 under tau_pd
+    sched = lambda lmin, lmax: theory_schedule("DGM", 1e-2, 1.0, 1.0, 1.0, 0.0, 2.0, 1.0, lmin, lmax)["case_id"]
+    assert (sched(1.0, 1.0), sched(0.0, 0.0), sched(1e-12, 1.0)) == (1, 2, 2)
     out = _lib.Schedule()
-    assert lib.duquad_theory_schedule(1, -1.0, 1, 1, 1, 0, 1, 1, 0, C.byref(out)) == _lib.DUQUAD_EINVAL
-    assert lib.duquad_theory_schedule(1, 1e-2, 1, 1, 1, float("nan"), 1, 1, 0, C.byref(out)) == _lib.DUQUAD_EINVAL
-    assert lib.duquad_theory_schedule(7, 1e-2, 1, 1, 1, 0, 1, 1, 0, C.byref(out)) == _lib.DUQUAD_EINVAL
+    assert lib.duquad_theory_schedule(1, -1.0, 1, 1, 1, 0, 1, 1, 0, 0, C.byref(out)) == _lib.DUQUAD_EINVAL
+    assert lib.duquad_theory_schedule(1, 1e-2, 1, 1, 1, float("nan"), 1, 1, 0, 0, C.byref(out)) == _lib.DUQUAD_EINVAL
+    assert lib.duquad_theory_schedule(7, 1e-2, 1, 1, 1, 0, 1, 1, 0, 0, C.byref(out)) == _lib.DUQUAD_EINVAL
+    assert lib.duquad_theory_schedule(1, 1e-2, 1, 1, 1, 0, 1, 1, 0, -1.0, C.byref(out)) == _lib.DUQUAD_EINVAL
     assert lib.duquad_status_string(_lib.DUQUAD_EMAXITER).startswith(b"inner iteration cap")
 
 

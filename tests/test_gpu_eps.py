@@ -117,6 +117,26 @@ def test_eps_mode_rho0_q_only_path(torch_cuda):
     _check(prob, 0.0, "DFGM", 6, 200, 1e-7, 0.1, L_in, L_d, info, xl, xa, lam)
 
 
+def test_eps_mode_pass_accounting_matches_fixed_counts(torch_cuda):
+    """The matvec accounting identity (SPEC.md:558, :604 item 12): an eps_in-mode solve reports the
+    passes a fixed-count solve with the same per-solve step counts reports -- 2 per inner step on the
+    two-pass path; on the Q-only (rho = 0) path 1 per inner step + 2 per inner solve (G u_bar, G' mu)."""
+    from paper_1504_05708_b200 import Solver
+    for rho, kw in ((0.0, dict(small_path=False)), (1.0, dict(small_path=False, fused_path=False))):
+        prob = qpgen.dense_ineq(600, 300, seed=2, shift=0.1)
+        L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, rho, 0.1)
+        s = Solver(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho=rho, **kw)
+        s.set_constants(L_in, L_d)
+        K, kmax = 4, 6                      # every inner solve capped: the counts are all kmax
+        info = s.solve_eps("DFGM", K, kmax, 1e-30, 0.1)
+        assert info["inner_counts"] == [kmax] * (K + 1)
+        fixed = s.solve("DFGM", K, kmax)
+        assert info["matrix_passes"] == fixed["matrix_passes"], (rho, info["matrix_passes"], fixed["matrix_passes"])
+        total = info["inner_iters_total"]
+        assert info["matrix_passes"] == (total + 2 * (K + 1) if rho == 0.0 else 2 * total)
+        s.close()
+
+
 def test_eps_mode_csr_path(torch_cuda):
     prob = qpgen.sparse_banded_eq(n=3001, p=1201, seed=4)
     Qd, Gd = prob.Q.toarray(), prob.G.toarray()

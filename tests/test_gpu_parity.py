@@ -319,6 +319,35 @@ def test_asymmetric_q_is_rejected(torch_cuda):
     Solver(Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho=1.0).close()
 
 
+def test_asymmetric_q_is_rejected_on_every_rank_count_and_format(torch_cuda):
+    """The symmetry check is not a single-GPU special case: a row-sharded rank (which holds only its
+    rows) checks the caller's full Q -- host or device input, both byte-floor and two-pass sizes --
+    and the CSR path compares Q with its transpose."""
+    import scipy.sparse as sp
+    from paper_1504_05708_b200 import Solver, DuquadError
+    for n, p in ((40, 10), (4096, 256)):
+        prob = qpgen.tiny(n, p, seed=9)
+        Q = prob.Q.copy()
+        Q[30, 3] += 1e-6           # below the diagonal: rank 1's rows
+        for dev in (False, True):
+            Qa = torch_cuda.from_numpy(Q).cuda() if dev else Q
+            args = [torch_cuda.from_numpy(a).cuda() if dev else a for a in (prob.q, prob.G, prob.g, prob.lb, prob.ub,
+                                                                           prob.cone)]
+            for r in range(2):
+                with pytest.raises(DuquadError, match="symmetric"):
+                    Solver(Qa, *args, rho=1.0, world_size=2, rank=r, emulate_ranks=True)
+    prob = qpgen.sparse_banded_eq(n=300, p=100, seed=3)
+    Q = prob.Q.tolil()
+    Q[5, 7] = Q[5, 7] + 1e-6
+    with pytest.raises(DuquadError, match="symmetric"):
+        Solver(sp.csr_matrix(Q), prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho=5.0)
+    Q = prob.Q.tolil()
+    Q[5, 150] = 0.3            # an entry without its mirror: the pattern is not symmetric
+    with pytest.raises(DuquadError, match="symmetric"):
+        Solver(sp.csr_matrix(Q), prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho=5.0)
+    Solver(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho=5.0).close()   # symmetric: accepted
+
+
 @pytest.mark.parametrize("n,p,kind,rho,alg", [(2000, 1000, "ineq", 1.0, "DFGM"), (2000, 1000, "ineq", 10.0, "DGM"),
                                                (777, 301, "mixed", 2.0, "DFGM"), (130, 0, "ineq", 1.0, "DFGM")])
 def test_persistent_solve_is_bitwise_the_multi_launch_path(torch_cuda, n, p, kind, rho, alg):

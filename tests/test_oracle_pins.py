@@ -433,6 +433,16 @@ def test_schedule_satisfies_theorem1_and_lemma1(alg, eps, R_d, L_d):
         assert s["rho_star"] == pytest.approx(8 * R_d ** 2 / eps, rel=1e-15)
     assert O.theory_schedule(alg, eps, R_d, L_d, 40.0, 0.5, 2.0, 3.0, lambda_min_Q=0.1)["case_id"] == 1
     assert O.theory_schedule(alg, eps, R_d, L_d, 40.0, 0.5, 2.0, 3.0, lambda_min_Q=0.0)["case_id"] == 2
+    # SPEC.md:412-414 classification examples, the eigenvalues from the matrices themselves:
+    # Q = I -> Case 1; Q = 0 -> Case 2; Q = diag(1, 1e-12) -> Case 2 under tau_pd = 1e-7 lambda_max
+    for Q, want in ((np.eye(3), 1), (np.zeros((3, 3)), 2), (np.diag([1.0, 1e-12]), 2), (np.diag([1e3, 2e-4]), 1),
+                    (np.diag([1e3, 5e-5]), 2)):
+        ev = np.linalg.eigvalsh(Q)
+        got = O.theory_schedule(alg, eps, R_d, L_d, 40.0, 0.5, 2.0, 3.0, lambda_min_Q=max(ev[0], 0.0),
+                                lambda_max_Q=ev[-1])["case_id"]
+        assert got == want, (np.diag(Q), got)
+    # ||G|| = 0 (no coupling): k_total = 0 rather than 0 * log(0)
+    assert O.theory_schedule(alg, eps, R_d, L_d, 40.0, 0.5, 2.0, 0.0)["k_total"] == 0
 
 
 @pytest.mark.parametrize("alg", [O.DGM, O.DFGM])
