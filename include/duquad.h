@@ -31,8 +31,9 @@
 extern "C" {
 #endif
 
-#define DUQUAD_ABI_VERSION 3   /* 2: options gained eq_precompute, checkpoint, dual_average;
-                                  3: nccl_self */
+#define DUQUAD_ABI_VERSION 4   /* 2: options gained eq_precompute, checkpoint, dual_average;
+                                  3: nccl_self; 4: sell_path, duquad_theory_schedule's
+                                  lambda_max_Q */
 
 typedef enum {
     DUQUAD_OK = 0,
@@ -175,6 +176,12 @@ typedef struct {
                               communicator the library creates itself (nccl_id ignored): the
                               collective call sequence of a P-GPU run, exercised on one GPU.
                               Results agree with the oracle like any solve.  0 (default)      */
+    int32_t sell_path;     /* 1 (default): CSR input whose rows are short (mean <= 48 nonzeros) is
+                              also stored as SELL-32 (slices of 32 rows, the k-th nonzeros of a
+                              slice in one coalesced 32-wide column; rows grouped by length
+                              inside windows of 1024 rows when that pads less) if the padding
+                              stays within 25 %; the passes then run one lane per row.  Each
+                              row is summed in CSR order either way.  0: the CSR kernels      */
 } duquad_options;
 
 /* Per-solve report. */
@@ -192,7 +199,7 @@ typedef struct {
     double flops_pass_a;        /* algorithmic flops per pass-A launch (2 per multiply-add) */
     double flops_pass_b;
     int32_t path;               /* duquad_path: which kernels ran the inner steps           */
-    int32_t reserved;
+    int32_t sell_mask;          /* CSR: bit 0 pass A, bit 1 pass B ran the SELL-32 kernels  */
 } duquad_result;
 
 /* Kernel path of a solve (duquad_result.path).  "pass A" / "pass B" in the report map to:

@@ -55,7 +55,7 @@ class Options(C.Structure):
         ("time_passes", C.c_int32), ("small_path", C.c_int32), ("rho0_path", C.c_int32),
         ("emulate_ranks", C.c_int32), ("fused_path", C.c_int32), ("persist_path", C.c_int32),
         ("eq_precompute", C.c_int32), ("checkpoint", C.c_int32), ("dual_average", C.c_int32),
-        ("nccl_self", C.c_int32),
+        ("nccl_self", C.c_int32), ("sell_path", C.c_int32),
     ]
 
 
@@ -73,7 +73,7 @@ class Result(C.Structure):
         ("n_timed_a", C.c_int64), ("n_timed_b", C.c_int64),
         ("bytes_pass_a", C.c_double), ("bytes_pass_b", C.c_double),
         ("flops_pass_a", C.c_double), ("flops_pass_b", C.c_double),
-        ("path", C.c_int32), ("reserved", C.c_int32),
+        ("path", C.c_int32), ("sell_mask", C.c_int32),
     ]
 
 

@@ -60,6 +60,8 @@ struct duquad_ctx {
     double *a_va = nullptr, *b_va = nullptr;
     int64_t nnz_a = 0, nnz_b = 0;
     int gs_a = 4, gs_b = 4;
+    SellStore sell_a, sell_b;   // SELL-32 copies of the two (options.sell_path; empty: CSR kernels)
+    bool use_sell_a = false, use_sell_b = false;
     // batched storage (batch > 1): QP-major per-QP vectors, strides ld (n-vectors) / ldp (p-vectors)
     int64_t Btot = 1, Bloc = 1, b0 = 0;
     double *Yb = nullptr, *Xb = nullptr, *XHb = nullptr, *QYb = nullptr, *qb = nullptr;
@@ -177,6 +179,8 @@ void free_all(duquad_ctx *c) {
         if (d) cudaFree(d);
     if (c->a_va) cudaFree(c->a_va);
     if (c->b_va) cudaFree(c->b_va);
+    sell_free(&c->sell_a);
+    sell_free(&c->sell_b);
     if (c->d_ops) cudaFree(c->d_ops);
     if (c->d_j) cudaFree(c->d_j);
     if (c->d_flag) cudaFree(c->d_flag);
@@ -277,6 +281,8 @@ PassAArgs make_a(duquad_ctx *c) {
     a.va = c->a_va;
     a.skip = c->eps_mode ? c->d_done : nullptr;
     a.lam_hat = c->davg ? c->lam_hat : nullptr;
+    a.use_sell = c->use_sell_a;
+    a.sell = sell_view(c->sell_a);
     return a;
 }
 
@@ -305,6 +311,8 @@ PassBArgs make_b(duquad_ctx *c) {
     b.va = c->b_va;
     b.skip = c->eps_mode ? c->d_done : nullptr;
     b.gm_sq = c->eps_mode ? c->gm_sq : nullptr;
+    b.use_sell = c->use_sell_b;
+    b.sell = sell_view(c->sell_b);
     return b;
 }
 
@@ -711,6 +719,10 @@ duquad_status upload_vec(duquad_ctx *ctx, double *dst, const double *src, int64_
 
 // CSR setup: device copies of Q and G (validated), the stacked local [Q_r; G_r]
 // and the local rows of G' (device transpose, deterministic order).
+// SELL-32 is used for a matrix whose mean row length is at most kSellMaxMean and whose padded
+// layout holds at most kSellMaxPad x its nonzeros
+constexpr double kSellMaxMean = 48.0, kSellMaxPad = 1.25;
+
 duquad_status setup_csr(duquad_ctx *ctx, const duquad_problem *prob) {
     cudaStream_t s = ctx->stream;
     const int64_t n = ctx->n, p = ctx->p;
@@ -802,6 +814,20 @@ duquad_status setup_csr(duquad_ctx *ctx, const duquad_problem *prob) {
     ctx->gs_a = csr_group_size((double)(qnnz + gnnz) / (double)(n + p));
     ctx->gs_b = csr_group_size((double)gnnz / (double)n);
     CK(cudaStreamSynchronize(s));
+    // SELL-32 copies for short rows (one lane per row, coalesced slice columns); the decision is
+    // per matrix and per rank (row sums are the same either way: each row summed in CSR order)
+    if (ctx->opt.sell_path && (double)(qnnz + gnnz) <= kSellMaxMean * (double)(n + p)) {
+        bool ok = false;
+        CK(sell_build(ctx->a_rp, ctx->a_ci, ctx->a_va, ctx->nloc + ctx->ploc, ctx->nloc, ctx->nnz_a, kSellMaxPad,
+                      &ctx->sell_a, &ok, s));
+        ctx->use_sell_a = ok;
+    }
+    if (ctx->opt.sell_path && p > 0 && (double)gnnz <= kSellMaxMean * (double)n) {
+        bool ok = false;
+        CK(sell_build(ctx->b_rp, ctx->b_ci, ctx->b_va, ctx->nloc, ctx->nloc, ctx->nnz_b, kSellMaxPad, &ctx->sell_b,
+                      &ok, s));
+        ctx->use_sell_b = ok;
+    }
     return DUQUAD_OK;
 }
 
@@ -852,6 +878,7 @@ void duquad_default_options(duquad_options *o) {
     o->eq_precompute = 1;
     o->checkpoint = 0;
     o->nccl_self = 0;
+    o->sell_path = 1;
 }
 
 duquad_status duquad_shard_range(int64_t rows, int32_t world, int32_t rank, int64_t *begin,
@@ -1183,9 +1210,11 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
             return bail(DUQUAD_EINVAL);
         }
     }
-    if (csr) {   // grid-stride sub-warp SpMV, full occupancy
-        ctx->cfg_a = {ctx->num_sms * csr_blocks_per_sm(0, ctx->gs_a), 256, 0};   // whole waves
-        ctx->cfg_b = {ctx->num_sms * csr_blocks_per_sm(1, ctx->gs_b), 256, 0};
+    if (csr) {   // grid-stride sub-warp SpMV / SELL-32 warp-per-slice, full occupancy
+        ctx->cfg_a = {ctx->num_sms * (ctx->use_sell_a ? sell_blocks_per_sm(0) : csr_blocks_per_sm(0, ctx->gs_a)), 256,
+                      0};   // whole waves
+        ctx->cfg_b = {ctx->num_sms * (ctx->use_sell_b ? sell_blocks_per_sm(1) : csr_blocks_per_sm(1, ctx->gs_b)), 256,
+                      0};
         CKS(cudaStreamSynchronize(s));
         *out = ctx;
         return DUQUAD_OK;
@@ -1988,6 +2017,7 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
                     : ctx->rho0 ? DUQUAD_PATH_RHO0
                     : ctx->Btot > 1 ? DUQUAD_PATH_BATCHED
                     : ctx->format == DUQUAD_CSR ? DUQUAD_PATH_CSR : DUQUAD_PATH_TWO_PASS;
+        res->sell_mask = (ctx->use_sell_a ? 1 : 0) | (ctx->use_sell_b ? 2 : 0);
         res->outer_iters = K;
         res->inner_iters_total = (int64_t)nout * Kin;
         res->kernel_launches = 1 + (int64_t)nout * (2 * Kin + 1);

@@ -26,6 +26,19 @@ struct OuterParam {
 
 enum PassMode : int { MODE_SOLVE = 0, MODE_LIN = 1 };
 
+// SELL-32 view of a sparse matrix (kernels_sell.cu): slice s holds 32 rows; its k-th column of
+// nonzeros is val/col[sptr[s] + 32 k + lane].  Rows form two segments, [0, nq) and [nq, rows),
+// that never share a slice (pass A: Q rows, then G rows).  row == NULL: slice s, lane l is row
+// 32 s + l of the first segment (s < nsl_q), else nq + 32 (s - nsl_q) + l; otherwise row[32 s + l]
+// (-1: an empty lane).
+struct SellMat {
+    const double *val;
+    const int32_t *col;
+    const int64_t *sptr;   // nsl + 1 element offsets (32 x the slice width apart)
+    const int32_t *row;    // slot -> row map of a length-sorted layout, or NULL
+    int64_t nsl, nsl_q, nq, rows;
+};
+
 // ---------------------------------------------------------------- pass A
 // Streams rows [row_begin, row_end) of the local stacked matrix A = [Q_r; G_r]
 // (row-major, leading dimension ld doubles, zero-padded) against y (full
@@ -60,6 +73,8 @@ struct PassAArgs {
     const int32_t *ci;   // column indices
     const double *va;    // values
     const int32_t *skip; // eps_in mode: the inner solve has converged -> the launch does nothing
+    int32_t use_sell;    // CSR input stored as SELL-32 (kernels_sell.cu)
+    SellMat sell;
 };
 
 // ---------------------------------------------------------------- pass B
@@ -91,6 +106,8 @@ struct PassBArgs {
     const double *va;
     const int32_t *skip; // eps_in mode: the inner solve has converged -> the launch does nothing
     double *gm_sq;       // eps_in mode: gm_sq[j] = (y_j - x+_j)^2 (gradient-map test)
+    int32_t use_sell;    // CSR input stored as SELL-32 (kernels_sell.cu)
+    SellMat sell;
 };
 
 // ---------------------------------------------------------------- batched (B QPs, shared Q, G)
@@ -185,6 +202,25 @@ cudaError_t csr_transpose_rows(const int32_t *rp, const int32_t *ci, const doubl
                                int64_t cols, int64_t nnz, int64_t c0, int64_t nc, int32_t **rp_t,
                                int32_t **ci_t, double **va_t, int64_t *nnz_t, cudaStream_t s);
 int csr_group_size(double avg_nnz_per_row);
+
+// kernels_sell.cu: SELL-32 storage built on the device from a (rebased) CSR matrix
+struct SellStore {
+    double *val = nullptr;
+    int32_t *col = nullptr;
+    int64_t *sptr = nullptr;
+    int32_t *row = nullptr;
+    int64_t nsl = 0, nsl_q = 0, nq = 0, rows = 0, padded = 0;
+};
+// rows [0, nq) and [nq, rows) sliced separately; rows are grouped by length inside windows of 1024
+// when that pads less.  *ok = false (nothing allocated) if the padded layout exceeds
+// max_pad * nnz (+1024): the CSR kernels stay in use.
+cudaError_t sell_build(const int32_t *rp, const int32_t *ci, const double *va, int64_t rows, int64_t nq,
+                       int64_t nnz, double max_pad, SellStore *out, bool *ok, cudaStream_t s);
+void sell_free(SellStore *st);
+SellMat sell_view(const SellStore &st);
+int sell_blocks_per_sm(int pass);
+cudaError_t launch_pass_a_sell(const PassAArgs &a, int mode, const LaunchCfg &cfg, cudaStream_t s);
+cudaError_t launch_pass_b_sell(const PassBArgs &b, int mode, const LaunchCfg &cfg, cudaStream_t s);
 
 // kernels_fused.cu
 bool fused_supported(int64_t n, int64_t ld, size_t smem_optin);

@@ -33,7 +33,7 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_abi_version_and_status_strings(lib):
-    assert lib.duquad_abi_version() == 3
+    assert lib.duquad_abi_version() == 4
     assert lib.duquad_status_string(0) == b"ok"
     assert b"invalid" in lib.duquad_status_string(1)
 
