@@ -176,12 +176,12 @@ typedef struct {
                               communicator the library creates itself (nccl_id ignored): the
                               collective call sequence of a P-GPU run, exercised on one GPU.
                               Results agree with the oracle like any solve.  0 (default)      */
-    int32_t sell_path;     /* 1 (default): CSR input whose rows are short (mean <= 48 nonzeros) is
-                              also stored as SELL-32 (slices of 32 rows, the k-th nonzeros of a
-                              slice in one coalesced 32-wide column; rows grouped by length
-                              inside windows of 1024 rows when that pads less) if the padding
-                              stays within 25 %; the passes then run one lane per row.  Each
-                              row is summed in CSR order either way.  0: the CSR kernels      */
+    int32_t sell_path;     /* 1 (default): a CSR matrix whose rows are short (mean <= 48 nonzeros)
+                              runs lane-per-row kernels: SELL-32 (slices of 32 rows, the k-th
+                              nonzeros of a slice in one coalesced 32-wide column; an extra
+                              copy of the matrix) when that pads at most 15 %, else
+                              thread-per-row CSR.  Both sum each row in CSR order.  0: the
+                              sub-warp CSR kernels (a group of lanes per row, tree sums)      */
 } duquad_options;
 
 /* Per-solve report. */
@@ -199,7 +199,8 @@ typedef struct {
     double flops_pass_a;        /* algorithmic flops per pass-A launch (2 per multiply-add) */
     double flops_pass_b;
     int32_t path;               /* duquad_path: which kernels ran the inner steps           */
-    int32_t sell_mask;          /* CSR: bit 0 pass A, bit 1 pass B ran the SELL-32 kernels  */
+    int32_t sparse_kernels;     /* CSR: pass A kind | pass B kind << 4, kind 0 = sub-warp CSR,
+                                   1 = SELL-32, 2 = thread-per-row CSR (options.sell_path)   */
 } duquad_result;
 
 /* Kernel path of a solve (duquad_result.path).  "pass A" / "pass B" in the report map to:

@@ -73,7 +73,7 @@ class Result(C.Structure):
         ("n_timed_a", C.c_int64), ("n_timed_b", C.c_int64),
         ("bytes_pass_a", C.c_double), ("bytes_pass_b", C.c_double),
         ("flops_pass_a", C.c_double), ("flops_pass_b", C.c_double),
-        ("path", C.c_int32), ("sell_mask", C.c_int32),
+        ("path", C.c_int32), ("sparse_kernels", C.c_int32),
     ]
 
 

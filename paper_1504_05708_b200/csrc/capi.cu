@@ -60,8 +60,8 @@ struct duquad_ctx {
     double *a_va = nullptr, *b_va = nullptr;
     int64_t nnz_a = 0, nnz_b = 0;
     int gs_a = 4, gs_b = 4;
-    SellStore sell_a, sell_b;   // SELL-32 copies of the two (options.sell_path; empty: CSR kernels)
-    bool use_sell_a = false, use_sell_b = false;
+    SellStore sell_a, sell_b;   // SELL-32 copies of the two (options.sell_path; empty unless kind SPK_SELL)
+    int kind_a = SPK_CSR, kind_b = SPK_CSR, u_a = 8, u_b = 8;   // SparseKind and load-round width per pass
     // batched storage (batch > 1): QP-major per-QP vectors, strides ld (n-vectors) / ldp (p-vectors)
     int64_t Btot = 1, Bloc = 1, b0 = 0;
     double *Yb = nullptr, *Xb = nullptr, *XHb = nullptr, *QYb = nullptr, *qb = nullptr;
@@ -281,7 +281,8 @@ PassAArgs make_a(duquad_ctx *c) {
     a.va = c->a_va;
     a.skip = c->eps_mode ? c->d_done : nullptr;
     a.lam_hat = c->davg ? c->lam_hat : nullptr;
-    a.use_sell = c->use_sell_a;
+    a.sp_kind = c->kind_a;
+    a.sp_u = c->u_a;
     a.sell = sell_view(c->sell_a);
     return a;
 }
@@ -311,7 +312,8 @@ PassBArgs make_b(duquad_ctx *c) {
     b.va = c->b_va;
     b.skip = c->eps_mode ? c->d_done : nullptr;
     b.gm_sq = c->eps_mode ? c->gm_sq : nullptr;
-    b.use_sell = c->use_sell_b;
+    b.sp_kind = c->kind_b;
+    b.sp_u = c->u_b;
     b.sell = sell_view(c->sell_b);
     return b;
 }
@@ -719,9 +721,9 @@ duquad_status upload_vec(duquad_ctx *ctx, double *dst, const double *src, int64_
 
 // CSR setup: device copies of Q and G (validated), the stacked local [Q_r; G_r]
 // and the local rows of G' (device transpose, deterministic order).
-// SELL-32 is used for a matrix whose mean row length is at most kSellMaxMean and whose padded
-// layout holds at most kSellMaxPad x its nonzeros
-constexpr double kSellMaxMean = 48.0, kSellMaxPad = 1.25;
+// Lane-per-row kernels serve matrices whose mean row length is at most kLaneMaxMean; among them
+// SELL-32 is used when its padded layout holds at most kSellMaxPad x the nonzeros
+constexpr double kLaneMaxMean = 48.0, kSellMaxPad = 1.15;
 
 duquad_status setup_csr(duquad_ctx *ctx, const duquad_problem *prob) {
     cudaStream_t s = ctx->stream;
@@ -814,20 +816,33 @@ duquad_status setup_csr(duquad_ctx *ctx, const duquad_problem *prob) {
     ctx->gs_a = csr_group_size((double)(qnnz + gnnz) / (double)(n + p));
     ctx->gs_b = csr_group_size((double)gnnz / (double)n);
     CK(cudaStreamSynchronize(s));
-    // SELL-32 copies for short rows (one lane per row, coalesced slice columns); the decision is
-    // per matrix and per rank (row sums are the same either way: each row summed in CSR order)
-    if (ctx->opt.sell_path && (double)(qnnz + gnnz) <= kSellMaxMean * (double)(n + p)) {
-        bool ok = false;
-        CK(sell_build(ctx->a_rp, ctx->a_ci, ctx->a_va, ctx->nloc + ctx->ploc, ctx->nloc, ctx->nnz_a, kSellMaxPad,
-                      &ctx->sell_a, &ok, s));
-        ctx->use_sell_a = ok;
-    }
-    if (ctx->opt.sell_path && p > 0 && (double)gnnz <= kSellMaxMean * (double)n) {
-        bool ok = false;
-        CK(sell_build(ctx->b_rp, ctx->b_ci, ctx->b_va, ctx->nloc, ctx->nloc, ctx->nnz_b, kSellMaxPad, &ctx->sell_b,
-                      &ok, s));
-        ctx->use_sell_b = ok;
-    }
+    // Lane-per-row kernels for short rows (kernels_sell.cu).  Lane kernels vs the sub-warp kernels
+    // sum a row in different orders, so that choice uses GLOBAL statistics (every rank alike); the
+    // lane layout (SELL-32 when it pads little, else thread-per-row CSR) is per rank: both sum
+    // each row in CSR order, so the results do not depend on it.
+    auto lane_choice = [&](const int32_t *rp, const int32_t *ci, const double *va, int64_t rows, int64_t nq,
+                           int64_t nnz_loc, double mean, SellStore *st, int *kind, int *u) -> duquad_status {
+        *kind = SPK_CSR;
+        if (!ctx->opt.sell_path || mean > kLaneMaxMean) return DUQUAD_OK;
+        SparsePlan pl;
+        CK(sparse_plan(rp, rows, nq, &pl, s));
+        if ((double)pl.padded <= kSellMaxPad * (double)nnz_loc + 1024.0 && pl.max_len <= 64) {
+            CK(sell_build(rp, ci, va, rows, nq, pl, st, s));
+            *kind = SPK_SELL;
+            *u = lane_unroll(SPK_SELL, pl.max_len, mean);
+        } else {
+            *kind = SPK_ROWT;
+            *u = lane_unroll(SPK_ROWT, pl.max_len, mean);
+        }
+        return DUQUAD_OK;
+    };
+    duquad_status st;
+    if ((st = lane_choice(ctx->a_rp, ctx->a_ci, ctx->a_va, ctx->nloc + ctx->ploc, ctx->nloc, ctx->nnz_a,
+                          (double)(qnnz + gnnz) / (double)(n + p), &ctx->sell_a, &ctx->kind_a, &ctx->u_a)) != DUQUAD_OK)
+        return st;
+    if (p > 0 && (st = lane_choice(ctx->b_rp, ctx->b_ci, ctx->b_va, ctx->nloc, ctx->nloc, ctx->nnz_b,
+                                   (double)gnnz / (double)n, &ctx->sell_b, &ctx->kind_b, &ctx->u_b)) != DUQUAD_OK)
+        return st;
     return DUQUAD_OK;
 }
 
@@ -1211,10 +1226,12 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         }
     }
     if (csr) {   // grid-stride sub-warp SpMV / SELL-32 warp-per-slice, full occupancy
-        ctx->cfg_a = {ctx->num_sms * (ctx->use_sell_a ? sell_blocks_per_sm(0) : csr_blocks_per_sm(0, ctx->gs_a)), 256,
-                      0};   // whole waves
-        ctx->cfg_b = {ctx->num_sms * (ctx->use_sell_b ? sell_blocks_per_sm(1) : csr_blocks_per_sm(1, ctx->gs_b)), 256,
-                      0};
+        ctx->cfg_a = {ctx->num_sms * (ctx->kind_a != SPK_CSR ? lane_blocks_per_sm(0, ctx->kind_a, ctx->u_a)
+                                                             : csr_blocks_per_sm(0, ctx->gs_a)),
+                      256, 0};   // whole waves
+        ctx->cfg_b = {ctx->num_sms * (ctx->kind_b != SPK_CSR ? lane_blocks_per_sm(1, ctx->kind_b, ctx->u_b)
+                                                             : csr_blocks_per_sm(1, ctx->gs_b)),
+                      256, 0};
         CKS(cudaStreamSynchronize(s));
         *out = ctx;
         return DUQUAD_OK;
@@ -2017,7 +2034,7 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
                     : ctx->rho0 ? DUQUAD_PATH_RHO0
                     : ctx->Btot > 1 ? DUQUAD_PATH_BATCHED
                     : ctx->format == DUQUAD_CSR ? DUQUAD_PATH_CSR : DUQUAD_PATH_TWO_PASS;
-        res->sell_mask = (ctx->use_sell_a ? 1 : 0) | (ctx->use_sell_b ? 2 : 0);
+        res->sparse_kernels = ctx->format == DUQUAD_CSR ? ctx->kind_a | (ctx->kind_b << 4) : 0;
         res->outer_iters = K;
         res->inner_iters_total = (int64_t)nout * Kin;
         res->kernel_launches = 1 + (int64_t)nout * (2 * Kin + 1);

@@ -26,16 +26,17 @@ struct OuterParam {
 
 enum PassMode : int { MODE_SOLVE = 0, MODE_LIN = 1 };
 
+// Sparse kernel kinds (kernels_csr.cu, kernels_sell.cu)
+enum SparseKind : int32_t { SPK_CSR = 0, SPK_SELL = 1, SPK_ROWT = 2 };
+
 // SELL-32 view of a sparse matrix (kernels_sell.cu): slice s holds 32 rows; its k-th column of
 // nonzeros is val/col[sptr[s] + 32 k + lane].  Rows form two segments, [0, nq) and [nq, rows),
-// that never share a slice (pass A: Q rows, then G rows).  row == NULL: slice s, lane l is row
-// 32 s + l of the first segment (s < nsl_q), else nq + 32 (s - nsl_q) + l; otherwise row[32 s + l]
-// (-1: an empty lane).
+// that never share a slice (pass A: Q rows, then G rows): slice s, lane l is row 32 s + l of the
+// first segment (s < nsl_q), else row nq + 32 (s - nsl_q) + l (an empty lane past a segment's end).
 struct SellMat {
     const double *val;
     const int32_t *col;
     const int64_t *sptr;   // nsl + 1 element offsets (32 x the slice width apart)
-    const int32_t *row;    // slot -> row map of a length-sorted layout, or NULL
     int64_t nsl, nsl_q, nq, rows;
 };
 
@@ -73,7 +74,8 @@ struct PassAArgs {
     const int32_t *ci;   // column indices
     const double *va;    // values
     const int32_t *skip; // eps_in mode: the inner solve has converged -> the launch does nothing
-    int32_t use_sell;    // CSR input stored as SELL-32 (kernels_sell.cu)
+    int32_t sp_kind;     // SparseKind: sub-warp CSR, SELL-32 or thread-per-row CSR
+    int32_t sp_u;        // lane kernels: nonzeros per load round
     SellMat sell;
 };
 
@@ -106,7 +108,8 @@ struct PassBArgs {
     const double *va;
     const int32_t *skip; // eps_in mode: the inner solve has converged -> the launch does nothing
     double *gm_sq;       // eps_in mode: gm_sq[j] = (y_j - x+_j)^2 (gradient-map test)
-    int32_t use_sell;    // CSR input stored as SELL-32 (kernels_sell.cu)
+    int32_t sp_kind;     // SparseKind: sub-warp CSR, SELL-32 or thread-per-row CSR
+    int32_t sp_u;        // lane kernels: nonzeros per load round
     SellMat sell;
 };
 
@@ -203,24 +206,28 @@ cudaError_t csr_transpose_rows(const int32_t *rp, const int32_t *ci, const doubl
                                int32_t **ci_t, double **va_t, int64_t *nnz_t, cudaStream_t s);
 int csr_group_size(double avg_nnz_per_row);
 
-// kernels_sell.cu: SELL-32 storage built on the device from a (rebased) CSR matrix
+// kernels_sell.cu: lane-per-row sparse kernels (SELL-32 storage built on the device from the
+// rebased local CSR; thread-per-row CSR on the CSR arrays)
 struct SellStore {
     double *val = nullptr;
     int32_t *col = nullptr;
     int64_t *sptr = nullptr;
-    int32_t *row = nullptr;
     int64_t nsl = 0, nsl_q = 0, nq = 0, rows = 0, padded = 0;
 };
-// rows [0, nq) and [nq, rows) sliced separately; rows are grouped by length inside windows of 1024
-// when that pads less.  *ok = false (nothing allocated) if the padded layout exceeds
-// max_pad * nnz (+1024): the CSR kernels stay in use.
+struct SparsePlan {        // row statistics of a local CSR matrix (rows [0, nq) and [nq, rows))
+    int64_t nsl = 0, nsl_q = 0;
+    int64_t padded = 0;    // SELL-32 element count (32 x the longest row of every slice)
+    int32_t max_len = 0;
+};
+cudaError_t sparse_plan(const int32_t *rp, int64_t rows, int64_t nq, SparsePlan *plan, cudaStream_t s);
 cudaError_t sell_build(const int32_t *rp, const int32_t *ci, const double *va, int64_t rows, int64_t nq,
-                       int64_t nnz, double max_pad, SellStore *out, bool *ok, cudaStream_t s);
+                       const SparsePlan &plan, SellStore *out, cudaStream_t s);
 void sell_free(SellStore *st);
 SellMat sell_view(const SellStore &st);
-int sell_blocks_per_sm(int pass);
-cudaError_t launch_pass_a_sell(const PassAArgs &a, int mode, const LaunchCfg &cfg, cudaStream_t s);
-cudaError_t launch_pass_b_sell(const PassBArgs &b, int mode, const LaunchCfg &cfg, cudaStream_t s);
+int lane_unroll(int kind, int64_t max_width, double mean_len);
+int lane_blocks_per_sm(int pass, int kind, int u);
+cudaError_t launch_pass_a_lane(const PassAArgs &a, int mode, const LaunchCfg &cfg, cudaStream_t s);
+cudaError_t launch_pass_b_lane(const PassBArgs &b, int mode, const LaunchCfg &cfg, cudaStream_t s);
 
 // kernels_fused.cu
 bool fused_supported(int64_t n, int64_t ld, size_t smem_optin);

@@ -521,7 +521,7 @@ cudaError_t configure_pass_kernels(size_t smem_a, size_t smem_b) {
 
 cudaError_t launch_pass_a(const PassAArgs &a, int mode, const LaunchCfg &cfg, cudaStream_t s) {
     if (a.row_end <= a.row_begin) return cudaSuccess;
-    if (a.fmt == DUQUAD_CSR) return a.use_sell ? launch_pass_a_sell(a, mode, cfg, s) : launch_pass_a_csr(a, mode, cfg, s);
+    if (a.fmt == DUQUAD_CSR) return a.sp_kind != SPK_CSR ? launch_pass_a_lane(a, mode, cfg, s) : launch_pass_a_csr(a, mode, cfg, s);
     if (mode == MODE_SOLVE)
         k_pass_a<MODE_SOLVE><<<cfg.grid, kThreads, cfg.smem, s>>>(a);
     else
@@ -531,7 +531,7 @@ cudaError_t launch_pass_a(const PassAArgs &a, int mode, const LaunchCfg &cfg, cu
 
 cudaError_t launch_pass_b(const PassBArgs &b, int mode, const LaunchCfg &cfg, cudaStream_t s) {
     if (b.nrows <= 0) return cudaSuccess;
-    if (b.fmt == DUQUAD_CSR) return b.use_sell ? launch_pass_b_sell(b, mode, cfg, s) : launch_pass_b_csr(b, mode, cfg, s);
+    if (b.fmt == DUQUAD_CSR) return b.sp_kind != SPK_CSR ? launch_pass_b_lane(b, mode, cfg, s) : launch_pass_b_csr(b, mode, cfg, s);
     if (mode == MODE_SOLVE)
         k_pass_b<MODE_SOLVE><<<cfg.grid, kThreads, cfg.smem, s>>>(b);
     else

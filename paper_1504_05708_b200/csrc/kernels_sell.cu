@@ -1,26 +1,33 @@
-// SELL-32 sm_100a kernels of the sparse DuQuad inner step (config 4).
+// Lane-per-row sparse kernels of the DuQuad inner step (config 4):
+// SELL-32 for rows of nearly equal length, thread-per-row CSR for short rows of unequal length.
 //
-// The same two passes and row epilogues (epilogue.cuh) as the CSR kernels, with the matrix
-// stored slice-major: 32 consecutive (or, after a windowed sort by length, length-grouped) rows
-// form a slice, and the k-th nonzero of every row of the slice sits in one 32-wide column, so
-// a warp owns a slice, lane l owns row l of it, and every matrix load of the warp is one
-// coalesced 256-byte (values) / 128-byte (indices) request.  The slice width is warp-uniform:
-// no divergence, no row-pointer load on the critical path (the CSR kernels' row-pointer ->
-// index -> gather chain), and each lane sums its row's nonzeros in their CSR order, so the row
-// sums do not depend on the slicing or on the row sharding.  Padding entries carry value 0 and a
-// valid column of the same row (their product adds an exact zero).
+// Both run the same two passes and row epilogues (epilogue.cuh) as the sub-warp CSR kernels
+// (kernels_csr.cu), with one lane per row, so the epilogue's vector accesses are coalesced and
+// each lane sums its row's nonzeros in their CSR order: the row sums do not depend on the storage
+// (SELL or CSR) or on the row sharding.
+//
+// SELL-32: 32 consecutive rows form a slice, and the k-th nonzero of every row of the slice sits
+// in one 32-wide column, so every matrix load of a warp is one coalesced 256-byte (values) /
+// 128-byte (indices) request and the slice width is warp-uniform (no divergence).  A slice costs
+// one load round (U >= the slice width) and one gather round; no row pointer is on the critical
+// path.  Padding entries carry value 0 and a valid column of the same row (an exact zero term).
+// Used when the padding stays small (config 4's pass A: Q rows of 11 and G rows of 8 nonzeros).
+//
+// Thread-per-row CSR: lane l of a warp owns row base + l and walks its own nonzeros.  A warp's 32
+// rows are contiguous in memory, so the lanes' scattered loads hit the same L1 lines round after
+// round (L1-allocating loads, L2 evict-first); no padding and no row permutation.  Used when rows
+// are short but unequal (config 4's pass B: G' rows with Poisson(4) nonzeros, where SELL-32
+// would pad 2.2x and a length-sorted SELL scatters the heavy pass-B epilogue).
 //
 // The paper's observation that sparse data make the method cheap (P:1272-1274, P:1317-1319:
-// "only sparse matrix-vector products") is where this layout pays: the matrix stream is bound by
-// HBM bandwidth, not by the latency of the index chain.
+// "only sparse matrix-vector products") is where these layouts pay: the matrix stream is bound by
+// HBM bandwidth rather than by the latency of the sub-warp kernels' row-pointer -> index chain.
 #include <cuda_runtime.h>
 #include <thrust/device_ptr.h>
 #include <thrust/execution_policy.h>
 #include <thrust/extrema.h>
 #include <thrust/reduce.h>
 #include <thrust/scan.h>
-#include <thrust/sequence.h>
-#include <thrust/sort.h>
 
 #include <algorithm>
 
@@ -31,28 +38,38 @@ namespace dq {
 
 namespace {
 
-constexpr int kSellThreads = 256;
-constexpr int kSellU = 8;   // nonzeros per lane in flight per round (loads issued together)
+constexpr int kLaneThreads = 256;
 
-__device__ __forceinline__ uint64_t sell_evict_first() {
+__device__ __forceinline__ uint64_t evict_first() {
     uint64_t pol;
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
-__device__ __forceinline__ double sell_ld_f64(const double *p, uint64_t pol) {
+// streamed once (SELL): bypass L1
+__device__ __forceinline__ double ld_na_f64(const double *p, uint64_t pol) {
     double r;
     asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
     return r;
 }
-__device__ __forceinline__ int32_t sell_ld_i32(const int32_t *p, uint64_t pol) {
+__device__ __forceinline__ int32_t ld_na_i32(const int32_t *p, uint64_t pol) {
     int32_t r;
     asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+    return r;
+}
+// re-read by neighbouring lanes in later rounds (thread-per-row CSR): allocate in L1
+__device__ __forceinline__ double ld_l1_f64(const double *p, uint64_t pol) {
+    double r;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ int32_t ld_l1_i32(const int32_t *p, uint64_t pol) {
+    int32_t r;
+    asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
     return r;
 }
 
 // row of lane `lane` of slice s (-1: an empty lane of a segment's last slice)
 __device__ __forceinline__ int64_t sell_row(const SellMat &m, int64_t s, int lane) {
-    if (m.row) return m.row[s * 32 + lane];
     if (s < m.nsl_q) {
         const int64_t r = s * 32 + lane;
         return r < m.nq ? r : -1;
@@ -61,32 +78,58 @@ __device__ __forceinline__ int64_t sell_row(const SellMat &m, int64_t s, int lan
     return r < m.rows ? r : -1;
 }
 
-// lane's row . v over the slice [base, base + 32 w): nonzeros in CSR order, U loads in flight
+// lane's row . v over the slice [base, base + 32 w): nonzeros in CSR order, U loads per round
+template <int U>
 __device__ __forceinline__ double sell_dot(const SellMat &m, int64_t base, int w, int lane,
                                            const double *__restrict__ v, uint64_t pol) {
     double acc = 0.0;
     const double *va = m.val + base + lane;
     const int32_t *ci = m.col + base + lane;
-    for (int k0 = 0; k0 < w; k0 += kSellU) {
-        int32_t c[kSellU];
-        double a[kSellU], x[kSellU];
+    for (int k0 = 0; k0 < w; k0 += U) {
+        int32_t c[U];
+        double a[U], x[U];
 #pragma unroll
-        for (int u = 0; u < kSellU; ++u) {
+        for (int u = 0; u < U; ++u) {
             const bool ok = k0 + u < w;   // warp-uniform
-            c[u] = ok ? sell_ld_i32(ci + (int64_t)(k0 + u) * 32, pol) : 0;
-            a[u] = ok ? sell_ld_f64(va + (int64_t)(k0 + u) * 32, pol) : 0.0;
+            c[u] = ok ? ld_na_i32(ci + (int64_t)(k0 + u) * 32, pol) : 0;
+            a[u] = ok ? ld_na_f64(va + (int64_t)(k0 + u) * 32, pol) : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < kSellU; ++u) x[u] = k0 + u < w ? __ldg(v + c[u]) : 0.0;
+        for (int u = 0; u < U; ++u) x[u] = k0 + u < w ? __ldg(v + c[u]) : 0.0;
 #pragma unroll
-        for (int u = 0; u < kSellU; ++u)
+        for (int u = 0; u < U; ++u)
             if (k0 + u < w) acc = fma(a[u], x[u], acc);
     }
     return acc;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kSellThreads) k_pass_a_sell(const PassAArgs a) {
+// lane's own CSR row [lo, lo + len) . v, rounds of U nonzeros (the warp's longest row bounds the
+// trip count; lanes past their row end are predicated off)
+template <int U>
+__device__ __forceinline__ double rowt_dot(const int32_t *__restrict__ ci, const double *__restrict__ va, int32_t lo,
+                                           int32_t len, const double *__restrict__ v, uint64_t pol) {
+    const int32_t wl = __reduce_max_sync(0xffffffffu, len);
+    double acc = 0.0;
+    for (int k0 = 0; k0 < wl; k0 += U) {
+        int32_t c[U];
+        double a[U], x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const bool ok = k0 + u < len;
+            c[u] = ok ? ld_l1_i32(ci + lo + k0 + u, pol) : -1;
+            a[u] = ok ? ld_l1_f64(va + lo + k0 + u, pol) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u] = c[u] >= 0 ? __ldg(v + c[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (c[u] >= 0) acc = fma(a[u], x[u], acc);
+    }
+    return acc;
+}
+
+template <int MODE, int U>
+__global__ void __launch_bounds__(kLaneThreads) k_pass_a_sell(const PassAArgs a) {
     if (a.skip && *a.skip) return;
     const SellMat &m = a.sell;
     const int lane = threadIdx.x & 31;
@@ -96,35 +139,73 @@ __global__ void __launch_bounds__(kSellThreads) k_pass_a_sell(const PassAArgs a)
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const OuterA o = outer_a(a, MODE);
-    const uint64_t pol = sell_evict_first();
+    const uint64_t pol = evict_first();
     for (int64_t s = s_lo + warp; s < s_hi; s += nwarps) {
         const int64_t r = sell_row(m, s, lane);
-        EpiA e{};
-        if (r >= 0) e = epi_a_load(a, MODE, r, o);
         const int64_t base = m.sptr[s];
         const int w = (int)((m.sptr[s + 1] - base) >> 5);
-        const double acc = sell_dot(m, base, w, lane, a.y, pol);
+        EpiA e{};
+        if (r >= 0) e = epi_a_load(a, MODE, r, o);
+        const double acc = sell_dot<U>(m, base, w, lane, a.y, pol);
         if (r >= 0) epi_a_store(a, MODE, r, acc, e, o);
     }
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kSellThreads) k_pass_b_sell(const PassBArgs b) {
+template <int MODE, int U>
+__global__ void __launch_bounds__(kLaneThreads) k_pass_b_sell(const PassBArgs b) {
     if (b.skip && *b.skip) return;
     const SellMat &m = b.sell;
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const double avg_w = avg_weight(b, MODE);
-    const uint64_t pol = sell_evict_first();
+    const uint64_t pol = evict_first();
     for (int64_t s = warp; s < m.nsl; s += nwarps) {
         const int64_t j = sell_row(m, s, lane);
-        EpiB e{};
-        if (j >= 0) e = epi_b_load(b, MODE, j, avg_w);
         const int64_t base = m.sptr[s];
         const int w = (int)((m.sptr[s + 1] - base) >> 5);
-        const double t = sell_dot(m, base, w, lane, b.w, pol);
+        EpiB e{};
+        if (j >= 0) e = epi_b_load(b, MODE, j, avg_w);
+        const double t = sell_dot<U>(m, base, w, lane, b.w, pol);
         if (j >= 0) epi_b_store(b, MODE, j, t, e, avg_w);
+    }
+}
+
+template <int MODE, int U>
+__global__ void __launch_bounds__(kLaneThreads) k_pass_a_rowt(const PassAArgs a) {
+    if (a.skip && *a.skip) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const OuterA o = outer_a(a, MODE);
+    const uint64_t pol = evict_first();
+    for (int64_t base = a.row_begin + warp * 32; base < a.row_end; base += nwarps * 32) {
+        const int64_t r = base + lane;
+        const bool v = r < a.row_end;
+        const int32_t lo = v ? a.rp[r] : 0, len = v ? a.rp[r + 1] - lo : 0;
+        EpiA e{};
+        if (v) e = epi_a_load(a, MODE, r, o);
+        const double acc = rowt_dot<U>(a.ci, a.va, lo, len, a.y, pol);
+        if (v) epi_a_store(a, MODE, r, acc, e, o);
+    }
+}
+
+template <int MODE, int U>
+__global__ void __launch_bounds__(kLaneThreads) k_pass_b_rowt(const PassBArgs b) {
+    if (b.skip && *b.skip) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const double avg_w = avg_weight(b, MODE);
+    const uint64_t pol = evict_first();
+    for (int64_t base = warp * 32; base < b.nrows; base += nwarps * 32) {
+        const int64_t j = base + lane;
+        const bool v = j < b.nrows;
+        const int32_t lo = v ? b.rp[j] : 0, len = v ? b.rp[j + 1] - lo : 0;
+        EpiB e{};
+        if (v) e = epi_b_load(b, MODE, j, avg_w);
+        const double t = rowt_dot<U>(b.ci, b.va, lo, len, b.w, pol);
+        if (v) epi_b_store(b, MODE, j, t, e, avg_w);
     }
 }
 
@@ -134,50 +215,25 @@ __global__ void k_row_len(const int32_t *rp, int64_t rows, int32_t *len) {
     if (i < rows) len[i] = rp[i + 1] - rp[i];
 }
 
-// sort keys: (window, -length); windows of `sigma` rows never straddle the two segments
-__global__ void k_sort_keys(const int32_t *len, int64_t rows, int64_t nq, int64_t sigma, int64_t *keys) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= rows) return;
-    const int64_t wq = (nq + sigma - 1) / sigma;
-    const int64_t win = i < nq ? i / sigma : wq + (i - nq) / sigma;
-    keys[i] = (win << 32) | (int64_t)(0x7fffffff - len[i]);
-}
-
-// row id of every (slice, lane) position from the sorted order (perm[t] = t-th row in sort order)
-__global__ void k_slot_rows(const int32_t *perm, int64_t rows, int64_t nq, int64_t nsl_q, int64_t nsl,
-                            int32_t *row) {
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= nsl * 32) return;
-    const int64_t s = t >> 5, l = t & 31;
-    int64_t pos;
-    bool ok;
-    if (s < nsl_q) {
-        pos = s * 32 + l;
-        ok = pos < nq;
-    } else {
-        pos = nq + (s - nsl_q) * 32 + l;
-        ok = pos < rows;
-    }
-    row[t] = ok ? (perm ? perm[pos] : (int32_t)pos) : -1;
-}
-
-__global__ void k_slice_width(const int32_t *row, const int32_t *len, int64_t nsl, int64_t *width) {
+// 32 x the longest row of every slice (slices never straddle the two segments)
+__global__ void k_slice_width(const int32_t *len, int64_t rows, int64_t nq, int64_t nsl_q, int64_t nsl,
+                              int64_t *width) {
     const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (s >= nsl) return;
+    const int64_t r0 = s < nsl_q ? s * 32 : nq + (s - nsl_q) * 32;
+    const int64_t r1 = s < nsl_q ? (r0 + 32 < nq ? r0 + 32 : nq) : (r0 + 32 < rows ? r0 + 32 : rows);
     int32_t w = 0;
-    for (int l = 0; l < 32; ++l) {
-        const int32_t r = row[s * 32 + l];
-        if (r >= 0) w = max(w, len[r]);
-    }
+    for (int64_t r = r0; r < r1; ++r) w = max(w, len[r]);
     width[s] = 32 * (int64_t)w;
 }
 
-__global__ void k_sell_fill(const int32_t *rp, const int32_t *ci, const double *va, const int32_t *row,
-                            const int64_t *sptr, int64_t nsl, double *sv, int32_t *sc) {
+__global__ void k_sell_fill(const int32_t *rp, const int32_t *ci, const double *va, int64_t rows, int64_t nq,
+                            int64_t nsl_q, int64_t nsl, const int64_t *sptr, double *sv, int32_t *sc) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= nsl * 32) return;
     const int64_t s = t >> 5, l = t & 31;
-    const int32_t r = row[t];
+    const int64_t r = s < nsl_q ? (s * 32 + l < nq ? s * 32 + l : -1)
+                                : (nq + (s - nsl_q) * 32 + l < rows ? nq + (s - nsl_q) * 32 + l : -1);
     const int32_t b = r >= 0 ? rp[r] : 0, len = r >= 0 ? rp[r + 1] - b : 0;
     const int32_t pad_col = len > 0 ? ci[b + len - 1] : 0;
     const int64_t base = sptr[s], w = (sptr[s + 1] - base) >> 5;
@@ -189,21 +245,10 @@ __global__ void k_sell_fill(const int32_t *rp, const int32_t *ci, const double *
 
 inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
-template <typename T>
-cudaError_t zalloc(T **p, int64_t count) {
-    *p = nullptr;
-    return cudaMalloc((void **)p, (size_t)std::max<int64_t>(count, 2) * sizeof(T));
-}
-
-// padded element count of the layout whose slot rows are in `row`
-cudaError_t padded_count(const int32_t *row, const int32_t *len, int64_t nsl, int64_t *width, int64_t *total,
-                         cudaStream_t s) {
-    k_slice_width<<<nblk(std::max<int64_t>(nsl, 1), 256), 256, 0, s>>>(row, len, nsl, width);
-    cudaError_t e = cudaGetLastError();
-    if (e) return e;
-    thrust::device_ptr<int64_t> wp(width);
-    *total = nsl > 0 ? thrust::reduce(thrust::cuda::par.on(s), wp, wp + nsl, (int64_t)0) : 0;
-    return cudaGetLastError();
+template <typename K>
+int occ_of(K kern) {
+    int b = 0;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kLaneThreads, 0) == cudaSuccess && b > 0 ? b : 1;
 }
 
 }  // namespace
@@ -212,100 +257,69 @@ void sell_free(SellStore *st) {
     if (st->val) cudaFree(st->val);
     if (st->col) cudaFree(st->col);
     if (st->sptr) cudaFree(st->sptr);
-    if (st->row) cudaFree(st->row);
     *st = SellStore{};
 }
 
+cudaError_t sparse_plan(const int32_t *rp, int64_t rows, int64_t nq, SparsePlan *plan, cudaStream_t s) {
+    *plan = SparsePlan{};
+    plan->nsl_q = (nq + 31) / 32;
+    plan->nsl = plan->nsl_q + (rows - nq + 31) / 32;
+    if (rows <= 0) return cudaSuccess;
+    int32_t *len = nullptr;
+    int64_t *width = nullptr;
+    cudaError_t e = cudaMalloc(&len, rows * sizeof(int32_t));
+    if (!e) e = cudaMalloc(&width, (plan->nsl + 1) * sizeof(int64_t));
+    if (!e) {
+        k_row_len<<<nblk(rows, 256), 256, 0, s>>>(rp, rows, len);
+        k_slice_width<<<nblk(plan->nsl, 256), 256, 0, s>>>(len, rows, nq, plan->nsl_q, plan->nsl, width);
+        e = cudaGetLastError();
+    }
+    if (!e) {
+        thrust::device_ptr<int64_t> wp(width);
+        thrust::device_ptr<int32_t> lp(len);
+        plan->padded = thrust::reduce(thrust::cuda::par.on(s), wp, wp + plan->nsl, (int64_t)0);
+        plan->max_len = *thrust::max_element(thrust::cuda::par.on(s), lp, lp + rows);
+        e = cudaGetLastError();
+    }
+    if (len) cudaFree(len);
+    if (width) cudaFree(width);
+    return e;
+}
+
 cudaError_t sell_build(const int32_t *rp, const int32_t *ci, const double *va, int64_t rows, int64_t nq,
-                       int64_t nnz, double max_pad, SellStore *out, bool *ok, cudaStream_t s) {
-    *ok = false;
+                       const SparsePlan &plan, SellStore *out, cudaStream_t s) {
     *out = SellStore{};
-    const int64_t nsl_q = (nq + 31) / 32, nsl = nsl_q + (rows - nq + 31) / 32;
+    const int64_t nsl_q = plan.nsl_q, nsl = plan.nsl;
     if (rows <= 0 || nsl <= 0) return cudaSuccess;
-    cudaError_t e;
-    int32_t *len = nullptr, *row_id = nullptr, *row_srt = nullptr, *perm = nullptr;
-    int64_t *width = nullptr, *keys = nullptr;
-    auto cleanup = [&]() {
-        for (void *q : {(void *)len, (void *)row_id, (void *)row_srt, (void *)perm, (void *)width, (void *)keys})
-            if (q) cudaFree(q);
-    };
-    if ((e = zalloc(&len, rows)) || (e = zalloc(&row_id, nsl * 32)) || (e = zalloc(&width, nsl + 1))) {
-        cleanup();
-        return e;
-    }
-    k_row_len<<<nblk(rows, 256), 256, 0, s>>>(rp, rows, len);
-    k_slot_rows<<<nblk(nsl * 32, 256), 256, 0, s>>>(nullptr, rows, nq, nsl_q, nsl, row_id);
-    int64_t pad_id = 0, pad_srt = INT64_MAX;
-    if ((e = padded_count(row_id, len, nsl, width, &pad_id, s))) {
-        cleanup();
-        return e;
-    }
-    // rows of unequal lengths: group them by length inside windows of 1024 rows (32 slices), so a
-    // slice's rows have nearly equal lengths; the epilogue's scattered row accesses stay inside a
-    // window (32 KB of each n-vector)
-    constexpr int64_t kSigma = 1024;
-    const bool try_sort = (double)pad_id > 1.05 * (double)nnz + 32.0 * 32.0;
-    if (try_sort) {
-        if ((e = zalloc(&keys, rows)) || (e = zalloc(&perm, rows)) || (e = zalloc(&row_srt, nsl * 32))) {
-            cleanup();
-            return e;
-        }
-        k_sort_keys<<<nblk(rows, 256), 256, 0, s>>>(len, rows, nq, kSigma, keys);
-        thrust::device_ptr<int64_t> kp(keys);
-        thrust::device_ptr<int32_t> pp(perm);
-        thrust::sequence(thrust::cuda::par.on(s), pp, pp + rows);
-        thrust::stable_sort_by_key(thrust::cuda::par.on(s), kp, kp + rows, pp);
-        k_slot_rows<<<nblk(nsl * 32, 256), 256, 0, s>>>(perm, rows, nq, nsl_q, nsl, row_srt);
-        if ((e = padded_count(row_srt, len, nsl, width, &pad_srt, s))) {
-            cleanup();
-            return e;
-        }
-    }
-    const bool sorted = pad_srt < pad_id;
-    const int64_t padded = sorted ? pad_srt : pad_id;
-    if ((double)padded > max_pad * (double)nnz + 32.0 * 32.0) {   // too ragged: keep the CSR kernels
-        cleanup();
-        return cudaGetLastError();
-    }
-    if (!sorted && (e = padded_count(row_id, len, nsl, width, &pad_id, s))) {   // widths of the kept layout
-        cleanup();
-        return e;
-    }
     SellStore st{};
     st.nsl = nsl;
     st.nsl_q = nsl_q;
     st.nq = nq;
     st.rows = rows;
-    st.padded = padded;
-    if ((e = zalloc(&st.sptr, nsl + 1)) || (e = zalloc(&st.val, padded)) || (e = zalloc(&st.col, padded))) {
-        sell_free(&st);
-        cleanup();
-        return e;
+    st.padded = plan.padded;
+    cudaError_t e = cudaMalloc(&st.sptr, (nsl + 1) * sizeof(int64_t));
+    if (!e) e = cudaMalloc(&st.val, std::max<int64_t>(plan.padded, 2) * sizeof(double));
+    if (!e) e = cudaMalloc(&st.col, std::max<int64_t>(plan.padded, 2) * sizeof(int32_t));
+    int32_t *len = nullptr;
+    if (!e) e = cudaMalloc(&len, rows * sizeof(int32_t));
+    if (!e) {
+        k_row_len<<<nblk(rows, 256), 256, 0, s>>>(rp, rows, len);
+        k_slice_width<<<nblk(nsl, 256), 256, 0, s>>>(len, rows, nq, nsl_q, nsl, st.sptr);
+        e = cudaMemsetAsync(st.sptr + nsl, 0, sizeof(int64_t), s);
     }
-    {
-        thrust::device_ptr<int64_t> wp(width), sp(st.sptr);
-        cudaMemsetAsync(width + nsl, 0, sizeof(int64_t), s);
-        thrust::exclusive_scan(thrust::cuda::par.on(s), wp, wp + nsl + 1, sp);
+    if (!e) {
+        thrust::device_ptr<int64_t> sp(st.sptr);
+        thrust::exclusive_scan(thrust::cuda::par.on(s), sp, sp + nsl + 1, sp);
+        k_sell_fill<<<nblk(nsl * 32, 256), 256, 0, s>>>(rp, ci, va, rows, nq, nsl_q, nsl, st.sptr, st.val, st.col);
+        e = cudaGetLastError();
     }
-    const int32_t *slot_rows = sorted ? row_srt : row_id;
-    k_sell_fill<<<nblk(nsl * 32, 256), 256, 0, s>>>(rp, ci, va, slot_rows, st.sptr, nsl, st.val, st.col);
-    if ((e = cudaGetLastError())) {
-        sell_free(&st);
-        cleanup();
-        return e;
-    }
-    if (sorted) {   // keep the slot -> row map; the identity layout computes it
-        st.row = row_srt;
-        row_srt = nullptr;
-    }
-    e = cudaStreamSynchronize(s);
-    cleanup();
+    if (!e) e = cudaStreamSynchronize(s);
+    if (len) cudaFree(len);
     if (e) {
         sell_free(&st);
         return e;
     }
     *out = st;
-    *ok = true;
     return cudaSuccess;
 }
 
@@ -314,7 +328,6 @@ SellMat sell_view(const SellStore &st) {
     m.val = st.val;
     m.col = st.col;
     m.sptr = st.sptr;
-    m.row = st.row;
     m.nsl = st.nsl;
     m.nsl_q = st.nsl_q;
     m.nq = st.nq;
@@ -322,30 +335,65 @@ SellMat sell_view(const SellStore &st) {
     return m;
 }
 
-int sell_blocks_per_sm(int pass) {
-    int b = 0;
-    cudaError_t e = pass == 0 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_pass_a_sell<MODE_SOLVE>,
-                                                                               kSellThreads, 0)
-                              : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_pass_b_sell<MODE_SOLVE>,
-                                                                               kSellThreads, 0);
-    return e == cudaSuccess && b > 0 ? b : 1;
+int lane_unroll(int kind, int64_t max_width, double mean_len) {
+    if (kind == SPK_SELL) return max_width <= 4 ? 4 : max_width <= 8 ? 8 : max_width <= 12 ? 12 : 16;
+    return mean_len <= 6.0 ? 4 : 8;
 }
 
-cudaError_t launch_pass_a_sell(const PassAArgs &a, int mode, const LaunchCfg &cfg, cudaStream_t s) {
+#define DQ_LANE_DISPATCH(KERN, MODE, U, GRID, ARG)                         \
+    switch (U) {                                                            \
+        case 4: KERN<MODE, 4><<<GRID, kLaneThreads, 0, s>>>(ARG); break;     \
+        case 8: KERN<MODE, 8><<<GRID, kLaneThreads, 0, s>>>(ARG); break;     \
+        case 12: KERN<MODE, 12><<<GRID, kLaneThreads, 0, s>>>(ARG); break;   \
+        default: KERN<MODE, 16><<<GRID, kLaneThreads, 0, s>>>(ARG); break;   \
+    }
+
+int lane_blocks_per_sm(int pass, int kind, int u) {
+    if (pass == 0) {
+        if (kind == SPK_SELL)
+            return u == 4 ? occ_of(k_pass_a_sell<MODE_SOLVE, 4>) : u == 8 ? occ_of(k_pass_a_sell<MODE_SOLVE, 8>)
+                   : u == 12 ? occ_of(k_pass_a_sell<MODE_SOLVE, 12>) : occ_of(k_pass_a_sell<MODE_SOLVE, 16>);
+        return u == 4 ? occ_of(k_pass_a_rowt<MODE_SOLVE, 4>) : occ_of(k_pass_a_rowt<MODE_SOLVE, 8>);
+    }
+    if (kind == SPK_SELL)
+        return u == 4 ? occ_of(k_pass_b_sell<MODE_SOLVE, 4>) : u == 8 ? occ_of(k_pass_b_sell<MODE_SOLVE, 8>)
+               : u == 12 ? occ_of(k_pass_b_sell<MODE_SOLVE, 12>) : occ_of(k_pass_b_sell<MODE_SOLVE, 16>);
+    return u == 4 ? occ_of(k_pass_b_rowt<MODE_SOLVE, 4>) : occ_of(k_pass_b_rowt<MODE_SOLVE, 8>);
+}
+
+cudaError_t launch_pass_a_lane(const PassAArgs &a, int mode, const LaunchCfg &cfg, cudaStream_t s) {
     if (a.row_end <= a.row_begin) return cudaSuccess;
-    if (mode == MODE_SOLVE)
-        k_pass_a_sell<MODE_SOLVE><<<cfg.grid, kSellThreads, 0, s>>>(a);
-    else
-        k_pass_a_sell<MODE_LIN><<<cfg.grid, kSellThreads, 0, s>>>(a);
+    if (a.sp_kind == SPK_SELL) {
+        if (mode == MODE_SOLVE) {
+            DQ_LANE_DISPATCH(k_pass_a_sell, MODE_SOLVE, a.sp_u, cfg.grid, a);
+        } else {
+            DQ_LANE_DISPATCH(k_pass_a_sell, MODE_LIN, a.sp_u, cfg.grid, a);
+        }
+    } else if (mode == MODE_SOLVE) {
+        if (a.sp_u == 4) k_pass_a_rowt<MODE_SOLVE, 4><<<cfg.grid, kLaneThreads, 0, s>>>(a);
+        else k_pass_a_rowt<MODE_SOLVE, 8><<<cfg.grid, kLaneThreads, 0, s>>>(a);
+    } else {
+        if (a.sp_u == 4) k_pass_a_rowt<MODE_LIN, 4><<<cfg.grid, kLaneThreads, 0, s>>>(a);
+        else k_pass_a_rowt<MODE_LIN, 8><<<cfg.grid, kLaneThreads, 0, s>>>(a);
+    }
     return cudaGetLastError();
 }
 
-cudaError_t launch_pass_b_sell(const PassBArgs &b, int mode, const LaunchCfg &cfg, cudaStream_t s) {
+cudaError_t launch_pass_b_lane(const PassBArgs &b, int mode, const LaunchCfg &cfg, cudaStream_t s) {
     if (b.nrows <= 0) return cudaSuccess;
-    if (mode == MODE_SOLVE)
-        k_pass_b_sell<MODE_SOLVE><<<cfg.grid, kSellThreads, 0, s>>>(b);
-    else
-        k_pass_b_sell<MODE_LIN><<<cfg.grid, kSellThreads, 0, s>>>(b);
+    if (b.sp_kind == SPK_SELL) {
+        if (mode == MODE_SOLVE) {
+            DQ_LANE_DISPATCH(k_pass_b_sell, MODE_SOLVE, b.sp_u, cfg.grid, b);
+        } else {
+            DQ_LANE_DISPATCH(k_pass_b_sell, MODE_LIN, b.sp_u, cfg.grid, b);
+        }
+    } else if (mode == MODE_SOLVE) {
+        if (b.sp_u == 4) k_pass_b_rowt<MODE_SOLVE, 4><<<cfg.grid, kLaneThreads, 0, s>>>(b);
+        else k_pass_b_rowt<MODE_SOLVE, 8><<<cfg.grid, kLaneThreads, 0, s>>>(b);
+    } else {
+        if (b.sp_u == 4) k_pass_b_rowt<MODE_LIN, 4><<<cfg.grid, kLaneThreads, 0, s>>>(b);
+        else k_pass_b_rowt<MODE_LIN, 8><<<cfg.grid, kLaneThreads, 0, s>>>(b);
+    }
     return cudaGetLastError();
 }
 

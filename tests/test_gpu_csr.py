@@ -172,11 +172,14 @@ def test_csr_empty_rows(torch_cuda):
         assert relerr(a, b) <= 1e-9, relerr(a, b)
 
 
-# ------------------------------------------------------------------ SELL-32 layout (sell_path)
+# ------------------------------------------------------------------ lane-per-row kernels (sell_path)
+SELL, ROWT = 1, 2
+
+
 def _skewed(n=2500, p=900, seed=11):
-    """Rows of very different lengths: a banded Q plus a few denser rows and G rows with 1..40
-    nonzeros, so the SELL builder groups rows by length (the sorted layout) while the padding stays
-    under its 25 % cap."""
+    """Rows of very different lengths: a banded Q plus a few denser symmetric rows, and G rows with
+    1..40 nonzeros (mean 20.5), so SELL-32 would pad too much and both passes take the
+    thread-per-row CSR kernels."""
     rng = np.random.default_rng(seed)
     base = qpgen.sparse_banded_eq(n=n, p=p, seed=seed)
     Q = base.Q.tolil()
@@ -200,20 +203,21 @@ def _skewed(n=2500, p=900, seed=11):
     return qpgen.SparseQP(Q, base.q, G, g, base.lb, base.ub, cone)
 
 
-@pytest.mark.parametrize("maker", ["banded", "skewed"])
+@pytest.mark.parametrize("maker,kinds", [("banded", (SELL, ROWT)), ("skewed", (ROWT, ROWT))])
 @pytest.mark.parametrize("alg", ["DGM", "DFGM"])
-def test_sell_layout_vs_csr_kernels_and_oracle(torch_cuda, maker, alg):
-    """The SELL-32 kernels (identity slices for the banded config-4 family, length-sorted slices
-    for skewed rows) against the CSR kernels (same per-row sums up to summation order: 1e-12) and
-    the oracle (1e-9), with the per-outer trace."""
+def test_lane_kernels_vs_subwarp_kernels_and_oracle(torch_cuda, maker, kinds, alg):
+    """The lane-per-row kernels -- SELL-32 for the banded config-4 family's [Q;G] (rows of 11 and 8
+    nonzeros), thread-per-row CSR for its G' (Poisson(4) rows) and for skewed rows -- against the
+    sub-warp CSR kernels (same row sums up to summation order: 1e-12) and the oracle (1e-9), with
+    the per-outer trace."""
     prob = qpgen.sparse_banded_eq(n=3001, p=1201, seed=2) if maker == "banded" else _skewed()
     rho = 5.0 if maker == "banded" else 2.0
     L_in, L_d, _ = _consts_dense(prob, rho, 0.5)
     a = _gpu(prob, rho, alg, 6, 7, L_in, L_d, trace=True, torch=torch_cuda)
     info = a["solver"].solve(alg, 6, 7)
-    assert info["path"] == 5 and info["sell_mask"] == 3, info
+    assert info["path"] == 5 and info["sparse_kernels"] == kinds[0] | (kinds[1] << 4), info
     b = _gpu(prob, rho, alg, 6, 7, L_in, L_d, sell_path=False)
-    assert b["solver"].solve(alg, 6, 7)["sell_mask"] == 0
+    assert b["solver"].solve(alg, 6, 7)["sparse_kernels"] == 0
     for k in ("x_last", "x_avg", "lam"):
         assert relerr(a[k], b[k]) <= 1e-12, k
     r = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho, alg, 6, 7, L_in, L_d,
@@ -223,53 +227,52 @@ def test_sell_layout_vs_csr_kernels_and_oracle(torch_cuda, maker, alg):
     b["solver"].close()
 
 
-def test_sell_is_deterministic_and_serves_lipschitz_and_residuals(torch_cuda):
-    """Two SELL solves are bitwise identical (fixed per-row order); the MODE_LIN launches
-    (Lanczos, residuals: Q rows only / G rows only sub-ranges) run on the SELL storage and match
-    the CSR kernels."""
+def test_lane_kernels_deterministic_and_serve_lipschitz_and_residuals(torch_cuda):
+    """Two lane-kernel solves are bitwise identical (fixed per-row order); the MODE_LIN launches
+    (Lanczos, residuals: Q-rows-only / G-rows-only sub-ranges of the stacked SELL storage) run on
+    the lane kernels and match the sub-warp kernels."""
     from paper_1504_05708_b200 import Solver
-    prob = _skewed(seed=12)
-    L_in, L_d, _ = _consts_dense(prob, 2.0, 0.5)
-    outs, lips, res = [], [], []
-    for sell in (True, True, False):
-        s = Solver(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho=2.0, lambda_min_lb=0.5,
-                   sell_path=sell)
-        lips.append(s.lipschitz(iters=60, safety=0.0))
-        s.set_constants(L_in, L_d)
-        s.solve("DFGM", 5, 6)
-        outs.append(s.result())
-        res.append(s.residuals("last"))
-        s.close()
-    for x, y in zip(outs[0], outs[1]):
-        assert np.array_equal(x, y)
-    for x, y in zip(outs[0], outs[2]):
-        assert relerr(x, y) <= 1e-12
-    assert np.allclose(lips[0], lips[2], rtol=1e-10, atol=0)
-    assert np.allclose(res[0], res[2], rtol=1e-10, atol=1e-12)
+    for prob, rho in ((qpgen.sparse_banded_eq(n=2000, p=700, seed=12), 5.0), (_skewed(seed=12), 2.0)):
+        L_in, L_d, _ = _consts_dense(prob, rho, 0.5)
+        outs, lips, res = [], [], []
+        for sell in (True, True, False):
+            s = Solver(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho=rho, lambda_min_lb=0.5,
+                       sell_path=sell)
+            lips.append(s.lipschitz(iters=60, safety=0.0))
+            s.set_constants(L_in, L_d)
+            s.solve("DFGM", 5, 6)
+            outs.append(s.result())
+            res.append(s.residuals("last"))
+            s.close()
+        for x, y in zip(outs[0], outs[1]):
+            assert np.array_equal(x, y)
+        for x, y in zip(outs[0], outs[2]):
+            assert relerr(x, y) <= 1e-12
+        assert np.allclose(lips[0], lips[2], rtol=1e-10, atol=0)
+        assert np.allclose(res[0], res[2], rtol=1e-10, atol=1e-12)
 
 
-def test_sell_too_ragged_falls_back_to_csr(torch_cuda):
-    """A G whose rows cannot be sliced without > 25 % padding (one row holding most nonzeros in
-    every window) keeps the CSR kernels for that pass; results still match the oracle."""
+def test_long_rows_keep_the_subwarp_kernels(torch_cuda):
+    """Mean row length above 48 (G rows of 80 nonzeros): both passes keep the sub-warp CSR
+    kernels; a G with one 400-nonzero row per 32 rows (SELL would pad > 15 %) takes thread-per-row
+    CSR for [Q;G].  Both agree with the oracle."""
     from paper_1504_05708_b200 import Solver
     rng = np.random.default_rng(5)
-    n, p = 1500, 64
-    base = qpgen.sparse_banded_eq(n=n, p=p, seed=5)
-    lens = np.ones(p, dtype=int)
-    lens[::32] = 400                                   # one long row per 32-row slice
-    rows = np.repeat(np.arange(p), lens)
-    cols = np.concatenate([np.sort(rng.choice(n, k, replace=False)) for k in lens])
-    G = sp.csr_matrix((rng.standard_normal(len(cols)), (rows, cols)), shape=(p, n))
-    G.sort_indices()
-    g = -(G @ rng.uniform(-0.5, 0.5, n))
-    prob = qpgen.SparseQP(base.Q, base.q, G, g, base.lb, base.ub, base.cone)
-    L_in, L_d, _ = _consts_dense(prob, 5.0, 0.5)
-    s = Solver(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho=5.0)
-    s.set_constants(L_in, L_d)
-    info = s.solve("DFGM", 3, 4)
-    assert info["sell_mask"] & 1 == 0          # stacked [Q;G]: too ragged
-    got = s.result()
-    s.close()
-    r = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 5.0, "DFGM", 3, 4, L_in, L_d)
-    for a_, b_ in zip(got, (r.x_last, r.x_avg, r.lam)):
-        assert relerr(a_, b_) <= TOL
+    for n, p, lens, kind_a in ((200, 400, np.full(400, 80), 0), (1500, 64, np.where(np.arange(64) % 32 == 0, 400, 1), ROWT)):
+        base = qpgen.sparse_banded_eq(n=n, p=p, seed=5)
+        rows = np.repeat(np.arange(p), lens)
+        cols = np.concatenate([np.sort(rng.choice(n, k, replace=False)) for k in lens])
+        G = sp.csr_matrix((rng.standard_normal(len(cols)), (rows, cols)), shape=(p, n))
+        G.sort_indices()
+        g = -(G @ rng.uniform(-0.5, 0.5, n))
+        prob = qpgen.SparseQP(base.Q, base.q, G, g, base.lb, base.ub, base.cone)
+        L_in, L_d, _ = _consts_dense(prob, 5.0, 0.5)
+        s = Solver(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho=5.0)
+        s.set_constants(L_in, L_d)
+        info = s.solve("DFGM", 3, 4)
+        assert info["sparse_kernels"] & 15 == kind_a, info["sparse_kernels"]
+        got = s.result()
+        s.close()
+        r = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 5.0, "DFGM", 3, 4, L_in, L_d)
+        for a_, b_ in zip(got, (r.x_last, r.x_avg, r.lam)):
+            assert relerr(a_, b_) <= TOL
