@@ -843,6 +843,15 @@ duquad_status setup_csr(duquad_ctx *ctx, const duquad_problem *prob) {
     if (p > 0 && (st = lane_choice(ctx->b_rp, ctx->b_ci, ctx->b_va, ctx->nloc, ctx->nloc, ctx->nnz_b,
                                    (double)gnnz / (double)n, &ctx->sell_b, &ctx->kind_b, &ctx->u_b)) != DUQUAD_OK)
         return st;
+    // measurement overrides (scripts/sparse_sweep.py): kind / load-round width per pass
+    auto env_int = [](const char *k, int d) { const char *v = getenv(k); return v ? atoi(v) : d; };
+    if (ctx->kind_a == SPK_ROWT || (ctx->kind_a == SPK_SELL && env_int("DUQUAD_SPK_A", 1) == SPK_ROWT)) {
+        ctx->kind_a = SPK_ROWT;
+        ctx->u_a = env_int("DUQUAD_LANE_UA", ctx->u_a == 4 ? 4 : 8) <= 4 ? 4 : 8;
+    } else if (ctx->kind_a == SPK_SELL) {
+        ctx->u_a = env_int("DUQUAD_LANE_UA", ctx->u_a);
+    }
+    if (ctx->kind_b == SPK_ROWT) ctx->u_b = env_int("DUQUAD_LANE_UB", ctx->u_b) <= 4 ? 4 : 8;
     return DUQUAD_OK;
 }
 
