@@ -182,6 +182,11 @@ typedef struct {
                               copy of the matrix) when that pads at most 15 %, else
                               thread-per-row CSR.  Both sum each row in CSR order.  0: the
                               sub-warp CSR kernels (a group of lanes per row, tree sums)      */
+    int32_t pair_rows;     /* 1 (default): a batched QP whose constraint rows come in +/- pairs,
+                              G = [G_t; -G_t] (two-sided bounds, e.g. config 3's |x_k| <= 5),
+                              streams [Q; G_t] in pass A (the bottom rows' product is -(G_t y),
+                              exactly) and forms G'w as G_t'(w_top - w_bottom) in pass B: half the
+                              G work, the same step.  0: the unpaired matrices             */
 } duquad_options;
 
 /* Per-solve report. */

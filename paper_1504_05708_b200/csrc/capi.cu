@@ -67,6 +67,9 @@ struct duquad_ctx {
     double *Yb = nullptr, *Xb = nullptr, *XHb = nullptr, *QYb = nullptr, *qb = nullptr;
     double *Wb = nullptr, *gb = nullptr, *mub = nullptr, *lpb = nullptr;
     double *hb = nullptr;   // batched: h = mu + rho g per (QP, G row), refreshed by every DFOM step
+    int64_t pairP = 0;       // batched, G = [G_t; -G_t] (options.pair_rows): P = p / 2 paired rows
+    double *Db = nullptr;    // paired rows: d = w_top - w_bottom per (QP, pair), stride ldd
+    int64_t ldd = 0;
     // rho = 0 specialisation (K3): second y replica (ping-pong) and c = q + G'mu
     bool rho0 = false;
     bool davg = false;
@@ -170,7 +173,7 @@ void free_all(duquad_ctx *c) {
     double *ds[] = {c->A,   c->GT,  c->y_full, c->w_full, c->qy,       c->x,        c->xhat,     c->q,
                     c->lb,  c->ub,  c->g,      c->mu,     c->lam_prev, c->lz_vprev, c->lz_w,     c->scal,
                     c->partials, c->Yb, c->Xb, c->XHb,   c->QYb,      c->qb,       c->Wb,       c->gb,
-                    c->mub, c->lpb, c->hb, c->d_beta, c->y_full2, c->cvec, c->ws, c->lam_hat, c->lhb, c->Hq, c->ck_x, c->ck_mu, c->ck_lp, c->ck_xh, c->fpart, c->rs_out};
+                    c->mub, c->lpb, c->hb, c->Db, c->d_beta, c->y_full2, c->cvec, c->ws, c->lam_hat, c->lhb, c->Hq, c->ck_x, c->ck_mu, c->ck_lp, c->ck_xh, c->fpart, c->rs_out};
     for (double *d : ds)
         if (d) cudaFree(d);
     if (c->cone) cudaFree(c->cone);
@@ -555,8 +558,10 @@ BatchedArgs make_batched(duquad_ctx *c, int pass) {
     ba.sn = c->ld;
     ba.sp = std::max<int64_t>(c->ldp, 2);
     ba.N = c->Bloc;
+    ba.pairP = c->pairP;
+    ba.sw = c->pairP ? c->ldd : ba.sp;
     ba.a.qy = c->QYb;
-    ba.a.w = c->Wb;
+    ba.a.w = c->pairP ? c->Db : c->Wb;
     ba.a.g = c->gb;
     ba.a.mu = c->mub;
     ba.a.lam_prev = c->lpb;
@@ -572,20 +577,21 @@ BatchedArgs make_batched(duquad_ctx *c, int pass) {
     ba.b.x = c->Xb;
     ba.b.y = c->Yb;
     ba.b.xhat = c->XHb;
-    if (pass == 0) {   // [Q;G] (n+p x n) . Y
+    if (pass == 0) {   // [Q;G] (n+p x n) . Y  (paired rows: [Q;G_t], the first n + P rows of [Q;G])
         ba.Aop = c->A;
         ba.lda = c->ld;
-        ba.M = c->n + c->p;
+        ba.M = c->n + (c->pairP ? c->pairP : c->p);
         ba.Bop = c->Yb;
         ba.ldb = c->ld;
         ba.K = c->ld;
-    } else {           // G' (n x p) . W
+    } else {           // G' (n x p) . W  (paired rows: G_t' . D over the first ldd columns of G'; D's
+                       // zero padding cancels the bottom rows' columns P .. ldd - 1)
         ba.Aop = c->GT;
         ba.lda = c->ldp;
         ba.M = c->n;
-        ba.Bop = c->Wb;
-        ba.ldb = ba.sp;
-        ba.K = c->ldp;
+        ba.Bop = c->pairP ? c->Db : c->Wb;
+        ba.ldb = c->pairP ? c->ldd : ba.sp;
+        ba.K = c->pairP ? c->ldd : c->ldp;
     }
     return ba;
 }
@@ -903,6 +909,7 @@ void duquad_default_options(duquad_options *o) {
     o->checkpoint = 0;
     o->nccl_self = 0;
     o->sell_path = 1;
+    o->pair_rows = 1;
 }
 
 duquad_status duquad_shard_range(int64_t rows, int32_t world, int32_t rank, int64_t *begin,
@@ -1185,6 +1192,23 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
                                       p * sizeof(double), B, cudaMemcpyDefault, s));
         }
         CKS(configure_batched_kernels());
+        // constraint rows in +/- pairs, G = [G_t; -G_t] (two-sided bounds, e.g. config 3's |x_k| <= 5):
+        // pass A streams [Q; G_t] and pass B G_t' (w_top - w_bottom) -- the same products (the bottom
+        // rows' G u is -(G_t u) exactly), half the G work
+        if (opt.pair_rows && p > 0 && p % 2 == 0) {
+            const int64_t P = p / 2;
+            CKS(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int32_t), s));
+            CKS(launch_check_pairs(ctx->A + n * ctx->ld, P, n, ctx->ld, ctx->d_flag, s));
+            int32_t flag = 1;
+            CKS(cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(flag), cudaMemcpyDeviceToHost, s));
+            CKS(cudaStreamSynchronize(s));
+            CKS(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int32_t), s));
+            if (!flag) {
+                ctx->pairP = P;
+                ctx->ldd = round_up(P, 32);
+                CKS(dalloc(&ctx->Db, B * ctx->ldd));   // zero padding: pass B's K runs to ldd
+            }
+        }
     }
     if (prob->on_device) {
         CKS(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int32_t), s));
@@ -2069,8 +2093,11 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
             res->bytes_pass_b = 0.0;
         } else if (ctx->Btot > 1) {   // shared matrices (L2-resident) + per-QP vectors
             const double B = (double)ctx->Bloc;
-            res->flops_pass_a = 2.0 * (nn + pp) * nn * B;
-            res->flops_pass_b = 2.0 * nn * pp * B;
+            // flops the kernels execute (paired rows: [Q;G_t] and G_t', P = p/2; the algorithmic
+            // 2B(n+p)n + 2Bnp of the unpaired step is what the step computes either way)
+            const double pe = ctx->pairP ? (double)ctx->pairP : pp;
+            res->flops_pass_a = 2.0 * (nn + pe) * nn * B;
+            res->flops_pass_b = 2.0 * nn * pe * B;
             res->bytes_pass_a = 8.0 * ((nn + pp) * nn + B * (nn + nn + 3.0 * pp));
             res->bytes_pass_b = 8.0 * (nn * pp + B * (pp + 8.0 * nn));
         } else if (ctx->format == DUQUAD_CSR) {   // values + indices + row pointers + vectors

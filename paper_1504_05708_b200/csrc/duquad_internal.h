@@ -122,6 +122,9 @@ struct BatchedArgs {
     int64_t ldb, N;      // valid QPs
     int64_t K;           // reduction length, padded to a multiple of 32 (zero padding)
     int64_t sn, sp;
+    int64_t sw;          // stride of pass A's G-row output a.w (sp, or the paired rows' D buffer stride)
+    int64_t pairP;       // > 0: G = [G_t; -G_t] with P = p/2 paired rows; pass A streams [Q; G_t] and
+                         // writes d = w_top - w_bottom (a.w, stride sw), pass B multiplies G_t' d
     int64_t ncol8;       // QP octets (set by launch_batched)
     // eps_in mode (else null): per-QP stop-test sums, stop flags, number of stopped QPs
     double *gm_b;
@@ -261,6 +264,8 @@ cudaError_t launch_batched_decide(double *gm_b, int32_t *done_b, int32_t *ndone,
 cudaError_t launch_batched_finish(const double *x, double *y, double *xhat, int64_t n, int64_t sn, int64_t B,
                                   const OuterParam *ops, const int32_t *d_j, int32_t *done_b, int32_t *ndone,
                                   int32_t *conv, int64_t nc, cudaStream_t s);
+// flag = 1 unless the rows of G (P + P rows, ld apart) satisfy G[k + P] == -G[k] (paired rows)
+cudaError_t launch_check_pairs(const double *G, int64_t P, int64_t n, int64_t ld, int32_t *flag, cudaStream_t s);
 cudaError_t launch_batched_h(double *h, const double *mu, const double *g, double rho, int64_t p, int64_t sp,
                              int64_t B, cudaStream_t s);
 

@@ -52,15 +52,16 @@ constexpr int kBlkM = 128;      // rows per block: 16 m8 tiles
 constexpr int LDC = kBlkM + 2;  // tiles Cs[qp][row]; 2 LDC = 4 mod 16 doubles: fragment-order accesses are conflict-free
 constexpr int kSmemCap = 225 * 1024;
 
-template <int PASS, int NT>
+template <int PASS, int NT, bool PAIR = false>
 struct Geo {
     static constexpr int EPIW = PASS == 0 ? 2 : 6;   // pass A: 2 h-staging warps; pass B: 6 epilogue warps
     static constexpr int THREADS = 32 * (kMathW + kProdW + EPIW);
     static constexpr int BN = 8 * NT;
     static constexpr int SA = kBlkM * PADK, SB = BN * PADK;   // doubles per stage
     static constexpr int CS = BN * LDC;   // pass B: parked C tile; pass A: staged h tile (same shape)
-    static constexpr int STAGES = (kSmemCap - 8 * CS - 128) / (8 * (SA + SB));
-    static constexpr size_t SMEM = 8 * ((size_t)STAGES * (SA + SB) + CS) + 128;
+    static constexpr int NCS = PAIR ? 2 : 1;   // pass A, paired rows: h tiles of the top and the bottom rows
+    static constexpr int STAGES = (kSmemCap - 8 * NCS * CS - 128) / (8 * (SA + SB));
+    static constexpr size_t SMEM = 8 * ((size_t)STAGES * (SA + SB) + NCS * CS) + 128;
     static_assert(STAGES >= 2, "ring too shallow");
 };
 
@@ -143,7 +144,7 @@ __device__ __forceinline__ Group group_of(const BatchedArgs &a, const Range &r, 
 
 struct MathCtx {
     const double *As, *Bs;
-    double *Cs;
+    double *Cs, *Cs2;
     uint64_t *full, *empty, *cs_full, *cs_empty;
     uint32_t s, blk;
     int nkc, warp, lane;
@@ -175,6 +176,77 @@ __device__ __forceinline__ void kloop(MathCtx &x, double (&acc)[2][C][2]) {
             }
         }
         mbar_arrive(x.empty + slot);
+    }
+}
+
+// The DFOM step for paired rows (G row k + P = -G row k): the block's reduced row k carries
+// s = G_k u_bar; row k takes r = s + g_k, row k + P takes r = -s + g_{k+P} (bitwise the unpaired
+// product, -s being exact), each with epilogue.cuh's dfom_row; the output is d_k = w_k - w_{k+P}
+// (the operand of pass B's G_t' d).
+__device__ __noinline__ void dual_block_pair(const double *Cs, const double *g, double *mu, double *lam_prev,
+                                             double *hh, double *w, double *qy, const uint8_t *cone, double rho,
+                                             double step, int project_dual, double beta_out, double *lam_hat,
+                                             int mu_hat, double lhat_w, int64_t sn, int64_t sp, int64_t nq,
+                                             int64_t M, int64_t q0, int nqp, int64_t m0, int ne, int ni, int warp,
+                                             int lane, int64_t P, int64_t sw) {
+    const int fr = lane >> 2, fk = lane & 3;
+    for (int i = 0; i < ni; ++i) {
+        const int rl = 8 * (warp + 8 * i) + fr;
+        const int64_t row = m0 + rl;
+        if (row >= M) continue;
+        if (row < nq) {   // Q row: qy
+            for (int e = 0; e < ne; ++e) {
+                const int qp = 8 * (e >> 1) + 2 * fk + (e & 1);
+                if (qp < nqp) qy[(q0 + qp) * sn + row] = Cs[qp * LDC + rl];
+            }
+            continue;
+        }
+        const int64_t k = row - nq;
+        const uint8_t c0 = cone[k], c1 = cone[k + P];
+        constexpr int E = 4;
+        for (int e0 = 0; e0 < ne; e0 += E) {
+            double gv[2][E], mv[2][E], lv[2][E];
+#pragma unroll
+            for (int u = 0; u < E; ++u) {
+                const int e = e0 + u, qp = 8 * (e >> 1) + 2 * fk + (e & 1);
+                if (e < ne && qp < nqp) {
+                    const int64_t off = (q0 + qp) * sp + k;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        gv[h][u] = g[off + h * P];
+                        mv[h][u] = mu[off + h * P];
+                        lv[h][u] = lam_prev[off + h * P];
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < E; ++u) {
+                const int e = e0 + u, qp = 8 * (e >> 1) + 2 * fk + (e & 1);
+                if (e < ne && qp < nqp) {
+                    const int64_t off = (q0 + qp) * sp + k;
+                    const double s = Cs[qp * LDC + rl];
+                    double wv[2];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const uint8_t c = h ? c1 : c0;
+                        const double r = (h ? -s : s) + gv[h][u];
+                        double lam;
+                        double m = dfom_row(r, mv[h][u], lv[h][u], c, rho, step, project_dual, beta_out, lam);
+                        if (lhat_w != 0.0) {   // DGM dual averaging
+                            OuterA oa{1, beta_out, mu_hat, lhat_w};
+                            double lh;
+                            m = dual_average(lam_hat[off + h * P], lam, m, oa, lh);
+                            lam_hat[off + h * P] = lh;
+                        }
+                        lam_prev[off + h * P] = lam;
+                        mu[off + h * P] = m;
+                        hh[off + h * P] = m + rho * gv[h][u];
+                        wv[h] = rho > 0.0 ? proj_polar(m + rho * r, c) : m;
+                    }
+                    w[(q0 + qp) * sw + k] = wv[0] - wv[1];
+                }
+            }
+        }
     }
 }
 
@@ -244,7 +316,7 @@ __device__ __noinline__ void dual_block(const double *Cs, const double *g, doubl
 // Arithmetic: epilogue.cuh's, with [mu + rho (s + g)]_{K°} regrouped as [h + rho s]_{K°} outside
 // the DFOM step (reading c22); h comes from the tile the producers staged in x.Cs
 // (Hs[qp][row - m0]).
-template <int ST, int SA, int SB, int C, bool TWO>
+template <int ST, int SA, int SB, int C, bool TWO, bool PAIR>
 __device__ __forceinline__ void block_a(MathCtx &x, const BatchedArgs &args, const Group &gr, int64_t m0,
                                         const OuterA &o) {
     constexpr int NI = TWO ? 2 : 1;
@@ -253,12 +325,13 @@ __device__ __forceinline__ void block_a(MathCtx &x, const BatchedArgs &args, con
     const double rho = A.rho;
     int64_t row[NI];
     int kr[NI];   // G-row index, -1 for a Q row, -2 beyond M
-    uint8_t cn[NI];
+    uint8_t cn[NI], cb[NI];   // cone tags of the G row (paired: of its top and bottom rows)
 #pragma unroll
     for (int i = 0; i < NI; ++i) {
         row[i] = m0 + 8 * (x.warp + 8 * i) + fr;
         kr[i] = row[i] >= args.M ? -2 : row[i] < A.nq ? -1 : (int)(row[i] - A.nq);
         cn[i] = kr[i] >= 0 ? A.cone[kr[i]] : 0;   // lands during the K loop
+        cb[i] = PAIR && kr[i] >= 0 ? A.cone[kr[i] + args.pairP] : 0;
     }
     double acc[2][C][2];
     BTRACE(8 * (x.blk & 63) + 0, x.warp == 0);
@@ -267,8 +340,11 @@ __device__ __forceinline__ void block_a(MathCtx &x, const BatchedArgs &args, con
     mbar_wait(x.cs_full, x.blk & 1);   // the h tile of this block
     BTRACE(8 * (x.blk & 63) + 3, x.warp == 0);
     if (!o.dual) {
-        // (1) results in place in the tile: Hs[qp][r] := qy (Q row) or w (G row); immediate offsets
+        // (1) results in place in the tile: Hs[qp][r] := qy (Q row) or w (G row); immediate offsets.
+        // Paired rows: the tiles hold h of the top and of the bottom row; d = w_top - w_bottom, the
+        // bottom row's product being -s (exactly the unpaired one)
         double *hs = x.Cs + (2 * fk) * LDC + 8 * x.warp + fr;
+        const double *hs2 = x.Cs2 + (2 * fk) * LDC + 8 * x.warp + fr;
 #pragma unroll
         for (int i = 0; i < NI; ++i) {
             const bool q_row = kr[i] == -1;
@@ -278,7 +354,14 @@ __device__ __forceinline__ void block_a(MathCtx &x, const BatchedArgs &args, con
                 for (int h = 0; h < 2; ++h) {
                     double *e = hs + (8 * j + h) * LDC + 64 * i;
                     const double sv = acc[i][j][h];
-                    *e = q_row ? sv : rho > 0.0 ? proj_polar(*e + rho * sv, cn[i]) : *e;
+                    if (PAIR) {
+                        const double hb = hs2[(8 * j + h) * LDC + 64 * i];
+                        const double wt = rho > 0.0 ? proj_polar(*e + rho * sv, cn[i]) : *e;
+                        const double wb = rho > 0.0 ? proj_polar(hb + rho * (-sv), cb[i]) : hb;
+                        *e = q_row ? sv : wt - wb;
+                    } else {
+                        *e = q_row ? sv : rho > 0.0 ? proj_polar(*e + rho * sv, cn[i]) : *e;
+                    }
                 }
         }
         __syncwarp();
@@ -290,7 +373,7 @@ __device__ __forceinline__ void block_a(MathCtx &x, const BatchedArgs &args, con
             const int64_t r = m0 + rl;
             if (r < args.M) {
                 const bool q_row = r < A.nq;
-                const int64_t ld = q_row ? args.sn : args.sp;
+                const int64_t ld = q_row ? args.sn : args.sw;
                 double *dst = (q_row ? A.qy + r : A.w + (r - A.nq)) + (gr.q0 + (x.lane >> 3)) * ld;
                 const double *src = x.Cs + (x.lane >> 3) * LDC + rl;
                 const int64_t step = 4 * ld;
@@ -307,8 +390,14 @@ __device__ __forceinline__ void block_a(MathCtx &x, const BatchedArgs &args, con
 #pragma unroll
                 for (int i = 0; i < NI; ++i) x.Cs[(8 * j + 2 * fk + h) * LDC + (int)(row[i] - m0)] = acc[i][j][h];
         __syncwarp();
-        dual_block(x.Cs, A.g, A.mu, A.lam_prev, A.h, A.w, A.qy, A.cone, rho, A.step, A.project_dual, o.beta_out,
-                   A.lam_hat, o.mu_hat, o.lhat_w, args.sn, args.sp, A.nq, args.M, gr.q0, gr.nq, m0, 2 * C, TWO ? 2 : 1, x.warp, x.lane);
+        if (PAIR)   // reduced row k is G row k (s) and G row k + P (-s, exactly)
+            dual_block_pair(x.Cs, A.g, A.mu, A.lam_prev, A.h, A.w, A.qy, A.cone, rho, A.step, A.project_dual,
+                            o.beta_out, A.lam_hat, o.mu_hat, o.lhat_w, args.sn, args.sp, A.nq, args.M, gr.q0, gr.nq,
+                            m0, 2 * C, TWO ? 2 : 1, x.warp, x.lane, args.pairP, args.sw);
+        else
+            dual_block(x.Cs, A.g, A.mu, A.lam_prev, A.h, A.w, A.qy, A.cone, rho, A.step, A.project_dual, o.beta_out,
+                       A.lam_hat, o.mu_hat, o.lhat_w, args.sn, args.sp, A.nq, args.M, gr.q0, gr.nq, m0, 2 * C,
+                       TWO ? 2 : 1, x.warp, x.lane);
     }
     mbar_arrive(x.cs_empty);
     BTRACE(8 * (x.blk & 63) + 2, x.warp == 0);
@@ -334,17 +423,17 @@ __device__ __forceinline__ void block_b(MathCtx &x) {
     ++x.blk;
 }
 
-template <int PASS, int NT, int C>
+template <int PASS, int NT, bool PAIR, int C>
 __device__ __forceinline__ void block_sel(MathCtx &x, const BatchedArgs &args, const Group &gr, int64_t m0,
                                           const OuterA &o) {
-    using GE = Geo<PASS, NT>;
+    using GE = Geo<PASS, NT, PAIR>;
     const bool two = m0 + 8 * (x.warp + 8) < args.M;
     if (gr.nc == C) {
         if (PASS == 0) {
             if (two)
-                block_a<GE::STAGES, GE::SA, GE::SB, C, true>(x, args, gr, m0, o);
+                block_a<GE::STAGES, GE::SA, GE::SB, C, true, PAIR>(x, args, gr, m0, o);
             else
-                block_a<GE::STAGES, GE::SA, GE::SB, C, false>(x, args, gr, m0, o);
+                block_a<GE::STAGES, GE::SA, GE::SB, C, false, PAIR>(x, args, gr, m0, o);
         } else {
             if (two)
                 block_b<GE::STAGES, GE::SA, GE::SB, C, true>(x);
@@ -352,7 +441,7 @@ __device__ __forceinline__ void block_sel(MathCtx &x, const BatchedArgs &args, c
                 block_b<GE::STAGES, GE::SA, GE::SB, C, false>(x);
         }
     } else if constexpr (C > 1) {
-        block_sel<PASS, NT, C - 1>(x, args, gr, m0, o);
+        block_sel<PASS, NT, PAIR, C - 1>(x, args, gr, m0, o);
     }
 }
 
@@ -420,16 +509,17 @@ __device__ __forceinline__ void epi_block_b(const BatchedArgs &args, const doubl
 }
 
 // C[m][b] = sum_k A[m][k] * Bop[b][k];  A: M x K row-major (lda), Bop: N x K (ldb), K padded to BK.
-template <int PASS, int NT>
-__global__ void __launch_bounds__(Geo<PASS, NT>::THREADS, 1) k_batched(const BatchedArgs args) {
-    using GE = Geo<PASS, NT>;
+template <int PASS, int NT, bool PAIR>
+__global__ void __launch_bounds__(Geo<PASS, NT, PAIR>::THREADS, 1) k_batched(const BatchedArgs args) {
+    using GE = Geo<PASS, NT, PAIR>;
     if (args.ndone && *args.ndone >= args.N) return;   // eps_in mode: every QP's inner solve has stopped
     constexpr int ST = GE::STAGES;
     extern __shared__ __align__(16) double smem[];
     double *As = smem;
     double *Bs = As + ST * GE::SA;
     double *Cs = Bs + ST * GE::SB;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(Cs + GE::CS);
+    double *Cs2 = Cs + (GE::NCS - 1) * GE::CS;   // paired rows: the bottom rows' h tile
+    uint64_t *bars = reinterpret_cast<uint64_t *>(Cs + GE::NCS * GE::CS);
     uint64_t *full = bars, *empty = bars + ST, *cs_full = bars + 2 * ST, *cs_empty = cs_full + 1;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
@@ -447,11 +537,11 @@ __global__ void __launch_bounds__(Geo<PASS, NT>::THREADS, 1) k_batched(const Bat
     const OuterA o = PASS == 0 ? outer_a(args.a, MODE_SOLVE) : OuterA{0, 0.0};
 
     if (warp < kMathW) {   // ------------------------------------------------ math warps
-        MathCtx x{As, Bs, Cs, full, empty, cs_full, cs_empty, 0u, 0u, nkc, warp, lane};
+        MathCtx x{As, Bs, Cs, Cs2, full, empty, cs_full, cs_empty, 0u, 0u, nkc, warp, lane};
         for (int k = 0; k < rg.ng; ++k) {
             const Group gr = group_of(args, rg, k);
             if (gr.nq == 0) continue;
-            for (int mb = 0; mb < nmb; ++mb) block_sel<PASS, NT, NT>(x, args, gr, (int64_t)mb * kBlkM, o);
+            for (int mb = 0; mb < nmb; ++mb) block_sel<PASS, NT, PAIR, NT>(x, args, gr, (int64_t)mb * kBlkM, o);
         }
     } else if (warp < kMathW + kProdW) {   // ----------------------------------- producer warps
         const int pt = tid - 32 * kMathW;
@@ -498,20 +588,25 @@ __global__ void __launch_bounds__(Geo<PASS, NT>::THREADS, 1) k_batched(const Bat
                 BTRACE(8 * (hb & 63) + 4, warp == kMathW + kProdW);
                 if (!o.dual && r1 > r0) {
                     const int nr = (int)(r1 - r0), k0 = (int)(r0 - args.a.nq), d0 = (int)(r0 - m0);
-                    if (((k0 | d0 | (int)args.sp) & 1) == 0) {   // 16-byte pairs (+ an odd tail element)
-                        const int np = (nr + 1) / 2;
-                        for (int i = st; i < gr.nq * np; i += nst) {
-                            const int c = i / np, r = 2 * (i % np);
-                            const double *src = args.a.h + (gr.q0 + c) * args.sp + k0 + r;
-                            if (r + 1 < nr)
-                                cp16(Cs + c * LDC + d0 + r, src);
-                            else
-                                cp8(Cs + c * LDC + d0 + r, src);
-                        }
-                    } else {
-                        for (int i = st; i < gr.nq * nr; i += nst) {
-                            const int c = i / nr, r = i % nr;
-                            cp8(Cs + c * LDC + d0 + r, args.a.h + (gr.q0 + c) * args.sp + k0 + r);
+                    // paired rows: tile 2 holds h of the bottom rows k + P
+                    for (int t = 0; t < GE::NCS; ++t) {
+                        double *ct = t ? Cs2 : Cs;
+                        const int kt = k0 + (t ? (int)args.pairP : 0);
+                        if (((kt | d0 | (int)args.sp) & 1) == 0) {   // 16-byte pairs (+ an odd tail element)
+                            const int np = (nr + 1) / 2;
+                            for (int i = st; i < gr.nq * np; i += nst) {
+                                const int c = i / np, r = 2 * (i % np);
+                                const double *src = args.a.h + (gr.q0 + c) * args.sp + kt + r;
+                                if (r + 1 < nr)
+                                    cp16(ct + c * LDC + d0 + r, src);
+                                else
+                                    cp8(ct + c * LDC + d0 + r, src);
+                            }
+                        } else {
+                            for (int i = st; i < gr.nq * nr; i += nst) {
+                                const int c = i / nr, r = i % nr;
+                                cp8(ct + c * LDC + d0 + r, args.a.h + (gr.q0 + c) * args.sp + kt + r);
+                            }
                         }
                     }
                 }
@@ -543,7 +638,7 @@ constexpr int kNTA = 7, kNTB = 4;
 
 int g_num_sms = 0;   // grid cap: the SM count, or DUQUAD_BATCHED_CTAS (tests: several groups per CTA)
 
-template <int PASS, int NT>
+template <int PASS, int NT, bool PAIR>
 cudaError_t launch_t(BatchedArgs a, cudaStream_t s) {
     if (!g_num_sms) {
         int dev = 0;
@@ -555,7 +650,7 @@ cudaError_t launch_t(BatchedArgs a, cudaStream_t s) {
     }
     a.ncol8 = (a.N + 7) / 8;
     const int64_t nctas = a.ncol8 < g_num_sms ? a.ncol8 : g_num_sms;
-    k_batched<PASS, NT><<<(unsigned)nctas, Geo<PASS, NT>::THREADS, Geo<PASS, NT>::SMEM, s>>>(a);
+    k_batched<PASS, NT, PAIR><<<(unsigned)nctas, Geo<PASS, NT, PAIR>::THREADS, Geo<PASS, NT, PAIR>::SMEM, s>>>(a);
 #ifdef DUQUAD_BATCHED_TRACE
     if (PASS == 0) {
         unsigned long long h[8 * 64];
@@ -573,24 +668,26 @@ cudaError_t launch_t(BatchedArgs a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <int PASS, int NT>
+template <int PASS, int NT, bool PAIR>
 cudaError_t configure_t() {
-    return cudaFuncSetAttribute(k_batched<PASS, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)Geo<PASS, NT>::SMEM);
+    return cudaFuncSetAttribute(k_batched<PASS, NT, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)Geo<PASS, NT, PAIR>::SMEM);
 }
 
 }  // namespace
 
 cudaError_t configure_batched_kernels() {
     cudaError_t e;
-    if ((e = configure_t<0, kNTA>())) return e;
-    return configure_t<1, kNTB>();
+    if ((e = configure_t<0, kNTA, false>())) return e;
+    if ((e = configure_t<0, kNTA, true>())) return e;
+    return configure_t<1, kNTB, false>();
 }
 
 cudaError_t launch_batched(const BatchedArgs &a, int pass, int mode, cudaStream_t s) {
     if (a.N <= 0 || a.M <= 0) return cudaSuccess;
     if (mode != MODE_SOLVE) return cudaErrorInvalidValue;   // the batched path runs solve passes only
-    return pass == 0 ? launch_t<0, kNTA>(a, s) : launch_t<1, kNTB>(a, s);
+    if (pass == 1) return launch_t<1, kNTB, false>(a, s);
+    return a.pairP > 0 ? launch_t<0, kNTA, true>(a, s) : launch_t<0, kNTA, false>(a, s);
 }
 
 // eps_in mode (per QP): the stop test on the QP's sum of (y - x+)^2, then the sum is cleared
@@ -646,6 +743,19 @@ cudaError_t launch_batched_finish(const double *x, double *y, double *xhat, int6
     k_batched_finish<<<(unsigned)std::min<int64_t>(1184, (m + 255) / 256), 256, 0, s>>>(x, y, xhat, n, sn, B, ops, d_j,
                                                                                        done_b, conv, nc);
     k_batched_reset<<<(unsigned)((B + 255) / 256), 256, 0, s>>>(done_b, ndone, conv, nc, d_j, B);
+    return cudaGetLastError();
+}
+
+// flag = 1 unless G row k + P == -G row k for every k < P (n columns, rows ld apart)
+__global__ void k_check_pairs(const double *G, int64_t P, int64_t n, int64_t ld, int32_t *flag) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < P * n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = t / n, j = t % n;
+        if (G[(k + P) * ld + j] != -G[k * ld + j]) *flag = 1;
+    }
+}
+
+cudaError_t launch_check_pairs(const double *G, int64_t P, int64_t n, int64_t ld, int32_t *flag, cudaStream_t s) {
+    if (P * n > 0) k_check_pairs<<<592, 256, 0, s>>>(G, P, n, ld, flag);
     return cudaGetLastError();
 }
 

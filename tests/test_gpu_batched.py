@@ -112,7 +112,9 @@ def test_config3_full_size_configured_counts(torch_cuda):
     xl, xa, lam, info = _solve(prob, 1.0, "DFGM", 50, 20, L_in, L_d)
     r = _oracle(prob, 1.0, O.DFGM, 50, 20, L_in, L_d)
     assert relerr(xl, r.x_last.T) <= TOL and relerr(xa, r.x_avg.T) <= TOL and relerr(lam, r.lam.T) <= TOL
-    assert info["flops_pass_a"] + info["flops_pass_b"] == pytest.approx(3.0672e9, rel=1e-3)
+    # paired rows (G = [Gamma; -Gamma]): [Q; Gamma] and Gamma' are streamed, 2B(n(n+P) + nP) flops,
+    # P = 360, instead of the unpaired 2B(n(n+p) + np) = 3.067 GFLOP
+    assert info["flops_pass_a"] + info["flops_pass_b"] == pytest.approx(2 * 8192 * (120 * 480 + 120 * 360), rel=1e-9)
 
 
 def test_tall_blocks_both_passes(torch_cuda):
@@ -158,6 +160,32 @@ def test_several_groups_per_cta(torch_cuda):
     assert err <= TOL, err
 
 
+@pytest.mark.parametrize("alg", ["DGM", "DFGM"])
+def test_paired_rows_match_unpaired_and_detection(torch_cuda, alg):
+    """pair_rows: G = [Gamma; -Gamma] runs the reduced matrices ([Q; Gamma] in pass A, Gamma'(w_top -
+    w_bottom) in pass B); the iterates equal the unpaired kernels' to rounding (1e-12) and the
+    oracle's (1e-9), incl. the DFOM step and DGM dual averaging.  A G whose halves are not exact
+    negatives (one entry off by 1 ulp) is not paired."""
+    prob = qpgen.mpc_batch(77, seed=8, N=9)              # n = 36, p = 216, P = 108
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 1.0, 0.1)
+    n, p, B = 36, 216, 77
+    kw = dict(dual_average=True) if alg == "DGM" else {}
+    a = _solve(prob, 1.0, alg, 6, 5, L_in, L_d, **kw)
+    b = _solve(prob, 1.0, alg, 6, 5, L_in, L_d, pair_rows=False, **kw)
+    assert a[3]["flops_pass_a"] == pytest.approx(2.0 * (n + p // 2) * n * B)
+    assert b[3]["flops_pass_a"] == pytest.approx(2.0 * (n + p) * n * B)
+    for k in range(3):
+        assert relerr(a[k], b[k]) <= 1e-12, k
+    r = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 1.0, alg, 6, 5, L_in, L_d,
+               dual_average=alg == "DGM")
+    assert relerr(a[0], r.x_last.T) <= TOL and relerr(a[1], r.x_avg.T) <= TOL and relerr(a[2], r.lam.T) <= TOL
+    G = prob.G.copy()
+    G[p // 2 + 3, 5] = np.nextafter(G[p // 2 + 3, 5], np.inf)
+    prob.G = G
+    c = _solve(prob, 1.0, alg, 2, 2, L_in, L_d, **kw)
+    assert c[3]["flops_pass_a"] == pytest.approx(2.0 * (n + p) * n * B)
+
+
 @pytest.mark.parametrize("seed", range(5))
 def test_random_batched_shapes(torch_cuda, seed):
     """Randomised batch sizes and horizons for the persistent DMMA kernels: ragged octets, n across
@@ -167,7 +195,8 @@ def test_random_batched_shapes(torch_cuda, seed):
     N = int([2, 9, 31, 33, 40][seed])                  # n = 4N: 8 ... 160
     prob = qpgen.mpc_batch(B, seed=seed, N=N)
     L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, 1.0, 0.1)
-    xl, xa, lam, info = _solve(prob, 1.0, "DFGM", 2, 3, L_in, L_d)
-    assert info["path"] == 4
     r = _oracle(prob, 1.0, O.DFGM, 2, 3, L_in, L_d)
-    assert relerr(xl, r.x_last.T) <= TOL and relerr(xa, r.x_avg.T) <= TOL and relerr(lam, r.lam.T) <= TOL
+    for pair in (True, False):
+        xl, xa, lam, info = _solve(prob, 1.0, "DFGM", 2, 3, L_in, L_d, pair_rows=pair)
+        assert info["path"] == 4
+        assert relerr(xl, r.x_last.T) <= TOL and relerr(xa, r.x_avg.T) <= TOL and relerr(lam, r.lam.T) <= TOL
