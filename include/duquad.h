@@ -204,9 +204,8 @@ typedef struct {
     double flops_pass_a;        /* algorithmic flops per pass-A launch (2 per multiply-add) */
     double flops_pass_b;
     int32_t path;               /* duquad_path: which kernels ran the inner steps           */
-    int32_t sparse_kernels;     /* CSR: pass A kind | pass B kind << 4, kind bits 0-1: 0 =
-                                   sub-warp CSR, 1 = SELL-32, 2 = thread-per-row CSR
-                                   (options.sell_path); bit 2: the cp.async-staged variant  */
+    int32_t sparse_kernels;     /* CSR: pass A kind | pass B kind << 4, kind 0 = sub-warp CSR,
+                                   1 = SELL-32, 2 = thread-per-row CSR (options.sell_path)   */
 } duquad_result;
 
 /* Kernel path of a solve (duquad_result.path).  "pass A" / "pass B" in the report map to:

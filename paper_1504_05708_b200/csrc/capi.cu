@@ -62,9 +62,6 @@ struct duquad_ctx {
     int gs_a = 4, gs_b = 4;
     SellStore sell_a, sell_b;   // SELL-32 copies of the two (options.sell_path; empty unless kind SPK_SELL)
     int kind_a = SPK_CSR, kind_b = SPK_CSR, u_a = 8, u_b = 8;   // SparseKind and load-round width per pass
-    int cap_a = 0, cap_b = 0;   // staged lane kernels: elements per warp buffer (0: register kernels)
-    double mean_a = 0.0, mean_b = 0.0;
-    int32_t maxlen_a = 0, maxlen_b = 0;
     // batched storage (batch > 1): QP-major per-QP vectors, strides ld (n-vectors) / ldp (p-vectors)
     int64_t Btot = 1, Bloc = 1, b0 = 0;
     double *Yb = nullptr, *Xb = nullptr, *XHb = nullptr, *QYb = nullptr, *qb = nullptr;
@@ -289,7 +286,6 @@ PassAArgs make_a(duquad_ctx *c) {
     a.lam_hat = c->davg ? c->lam_hat : nullptr;
     a.sp_kind = c->kind_a;
     a.sp_u = c->u_a;
-    a.sp_cap = c->cap_a;
     a.sell = sell_view(c->sell_a);
     return a;
 }
@@ -321,7 +317,6 @@ PassBArgs make_b(duquad_ctx *c) {
     b.gm_sq = c->eps_mode ? c->gm_sq : nullptr;
     b.sp_kind = c->kind_b;
     b.sp_u = c->u_b;
-    b.sp_cap = c->cap_b;
     b.sell = sell_view(c->sell_b);
     return b;
 }
@@ -803,8 +798,8 @@ duquad_status setup_csr(duquad_ctx *ctx, const duquad_problem *prob) {
     const int64_t nq = qb[1] - qb[0], ng = gb[1] - gb[0];
     ctx->nnz_a = nq + ng;
     CK(dalloc(&ctx->a_rp, ctx->nloc + ctx->ploc + 1));
-    CK(dalloc(&ctx->a_ci, ctx->nnz_a + 8));   // + 8: tail padding for the staged lane kernels' 16-byte copies
-    CK(dalloc(&ctx->a_va, ctx->nnz_a + 8));
+    CK(dalloc(&ctx->a_ci, ctx->nnz_a));
+    CK(dalloc(&ctx->a_va, ctx->nnz_a));
     CK(launch_rebase(ctx->a_rp, Qrp + ctx->r0, ctx->nloc + 1, qb[0], 0, s));
     if (ctx->ploc > 0) CK(launch_rebase(ctx->a_rp + ctx->nloc, Grp + ctx->s0, ctx->ploc + 1, gb[0], (int32_t)nq, s));
     if (nq) {
@@ -832,13 +827,11 @@ duquad_status setup_csr(duquad_ctx *ctx, const duquad_problem *prob) {
     // lane layout (SELL-32 when it pads little, else thread-per-row CSR) is per rank: both sum
     // each row in CSR order, so the results do not depend on it.
     auto lane_choice = [&](const int32_t *rp, const int32_t *ci, const double *va, int64_t rows, int64_t nq,
-                           int64_t nnz_loc, double mean, SellStore *st, int *kind, int *u, int32_t *maxlen)
-        -> duquad_status {
+                           int64_t nnz_loc, double mean, SellStore *st, int *kind, int *u) -> duquad_status {
         *kind = SPK_CSR;
         if (!ctx->opt.sell_path || mean > kLaneMaxMean) return DUQUAD_OK;
         SparsePlan pl;
         CK(sparse_plan(rp, rows, nq, &pl, s));
-        *maxlen = pl.max_len;
         if ((double)pl.padded <= kSellMaxPad * (double)nnz_loc + 1024.0 && pl.max_len <= 64) {
             CK(sell_build(rp, ci, va, rows, nq, pl, st, s));
             *kind = SPK_SELL;
@@ -850,13 +843,11 @@ duquad_status setup_csr(duquad_ctx *ctx, const duquad_problem *prob) {
         return DUQUAD_OK;
     };
     duquad_status st;
-    ctx->mean_a = (double)(qnnz + gnnz) / (double)(n + p);
-    ctx->mean_b = (double)gnnz / (double)n;
-    if ((st = lane_choice(ctx->a_rp, ctx->a_ci, ctx->a_va, ctx->nloc + ctx->ploc, ctx->nloc, ctx->nnz_a, ctx->mean_a,
-                          &ctx->sell_a, &ctx->kind_a, &ctx->u_a, &ctx->maxlen_a)) != DUQUAD_OK)
+    if ((st = lane_choice(ctx->a_rp, ctx->a_ci, ctx->a_va, ctx->nloc + ctx->ploc, ctx->nloc, ctx->nnz_a,
+                          (double)(qnnz + gnnz) / (double)(n + p), &ctx->sell_a, &ctx->kind_a, &ctx->u_a)) != DUQUAD_OK)
         return st;
-    if (p > 0 && (st = lane_choice(ctx->b_rp, ctx->b_ci, ctx->b_va, ctx->nloc, ctx->nloc, ctx->nnz_b, ctx->mean_b,
-                                   &ctx->sell_b, &ctx->kind_b, &ctx->u_b, &ctx->maxlen_b)) != DUQUAD_OK)
+    if (p > 0 && (st = lane_choice(ctx->b_rp, ctx->b_ci, ctx->b_va, ctx->nloc, ctx->nloc, ctx->nnz_b,
+                                   (double)gnnz / (double)n, &ctx->sell_b, &ctx->kind_b, &ctx->u_b)) != DUQUAD_OK)
         return st;
     // measurement overrides (scripts/sparse_sweep.py): kind / load-round width per pass
     auto env_int = [](const char *k, int d) { const char *v = getenv(k); return v ? atoi(v) : d; };
@@ -867,16 +858,6 @@ duquad_status setup_csr(duquad_ctx *ctx, const duquad_problem *prob) {
         ctx->u_a = env_int("DUQUAD_LANE_UA", ctx->u_a);
     }
     if (ctx->kind_b == SPK_ROWT) ctx->u_b = env_int("DUQUAD_LANE_UB", ctx->u_b) <= 4 ? 4 : 8;
-    // cp.async-staged variants (default): a warp buffer holds a SELL slice (32 x the longest row) or
-    // 32 CSR rows (1.5 x their mean + slack); wider groups are summed from global memory
-    auto cap_of = [](int kind, int32_t maxlen, double mean) {
-        const double c = kind == SPK_SELL ? 32.0 * maxlen : 48.0 * mean + 64.0;
-        return (int)std::min<int64_t>(1024, round_up((int64_t)std::ceil(c), 8));
-    };
-    if (env_int("DUQUAD_STAGED", 1)) {
-        if (ctx->kind_a != SPK_CSR) ctx->cap_a = cap_of(ctx->kind_a, ctx->maxlen_a, ctx->mean_a);
-        if (ctx->kind_b != SPK_CSR) ctx->cap_b = cap_of(ctx->kind_b, ctx->maxlen_b, ctx->mean_b);
-    }
     return DUQUAD_OK;
 }
 
@@ -1278,17 +1259,12 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         }
     }
     if (csr) {   // grid-stride sub-warp SpMV / SELL-32 warp-per-slice, full occupancy
-        int ba = 0, bb = 0;   // staged variants: resident blocks with their buffers (0: register kernels)
-        if (ctx->cap_a > 0 && (ba = staged_blocks_per_sm(0, ctx->kind_a, ctx->cap_a)) <= 0) ctx->cap_a = 0;
-        if (ctx->cap_b > 0 && (bb = staged_blocks_per_sm(1, ctx->kind_b, ctx->cap_b)) <= 0) ctx->cap_b = 0;
-        ctx->cfg_a = {ctx->num_sms * (ctx->cap_a > 0 ? ba
-                                      : ctx->kind_a != SPK_CSR ? lane_blocks_per_sm(0, ctx->kind_a, ctx->u_a)
-                                                               : csr_blocks_per_sm(0, ctx->gs_a)),
-                      256, ctx->cap_a > 0 ? staged_smem(ctx->cap_a) : 0};   // whole waves
-        ctx->cfg_b = {ctx->num_sms * (ctx->cap_b > 0 ? bb
-                                      : ctx->kind_b != SPK_CSR ? lane_blocks_per_sm(1, ctx->kind_b, ctx->u_b)
-                                                               : csr_blocks_per_sm(1, ctx->gs_b)),
-                      256, ctx->cap_b > 0 ? staged_smem(ctx->cap_b) : 0};
+        ctx->cfg_a = {ctx->num_sms * (ctx->kind_a != SPK_CSR ? lane_blocks_per_sm(0, ctx->kind_a, ctx->u_a)
+                                                             : csr_blocks_per_sm(0, ctx->gs_a)),
+                      256, 0};   // whole waves
+        ctx->cfg_b = {ctx->num_sms * (ctx->kind_b != SPK_CSR ? lane_blocks_per_sm(1, ctx->kind_b, ctx->u_b)
+                                                             : csr_blocks_per_sm(1, ctx->gs_b)),
+                      256, 0};
         CKS(cudaStreamSynchronize(s));
         *out = ctx;
         return DUQUAD_OK;
@@ -2091,9 +2067,7 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
                     : ctx->rho0 ? DUQUAD_PATH_RHO0
                     : ctx->Btot > 1 ? DUQUAD_PATH_BATCHED
                     : ctx->format == DUQUAD_CSR ? DUQUAD_PATH_CSR : DUQUAD_PATH_TWO_PASS;
-        res->sparse_kernels = ctx->format == DUQUAD_CSR ? (ctx->kind_a | (ctx->cap_a > 0 ? 4 : 0)) |
-                                                              ((ctx->kind_b | (ctx->cap_b > 0 ? 4 : 0)) << 4)
-                                                        : 0;
+        res->sparse_kernels = ctx->format == DUQUAD_CSR ? ctx->kind_a | (ctx->kind_b << 4) : 0;
         res->outer_iters = K;
         res->inner_iters_total = (int64_t)nout * Kin;
         res->kernel_launches = 1 + (int64_t)nout * (2 * Kin + 1);

@@ -76,7 +76,6 @@ struct PassAArgs {
     const int32_t *skip; // eps_in mode: the inner solve has converged -> the launch does nothing
     int32_t sp_kind;     // SparseKind: sub-warp CSR, SELL-32 or thread-per-row CSR
     int32_t sp_u;        // lane kernels: nonzeros per load round
-    int32_t sp_cap;      // lane kernels: > 0 = cp.async-staged variant, elements per warp buffer
     SellMat sell;
 };
 
@@ -111,7 +110,6 @@ struct PassBArgs {
     double *gm_sq;       // eps_in mode: gm_sq[j] = (y_j - x+_j)^2 (gradient-map test)
     int32_t sp_kind;     // SparseKind: sub-warp CSR, SELL-32 or thread-per-row CSR
     int32_t sp_u;        // lane kernels: nonzeros per load round
-    int32_t sp_cap;      // lane kernels: > 0 = cp.async-staged variant, elements per warp buffer
     SellMat sell;
 };
 
@@ -231,10 +229,6 @@ void sell_free(SellStore *st);
 SellMat sell_view(const SellStore &st);
 int lane_unroll(int kind, int64_t max_width, double mean_len);
 int lane_blocks_per_sm(int pass, int kind, int u);
-// staged variants: dynamic shared memory per 256-thread block for `cap` elements per warp buffer,
-// and resident blocks per SM (after raising the kernels' shared-memory limit)
-size_t staged_smem(int cap);
-int staged_blocks_per_sm(int pass, int kind, int cap);
 cudaError_t launch_pass_a_lane(const PassAArgs &a, int mode, const LaunchCfg &cfg, cudaStream_t s);
 cudaError_t launch_pass_b_lane(const PassBArgs &b, int mode, const LaunchCfg &cfg, cudaStream_t s);
 

@@ -349,11 +349,8 @@ cudaError_t csr_transpose_rows(const int32_t *rp, const int32_t *ci, const doubl
     if ((e = cudaStreamSynchronize(s))) return e;
     const int64_t cnt = hi - lo;
     k_sub_i64_to_i32<<<nblk(nc + 1, 256), 256, 0, s>>>(bounds, nc + 1, lo, *rp_t);
-    // + 8 elements of tail padding (zeroed): the staged lane kernels copy 16-byte pieces past a range's end
-    if ((e = cudaMalloc(ci_t, (cnt + 8) * sizeof(int32_t)))) return e;
-    if ((e = cudaMalloc(va_t, (cnt + 8) * sizeof(double)))) return e;
-    cudaMemsetAsync(*ci_t + cnt, 0, 8 * sizeof(int32_t), s);
-    cudaMemsetAsync(*va_t + cnt, 0, 8 * sizeof(double), s);
+    if ((e = cudaMalloc(ci_t, std::max<int64_t>(cnt, 1) * sizeof(int32_t)))) return e;
+    if ((e = cudaMalloc(va_t, std::max<int64_t>(cnt, 1) * sizeof(double)))) return e;
     if (cnt > 0) {
         k_split_keys<<<nblk(cnt, 256), 256, 0, s>>>(keys + lo, rows, cnt, *ci_t);
         cudaMemcpyAsync(*va_t, vals + lo, cnt * sizeof(double), cudaMemcpyDeviceToDevice, s);

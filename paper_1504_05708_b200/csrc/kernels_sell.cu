@@ -209,238 +209,6 @@ __global__ void __launch_bounds__(kLaneThreads) k_pass_b_rowt(const PassBArgs b)
     }
 }
 
-// ------------------------------------------------------------------ cp.async-staged variants
-// The register kernels above keep a round of U nonzeros in flight per lane and then wait for the
-// gathers: memory-level parallelism is bounded by registers (config 4 pass A: 4.0 TB/s).  Here a
-// warp's group of 32 rows -- a SELL slice, or 32 consecutive CSR rows -- is one contiguous range
-// [lo, hi) of the value and index arrays, which the warp copies into its shared-memory buffer
-// with 16-byte cp.async (no registers held while in flight), double-buffered: group g + 2 is in
-// flight while group g is summed.  A group wider than the buffer is summed from global memory
-// (the register path).  Same per-row CSR summation order as everywhere.
-__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void cpa16(void *s, const void *g) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(s)), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cpa_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-
-// buffer geometry: cap (a multiple of 8) elements + 8 of alignment slack, values then indices
-__host__ __device__ constexpr int stage_capv(int cap) { return cap + 8; }
-__host__ __device__ constexpr size_t stage_warp_bytes(int cap) { return 2 * (size_t)stage_capv(cap) * 12; }
-
-// copy [lo, hi) of va / ci to (vb, cb) in 16-byte pieces from the aligned-down starts la / lc
-// (the arrays carry >= 8 elements of tail padding, so the rounded-up ends stay in bounds)
-__device__ __forceinline__ void stage_chunk(double *vb, int32_t *cb, const double *va, const int32_t *ci, int64_t lo,
-                                            int64_t hi, int lane) {
-    const int64_t la = lo & ~(int64_t)1, lc = lo & ~(int64_t)3;
-    for (int64_t e = la + 2 * lane; e < hi; e += 64) cpa16(vb + (e - la), va + e);
-    for (int64_t e = lc + 4 * lane; e < hi; e += 128) cpa16(cb + (e - lc), ci + e);
-}
-
-// group g of a pass: its rows [r0, r0 + 32) (SELL: slice rows, row -1 for an empty lane) and its
-// nonzero range [lo, hi)
-template <int KIND>
-struct Groups {
-    const int64_t *sptr;   // SELL
-    const int32_t *rp;     // CSR
-    SellMat m;
-    int64_t row_begin, row_end;   // CSR rows
-    __device__ __forceinline__ void range(int64_t g, int64_t &lo, int64_t &hi) const {
-        if (KIND == SPK_SELL) {
-            lo = sptr[g];
-            hi = sptr[g + 1];
-        } else {
-            const int64_t r0 = row_begin + g * 32, r1 = r0 + 32 < row_end ? r0 + 32 : row_end;
-            lo = rp[r0];
-            hi = rp[r1];
-        }
-    }
-    __device__ __forceinline__ int64_t row(int64_t g, int lane) const {
-        if (KIND == SPK_SELL) return sell_row(m, g, lane);
-        const int64_t r = row_begin + g * 32 + lane;
-        return r < row_end ? r : -1;
-    }
-};
-
-// lane's row sum from the staged group (SELL: entry k of the lane at 32 k + lane; CSR: the lane's
-// row [rlo, rlo + len) inside the group), gathers of v in rounds of 8
-template <int KIND>
-__device__ __forceinline__ double staged_dot(const double *vb, const int32_t *cb, int64_t lo, int64_t hi, int64_t rlo,
-                                             int32_t len, int lane, const double *__restrict__ v) {
-    const int64_t la = lo & ~(int64_t)1, lc = lo & ~(int64_t)3;
-    int w, stride;
-    const double *vp;
-    const int32_t *cp;
-    if (KIND == SPK_SELL) {
-        w = (int)((hi - lo) >> 5);
-        stride = 32;
-        vp = vb + (lo - la) + lane;
-        cp = cb + (lo - lc) + lane;
-    } else {
-        w = len;
-        stride = 1;
-        vp = vb + (rlo - la);
-        cp = cb + (rlo - lc);
-    }
-    const int wl = KIND == SPK_SELL ? w : __reduce_max_sync(0xffffffffu, w);
-    double acc = 0.0;
-    constexpr int R = 8;
-    for (int k0 = 0; k0 < wl; k0 += R) {
-        double x[R];
-#pragma unroll
-        for (int u = 0; u < R; ++u) x[u] = k0 + u < w ? __ldg(v + cp[(k0 + u) * stride]) : 0.0;
-#pragma unroll
-        for (int u = 0; u < R; ++u)
-            if (k0 + u < w) acc = fma(vp[(k0 + u) * stride], x[u], acc);
-    }
-    return acc;
-}
-
-template <int MODE, int KIND>
-__global__ void __launch_bounds__(kLaneThreads) k_pass_a_staged(const PassAArgs a) {
-    if (a.skip && *a.skip) return;
-    extern __shared__ __align__(16) unsigned char stage_sm[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int cap = a.sp_cap, capv = stage_capv(cap);
-    double *vbuf = reinterpret_cast<double *>(stage_sm + wib * stage_warp_bytes(cap));
-    int32_t *cbuf = reinterpret_cast<int32_t *>(vbuf + 2 * capv);
-    Groups<KIND> G{a.sell.sptr, a.rp, a.sell, a.row_begin, a.row_end};
-    int64_t g_lo, g_hi;
-    if (KIND == SPK_SELL) {   // slice range of the sub-range (segments never share a slice)
-        g_lo = a.row_begin >= a.sell.nq ? a.sell.nsl_q : 0;
-        g_hi = a.row_end <= a.sell.nq ? a.sell.nsl_q : a.sell.nsl;
-    } else {
-        g_lo = 0;
-        g_hi = (a.row_end - a.row_begin + 31) / 32;
-    }
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t step = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const OuterA o = outer_a(a, MODE);
-    const uint64_t pol = evict_first();
-    const double *va = KIND == SPK_SELL ? a.sell.val : a.va;
-    const int32_t *ci = KIND == SPK_SELL ? a.sell.col : a.ci;
-    // the two buffers' ranges in registers (selected by `cur`, never indexed: no local memory)
-    int64_t lo0 = 0, hi0 = 0, lo1 = 0, hi1 = 0;
-    {   // prologue: groups warp, warp + step in flight
-        const int64_t g = g_lo + warp;
-        if (g < g_hi) {
-            G.range(g, lo0, hi0);
-            if (hi0 - lo0 <= cap) stage_chunk(vbuf, cbuf, va, ci, lo0, hi0, lane);
-        }
-        cpa_commit();
-        if (g + step < g_hi) {
-            G.range(g + step, lo1, hi1);
-            if (hi1 - lo1 <= cap) stage_chunk(vbuf + capv, cbuf + capv, va, ci, lo1, hi1, lane);
-        }
-        cpa_commit();
-    }
-    int cur = 0;
-    for (int64_t g = g_lo + warp; g < g_hi; g += step, cur ^= 1) {
-        const int64_t gn = g + 2 * step;
-        int64_t nlo = 0, nhi = 0;
-        if (gn < g_hi) G.range(gn, nlo, nhi);   // bounds of the group staged after this one
-        const int64_t r = G.row(g, lane);
-        int64_t rlo = 0;
-        int32_t len = 0;
-        if (KIND != SPK_SELL && r >= 0) {
-            rlo = a.rp[r];
-            len = a.rp[r + 1] - (int32_t)rlo;
-        }
-        EpiA e{};
-        if (r >= 0) e = epi_a_load(a, MODE, r, o);
-        cpa_wait1();
-        __syncwarp();
-        const int64_t clo = cur ? lo1 : lo0, chi = cur ? hi1 : hi0;
-        double acc;
-        if (chi - clo <= cap)
-            acc = staged_dot<KIND>(vbuf + cur * capv, cbuf + cur * capv, clo, chi, rlo, len, lane, a.y);
-        else if (KIND == SPK_SELL)
-            acc = sell_dot<4>(a.sell, clo, (int)((chi - clo) >> 5), lane, a.y, pol);
-        else
-            acc = rowt_dot<4>(a.ci, a.va, (int32_t)rlo, len, a.y, pol);
-        if (r >= 0) epi_a_store(a, MODE, r, acc, e, o);
-        __syncwarp();   // the buffer is free
-        if (cur) {
-            lo1 = nlo;
-            hi1 = nhi;
-        } else {
-            lo0 = nlo;
-            hi0 = nhi;
-        }
-        if (gn < g_hi && nhi - nlo <= cap) stage_chunk(vbuf + cur * capv, cbuf + cur * capv, va, ci, nlo, nhi, lane);
-        cpa_commit();
-    }
-}
-
-template <int MODE, int KIND>
-__global__ void __launch_bounds__(kLaneThreads) k_pass_b_staged(const PassBArgs b) {
-    if (b.skip && *b.skip) return;
-    extern __shared__ __align__(16) unsigned char stage_sm[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int cap = b.sp_cap, capv = stage_capv(cap);
-    double *vbuf = reinterpret_cast<double *>(stage_sm + wib * stage_warp_bytes(cap));
-    int32_t *cbuf = reinterpret_cast<int32_t *>(vbuf + 2 * capv);
-    Groups<KIND> G{b.sell.sptr, b.rp, b.sell, 0, b.nrows};
-    const int64_t g_hi = KIND == SPK_SELL ? b.sell.nsl : (b.nrows + 31) / 32;
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t step = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const double avg_w = avg_weight(b, MODE);
-    const uint64_t pol = evict_first();
-    const double *va = KIND == SPK_SELL ? b.sell.val : b.va;
-    const int32_t *ci = KIND == SPK_SELL ? b.sell.col : b.ci;
-    // the two buffers' ranges in registers (selected by `cur`, never indexed: no local memory)
-    int64_t lo0 = 0, hi0 = 0, lo1 = 0, hi1 = 0;
-    {   // prologue: groups warp, warp + step in flight
-        const int64_t g = warp;
-        if (g < g_hi) {
-            G.range(g, lo0, hi0);
-            if (hi0 - lo0 <= cap) stage_chunk(vbuf, cbuf, va, ci, lo0, hi0, lane);
-        }
-        cpa_commit();
-        if (g + step < g_hi) {
-            G.range(g + step, lo1, hi1);
-            if (hi1 - lo1 <= cap) stage_chunk(vbuf + capv, cbuf + capv, va, ci, lo1, hi1, lane);
-        }
-        cpa_commit();
-    }
-    int cur = 0;
-    for (int64_t g = warp; g < g_hi; g += step, cur ^= 1) {
-        const int64_t gn = g + 2 * step;
-        int64_t nlo = 0, nhi = 0;
-        if (gn < g_hi) G.range(gn, nlo, nhi);
-        const int64_t j = G.row(g, lane);
-        int64_t rlo = 0;
-        int32_t len = 0;
-        if (KIND != SPK_SELL && j >= 0) {
-            rlo = b.rp[j];
-            len = b.rp[j + 1] - (int32_t)rlo;
-        }
-        EpiB e{};
-        if (j >= 0) e = epi_b_load(b, MODE, j, avg_w);
-        cpa_wait1();
-        __syncwarp();
-        const int64_t clo = cur ? lo1 : lo0, chi = cur ? hi1 : hi0;
-        double t;
-        if (chi - clo <= cap)
-            t = staged_dot<KIND>(vbuf + cur * capv, cbuf + cur * capv, clo, chi, rlo, len, lane, b.w);
-        else if (KIND == SPK_SELL)
-            t = sell_dot<4>(b.sell, clo, (int)((chi - clo) >> 5), lane, b.w, pol);
-        else
-            t = rowt_dot<4>(b.ci, b.va, (int32_t)rlo, len, b.w, pol);
-        if (j >= 0) epi_b_store(b, MODE, j, t, e, avg_w);
-        __syncwarp();
-        if (cur) {
-            lo1 = nlo;
-            hi1 = nhi;
-        } else {
-            lo0 = nlo;
-            hi0 = nhi;
-        }
-        if (gn < g_hi && nhi - nlo <= cap) stage_chunk(vbuf + cur * capv, cbuf + cur * capv, va, ci, nlo, nhi, lane);
-        cpa_commit();
-    }
-}
-
 // ------------------------------------------------------------------ layout construction
 __global__ void k_row_len(const int32_t *rp, int64_t rows, int32_t *len) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -530,11 +298,8 @@ cudaError_t sell_build(const int32_t *rp, const int32_t *ci, const double *va, i
     st.rows = rows;
     st.padded = plan.padded;
     cudaError_t e = cudaMalloc(&st.sptr, (nsl + 1) * sizeof(int64_t));
-    // + 8 elements of tail padding: the staged kernels copy 16-byte pieces past a range's end
-    if (!e) e = cudaMalloc(&st.val, (plan.padded + 8) * sizeof(double));
-    if (!e) e = cudaMalloc(&st.col, (plan.padded + 8) * sizeof(int32_t));
-    if (!e) e = cudaMemsetAsync(st.val + plan.padded, 0, 8 * sizeof(double), s);
-    if (!e) e = cudaMemsetAsync(st.col + plan.padded, 0, 8 * sizeof(int32_t), s);
+    if (!e) e = cudaMalloc(&st.val, std::max<int64_t>(plan.padded, 2) * sizeof(double));
+    if (!e) e = cudaMalloc(&st.col, std::max<int64_t>(plan.padded, 2) * sizeof(int32_t));
     int32_t *len = nullptr;
     if (!e) e = cudaMalloc(&len, rows * sizeof(int32_t));
     if (!e) {
@@ -601,50 +366,8 @@ int lane_blocks_per_sm(int pass, int kind, int u) {
     return u == 4 ? occ_of(k_pass_b_rowt<MODE_SOLVE, 4>) : occ_of(k_pass_b_rowt<MODE_SOLVE, 8>);
 }
 
-size_t staged_smem(int cap) { return (kLaneThreads / 32) * stage_warp_bytes(cap); }
-
-namespace {
-template <typename K>
-int staged_occ(K kern, int cap) {
-    const size_t sm = staged_smem(cap);
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) return 0;
-    int b = 0;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kLaneThreads, sm) == cudaSuccess ? b : 0;
-}
-}  // namespace
-
-// raises the staged kernels' shared-memory limit (all modes) and returns the solve kernel's
-// resident blocks per SM (0: does not fit)
-int staged_blocks_per_sm(int pass, int kind, int cap) {
-    if (pass == 0) {
-        if (kind == SPK_SELL) {
-            staged_occ(k_pass_a_staged<MODE_LIN, SPK_SELL>, cap);
-            return staged_occ(k_pass_a_staged<MODE_SOLVE, SPK_SELL>, cap);
-        }
-        staged_occ(k_pass_a_staged<MODE_LIN, SPK_ROWT>, cap);
-        return staged_occ(k_pass_a_staged<MODE_SOLVE, SPK_ROWT>, cap);
-    }
-    if (kind == SPK_SELL) {
-        staged_occ(k_pass_b_staged<MODE_LIN, SPK_SELL>, cap);
-        return staged_occ(k_pass_b_staged<MODE_SOLVE, SPK_SELL>, cap);
-    }
-    staged_occ(k_pass_b_staged<MODE_LIN, SPK_ROWT>, cap);
-    return staged_occ(k_pass_b_staged<MODE_SOLVE, SPK_ROWT>, cap);
-}
-
 cudaError_t launch_pass_a_lane(const PassAArgs &a, int mode, const LaunchCfg &cfg, cudaStream_t s) {
     if (a.row_end <= a.row_begin) return cudaSuccess;
-    if (a.sp_cap > 0) {
-        const size_t sm = staged_smem(a.sp_cap);
-        if (a.sp_kind == SPK_SELL) {
-            if (mode == MODE_SOLVE) k_pass_a_staged<MODE_SOLVE, SPK_SELL><<<cfg.grid, kLaneThreads, sm, s>>>(a);
-            else k_pass_a_staged<MODE_LIN, SPK_SELL><<<cfg.grid, kLaneThreads, sm, s>>>(a);
-        } else {
-            if (mode == MODE_SOLVE) k_pass_a_staged<MODE_SOLVE, SPK_ROWT><<<cfg.grid, kLaneThreads, sm, s>>>(a);
-            else k_pass_a_staged<MODE_LIN, SPK_ROWT><<<cfg.grid, kLaneThreads, sm, s>>>(a);
-        }
-        return cudaGetLastError();
-    }
     if (a.sp_kind == SPK_SELL) {
         if (mode == MODE_SOLVE) {
             DQ_LANE_DISPATCH(k_pass_a_sell, MODE_SOLVE, a.sp_u, cfg.grid, a);
@@ -663,17 +386,6 @@ cudaError_t launch_pass_a_lane(const PassAArgs &a, int mode, const LaunchCfg &cf
 
 cudaError_t launch_pass_b_lane(const PassBArgs &b, int mode, const LaunchCfg &cfg, cudaStream_t s) {
     if (b.nrows <= 0) return cudaSuccess;
-    if (b.sp_cap > 0) {
-        const size_t sm = staged_smem(b.sp_cap);
-        if (b.sp_kind == SPK_SELL) {
-            if (mode == MODE_SOLVE) k_pass_b_staged<MODE_SOLVE, SPK_SELL><<<cfg.grid, kLaneThreads, sm, s>>>(b);
-            else k_pass_b_staged<MODE_LIN, SPK_SELL><<<cfg.grid, kLaneThreads, sm, s>>>(b);
-        } else {
-            if (mode == MODE_SOLVE) k_pass_b_staged<MODE_SOLVE, SPK_ROWT><<<cfg.grid, kLaneThreads, sm, s>>>(b);
-            else k_pass_b_staged<MODE_LIN, SPK_ROWT><<<cfg.grid, kLaneThreads, sm, s>>>(b);
-        }
-        return cudaGetLastError();
-    }
     if (b.sp_kind == SPK_SELL) {
         if (mode == MODE_SOLVE) {
             DQ_LANE_DISPATCH(k_pass_b_sell, MODE_SOLVE, b.sp_u, cfg.grid, b);
