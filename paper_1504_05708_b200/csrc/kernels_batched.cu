@@ -680,14 +680,25 @@ cudaError_t configure_batched_kernels() {
     cudaError_t e;
     if ((e = configure_t<0, kNTA, false>())) return e;
     if ((e = configure_t<0, kNTA, true>())) return e;
+    if ((e = configure_t<0, 5, true>())) return e;
+    if ((e = configure_t<0, 4, true>())) return e;
+    if ((e = configure_t<1, 7, false>())) return e;
+    if ((e = configure_t<1, 3, false>())) return e;
     return configure_t<1, kNTB, false>();
 }
 
 cudaError_t launch_batched(const BatchedArgs &a, int pass, int mode, cudaStream_t s) {
     if (a.N <= 0 || a.M <= 0) return cudaSuccess;
     if (mode != MODE_SOLVE) return cudaErrorInvalidValue;   // the batched path runs solve passes only
-    if (pass == 1) return launch_t<1, kNTB, false>(a, s);
-    return a.pairP > 0 ? launch_t<0, kNTA, true>(a, s) : launch_t<0, kNTA, false>(a, s);
+    // group widths (octets per group): measurement overrides DUQUAD_NTA_PAIR / DUQUAD_NTB
+    static const int nta_pair = getenv("DUQUAD_NTA_PAIR") ? atoi(getenv("DUQUAD_NTA_PAIR")) : kNTA;
+    static const int ntb = getenv("DUQUAD_NTB") ? atoi(getenv("DUQUAD_NTB")) : kNTB;
+    if (pass == 1) return ntb == 7 ? launch_t<1, 7, false>(a, s) : ntb == 3 ? launch_t<1, 3, false>(a, s)
+                                                                             : launch_t<1, kNTB, false>(a, s);
+    if (a.pairP > 0)
+        return nta_pair == 5 ? launch_t<0, 5, true>(a, s) : nta_pair == 4 ? launch_t<0, 4, true>(a, s)
+                                                                            : launch_t<0, kNTA, true>(a, s);
+    return launch_t<0, kNTA, false>(a, s);
 }
 
 // eps_in mode (per QP): the stop test on the QP's sum of (y - x+)^2, then the sum is cleared
