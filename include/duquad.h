@@ -187,6 +187,10 @@ typedef struct {
                               streams [Q; G_t] in pass A (the bottom rows' product is -(G_t y),
                               exactly) and forms G'w as G_t'(w_top - w_bottom) in pass B: half the
                               G work, the same step.  0: the unpaired matrices             */
+    int32_t pdl;           /* 1 (default): the inner-step kernels are launched with programmatic
+                              dependent launch -- each starts while its predecessor drains and
+                              streams matrix data before its dependency wait; iterates are
+                              read and written only after it (same results).  0: plain launches */
 } duquad_options;
 
 /* Per-solve report. */

@@ -55,7 +55,7 @@ class Options(C.Structure):
         ("time_passes", C.c_int32), ("small_path", C.c_int32), ("rho0_path", C.c_int32),
         ("emulate_ranks", C.c_int32), ("fused_path", C.c_int32), ("persist_path", C.c_int32),
         ("eq_precompute", C.c_int32), ("checkpoint", C.c_int32), ("dual_average", C.c_int32),
-        ("nccl_self", C.c_int32), ("sell_path", C.c_int32), ("pair_rows", C.c_int32),
+        ("nccl_self", C.c_int32), ("sell_path", C.c_int32), ("pair_rows", C.c_int32), ("pdl", C.c_int32),
     ]
 
 

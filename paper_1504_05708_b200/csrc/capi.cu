@@ -727,6 +727,16 @@ duquad_status upload_vec(duquad_ctx *ctx, double *dst, const double *src, int64_
 
 // CSR setup: device copies of Q and G (validated), the stacked local [Q_r; G_r]
 // and the local rows of G' (device transpose, deterministic order).
+// Programmatic dependent launch for the inner-step kernels (options.pdl; DUQUAD_PDL=0 disables it
+// for measurements): each kernel starts while its predecessor drains and streams matrix data
+// before its dependency wait (epilogue.cuh pdl_wait)
+void apply_pdl(duquad_ctx *ctx) {
+    const char *ev = getenv("DUQUAD_PDL");
+    const int on = ctx->opt.pdl && !(ev && atoi(ev) == 0) ? 1 : 0;
+    ctx->cfg_a.pdl = ctx->cfg_b.pdl = ctx->cfg_k3.pdl = on;
+    ctx->fz.pdl = on;
+}
+
 // Lane-per-row kernels serve matrices whose mean row length is at most kLaneMaxMean; among them
 // SELL-32 is used when its padded layout holds at most kSellMaxPad x the nonzeros
 constexpr double kLaneMaxMean = 48.0, kSellMaxPad = 1.15;
@@ -910,6 +920,7 @@ void duquad_default_options(duquad_options *o) {
     o->nccl_self = 0;
     o->sell_path = 1;
     o->pair_rows = 1;
+    o->pdl = 1;
 }
 
 duquad_status duquad_shard_range(int64_t rows, int32_t world, int32_t rank, int64_t *begin,
@@ -1266,6 +1277,7 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
                                                              : csr_blocks_per_sm(1, ctx->gs_b)),
                       256, 0};
         CKS(cudaStreamSynchronize(s));
+        apply_pdl(ctx);
         *out = ctx;
         return DUQUAD_OK;
     }
@@ -1417,6 +1429,7 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         }
     }
     CKS(cudaStreamSynchronize(s));
+    apply_pdl(ctx);
     *out = ctx;
     return DUQUAD_OK;
 #undef CKS

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/duquad.h"
@@ -177,6 +178,7 @@ struct FusedArgs {
     int64_t qa, qb;        // this rank's Q rows [qa, qb) (global; Q row 0 is row qa); single GPU: [0, n)
     double *partial;       // row-sharded epilogue mode: write the rank's partial n-vector here, no epilogue
     size_t smem;
+    int32_t pdl;           // launch the stream and epilogue kernels with programmatic dependent launch
     PassAArgs a;           // G-row epilogue (g, mu, lam_prev, cone, rho, step, ops, first_inner)
 };
 
@@ -184,7 +186,36 @@ struct LaunchCfg {
     int grid;
     int threads;
     size_t smem;
+    int pdl = 0;   // launch with programmatic dependent launch (epilogue.cuh pdl_wait)
 };
+
+// cudaLaunchKernelEx with the PDL attribute when `pdl` (plus an optional cluster width)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, int pdl,
+                             int cluster, Args &&...args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (pdl) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (cluster > 0) {
+        at[na].id = cudaLaunchAttributeClusterDimension;
+        at[na].val.clusterDim.x = cluster;
+        at[na].val.clusterDim.y = 1;
+        at[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    cfg.attrs = na ? at : nullptr;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // kernels_csr.cu
 int csr_blocks_per_sm(int pass, int gs);

@@ -11,6 +11,15 @@
 
 namespace dq {
 
+// Programmatic dependent launch (PDL).  A kernel launched with the programmatic-serialization
+// attribute (launch_ex, LaunchCfg.pdl) may start while the previous kernel of the stream drains:
+// before pdl_wait() it may only read data no kernel of the solve writes (the stored matrices);
+// every read of an iterate / flag and every global write comes after it.  Without the attribute
+// griddepcontrol.wait returns at once.  pdl_trigger() lets the next kernel's CTAs be scheduled as
+// soon as resources free up.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // [v]_K per row tag: ZERO -> 0, NONPOS -> min(v, 0)
 // (select forms: a NaN maps to 0 exactly as fmin/fmax(NaN, 0) would, in 3 SASS instead of ~14)
 __device__ __forceinline__ double proj_K(double v, uint8_t c) {

@@ -108,6 +108,8 @@ __device__ __forceinline__ void csr_row_dot2(const int32_t *__restrict__ ci, con
 template <int MODE, int GS>
 // (kCsrThreads, 4): <= 64 registers, 4 resident CTAs per SM (was 3 at 76): more rows in flight
 __global__ void __launch_bounds__(kCsrThreads, 4) k_pass_a_csr(const PassAArgs a) {
+    pdl_wait();   // everything below reads iterates or writes (PDL, epilogue.cuh)
+    pdl_trigger();
     if (a.skip && *a.skip) return;
     const int lane = threadIdx.x & 31, gl = lane & (GS - 1), gw = lane / GS;
     const int64_t gpw = 32 / GS;   // lane groups per warp; a warp covers 2 * gpw consecutive rows
@@ -138,6 +140,8 @@ __global__ void __launch_bounds__(kCsrThreads, 4) k_pass_a_csr(const PassAArgs a
 
 template <int MODE, int GS>
 __global__ void __launch_bounds__(kCsrThreads) k_pass_b_csr(const PassBArgs b) {
+    pdl_wait();
+    pdl_trigger();
     if (b.skip && *b.skip) return;
     const int lane = threadIdx.x & 31, gl = lane & (GS - 1), gw = lane / GS;
     const int64_t gpw = 32 / GS;
@@ -182,11 +186,11 @@ int occ(K kern) {
 template <int MODE>
 cudaError_t dispatch_a(const PassAArgs &a, const LaunchCfg &cfg, cudaStream_t s) {
     switch (a.gs) {
-        case 2: k_pass_a_csr<MODE, 2><<<cfg.grid, kCsrThreads, 0, s>>>(a); break;
-        case 4: k_pass_a_csr<MODE, 4><<<cfg.grid, kCsrThreads, 0, s>>>(a); break;
-        case 8: k_pass_a_csr<MODE, 8><<<cfg.grid, kCsrThreads, 0, s>>>(a); break;
-        case 16: k_pass_a_csr<MODE, 16><<<cfg.grid, kCsrThreads, 0, s>>>(a); break;
-        default: k_pass_a_csr<MODE, 32><<<cfg.grid, kCsrThreads, 0, s>>>(a); break;
+        case 2: return launch_ex(k_pass_a_csr<MODE, 2>, cfg.grid, kCsrThreads, 0, s, cfg.pdl, 0, a);
+        case 4: return launch_ex(k_pass_a_csr<MODE, 4>, cfg.grid, kCsrThreads, 0, s, cfg.pdl, 0, a);
+        case 8: return launch_ex(k_pass_a_csr<MODE, 8>, cfg.grid, kCsrThreads, 0, s, cfg.pdl, 0, a);
+        case 16: return launch_ex(k_pass_a_csr<MODE, 16>, cfg.grid, kCsrThreads, 0, s, cfg.pdl, 0, a);
+        default: return launch_ex(k_pass_a_csr<MODE, 32>, cfg.grid, kCsrThreads, 0, s, cfg.pdl, 0, a);
     }
     return cudaGetLastError();
 }
@@ -194,11 +198,11 @@ cudaError_t dispatch_a(const PassAArgs &a, const LaunchCfg &cfg, cudaStream_t s)
 template <int MODE>
 cudaError_t dispatch_b(const PassBArgs &b, const LaunchCfg &cfg, cudaStream_t s) {
     switch (b.gs) {
-        case 2: k_pass_b_csr<MODE, 2><<<cfg.grid, kCsrThreads, 0, s>>>(b); break;
-        case 4: k_pass_b_csr<MODE, 4><<<cfg.grid, kCsrThreads, 0, s>>>(b); break;
-        case 8: k_pass_b_csr<MODE, 8><<<cfg.grid, kCsrThreads, 0, s>>>(b); break;
-        case 16: k_pass_b_csr<MODE, 16><<<cfg.grid, kCsrThreads, 0, s>>>(b); break;
-        default: k_pass_b_csr<MODE, 32><<<cfg.grid, kCsrThreads, 0, s>>>(b); break;
+        case 2: return launch_ex(k_pass_b_csr<MODE, 2>, cfg.grid, kCsrThreads, 0, s, cfg.pdl, 0, b);
+        case 4: return launch_ex(k_pass_b_csr<MODE, 4>, cfg.grid, kCsrThreads, 0, s, cfg.pdl, 0, b);
+        case 8: return launch_ex(k_pass_b_csr<MODE, 8>, cfg.grid, kCsrThreads, 0, s, cfg.pdl, 0, b);
+        case 16: return launch_ex(k_pass_b_csr<MODE, 16>, cfg.grid, kCsrThreads, 0, s, cfg.pdl, 0, b);
+        default: return launch_ex(k_pass_b_csr<MODE, 32>, cfg.grid, kCsrThreads, 0, s, cfg.pdl, 0, b);
     }
     return cudaGetLastError();
 }

@@ -39,6 +39,9 @@ namespace dq {
 namespace {
 
 constexpr int kLaneThreads = 256;
+#ifndef DQ_LANE_MINB   // minimum resident blocks per SM of the lane kernels (register cap)
+#define DQ_LANE_MINB 1
+#endif
 
 __device__ __forceinline__ uint64_t evict_first() {
     uint64_t pol;
@@ -129,7 +132,9 @@ __device__ __forceinline__ double rowt_dot(const int32_t *__restrict__ ci, const
 }
 
 template <int MODE, int U>
-__global__ void __launch_bounds__(kLaneThreads) k_pass_a_sell(const PassAArgs a) {
+__global__ void __launch_bounds__(kLaneThreads, DQ_LANE_MINB) k_pass_a_sell(const PassAArgs a) {
+    pdl_wait();   // everything below reads iterates or writes (PDL, epilogue.cuh)
+    pdl_trigger();
     if (a.skip && *a.skip) return;
     const SellMat &m = a.sell;
     const int lane = threadIdx.x & 31;
@@ -152,7 +157,9 @@ __global__ void __launch_bounds__(kLaneThreads) k_pass_a_sell(const PassAArgs a)
 }
 
 template <int MODE, int U>
-__global__ void __launch_bounds__(kLaneThreads) k_pass_b_sell(const PassBArgs b) {
+__global__ void __launch_bounds__(kLaneThreads, DQ_LANE_MINB) k_pass_b_sell(const PassBArgs b) {
+    pdl_wait();
+    pdl_trigger();
     if (b.skip && *b.skip) return;
     const SellMat &m = b.sell;
     const int lane = threadIdx.x & 31;
@@ -172,7 +179,9 @@ __global__ void __launch_bounds__(kLaneThreads) k_pass_b_sell(const PassBArgs b)
 }
 
 template <int MODE, int U>
-__global__ void __launch_bounds__(kLaneThreads) k_pass_a_rowt(const PassAArgs a) {
+__global__ void __launch_bounds__(kLaneThreads, DQ_LANE_MINB) k_pass_a_rowt(const PassAArgs a) {
+    pdl_wait();   // everything below reads iterates or writes (PDL, epilogue.cuh)
+    pdl_trigger();
     if (a.skip && *a.skip) return;
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -191,7 +200,9 @@ __global__ void __launch_bounds__(kLaneThreads) k_pass_a_rowt(const PassAArgs a)
 }
 
 template <int MODE, int U>
-__global__ void __launch_bounds__(kLaneThreads) k_pass_b_rowt(const PassBArgs b) {
+__global__ void __launch_bounds__(kLaneThreads, DQ_LANE_MINB) k_pass_b_rowt(const PassBArgs b) {
+    pdl_wait();
+    pdl_trigger();
     if (b.skip && *b.skip) return;
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -345,12 +356,12 @@ int lane_unroll(int kind, int64_t max_width, double mean_len) {
     return kind == SPK_SELL ? 4 : 4;
 }
 
-#define DQ_LANE_DISPATCH(KERN, MODE, U, GRID, ARG)                         \
-    switch (U) {                                                            \
-        case 4: KERN<MODE, 4><<<GRID, kLaneThreads, 0, s>>>(ARG); break;     \
-        case 8: KERN<MODE, 8><<<GRID, kLaneThreads, 0, s>>>(ARG); break;     \
-        case 12: KERN<MODE, 12><<<GRID, kLaneThreads, 0, s>>>(ARG); break;   \
-        default: KERN<MODE, 16><<<GRID, kLaneThreads, 0, s>>>(ARG); break;   \
+#define DQ_LANE_DISPATCH(KERN, MODE, U, GRID, ARG)                                         \
+    switch (U) {                                                                            \
+        case 4: return launch_ex(KERN<MODE, 4>, GRID, kLaneThreads, 0, s, cfg.pdl, 0, ARG);   \
+        case 8: return launch_ex(KERN<MODE, 8>, GRID, kLaneThreads, 0, s, cfg.pdl, 0, ARG);   \
+        case 12: return launch_ex(KERN<MODE, 12>, GRID, kLaneThreads, 0, s, cfg.pdl, 0, ARG); \
+        default: return launch_ex(KERN<MODE, 16>, GRID, kLaneThreads, 0, s, cfg.pdl, 0, ARG); \
     }
 
 int lane_blocks_per_sm(int pass, int kind, int u) {
@@ -375,11 +386,11 @@ cudaError_t launch_pass_a_lane(const PassAArgs &a, int mode, const LaunchCfg &cf
             DQ_LANE_DISPATCH(k_pass_a_sell, MODE_LIN, a.sp_u, cfg.grid, a);
         }
     } else if (mode == MODE_SOLVE) {
-        if (a.sp_u == 4) k_pass_a_rowt<MODE_SOLVE, 4><<<cfg.grid, kLaneThreads, 0, s>>>(a);
-        else k_pass_a_rowt<MODE_SOLVE, 8><<<cfg.grid, kLaneThreads, 0, s>>>(a);
+        if (a.sp_u == 4) return launch_ex(k_pass_a_rowt<MODE_SOLVE, 4>, cfg.grid, kLaneThreads, 0, s, cfg.pdl, 0, a);
+        else return launch_ex(k_pass_a_rowt<MODE_SOLVE, 8>, cfg.grid, kLaneThreads, 0, s, cfg.pdl, 0, a);
     } else {
-        if (a.sp_u == 4) k_pass_a_rowt<MODE_LIN, 4><<<cfg.grid, kLaneThreads, 0, s>>>(a);
-        else k_pass_a_rowt<MODE_LIN, 8><<<cfg.grid, kLaneThreads, 0, s>>>(a);
+        if (a.sp_u == 4) return launch_ex(k_pass_a_rowt<MODE_LIN, 4>, cfg.grid, kLaneThreads, 0, s, cfg.pdl, 0, a);
+        else return launch_ex(k_pass_a_rowt<MODE_LIN, 8>, cfg.grid, kLaneThreads, 0, s, cfg.pdl, 0, a);
     }
     return cudaGetLastError();
 }
@@ -393,11 +404,11 @@ cudaError_t launch_pass_b_lane(const PassBArgs &b, int mode, const LaunchCfg &cf
             DQ_LANE_DISPATCH(k_pass_b_sell, MODE_LIN, b.sp_u, cfg.grid, b);
         }
     } else if (mode == MODE_SOLVE) {
-        if (b.sp_u == 4) k_pass_b_rowt<MODE_SOLVE, 4><<<cfg.grid, kLaneThreads, 0, s>>>(b);
-        else k_pass_b_rowt<MODE_SOLVE, 8><<<cfg.grid, kLaneThreads, 0, s>>>(b);
+        if (b.sp_u == 4) return launch_ex(k_pass_b_rowt<MODE_SOLVE, 4>, cfg.grid, kLaneThreads, 0, s, cfg.pdl, 0, b);
+        else return launch_ex(k_pass_b_rowt<MODE_SOLVE, 8>, cfg.grid, kLaneThreads, 0, s, cfg.pdl, 0, b);
     } else {
-        if (b.sp_u == 4) k_pass_b_rowt<MODE_LIN, 4><<<cfg.grid, kLaneThreads, 0, s>>>(b);
-        else k_pass_b_rowt<MODE_LIN, 8><<<cfg.grid, kLaneThreads, 0, s>>>(b);
+        if (b.sp_u == 4) return launch_ex(k_pass_b_rowt<MODE_LIN, 4>, cfg.grid, kLaneThreads, 0, s, cfg.pdl, 0, b);
+        else return launch_ex(k_pass_b_rowt<MODE_LIN, 8>, cfg.grid, kLaneThreads, 0, s, cfg.pdl, 0, b);
     }
     return cudaGetLastError();
 }

@@ -116,12 +116,13 @@ class Solver:
                  rho0_path: bool = True, emulate_ranks: bool = False, fused_path: bool = True,
                  persist_path: bool = False, dual_average: bool = False, eq_precompute: bool = True,
                  checkpoint: bool = False, nccl_self: bool = False, sell_path: bool = True,
-                 pair_rows: bool = True):
+                 pair_rows: bool = True, pdl: bool = True):
         """Dense Q (n x n) and G (p x n), or scipy.sparse matrices (-> CSR path, row a10).
         dual_average: DGM final dual point from the average of lambda^0..lambda^K.
         nccl_self: world_size 1 on the row-sharded code path over a one-rank NCCL communicator.
         sell_path: CSR input with short rows runs lane-per-row kernels (SELL-32 / thread-per-row).
-        pair_rows: batched QPs with G = [G_t; -G_t] stream G_t only (half the G work)."""
+        pair_rows: batched QPs with G = [G_t; -G_t] stream G_t only (half the G work).
+        pdl: programmatic dependent launch of the inner-step kernels."""
         if hasattr(Q, "tocsr"):
             Qc = Q.tocsr()
             Qc.sort_indices()
@@ -144,7 +145,7 @@ class Solver:
                         time_passes=time_passes, small_path=small_path, rho0_path=rho0_path,
                         emulate_ranks=emulate_ranks, fused_path=fused_path, persist_path=persist_path,
                         dual_average=dual_average, eq_precompute=eq_precompute, checkpoint=checkpoint,
-                        nccl_self=nccl_self, sell_path=sell_path, pair_rows=pair_rows))
+                        nccl_self=nccl_self, sell_path=sell_path, pair_rows=pair_rows, pdl=pdl))
 
     @classmethod
     def csr(cls, n, p, Q_rowptr, Q_col, Q_val, G_rowptr, G_col, G_val, q, g, lb, ub, cone=None,
@@ -212,6 +213,7 @@ class Solver:
         opt.nccl_self = int(o.get("nccl_self", False))
         opt.sell_path = int(o.get("sell_path", True))
         opt.pair_rows = int(o.get("pair_rows", True))
+        opt.pdl = int(o.get("pdl", True))
         ctx = C.c_void_p()
         L.check(lib.duquad_setup(C.byref(ctx), C.byref(prob), float(rho), C.byref(opt)))
         self._ctx = ctx
