@@ -187,10 +187,11 @@ typedef struct {
                               streams [Q; G_t] in pass A (the bottom rows' product is -(G_t y),
                               exactly) and forms G'w as G_t'(w_top - w_bottom) in pass B: half the
                               G work, the same step.  0: the unpaired matrices             */
-    int32_t pdl;           /* 1 (default): the inner-step kernels are launched with programmatic
-                              dependent launch -- each starts while its predecessor drains and
-                              streams matrix data before its dependency wait; iterates are
-                              read and written only after it (same results).  0: plain launches */
+    int32_t pdl;           /* 1 (default): the dense inner-step kernels are launched with
+                              programmatic dependent launch -- a kernel's launch overlaps its
+                              predecessor's tail; it reads and writes iterates only after its
+                              dependency wait (same results).  CSR contexts launch plainly
+                              (measured slower with it).  0: plain launches                  */
 } duquad_options;
 
 /* Per-solve report. */

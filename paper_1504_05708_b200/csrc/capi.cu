@@ -727,12 +727,15 @@ duquad_status upload_vec(duquad_ctx *ctx, double *dst, const double *src, int64_
 
 // CSR setup: device copies of Q and G (validated), the stacked local [Q_r; G_r]
 // and the local rows of G' (device transpose, deterministic order).
-// Programmatic dependent launch for the inner-step kernels (options.pdl; DUQUAD_PDL=0 disables it
-// for measurements): each kernel starts while its predecessor drains and streams matrix data
-// before its dependency wait (epilogue.cuh pdl_wait)
+// Programmatic dependent launch for the inner-step kernels (options.pdl; DUQUAD_PDL=0 / =2 force it
+// off / on for measurements): a kernel's launch and prologue overlap its predecessor's tail
+// (epilogue.cuh pdl_wait).  Measured (profiles/r02_pdl_ab.jsonl): config 1 (dense two-pass, L2-
+// resident, launch-bound) 11.7 -> 10.1 us per step; the sparse lane kernels 75.6 -> 78.0 us (their
+// waiting CTAs take the slots of the grid-stride waves), so CSR contexts launch plainly.
 void apply_pdl(duquad_ctx *ctx) {
     const char *ev = getenv("DUQUAD_PDL");
-    const int on = ctx->opt.pdl && !(ev && atoi(ev) == 0) ? 1 : 0;
+    int on = ctx->opt.pdl && ctx->format != DUQUAD_CSR ? 1 : 0;
+    if (ev) on = atoi(ev) == 2 ? 1 : atoi(ev) == 0 ? 0 : on;
     ctx->cfg_a.pdl = ctx->cfg_b.pdl = ctx->cfg_k3.pdl = on;
     ctx->fz.pdl = on;
 }

@@ -30,9 +30,6 @@ namespace {
 
 constexpr int kThreads = 512;  // threads per CTA of the pass kernels
 constexpr int kUnroll = 16;    // 16-byte loads in flight per lane per row chunk
-#ifndef DQ_PDL_PF              // 1: each warp's first row chunk is loaded before the PDL dependency wait
-#define DQ_PDL_PF 1
-#endif
 
 __device__ __forceinline__ double2 ldg_stream(const double2 *p) {
     double2 r;
@@ -67,40 +64,6 @@ __device__ __forceinline__ double row_dot(const double2 *__restrict__ row,
     return warp_sum((acc0 + acc1) + (acc2 + acc3));
 }
 
-// row_dot with the row's first chunk (the lane's kUnroll loads) already in registers -- issued
-// before the PDL dependency wait, so the matrix latency overlaps the previous kernel's tail and
-// the vector staging.  The same accumulators in the same order: bitwise row_dot.
-__device__ __forceinline__ void row_first(const double2 *__restrict__ row, int nv2, int lane, double2 (&v)[kUnroll]) {
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u)
-        v[u] = lane + 32 * u < nv2 ? ldg_stream(row + lane + 32 * u) : make_double2(0.0, 0.0);
-}
-__device__ __forceinline__ double row_dot_pf(const double2 *__restrict__ row, const double2 *__restrict__ sv, int nv2,
-                                             int lane, const double2 (&pf)[kUnroll]) {
-    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-    for (int c = lane; c - lane < nv2; c += 32 * kUnroll) {
-        double2 v[kUnroll];
-        if (c == lane) {
-#pragma unroll
-            for (int u = 0; u < kUnroll; ++u) v[u] = pf[u];
-        } else {
-#pragma unroll
-            for (int u = 0; u < kUnroll; ++u)
-                v[u] = c + 32 * u < nv2 ? ldg_stream(row + c + 32 * u) : make_double2(0.0, 0.0);
-        }
-#pragma unroll
-        for (int u = 0; u < kUnroll; u += 2) {
-            const double2 y0 = c + 32 * u < nv2 ? sv[c + 32 * u] : make_double2(0.0, 0.0);
-            const double2 y1 = c + 32 * (u + 1) < nv2 ? sv[c + 32 * (u + 1)] : make_double2(0.0, 0.0);
-            acc0 = fma(v[u].x, y0.x, acc0);
-            acc1 = fma(v[u].y, y0.y, acc1);
-            acc2 = fma(v[u + 1].x, y1.x, acc2);
-            acc3 = fma(v[u + 1].y, y1.y, acc3);
-        }
-    }
-    return warp_sum((acc0 + acc1) + (acc2 + acc3));
-}
-
 __device__ __forceinline__ void stage(double *s, const double *g, int64_t len) {
     const double2 *g2 = reinterpret_cast<const double2 *>(g);
     double2 *s2 = reinterpret_cast<double2 *>(s);
@@ -117,10 +80,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass_a(const PassAArgs a) {
     const int64_t r0 = a.row_begin + rows * blockIdx.x / gridDim.x;
     const int64_t r1 = a.row_begin + rows * (blockIdx.x + 1) / gridDim.x;
     const int nv2 = (int)(a.ld >> 1);
-    // before the dependency wait: the first chunk of the warp's first row (matrix data only)
-    double2 pf[kUnroll];
-    if (DQ_PDL_PF && r0 + warp < r1) row_first(reinterpret_cast<const double2 *>(a.A + (r0 + warp) * a.ld), nv2, lane, pf);
-    pdl_wait();
+    pdl_wait();   // PDL (epilogue.cuh): the launch overlaps the previous kernel's tail
     pdl_trigger();
     if (a.skip && *a.skip) return;
     stage(smem, a.y, a.ld);
@@ -131,8 +91,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass_a(const PassAArgs a) {
         // epilogue operands are fetched before the stream so their latency overlaps it
         EpiA e{};
         if (lane == 0) e = epi_a_load(a, MODE, row, o);
-        const double2 *rp = reinterpret_cast<const double2 *>(a.A + row * a.ld);
-        const double s = DQ_PDL_PF && row == r0 + warp ? row_dot_pf(rp, sv, nv2, lane, pf) : row_dot(rp, sv, nv2, lane);
+        const double s = row_dot(reinterpret_cast<const double2 *>(a.A + row * a.ld), sv, nv2, lane);
         if (lane == 0) epi_a_store(a, MODE, row, s, e, o);
     }
 }
@@ -145,10 +104,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass_b(const PassBArgs b) {
     const int64_t r0 = b.nrows * blockIdx.x / gridDim.x;
     const int64_t r1 = b.nrows * (blockIdx.x + 1) / gridDim.x;
     const int nv2 = (int)(b.ldp >> 1);
-    double2 pf[kUnroll];   // before the dependency wait: the first chunk of the warp's first row
-    if (DQ_PDL_PF && r0 + warp < r1 && nv2 > 0)
-        row_first(reinterpret_cast<const double2 *>(b.GT + (r0 + warp) * b.ldp), nv2, lane, pf);
-    pdl_wait();
+    pdl_wait();   // PDL (epilogue.cuh): the launch overlaps the previous kernel's tail
     pdl_trigger();
     if (b.skip && *b.skip) return;
     stage(smem, b.w, b.ldp);
@@ -158,10 +114,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass_b(const PassBArgs b) {
     for (int64_t j = r0 + warp; j < r1; j += nw) {
         EpiB e{};
         if (lane == 0) e = epi_b_load(b, MODE, j, avg_w);
-        const double2 *rp = reinterpret_cast<const double2 *>(b.GT + j * b.ldp);
-        const double t = nv2 <= 0                          ? 0.0
-                         : DQ_PDL_PF && j == r0 + warp ? row_dot_pf(rp, sv, nv2, lane, pf)
-                                                       : row_dot(rp, sv, nv2, lane);
+        const double t = nv2 > 0 ? row_dot(reinterpret_cast<const double2 *>(b.GT + j * b.ldp), sv, nv2, lane)
+                                 : 0.0;
         if (lane == 0) epi_b_store(b, MODE, j, t, e, avg_w);
     }
 }
@@ -260,9 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rho0_step(const PassAArgs a, co
     const int64_t r0 = a.nq * blockIdx.x / gridDim.x;
     const int64_t r1 = a.nq * (blockIdx.x + 1) / gridDim.x;
     const int nv2 = (int)(a.ld >> 1);
-    double2 pf[kUnroll];   // before the dependency wait: the first chunk of the warp's first row
-    if (DQ_PDL_PF && r0 + warp < r1) row_first(reinterpret_cast<const double2 *>(a.A + (r0 + warp) * a.ld), nv2, lane, pf);
-    pdl_wait();
+    pdl_wait();   // PDL (epilogue.cuh): the launch overlaps the previous kernel's tail
     pdl_trigger();
     if (a.skip && *a.skip) return;
     stage(smem, a.y, a.ld);
@@ -272,8 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rho0_step(const PassAArgs a, co
     for (int64_t j = r0 + warp; j < r1; j += nw) {
         EpiB e{};
         if (lane == 0) e = epi_b_load(bl, MODE_SOLVE, j, avg_w);     // bl.q = c, bl.y = yin slice
-        const double2 *rp = reinterpret_cast<const double2 *>(a.A + j * a.ld);
-        const double s = DQ_PDL_PF && j == r0 + warp ? row_dot_pf(rp, sv, nv2, lane, pf) : row_dot(rp, sv, nv2, lane);
+        const double s = row_dot(reinterpret_cast<const double2 *>(a.A + j * a.ld), sv, nv2, lane);
         if (lane == 0) {
             e.qy = s;                                                  // grad = (Qy + c) + 0
             epi_b_store(bs, MODE_SOLVE, j, 0.0, e, avg_w);             // bs.y = yout slice

@@ -156,9 +156,9 @@ __device__ __forceinline__ Tile tile_of(const FusedArgs &f, int J) {
 // Launched with a cluster dimension of 2 when there is a G role (pairs), 1 otherwise.
 template <int NCHG>
 __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f) {
-    // PDL (epilogue.cuh): each role fills its ring with matrix data (Q / G, never written by a
-    // solve) before pdl_wait(); y, the epilogue operands, the eps_in skip flag and every global write
-    // come after it, so the ring fill overlaps the previous kernel (k_fused_epi) and the launch.
+    pdl_wait();   // PDL (epilogue.cuh): only the launch overlaps the previous kernel
+    pdl_trigger();
+    if (f.a.skip && *f.a.skip) return;   // eps_in mode: converged (uniform over the grid)
     constexpr int kSlotsG = kSlots - (NCHG > 0 ? NCHG : 1);
     extern __shared__ __align__(128) uint8_t fsm[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -220,12 +220,6 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
             if (++ps == kSlots) ps = 0;
         };
         for (int t = 0; t < kSlots; ++t) issue();
-        pdl_wait();
-        pdl_trigger();
-        if (f.a.skip && *f.a.skip) {   // eps_in mode: converged (uniform over the grid)
-            cp_wait<0>();
-            return;
-        }
         int cs = 0;
         auto load_q = [&](double *q) {
 #pragma unroll
@@ -349,6 +343,13 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
         // as soon as it is read (kSlotsG chunks in flight).  Half-row lag: the first chunk of row
         // it+1 is read and dotted before waiting for w_it, which hides the cluster exchange.
         double2 *ysm = reinterpret_cast<double2 *>(fsm + kHdr + kSlotsG * kChunk * 8) + tid;   // [NCHG][kV][512]
+        for (int m = 0; m < NCHG; ++m)
+#pragma unroll
+            for (int k = 0; k < kV; ++k) {
+                const int c = a + m * kChunk + 2 * tid + 1024 * k;
+                ysm[(m * kV + k) * kThreadsF] = (m < nch && c < b) ? *reinterpret_cast<const double2 *>(f.y + c)
+                                                                    : make_double2(0.0, 0.0);
+            }
         int p_it = 0, p_m = 0, ps = 0;   // prefetch cursor
         auto issue = [&]() {
             if (p_it < nr) {
@@ -366,20 +367,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
             cp_commit();
             if (++ps == kSlotsG) ps = 0;
         };
-        for (int t = 0; t < kSlotsG; ++t) issue();   // G rows: matrix data, before the dependency wait
-        pdl_wait();
-        pdl_trigger();
-        if (f.a.skip && *f.a.skip) {   // eps_in mode: converged (uniform over the grid)
-            cp_wait<0>();
-            return;
-        }
-        for (int m = 0; m < NCHG; ++m)
-#pragma unroll
-            for (int k = 0; k < kV; ++k) {
-                const int c = a + m * kChunk + 2 * tid + 1024 * k;
-                ysm[(m * kV + k) * kThreadsF] = (m < nch && c < b) ? *reinterpret_cast<const double2 *>(f.y + c)
-                                                                    : make_double2(0.0, 0.0);
-            }
+        for (int t = 0; t < kSlotsG; ++t) issue();
         double acc[NCHG][8];
 #pragma unroll
         for (int m = 0; m < NCHG; ++m)
