@@ -274,6 +274,45 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
                         acc[e] = fma(q1[e], y1, acc[e]);
                         acc[e + 1] = fma(q1[e + 1], y1, acc[e + 1]);
                     }
+                } else if (!rag) {
+                    // diagonal tile (40 % of the row steps at config 2): per 1024-column quarter k the
+                    // warp's 64 columns [lo, lo + 64) are all right of both rows' diagonals, all left,
+                    // or straddle -- a warp-uniform choice, so only the straddling quarter pays the
+                    // per-element masks.  Same accumulators and order as the masked loop (a masked
+                    // term adds an exact zero), so the sums are unchanged.
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int lo = t.a + 1024 * k + 64 * warp;
+                        if (lo > r + 1) {
+#pragma unroll
+                            for (int e = 2 * k; e < 2 * k + 2; ++e) {
+                                if (e & 1) {
+                                    b0 = fma(q0[e], yv[e], b0);
+                                    b1 = fma(q1[e], yv[e], b1);
+                                } else {
+                                    a0 = fma(q0[e], yv[e], a0);
+                                    a1 = fma(q1[e], yv[e], a1);
+                                }
+                                acc[e] = fma(q0[e], y0, acc[e]);
+                                acc[e] = fma(q1[e], y1, acc[e]);
+                            }
+                        } else if (lo + 63 >= r) {
+#pragma unroll
+                            for (int e = 2 * k; e < 2 * k + 2; ++e) {
+                                const int c = cb + (e >> 1) * 1024 + (e & 1);
+                                const double d0 = c >= r ? q0[e] : 0.0, d1 = c >= r + 1 ? q1[e] : 0.0;
+                                if (e & 1) {
+                                    b0 = fma(d0, yv[e], b0);
+                                    b1 = fma(d1, yv[e], b1);
+                                } else {
+                                    a0 = fma(d0, yv[e], a0);
+                                    a1 = fma(d1, yv[e], a1);
+                                }
+                                acc[e] = fma(c > r ? d0 : 0.0, y0, acc[e]);
+                                acc[e] = fma(c > r + 1 ? d1 : 0.0, y1, acc[e]);
+                            }
+                        }
+                    }
                 } else {
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
