@@ -392,20 +392,11 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
         int p_it = 0, p_m = 0, ps = 0;   // prefetch cursor
         auto issue = [&]() {
             if (p_it < nr) {
-                const double *row = f.G + (g0 + p_it) * f.ld + a + p_m * kChunk + 2 * tid;
-                if (!ragged || p_m < nch - 1) {   // full chunk (all but a ragged block's last): no masks
+                const double *row = f.G + (g0 + p_it) * f.ld;
 #pragma unroll
-                    for (int k = 0; k < kV; ++k) cp16(slot_addr(ps, k), row + 1024 * k);
-                } else {   // the ragged last chunk: the positions past the block end are zeroed
-                           // here, by the thread that will read them, so take() needs no mask
-#pragma unroll
-                    for (int k = 0; k < kV; ++k) {
-                        if (a + p_m * kChunk + 2 * tid + 1024 * k < b)
-                            cp16(slot_addr(ps, k), row + 1024 * k);
-                        else
-                            asm volatile("st.shared.v2.f64 [%0], {%1, %1};" ::"r"(slot_addr(ps, k)), "d"(0.0)
-                                         : "memory");
-                    }
+                for (int k = 0; k < kV; ++k) {
+                    const int c = a + p_m * kChunk + 2 * tid + 1024 * k;
+                    if (c < b) cp16(slot_addr(ps, k), row + c);
                 }
                 if (++p_m == nch) {
                     p_m = 0;
@@ -425,9 +416,11 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
         // read chunk m of the next row from the ring into v (slot refilled at once); its dot with y
         auto take = [&](int m, double *v, double part) -> double {
             cp_wait<kSlotsG - 1>();
+            const bool rg = ragged && m == nch - 1;
 #pragma unroll
-            for (int k = 0; k < kV; ++k) {   // (a ragged chunk's unloaded positions hold zeros, issue())
-                const double2 q = ring[(cs * kV + k) * kThreadsF];
+            for (int k = 0; k < kV; ++k) {
+                double2 q = ring[(cs * kV + k) * kThreadsF];
+                if (rg && a + m * kChunk + 2 * tid + 1024 * k >= b) q = make_double2(0.0, 0.0);   // not loaded
                 v[2 * k] = q.x;
                 v[2 * k + 1] = q.y;
             }
