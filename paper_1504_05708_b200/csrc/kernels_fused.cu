@@ -248,6 +248,19 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
             int ybase = rb;
             double ycache = rb + lane < t.rows ? f.y[rb + lane] : 0.0;
             int r = rb;
+            // the row-pair butterfly is software-pipelined: pair i's sums are reduced after pair i+1's
+            // FMAs, so its dependent shuffle chain overlaps independent work (same sums, same order)
+            double p0 = 0.0, p1 = 0.0;
+            int pr_ = -1;
+            auto finish_pair = [&](double u0, double u1, int rr) {
+                double mine = (lane & 16) ? u1 : u0;
+                mine += __shfl_xor_sync(0xffffffffu, (lane & 16) ? u0 : u1, 16);
+                mine += __shfl_xor_sync(0xffffffffu, mine, 8);
+                mine += __shfl_xor_sync(0xffffffffu, mine, 4);
+                mine += __shfl_xor_sync(0xffffffffu, mine, 2);
+                mine += __shfl_xor_sync(0xffffffffu, mine, 1);
+                if ((lane & 15) == 0) rowp[rr + (lane >> 4)] = mine;
+            };
             for (; r + 1 < re; r += 2) {   // two row steps per iteration (independent chains)
                 if (r + 1 - ybase >= 32) {
                     ybase = r;
@@ -330,16 +343,14 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
                         acc[e] = fma(c > r + 1 ? d1 : 0.0, y1, acc[e]);
                     }
                 }
-                // both row sums with one butterfly: lanes < 16 reduce row r, lanes >= 16 row r + 1
-                const double s0 = a0 + b0, s1 = a1 + b1;
-                double mine = (lane & 16) ? s1 : s0;
-                mine += __shfl_xor_sync(0xffffffffu, (lane & 16) ? s0 : s1, 16);
-                mine += __shfl_xor_sync(0xffffffffu, mine, 8);
-                mine += __shfl_xor_sync(0xffffffffu, mine, 4);
-                mine += __shfl_xor_sync(0xffffffffu, mine, 2);
-                mine += __shfl_xor_sync(0xffffffffu, mine, 1);
-                if ((lane & 15) == 0) rowp[r + (lane >> 4)] = mine;
+                // both row sums with one butterfly (lanes < 16 reduce row r, lanes >= 16 row r + 1),
+                // the previous pair's first
+                if (pr_ >= 0) finish_pair(p0, p1, pr_);
+                p0 = a0 + b0;
+                p1 = a1 + b1;
+                pr_ = r;
             }
+            if (pr_ >= 0) finish_pair(p0, p1, pr_);
             if (r < re) {   // last row of the segment
                 if (r - ybase >= 32) {
                     ybase = r;
