@@ -37,6 +37,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "duquad_internal.h"
@@ -400,138 +401,147 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
                 ysm[(m * kV + k) * kThreadsF] = (m < nch && c < b) ? *reinterpret_cast<const double2 *>(f.y + c)
                                                                     : make_double2(0.0, 0.0);
             }
-        int p_it = 0, p_m = 0, ps = 0;   // prefetch cursor
-        auto issue = [&]() {
-            if (p_it < nr) {
-                const double *row = f.G + (g0 + p_it) * f.ld;
-#pragma unroll
-                for (int k = 0; k < kV; ++k) {
-                    const int c = a + p_m * kChunk + 2 * tid + 1024 * k;
-                    if (c < b) cp16(slot_addr(ps, k), row + c);
+        // the G loop is compiled twice: RAG (the rank's block ends in a partial chunk: per-element
+        // masks on that chunk) and not (config 2: no masks at all in the hot loop)
+        auto g_body = [&](auto rag_c) {
+            constexpr bool RAG = decltype(rag_c)::value;
+            int p_it = 0, p_m = 0, ps = 0;   // prefetch cursor
+            auto issue = [&]() {
+                if (p_it < nr) {
+                    const double *row = f.G + (g0 + p_it) * f.ld;
+    #pragma unroll
+                    for (int k = 0; k < kV; ++k) {
+                        const int c = a + p_m * kChunk + 2 * tid + 1024 * k;
+                        if (!RAG || c < b) cp16(slot_addr(ps, k), row + c);
+                    }
+                    if (++p_m == nch) {
+                        p_m = 0;
+                        ++p_it;
+                    }
                 }
-                if (++p_m == nch) {
-                    p_m = 0;
-                    ++p_it;
-                }
-            }
-            cp_commit();
-            if (++ps == kSlotsG) ps = 0;
-        };
-        for (int t = 0; t < kSlotsG; ++t) issue();
-        double acc[NCHG][8];
-#pragma unroll
-        for (int m = 0; m < NCHG; ++m)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) acc[m][e] = 0.0;
-        int cs = 0;
-        // read chunk m of the next row from the ring into v (slot refilled at once); its dot with y
-        auto take = [&](int m, double *v, double part) -> double {
-            cp_wait<kSlotsG - 1>();
-            const bool rg = ragged && m == nch - 1;
-#pragma unroll
-            for (int k = 0; k < kV; ++k) {
-                double2 q = ring[(cs * kV + k) * kThreadsF];
-                if (rg && a + m * kChunk + 2 * tid + 1024 * k >= b) q = make_double2(0.0, 0.0);   // not loaded
-                v[2 * k] = q.x;
-                v[2 * k + 1] = q.y;
-            }
-            issue();
-            if (++cs == kSlotsG) cs = 0;
-#pragma unroll
-            for (int k = 0; k < kV; ++k) {
-                const double2 yk = ysm[(m * kV + k) * kThreadsF];
-                part = fma(v[2 * k], yk.x, part);
-                part = fma(v[2 * k + 1], yk.y, part);
-            }
-            return part;
-        };
-        // Row finishing: the LAST warp to post its partial (shared-memory counter) forms the CTA sum
-        // of the 16 warp partials (fixed tree) and sends it to every CTA of the cluster with
-        // st.async (completing the rows' exchange barrier); every warp then forms w itself (row_w).
-        // The epilogue operands of row it are prefetched into shared memory two rows ahead.
-        const OuterA o = outer_a(f.a, MODE_SOLVE);
-        const uint32_t xb_r = map_to_cta(smem_u32(xbuf), (uint32_t)(lane & 1));
-        const uint32_t xm_r = map_to_cta(smem_u32(xbar), (uint32_t)(lane & 1));
-        auto prefetch_epi = [&](int it) {
-            if (tid == 0 && it < nr) {
-                const EpiA e = epi_a_load(f.a, MODE_SOLVE, f.a.nq + g0 + it, o);
-                double *eb = epib + (it % kD) * 5;
-                eb[0] = e.g;
-                eb[1] = e.mu;
-                eb[2] = e.lp;
-                eb[3] = (double)e.c;
-                eb[4] = e.lh;
-            }
-        };
-        // Row finishing without any intra-CTA hand-off: every warp sends its partial of the row to
-        // both CTAs of the pair (st.async into xbuf[d][rank * 16 + warp], completing 8 bytes of the
-        // row's exchange barrier there; warp 0 arms the barrier for all 32 partials), then waits for
-        // the barrier and forms w itself: fixed butterfly over the 32 partials, pass-A epilogue.
-        auto post = [&](int it, double part) {
-            part = warp_sum(part);
-            const int d = it % kD;
-            if (lane < 2)   // lane c -> CTA c of the pair
-                st_async_f64(xb_r + (uint32_t)(d * 32 + (int)rank * kWarps + warp) * 8, part,
-                             xm_r + (uint32_t)d * 8);
-            if (warp == 0 && lane == 0) mbar_arrive_expect_tx(&xbar[d], 2u * kWarps * 8u);
-        };
-        auto row_w = [&](int it) -> double {
-            const int d = it % kD;
-            mbar_wait(&xbar[d], (uint32_t)((it / kD) & 1));
-            double s_row = xbuf[d * 32 + lane];
-            s_row += __shfl_xor_sync(0xffffffffu, s_row, 16);
-            s_row += __shfl_xor_sync(0xffffffffu, s_row, 8);
-            s_row += __shfl_xor_sync(0xffffffffu, s_row, 4);
-            s_row += __shfl_xor_sync(0xffffffffu, s_row, 2);
-            s_row += __shfl_xor_sync(0xffffffffu, s_row, 1);
-            const double *eb = epib + d * 5;
-            EpiA e;
-            e.g = eb[0];
-            e.mu = eb[1];
-            e.lp = eb[2];
-            e.c = (uint8_t)eb[3];
-            e.lh = eb[4];
-            return g_row_w(f.a, g0 + it, s_row, e, o, rank == 0 && warp == 0 && lane == 0);
-        };
-        prefetch_epi(0);
-        prefetch_epi(1);
-        double hold[NCHG][8];   // the current row's values (chunks 0..nch-1)
-        if (nr > 0) {
-            double part = 0.0;
-#pragma unroll
+                cp_commit();
+                if (++ps == kSlotsG) ps = 0;
+            };
+            for (int t = 0; t < kSlotsG; ++t) issue();
+            double acc[NCHG][8];
+    #pragma unroll
             for (int m = 0; m < NCHG; ++m)
-                if (m < nch) part = take(m, hold[m], part);
-            post(0, part);
-        }
-        for (int it = 0; it < nr; ++it) {
-            const bool nxt = it + 1 < nr;
-            prefetch_epi(it + 2);
-            double next0[8];
-            double part = 0.0;
-            if (nxt) part = take(0, next0, part);                    // row it+1, chunk 0
-            const double w = row_w(it);
-#pragma unroll
-            for (int m = 0; m < NCHG; ++m)                              // w G of row it
-#pragma unroll
-                for (int e = 0; e < 8; ++e) acc[m][e] = fma(w, hold[m][e], acc[m][e]);
-            if (nxt) {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) hold[0][e] = next0[e];
-#pragma unroll
-                for (int m = 1; m < NCHG; ++m)
-                    if (m < nch) part = take(m, hold[m], part);         // row it+1, chunks 1..
-                post(it + 1, part);
+    #pragma unroll
+                for (int e = 0; e < 8; ++e) acc[m][e] = 0.0;
+            int cs = 0;
+            // read chunk m of the next row from the ring into v (slot refilled at once); its dot with y
+            auto take = [&](int m, double *v, double part) -> double {
+                cp_wait<kSlotsG - 1>();
+                const bool rg = RAG && m == nch - 1;
+    #pragma unroll
+                for (int k = 0; k < kV; ++k) {
+                    double2 q = ring[(cs * kV + k) * kThreadsF];
+                    if (rg && a + m * kChunk + 2 * tid + 1024 * k >= b) q = make_double2(0.0, 0.0);   // not loaded
+                    v[2 * k] = q.x;
+                    v[2 * k + 1] = q.y;
+                }
+                issue();
+                if (++cs == kSlotsG) cs = 0;
+    #pragma unroll
+                for (int k = 0; k < kV; ++k) {
+                    const double2 yk = ysm[(m * kV + k) * kThreadsF];
+                    part = fma(v[2 * k], yk.x, part);
+                    part = fma(v[2 * k + 1], yk.y, part);
+                }
+                return part;
+            };
+            // Row finishing: the LAST warp to post its partial (shared-memory counter) forms the CTA sum
+            // of the 16 warp partials (fixed tree) and sends it to every CTA of the cluster with
+            // st.async (completing the rows' exchange barrier); every warp then forms w itself (row_w).
+            // The epilogue operands of row it are prefetched into shared memory two rows ahead.
+            const OuterA o = outer_a(f.a, MODE_SOLVE);
+            const uint32_t xb_r = map_to_cta(smem_u32(xbuf), (uint32_t)(lane & 1));
+            const uint32_t xm_r = map_to_cta(smem_u32(xbar), (uint32_t)(lane & 1));
+            auto prefetch_epi = [&](int it) {
+                if (tid == 0 && it < nr) {
+                    const EpiA e = epi_a_load(f.a, MODE_SOLVE, f.a.nq + g0 + it, o);
+                    double *eb = epib + (it % kD) * 5;
+                    eb[0] = e.g;
+                    eb[1] = e.mu;
+                    eb[2] = e.lp;
+                    eb[3] = (double)e.c;
+                    eb[4] = e.lh;
+                }
+            };
+            // Row finishing without any intra-CTA hand-off: every warp sends its partial of the row to
+            // both CTAs of the pair (st.async into xbuf[d][rank * 16 + warp], completing 8 bytes of the
+            // row's exchange barrier there; warp 0 arms the barrier for all 32 partials), then waits for
+            // the barrier and forms w itself: fixed butterfly over the 32 partials, pass-A epilogue.
+            auto post = [&](int it, double part) {
+                part = warp_sum(part);
+                const int d = it % kD;
+                if (lane < 2)   // lane c -> CTA c of the pair
+                    st_async_f64(xb_r + (uint32_t)(d * 32 + (int)rank * kWarps + warp) * 8, part,
+                                 xm_r + (uint32_t)d * 8);
+                if (warp == 0 && lane == 0) mbar_arrive_expect_tx(&xbar[d], 2u * kWarps * 8u);
+            };
+            auto row_w = [&](int it) -> double {
+                const int d = it % kD;
+                mbar_wait(&xbar[d], (uint32_t)((it / kD) & 1));
+                double s_row = xbuf[d * 32 + lane];
+                s_row += __shfl_xor_sync(0xffffffffu, s_row, 16);
+                s_row += __shfl_xor_sync(0xffffffffu, s_row, 8);
+                s_row += __shfl_xor_sync(0xffffffffu, s_row, 4);
+                s_row += __shfl_xor_sync(0xffffffffu, s_row, 2);
+                s_row += __shfl_xor_sync(0xffffffffu, s_row, 1);
+                const double *eb = epib + d * 5;
+                EpiA e;
+                e.g = eb[0];
+                e.mu = eb[1];
+                e.lp = eb[2];
+                e.c = (uint8_t)eb[3];
+                e.lh = eb[4];
+                return g_row_w(f.a, g0 + it, s_row, e, o, rank == 0 && warp == 0 && lane == 0);
+            };
+            prefetch_epi(0);
+            prefetch_epi(1);
+            double hold[NCHG][8];   // the current row's values (chunks 0..nch-1)
+            if (nr > 0) {
+                double part = 0.0;
+    #pragma unroll
+                for (int m = 0; m < NCHG; ++m)
+                    if (m < nch) part = take(m, hold[m], part);
+                post(0, part);
             }
-        }
-        cp_wait<0>();
-        double *pt = f.ws_g + (int64_t)gi * f.ld;
-#pragma unroll
-        for (int m = 0; m < NCHG; ++m)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const int c = a + m * kChunk + own_col(tid, e);
-                if (m < nch && c < b) pt[c] = acc[m][e];
+            for (int it = 0; it < nr; ++it) {
+                const bool nxt = it + 1 < nr;
+                prefetch_epi(it + 2);
+                double next0[8];
+                double part = 0.0;
+                if (nxt) part = take(0, next0, part);                    // row it+1, chunk 0
+                const double w = row_w(it);
+    #pragma unroll
+                for (int m = 0; m < NCHG; ++m)                              // w G of row it
+    #pragma unroll
+                    for (int e = 0; e < 8; ++e) acc[m][e] = fma(w, hold[m][e], acc[m][e]);
+                if (nxt) {
+    #pragma unroll
+                    for (int e = 0; e < 8; ++e) hold[0][e] = next0[e];
+    #pragma unroll
+                    for (int m = 1; m < NCHG; ++m)
+                        if (m < nch) part = take(m, hold[m], part);         // row it+1, chunks 1..
+                    post(it + 1, part);
+                }
             }
+            cp_wait<0>();
+            double *pt = f.ws_g + (int64_t)gi * f.ld;
+    #pragma unroll
+            for (int m = 0; m < NCHG; ++m)
+    #pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int c = a + m * kChunk + own_col(tid, e);
+                    if (m < nch && c < b) pt[c] = acc[m][e];
+                }
+        };
+        if (ragged)
+            g_body(std::true_type{});
+        else
+            g_body(std::false_type{});
     }
     __syncthreads();
     cluster_sync_all();   // no CTA leaves while its partner may still write its shared memory
