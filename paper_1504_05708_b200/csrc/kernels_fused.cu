@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
     pdl_wait();   // PDL (epilogue.cuh): only the launch overlaps the previous kernel
     pdl_trigger();
     if (f.a.skip && *f.a.skip) return;   // eps_in mode: converged (uniform over the grid)
+    constexpr int kSlotsG = kSlots - (NCHG > 0 ? NCHG : 1);
     extern __shared__ __align__(128) uint8_t fsm[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int cta = blockIdx.x;
@@ -388,29 +389,27 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
         const int gi = (cta - f.nq_ctas) >> 1;
         const int64_t g0 = f.p * gi / f.ng, g1 = f.p * (gi + 1) / f.ng;
         const int nr = (int)(g1 - g0);
-        // The G role streams its rows through the whole kSlots ring and keeps a row's chunks IN THE
-        // RING until its w is known: per iteration it dots row it+1 (its chunks stay held), posts that
-        // partial to the pair, and only then waits for w_it and applies w_it G_it from row it's held
-        // slots, refilling each as it is released (slots are used and refilled in FIFO order, so row
-        // i's chunk m sits in slot (i nch + m) mod kSlots).  A full row of work hides each pair
-        // exchange; the CTA's block of y lives in registers.  Summation orders: as before.
+        // The G role keeps this CTA's block of y in shared memory (after a kSlotsG-slot ring) and
+        // row values in registers between their dot and their w G, so every ring slot is refilled
+        // as soon as it is read (kSlotsG chunks in flight).  Half-row lag: the first chunk of row
+        // it+1 is read and dotted before waiting for w_it, which hides the cluster exchange.
+        double2 *ysm = reinterpret_cast<double2 *>(fsm + kHdr + kSlotsG * kChunk * 8) + tid;   // [NCHG][kV][512]
+        for (int m = 0; m < NCHG; ++m)
+#pragma unroll
+            for (int k = 0; k < kV; ++k) {
+                const int c = a + m * kChunk + 2 * tid + 1024 * k;
+                ysm[(m * kV + k) * kThreadsF] = (m < nch && c < b) ? *reinterpret_cast<const double2 *>(f.y + c)
+                                                                    : make_double2(0.0, 0.0);
+            }
         // the G loop is compiled twice: RAG (the rank's block ends in a partial chunk: per-element
         // masks on that chunk) and not (config 2: no masks at all in the hot loop)
         auto g_body = [&](auto rag_c) {
             constexpr bool RAG = decltype(rag_c)::value;
-            double yreg[NCHG][8];   // this thread's columns of the CTA's y block
-#pragma unroll
-            for (int m = 0; m < NCHG; ++m)
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const int c = a + m * kChunk + own_col(tid, e);
-                    yreg[m][e] = (m < nch && c < b) ? f.y[c] : 0.0;
-                }
-            int p_it = 0, p_m = 0, ps = 0;   // prefetch cursor (FIFO over the ring)
+            int p_it = 0, p_m = 0, ps = 0;   // prefetch cursor
             auto issue = [&]() {
                 if (p_it < nr) {
                     const double *row = f.G + (g0 + p_it) * f.ld;
-#pragma unroll
+    #pragma unroll
                     for (int k = 0; k < kV; ++k) {
                         const int c = a + p_m * kChunk + 2 * tid + 1024 * k;
                         if (!RAG || c < b) cp16(slot_addr(ps, k), row + c);
@@ -421,73 +420,40 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
                     }
                 }
                 cp_commit();
-                if (++ps == kSlots) ps = 0;
+                if (++ps == kSlotsG) ps = 0;
             };
-            for (int t = 0; t < kSlots; ++t) issue();
+            for (int t = 0; t < kSlotsG; ++t) issue();
             double acc[NCHG][8];
-#pragma unroll
+    #pragma unroll
             for (int m = 0; m < NCHG; ++m)
-#pragma unroll
+    #pragma unroll
                 for (int e = 0; e < 8; ++e) acc[m][e] = 0.0;
-            // wait until at most `n` cp.async groups of this thread are pending
-            auto wait_pending = [](int n) {
-                switch (n) {
-                    case 0: cp_wait<0>(); break;
-                    case 1: cp_wait<1>(); break;
-                    case 2: cp_wait<2>(); break;
-                    case 3: cp_wait<3>(); break;
-                    case 4: cp_wait<4>(); break;
-                    case 5: cp_wait<5>(); break;
-                    default: cp_wait<6>(); break;
-                }
-            };
-            // chunk m of row i: its values (the ragged chunk's unloaded positions as zeros)
-            auto row_chunk = [&](int i, int m, double *v) {
-                const int sl = (i * nch + m) % kSlots;
-#pragma unroll
+            int cs = 0;
+            // read chunk m of the next row from the ring into v (slot refilled at once); its dot with y
+            auto take = [&](int m, double *v, double part) -> double {
+                cp_wait<kSlotsG - 1>();
+                const bool rg = RAG && m == nch - 1;
+    #pragma unroll
                 for (int k = 0; k < kV; ++k) {
-                    double2 q = ring[(sl * kV + k) * kThreadsF];
-                    if (RAG && m == nch - 1 && a + m * kChunk + 2 * tid + 1024 * k >= b) q = make_double2(0.0, 0.0);
+                    double2 q = ring[(cs * kV + k) * kThreadsF];
+                    if (rg && a + m * kChunk + 2 * tid + 1024 * k >= b) q = make_double2(0.0, 0.0);   // not loaded
                     v[2 * k] = q.x;
                     v[2 * k + 1] = q.y;
                 }
-            };
-            // dot of row i with y (its chunks stay held in the ring).  When row i is read, the held
-            // slots are row i-1's nch and row i's first m: the groups issued after chunk m's are
-            // kSlots - nch - m - 1 (row 0 waits a little longer than needed).
-            auto dot_row = [&](int i) -> double {
-                double part = 0.0;
-#pragma unroll
-                for (int m = 0; m < NCHG; ++m)
-                    if (m < nch) {
-                        wait_pending(kSlots - nch - m - 1);
-                        double v[8];
-                        row_chunk(i, m, v);
-#pragma unroll
-                        for (int k = 0; k < kV; ++k) {
-                            part = fma(v[2 * k], yreg[m][2 * k], part);
-                            part = fma(v[2 * k + 1], yreg[m][2 * k + 1], part);
-                        }
-                    }
+                issue();
+                if (++cs == kSlotsG) cs = 0;
+    #pragma unroll
+                for (int k = 0; k < kV; ++k) {
+                    const double2 yk = ysm[(m * kV + k) * kThreadsF];
+                    part = fma(v[2 * k], yk.x, part);
+                    part = fma(v[2 * k + 1], yk.y, part);
+                }
                 return part;
             };
-            // w_i G_i from row i's held chunks; each slot is refilled as it is released
-            auto wg_row = [&](int i, double w) {
-#pragma unroll
-                for (int m = 0; m < NCHG; ++m)
-                    if (m < nch) {
-                        double v[8];
-                        row_chunk(i, m, v);
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) acc[m][e] = fma(w, v[e], acc[m][e]);
-                        issue();
-                    }
-            };
-            // Row finishing: every warp sends its partial of the row to both CTAs of the pair (st.async
-            // into xbuf[d][rank * 16 + warp], completing 8 bytes of the row's exchange barrier there;
-            // warp 0 arms the barrier for all 32 partials), then -- a row later -- waits for the
-            // barrier and forms w itself: fixed butterfly over the 32 partials, pass-A epilogue.  The
-            // epilogue operands of row it are prefetched into shared memory two rows ahead.
+            // Row finishing: the LAST warp to post its partial (shared-memory counter) forms the CTA sum
+            // of the 16 warp partials (fixed tree) and sends it to every CTA of the cluster with
+            // st.async (completing the rows' exchange barrier); every warp then forms w itself (row_w).
+            // The epilogue operands of row it are prefetched into shared memory two rows ahead.
             const OuterA o = outer_a(f.a, MODE_SOLVE);
             const uint32_t xb_r = map_to_cta(smem_u32(xbuf), (uint32_t)(lane & 1));
             const uint32_t xm_r = map_to_cta(smem_u32(xbar), (uint32_t)(lane & 1));
@@ -502,6 +468,10 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
                     eb[4] = e.lh;
                 }
             };
+            // Row finishing without any intra-CTA hand-off: every warp sends its partial of the row to
+            // both CTAs of the pair (st.async into xbuf[d][rank * 16 + warp], completing 8 bytes of the
+            // row's exchange barrier there; warp 0 arms the barrier for all 32 partials), then waits for
+            // the barrier and forms w itself: fixed butterfly over the 32 partials, pass-A epilogue.
             auto post = [&](int it, double part) {
                 part = warp_sum(part);
                 const int d = it % kD;
@@ -512,8 +482,12 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
             };
             auto row_w = [&](int it) -> double {
                 const int d = it % kD;
+#ifndef DQ_EXP_NOWAIT   // timing experiment only (wrong results): skip the pair exchange wait
                 mbar_wait(&xbar[d], (uint32_t)((it / kD) & 1));
                 double s_row = xbuf[d * 32 + lane];
+#else
+                double s_row = 0.0 * (double)d;
+#endif
                 s_row += __shfl_xor_sync(0xffffffffu, s_row, 16);
                 s_row += __shfl_xor_sync(0xffffffffu, s_row, 8);
                 s_row += __shfl_xor_sync(0xffffffffu, s_row, 4);
@@ -530,17 +504,39 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
             };
             prefetch_epi(0);
             prefetch_epi(1);
-            if (nr > 0) post(0, dot_row(0));
+            double hold[NCHG][8];   // the current row's values (chunks 0..nch-1)
+            if (nr > 0) {
+                double part = 0.0;
+    #pragma unroll
+                for (int m = 0; m < NCHG; ++m)
+                    if (m < nch) part = take(m, hold[m], part);
+                post(0, part);
+            }
             for (int it = 0; it < nr; ++it) {
+                const bool nxt = it + 1 < nr;
                 prefetch_epi(it + 2);
-                if (it + 1 < nr) post(it + 1, dot_row(it + 1));   // row it+1 first: hides it's exchange
-                wg_row(it, row_w(it));
+                double next0[8];
+                double part = 0.0;
+                if (nxt) part = take(0, next0, part);                    // row it+1, chunk 0
+                const double w = row_w(it);
+    #pragma unroll
+                for (int m = 0; m < NCHG; ++m)                              // w G of row it
+    #pragma unroll
+                    for (int e = 0; e < 8; ++e) acc[m][e] = fma(w, hold[m][e], acc[m][e]);
+                if (nxt) {
+    #pragma unroll
+                    for (int e = 0; e < 8; ++e) hold[0][e] = next0[e];
+    #pragma unroll
+                    for (int m = 1; m < NCHG; ++m)
+                        if (m < nch) part = take(m, hold[m], part);         // row it+1, chunks 1..
+                    post(it + 1, part);
+                }
             }
             cp_wait<0>();
             double *pt = f.ws_g + (int64_t)gi * f.ld;
-#pragma unroll
+    #pragma unroll
             for (int m = 0; m < NCHG; ++m)
-#pragma unroll
+    #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                     const int c = a + m * kChunk + own_col(tid, e);
                     if (m < nch && c < b) pt[c] = acc[m][e];
