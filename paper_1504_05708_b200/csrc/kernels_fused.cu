@@ -482,12 +482,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
             };
             auto row_w = [&](int it) -> double {
                 const int d = it % kD;
-#ifndef DQ_EXP_NOWAIT   // timing experiment only (wrong results): skip the pair exchange wait
                 mbar_wait(&xbar[d], (uint32_t)((it / kD) & 1));
                 double s_row = xbuf[d * 32 + lane];
-#else
-                double s_row = 0.0 * (double)d;
-#endif
                 s_row += __shfl_xor_sync(0xffffffffu, s_row, 16);
                 s_row += __shfl_xor_sync(0xffffffffu, s_row, 8);
                 s_row += __shfl_xor_sync(0xffffffffu, s_row, 4);
