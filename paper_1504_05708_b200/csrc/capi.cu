@@ -62,6 +62,8 @@ struct duquad_ctx {
     int gs_a = 4, gs_b = 4;
     SellStore sell_a, sell_b;   // SELL-32 copies of the two (options.sell_path; empty unless kind SPK_SELL)
     int kind_a = SPK_CSR, kind_b = SPK_CSR, u_a = 8, u_b = 8;   // SparseKind and load-round width per pass
+    int box_uniform = 0;        // this context's lb / ub are constant vectors (lb_u, ub_u)
+    double lb_u = 0.0, ub_u = 0.0;
     // batched storage (batch > 1): QP-major per-QP vectors, strides ld (n-vectors) / ldp (p-vectors)
     int64_t Btot = 1, Bloc = 1, b0 = 0;
     double *Yb = nullptr, *Xb = nullptr, *XHb = nullptr, *QYb = nullptr, *qb = nullptr;
@@ -315,6 +317,9 @@ PassBArgs make_b(duquad_ctx *c) {
     b.va = c->b_va;
     b.skip = c->eps_mode ? c->d_done : nullptr;
     b.gm_sq = c->eps_mode ? c->gm_sq : nullptr;
+    b.box_uniform = c->box_uniform;
+    b.lb_u = c->lb_u;
+    b.ub_u = c->ub_u;
     b.sp_kind = c->kind_b;
     b.sp_u = c->u_b;
     b.sell = sell_view(c->sell_b);
@@ -1180,6 +1185,18 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         upload_vec(ctx, ctx->ub, prob->ub + ctx->r0, ctx->nloc) ||
         (p > 0 && upload_vec(ctx, ctx->g, prob->g + ctx->s0, ctx->ploc)))
         return bail(DUQUAD_ECUDA);
+    if (ctx->nloc > 0) {   // a box with scalar bounds (every lb_j, ub_j equal): the epilogues skip their loads
+        std::vector<double> hl(ctx->nloc), hu(ctx->nloc);
+        CKS(cudaMemcpyAsync(hl.data(), ctx->lb, ctx->nloc * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CKS(cudaMemcpyAsync(hu.data(), ctx->ub, ctx->nloc * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CKS(cudaStreamSynchronize(s));
+        bool uni = true;
+        for (int64_t i = 1; i < ctx->nloc && uni; ++i)
+            uni = std::memcmp(&hl[i], &hl[0], sizeof(double)) == 0 && std::memcmp(&hu[i], &hu[0], sizeof(double)) == 0;
+        ctx->box_uniform = uni ? 1 : 0;
+        ctx->lb_u = hl[0];
+        ctx->ub_u = hu[0];
+    }
     if (p > 0 && ctx->ploc > 0) {
         if (prob->cone)
             CKS(cudaMemcpyAsync(ctx->cone, prob->cone + ctx->s0, ctx->ploc, cudaMemcpyDefault, s));

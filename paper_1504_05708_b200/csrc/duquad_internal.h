@@ -109,6 +109,8 @@ struct PassBArgs {
     const double *va;
     const int32_t *skip; // eps_in mode: the inner solve has converged -> the launch does nothing
     double *gm_sq;       // eps_in mode: gm_sq[j] = (y_j - x+_j)^2 (gradient-map test)
+    int32_t box_uniform; // every lb_j == lb_u and ub_j == ub_u: the epilogue skips the lb / ub loads
+    double lb_u, ub_u;
     int32_t sp_kind;     // SparseKind: sub-warp CSR, SELL-32 or thread-per-row CSR
     int32_t sp_u;        // lane kernels: nonzeros per load round
     SellMat sell;

@@ -145,8 +145,13 @@ __device__ __forceinline__ EpiB epi_b_load(const PassBArgs &b, int mode, int64_t
     if (mode == MODE_SOLVE || b.use_qy) e.qy = b.qy[j];
     if (mode == MODE_SOLVE) {
         e.q = b.q[j];
-        e.lb = b.lb[j];
-        e.ub = b.ub[j];
+        if (b.box_uniform) {   // U = [lb, ub]^n with scalar bounds (c4's [-1, 1]): no per-row loads
+            e.lb = b.lb_u;
+            e.ub = b.ub_u;
+        } else {
+            e.lb = b.lb[j];
+            e.ub = b.ub[j];
+        }
         e.x = b.x[j];
         e.y = b.y[j];
         if (avg_w != 0.0) e.xh = b.xhat[j];

@@ -203,15 +203,21 @@ def _skewed(n=2500, p=900, seed=11):
     return qpgen.SparseQP(Q, base.q, G, g, base.lb, base.ub, cone)
 
 
-@pytest.mark.parametrize("maker,kinds", [("banded", (SELL, ROWT)), ("skewed", (ROWT, ROWT))])
+@pytest.mark.parametrize("maker,kinds", [("banded", (SELL, ROWT)), ("skewed", (ROWT, ROWT)), ("box", (SELL, ROWT))])
 @pytest.mark.parametrize("alg", ["DGM", "DFGM"])
 def test_lane_kernels_vs_subwarp_kernels_and_oracle(torch_cuda, maker, kinds, alg):
     """The lane-per-row kernels -- SELL-32 for the banded config-4 family's [Q;G] (rows of 11 and 8
     nonzeros), thread-per-row CSR for its G' (Poisson(4) rows) and for skewed rows -- against the
     sub-warp CSR kernels (same row sums up to summation order: 1e-12) and the oracle (1e-9), with
     the per-outer trace."""
-    prob = qpgen.sparse_banded_eq(n=3001, p=1201, seed=2) if maker == "banded" else _skewed()
-    rho = 5.0 if maker == "banded" else 2.0
+    prob = qpgen.sparse_banded_eq(n=3001, p=1201, seed=2) if maker != "skewed" else _skewed()
+    if maker == "box":   # per-coordinate bounds (the uniform-box shortcut off), some infinite
+        rng = np.random.default_rng(4)
+        prob.lb = -rng.uniform(0.5, 1.5, prob.lb.shape)
+        prob.ub = rng.uniform(0.5, 1.5, prob.ub.shape)
+        prob.lb[::7] = -np.inf
+        prob.ub[3::11] = np.inf
+    rho = 2.0 if maker == "skewed" else 5.0
     L_in, L_d, _ = _consts_dense(prob, rho, 0.5)
     a = _gpu(prob, rho, alg, 6, 7, L_in, L_d, trace=True, torch=torch_cuda)
     info = a["solver"].solve(alg, 6, 7)
