@@ -210,7 +210,8 @@ typedef struct {
     double flops_pass_b;
     int32_t path;               /* duquad_path: which kernels ran the inner steps           */
     int32_t sparse_kernels;     /* CSR: pass A kind | pass B kind << 4, kind 0 = sub-warp CSR,
-                                   1 = SELL-32, 2 = thread-per-row CSR (options.sell_path)   */
+                                   1 = SELL-32, 2 = thread-per-row CSR (options.sell_path);
+                                   + 8: pass A reads the banded Q rows as diagonals (DIA)     */
 } duquad_result;
 
 /* Kernel path of a solve (duquad_result.path).  "pass A" / "pass B" in the report map to:

@@ -62,6 +62,8 @@ struct duquad_ctx {
     int gs_a = 4, gs_b = 4;
     SellStore sell_a, sell_b;   // SELL-32 copies of the two (options.sell_path; empty unless kind SPK_SELL)
     int kind_a = SPK_CSR, kind_b = SPK_CSR, u_a = 8, u_b = 8;   // SparseKind and load-round width per pass
+    DiaMat dia{};               // pass A's Q rows in DIA form (banded Q; SELL pass A only)
+    double *dia_val = nullptr;
     int box_uniform = 0;        // this context's lb / ub are constant vectors (lb_u, ub_u)
     double lb_u = 0.0, ub_u = 0.0;
     // batched storage (batch > 1): QP-major per-QP vectors, strides ld (n-vectors) / ldp (p-vectors)
@@ -186,6 +188,7 @@ void free_all(duquad_ctx *c) {
     if (c->b_va) cudaFree(c->b_va);
     sell_free(&c->sell_a);
     sell_free(&c->sell_b);
+    if (c->dia_val) cudaFree(c->dia_val);
     if (c->d_ops) cudaFree(c->d_ops);
     if (c->d_j) cudaFree(c->d_j);
     if (c->d_flag) cudaFree(c->d_flag);
@@ -289,6 +292,7 @@ PassAArgs make_a(duquad_ctx *c) {
     a.sp_kind = c->kind_a;
     a.sp_u = c->u_a;
     a.sell = sell_view(c->sell_a);
+    a.dia = c->dia;
     return a;
 }
 
@@ -869,6 +873,10 @@ duquad_status setup_csr(duquad_ctx *ctx, const duquad_problem *prob) {
         return st;
     // measurement overrides (scripts/sparse_sweep.py): kind / load-round width per pass
     auto env_int = [](const char *k, int d) { const char *v = getenv(k); return v ? atoi(v) : d; };
+    // banded Q (config 4: 11 diagonals): pass A reads the Q rows as diagonals -- no column indices,
+    // every load coalesced (8 instead of 12 bytes per nonzero); same per-row order (ascending columns)
+    if (ctx->kind_a == SPK_SELL && ctx->nloc > 0 && env_int("DUQUAD_DIA", 1))
+        CK(dia_build(ctx->a_rp, ctx->a_ci, ctx->a_va, ctx->nloc, ctx->r0, n, nq, 1.15, &ctx->dia, &ctx->dia_val, s));
     if (ctx->kind_a == SPK_ROWT || (ctx->kind_a == SPK_SELL && env_int("DUQUAD_SPK_A", 1) == SPK_ROWT)) {
         ctx->kind_a = SPK_ROWT;
         ctx->u_a = env_int("DUQUAD_LANE_UA", ctx->u_a == 4 ? 4 : 8) <= 4 ? 4 : 8;
@@ -2100,7 +2108,8 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
                     : ctx->rho0 ? DUQUAD_PATH_RHO0
                     : ctx->Btot > 1 ? DUQUAD_PATH_BATCHED
                     : ctx->format == DUQUAD_CSR ? DUQUAD_PATH_CSR : DUQUAD_PATH_TWO_PASS;
-        res->sparse_kernels = ctx->format == DUQUAD_CSR ? ctx->kind_a | (ctx->kind_b << 4) : 0;
+        res->sparse_kernels = ctx->format == DUQUAD_CSR ? (ctx->kind_a | (ctx->dia.nd > 0 ? 8 : 0)) | (ctx->kind_b << 4)
+                                                        : 0;
         res->outer_iters = K;
         res->inner_iters_total = (int64_t)nout * Kin;
         res->kernel_launches = 1 + (int64_t)nout * (2 * Kin + 1);

@@ -41,6 +41,18 @@ struct SellMat {
     int64_t nsl, nsl_q, nq, rows;
 };
 
+// Diagonal (DIA) view of the Q rows of pass A when Q is banded (config 4: 11 diagonals): value k of
+// local row i sits in val[k * ldv + i] for the diagonal at column offset off[k] (ascending = CSR
+// column order; 0 where the diagonal leaves the matrix).  No column indices, coalesced loads.
+constexpr int kDiaMax = 16;
+struct DiaMat {
+    const double *val;
+    int32_t nd;            // diagonals (0: Q rows are not in DIA form)
+    int32_t off[kDiaMax];
+    int64_t ldv;           // rows padded to a multiple of 32
+    int64_t r0, n;         // global index of local row 0, columns
+};
+
 // ---------------------------------------------------------------- pass A
 // Streams rows [row_begin, row_end) of the local stacked matrix A = [Q_r; G_r]
 // (row-major, leading dimension ld doubles, zero-padded) against y (full
@@ -78,6 +90,7 @@ struct PassAArgs {
     int32_t sp_kind;     // SparseKind: sub-warp CSR, SELL-32 or thread-per-row CSR
     int32_t sp_u;        // lane kernels: nonzeros per load round
     SellMat sell;
+    DiaMat dia;          // SELL pass A: the Q rows in DIA form (dia.nd > 0)
 };
 
 // ---------------------------------------------------------------- pass B
@@ -259,6 +272,11 @@ cudaError_t sparse_plan(const int32_t *rp, int64_t rows, int64_t nq, SparsePlan 
 cudaError_t sell_build(const int32_t *rp, const int32_t *ci, const double *va, int64_t rows, int64_t nq,
                        const SparsePlan &plan, SellStore *out, cudaStream_t s);
 void sell_free(SellStore *st);
+// DIA form of rows [0, rows) of a rebased CSR matrix (global row of local row i: r0 + i) when it has at
+// most kDiaMax distinct column offsets within [-64, 64] and the diagonals hold at most `max_pad` x its
+// nonzeros; *val = NULL (nothing allocated) otherwise
+cudaError_t dia_build(const int32_t *rp, const int32_t *ci, const double *va, int64_t rows, int64_t r0, int64_t n,
+                      int64_t nnz, double max_pad, DiaMat *out, double **val, cudaStream_t s);
 SellMat sell_view(const SellStore &st);
 int lane_unroll(int kind, int64_t max_width, double mean_len);
 int lane_blocks_per_sm(int pass, int kind, int u);

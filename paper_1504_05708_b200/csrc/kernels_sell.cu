@@ -42,6 +42,9 @@ constexpr int kLaneThreads = 256;
 #ifndef DQ_LANE_MINB   // minimum resident blocks per SM of the lane kernels (register cap)
 #define DQ_LANE_MINB 1
 #endif
+#ifndef DQ_SELLA_MINB  // SELL pass A: its solve-mode epilogue (the DFOM step) alone would take ~80
+#define DQ_SELLA_MINB 4 // registers (2-3 CTAs/SM); capped at 64 for 4 CTAs/SM
+#endif
 
 __device__ __forceinline__ uint64_t evict_first() {
     uint64_t pol;
@@ -131,8 +134,36 @@ __device__ __forceinline__ double rowt_dot(const int32_t *__restrict__ ci, const
     return acc;
 }
 
+// lane's row of the DIA Q block (local row i, global row gi): the diagonals in ascending column
+// order, rounds of U, no index loads (the y loads of a round are contiguous per diagonal)
+template <int U>
+__device__ __forceinline__ double dia_dot(const DiaMat &d, int64_t i, const double *__restrict__ v, uint64_t pol) {
+    const int64_t gi = d.r0 + i;
+    double acc = 0.0;
+    for (int k0 = 0; k0 < d.nd; k0 += U) {
+        double a[U], x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int k = k0 + u;
+            if (k < d.nd) {   // warp-uniform
+                int64_t c = gi + d.off[k];
+                c = c < 0 ? 0 : (c >= d.n ? d.n - 1 : c);   // outside the matrix: the stored value is 0
+                a[u] = ld_na_f64(d.val + (int64_t)k * d.ldv + i, pol);
+                x[u] = __ldg(v + c);
+            } else {
+                a[u] = 0.0;
+                x[u] = 0.0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (k0 + u < d.nd) acc = fma(a[u], x[u], acc);
+    }
+    return acc;
+}
+
 template <int MODE, int U>
-__global__ void __launch_bounds__(kLaneThreads, DQ_LANE_MINB) k_pass_a_sell(const PassAArgs a) {
+__global__ void __launch_bounds__(kLaneThreads, DQ_SELLA_MINB) k_pass_a_sell(const PassAArgs a) {
     pdl_wait();   // everything below reads iterates or writes (PDL, epilogue.cuh)
     pdl_trigger();
     if (a.skip && *a.skip) return;
@@ -151,7 +182,8 @@ __global__ void __launch_bounds__(kLaneThreads, DQ_LANE_MINB) k_pass_a_sell(cons
         const int w = (int)((m.sptr[s + 1] - base) >> 5);
         EpiA e{};
         if (r >= 0) e = epi_a_load(a, MODE, r, o);
-        const double acc = sell_dot<U>(m, base, w, lane, a.y, pol);
+        const double acc = (s < m.nsl_q && a.dia.nd > 0) ? dia_dot<U>(a.dia, s * 32 + lane, a.y, pol)
+                                                         : sell_dot<U>(m, base, w, lane, a.y, pol);
         if (r >= 0) epi_a_store(a, MODE, r, acc, e, o);
     }
 }
@@ -332,6 +364,88 @@ cudaError_t sell_build(const int32_t *rp, const int32_t *ci, const double *va, i
     }
     *out = st;
     return cudaSuccess;
+}
+
+// ------------------------------------------------------------------ DIA (banded Q rows)
+namespace {
+constexpr int kDiaWin = 64;   // column offsets considered: [-64, 64]
+__global__ void k_dia_hist(const int32_t *rp, const int32_t *ci, int64_t rows, int64_t r0, int32_t *hist,
+                           int32_t *bad) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    int32_t prev = -1;
+    for (int32_t e = rp[i]; e < rp[i + 1]; ++e) {
+        const int64_t off = (int64_t)ci[e] - (r0 + i);
+        if (off < -kDiaWin || off > kDiaWin || ci[e] == prev) {   // wide band or a duplicate column
+            *bad = 1;
+            return;
+        }
+        prev = ci[e];
+        atomicAdd(&hist[off + kDiaWin], 1);
+    }
+}
+__global__ void k_dia_fill(const int32_t *rp, const int32_t *ci, const double *va, int64_t rows, int64_t r0,
+                           const int32_t *slot, int64_t ldv, double *val) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    for (int32_t e = rp[i]; e < rp[i + 1]; ++e) val[(int64_t)slot[ci[e] - (r0 + i) + kDiaWin] * ldv + i] = va[e];
+}
+}  // namespace
+
+cudaError_t dia_build(const int32_t *rp, const int32_t *ci, const double *va, int64_t rows, int64_t r0, int64_t n,
+                      int64_t nnz, double max_pad, DiaMat *out, double **val, cudaStream_t s) {
+    *out = DiaMat{};
+    *val = nullptr;
+    if (rows <= 0 || nnz <= 0) return cudaSuccess;
+    int32_t *hist = nullptr, *slot = nullptr;
+    cudaError_t e = cudaMalloc(&hist, (2 * kDiaWin + 2) * sizeof(int32_t));
+    if (!e) e = cudaMalloc(&slot, (2 * kDiaWin + 1) * sizeof(int32_t));
+    if (!e) e = cudaMemsetAsync(hist, 0, (2 * kDiaWin + 2) * sizeof(int32_t), s);
+    int32_t h[2 * kDiaWin + 2];
+    if (!e) {
+        k_dia_hist<<<nblk(rows, 256), 256, 0, s>>>(rp, ci, rows, r0, hist, hist + 2 * kDiaWin + 1);
+        e = cudaMemcpyAsync(h, hist, sizeof(h), cudaMemcpyDeviceToHost, s);
+    }
+    if (!e) e = cudaStreamSynchronize(s);
+    DiaMat d{};
+    int32_t sl[2 * kDiaWin + 1];
+    bool ok = !e && h[2 * kDiaWin + 1] == 0;
+    if (ok) {
+        for (int o = 0; o <= 2 * kDiaWin; ++o) {
+            sl[o] = -1;
+            if (h[o] > 0) {
+                if (d.nd == kDiaMax) {
+                    ok = false;
+                    break;
+                }
+                sl[o] = d.nd;
+                d.off[d.nd++] = o - kDiaWin;
+            }
+        }
+    }
+    d.ldv = (rows + 31) / 32 * 32;
+    ok = ok && d.nd > 0 && (double)d.nd * (double)rows <= max_pad * (double)nnz;
+    if (ok) {
+        e = cudaMemcpyAsync(slot, sl, sizeof(sl), cudaMemcpyHostToDevice, s);
+        if (!e) e = cudaMalloc(val, (size_t)d.nd * d.ldv * sizeof(double));
+        if (!e) e = cudaMemsetAsync(*val, 0, (size_t)d.nd * d.ldv * sizeof(double), s);
+        if (!e) {
+            k_dia_fill<<<nblk(rows, 256), 256, 0, s>>>(rp, ci, va, rows, r0, slot, d.ldv, *val);
+            e = cudaGetLastError();
+        }
+        if (!e) e = cudaStreamSynchronize(s);
+        d.val = *val;
+        d.r0 = r0;
+        d.n = n;
+        if (!e) *out = d;
+    }
+    cudaFree(hist);
+    cudaFree(slot);
+    if (e && *val) {
+        cudaFree(*val);
+        *val = nullptr;
+    }
+    return e;
 }
 
 SellMat sell_view(const SellStore &st) {

@@ -221,7 +221,9 @@ def test_lane_kernels_vs_subwarp_kernels_and_oracle(torch_cuda, maker, kinds, al
     L_in, L_d, _ = _consts_dense(prob, rho, 0.5)
     a = _gpu(prob, rho, alg, 6, 7, L_in, L_d, trace=True, torch=torch_cuda)
     info = a["solver"].solve(alg, 6, 7)
-    assert info["path"] == 5 and info["sparse_kernels"] == kinds[0] | (kinds[1] << 4), info
+    sk = info["sparse_kernels"]
+    assert info["path"] == 5 and (sk & 3, (sk >> 4) & 3) == kinds, info
+    assert bool(sk & 8) == (maker != "skewed")       # banded Q rows read as diagonals (DIA)
     b = _gpu(prob, rho, alg, 6, 7, L_in, L_d, sell_path=False)
     assert b["solver"].solve(alg, 6, 7)["sparse_kernels"] == 0
     for k in ("x_last", "x_avg", "lam"):
