@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(kLaneThreads, DQ_LANE_MINB) k_pass_a_rowt(cons
 }
 
 template <int MODE, int U>
-__global__ void __launch_bounds__(kLaneThreads, 5) k_pass_b_rowt(const PassBArgs b) {
+__global__ void __launch_bounds__(kLaneThreads, DQ_LANE_MINB) k_pass_b_rowt(const PassBArgs b) {
     pdl_wait();
     pdl_trigger();
     if (b.skip && *b.skip) return;
@@ -241,27 +241,14 @@ __global__ void __launch_bounds__(kLaneThreads, 5) k_pass_b_rowt(const PassBArgs
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const double avg_w = avg_weight(b, MODE);
     const uint64_t pol = evict_first();
-    // row pointers one group ahead (the row-pointer -> index -> gather chain loses a link)
-    int32_t lo = 0, hi = 0;
-    if (warp * 32 + lane < b.nrows) {
-        lo = b.rp[warp * 32 + lane];
-        hi = b.rp[warp * 32 + lane + 1];
-    }
     for (int64_t base = warp * 32; base < b.nrows; base += nwarps * 32) {
         const int64_t j = base + lane;
         const bool v = j < b.nrows;
-        const int64_t jn = j + nwarps * 32;
-        int32_t lon = 0, hin = 0;
-        if (jn < b.nrows) {
-            lon = b.rp[jn];
-            hin = b.rp[jn + 1];
-        }
+        const int32_t lo = v ? b.rp[j] : 0, len = v ? b.rp[j + 1] - lo : 0;
         EpiB e{};
         if (v) e = epi_b_load(b, MODE, j, avg_w);
-        const double t = rowt_dot<U>(b.ci, b.va, lo, hi - lo, b.w, pol);
+        const double t = rowt_dot<U>(b.ci, b.va, lo, len, b.w, pol);
         if (v) epi_b_store(b, MODE, j, t, e, avg_w);
-        lo = lon;
-        hi = hin;
     }
 }
 
