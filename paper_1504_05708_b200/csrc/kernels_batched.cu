@@ -409,9 +409,12 @@ template <int ST, int SA, int SB, int C, bool TWO>
 __device__ __forceinline__ void block_b(MathCtx &x) {
     const int fr = x.lane >> 2, fk = x.lane & 3;
     double acc[2][C][2];
+    BTRACE(8 * (x.blk & 63) + 0, x.warp == 0);
     kloop<ST, SA, SB, C, TWO>(x, acc);
+    BTRACE(8 * (x.blk & 63) + 1, x.warp == 0);
     // park the C tile QP-major (fragment: row fr, cols 2fk, 2fk+1 of each 8x8 tile)
     mbar_wait(x.cs_empty, (x.blk & 1) ^ 1);
+    BTRACE(8 * (x.blk & 63) + 2, x.warp == 0);
 #pragma unroll
     for (int j = 0; j < C; ++j)
 #pragma unroll
@@ -555,7 +558,7 @@ __global__ void __launch_bounds__(Geo<PASS, NT, PAIR>::THREADS, 1) k_batched(con
                 for (int kc = 0; kc < nkc; ++kc, ++s) {
                     const int slot = (int)(s % ST);
                     mbar_wait(empty + slot, ((s / ST) & 1) ^ 1);
-                    BTRACE(8 * ((mb + k * nmb) & 63) + 6, PASS == 0 && kc == 0 && warp == kMathW);
+                    BTRACE(8 * ((mb + k * nmb) & 63) + 6, kc == 0 && warp == kMathW);
                     double *as = As + slot * GE::SA;
                     const double *ag = args.Aop + m0 * args.lda + (int64_t)kc * BK;
                     for (int i = pt; i < rows * (BK / 2); i += 32 * kProdW) {
@@ -623,7 +626,9 @@ __global__ void __launch_bounds__(Geo<PASS, NT, PAIR>::THREADS, 1) k_batched(con
             if (gr.nq == 0) continue;
             for (int mb = 0; mb < nmb; ++mb) {
                 mbar_wait(cs_full, blk & 1);
+                BTRACE(8 * (blk & 63) + 4, wid == 0);
                 epi_block_b(args, Cs, (int64_t)mb * kBlkM, gr, wid, GE::EPIW, lane, avg_w);
+                BTRACE(8 * (blk & 63) + 5, wid == 0);
                 mbar_arrive(cs_empty);
                 ++blk;
             }
@@ -652,17 +657,17 @@ cudaError_t launch_t(BatchedArgs a, cudaStream_t s) {
     const int64_t nctas = a.ncol8 < g_num_sms ? a.ncol8 : g_num_sms;
     k_batched<PASS, NT, PAIR><<<(unsigned)nctas, Geo<PASS, NT, PAIR>::THREADS, Geo<PASS, NT, PAIR>::SMEM, s>>>(a);
 #ifdef DUQUAD_BATCHED_TRACE
-    if (PASS == 0) {
+    {
         unsigned long long h[8 * 64];
         cudaStreamSynchronize(s);
         cudaMemcpyFromSymbol(h, g_btrace, sizeof h);
         const unsigned long long t0 = h[0];
         for (int b = 0; b < 8 && h[8 * b]; ++b) {
-            fprintf(stderr, "blk %d:", b);
+            fprintf(stderr, "pass %c blk %d:", PASS == 0 ? 'A' : 'B', b);
             for (int c = 0; c < 8; ++c) fprintf(stderr, " %7.2f", h[8 * b + c] ? (double)(h[8 * b + c] - t0) / 1e3 : -1.0);
             fprintf(stderr, "\n");
         }
-        cudaMemset(g_btrace, 0, 0);
+        cudaMemset(g_btrace, 0, sizeof h);
     }
 #endif
     return cudaGetLastError();
