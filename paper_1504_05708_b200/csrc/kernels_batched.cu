@@ -36,6 +36,7 @@
 #include <algorithm>
 #ifdef DUQUAD_BATCHED_TRACE
 #include <cstdio>
+#include <cstring>
 #endif
 
 #include "duquad_internal.h"
@@ -667,7 +668,8 @@ cudaError_t launch_t(BatchedArgs a, cudaStream_t s) {
             for (int c = 0; c < 8; ++c) fprintf(stderr, " %7.2f", h[8 * b + c] ? (double)(h[8 * b + c] - t0) / 1e3 : -1.0);
             fprintf(stderr, "\n");
         }
-        cudaMemset(g_btrace, 0, sizeof h);
+        memset(h, 0, sizeof h);
+        cudaMemcpyToSymbol(g_btrace, h, sizeof h);
     }
 #endif
     return cudaGetLastError();
