@@ -468,59 +468,45 @@ __device__ __forceinline__ void epi_block_b(const BatchedArgs &args, const doubl
         ubv[t] = jj[t] >= 0 ? B.ub[j] : 0.0;
     }
     bool bad = false;
-    // two columns (QPs) per trip: both columns' operands are loaded before either is computed, so a
-    // warp keeps 2 x 5 x RPL loads in flight (the epilogue is latency-bound)
-    constexpr int CP = 2;
-    for (int col0 = wid; col0 < gr.nq; col0 += CP * nwk) {
-        double vq[CP][RPL], vqy[CP][RPL], vx[CP][RPL], vy[CP][RPL], vh[CP][RPL];
-        bool on[CP];
+    for (int col = wid; col < gr.nq; col += nwk) {
+        if (args.done_b && args.done_b[gr.q0 + col]) continue;   // eps_in mode: this QP's inner solve stopped
+        const int64_t off = (gr.q0 + col) * args.sn;
+        const double *qyp = B.qy + off, *qp = B.q + off;
+        double *xp = B.x + off, *yp = B.y + off, *hp = B.xhat + off;
+        const double *cs = Cs + col * LDC + lane;
+        double vq[RPL], vqy[RPL], vx[RPL], vy[RPL], vh[RPL];
 #pragma unroll
-        for (int c = 0; c < CP; ++c) {
-            const int col = col0 + c * nwk;
-            // eps_in mode: a QP whose inner solve stopped is left alone
-            on[c] = col < gr.nq && !(args.done_b && args.done_b[gr.q0 + col]);
-            const int64_t off = (gr.q0 + (on[c] ? col : 0)) * args.sn;
-#pragma unroll
-            for (int t = 0; t < RPL; ++t)
-                if (on[c] && jj[t] >= 0) {
-                    vqy[c][t] = B.qy[off + jj[t]];
-                    vq[c][t] = B.q[off + jj[t]];
-                    vx[c][t] = B.x[off + jj[t]];
-                    vy[c][t] = B.y[off + jj[t]];
-                    vh[c][t] = avg_w != 0.0 ? B.xhat[off + jj[t]] : 0.0;
-                }
-        }
-#pragma unroll
-        for (int c = 0; c < CP; ++c) {
-            if (!on[c]) continue;
-            const int col = col0 + c * nwk;
-            const int64_t off = (gr.q0 + col) * args.sn;
-            double *xp = B.x + off, *yp = B.y + off, *hp = B.xhat + off;
-            const double *cs = Cs + col * LDC + lane;
-#pragma unroll
-            for (int t = 0; t < RPL; ++t)
-                if (jj[t] >= 0) {
-                    const double grad = (vqy[c][t] + vq[c][t]) + cs[32 * t];
-                    const double xn = fmin(fmax(vy[c][t] - grad / L, lbv[t]), ubv[t]);
-                    const double yn = last ? xn : xn + beta * (xn - vx[c][t]);
-                    if (avg_w != 0.0) hp[jj[t]] = vh[c][t] + avg_w * (xn - vh[c][t]);
-                    xp[jj[t]] = xn;
-                    yp[jj[t]] = yn;
-                    bad |= !isfinite(xn) || !isfinite(yn);
-                    if (args.gm_b) {   // eps_in mode: (y - x+)^2, this column's rows
-                        const double dd = vy[c][t] - xn;
-                        vh[c][t] = dd * dd;
-                    }
-                } else {
-                    vh[c][t] = 0.0;
-                }
-            if (args.gm_b) {   // the QP's sum: rows in lane order, blocks in order (one warp per column)
-                double gsum = 0.0;
-#pragma unroll
-                for (int t = 0; t < RPL; ++t) gsum += vh[c][t];
-                gsum = warp_sum(gsum);
-                if (lane == 0) atomicAdd(&args.gm_b[gr.q0 + col], gsum);
+        for (int t = 0; t < RPL; ++t)
+            if (jj[t] >= 0) {
+                vqy[t] = qyp[jj[t]];
+                vq[t] = qp[jj[t]];
+                vx[t] = xp[jj[t]];
+                vy[t] = yp[jj[t]];
+                vh[t] = avg_w != 0.0 ? hp[jj[t]] : 0.0;
             }
+#pragma unroll
+        for (int t = 0; t < RPL; ++t)
+            if (jj[t] >= 0) {
+                const double grad = (vqy[t] + vq[t]) + cs[32 * t];
+                const double xn = fmin(fmax(vy[t] - grad / L, lbv[t]), ubv[t]);
+                const double yn = last ? xn : xn + beta * (xn - vx[t]);
+                if (avg_w != 0.0) hp[jj[t]] = vh[t] + avg_w * (xn - vh[t]);
+                xp[jj[t]] = xn;
+                yp[jj[t]] = yn;
+                bad |= !isfinite(xn) || !isfinite(yn);
+                if (args.gm_b) {   // eps_in mode: (y - x+)^2, this column's rows
+                    const double dd = vy[t] - xn;
+                    vh[t] = dd * dd;
+                }
+            } else {
+                vh[t] = 0.0;
+            }
+        if (args.gm_b) {   // the QP's sum: rows in lane order, blocks in order (one warp per column)
+            double gsum = 0.0;
+#pragma unroll
+            for (int t = 0; t < RPL; ++t) gsum += vh[t];
+            gsum = warp_sum(gsum);
+            if (lane == 0) atomicAdd(&args.gm_b[gr.q0 + col], gsum);
         }
     }
     if (bad) *B.flag = 1;
