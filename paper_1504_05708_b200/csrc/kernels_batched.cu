@@ -341,40 +341,47 @@ __device__ __forceinline__ void block_a(MathCtx &x, const BatchedArgs &args, con
     mbar_wait(x.cs_full, x.blk & 1);   // the h tile of this block
     BTRACE(8 * (x.blk & 63) + 3, x.warp == 0);
     if (!o.dual) {
-        // Results straight from the accumulators to global memory in fragment order: for each
-        // (i, j, h) the lanes with the same fk write 8 consecutive rows of QP 8 j + 2 fk + h -- four
-        // 64-byte runs per instruction, the coalescing of a staged write-out without its shared-memory
-        // round trip.  Q rows: qy; G rows: w = [h + rho s]_{K°} (h from the staged tile).  Paired rows:
-        // the tiles hold h of the top and of the bottom row; d = w_top - w_bottom, the bottom row's
-        // product being -s (exactly the unpaired one)
-        const double *hs = x.Cs + (2 * fk) * LDC + 8 * x.warp + fr;
+        // (1) results in place in the tile: Hs[qp][r] := qy (Q row) or w (G row); immediate offsets.
+        // Paired rows: the tiles hold h of the top and of the bottom row; d = w_top - w_bottom, the
+        // bottom row's product being -s (exactly the unpaired one)
+        double *hs = x.Cs + (2 * fk) * LDC + 8 * x.warp + fr;
         const double *hs2 = x.Cs2 + (2 * fk) * LDC + 8 * x.warp + fr;
 #pragma unroll
         for (int i = 0; i < NI; ++i) {
-            if (kr[i] == -2) continue;   // beyond M
             const bool q_row = kr[i] == -1;
-            const int64_t ld = q_row ? args.sn : args.sw;
-            double *dst = (q_row ? A.qy + row[i] : A.w + kr[i]) + (gr.q0 + 2 * fk) * ld;
 #pragma unroll
             for (int j = 0; j < C; ++j)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    if (8 * j + 2 * fk + h >= gr.nq) continue;   // ragged last octet
+                    double *e = hs + (8 * j + h) * LDC + 64 * i;
                     const double sv = acc[i][j][h];
-                    const double ht = hs[(8 * j + h) * LDC + 64 * i];
-                    double v;
                     if (PAIR) {
                         const double hb = hs2[(8 * j + h) * LDC + 64 * i];
-                        const double wt = rho > 0.0 ? proj_polar(ht + rho * sv, cn[i]) : ht;
+                        const double wt = rho > 0.0 ? proj_polar(*e + rho * sv, cn[i]) : *e;
                         const double wb = rho > 0.0 ? proj_polar(hb + rho * (-sv), cb[i]) : hb;
-                        v = q_row ? sv : wt - wb;
+                        *e = q_row ? sv : wt - wb;
                     } else {
-                        v = q_row ? sv : rho > 0.0 ? proj_polar(ht + rho * sv, cn[i]) : ht;
+                        *e = q_row ? sv : rho > 0.0 ? proj_polar(*e + rho * sv, cn[i]) : *e;
                     }
-                    dst[(int64_t)(8 * j + h) * ld] = v;
                 }
         }
+        __syncwarp();
         BTRACE(8 * (x.blk & 63) + 7, x.warp == 0);
+        // (2) the warp's rows to global: lane -> (QP it * 4 + lane / 8, row lane % 8), 64-byte runs
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+            const int rl = 8 * (x.warp + 8 * i) + (x.lane & 7);   // block row of this lane
+            const int64_t r = m0 + rl;
+            if (r < args.M) {
+                const bool q_row = r < A.nq;
+                const int64_t ld = q_row ? args.sn : args.sw;
+                double *dst = (q_row ? A.qy + r : A.w + (r - A.nq)) + (gr.q0 + (x.lane >> 3)) * ld;
+                const double *src = x.Cs + (x.lane >> 3) * LDC + rl;
+                const int64_t step = 4 * ld;
+#pragma unroll 4
+                for (int qp = x.lane >> 3; qp < gr.nq; qp += 4, dst += step, src += 4 * LDC) *dst = *src;
+            }
+        }
     } else {   // the DFOM step (first inner step of an outer iteration), epilogue.cuh's dfom_row
         // park the accumulators in the (unused) h tile first, so they are not live across the loads
 #pragma unroll
