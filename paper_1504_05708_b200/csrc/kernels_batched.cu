@@ -100,6 +100,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity) {
 
 #ifdef DUQUAD_BATCHED_TRACE   // instrumentation build only: per-block timeline of CTA 0
 __device__ unsigned long long g_btrace[8 * 64];
+__device__ unsigned long long g_ctatrace[2 * 256];   // per CTA: start, end (globaltimer)
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 #define BTRACE(slot, cond)                                                             \
     do {                                                                               \
         if ((cond) && blockIdx.x == 0 && (threadIdx.x & 31) == 0) {                    \
@@ -526,6 +532,9 @@ __global__ void __launch_bounds__(Geo<PASS, NT, PAIR>::THREADS, 1) k_batched(con
     uint64_t *bars = reinterpret_cast<uint64_t *>(Cs + GE::NCS * GE::CS);
     uint64_t *full = bars, *empty = bars + ST, *cs_full = bars + 2 * ST, *cs_empty = cs_full + 1;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#ifdef DUQUAD_BATCHED_TRACE
+    if (tid == 0 && blockIdx.x < 256) g_ctatrace[2 * blockIdx.x] = gtimer();
+#endif
     if (tid == 0) {
         for (int s = 0; s < ST; ++s) {
             mbar_init(full + s, kProdW * 32);
@@ -635,6 +644,10 @@ __global__ void __launch_bounds__(Geo<PASS, NT, PAIR>::THREADS, 1) k_batched(con
             }
         }
     }
+#ifdef DUQUAD_BATCHED_TRACE
+    __syncthreads();
+    if (tid == 0 && blockIdx.x < 256) g_ctatrace[2 * blockIdx.x + 1] = gtimer();
+#endif
 }
 
 // Pass A reuses each (128 x 32) A chunk over 7 octets (56 QPs); pass B (one row block for
@@ -670,6 +683,17 @@ cudaError_t launch_t(BatchedArgs a, cudaStream_t s) {
         }
         memset(h, 0, sizeof h);
         cudaMemcpyToSymbol(g_btrace, h, sizeof h);
+        unsigned long long c[2 * 256];
+        cudaMemcpyFromSymbol(c, g_ctatrace, sizeof c);
+        unsigned long long s0 = ~0ull, s1 = 0, e0 = ~0ull, e1 = 0;
+        for (int b = 0; b < (int)nctas && b < 256; ++b) {
+            s0 = c[2 * b] < s0 ? c[2 * b] : s0;
+            s1 = c[2 * b] > s1 ? c[2 * b] : s1;
+            e0 = c[2 * b + 1] < e0 ? c[2 * b + 1] : e0;
+            e1 = c[2 * b + 1] > e1 ? c[2 * b + 1] : e1;
+        }
+        fprintf(stderr, "pass %c CTAs: start %.2f..%.2f us, end %.2f..%.2f us (from the first start; CTA 0 ends %.2f)\n",
+                PASS == 0 ? 'A' : 'B', 0.0, (s1 - s0) / 1e3, (e0 - s0) / 1e3, (e1 - s0) / 1e3, (c[1] - s0) / 1e3);
     }
 #endif
     return cudaGetLastError();
