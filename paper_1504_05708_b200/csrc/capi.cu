@@ -568,6 +568,7 @@ BatchedArgs make_batched(duquad_ctx *c, int pass) {
     ba.sp = std::max<int64_t>(c->ldp, 2);
     ba.N = c->Bloc;
     ba.pairP = c->pairP;
+    ba.pdl = c->cfg_a.pdl;
     ba.sw = c->pairP ? c->ldd : ba.sp;
     ba.a.qy = c->QYb;
     ba.a.w = c->pairP ? c->Db : c->Wb;

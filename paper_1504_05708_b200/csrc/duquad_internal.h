@@ -142,6 +142,7 @@ struct BatchedArgs {
     int64_t pairP;       // > 0: G = [G_t; -G_t] with P = p/2 paired rows; pass A streams [Q; G_t] and
                          // writes d = w_top - w_bottom (a.w, stride sw), pass B multiplies G_t' d
     int64_t ncol8;       // QP octets (set by launch_batched)
+    int32_t pdl;         // launch with programmatic dependent launch (epilogue.cuh pdl_wait)
     // eps_in mode (else null): per-QP stop-test sums, stop flags, number of stopped QPs
     double *gm_b;
     int32_t *done_b;

@@ -522,7 +522,6 @@ __device__ __forceinline__ void epi_block_b(const BatchedArgs &args, const doubl
 template <int PASS, int NT, bool PAIR>
 __global__ void __launch_bounds__(Geo<PASS, NT, PAIR>::THREADS, 1) k_batched(const BatchedArgs args) {
     using GE = Geo<PASS, NT, PAIR>;
-    if (args.ndone && *args.ndone >= args.N) return;   // eps_in mode: every QP's inner solve has stopped
     constexpr int ST = GE::STAGES;
     extern __shared__ __align__(16) double smem[];
     double *As = smem;
@@ -547,6 +546,34 @@ __global__ void __launch_bounds__(Geo<PASS, NT, PAIR>::THREADS, 1) k_batched(con
     __syncthreads();
     const int nmb = (int)((args.M + kBlkM - 1) / kBlkM), nkc = (int)(args.K / BK);
     const Range rg = cta_range<NT>(args);
+    // the producers' A operand (the shared matrix: never written by a solve) of the first ST ring
+    // chunks, before the PDL dependency wait (epilogue.cuh): the ring fill overlaps the previous
+    // kernel's tail; the B operand (the iterates) and everything else come after it
+    const bool producer = warp >= kMathW && warp < kMathW + kProdW;
+    const int pt = tid - 32 * kMathW;
+    auto issue_a = [&](int64_t m0, int kc, int slot) {
+        const int rows = (int)(args.M - m0 < kBlkM ? args.M - m0 : kBlkM);
+        double *as = As + slot * GE::SA;
+        const double *ag = args.Aop + m0 * args.lda + (int64_t)kc * BK;
+        for (int i = pt; i < rows * (BK / 2); i += 32 * kProdW) {
+            const int r = i / (BK / 2), c = (i % (BK / 2)) * 2;
+            cp16(as + r * PADK + c, ag + r * args.lda + c);
+        }
+    };
+    uint32_t pre = 0;   // chunks whose A part is in flight already
+    if (producer) {
+        for (int k = 0; k < rg.ng && pre < (uint32_t)ST; ++k) {
+            if (group_of(args, rg, k).nq == 0) continue;
+            for (int mb = 0; mb < nmb && pre < (uint32_t)ST; ++mb)
+                for (int kc = 0; kc < nkc && pre < (uint32_t)ST; ++kc, ++pre) issue_a((int64_t)mb * kBlkM, kc, (int)pre);
+        }
+    }
+    pdl_wait();
+    pdl_trigger();
+    if (args.ndone && *args.ndone >= args.N) {   // eps_in mode: every QP's inner solve has stopped
+        if (producer) asm volatile("cp.async.wait_all;" ::: "memory");
+        return;
+    }
     const OuterA o = PASS == 0 ? outer_a(args.a, MODE_SOLVE) : OuterA{0, 0.0};
 
     if (warp < kMathW) {   // ------------------------------------------------ math warps
@@ -556,25 +583,18 @@ __global__ void __launch_bounds__(Geo<PASS, NT, PAIR>::THREADS, 1) k_batched(con
             if (gr.nq == 0) continue;
             for (int mb = 0; mb < nmb; ++mb) block_sel<PASS, NT, PAIR, NT>(x, args, gr, (int64_t)mb * kBlkM, o);
         }
-    } else if (warp < kMathW + kProdW) {   // ----------------------------------- producer warps
-        const int pt = tid - 32 * kMathW;
+    } else if (producer) {   // ------------------------------------------------------ producer warps
         uint32_t s = 0;
         for (int k = 0; k < rg.ng; ++k) {
             const Group gr = group_of(args, rg, k);
             if (gr.nq == 0) continue;
             for (int mb = 0; mb < nmb; ++mb) {
                 const int64_t m0 = (int64_t)mb * kBlkM;
-                const int rows = (int)(args.M - m0 < kBlkM ? args.M - m0 : kBlkM);
                 for (int kc = 0; kc < nkc; ++kc, ++s) {
                     const int slot = (int)(s % ST);
                     mbar_wait(empty + slot, ((s / ST) & 1) ^ 1);
                     BTRACE(8 * ((mb + k * nmb) & 63) + 6, kc == 0 && warp == kMathW);
-                    double *as = As + slot * GE::SA;
-                    const double *ag = args.Aop + m0 * args.lda + (int64_t)kc * BK;
-                    for (int i = pt; i < rows * (BK / 2); i += 32 * kProdW) {
-                        const int r = i / (BK / 2), c = (i % (BK / 2)) * 2;
-                        cp16(as + r * PADK + c, ag + r * args.lda + c);
-                    }
+                    if (s >= pre) issue_a(m0, kc, slot);
                     double *bs = Bs + slot * GE::SB;
                     const double *bg = args.Bop + gr.q0 * args.ldb + (int64_t)kc * BK;
                     for (int i = pt; i < gr.nq * (BK / 2); i += 32 * kProdW) {
@@ -669,7 +689,9 @@ cudaError_t launch_t(BatchedArgs a, cudaStream_t s) {
     }
     a.ncol8 = (a.N + 7) / 8;
     const int64_t nctas = a.ncol8 < g_num_sms ? a.ncol8 : g_num_sms;
-    k_batched<PASS, NT, PAIR><<<(unsigned)nctas, Geo<PASS, NT, PAIR>::THREADS, Geo<PASS, NT, PAIR>::SMEM, s>>>(a);
+    cudaError_t e = launch_ex(k_batched<PASS, NT, PAIR>, (unsigned)nctas, Geo<PASS, NT, PAIR>::THREADS,
+                              Geo<PASS, NT, PAIR>::SMEM, s, a.pdl, 0, a);
+    if (e) return e;
 #ifdef DUQUAD_BATCHED_TRACE
     {
         unsigned long long h[8 * 64];
