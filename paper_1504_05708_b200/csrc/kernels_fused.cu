@@ -157,9 +157,8 @@ __device__ __forceinline__ Tile tile_of(const FusedArgs &f, int J) {
 // Launched with a cluster dimension of 2 when there is a G role (pairs), 1 otherwise.
 template <int NCHG>
 __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f) {
-    pdl_wait();   // PDL (epilogue.cuh): only the launch overlaps the previous kernel
-    pdl_trigger();
-    if (f.a.skip && *f.a.skip) return;   // eps_in mode: converged (uniform over the grid)
+    // PDL (epilogue.cuh): the Q role fills its ring with Q rows (never written by a solve) before
+    // pdl_wait(); every other read and write of both roles comes after it
     constexpr int kSlotsG = kSlots - (NCHG > 0 ? NCHG : 1);
     extern __shared__ __align__(128) uint8_t fsm[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -179,6 +178,11 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
     __syncthreads();
     cluster_sync_all();
 
+    if (!(NCHG == 0 || cta < f.nq_ctas)) {
+        pdl_wait();
+        pdl_trigger();
+        if (f.a.skip && *f.a.skip) return;   // eps_in mode: converged (uniform over the grid)
+    }
     if (NCHG == 0 || cta < f.nq_ctas) {
         // ================================ Q role: triangle row steps (J, r) of this piece
         const FusedPiece pc = f.pieces[cta];
@@ -220,7 +224,13 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
             cp_commit();
             if (++ps == kSlots) ps = 0;
         };
-        for (int t = 0; t < kSlots; ++t) issue();
+        for (int t = 0; t < kSlots; ++t) issue();   // Q rows: matrix data, before the dependency wait
+        pdl_wait();
+        pdl_trigger();
+        if (f.a.skip && *f.a.skip) {   // eps_in mode: converged (uniform over the grid)
+            cp_wait<0>();
+            return;
+        }
         int cs = 0;
         auto load_q = [&](double *q) {
 #pragma unroll
