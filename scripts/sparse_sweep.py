@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Config 4 (CSR, n = 1e6) pass timings for the sparse kernel variants (env overrides read at
 setup: DUQUAD_SPK_A = 1 SELL / 2 thread-per-row for pass A, DUQUAD_LANE_UA / _UB = load-round
-width).  One JSON line per variant: us per inner step and per pass (CUDA events)."""
+width, DUQUAD_PDL = 2 forces programmatic dependent launch, DUQUAD_DIA = 0 keeps banded Q rows in
+SELL).  One JSON line per variant: us per inner step and per pass (CUDA events)."""
 import json
 import os
 import sys
@@ -16,11 +17,10 @@ def main():
     from paper_1504_05708_b200 import Solver
     prob = qpgen.sparse_banded_eq()
     stream = torch.cuda.Stream()
-    variants = [dict(), dict(DUQUAD_LANE_UA="8"), dict(DUQUAD_LANE_UA="16"), dict(DUQUAD_LANE_UA="4"),
-                dict(DUQUAD_SPK_A="2", DUQUAD_LANE_UA="4"), dict(DUQUAD_SPK_A="2", DUQUAD_LANE_UA="8"),
-                dict(DUQUAD_LANE_UB="8"), dict(sell=False)]
+    variants = [dict(), dict(DUQUAD_LANE_UA="8"), dict(DUQUAD_PDL="2"), dict(DUQUAD_DIA="0"), dict(),
+                dict(sell=False)]
     for v in variants:
-        for k in ("DUQUAD_SPK_A", "DUQUAD_LANE_UA", "DUQUAD_LANE_UB"):
+        for k in ("DUQUAD_SPK_A", "DUQUAD_LANE_UA", "DUQUAD_LANE_UB", "DUQUAD_PDL", "DUQUAD_DIA"):
             os.environ.pop(k, None)
         for k, x in v.items():
             if k.startswith("DUQUAD"):
