@@ -485,23 +485,15 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
             auto post = [&](int it, double part) {
                 part = warp_sum(part);
                 const int d = it % kD;
-#ifndef DQ_EXP_NOXCHG   // timing experiment only (wrong results): no pair exchange at all
                 if (lane < 2)   // lane c -> CTA c of the pair
                     st_async_f64(xb_r + (uint32_t)(d * 32 + (int)rank * kWarps + warp) * 8, part,
                                  xm_r + (uint32_t)d * 8);
                 if (warp == 0 && lane == 0) mbar_arrive_expect_tx(&xbar[d], 2u * kWarps * 8u);
-#else
-                if (part == 12345.678) xbuf[d] = part;   // keep the reduction alive
-#endif
             };
             auto row_w = [&](int it) -> double {
                 const int d = it % kD;
-#ifndef DQ_EXP_NOXCHG
                 mbar_wait(&xbar[d], (uint32_t)((it / kD) & 1));
                 double s_row = xbuf[d * 32 + lane];
-#else
-                double s_row = 0.0 * (double)d;
-#endif
                 s_row += __shfl_xor_sync(0xffffffffu, s_row, 16);
                 s_row += __shfl_xor_sync(0xffffffffu, s_row, 8);
                 s_row += __shfl_xor_sync(0xffffffffu, s_row, 4);
