@@ -363,3 +363,33 @@ def test_persistent_solve_is_bitwise_the_multi_launch_path(torch_cuda, n, p, kin
         assert np.array_equal(a[k], b[k]), k
     r = run_oracle(prob, rho, O.DFGM if alg == "DFGM" else O.DGM, 7, 9, L_in, L_d)
     assert_parity(a, r)
+
+
+@pytest.mark.parametrize("kind", ["two_pass", "byte_floor", "rho0", "batched"])
+def test_pdl_launch_does_not_change_results(torch_cuda, kind):
+    """Programmatic dependent launch (options.pdl) only overlaps a kernel's launch and matrix
+    prefetch with its predecessor; every read of an iterate happens after the dependency wait, so
+    the iterates are bitwise those of plain launches (graph-captured, several outer iterations)."""
+    from paper_1504_05708_b200 import Solver
+    if kind == "batched":
+        prob = qpgen.mpc_batch(300, seed=3, N=12)
+        args = (prob.Q, prob.q.T.copy(), prob.G, prob.g.T.copy(), prob.lb, prob.ub, prob.cone)
+        kw, rho = {}, 1.0
+    else:
+        n, p = (4096, 700) if kind == "byte_floor" else (900, 400)
+        prob = qpgen.tiny(n, p, seed=17, kind="mixed", shift=0.2)
+        args = (prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone)
+        kw = dict(small_path=False, fused_path=kind == "byte_floor")
+        rho = 0.0 if kind == "rho0" else 1.0
+    L_in, L_d, _ = O.lipschitz_constants(prob.Q, prob.G, rho, 0.2 if kind != "batched" else 0.1)
+    outs = []
+    for pdl in (True, False):
+        s = Solver(*args, rho=rho, pdl=pdl, **kw)
+        s.set_constants(L_in, L_d)
+        info = s.solve("DFGM", 5, 6)
+        outs.append(s.result())
+        s.close()
+    want = {"two_pass": 0, "byte_floor": 1, "rho0": 2, "batched": 4}[kind]
+    assert info["path"] == want, info["path"]
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
