@@ -460,14 +460,16 @@ SellMat sell_view(const SellStore &st) {
     return m;
 }
 
-// Load-round width.  Measured on config 4 (scripts/sparse_sweep.py, profiles/r02_sparse_sweep.jsonl):
-// SELL pass A (slices of width 11 / 8) 50.3 us at U = 4, 52.0 at 8, 60.7 at 12, 62.1 at 16 -- the
-// kernel is bound by memory-level parallelism, and fewer registers per lane (more resident warps)
-// beat fewer rounds per slice; thread-per-row pass B 31.9 us at U = 4, 32.3 at 8.
+// Load-round width: 4 for both kinds, whatever the row lengths.  Measured on config 4
+// (scripts/sparse_sweep.py, profiles/r02_sparse_sweep*.jsonl): SELL pass A (slices of width 11 / 8)
+// 50.3 us at U = 4, 52.0 at 8, 60.7 at 12, 62.1 at 16 (with DIA for the Q rows: 45.6 at 4, 46.7 at
+// 8) -- the kernel is bound by memory-level parallelism, and fewer registers per lane (more
+// resident warps) beat fewer rounds per slice; thread-per-row pass B 31.9 us at U = 4, 32.3 at 8.
 int lane_unroll(int kind, int64_t max_width, double mean_len) {
+    (void)kind;
     (void)max_width;
     (void)mean_len;
-    return kind == SPK_SELL ? 4 : 4;
+    return 4;
 }
 
 #define DQ_LANE_DISPATCH(KERN, MODE, U, GRID, ARG)                                         \
