@@ -239,6 +239,10 @@ typedef enum {
 } duquad_path;
 
 int32_t duquad_abi_version(void);
+/* sizeof of the ABI structs, for bindings to check their mirrors: which = 0 duquad_problem,
+ * 1 duquad_options, 2 duquad_result, 3 duquad_schedule, 4 duquad_bounds, 5 duquad_monitor;
+ * -1 for an unknown `which`.  Host only. */
+int64_t duquad_struct_size(int32_t which);
 const char *duquad_status_string(int32_t status);
 void duquad_default_options(duquad_options *opts);
 

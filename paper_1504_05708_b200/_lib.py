@@ -95,6 +95,7 @@ PATHS = {0: "two_pass", 1: "byte_floor", 2: "rho0", 3: "rho0_floor", 4: "batched
 
 _SIGS = {
     "duquad_abi_version": (C.c_int32, []),
+    "duquad_struct_size": (C.c_int64, [C.c_int32]),
     "duquad_status_string": (C.c_char_p, [C.c_int32]),
     "duquad_default_options": (None, [C.POINTER(Options)]),
     "duquad_shard_range": (C.c_int, [C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),

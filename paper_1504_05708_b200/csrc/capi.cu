@@ -895,6 +895,18 @@ extern "C" {
 
 int32_t duquad_abi_version(void) { return DUQUAD_ABI_VERSION; }
 
+int64_t duquad_struct_size(int32_t which) {
+    switch (which) {
+        case 0: return (int64_t)sizeof(duquad_problem);
+        case 1: return (int64_t)sizeof(duquad_options);
+        case 2: return (int64_t)sizeof(duquad_result);
+        case 3: return (int64_t)sizeof(duquad_schedule);
+        case 4: return (int64_t)sizeof(duquad_bounds);
+        case 5: return (int64_t)sizeof(duquad_monitor);
+        default: return -1;
+    }
+}
+
 const char *duquad_status_string(int32_t s) {
     switch (s) {
         case DUQUAD_OK: return "ok";

@@ -43,6 +43,16 @@ def test_default_options(lib):
     o = _lib.Options()
     lib.duquad_default_options(C.byref(o))
     assert o.dual_step_scale == 0.5 and o.project_dual == 1 and o.world_size == 1 and o.use_graphs == 1
+    assert o.sell_path == 1 and o.pair_rows == 1 and o.pdl == 1 and o.fused_path == 1 and o.nccl_self == 0
+
+
+def test_ctypes_mirrors_match_the_abi_structs(lib):
+    """Every ctypes mirror of an ABI struct has the C struct's size (a field added on one side only
+    would shift every later field)."""
+    from paper_1504_05708_b200 import _lib
+    for which, cls in enumerate((_lib.Problem, _lib.Options, _lib.Result, _lib.Schedule, _lib.Bounds, _lib.Monitor)):
+        assert lib.duquad_struct_size(which) == C.sizeof(cls), cls.__name__
+    assert lib.duquad_struct_size(99) == -1
 
 
 @pytest.mark.parametrize("rows,world", [(16384, 8), (10, 3), (5, 8), (0, 2), (2000, 1)])
