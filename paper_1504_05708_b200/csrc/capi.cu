@@ -2156,7 +2156,6 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
             res->bytes_pass_a = 8.0 * ((nn + pp) * nn + B * (nn + nn + 3.0 * pp));
             res->bytes_pass_b = 8.0 * (nn * pp + B * (pp + 8.0 * nn));
         } else if (ctx->format == DUQUAD_CSR) {   // values + indices + row pointers + vectors
-            if (ctx->dia.nd > 0) res->kernel_launches += (int64_t)nout * Kin;   // pass A: DIA + SELL launches
             res->bytes_pass_a = 12.0 * ctx->nnz_a + 4.0 * (nl + pl + 1) + 8.0 * (nn + nl + 3.0 * pl);
             res->bytes_pass_b = 12.0 * ctx->nnz_b + 4.0 * (nl + 1) + 8.0 * (pp + 8.0 * nl);
         } else {

@@ -134,40 +134,32 @@ __device__ __forceinline__ double rowt_dot(const int32_t *__restrict__ ci, const
     return acc;
 }
 
-// Pass A over the DIA Q block (its own launch, so the diagonal stream keeps all of a row's loads
-// in flight without the SELL kernel's register cap): thread per row, every diagonal's value and
-// its y entry loaded in one round (UD >= the diagonal count), summed in ascending column order
-// (the CSR order of the row); Q rows only store qy.
-template <int MODE, int UD>
-__global__ void __launch_bounds__(kLaneThreads) k_pass_a_dia(const PassAArgs a) {
-    pdl_wait();   // everything below reads iterates or writes (PDL, epilogue.cuh)
-    pdl_trigger();
-    if (a.skip && *a.skip) return;
-    const DiaMat &d = a.dia;
-    const int64_t r_hi = a.row_end < a.nq ? a.row_end : a.nq;
-    const uint64_t pol = evict_first();
-    for (int64_t i = a.row_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r_hi;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t gi = d.r0 + i;
-        double v[UD], x[UD];
+// lane's row of the DIA Q block (local row i, global row gi): the diagonals in ascending column
+// order, rounds of U, no index loads (the y loads of a round are contiguous per diagonal)
+template <int U>
+__device__ __forceinline__ double dia_dot(const DiaMat &d, int64_t i, const double *__restrict__ v, uint64_t pol) {
+    const int64_t gi = d.r0 + i;
+    double acc = 0.0;
+    for (int k0 = 0; k0 < d.nd; k0 += U) {
+        double a[U], x[U];
 #pragma unroll
-        for (int k = 0; k < UD; ++k) {
-            if (k < d.nd) {   // uniform
+        for (int u = 0; u < U; ++u) {
+            const int k = k0 + u;
+            if (k < d.nd) {   // warp-uniform
                 int64_t c = gi + d.off[k];
                 c = c < 0 ? 0 : (c >= d.n ? d.n - 1 : c);   // outside the matrix: the stored value is 0
-                v[k] = ld_na_f64(d.val + (int64_t)k * d.ldv + i, pol);
-                x[k] = __ldg(a.y + c);
+                a[u] = ld_na_f64(d.val + (int64_t)k * d.ldv + i, pol);
+                x[u] = __ldg(v + c);
             } else {
-                v[k] = 0.0;
-                x[k] = 0.0;
+                a[u] = 0.0;
+                x[u] = 0.0;
             }
         }
-        double acc = 0.0;
 #pragma unroll
-        for (int k = 0; k < UD; ++k)
-            if (k < d.nd) acc = fma(v[k], x[k], acc);
-        epi_a_store(a, MODE, i, acc, EpiA{}, OuterA{});   // a Q row: qy
+        for (int u = 0; u < U; ++u)
+            if (k0 + u < d.nd) acc = fma(a[u], x[u], acc);
     }
+    return acc;
 }
 
 template <int MODE, int U>
@@ -190,7 +182,8 @@ __global__ void __launch_bounds__(kLaneThreads, DQ_SELLA_MINB) k_pass_a_sell(con
         const int w = (int)((m.sptr[s + 1] - base) >> 5);
         EpiA e{};
         if (r >= 0) e = epi_a_load(a, MODE, r, o);
-        const double acc = sell_dot<U>(m, base, w, lane, a.y, pol);
+        const double acc = (s < m.nsl_q && a.dia.nd > 0) ? dia_dot<U>(a.dia, s * 32 + lane, a.y, pol)
+                                                         : sell_dot<U>(m, base, w, lane, a.y, pol);
         if (r >= 0) epi_a_store(a, MODE, r, acc, e, o);
     }
 }
@@ -500,31 +493,8 @@ int lane_blocks_per_sm(int pass, int kind, int u) {
     return u == 4 ? occ_of(k_pass_b_rowt<MODE_SOLVE, 4>) : occ_of(k_pass_b_rowt<MODE_SOLVE, 8>);
 }
 
-cudaError_t launch_pass_a_lane(const PassAArgs &a0, int mode, const LaunchCfg &cfg, cudaStream_t s) {
-    if (a0.row_end <= a0.row_begin) return cudaSuccess;
-    PassAArgs a = a0;
-    if (a.sp_kind == SPK_SELL && a.dia.nd > 0 && a.row_begin < a.nq) {   // the Q rows: DIA launch
-        const int64_t rows = (a.row_end < a.nq ? a.row_end : a.nq) - a.row_begin;
-        const int grid = (int)std::min<int64_t>((rows + kLaneThreads - 1) / kLaneThreads, 148LL * 8);
-        cudaError_t e;
-        const int ud = a.dia.nd <= 4 ? 4 : a.dia.nd <= 8 ? 8 : a.dia.nd <= 12 ? 12 : 16;
-#define DQ_DIA(MODE)                                                                             \
-        switch (ud) {                                                                            \
-            case 4: e = launch_ex(k_pass_a_dia<MODE, 4>, grid, kLaneThreads, 0, s, cfg.pdl, 0, a); break;   \
-            case 8: e = launch_ex(k_pass_a_dia<MODE, 8>, grid, kLaneThreads, 0, s, cfg.pdl, 0, a); break;   \
-            case 12: e = launch_ex(k_pass_a_dia<MODE, 12>, grid, kLaneThreads, 0, s, cfg.pdl, 0, a); break; \
-            default: e = launch_ex(k_pass_a_dia<MODE, 16>, grid, kLaneThreads, 0, s, cfg.pdl, 0, a); break; \
-        }
-        if (mode == MODE_SOLVE) {
-            DQ_DIA(MODE_SOLVE)
-        } else {
-            DQ_DIA(MODE_LIN)
-        }
-#undef DQ_DIA
-        if (e) return e;
-        a.row_begin = a.nq;   // the SELL launch: G rows only
-        if (a.row_end <= a.row_begin) return cudaSuccess;
-    }
+cudaError_t launch_pass_a_lane(const PassAArgs &a, int mode, const LaunchCfg &cfg, cudaStream_t s) {
+    if (a.row_end <= a.row_begin) return cudaSuccess;
     if (a.sp_kind == SPK_SELL) {
         if (mode == MODE_SOLVE) {
             DQ_LANE_DISPATCH(k_pass_a_sell, MODE_SOLVE, a.sp_u, cfg.grid, a);
