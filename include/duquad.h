@@ -211,7 +211,9 @@ typedef struct {
     int32_t path;               /* duquad_path: which kernels ran the inner steps           */
     int32_t sparse_kernels;     /* CSR: pass A kind | pass B kind << 4, kind 0 = sub-warp CSR,
                                    1 = SELL-32, 2 = thread-per-row CSR (options.sell_path);
-                                   + 8: pass A reads the banded Q rows as diagonals (DIA)     */
+                                   + 8: pass A reads the banded Q rows as diagonals (DIA);
+                                   + 64: only the band's upper half is stored and streamed
+                                   (symmetric DIA; the lower entries re-read from it)         */
 } duquad_result;
 
 /* Kernel path of a solve (duquad_result.path).  "pass A" / "pass B" in the report map to:

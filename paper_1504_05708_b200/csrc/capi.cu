@@ -875,9 +875,11 @@ duquad_status setup_csr(duquad_ctx *ctx, const duquad_problem *prob) {
     // measurement overrides (scripts/sparse_sweep.py): kind / load-round width per pass
     auto env_int = [](const char *k, int d) { const char *v = getenv(k); return v ? atoi(v) : d; };
     // banded Q (config 4: 11 diagonals): pass A reads the Q rows as diagonals -- no column indices,
-    // every load coalesced (8 instead of 12 bytes per nonzero); same per-row order (ascending columns)
+    // every load coalesced (8 instead of 12 bytes per nonzero); for a symmetric band only its upper
+    // half is stored and streamed (6 of config 4's 11 diagonals), the lower half re-read from it
     if (ctx->kind_a == SPK_SELL && ctx->nloc > 0 && env_int("DUQUAD_DIA", 1))
-        CK(dia_build(ctx->a_rp, ctx->a_ci, ctx->a_va, ctx->nloc, ctx->r0, n, nq, 1.15, &ctx->dia, &ctx->dia_val, s));
+        CK(dia_build(ctx->a_rp, ctx->a_ci, ctx->a_va, ctx->nloc, ctx->r0, n, nq, 1.15, env_int("DUQUAD_DIA_SYM", 1) != 0,
+                     &ctx->dia, &ctx->dia_val, s));
     if (ctx->kind_a == SPK_ROWT || (ctx->kind_a == SPK_SELL && env_int("DUQUAD_SPK_A", 1) == SPK_ROWT)) {
         ctx->kind_a = SPK_ROWT;
         ctx->u_a = env_int("DUQUAD_LANE_UA", ctx->u_a == 4 ? 4 : 8) <= 4 ? 4 : 8;
@@ -2121,7 +2123,7 @@ static duquad_status solve_body(duquad_ctx *ctx, int32_t alg, int32_t outer, int
                     : ctx->rho0 ? DUQUAD_PATH_RHO0
                     : ctx->Btot > 1 ? DUQUAD_PATH_BATCHED
                     : ctx->format == DUQUAD_CSR ? DUQUAD_PATH_CSR : DUQUAD_PATH_TWO_PASS;
-        res->sparse_kernels = ctx->format == DUQUAD_CSR ? (ctx->kind_a | (ctx->dia.nd > 0 ? 8 : 0)) | (ctx->kind_b << 4)
+        res->sparse_kernels = ctx->format == DUQUAD_CSR ? (ctx->kind_a | (ctx->dia.nd > 0 ? 8 : 0) | (ctx->dia.sym ? 64 : 0)) | (ctx->kind_b << 4)
                                                         : 0;
         res->outer_iters = K;
         res->inner_iters_total = (int64_t)nout * Kin;

@@ -44,13 +44,20 @@ struct SellMat {
 // Diagonal (DIA) view of the Q rows of pass A when Q is banded (config 4: 11 diagonals): value k of
 // local row i sits in val[k * ldv + i] for the diagonal at column offset off[k] (ascending = CSR
 // column order; 0 where the diagonal leaves the matrix).  No column indices, coalesced loads.
+// Symmetric form (sym = 1; Q = Q'): only the diagonals off[k] >= 0 are stored, at
+// val[k * ldv + halo + i] for i in [-halo, rows) (halo = the widest offset): row i's lower entry
+// Q[gi, gi - o] is the stored upper entry of row i - o, Q[gi - o, gi]; the halo rows before the
+// slice are filled from the local rows' own lower entries (so a row shard needs no remote data).
+// Half the diagonal bytes of the band per step (config 4: 6 of 11 diagonals).
 constexpr int kDiaMax = 16;
 struct DiaMat {
     const double *val;
-    int32_t nd;            // diagonals (0: Q rows are not in DIA form)
+    int32_t nd;            // stored diagonals (0: Q rows are not in DIA form)
     int32_t off[kDiaMax];
-    int64_t ldv;           // rows padded to a multiple of 32
+    int64_t ldv;           // rows (+ halo) padded to a multiple of 32
     int64_t r0, n;         // global index of local row 0, columns
+    int32_t sym;           // 1: symmetric half-band form (off[] >= 0 only)
+    int32_t halo;          // sym: rows stored before local row 0 (= the widest offset)
 };
 
 // ---------------------------------------------------------------- pass A
@@ -275,9 +282,11 @@ cudaError_t sell_build(const int32_t *rp, const int32_t *ci, const double *va, i
 void sell_free(SellStore *st);
 // DIA form of rows [0, rows) of a rebased CSR matrix (global row of local row i: r0 + i) when it has at
 // most kDiaMax distinct column offsets within [-64, 64] and the diagonals hold at most `max_pad` x its
-// nonzeros; *val = NULL (nothing allocated) otherwise
+// nonzeros; *val = NULL (nothing allocated) otherwise.  allow_sym: store the symmetric half band
+// (DiaMat.sym) when the offsets are symmetric and every in-slice pair Q[i, i-o] == Q[i-o, i] bitwise
+// (else the full band is kept)
 cudaError_t dia_build(const int32_t *rp, const int32_t *ci, const double *va, int64_t rows, int64_t r0, int64_t n,
-                      int64_t nnz, double max_pad, DiaMat *out, double **val, cudaStream_t s);
+                      int64_t nnz, double max_pad, bool allow_sym, DiaMat *out, double **val, cudaStream_t s);
 SellMat sell_view(const SellStore &st);
 int lane_unroll(int kind, int64_t max_width, double mean_len);
 int lane_blocks_per_sm(int pass, int kind, int u);

@@ -162,6 +162,62 @@ __device__ __forceinline__ double dia_dot(const DiaMat &d, int64_t i, const doub
     return acc;
 }
 
+// symmetric half band (DiaMat.sym): row i's lower entries Q[gi, gi-o] = Q[gi-o, gi] read from the
+// stored upper diagonals shifted by o, then its upper entries; both in ascending column order, so
+// the row sum is bitwise the full band's / the CSR kernels' for a bitwise symmetric Q.  One DRAM
+// round per row (rounds of DU: config 4's 5 + 6 loads): the upper round re-reads lines the lower
+// round has just pulled into L1.
+template <int DU>
+__device__ __forceinline__ double dia_dot_sym(const DiaMat &d, int64_t i, const double *__restrict__ v,
+                                              uint64_t pol) {
+    const int64_t gi = d.r0 + i;
+    const double *base = d.val + d.halo + i;
+    double acc = 0.0;
+    const int k1 = d.off[0] == 0 ? 1 : 0;          // lower half: the strictly positive offsets,
+    for (int k0 = d.nd - 1; k0 >= k1; k0 -= DU) {  // widest first (ascending columns)
+        double a[DU], x[DU];
+#pragma unroll
+        for (int u = 0; u < DU; ++u) {
+            const int k = k0 - u;
+            if (k >= k1) {   // warp-uniform
+                const int o = d.off[k];
+                const int64_t c = gi - o;
+                a[u] = ld_l1_f64(base + (int64_t)k * d.ldv - o, pol);
+                x[u] = __ldg(v + (c < 0 ? 0 : c));                // before column 0: stored 0
+            } else {
+                a[u] = 0.0;
+                x[u] = 0.0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < DU; ++u)
+            if (k0 - u >= k1) acc = fma(a[u], x[u], acc);
+    }
+    for (int k0 = 0; k0 < d.nd; k0 += DU) {        // upper half, ascending offsets
+        double a[DU], x[DU];
+#pragma unroll
+        for (int u = 0; u < DU; ++u) {
+            const int k = k0 + u;
+            if (k < d.nd) {
+                const int64_t c = gi + d.off[k];
+                a[u] = ld_l1_f64(base + (int64_t)k * d.ldv, pol);
+                x[u] = __ldg(v + (c >= d.n ? d.n - 1 : c));   // past the last column: stored 0
+            } else {
+                a[u] = 0.0;
+                x[u] = 0.0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < DU; ++u)
+            if (k0 + u < d.nd) acc = fma(a[u], x[u], acc);
+    }
+    return acc;
+}
+
+#ifndef DQ_DIA_DU
+#define DQ_DIA_DU 6
+#endif
+
 template <int MODE, int U>
 __global__ void __launch_bounds__(kLaneThreads, DQ_SELLA_MINB) k_pass_a_sell(const PassAArgs a) {
     pdl_wait();   // everything below reads iterates or writes (PDL, epilogue.cuh)
@@ -182,8 +238,10 @@ __global__ void __launch_bounds__(kLaneThreads, DQ_SELLA_MINB) k_pass_a_sell(con
         const int w = (int)((m.sptr[s + 1] - base) >> 5);
         EpiA e{};
         if (r >= 0) e = epi_a_load(a, MODE, r, o);
-        const double acc = (s < m.nsl_q && a.dia.nd > 0) ? dia_dot<U>(a.dia, s * 32 + lane, a.y, pol)
-                                                         : sell_dot<U>(m, base, w, lane, a.y, pol);
+        const double acc = (s < m.nsl_q && a.dia.nd > 0)
+                               ? (a.dia.sym ? dia_dot_sym<DQ_DIA_DU>(a.dia, s * 32 + lane, a.y, pol)
+                                            : dia_dot<U>(a.dia, s * 32 + lane, a.y, pol))
+                               : sell_dot<U>(m, base, w, lane, a.y, pol);
         if (r >= 0) epi_a_store(a, MODE, r, acc, e, o);
     }
 }
@@ -390,10 +448,28 @@ __global__ void k_dia_fill(const int32_t *rp, const int32_t *ci, const double *v
     if (i >= rows) return;
     for (int32_t e = rp[i]; e < rp[i + 1]; ++e) val[(int64_t)slot[ci[e] - (r0 + i) + kDiaWin] * ldv + i] = va[e];
 }
+// symmetric half band from the full band (full diagonals f = 0..nd-1, offsets ascending and
+// symmetric: diagonal f's mirror is nd-1-f).  Stored diagonal k (offset o = off[kf0 + k] >= 0):
+// sv[k][halo + i] = full[kf0 + k][i]; for o > 0 the lower entry full[nd-1-kf0-k][i] = Q[gi, gi-o]
+// either fills the halo (i - o < 0: row gi - o is not in the slice) or must equal the stored upper
+// entry of row i - o bitwise (else *bad = 1 and the full band is kept)
+__global__ void k_dia_sym(const double *full, int64_t ldf, int32_t nd, int32_t kf0, const int32_t *off_s, int32_t ns,
+                          int64_t rows, int64_t halo, int64_t ldv, double *sv, int32_t *bad) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    for (int k = 0; k < ns; ++k) {
+        const int o = off_s[k];
+        sv[(int64_t)k * ldv + halo + i] = full[(int64_t)(kf0 + k) * ldf + i];
+        if (o == 0) continue;
+        const double lo = full[(int64_t)(nd - 1 - kf0 - k) * ldf + i];
+        if (i - o < 0) sv[(int64_t)k * ldv + halo + i - o] = lo;
+        else if (lo != full[(int64_t)(kf0 + k) * ldf + i - o]) *bad = 1;
+    }
+}
 }  // namespace
 
 cudaError_t dia_build(const int32_t *rp, const int32_t *ci, const double *va, int64_t rows, int64_t r0, int64_t n,
-                      int64_t nnz, double max_pad, DiaMat *out, double **val, cudaStream_t s) {
+                      int64_t nnz, double max_pad, bool allow_sym, DiaMat *out, double **val, cudaStream_t s) {
     *out = DiaMat{};
     *val = nullptr;
     if (rows <= 0 || nnz <= 0) return cudaSuccess;
@@ -437,6 +513,39 @@ cudaError_t dia_build(const int32_t *rp, const int32_t *ci, const double *va, in
         d.val = *val;
         d.r0 = r0;
         d.n = n;
+        // symmetric half band: offsets symmetric about 0 with at least one off-diagonal
+        bool symm = allow_sym && !e && d.off[d.nd - 1] > 0;
+        for (int k = 0; symm && k < d.nd; ++k) symm = d.off[k] == -d.off[d.nd - 1 - k];
+        if (symm) {
+            DiaMat h = d;
+            const int32_t kf0 = d.nd / 2;   // first offset >= 0 (the offsets are symmetric)
+            h.nd = d.nd - kf0;
+            for (int k = 0; k < h.nd; ++k) h.off[k] = d.off[kf0 + k];
+            h.halo = h.off[h.nd - 1];
+            h.ldv = (rows + h.halo + 31) / 32 * 32;
+            h.sym = 1;
+            double *sv = nullptr;
+            int32_t bad = 0;
+            e = cudaMemcpyAsync(slot, h.off, h.nd * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+            if (!e) e = cudaMemsetAsync(hist, 0, sizeof(int32_t), s);
+            if (!e) e = cudaMalloc(&sv, (size_t)h.nd * h.ldv * sizeof(double));
+            if (!e) e = cudaMemsetAsync(sv, 0, (size_t)h.nd * h.ldv * sizeof(double), s);
+            if (!e) {
+                k_dia_sym<<<nblk(rows, 256), 256, 0, s>>>(*val, d.ldv, d.nd, kf0, slot, h.nd, rows, h.halo, h.ldv,
+                                                          sv, hist);
+                e = cudaGetLastError();
+            }
+            if (!e) e = cudaMemcpyAsync(&bad, hist, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+            if (!e) e = cudaStreamSynchronize(s);
+            if (!e && !bad) {
+                cudaFree(*val);
+                *val = sv;
+                h.val = sv;
+                d = h;
+            } else if (sv) {
+                cudaFree(sv);
+            }
+        }
         if (!e) *out = d;
     }
     cudaFree(hist);

@@ -224,6 +224,7 @@ def test_lane_kernels_vs_subwarp_kernels_and_oracle(torch_cuda, maker, kinds, al
     sk = info["sparse_kernels"]
     assert info["path"] == 5 and (sk & 3, (sk >> 4) & 3) == kinds, info
     assert bool(sk & 8) == (maker != "skewed")       # banded Q rows read as diagonals (DIA)
+    assert bool(sk & 64) == (maker != "skewed")      # ... only the band's upper half stored (symmetric)
     b = _gpu(prob, rho, alg, 6, 7, L_in, L_d, sell_path=False)
     assert b["solver"].solve(alg, 6, 7)["sparse_kernels"] == 0
     for k in ("x_last", "x_avg", "lam"):
@@ -284,3 +285,74 @@ def test_long_rows_keep_the_subwarp_kernels(torch_cuda):
         r = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 5.0, "DFGM", 3, 4, L_in, L_d)
         for a_, b_ in zip(got, (r.x_last, r.x_avg, r.lam)):
             assert relerr(a_, b_) <= TOL
+
+
+def _perturbed_mirror(Q, i, j, rel):
+    """Q with Q[i, j] (not Q[j, i]) scaled by 1 + rel: symmetric within setup's 1e-12 tolerance but
+    not bitwise."""
+    Q = Q.tolil(copy=True)
+    Q[i, j] = Q[i, j] * (1.0 + rel)
+    Q = Q.tocsr()
+    Q.sort_indices()
+    return Q
+
+
+@pytest.mark.parametrize("half_band", [1, 5, 7])
+def test_symmetric_half_band_dia(torch_cuda, monkeypatch, half_band):
+    """Pass A's banded Q rows from the stored upper half of the band (symmetric DIA: Q[i, i-o] read
+    as the stored Q[i-o, i]), summed in the same ascending column order: bitwise the
+    full-band DIA kernels' iterates for a bitwise symmetric Q, and the oracle's to 1e-9 with the
+    per-outer trace; a Q that is symmetric only to within setup's 1e-12 tolerance (one mirrored value
+    1e-14 off) keeps the full band."""
+    prob = qpgen.sparse_banded_eq(n=2500, p=900, seed=21, half_band=half_band)
+    L_in, L_d, _ = _consts_dense(prob, 5.0, 0.5)
+    a = _gpu(prob, 5.0, "DFGM", 5, 6, L_in, L_d, trace=True, torch=torch_cuda)
+    assert a["solver"].solve("DFGM", 5, 6)["sparse_kernels"] & (8 | 64) == 8 | 64
+    monkeypatch.setenv("DUQUAD_DIA_SYM", "0")
+    b = _gpu(prob, 5.0, "DFGM", 5, 6, L_in, L_d)
+    assert b["solver"].solve("DFGM", 5, 6)["sparse_kernels"] & (8 | 64) == 8
+    monkeypatch.delenv("DUQUAD_DIA_SYM")
+    for k in ("x_last", "x_avg", "lam"):
+        assert np.array_equal(a[k], b[k]), k
+    r = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 5.0, "DFGM", 5, 6, L_in, L_d,
+               keep_trace=True)
+    _check(a, r, trace=True)
+    a["solver"].close()
+    b["solver"].close()
+    # not bitwise symmetric: the full band is kept, and the oracle (which uses Q as given) agrees
+    Qp = _perturbed_mirror(prob.Q, 1200, 1200 - half_band, 1e-14)
+    pp = qpgen.SparseQP(Qp, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone)
+    c = _gpu(pp, 5.0, "DFGM", 5, 6, L_in, L_d)
+    assert c["solver"].solve("DFGM", 5, 6)["sparse_kernels"] & (8 | 64) == 8
+    r = O.dfom(Qp, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 5.0, "DFGM", 5, 6, L_in, L_d)
+    _check(c, r)
+    c["solver"].close()
+
+
+@pytest.mark.parametrize("n,P", [(3001, 3), (37, 5)])
+def test_symmetric_half_band_dia_row_sharded(torch_cuda, n, P):
+    """Row shards of the symmetric half band: each rank fills the halo rows before its slice from
+    its own rows' lower entries (no remote data), down to slices shorter than the halo (n = 37 over
+    5 ranks, half band 7): the emulated ranks' iterates equal the 1-GPU solve bit for bit and match
+    the oracle."""
+    from paper_1504_05708_b200 import Solver, solve_emulated
+    prob = qpgen.sparse_banded_eq(n=n, p=max(n // 3, 4), seed=23, half_band=7)
+    L_in, L_d, _ = _consts_dense(prob, 5.0, 0.5)
+    args = [prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone]
+    stream = torch_cuda.cuda.Stream().cuda_stream
+    ss = [Solver(*args, rho=5.0, world_size=P, rank=r, emulate_ranks=True, stream=stream) for r in range(P)]
+    for s_ in ss:
+        s_.set_constants(L_in, L_d)
+    solve_emulated(ss, "DFGM", 4, 5)
+    parts = [s_.result() for s_ in ss]
+    for s_ in ss:
+        s_.close()
+    got = [np.concatenate([pt[i] for pt in parts]) for i in range(3)]
+    one = _gpu(prob, 5.0, "DFGM", 4, 5, L_in, L_d)
+    assert one["solver"].solve("DFGM", 4, 5)["sparse_kernels"] & 64
+    for g_, k in zip(got, ("x_last", "x_avg", "lam")):
+        assert np.array_equal(g_, one[k]), k
+    one["solver"].close()
+    r = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 5.0, "DFGM", 4, 5, L_in, L_d)
+    for g_, w_ in zip(got, (r.x_last, r.x_avg, r.lam)):
+        assert relerr(g_, w_) <= TOL
