@@ -218,11 +218,16 @@ def main():
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    nccl_id = None
-    if world > 1:
+    def fresh_nccl_id():
+        # one NCCL unique id per communicator: an id's bootstrap root serves a single
+        # ncclCommInitRank round, so every Solver of a multi-rank run gets a new one from rank 0
+        if world == 1:
+            return None
         obj = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        return obj[0]
+
+    nccl_id = fresh_nccl_id()
 
     d = qpgen.dense_ineq_torch(n, p, seed=0, shift=0.05, device=str(dev))
     stream = torch.cuda.Stream(dev)     # the library runs on this stream; events are recorded on it
@@ -292,7 +297,8 @@ def main():
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
             se = Solver(hp["Q"], hp["q"], hp["G"], hp["g"], hp["lb"], hp["ub"], hp["cone"], rho=rho,
-                        lambda_min_lb=0.05, world_size=world, rank=rank, nccl_id=nccl_id, device=local_rank)
+                        lambda_min_lb=0.05, world_size=world, rank=rank, nccl_id=fresh_nccl_id(),
+                        device=local_rank)
             se.lipschitz(iters=60, safety=1e-3)
             se.solve("DFGM", K, Kin)
             xl, xa, lam = se.result()
