@@ -99,22 +99,8 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
 }
-#ifndef DQ_STREAM_EVF   // matrix stream marked L2 evict-first: the step's partials (ws_*), written
-#define DQ_STREAM_EVF 1  // during the stream and read by k_fused_epi, are not the lines it evicts
-#endif
-__device__ __forceinline__ uint64_t stream_policy() {
-    uint64_t pol;
-    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));   // no side effects: hoisted
-    return pol;
-}
 __device__ __forceinline__ void cp16(uint32_t dst, const double *src) {
-#if DQ_STREAM_EVF
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
-                 "l"(stream_policy())
-                 : "memory");
-#else
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-#endif
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
