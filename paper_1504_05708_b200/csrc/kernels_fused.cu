@@ -155,6 +155,10 @@ __device__ __forceinline__ Tile tile_of(const FusedArgs &f, int J) {
 
 // NCHG: G chunks per column block (0: no G role in this launch -- Q only)
 // Launched with a cluster dimension of 2 when there is a G role (pairs), 1 otherwise.
+#ifdef DQ_TRACE_G   // instrumentation build only: cumulative per-role cycle counters, printed periodically
+__device__ unsigned long long g_trg[8];   // G: wait, loop, epi-prefetch (warp 0), rows; Q: loop, steps
+__device__ unsigned g_trlaunch;
+#endif
 template <int NCHG>
 __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f) {
     // PDL (epilogue.cuh): the Q role fills its ring with Q rows (never written by a solve) before
@@ -171,6 +175,15 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
     const uint32_t ring_u32 = smem_u32(ring);
     auto slot_addr = [&](int s, int k) -> uint32_t { return ring_u32 + (uint32_t)((s * kV + k) * kThreadsF) * 16; };
 
+#ifdef DQ_TRACE_G
+    if (cta == 0 && tid == 0) {
+        const unsigned c = atomicAdd(&g_trlaunch, 1u);
+        if (c % 4000 == 3999)
+            printf("TRACE_G launches %u G: wait %llu loop %llu epipf %llu rows %llu | Q: loop %llu steps %llu\n", c + 1,
+                   g_trg[0], g_trg[1], g_trg[2], g_trg[3], g_trg[4], g_trg[5]);
+    }
+    unsigned long long tr_wait = 0, tr_pf = 0, tr_t0 = clock64();
+#endif
     if (tid == 0) {
         for (int s = 0; s < kD; ++s) mbar_init(&xbar[s], 1);   // warp 0's expect_tx + 32 x 8 bytes of st.async
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -390,6 +403,12 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
                 if (cb + (e >> 1) * 1024 + (e & 1) < t.b) dst[(e >> 1) * 1024 + (e & 1)] = acc[e];
         }
         cp_wait<0>();
+#ifdef DQ_TRACE_G
+        if (tid == 0) {
+            atomicAdd(&g_trg[4], clock64() - tr_t0);
+            atomicAdd(&g_trg[5], (unsigned long long)nsteps);
+        }
+#endif
     } else if constexpr (NCHG > 0) {
         // ================================ G role: pair gi owns rows [g0, g1); this CTA block `rank`
         const uint32_t rank = cluster_rank();
@@ -468,6 +487,9 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
             const uint32_t xb_r = map_to_cta(smem_u32(xbuf), (uint32_t)(lane & 1));
             const uint32_t xm_r = map_to_cta(smem_u32(xbar), (uint32_t)(lane & 1));
             auto prefetch_epi = [&](int it) {
+#ifdef DQ_TRACE_G
+                const unsigned long long t0_ = clock64();
+#endif
                 if (tid == 0 && it < nr) {
                     const EpiA e = epi_a_load(f.a, MODE_SOLVE, f.a.nq + g0 + it, o);
                     double *eb = epib + (it % kD) * 5;
@@ -477,6 +499,10 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
                     eb[3] = (double)e.c;
                     eb[4] = e.lh;
                 }
+#ifdef DQ_TRACE_G
+                __syncwarp();
+                tr_pf += clock64() - t0_;
+#endif
             };
             // Row finishing without any intra-CTA hand-off: every warp sends its partial of the row to
             // both CTAs of the pair (st.async into xbuf[d][rank * 16 + warp], completing 8 bytes of the
@@ -492,7 +518,13 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
             };
             auto row_w = [&](int it) -> double {
                 const int d = it % kD;
+#ifdef DQ_TRACE_G
+                const unsigned long long tw_ = clock64();
                 mbar_wait(&xbar[d], (uint32_t)((it / kD) & 1));
+                tr_wait += clock64() - tw_;
+#else
+                mbar_wait(&xbar[d], (uint32_t)((it / kD) & 1));
+#endif
                 double s_row = xbuf[d * 32 + lane];
                 s_row += __shfl_xor_sync(0xffffffffu, s_row, 16);
                 s_row += __shfl_xor_sync(0xffffffffu, s_row, 8);
@@ -539,6 +571,14 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
                 }
             }
             cp_wait<0>();
+#ifdef DQ_TRACE_G
+            if (lane == 0) {
+                atomicAdd(&g_trg[0], tr_wait);
+                atomicAdd(&g_trg[1], clock64() - tr_t0);
+                if (warp == 0) atomicAdd(&g_trg[2], tr_pf);
+                if (warp == 0) atomicAdd(&g_trg[3], (unsigned long long)nr);
+            }
+#endif
             double *pt = f.ws_g + (int64_t)gi * f.ld;
     #pragma unroll
             for (int m = 0; m < NCHG; ++m)
