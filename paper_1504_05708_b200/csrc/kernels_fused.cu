@@ -55,6 +55,8 @@ constexpr int kSlots = 7;               // per-thread ring depth (chunks; 224 KB
 // G role: a (kSlots - NCHG)-chunk ring + this CTA's block of y (NCHG chunks) in the same space
 constexpr int kD = 8;                   // depth of the per-row buffers / barriers (G rows)
 constexpr int kHdr = 3072;              // barriers + per-row buffers; header + ring = 227 KB
+constexpr int kE_ = 16;                 // (= kE) per-row epilogue-operand buffers in the header
+static_assert(128 + kD * 32 * 8 + kE_ * 5 * 8 <= kHdr, "header overflow");
 static_assert(kThreadsF * kV * 2 == kChunk, "chunk = 512 threads x 8 doubles");
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -106,6 +108,27 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// G rows' epilogue operands (g, mu, lambda_prev, cone, lam_hat) reach shared memory by cp.async,
+// kEpiAhead rows ahead (DQ_EPI_ASYNC), instead of loads by thread 0 that stall warp 0 -- the warp
+// every row's exchange waits for -- until they return (measured, DQ_TRACE_G: 20 % of warp 0's time)
+#ifndef DQ_EPI_ASYNC
+#define DQ_EPI_ASYNC 1
+#endif
+constexpr int kEpiAhead = 7;   // >= kSlotsG + 1: one ring group per row is the worst case (nch = 1)
+constexpr int kE = kE_;        // per-row epilogue buffers: a slot is rewritten kE - kEpiAhead rows after its
+                               // row, when every warp has long read it (a warp lags by at most one row)
+static_assert(kEpiAhead + 2 <= kE, "per-row epilogue buffers in flight");
+__device__ __forceinline__ void cp8s(double *smem, const double *gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp4s(void *smem, const uint32_t *gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+// the aligned 32-bit word holding the cone byte *c (decoded with the byte's offset in the word)
+__device__ __forceinline__ uint32_t cone_word(const uint8_t *c) {
+    return *reinterpret_cast<const uint32_t *>(reinterpret_cast<uintptr_t>(c) & ~(uintptr_t)3);
 }
 
 // column (relative to the chunk base) of element e (0..7) owned by thread t
@@ -170,7 +193,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
     // ---- shared memory: barriers + small per-row buffers (first 8 KB), then the ring
     uint64_t *xbar = reinterpret_cast<uint64_t *>(fsm);    // [kD] pair exchange (st.async bytes)
     double *xbuf = reinterpret_cast<double *>(fsm + 128);  // [kD][32] warp partials of a G row, rank-major
-    double *epib = xbuf + kD * 32;                         // [kD][5] g, mu, lambda_prev, cone, lam_hat of the row
+    double *epib = xbuf + kD * 32;                         // [kE][5] g, mu, lambda_prev, cone, lam_hat of the row
     const double2 *ring = reinterpret_cast<const double2 *>(fsm + kHdr) + tid;   // [kSlots][kV][512]
     const uint32_t ring_u32 = smem_u32(ring);
     auto slot_addr = [&](int s, int k) -> uint32_t { return ring_u32 + (uint32_t)((s * kV + k) * kThreadsF) * 16; };
@@ -492,11 +515,11 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
 #endif
                 if (tid == 0 && it < nr) {
                     const EpiA e = epi_a_load(f.a, MODE_SOLVE, f.a.nq + g0 + it, o);
-                    double *eb = epib + (it % kD) * 5;
+                    double *eb = epib + (it % kE) * 5;
                     eb[0] = e.g;
                     eb[1] = e.mu;
                     eb[2] = e.lp;
-                    eb[3] = (double)e.c;
+                    *reinterpret_cast<uint32_t *>(eb + 3) = cone_word(f.a.cone + g0 + it);
                     eb[4] = e.lh;
                 }
 #ifdef DQ_TRACE_G
@@ -504,6 +527,25 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
                 tr_pf += clock64() - t0_;
 #endif
             };
+#if DQ_EPI_ASYNC
+            // the same operands with cp.async (thread 0), kEpiAhead rows ahead: nothing waits for
+            // them here.  They join thread 0's next ring group; post(it) -- warp 0's arrive that
+            // publishes row it's buffer -- comes after a take() whose cp_wait<kSlotsG - 1> retired
+            // every group at least kSlotsG - 1 newer ones old, i.e. (one or more groups per row) the
+            // group of row it's copies, issued kEpiAhead >= kSlotsG + 1 rows earlier.
+            auto prefetch_epi_async = [&](int it) {
+                if (tid == 0 && it < nr) {
+                    const int64_t k = g0 + it;
+                    double *eb = epib + (it % kE) * 5;
+                    cp8s(eb + 0, f.a.g + k);
+                    cp8s(eb + 1, f.a.mu + k);
+                    if (o.dual) cp8s(eb + 2, f.a.lam_prev + k);
+                    if (o.lhat_w != 0.0) cp8s(eb + 4, f.a.lam_hat + k);
+                    cp4s(eb + 3, reinterpret_cast<const uint32_t *>(reinterpret_cast<uintptr_t>(f.a.cone + k) &
+                                                                    ~(uintptr_t)3));
+                }
+            };
+#endif
             // Row finishing without any intra-CTA hand-off: every warp sends its partial of the row to
             // both CTAs of the pair (st.async into xbuf[d][rank * 16 + warp], completing 8 bytes of the
             // row's exchange barrier there; warp 0 arms the barrier for all 32 partials), then waits for
@@ -531,17 +573,22 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
                 s_row += __shfl_xor_sync(0xffffffffu, s_row, 4);
                 s_row += __shfl_xor_sync(0xffffffffu, s_row, 2);
                 s_row += __shfl_xor_sync(0xffffffffu, s_row, 1);
-                const double *eb = epib + d * 5;
+                const double *eb = epib + (it % kE) * 5;
                 EpiA e;
                 e.g = eb[0];
                 e.mu = eb[1];
                 e.lp = eb[2];
-                e.c = (uint8_t)eb[3];
+                e.c = (uint8_t)(*reinterpret_cast<const uint32_t *>(eb + 3) >>
+                                (8 * (reinterpret_cast<uintptr_t>(f.a.cone + g0 + it) & 3)));
                 e.lh = eb[4];
                 return g_row_w(f.a, g0 + it, s_row, e, o, rank == 0 && warp == 0 && lane == 0);
             };
+#if DQ_EPI_ASYNC
+            for (int r = 0; r < kEpiAhead; ++r) prefetch_epi(r);
+#else
             prefetch_epi(0);
             prefetch_epi(1);
+#endif
             double hold[NCHG][8];   // the current row's values (chunks 0..nch-1)
             if (nr > 0) {
                 double part = 0.0;
@@ -552,7 +599,11 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
             }
             for (int it = 0; it < nr; ++it) {
                 const bool nxt = it + 1 < nr;
+#if DQ_EPI_ASYNC
+                prefetch_epi_async(it + kEpiAhead);
+#else
                 prefetch_epi(it + 2);
+#endif
                 double next0[8];
                 double part = 0.0;
                 if (nxt) part = take(0, next0, part);                    // row it+1, chunk 0
