@@ -182,6 +182,10 @@ __device__ __forceinline__ Tile tile_of(const FusedArgs &f, int J) {
 __device__ unsigned long long g_trg[8];   // G: wait, loop, epi-prefetch (warp 0), rows; Q: loop, steps
 __device__ unsigned g_trlaunch;
 #endif
+#ifdef DQ_TRACE_ROLE   // instrumentation build only: per-CTA durations (globaltimer) of one launch
+__device__ unsigned long long g_trd[2 * 160];
+__device__ unsigned g_trrl;
+#endif
 template <int NCHG>
 __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f) {
     // PDL (epilogue.cuh): the Q role fills its ring with Q rows (never written by a solve) before
@@ -198,6 +202,20 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
     const uint32_t ring_u32 = smem_u32(ring);
     auto slot_addr = [&](int s, int k) -> uint32_t { return ring_u32 + (uint32_t)((s * kV + k) * kThreadsF) * 16; };
 
+#ifdef DQ_TRACE_ROLE
+    unsigned long long trr_t0 = 0;
+    unsigned trr_l = 0;
+    if (tid == 0) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trr_t0));
+        trr_l = *(volatile unsigned *)&g_trrl;
+        if (cta == 0 && trr_l == 4001) {   // the launch after the recorded one: print it
+            printf("TRACE_ROLE nq %d nb %d\n", f.nq_ctas, (int)gridDim.x);
+            for (int c = 0; c < (int)gridDim.x && c < 160; c += 8)
+                printf("TRACE_ROLE %3d: %llu %llu %llu %llu %llu %llu %llu %llu\n", c, g_trd[c], g_trd[c + 1],
+                       g_trd[c + 2], g_trd[c + 3], g_trd[c + 4], g_trd[c + 5], g_trd[c + 6], g_trd[c + 7]);
+        }
+    }
+#endif
 #ifdef DQ_TRACE_G
     if (cta == 0 && tid == 0) {
         const unsigned c = atomicAdd(&g_trlaunch, 1u);
@@ -645,6 +663,15 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
             g_body(std::false_type{});
     }
     __syncthreads();
+#ifdef DQ_TRACE_ROLE
+    if (tid == 0) {
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (trr_l == 4000 && cta < 160) g_trd[cta] = t1 - trr_t0;   // ns from this CTA's start
+        __threadfence();
+        if (cta == 0) atomicAdd(&g_trrl, 1u);   // launch counter (CTA 0 of each launch)
+    }
+#endif
     cluster_sync_all();   // no CTA leaves while its partner may still write its shared memory
 }
 
