@@ -1411,7 +1411,7 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         }
         double row_cost = 32768.0;          // bytes-equivalent cost of one Q row step (latency-bound: ~a full step)
         if (const char *ov = std::getenv("DUQUAD_FUSED_ROWCOST")) row_cost = std::atof(ov);
-        double diag_fac = 1.0;              // extra cost of a diagonal-tile row step
+        double diag_fac = 1.12;             // extra cost of a diagonal-tile row step (measured: r02_diag_sweep.txt)
         if (const char *ov = std::getenv("DUQUAD_FUSED_DIAG")) diag_fac = std::atof(ov);
         FusedArgs &fz = ctx->fz;
         fz.n = n;
