@@ -113,9 +113,6 @@ __device__ __forceinline__ void cp_wait() {
 // G rows' epilogue operands (g, mu, lambda_prev, cone, lam_hat) reach shared memory by cp.async,
 // kEpiAhead rows ahead (DQ_EPI_ASYNC), instead of loads by thread 0 that stall warp 0 -- the warp
 // every row's exchange waits for -- until they return (measured, DQ_TRACE_G: 20 % of warp 0's time)
-#ifndef DQ_YNEXT
-#define DQ_YNEXT 1
-#endif
 #ifndef DQ_EPI_ASYNC
 #define DQ_EPI_ASYNC 1
 #endif
@@ -309,9 +306,6 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
             // y_r for 32 rows at a time, one per lane (broadcast by shuffle)
             int ybase = rb;
             double ycache = rb + lane < t.rows ? f.y[rb + lane] : 0.0;
-#if DQ_YNEXT   // the next 32 rows' y, loaded 32 row steps before use (no load-to-use stall per window)
-            double ynext = rb + 32 + lane < t.rows ? f.y[rb + 32 + lane] : 0.0;
-#endif
             int r = rb;
             // the row-pair butterfly is software-pipelined: pair i's sums are reduced after pair i+1's
             // FMAs, so its dependent shuffle chain overlaps independent work (same sums, same order)
@@ -327,14 +321,9 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
                 if ((lane & 15) == 0) rowp[rr + (lane >> 4)] = mine;
             };
             for (; r + 1 < re; r += 2) {   // two row steps per iteration (independent chains)
-                if (r + 1 - ybase >= 32) {   // r - ybase even: r = ybase + 32
+                if (r + 1 - ybase >= 32) {
                     ybase = r;
-#if DQ_YNEXT
-                    ycache = ynext;
-                    ynext = r + 32 + lane < t.rows ? f.y[r + 32 + lane] : 0.0;
-#else
                     ycache = r + lane < t.rows ? f.y[r + lane] : 0.0;
-#endif
                 }
                 const double y0 = __shfl_sync(0xffffffffu, ycache, r - ybase);
                 const double y1 = __shfl_sync(0xffffffffu, ycache, r + 1 - ybase);
@@ -422,13 +411,9 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
             }
             if (pr_ >= 0) finish_pair(p0, p1, pr_);
             if (r < re) {   // last row of the segment
-                if (r - ybase >= 32) {   // r = ybase + 32
+                if (r - ybase >= 32) {
                     ybase = r;
-#if DQ_YNEXT
-                    ycache = ynext;
-#else
                     ycache = r + lane < t.rows ? f.y[r + lane] : 0.0;
-#endif
                 }
                 const double y0 = __shfl_sync(0xffffffffu, ycache, r - ybase);
                 cp_wait<kSlots - 1>();
