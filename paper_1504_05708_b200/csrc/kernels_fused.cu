@@ -113,9 +113,6 @@ __device__ __forceinline__ void cp_wait() {
 // G rows' epilogue operands (g, mu, lambda_prev, cone, lam_hat) reach shared memory by cp.async,
 // kEpiAhead rows ahead (DQ_EPI_ASYNC), instead of loads by thread 0 that stall warp 0 -- the warp
 // every row's exchange waits for -- until they return (measured, DQ_TRACE_G: 20 % of warp 0's time)
-#ifndef DQ_G_INTERLEAVE   // G rows dealt to the pairs round robin (1) or in contiguous blocks (0)
-#define DQ_G_INTERLEAVE 0
-#endif
 #ifndef DQ_EPI_ASYNC
 #define DQ_EPI_ASYNC 1
 #endif
@@ -454,13 +451,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
         const int nch = (b - a + kChunk - 1) / kChunk;
         const bool ragged = ((b - a) % kChunk) != 0;
         const int gi = (cta - f.nq_ctas) >> 1;
-#if DQ_G_INTERLEAVE   // pair gi owns rows gi, gi + ng, gi + 2 ng, ... (row it of the pair: g0 + gs * it)
-        const int64_t g0 = gi, gs = f.ng;
-        const int nr = (int)(gi < f.p ? (f.p - gi + f.ng - 1) / f.ng : 0);
-#else                 // pair gi owns the contiguous rows [g0, g1)
-        const int64_t g0 = f.p * gi / f.ng, gs = 1;
-        const int nr = (int)(f.p * (gi + 1) / f.ng - g0);
-#endif
+        const int64_t g0 = f.p * gi / f.ng, g1 = f.p * (gi + 1) / f.ng;
+        const int nr = (int)(g1 - g0);
         // The G role keeps this CTA's block of y in shared memory (after a kSlotsG-slot ring) and
         // row values in registers between their dot and their w G, so every ring slot is refilled
         // as soon as it is read (kSlotsG chunks in flight).  Half-row lag: the first chunk of row
@@ -480,7 +472,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
             int p_it = 0, p_m = 0, ps = 0;   // prefetch cursor
             auto issue = [&]() {
                 if (p_it < nr) {
-                    const double *row = f.G + (g0 + gs * p_it) * f.ld;
+                    const double *row = f.G + (g0 + p_it) * f.ld;
     #pragma unroll
                     for (int k = 0; k < kV; ++k) {
                         const int c = a + p_m * kChunk + 2 * tid + 1024 * k;
@@ -534,12 +526,12 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
                 const unsigned long long t0_ = clock64();
 #endif
                 if (tid == 0 && it < nr) {
-                    const EpiA e = epi_a_load(f.a, MODE_SOLVE, f.a.nq + g0 + gs * it, o);
+                    const EpiA e = epi_a_load(f.a, MODE_SOLVE, f.a.nq + g0 + it, o);
                     double *eb = epib + (it % kE) * 5;
                     eb[0] = e.g;
                     eb[1] = e.mu;
                     eb[2] = e.lp;
-                    *reinterpret_cast<uint32_t *>(eb + 3) = cone_word(f.a.cone + g0 + gs * it);
+                    *reinterpret_cast<uint32_t *>(eb + 3) = cone_word(f.a.cone + g0 + it);
                     eb[4] = e.lh;
                 }
 #ifdef DQ_TRACE_G
@@ -555,7 +547,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
             // group of row it's copies, issued kEpiAhead >= kSlotsG + 1 rows earlier.
             auto prefetch_epi_async = [&](int it) {
                 if (tid == 0 && it < nr) {
-                    const int64_t k = g0 + gs * it;
+                    const int64_t k = g0 + it;
                     double *eb = epib + (it % kE) * 5;
                     cp8s(eb + 0, f.a.g + k);
                     cp8s(eb + 1, f.a.mu + k);
@@ -599,9 +591,9 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_fused_stream(const FusedArgs f
                 e.mu = eb[1];
                 e.lp = eb[2];
                 e.c = (uint8_t)(*reinterpret_cast<const uint32_t *>(eb + 3) >>
-                                (8 * (reinterpret_cast<uintptr_t>(f.a.cone + g0 + gs * it) & 3)));
+                                (8 * (reinterpret_cast<uintptr_t>(f.a.cone + g0 + it) & 3)));
                 e.lh = eb[4];
-                return g_row_w(f.a, g0 + gs * it, s_row, e, o, rank == 0 && warp == 0 && lane == 0);
+                return g_row_w(f.a, g0 + it, s_row, e, o, rank == 0 && warp == 0 && lane == 0);
             };
 #if DQ_EPI_ASYNC
             for (int r = 0; r < kEpiAhead; ++r) prefetch_epi(r);
