@@ -1411,8 +1411,9 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         }
         double row_cost = 32768.0;          // bytes-equivalent cost of one Q row step (latency-bound: ~a full step)
         if (const char *ov = std::getenv("DUQUAD_FUSED_ROWCOST")) row_cost = std::atof(ov);
-        double diag_fac = 1.12;             // extra cost of a diagonal-tile row step (measured: r02_diag_sweep.txt)
+        double diag_fac = 1.145, diag_slope = 0.0746;   // diagonal-tile row step: fit to per-CTA times
         if (const char *ov = std::getenv("DUQUAD_FUSED_DIAG")) diag_fac = std::atof(ov);
+        if (const char *ov = std::getenv("DUQUAD_FUSED_DSLOPE")) diag_slope = std::atof(ov);
         FusedArgs &fz = ctx->fz;
         fz.n = n;
         fz.p = p;
@@ -1429,7 +1430,7 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         fz.qa = ctx->r0;
         fz.qb = ctx->r0 + ctx->nloc;
         fz.partial = nullptr;
-        fz.cslots = fused_partition(n, ctx->ld, nq, row_cost, diag_fac, pcs, fz.qlo, fz.qhi, fz.qa, fz.qb);
+        fz.cslots = fused_partition(n, ctx->ld, nq, row_cost, diag_fac, diag_slope, pcs, fz.qlo, fz.qhi, fz.qa, fz.qb);
         const int64_t wrow = (int64_t)fz.nt * 16 * ctx->ld, wcol = (int64_t)nq * fz.cslots * 4096,
                       wg = (int64_t)fz.ng * ctx->ld;
         CKS(dalloc(&ctx->ws, wrow + wcol + wg));

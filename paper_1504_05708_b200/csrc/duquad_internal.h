@@ -302,8 +302,8 @@ int fused_tiles(int64_t ld);
 size_t fused_smem_bytes();
 cudaError_t launch_slice_epi(const PassBArgs &bl, const PassBArgs &bs, const double *sum, cudaStream_t s);
 cudaError_t launch_vec_add(double *dst, const double *src, int64_t n, cudaStream_t s);
-int fused_partition(int64_t n, int64_t ld, int nq, double row_cost, double diag_fac, std::vector<FusedPiece> &pieces,
-                    int32_t *qlo, int32_t *qhi, int64_t qa, int64_t qb);
+int fused_partition(int64_t n, int64_t ld, int nq, double row_cost, double diag_fac, double diag_slope,
+                    std::vector<FusedPiece> &pieces, int32_t *qlo, int32_t *qhi, int64_t qa, int64_t qb);
 cudaError_t configure_fused_kernels(int nchg, size_t smem);
 cudaError_t launch_fused_stream(const FusedArgs &f, cudaStream_t s);
 cudaError_t launch_fused_epi(const PassBArgs &bl, const PassBArgs &bs, const FusedArgs &f, cudaStream_t s);

@@ -817,12 +817,13 @@ int fused_max_clusters(int nchg, int cg, size_t smem) {
 }
 
 // Cut of the Q triangle sequence (J, r) into nq pieces of equal estimated time: a row step costs
-// max(bytes, row_cost) (the per-step instruction cost dominates short steps near the diagonal),
-// times diag_fac for the steps of a diagonal tile (masks on the straddling quarter, two rows of
-// unequal length per pair).  qlo / qhi: the pieces with rows in each tile column; returns the most
-// tile columns a piece spans.
-int fused_partition(int64_t n, int64_t ld, int nq, double row_cost, double diag_fac, std::vector<FusedPiece> &pieces,
-                    int32_t *qlo, int32_t *qhi, int64_t qa, int64_t qb) {
+// max(bytes, row_cost) (the per-step instruction cost dominates short steps near the diagonal);
+// a step of a diagonal tile (masks on the straddling quarter, two rows of unequal length per pair)
+// costs diag_fac * row_cost + diag_slope * bytes (fit to per-CTA end times of config 2,
+// profiles/r02_role_trace3.txt: 1.145 and 0.0746).  qlo / qhi: the pieces with rows in each tile
+// column; returns the most tile columns a piece spans.
+int fused_partition(int64_t n, int64_t ld, int nq, double row_cost, double diag_fac, double diag_slope,
+                    std::vector<FusedPiece> &pieces, int32_t *qlo, int32_t *qhi, int64_t qa, int64_t qb) {
     const int nt = fused_tiles(ld);
     // rows of tile column J in this rank's row range [qa, qb) (single GPU: [0, n)): [qa, rows(J))
     auto rows = [&](int J) -> int64_t {
@@ -831,7 +832,8 @@ int fused_partition(int64_t n, int64_t ld, int nq, double row_cost, double diag_
     auto cost = [&](int J, int64_t r) -> double {
         const int64_t a = (int64_t)J * kChunk, b = std::min<int64_t>(a + kChunk, ld);
         const int64_t st = r > a ? (r & ~1LL) : a;
-        return std::max(8.0 * (double)(b - st), row_cost) * (r >= a ? diag_fac : 1.0);
+        const double bytes = 8.0 * (double)(b - st);
+        return r >= a ? diag_fac * row_cost + diag_slope * bytes : std::max(bytes, row_cost);
     };
     double total = 0.0;
     for (int J = 0; J < nt; ++J)
