@@ -10,3 +10,8 @@ for i in 1 2; do
   done
 done | tee gpurun_out/c4_sweep.txt
 cp /tmp/keep.so paper_1504_05708_b200/libduquad.so
+# config 1 re-check (its two-pass / K3 kernels were not changed this session)
+timeout 600 python scripts/bench_configs.py --configs 1 > gpurun_out/c1_recheck.jsonl 2>/dev/null; python -c "
+import json
+for l in open('gpurun_out/c1_recheck.jsonl'):
+    d=json.loads(l); print('c1', d['alg'], d['rho'], round(d['us_per_inner_step'],2))"
