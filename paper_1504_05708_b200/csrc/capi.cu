@@ -1021,8 +1021,15 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         return fail(nullptr, DUQUAD_EINVAL, "bad world_size / rank");
     if (opt.world_size > 1 && !batched && !opt.nccl_id && !opt.emulate_ranks)
         return fail(nullptr, DUQUAD_EINVAL, "row-sharded setup needs nccl_id");
-    if (!prob->on_device) {   // host data: validate here (device data is validated by a kernel)
-        if ((!csr && (!finite_host(prob->Q, n, n, prob->ldQ) || (p > 0 && !finite_host(prob->G, p, n, prob->ldG)))) ||
+    // host data: validate here (device data is validated by a kernel); a single rank's dense Q and G
+    // are checked on the device after their upload instead (3.2 GB at config 2: a host scan costs
+    // tens of ms of every end-to-end solve, the device check ~1 ms)
+    int ndev0 = 0;
+    if (cudaGetDeviceCount(&ndev0) != cudaSuccess) ndev0 = 0;
+    const bool qg_dev_check = !prob->on_device && !csr && opt.world_size == 1 && ndev0 > 0;
+    if (!prob->on_device) {
+        if ((!csr && !qg_dev_check &&
+             (!finite_host(prob->Q, n, n, prob->ldQ) || (p > 0 && !finite_host(prob->G, p, n, prob->ldG)))) ||
             !finite_host(prob->q, prob->batch, n, n) || (p > 0 && !finite_host(prob->g, prob->batch, p, p)))
             return fail(nullptr, DUQUAD_EINVAL, "non-finite problem data");
         for (int64_t i = 0; i < n; ++i)
@@ -1186,16 +1193,19 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
                                   prob->G + ctx->s0 * prob->ldG, prob->ldG * sizeof(double),
                                   n * sizeof(double), ctx->ploc, cudaMemcpyDefault, s));
         // G' rows r0..r0+nloc = columns r0.. of G; stage G on the device when it is on the host
+        // (a rank holding every G row transposes its own device copy: no second upload)
         const double *Gd = prob->G;
         double *Gtmp = nullptr;
-        if (!prob->on_device) {
+        const bool g_local = !prob->on_device && ctx->s0 == 0 && ctx->ploc == p;
+        if (g_local) Gd = ctx->A + ctx->nloc * ctx->ld;
+        if (!prob->on_device && !g_local) {
             CKS(cudaMalloc(&Gtmp, (size_t)p * n * sizeof(double)));
             CKS(cudaMemcpy2DAsync(Gtmp, n * sizeof(double), prob->G, prob->ldG * sizeof(double),
                                   n * sizeof(double), p, cudaMemcpyHostToDevice, s));
             Gd = Gtmp;
         }
-        cudaError_t e = launch_transpose(Gd, prob->on_device ? prob->ldG : n, p, ctx->r0, ctx->nloc,
-                                         ctx->GT, ctx->ldp, s);
+        cudaError_t e = launch_transpose(Gd, prob->on_device ? prob->ldG : g_local ? ctx->ld : n, p, ctx->r0,
+                                         ctx->nloc, ctx->GT, ctx->ldp, s);
         if (Gtmp) {
             cudaStreamSynchronize(s);
             cudaFree(Gtmp);
@@ -1262,6 +1272,17 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
                 ctx->ldd = round_up(P, 32);
                 CKS(dalloc(&ctx->Db, B * ctx->ldd));   // zero padding: pass B's K runs to ldd
             }
+        }
+    }
+    if (qg_dev_check) {   // the uploaded [Q;G] of a single rank (host input)
+        CKS(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int32_t), s));
+        CKS(launch_check(ctx->A, rows, n, ctx->ld, ctx->d_flag, s));
+        int32_t flag = 0;
+        CKS(cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(flag), cudaMemcpyDeviceToHost, s));
+        CKS(cudaStreamSynchronize(s));
+        if (flag) {
+            ctx->err = "non-finite problem data";
+            return bail(DUQUAD_EINVAL);
         }
     }
     if (prob->on_device) {

@@ -257,6 +257,21 @@ def test_device_input_validation(torch_cuda, c0):
     assert e.value.status == 1
 
 
+def test_host_input_validation_on_device(torch_cuda, c0):
+    """A single rank's host Q and G are checked for non-finite values on the device after their
+    upload (no host scan): a NaN / inf in Q or G is still rejected with EINVAL, and an emulated
+    2-rank setup (host scan) rejects it alike."""
+    from paper_1504_05708_b200 import Solver, DuquadError
+    for name, (i, j), v in (("Q", (3, 4), float("nan")), ("G", (7, 11), float("inf")),
+                            ("G", (c0.G.shape[0] - 1, c0.G.shape[1] - 1), float("nan"))):
+        arrs = {k: getattr(c0, k).copy() for k in ("Q", "G")}
+        arrs[name][i, j] = v
+        for kw in ({}, dict(world_size=2, rank=1, emulate_ranks=True)):
+            with pytest.raises(DuquadError, match="non-finite") as e:
+                Solver(arrs["Q"], c0.q, arrs["G"], c0.g, c0.lb, c0.ub, c0.cone, rho=1.0, **kw)
+            assert e.value.status == 1
+
+
 # ------------------------------------------------------------- config 2 at full size
 @pytest.mark.slow
 def test_config2_full_size_prefix(torch_cuda):
