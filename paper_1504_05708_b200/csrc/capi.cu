@@ -1171,7 +1171,7 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
     CKS(dalloc(&ctx->g, ctx->ploc));
     CKS(dalloc(&ctx->mu, ctx->ploc));
     CKS(dalloc(&ctx->lam_prev, ctx->ploc));
-    CKS(dalloc(&ctx->cone, ctx->ploc));
+    CKS(dalloc(&ctx->cone, (ctx->ploc + 7) / 8 * 8));   // whole 32-bit words (the byte floor reads cone words)
     CKS(dalloc(&ctx->scal, SC_NSCAL));
     CKS(dalloc(&ctx->partials, kRedGrid * 8));
     CKS(dalloc(&ctx->d_j, 4));
