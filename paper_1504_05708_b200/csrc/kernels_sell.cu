@@ -214,6 +214,9 @@ __device__ __forceinline__ double dia_dot_sym(const DiaMat &d, int64_t i, const 
     return acc;
 }
 
+#ifndef DQ_SELL_MIX
+#define DQ_SELL_MIX 1
+#endif
 #ifndef DQ_DIA_DU
 #define DQ_DIA_DU 6
 #endif
@@ -232,7 +235,15 @@ __global__ void __launch_bounds__(kLaneThreads, DQ_SELLA_MINB) k_pass_a_sell(con
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const OuterA o = outer_a(a, MODE);
     const uint64_t pol = evict_first();
-    for (int64_t s = s_lo + warp; s < s_hi; s += nwarps) {
+    // whole range: Q and G slices interleaved in proportion (DQ_SELL_MIX), so the DIA Q rows (one
+    // DRAM round each) and the G rows (index -> gather chains) are in flight together
+    const bool mix = DQ_SELL_MIX && s_lo == 0 && s_hi == m.nsl && m.nsl_q > 0 && m.nsl > m.nsl_q;
+    for (int64_t t = s_lo + warp; t < s_hi; t += nwarps) {
+        int64_t s = t;
+        if (mix) {
+            const int64_t qb = t * m.nsl_q / m.nsl, qn = (t + 1) * m.nsl_q / m.nsl;
+            s = qn > qb ? qb : m.nsl_q + (t - qb);
+        }
         const int64_t r = sell_row(m, s, lane);
         const int64_t base = m.sptr[s];
         const int w = (int)((m.sptr[s + 1] - base) >> 5);
