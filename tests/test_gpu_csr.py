@@ -356,24 +356,3 @@ def test_symmetric_half_band_dia_row_sharded(torch_cuda, n, P):
     r = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 5.0, "DFGM", 4, 5, L_in, L_d)
     for g_, w_ in zip(got, (r.x_last, r.x_avg, r.lam)):
         assert relerr(g_, w_) <= TOL
-
-
-@pytest.mark.parametrize("window", ["64", "1000"])
-def test_rowt_length_sorted_windows_bitwise(torch_cuda, monkeypatch, window):
-    """Thread-per-row G' stored with its rows sorted by length inside windows (position -> row map
-    for the epilogue): every row is still summed by one lane in CSR order, so the iterates equal the
-    storage-order kernel's bit for bit, for the banded family and for skewed rows (ROWT in both
-    passes), and match the oracle."""
-    for prob, rho in ((qpgen.sparse_banded_eq(n=2777, p=1111, seed=31), 5.0), (_skewed(seed=31), 2.0)):
-        L_in, L_d, _ = _consts_dense(prob, rho, 0.5)
-        outs = []
-        for w in (window, "0"):
-            monkeypatch.setenv("DUQUAD_ROWT_SORT", w)
-            g = _gpu(prob, rho, "DFGM", 4, 6, L_in, L_d)
-            outs.append(g)
-            g["solver"].close()
-        monkeypatch.delenv("DUQUAD_ROWT_SORT")
-        for k in ("x_last", "x_avg", "lam"):
-            assert np.array_equal(outs[0][k], outs[1][k]), k
-        r = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, rho, "DFGM", 4, 6, L_in, L_d)
-        _check(outs[0], r)
