@@ -57,7 +57,6 @@ struct duquad_ctx {
     double *lz_vprev = nullptr, *lz_w = nullptr;
     // CSR storage (format == DUQUAD_CSR): stacked local [Q_r; G_r] and local rows of G'
     int32_t *a_rp = nullptr, *a_ci = nullptr, *b_rp = nullptr, *b_ci = nullptr;
-    int32_t *b_pidx = nullptr;  // G' rows of the thread-per-row kernel sorted by length in windows
     double *a_va = nullptr, *b_va = nullptr;
     int64_t nnz_a = 0, nnz_b = 0;
     int gs_a = 4, gs_b = 4;
@@ -182,7 +181,7 @@ void free_all(duquad_ctx *c) {
     for (double *d : ds)
         if (d) cudaFree(d);
     if (c->cone) cudaFree(c->cone);
-    int32_t *is[] = {c->a_rp, c->a_ci, c->b_rp, c->b_ci, c->b_pidx};
+    int32_t *is[] = {c->a_rp, c->a_ci, c->b_rp, c->b_ci};
     for (int32_t *d : is)
         if (d) cudaFree(d);
     if (c->a_va) cudaFree(c->a_va);
@@ -320,7 +319,6 @@ PassBArgs make_b(duquad_ctx *c) {
     b.rp = c->b_rp;
     b.ci = c->b_ci;
     b.va = c->b_va;
-    b.pidx = c->b_pidx;
     b.skip = c->eps_mode ? c->d_done : nullptr;
     b.gm_sq = c->eps_mode ? c->gm_sq : nullptr;
     b.box_uniform = c->box_uniform;
@@ -889,11 +887,6 @@ duquad_status setup_csr(duquad_ctx *ctx, const duquad_problem *prob) {
         ctx->u_a = env_int("DUQUAD_LANE_UA", ctx->u_a);
     }
     if (ctx->kind_b == SPK_ROWT) ctx->u_b = env_int("DUQUAD_LANE_UB", ctx->u_b) <= 4 ? 4 : 8;
-    // thread-per-row G': rows reordered by length within windows of 256 (8 warps), so a warp's 32
-    // rows need about as many load rounds as their mean, not as the longest of 32 random rows
-    if (ctx->kind_b == SPK_ROWT && env_int("DUQUAD_ROWT_SORT", 256) > 0)
-        CK(rowt_window_sort(&ctx->b_rp, &ctx->b_ci, &ctx->b_va, ctx->nloc, ctx->nnz_b,
-                            env_int("DUQUAD_ROWT_SORT", 256), &ctx->b_pidx, s));
     return DUQUAD_OK;
 }
 

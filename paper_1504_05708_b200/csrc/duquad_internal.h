@@ -127,8 +127,6 @@ struct PassBArgs {
     const int32_t *rp;
     const int32_t *ci;
     const double *va;
-    const int32_t *pidx; // thread-per-row CSR stored in windows sorted by row length: position -> row
-                         // (rp / ci / va in that order; NULL: storage order = row order)
     const int32_t *skip; // eps_in mode: the inner solve has converged -> the launch does nothing
     double *gm_sq;       // eps_in mode: gm_sq[j] = (y_j - x+_j)^2 (gradient-map test)
     int32_t box_uniform; // every lb_j == lb_u and ub_j == ub_u: the epilogue skips the lb / ub loads
@@ -294,11 +292,6 @@ int lane_unroll(int kind, int64_t max_width, double mean_len);
 int lane_blocks_per_sm(int pass, int kind, int u);
 cudaError_t launch_pass_a_lane(const PassAArgs &a, int mode, const LaunchCfg &cfg, cudaStream_t s);
 cudaError_t launch_pass_b_lane(const PassBArgs &b, int mode, const LaunchCfg &cfg, cudaStream_t s);
-// Thread-per-row CSR: reorder the rows within windows of `window` rows by descending length (stable),
-// so the 32 rows of a warp have similar lengths (fewer load rounds per warp).  Replaces *rp / *ci / *va
-// (freed) with the reordered arrays and allocates *pidx (position -> row).
-cudaError_t rowt_window_sort(int32_t **rp, int32_t **ci, double **va, int64_t rows, int64_t nnz, int window,
-                             int32_t **pidx, cudaStream_t s);
 
 // kernels_fused.cu
 bool fused_supported(int64_t n, int64_t ld, size_t smem_optin);

@@ -28,7 +28,6 @@
 #include <thrust/extrema.h>
 #include <thrust/reduce.h>
 #include <thrust/scan.h>
-#include <thrust/sort.h>
 
 #include <algorithm>
 
@@ -312,10 +311,9 @@ __global__ void __launch_bounds__(kLaneThreads, DQ_LANE_MINB) k_pass_b_rowt(cons
     const double avg_w = avg_weight(b, MODE);
     const uint64_t pol = evict_first();
     for (int64_t base = warp * 32; base < b.nrows; base += nwarps * 32) {
-        const int64_t pos = base + lane;   // storage position; its row j (length-sorted windows)
-        const bool v = pos < b.nrows;
-        const int64_t j = (v && b.pidx) ? b.pidx[pos] : pos;
-        const int32_t lo = v ? b.rp[pos] : 0, len = v ? b.rp[pos + 1] - lo : 0;
+        const int64_t j = base + lane;
+        const bool v = j < b.nrows;
+        const int32_t lo = v ? b.rp[j] : 0, len = v ? b.rp[j + 1] - lo : 0;
         EpiB e{};
         if (v) e = epi_b_load(b, MODE, j, avg_w);
         const double t = rowt_dot<U>(b.ci, b.va, lo, len, b.w, pol);
@@ -324,28 +322,6 @@ __global__ void __launch_bounds__(kLaneThreads, DQ_LANE_MINB) k_pass_b_rowt(cons
 }
 
 // ------------------------------------------------------------------ layout construction
-__global__ void k_window_keys(const int32_t *rp, int64_t rows, int window, unsigned long long *key, int32_t *idx) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= rows) return;
-    const uint32_t len = (uint32_t)(rp[i + 1] - rp[i]);
-    key[i] = ((unsigned long long)(i / window) << 32) | (unsigned long long)(0xffffffffu - len);
-    idx[i] = (int32_t)i;
-}
-__global__ void k_perm_len(const int32_t *rp, const int32_t *perm, int64_t rows, int32_t *nlen) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < rows) nlen[i] = rp[perm[i] + 1] - rp[perm[i]];
-    if (i == rows) nlen[i] = 0;
-}
-__global__ void k_perm_copy(const int32_t *rp, const int32_t *ci, const double *va, const int32_t *perm,
-                            const int32_t *nrp, int64_t rows, int32_t *nci, double *nva) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= rows) return;
-    const int32_t src = rp[perm[i]], len = rp[perm[i] + 1] - src, dst = nrp[i];
-    for (int32_t k = 0; k < len; ++k) {
-        nci[dst + k] = ci[src + k];
-        nva[dst + k] = va[src + k];
-    }
-}
 __global__ void k_row_len(const int32_t *rp, int64_t rows, int32_t *len) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < rows) len[i] = rp[i + 1] - rp[i];
@@ -394,51 +370,6 @@ void sell_free(SellStore *st) {
     if (st->col) cudaFree(st->col);
     if (st->sptr) cudaFree(st->sptr);
     *st = SellStore{};
-}
-
-cudaError_t rowt_window_sort(int32_t **rp, int32_t **ci, double **va, int64_t rows, int64_t nnz, int window,
-                             int32_t **pidx, cudaStream_t s) {
-    *pidx = nullptr;
-    if (rows <= 0) return cudaSuccess;
-    unsigned long long *key = nullptr;
-    int32_t *perm = nullptr, *nrp = nullptr, *nci = nullptr;
-    double *nva = nullptr;
-    cudaError_t e = cudaMalloc(&key, rows * sizeof(unsigned long long));
-    if (!e) e = cudaMalloc(&perm, rows * sizeof(int32_t));
-    if (!e) e = cudaMalloc(&nrp, (rows + 1) * sizeof(int32_t));
-    if (!e) e = cudaMalloc(&nci, std::max<int64_t>(nnz, 2) * sizeof(int32_t));
-    if (!e) e = cudaMalloc(&nva, std::max<int64_t>(nnz, 2) * sizeof(double));
-    if (!e) {
-        k_window_keys<<<nblk(rows, 256), 256, 0, s>>>(*rp, rows, window, key, perm);
-        e = cudaGetLastError();
-    }
-    if (!e) {
-        thrust::device_ptr<unsigned long long> kp(key);
-        thrust::device_ptr<int32_t> pp(perm);
-        thrust::stable_sort_by_key(thrust::cuda::par.on(s), kp, kp + rows, pp);
-        k_perm_len<<<nblk(rows + 1, 256), 256, 0, s>>>(*rp, perm, rows, nrp);
-        thrust::device_ptr<int32_t> np(nrp);
-        thrust::exclusive_scan(thrust::cuda::par.on(s), np, np + rows + 1, np);
-        k_perm_copy<<<nblk(rows, 256), 256, 0, s>>>(*rp, *ci, *va, perm, nrp, rows, nci, nva);
-        e = cudaGetLastError();
-    }
-    if (!e) e = cudaStreamSynchronize(s);
-    cudaFree(key);
-    if (e) {
-        cudaFree(perm);
-        cudaFree(nrp);
-        cudaFree(nci);
-        cudaFree(nva);
-        return e;
-    }
-    cudaFree(*rp);
-    cudaFree(*ci);
-    cudaFree(*va);
-    *rp = nrp;
-    *ci = nci;
-    *va = nva;
-    *pidx = perm;
-    return cudaSuccess;
 }
 
 cudaError_t sparse_plan(const int32_t *rp, int64_t rows, int64_t nq, SparsePlan *plan, cudaStream_t s) {
