@@ -57,7 +57,6 @@ struct duquad_ctx {
     double *lz_vprev = nullptr, *lz_w = nullptr;
     // CSR storage (format == DUQUAD_CSR): stacked local [Q_r; G_r] and local rows of G'
     int32_t *a_rp = nullptr, *a_ci = nullptr, *b_rp = nullptr, *b_ci = nullptr;
-    int32_t qfold = 0;          // CSR, rho > 0: pass A stores Q y + q (make_a / make_b)
     double *a_va = nullptr, *b_va = nullptr;
     int64_t nnz_a = 0, nnz_b = 0;
     int gs_a = 4, gs_b = 4;
@@ -294,9 +293,6 @@ PassAArgs make_a(duquad_ctx *c) {
     a.sp_u = c->u_a;
     a.sell = sell_view(c->sell_a);
     a.dia = c->dia;
-    // CSR, rho > 0: q folded into pass A's Q-row stores (its lane kernels have load slots to spare;
-    // pass B's epilogue is the heavier one)
-    a.qfold = c->qfold ? c->q : nullptr;
     return a;
 }
 
@@ -323,7 +319,6 @@ PassBArgs make_b(duquad_ctx *c) {
     b.rp = c->b_rp;
     b.ci = c->b_ci;
     b.va = c->b_va;
-    b.q_in_qy = c->qfold;
     b.skip = c->eps_mode ? c->d_done : nullptr;
     b.gm_sq = c->eps_mode ? c->gm_sq : nullptr;
     b.box_uniform = c->box_uniform;
@@ -1369,10 +1364,6 @@ duquad_status duquad_setup(duquad_ctx **out, const duquad_problem *prob, double 
         CKS(dalloc(&ctx->cvec, ctx->nloc));
         ctx->cfg_k3 = {ctx->cfg_b.grid, pass_threads(), smem_a};
         ctx->rho0 = true;
-    }
-    {   // CSR generic path: pass A's Q rows store Q y + q (measurement override DUQUAD_QFOLD=0)
-        const char *ov = std::getenv("DUQUAD_QFOLD");
-        ctx->qfold = csr && !ctx->rho0 && !(ov && std::atoi(ov) == 0);
     }
     if (!batched && !csr && !ctx->sharded && rho > 0.0 && p > 0 && opt.eq_precompute) {
         // NEXT-3: with every row an equality (K = {0}) the inner gradient is

@@ -71,7 +71,6 @@ struct PassAArgs {
     int64_t row_begin, row_end;
     const double *y;
     double *qy;          // Q rows: qy[row] = (Q y)_row
-    const double *qfold; // solve mode (CSR): Q rows store qy[row] = (Q y)_row + q_row (pass B then reads no q)
     // G rows (k = row - nq):
     double *w;           // w[k]  (local slice of the full w replica)
     const double *g;
@@ -111,7 +110,6 @@ struct PassBArgs {
     const double *w;
     const double *qy;
     const double *q, *lb, *ub;
-    int32_t q_in_qy;     // pass A folded q into qy (PassAArgs.qfold): the solve epilogue loads no q
     double *x;
     double *y;           // local slice of the full y replica
     double *xhat;

@@ -79,7 +79,6 @@ __device__ __forceinline__ double dual_average(double lh, double lam, double m, 
 
 __device__ __forceinline__ EpiA epi_a_load(const PassAArgs &a, int mode, int64_t row, const OuterA &o) {
     EpiA e{0.0, 0.0, 0.0, 0.0, 0};
-    if (mode == MODE_SOLVE && row < a.nq && a.qfold) e.g = a.qfold[row];   // Q row: q_row in e.g
     if (mode == MODE_SOLVE && row >= a.nq) {
         const int64_t k = row - a.nq;
         e.g = a.g[k];
@@ -105,7 +104,7 @@ __device__ __forceinline__ double dfom_row(double r, double mu, double lp, uint8
 __device__ __forceinline__ void epi_a_store(const PassAArgs &a, int mode, int64_t row, double s,
                                             const EpiA &e, const OuterA &o) {
     if (row < a.nq) {
-        a.qy[row] = (mode == MODE_SOLVE && a.qfold) ? s + e.g : s;   // (Q y + q) rounded once, as pass B would
+        a.qy[row] = s;
         return;
     }
     const int64_t k = row - a.nq;
@@ -145,7 +144,7 @@ __device__ __forceinline__ EpiB epi_b_load(const PassBArgs &b, int mode, int64_t
     EpiB e{0, 0, 0, 0, 0, 0, 0};
     if (mode == MODE_SOLVE || b.use_qy) e.qy = b.qy[j];
     if (mode == MODE_SOLVE) {
-        e.q = b.q_in_qy ? 0.0 : b.q[j];   // folded: (qy + q) + 0 == the unfolded (qy + q) bit for bit
+        e.q = b.q[j];
         if (b.box_uniform) {   // U = [lb, ub]^n with scalar bounds (c4's [-1, 1]): no per-row loads
             e.lb = b.lb_u;
             e.ub = b.ub_u;

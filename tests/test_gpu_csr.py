@@ -356,26 +356,3 @@ def test_symmetric_half_band_dia_row_sharded(torch_cuda, n, P):
     r = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 5.0, "DFGM", 4, 5, L_in, L_d)
     for g_, w_ in zip(got, (r.x_last, r.x_avg, r.lam)):
         assert relerr(g_, w_) <= TOL
-
-
-@pytest.mark.parametrize("alg", ["DGM", "DFGM"])
-def test_q_folded_into_pass_a_is_bitwise(torch_cuda, monkeypatch, alg):
-    """CSR solves with q folded into pass A's Q-row stores (qy := Q y + q, pass B loads no q) give
-    the iterates of the unfolded step bit for bit ((qy + q) + t either way), lane and sub-warp
-    kernels alike, including the per-outer trace and the residuals afterwards."""
-    prob = qpgen.sparse_banded_eq(n=2345, p=777, seed=41)
-    L_in, L_d, _ = _consts_dense(prob, 5.0, 0.5)
-    for sell in (True, False):
-        outs = []
-        for fold in ("1", "0"):
-            monkeypatch.setenv("DUQUAD_QFOLD", fold)
-            g = _gpu(prob, 5.0, alg, 5, 6, L_in, L_d, trace=True, torch=torch_cuda, sell_path=sell)
-            g["res"] = g["solver"].residuals("last")
-            outs.append(g)
-            g["solver"].close()
-        monkeypatch.delenv("DUQUAD_QFOLD")
-        for k in ("x_last", "x_avg", "lam", "trace_lam", "trace_u", "res"):
-            assert np.array_equal(np.asarray(outs[0][k]), np.asarray(outs[1][k])), (k, sell)
-        r = O.dfom(prob.Q, prob.q, prob.G, prob.g, prob.lb, prob.ub, prob.cone, 5.0, alg, 5, 6, L_in, L_d,
-                   keep_trace=True)
-        _check(outs[0], r, trace=True)
