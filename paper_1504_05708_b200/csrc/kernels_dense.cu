@@ -64,6 +64,38 @@ __device__ __forceinline__ double row_dot(const double2 *__restrict__ row,
     return warp_sum((acc0 + acc1) + (acc2 + acc3));
 }
 
+// The same row dot with its first chunk already in registers (v, loaded by chunk_load), and the
+// next row's first chunk loaded into v after the last FMA of this row (next != nullptr): the
+// matrix stream of a warp's next row, or of its first row before griddepcontrol.wait (the stored
+// matrices are written by no kernel of a solve, epilogue.cuh), is in flight while this row's
+// butterfly, epilogue and the y / w staging run.  Same loads, FMAs and order as row_dot: bitwise
+// the same row value.
+__device__ __forceinline__ void chunk_load(const double2 *__restrict__ row, int c, int nv2, double2 (&v)[kUnroll]) {
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+        v[u] = c + 32 * u < nv2 ? ldg_stream(row + c + 32 * u) : make_double2(0.0, 0.0);
+}
+
+__device__ __forceinline__ double row_dot_pre(const double2 *__restrict__ row, const double2 *__restrict__ sv,
+                                              int nv2, int lane, double2 (&v)[kUnroll],
+                                              const double2 *__restrict__ next) {
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+    for (int c = lane; c - lane < nv2; c += 32 * kUnroll) {
+        if (c != lane) chunk_load(row, c, nv2, v);
+#pragma unroll
+        for (int u = 0; u < kUnroll; u += 2) {
+            const double2 y0 = c + 32 * u < nv2 ? sv[c + 32 * u] : make_double2(0.0, 0.0);
+            const double2 y1 = c + 32 * (u + 1) < nv2 ? sv[c + 32 * (u + 1)] : make_double2(0.0, 0.0);
+            acc0 = fma(v[u].x, y0.x, acc0);
+            acc1 = fma(v[u].y, y0.y, acc1);
+            acc2 = fma(v[u + 1].x, y1.x, acc2);
+            acc3 = fma(v[u + 1].y, y1.y, acc3);
+        }
+    }
+    if (next) chunk_load(next, lane, nv2, v);
+    return warp_sum((acc0 + acc1) + (acc2 + acc3));
+}
+
 __device__ __forceinline__ void stage(double *s, const double *g, int64_t len) {
     const double2 *g2 = reinterpret_cast<const double2 *>(g);
     double2 *s2 = reinterpret_cast<double2 *>(s);
@@ -80,6 +112,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass_a(const PassAArgs a) {
     const int64_t r0 = a.row_begin + rows * blockIdx.x / gridDim.x;
     const int64_t r1 = a.row_begin + rows * (blockIdx.x + 1) / gridDim.x;
     const int nv2 = (int)(a.ld >> 1);
+    const double2 *A2 = reinterpret_cast<const double2 *>(a.A);
+    const int64_t ld2 = a.ld >> 1;
+    double2 v[kUnroll];
+    if (r0 + warp < r1) chunk_load(A2 + (r0 + warp) * ld2, lane, nv2, v);   // matrix only: before the wait
     pdl_wait();   // PDL (epilogue.cuh): the launch overlaps the previous kernel's tail
     pdl_trigger();
     if (a.skip && *a.skip) return;
@@ -91,7 +127,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass_a(const PassAArgs a) {
         // epilogue operands are fetched before the stream so their latency overlaps it
         EpiA e{};
         if (lane == 0) e = epi_a_load(a, MODE, row, o);
-        const double s = row_dot(reinterpret_cast<const double2 *>(a.A + row * a.ld), sv, nv2, lane);
+        const double s = row_dot_pre(A2 + row * ld2, sv, nv2, lane, v, row + nw < r1 ? A2 + (row + nw) * ld2 : nullptr);
         if (lane == 0) epi_a_store(a, MODE, row, s, e, o);
     }
 }
@@ -104,6 +140,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass_b(const PassBArgs b) {
     const int64_t r0 = b.nrows * blockIdx.x / gridDim.x;
     const int64_t r1 = b.nrows * (blockIdx.x + 1) / gridDim.x;
     const int nv2 = (int)(b.ldp >> 1);
+    const double2 *G2 = reinterpret_cast<const double2 *>(b.GT);
+    const int64_t ld2 = b.ldp >> 1;
+    double2 v[kUnroll];
+    if (nv2 > 0 && r0 + warp < r1) chunk_load(G2 + (r0 + warp) * ld2, lane, nv2, v);   // before the wait
     pdl_wait();   // PDL (epilogue.cuh): the launch overlaps the previous kernel's tail
     pdl_trigger();
     if (b.skip && *b.skip) return;
@@ -114,7 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass_b(const PassBArgs b) {
     for (int64_t j = r0 + warp; j < r1; j += nw) {
         EpiB e{};
         if (lane == 0) e = epi_b_load(b, MODE, j, avg_w);
-        const double t = nv2 > 0 ? row_dot(reinterpret_cast<const double2 *>(b.GT + j * b.ldp), sv, nv2, lane)
+        const double t = nv2 > 0 ? row_dot_pre(G2 + j * ld2, sv, nv2, lane, v, j + nw < r1 ? G2 + (j + nw) * ld2 : nullptr)
                                  : 0.0;
         if (lane == 0) epi_b_store(b, MODE, j, t, e, avg_w);
     }
@@ -214,6 +254,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_rho0_step(const PassAArgs a, co
     const int64_t r0 = a.nq * blockIdx.x / gridDim.x;
     const int64_t r1 = a.nq * (blockIdx.x + 1) / gridDim.x;
     const int nv2 = (int)(a.ld >> 1);
+    const double2 *A2 = reinterpret_cast<const double2 *>(a.A);
+    const int64_t ld2 = a.ld >> 1;
+    double2 v[kUnroll];
+    if (r0 + warp < r1) chunk_load(A2 + (r0 + warp) * ld2, lane, nv2, v);   // matrix only: before the wait
     pdl_wait();   // PDL (epilogue.cuh): the launch overlaps the previous kernel's tail
     pdl_trigger();
     if (a.skip && *a.skip) return;
@@ -224,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rho0_step(const PassAArgs a, co
     for (int64_t j = r0 + warp; j < r1; j += nw) {
         EpiB e{};
         if (lane == 0) e = epi_b_load(bl, MODE_SOLVE, j, avg_w);     // bl.q = c, bl.y = yin slice
-        const double s = row_dot(reinterpret_cast<const double2 *>(a.A + j * a.ld), sv, nv2, lane);
+        const double s = row_dot_pre(A2 + j * ld2, sv, nv2, lane, v, j + nw < r1 ? A2 + (j + nw) * ld2 : nullptr);
         if (lane == 0) {
             e.qy = s;                                                  // grad = (Qy + c) + 0
             epi_b_store(bs, MODE_SOLVE, j, 0.0, e, avg_w);             // bs.y = yout slice
