@@ -134,38 +134,6 @@ __device__ __forceinline__ double rowt_dot(const int32_t *__restrict__ ci, const
     return acc;
 }
 
-// one round of a lane's own CSR row (thread-per-row): indices and values only (the stored matrix)
-template <int U>
-__device__ __forceinline__ void rowt_load(const int32_t *__restrict__ ci, const double *__restrict__ va, int32_t lo,
-                                          int32_t len, int k0, int32_t (&c)[U], double (&a)[U], uint64_t pol) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-        const bool ok = k0 + u < len;
-        c[u] = ok ? ld_l1_i32(ci + lo + k0 + u, pol) : -1;
-        a[u] = ok ? ld_l1_f64(va + lo + k0 + u, pol) : 0.0;
-    }
-}
-
-// rowt_dot with its first round already loaded (c, a; by rowt_load before griddepcontrol.wait):
-// same loads, FMAs and order
-template <int U>
-__device__ __forceinline__ double rowt_dot_pre(const int32_t *__restrict__ ci, const double *__restrict__ va,
-                                               int32_t lo, int32_t len, const double *__restrict__ v, uint64_t pol,
-                                               int32_t (&c)[U], double (&a)[U]) {
-    const int32_t wl = __reduce_max_sync(0xffffffffu, len);
-    double acc = 0.0;
-    for (int k0 = 0; k0 < wl; k0 += U) {
-        if (k0 > 0) rowt_load<U>(ci, va, lo, len, k0, c, a, pol);
-        double x[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) x[u] = c[u] >= 0 ? __ldg(v + c[u]) : 0.0;
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            if (c[u] >= 0) acc = fma(a[u], x[u], acc);
-    }
-    return acc;
-}
-
 // lane's row of the DIA Q block (local row i, global row gi): the diagonals in ascending column
 // order, rounds of U, no index loads (the y loads of a round are contiguous per diagonal)
 template <int U>
@@ -246,9 +214,6 @@ __device__ __forceinline__ double dia_dot_sym(const DiaMat &d, int64_t i, const 
     return acc;
 }
 
-__device__ __forceinline__ void prefetch_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
-__device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
-
 #ifndef DQ_SELL_MIX
 #define DQ_SELL_MIX 1
 #endif
@@ -258,6 +223,9 @@ __device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefe
 
 template <int MODE, int U>
 __global__ void __launch_bounds__(kLaneThreads, DQ_SELLA_MINB) k_pass_a_sell(const PassAArgs a) {
+    pdl_wait();   // everything below reads iterates or writes (PDL, epilogue.cuh)
+    pdl_trigger();
+    if (a.skip && *a.skip) return;
     const SellMat &m = a.sell;
     const int lane = threadIdx.x & 31;
     // sub-ranges: Q rows only [0, nq), G rows only [nq, rows), or all (segments never share a slice)
@@ -265,37 +233,11 @@ __global__ void __launch_bounds__(kLaneThreads, DQ_SELLA_MINB) k_pass_a_sell(con
     const int64_t s_hi = a.row_end <= m.nq ? m.nsl_q : m.nsl;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const OuterA o = outer_a(a, MODE);
+    const uint64_t pol = evict_first();
     // whole range: Q and G slices interleaved in proportion (DQ_SELL_MIX), so the DIA Q rows (one
     // DRAM round each) and the G rows (index -> gather chains) are in flight together
     const bool mix = DQ_SELL_MIX && s_lo == 0 && s_hi == m.nsl && m.nsl_q > 0 && m.nsl > m.nsl_q;
-    if (s_lo + warp < s_hi) {   // the first slice's stored matrix lines, prefetched before the wait
-        const int64_t t = s_lo + warp;
-        int64_t s = t;
-        if (mix) {
-            const int64_t qb = t * m.nsl_q / m.nsl, qn = (t + 1) * m.nsl_q / m.nsl;
-            s = qn > qb ? qb : m.nsl_q + (t - qb);
-        }
-        if (s < m.nsl_q && a.dia.nd > 0) {
-            const int64_t i = s * 32 + lane;
-            const double *b0 = a.dia.val + (a.dia.sym ? a.dia.halo : 0) + i;
-            for (int k = 0; k < a.dia.nd; ++k) {
-                prefetch_l1(b0 + (int64_t)k * a.dia.ldv);
-                if (a.dia.sym) prefetch_l1(b0 + (int64_t)k * a.dia.ldv - a.dia.off[k]);
-            }
-        } else {
-            const int64_t base = m.sptr[s];
-            const int w = (int)((m.sptr[s + 1] - base) >> 5);
-            for (int k = 0; k < w; ++k) {
-                prefetch_l2(m.val + base + (int64_t)k * 32 + lane);
-                prefetch_l2(m.col + base + (int64_t)k * 32 + lane);
-            }
-        }
-    }
-    pdl_wait();   // everything below reads iterates or writes (PDL, epilogue.cuh)
-    pdl_trigger();
-    if (a.skip && *a.skip) return;
-    const OuterA o = outer_a(a, MODE);
-    const uint64_t pol = evict_first();
     for (int64_t t = s_lo + warp; t < s_hi; t += nwarps) {
         int64_t s = t;
         if (mix) {
@@ -360,38 +302,21 @@ __global__ void __launch_bounds__(kLaneThreads, DQ_LANE_MINB) k_pass_a_rowt(cons
 
 template <int MODE, int U>
 __global__ void __launch_bounds__(kLaneThreads, DQ_LANE_MINB) k_pass_b_rowt(const PassBArgs b) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t pol = evict_first();
-    // the first group's row pointers and first round of G' (stored matrix) before the wait: under
-    // PDL they load while the previous kernel drains
-    int32_t c[U];
-    double a[U];
-    int32_t lo = 0, len = 0;
-    {
-        const int64_t j = warp * 32 + lane;
-        if (j < b.nrows) {
-            lo = b.rp[j];
-            len = b.rp[j + 1] - lo;
-        }
-        rowt_load<U>(b.ci, b.va, lo, len, 0, c, a, pol);
-    }
     pdl_wait();
     pdl_trigger();
     if (b.skip && *b.skip) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const double avg_w = avg_weight(b, MODE);
+    const uint64_t pol = evict_first();
     for (int64_t base = warp * 32; base < b.nrows; base += nwarps * 32) {
         const int64_t j = base + lane;
         const bool v = j < b.nrows;
-        if (base != warp * 32) {
-            lo = v ? b.rp[j] : 0;
-            len = v ? b.rp[j + 1] - lo : 0;
-            rowt_load<U>(b.ci, b.va, lo, len, 0, c, a, pol);
-        }
+        const int32_t lo = v ? b.rp[j] : 0, len = v ? b.rp[j + 1] - lo : 0;
         EpiB e{};
         if (v) e = epi_b_load(b, MODE, j, avg_w);
-        const double t = rowt_dot_pre<U>(b.ci, b.va, lo, len, b.w, pol, c, a);
+        const double t = rowt_dot<U>(b.ci, b.va, lo, len, b.w, pol);
         if (v) epi_b_store(b, MODE, j, t, e, avg_w);
     }
 }
