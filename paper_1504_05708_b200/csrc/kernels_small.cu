@@ -12,6 +12,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "duquad_internal.h"
 #include "epilogue.cuh"
 
@@ -189,7 +191,12 @@ cudaError_t configure_small_kernel(size_t smem) {
 }
 
 cudaError_t launch_small_solve(const SmallArgs &sa, size_t smem, cudaStream_t s) {
-    k_small_solve<<<1, kSmallThreads, smem, s>>>(sa);
+    // kTpr threads per row of the larger pass ([Q;G]: n + p rows), whole warps, at most 1024: warps
+    // that would own no row of either pass only add issue slots and barrier arrivals (config 0:
+    // 600 of 1024 threads busy in pass A); the per-row arithmetic does not depend on the block size
+    const int64_t need = ((sa.n + sa.p) * kTpr + 31) / 32 * 32;
+    const int threads = (int)std::min<int64_t>(kSmallThreads, std::max<int64_t>(32, need));
+    k_small_solve<<<1, threads, smem, s>>>(sa);
     return cudaGetLastError();
 }
 
