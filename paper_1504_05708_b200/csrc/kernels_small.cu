@@ -39,32 +39,6 @@ __device__ __forceinline__ double col_part(const double *M, int ldm, int col, co
     return a0 + a1;
 }
 
-// col_part for len <= kTpr * MK: every load of the thread issued before its first FMA (one
-// shared-memory latency instead of one per loop trip), the same two accumulators in the same
-// order (entries sub + kTpr k: even k into a0, odd k into a1, ascending; absent entries skipped)
-template <int MK>
-__device__ __forceinline__ double col_part_short(const double *M, int ldm, int col, const double *v, int len,
-                                                 int sub) {
-    double m[MK], x[MK];
-#pragma unroll
-    for (int k = 0; k < MK; ++k) {
-        const int c = sub + kTpr * k;
-        m[k] = c < len ? M[c * ldm + col] : 0.0;
-        x[k] = c < len ? v[c] : 0.0;
-    }
-    double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-    for (int k = 0; k < MK; ++k)
-        if (sub + kTpr * k < len) {
-            if (k & 1) a1 = fma(m[k], x[k], a1);
-            else a0 = fma(m[k], x[k], a0);
-        }
-    return a0 + a1;
-}
-__device__ __forceinline__ double col_part_any(const double *M, int ldm, int col, const double *v, int len, int sub) {
-    return len <= kTpr * 8 ? col_part_short<8>(M, ldm, col, v, len, sub) : col_part(M, ldm, col, v, len, sub);
-}
-
 // sum over the kTpr threads of a row (fixed xor tree); every lane of the warp must call it
 __device__ __forceinline__ double row_sum8(double s) {
     s += __shfl_xor_sync(0xffffffffu, s, 4);
@@ -164,8 +138,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_solve(const SmallArg
             for (int base = 0; base < rowsi; base += nunit) {
                 const int row = base + unit0;
                 double s = 0.0;
-                if (row < ni) s = col_part_any(A, lda, row, y, ni, sub);                  // (Q y)_row, Q symmetric
-                else if (row < rowsi) s = col_part_any(GT, ldg, row - ni, y, ni, sub);     // (G y)_{row-n} via G'
+                if (row < ni) s = col_part(A, lda, row, y, ni, sub);                      // (Q y)_row, Q symmetric
+                else if (row < rowsi) s = col_part(GT, ldg, row - ni, y, ni, sub);         // (G y)_{row-n} via G'
                 s = row_sum8(s);   // all lanes (converged)
                 if (sub == 0 && row < rowsi) {
                     const EpiA e = epi_a_load(a, MODE_SOLVE, row, o);
@@ -180,7 +154,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_solve(const SmallArg
             const double avg_w = avg_weight(b, MODE_SOLVE);
             for (int base = 0; base < ni; base += nunit) {                                  // pass B
                 const int r = base + unit0;
-                const double t = row_sum8((r < ni && pi > 0) ? col_part_any(Gm, lda, r, w, pi, sub) : 0.0);
+                const double t = row_sum8((r < ni && pi > 0) ? col_part(Gm, lda, r, w, pi, sub) : 0.0);
                 if (sub == 0 && r < ni) {
                     const EpiB e = epi_b_load(b, MODE_SOLVE, r, avg_w);
                     epi_b_store(b, MODE_SOLVE, r, t, e, avg_w);
