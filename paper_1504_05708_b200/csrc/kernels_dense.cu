@@ -96,11 +96,26 @@ __device__ __forceinline__ double row_dot_pre(const double2 *__restrict__ row, c
     return warp_sum((acc0 + acc1) + (acc2 + acc3));
 }
 
+// Four loads per thread in flight before the first shared-memory store, so a vector of up to
+// 4 x blockDim double2 (config 1's y: 1000 double2 over 512 threads) costs one L2 round trip
+// (the plain loop was compiled as a one-trip-at-a-time remainder loop: load, store, load, ...).
 __device__ __forceinline__ void stage(double *s, const double *g, int64_t len) {
     const double2 *g2 = reinterpret_cast<const double2 *>(g);
     double2 *s2 = reinterpret_cast<double2 *>(s);
     const int64_t n2 = len >> 1;
-    for (int64_t i = threadIdx.x; i < n2; i += blockDim.x) s2[i] = g2[i];
+    for (int64_t i0 = threadIdx.x; i0 < n2; i0 += 4 * (int64_t)blockDim.x) {
+        double2 t[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t i = i0 + k * (int64_t)blockDim.x;
+            if (i < n2) t[k] = g2[i];
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t i = i0 + k * (int64_t)blockDim.x;
+            if (i < n2) s2[i] = t[k];
+        }
+    }
 }
 
 template <int MODE>
